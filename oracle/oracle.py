@@ -1,0 +1,155 @@
+"""TEST INFRASTRUCTURE ONLY — the parity oracle, never the product path.
+
+ctypes wrapper over ``oracle/_ref/libocldec_ref.so``: the unmodified reference
+decompiler (``/root/reference/proj/core/src``) compiled by ``oracle/Makefile``.
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline /
+``--impl reference`` leg may import this module, and only as the checker or
+the timed CPU arm.
+
+Wrapped reference entry points:
+  * ``ocldec::decompile_listing``        proj/core/src/decompiler.cpp:117-133
+  * ``DecompileResult::combined_source`` proj/core/src/decompiler.cpp:105-115
+  * ``ocldec_tests::corpus``             proj/tests/support/corpus.cpp:44-664
+  * ``ocldec_tests::make_nest``          proj/tests/support/nestgen.cpp:219-243
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_ref", "libocldec_ref.so")
+_lib = None
+
+
+def available() -> bool:
+    return os.path.exists(LIB_PATH)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not available():
+            raise RuntimeError(f"oracle library missing: {LIB_PATH} (run `make -C oracle`)")
+        L = ctypes.CDLL(LIB_PATH)
+        L.ref_decompile.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_char_p,
+                                    ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_size_t)]
+        L.ref_decompile.restype = ctypes.c_int
+        L.ref_free.argtypes = [ctypes.c_void_p]
+        L.ref_decompile_batch.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
+                                          ctypes.c_void_p, ctypes.c_void_p,
+                                          ctypes.POINTER(ctypes.c_uint64)]
+        L.ref_decompile_batch.restype = ctypes.c_double
+        L.ref_corpus_count.restype = ctypes.c_int
+        L.ref_corpus_get.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p),
+                                     ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+        L.ref_make_nest.argtypes = [ctypes.c_uint64, ctypes.POINTER(ctypes.c_int)]
+        L.ref_make_nest.restype = ctypes.c_void_p
+        _lib = L
+    return _lib
+
+
+@dataclass
+class RefKernel:
+    name: bytes
+    source: bytes
+    failed: bool
+    structured: bool
+    fallback_count: int
+
+
+@dataclass
+class RefDiag:
+    severity: int  # 0 note, 1 warning, 2 error (diagnostics.hpp:16)
+    line: int
+    message: bytes
+
+
+@dataclass
+class RefResult:
+    kernels: List[RefKernel] = field(default_factory=list)
+    diagnostics: List[RefDiag] = field(default_factory=list)
+    combined: bytes = b""
+
+
+def _take(ptr: int, n: int) -> bytes:
+    return ctypes.string_at(ptr, n)
+
+
+def decompile(listing: bytes, fold_local_size: bool = False, only_kernel: Optional[bytes] = None) -> RefResult:
+    if isinstance(listing, str):
+        listing = listing.encode()
+    L = lib()
+    out = ctypes.c_void_p()
+    n = ctypes.c_size_t()
+    L.ref_decompile(listing, len(listing), int(fold_local_size), only_kernel, ctypes.byref(out), ctypes.byref(n))
+    blob = _take(out.value, n.value)
+    L.ref_free(out)
+    res = RefResult()
+    pos = 0
+    while pos < len(blob):
+        nl = blob.index(b"\n", pos)
+        head = blob[pos:nl].split()
+        pos = nl + 1
+        if head[0] == b"K":
+            failed, structured, fb, nlen, slen = (int(x) for x in head[1:])
+            name = blob[pos:pos + nlen]
+            pos += nlen
+            src = blob[pos:pos + slen]
+            pos += slen
+            res.kernels.append(RefKernel(name, src, bool(failed), bool(structured), fb))
+        elif head[0] == b"D":
+            sev, line, mlen = (int(x) for x in head[1:])
+            res.diagnostics.append(RefDiag(sev, line, blob[pos:pos + mlen]))
+            pos += mlen
+        elif head[0] == b"C":
+            clen = int(head[1])
+            res.combined = blob[pos:pos + clen]
+            pos += clen
+        else:  # pragma: no cover
+            raise ValueError(f"bad oracle record {head!r}")
+    return res
+
+
+def corpus():
+    """[(name, listing, comparable, expected_fallbacks)] — corpus.cpp:44-664."""
+    L = lib()
+    out = []
+    for i in range(L.ref_corpus_count()):
+        nm, ls = ctypes.c_void_p(), ctypes.c_void_p()
+        cmp_, fb = ctypes.c_int(), ctypes.c_int()
+        L.ref_corpus_get(i, ctypes.byref(nm), ctypes.byref(ls), ctypes.byref(cmp_), ctypes.byref(fb))
+        out.append((ctypes.string_at(nm.value), ctypes.string_at(ls.value), bool(cmp_.value), fb.value))
+        L.ref_free(nm)
+        L.ref_free(ls)
+    return out
+
+
+def make_nest(seed: int) -> bytes:
+    L = lib()
+    c = ctypes.c_int()
+    p = L.ref_make_nest(seed, ctypes.byref(c))
+    s = ctypes.string_at(p)
+    L.ref_free(p)
+    return s
+
+
+def decompile_batch(corpus_bytes: bytes, offsets, nthreads: int, want_hashes: bool = False):
+    """Times the reference on per-kernel listings corpus[offsets[k]:offsets[k+1]].
+
+    Returns (seconds, instructions, hashes|None, lengths|None)."""
+    import numpy as np
+    L = lib()
+    offs = np.ascontiguousarray(offsets, dtype=np.uint64)
+    nk = len(offs) - 1
+    buf = ctypes.create_string_buffer(corpus_bytes, len(corpus_bytes)) if isinstance(corpus_bytes, bytes) else corpus_bytes
+    hashes = np.zeros(nk, dtype=np.uint64) if want_hashes else None
+    lens = np.zeros(nk, dtype=np.uint64) if want_hashes else None
+    ninstr = ctypes.c_uint64()
+    secs = L.ref_decompile_batch(ctypes.cast(buf, ctypes.c_void_p), offs.ctypes.data, nk, nthreads,
+                                 hashes.ctypes.data if hashes is not None else None,
+                                 lens.ctypes.data if lens is not None else None,
+                                 ctypes.byref(ninstr))
+    return secs, ninstr.value, hashes, lens

@@ -1,0 +1,210 @@
+// TEST INFRASTRUCTURE ONLY — the parity oracle, never the product path.
+//
+// Thin C ABI over the *unmodified* reference decompiler, compiled straight
+// from its sources under /root/reference/proj/core/src by oracle/Makefile
+// into oracle/_ref/libocldec_ref.so.  Only tests/, __graft_entry__.smoke()
+// and bench.py's cpu_baseline / --impl reference leg may load it.
+//
+// Entry points wrap:
+//   ocldec::decompile_listing          proj/core/src/decompiler.cpp:117-133
+//   DecompileResult::combined_source   proj/core/src/decompiler.cpp:105-115
+//   Diagnostic::render                 proj/core/src/diagnostics.cpp:22-26
+//   ocldec_tests::corpus / make_nest   proj/tests/support/{corpus,nestgen}.cpp
+//
+// The reference recurses per region nesting level (lower.cpp:123-172) and
+// overflows an 8 MB stack at ~230 nested regions, so every call
+// runs on a pthread with a 1 GiB stack.
+
+#include <pthread.h>
+
+#include <atomic>
+#include <chrono>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ocldec/decompiler.hpp"
+#include "corpus.hpp"
+#include "nestgen.hpp"
+
+namespace {
+
+constexpr size_t kBigStack = size_t(1) << 30;
+
+void run_on_big_stack(void *(*fn)(void *), void *arg) {
+    pthread_attr_t attr;
+    pthread_attr_init(&attr);
+    pthread_attr_setstacksize(&attr, kBigStack);
+    pthread_t th;
+    if (pthread_create(&th, &attr, fn, arg) != 0) {
+        fn(arg); // fall back to the caller's stack
+    } else {
+        pthread_join(th, nullptr);
+    }
+    pthread_attr_destroy(&attr);
+}
+
+char *dup_out(const std::string &s, size_t *len) {
+    char *p = static_cast<char *>(std::malloc(s.size() + 1));
+    std::memcpy(p, s.data(), s.size());
+    p[s.size()] = 0;
+    if (len)
+        *len = s.size();
+    return p;
+}
+
+struct DecompileJob {
+    const char *listing;
+    size_t len;
+    int fold_local_size;
+    const char *only_kernel;
+    std::string serialized;
+};
+
+// Serialization (parsed by oracle/oracle.py):
+//   "K <failed> <structured> <fallbacks> <name_len> <src_len>\n" name source
+//   "D <severity> <line> <msg_len>\n" message
+//   "C <len>\n" combined_source
+void *decompile_job(void *p) {
+    auto *job = static_cast<DecompileJob *>(p);
+    ocldec::DecompileOptions opts;
+    opts.folds.fold_local_size = job->fold_local_size != 0;
+    if (job->only_kernel)
+        opts.only_kernel = std::string(job->only_kernel);
+    ocldec::DecompileResult res =
+        ocldec::decompile_listing(std::string(job->listing, job->len), opts);
+    std::string out;
+    for (const auto &k : res.kernels) {
+        out += "K " + std::to_string(int(k.failed)) + " " + std::to_string(int(k.structured)) +
+               " " + std::to_string(k.body.fallback_count) + " " + std::to_string(k.name.size()) +
+               " " + std::to_string(k.source.size()) + "\n";
+        out += k.name;
+        out += k.source;
+    }
+    for (const auto &d : res.diagnostics.all()) {
+        out += "D " + std::to_string(int(d.severity)) + " " + std::to_string(d.line) + " " +
+               std::to_string(d.message.size()) + "\n";
+        out += d.message;
+    }
+    std::string combined = res.combined_source();
+    out += "C " + std::to_string(combined.size()) + "\n";
+    out += combined;
+    job->serialized = std::move(out);
+    return nullptr;
+}
+
+struct BatchJob {
+    const char *corpus;
+    const uint64_t *offsets; // nkernels + 1 byte offsets of per-kernel listings
+    size_t nkernels;
+    std::atomic<size_t> *next;
+    uint64_t *out_hash; // per kernel FNV-1a of source (0 when null)
+    uint64_t *out_len;  // per kernel source length
+    uint64_t instructions = 0;
+};
+
+uint64_t fnv1a(const std::string &s) {
+    uint64_t h = 1469598103934665603ull;
+    for (unsigned char c : s) {
+        h ^= c;
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+
+void *batch_worker(void *p) {
+    auto *job = static_cast<BatchJob *>(p);
+    for (;;) {
+        size_t k = job->next->fetch_add(1);
+        if (k >= job->nkernels)
+            break;
+        std::string listing(job->corpus + job->offsets[k], job->offsets[k + 1] - job->offsets[k]);
+        ocldec::DecompileResult res = ocldec::decompile_listing(listing);
+        std::string src = res.combined_source();
+        if (job->out_hash)
+            job->out_hash[k] = fnv1a(src);
+        if (job->out_len)
+            job->out_len[k] = src.size();
+        for (const auto &kk : res.kernels)
+            job->instructions += kk.instructions.size();
+    }
+    return nullptr;
+}
+
+} // namespace
+
+extern "C" {
+
+// Decompiles one listing; *out receives the serialized result (free with
+// ref_free). Returns 0.
+int ref_decompile(const char *listing, size_t len, int fold_local_size, const char *only_kernel,
+                  char **out, size_t *out_len) {
+    DecompileJob job{listing, len, fold_local_size, only_kernel, {}};
+    run_on_big_stack(decompile_job, &job);
+    *out = dup_out(job.serialized, out_len);
+    return 0;
+}
+
+void ref_free(void *p) { std::free(p); }
+
+// Decompiles nkernels independent per-kernel listings, slices
+// corpus[offsets[k], offsets[k+1]), on nthreads pthreads with 1 GiB stacks
+// pulling an atomic work index (the CPU-baseline recipe of SURVEY §8(d)).
+// Writes per-kernel source hash/length when the arrays are non-null.
+// Returns wall seconds; *instructions gets the parse_text instruction count
+// (DecompiledKernel::instructions includes a synthetic trailing s_endpgm
+// only when a listing ends on a label; the synthetic generator never does).
+double ref_decompile_batch(const char *corpus, const uint64_t *offsets, size_t nkernels,
+                           int nthreads, uint64_t *out_hash, uint64_t *out_len,
+                           uint64_t *instructions) {
+    if (nthreads < 1)
+        nthreads = 1;
+    std::atomic<size_t> next{0};
+    std::vector<BatchJob> jobs(static_cast<size_t>(nthreads));
+    std::vector<pthread_t> threads(static_cast<size_t>(nthreads));
+    pthread_attr_t attr;
+    pthread_attr_init(&attr);
+    pthread_attr_setstacksize(&attr, kBigStack);
+    auto t0 = std::chrono::steady_clock::now();
+    for (int t = 0; t < nthreads; ++t) {
+        jobs[size_t(t)] = BatchJob{corpus, offsets, nkernels, &next, out_hash, out_len, 0};
+        pthread_create(&threads[size_t(t)], &attr, batch_worker, &jobs[size_t(t)]);
+    }
+    uint64_t total = 0;
+    for (int t = 0; t < nthreads; ++t) {
+        pthread_join(threads[size_t(t)], nullptr);
+        total += jobs[size_t(t)].instructions;
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    pthread_attr_destroy(&attr);
+    if (instructions)
+        *instructions = total;
+    return std::chrono::duration<double>(t1 - t0).count();
+}
+
+// The reference's 26-kernel test corpus (proj/tests/support/corpus.cpp).
+int ref_corpus_count(void) { return int(ocldec_tests::corpus().size()); }
+
+int ref_corpus_get(int i, char **name, char **listing, int *comparable, int *expected_fallbacks) {
+    const auto &ks = ocldec_tests::corpus();
+    if (i < 0 || size_t(i) >= ks.size())
+        return -1;
+    const auto &k = ks[size_t(i)];
+    *name = dup_out(k.name, nullptr);
+    *listing = dup_out(k.listing, nullptr);
+    *comparable = k.comparable ? 1 : 0;
+    *expected_fallbacks = k.expected_fallbacks;
+    return 0;
+}
+
+// The reference's deterministic nest generator (proj/tests/support/nestgen.cpp).
+char *ref_make_nest(uint64_t seed, int *conditionals) {
+    ocldec_tests::NestSpec spec = ocldec_tests::make_nest(seed);
+    if (conditionals)
+        *conditionals = spec.conditionals;
+    return dup_out(spec.listing, nullptr);
+}
+
+} // extern "C"

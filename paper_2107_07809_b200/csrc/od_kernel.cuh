@@ -1,0 +1,1718 @@
+// ocldec-b200: the per-kernel decompilation pipeline (passes P1c-P4a), run by
+// one thread per .kernel section over its own arena in HBM.
+//
+//   parse_config / type_from_arg_decl   asm_frontend.cpp:283-373, type_recovery.cpp:151-169
+//   build_abi_map / find / find_dword   abi_model.cpp:15-55, 155-245
+//   build_cfg / annotate_exec            cfg.cpp:64-226
+//   normalize_if_else (+ helpers)        structurizer.cpp:407-654
+//   RegionGraph / reduce / matchers      structurizer.cpp:70-403
+//   instruction_use_def / live_in_sets   cfg.cpp:230-398
+//   step / merge_at_join                 sym_state.cpp:56-957
+//   lower_kernel / lower_goto_form       lower.cpp:17-269
+//   hoist_fresh_decls / decompile_section decompiler.cpp:37-101
+//   emit_kernel / emit_statement         codegen.cpp:358-467
+//
+// Every data structure is a fixed-width array in the arena; recursion in the
+// reference (lower_region, render, expr_equal, fold_expr) is replaced by
+// explicit stacks, and RegisterFile snapshots by an undo log.
+#pragma once
+
+#include "od_parse.cuh"
+#include "od_render.cuh"
+
+namespace od {
+
+// ---------------------------------------------------------------- arena
+struct Bump {
+    u8 *base;
+    u64 top, cap;
+    bool oom;
+    template <class T> OD_INL T *get(u64 n) {
+        u64 a = (top + 15) & ~15ull;
+        u64 bytes = n * sizeof(T);
+        if (a + bytes > cap) {
+            oom = true;
+            return nullptr;
+        }
+        top = a + bytes;
+        return (T *)(base + a);
+    }
+};
+
+enum KStatus : u32 { KS_OK = 0, KS_FAILED = 1, KS_OOM = 2, KS_SPLIT_ERROR = 3 };
+
+// Inputs for one kernel section.
+struct KIn {
+    const u8 *t;          // listing bytes (+ aux area)
+    const LineRec *lines; // chunk line records
+    const LineIns *lins;  // decoded text lines
+    const Opnd *ops;      // operand pool
+    const Label *labs;    // label pool
+    u32 lbeg, lend;       // [.kernel line, next .kernel line) (chunk-relative)
+    u32 line_base;        // global 1-based line number of chunk line 0 is line_base + 1
+    u32 fold_local_size;
+};
+
+struct KOut {
+    u32 status;
+    u32 structured;
+    u32 fallbacks;
+    u32 ninstr;      // parse_text instructions (synthetic s_endpgm excluded)
+    u32 out_len;     // bytes of source written to the writer
+};
+
+// -------------------------------------------------------- instructions
+enum ExecKind : u8 { XK_NONE = 0, XK_SAVE, XK_INVERT, XK_RESTORE };
+
+struct Ins {
+    u16 root;
+    u8 prefix;
+    u8 rflags;
+    u16 sfx[2];
+    u16 nops;
+    u8 flags;
+    u8 xkind;      // static exec-op classification (annotate_exec), suppression aside
+    u32 xmask;     // saved-mask first SGPR
+    u32 op_start;  // operand pool index
+    u32 line;      // 1-based listing line
+    Span src;      // source_text
+    u32 lab_b, lab_n; // labels (indices into the kernel label list)
+};
+
+enum TermKind : u8 { T_FALL = 0, T_UNCOND, T_COND, T_END };
+enum CondCode : u8 { C_SCC0 = 0, C_SCC1, C_VCCZ, C_VCCNZ, C_EXECZ, C_EXECNZ, C_MASKED };
+
+struct Term {
+    u8 kind, cc;
+    u16 pad;
+    i32 taken, not_taken;
+    Opnd mask_source;
+    u32 line;
+};
+
+OD_INL void term_default(Term &t) {
+    t.kind = T_FALL;
+    t.cc = C_SCC0;
+    t.pad = 0;
+    t.taken = -1;
+    t.not_taken = -1;
+    t.mask_source.kind = OK_ANNOT; // Operand{} default: Annotation, count 1
+    t.mask_source.special = SP_EXEC;
+    t.mask_source.pad = 0;
+    t.mask_source.count = 1;
+    t.mask_source.value = 0;
+    t.line = 0;
+}
+
+struct XOp {
+    u8 kind;   // ExecKind (0 = none)
+    u32 index; // within block
+    u32 mask;
+    u32 ins;   // global instruction index
+};
+
+struct Block {
+    u32 ib, ie;       // instruction range
+    u32 lab_b, lab_n; // labels of the leader (split-off blocks: none)
+    Term term;
+    i32 succ[2];
+    u8 nsucc;
+    u8 reachable;
+    u8 absorbed;
+    u8 pad;
+    XOp xfront, xback; // annotate_exec: first / last exec op
+};
+
+// ------------------------------------------------------------ regions
+enum RKind : u8 { RK_BLOCK = 0, RK_LINEAR, RK_IFTHEN, RK_IFELSE };
+
+struct Region {
+    u8 kind;
+    u8 join_absorbed;
+    u8 cc;
+    u8 then_is_taken;
+    i32 block_id;
+    i32 join_block;
+    u8 has_term; // cond came from a terminator (make_cond(term))
+    u8 pad[3];
+    Opnd mask_source;
+    u32 ch_b, ch_n; // children (region ids) in the child pool
+    i32 succ[2];
+    u32 nsucc;
+};
+
+// -------------------------------------------------------------- lowering
+enum Integrity : u8 { IN_ENTIRE = 0, IN_LOW, IN_HIGH };
+
+struct Slot {
+    u32 version;
+    u32 expr;
+    DT type;
+    u8 integ;
+    u8 pad[3];
+};
+
+struct UndoRec {
+    u32 phys;
+    u32 version;
+    u32 expr;
+    DT type;
+    u32 integ;
+};
+
+struct Pending {
+    u32 valid;
+    u32 lo_vgpr;
+    u32 lo_version;
+    u32 base64;
+    u32 addend;
+};
+
+enum SKind : u8 { SK_ASSIGN = 0, SK_DECL, SK_STORE, SK_RAW, SK_IF, SK_LABEL, SK_GOTO };
+
+struct Stmt {
+    u8 kind;
+    u8 pad;
+    u16 cls;   // Assign/Decl: var name class
+    u32 next;  // list link (0 = end)
+    u32 a;     // Assign/Decl: var number; Store: addr; If/Goto: cond; Raw: text off; Label/Goto: block
+    u32 b;     // Assign/Decl/Store: value; If: then head; Raw: text len
+    u32 c;     // Decl: type; Store: elem type; If: else head; Goto: target block
+    u32 d;     // Raw/Goto/Label spare
+};
+
+struct SList {
+    u32 head, tail;
+};
+
+struct Fresh {
+    u32 cls, num;
+    DT type;
+};
+
+// One lowering frame (lower_region made iterative).
+struct Frame {
+    u32 region;
+    u32 phase;
+    u32 out;       // SList index receiving statements
+    u32 then_l;    // SList index (If)
+    u32 else_l;    // SList index (If)
+    u32 cond;      // If condition
+    u32 log_p0;    // undo log position at the split
+    u32 dstk_p0;   // delta stack position
+    u32 then_d, then_n; // then-arm delta (slot records in delta stack)
+    u32 child;     // Linear: next child
+    Pending pend;  // pending add at the split
+};
+
+// Name set (std::set<std::string> name_pool / hoist dedup) as open addressing
+// over (class, number) keys.
+struct NameSet {
+    u64 *keys; // 0 = empty; key = (cls+1)<<32 | num
+    u32 cap, count;
+    bool oom;
+    OD_INL bool insert(u32 cls, u32 num) {
+        u64 k = ((u64)(cls + 1) << 32) | num;
+        if (count * 2 >= cap) {
+            oom = true;
+            return true;
+        }
+        u64 h = k * 0x9E3779B97F4A7C15ull;
+        u32 i = (u32)(h >> 32) & (cap - 1);
+        while (keys[i]) {
+            if (keys[i] == k)
+                return false;
+            i = (i + 1) & (cap - 1);
+        }
+        keys[i] = k;
+        ++count;
+        return true;
+    }
+};
+
+struct AbiEntry {
+    u32 offset;
+    u8 dwords;
+    u8 has_builtin;
+    u8 fn;
+    u8 dim;
+    i32 arg_index;
+    DT type;
+};
+
+// The whole per-kernel working set.
+struct KCtx {
+    const KIn *in;
+    Bump *mem;
+    bool failed;  // ParseError
+    bool oom;
+
+    KConfig cfg;
+    Span *arg_sname;
+    AbiEntry *abi;
+    u32 nabi;
+
+    Ins *ins;
+    u32 nins, nins_real;
+    u32 *kl;     // kernel label list (global label pool indices)
+    u32 nkl;
+    u8 *supp;    // suppressed flag per instruction
+
+    Block *blk;
+    u32 nblk, blk_cap;
+    u32 *stamp;  // per-block traversal stamps
+    u32 stamp_gen;
+    u32 *work;   // block work stack
+
+    // label map
+    u32 *lmap;   // label-list index + 1 (0 empty)
+    u32 lmap_cap;
+
+    // regions
+    Region *rg;  // 1-based
+    u32 nrg, rg_cap;
+    u32 *child;  // child pool
+    u32 nchild, child_cap;
+    u32 *live;   // live region list
+    u32 nlive;
+    u32 *pred_b, *pred_n, *pred_l; // CSR preds per region
+    u32 *rstamp; // region stamps
+    u32 rstamp_gen;
+    u32 *rpo;    // rpo output
+    u32 *dfs;    // dfs stack (pairs)
+    i32 entry_r;
+    u32 root_r;
+    bool reduced;
+
+    // liveness
+    u32 *live_in; // [nblk][12]
+
+    // expressions / lowering
+    EArena E;
+    FoldScratch fs;
+    U32Stack eqst;
+    Slot *regs;   // kPhysSlots
+    UndoRec *log;
+    u32 nlog, log_cap;
+    u32 log_depth; // > 0 while inside an if arm
+    Pending pend;
+    Stmt *st;
+    u32 nst, st_cap;
+    SList *lists;
+    u32 nlists, lists_cap;
+    Fresh *fresh;
+    u32 nfresh, fresh_cap;
+    NameSet pool;
+    u32 fallbacks;
+    Frame *frames;
+    u32 nframes, frames_cap;
+    Slot *dstk;   // delta stack (values)
+    u32 *dstk_id; // delta stack (phys ids)
+    u32 ndstk, dstk_cap;
+
+    // rendering
+    RenderCtx rc;
+};
+
+OD_INL const Opnd &op_at(const KCtx &K, const Ins &I, u32 k) { return K.in->ops[I.op_start + k]; }
+OD_INL DT suffix_type0(const Ins &I, DT fb) { return I.sfx[0] ? dt_from_suffix(I.sfx[0]) : fb; }
+
+// ============================================================ config
+// split_fields (asm_frontend.cpp:80-107) returning up to maxf field spans;
+// the return value is the field count after dropping trailing empties.
+OD_INL u32 split_fields_spans(const u8 *t, Span s, Span *f, u32 maxf) {
+    int depth = 0;
+    bool inq = false;
+    u32 nf = 0, last_nonempty = 0;
+    u32 start = s.off, end = s.off + s.len;
+    for (u32 i = s.off; i <= end; ++i) {
+        bool cut = false;
+        if (i == end)
+            cut = true;
+        else {
+            u8 c = t[i];
+            if (c == '"')
+                inq = !inq;
+            if (!inq) {
+                if (c == '[' || c == '(')
+                    ++depth;
+                else if (c == ']' || c == ')')
+                    --depth;
+                else if (c == ',' && depth == 0)
+                    cut = true;
+            }
+        }
+        if (!cut)
+            continue;
+        u32 b = start, e = i;
+        while (b < e && c_space(t[b]))
+            ++b;
+        while (e > b && c_space(t[e - 1]))
+            --e;
+        if (i == end && e == b) {
+            // final empty field is never pushed
+        } else {
+            if (nf < maxf) {
+                f[nf].off = b;
+                f[nf].len = e - b;
+            }
+            ++nf;
+            if (e > b)
+                last_nonempty = nf;
+        }
+        start = i + 1;
+    }
+    return last_nonempty;
+}
+
+// type_from_arg_decl  type_recovery.cpp:151-169
+OD_INL DT type_from_arg_decl(const u8 *t, Span m, u32 space) {
+    u32 n = m.len;
+    u32 depth = 0;
+    while (n > 0 && t[m.off + n - 1] == '*') {
+        --n;
+        while (n > 0 && t[m.off + n - 1] == ' ')
+            --n;
+        ++depth;
+    }
+    Span nm = {m.off, n};
+    DT ty = DT_UNKNOWN;
+    if (span_eq(t, nm, "char")) ty = dt_make(B_SIGNED, 8);
+    else if (span_eq(t, nm, "uchar")) ty = dt_make(B_UNSIGNED, 8);
+    else if (span_eq(t, nm, "short")) ty = dt_make(B_SIGNED, 16);
+    else if (span_eq(t, nm, "ushort")) ty = dt_make(B_UNSIGNED, 16);
+    else if (span_eq(t, nm, "int")) ty = dt_make(B_SIGNED, 32);
+    else if (span_eq(t, nm, "uint")) ty = dt_make(B_UNSIGNED, 32);
+    else if (span_eq(t, nm, "long")) ty = dt_make(B_SIGNED, 64);
+    else if (span_eq(t, nm, "ulong")) ty = dt_make(B_UNSIGNED, 64);
+    else if (span_eq(t, nm, "size_t")) ty = dt_make(B_UNSIGNED, 64);
+    else if (span_eq(t, nm, "float")) ty = dt_make(B_FLOAT, 32);
+    else if (span_eq(t, nm, "double")) ty = dt_make(B_FLOAT, 64);
+    else if (span_eq(t, nm, "void")) ty = dt_make(B_VOID, 0);
+    else if (span_eq(t, nm, "structure")) ty = dt_make(B_UNSIGNED, 8);
+    for (u32 i = 0; i < depth; ++i)
+        ty = dt_pointer_to(ty, space);
+    return ty;
+}
+
+OD_INL bool sanitized_eq(const u8 *t, Span a, Span b) {
+    if (a.len != b.len)
+        return false;
+    for (u32 i = 0; i < a.len; ++i) {
+        u8 x = t[a.off + i], y = t[b.off + i];
+        if (x == '.')
+            x = '_';
+        if (y == '.')
+            y = '_';
+        if (x != y)
+            return false;
+    }
+    return true;
+}
+
+// parse_config  asm_frontend.cpp:283-373 (diagnostics are not materialized)
+OD_INL bool parse_config(KCtx &K) {
+    const KIn &in = *K.in;
+    const u8 *t = in.t;
+    KConfig &c = K.cfg;
+    c.dims = 1;
+    c.cws[0] = c.cws[1] = c.cws[2] = 1;
+    c.useargs = 0;
+    c.nargs = 0;
+    c.fold_local_size = in.fold_local_size;
+    // name: second word of the .kernel line
+    {
+        const LineRec &L = in.lines[in.lbeg];
+        Span w, rest, nm, extra;
+        split_word(t, Span{L.off, L.len}, &w, &rest);
+        split_word(t, rest, &nm, &extra);
+        c.name = nm;
+    }
+    u32 ncfg = 0;
+    for (u32 l = in.lbeg + 1; l < in.lend; ++l)
+        if (in.lines[l].role == LR_CONFIG)
+            ++ncfg;
+    c.args = K.mem->get<KArg>(ncfg + 1);
+    K.arg_sname = K.mem->get<Span>(ncfg + 1);
+    if (!c.args || !K.arg_sname)
+        return false;
+    for (u32 l = in.lbeg + 1; l < in.lend; ++l) {
+        const LineRec &L = in.lines[l];
+        if (L.role != LR_CONFIG)
+            continue;
+        Span w, rest;
+        split_word(t, Span{L.off, L.len}, &w, &rest);
+        Span key = w;
+        if (key.len && t[key.off] == '.') {
+            key.off++;
+            key.len--;
+        }
+        if (span_eq(t, key, "dims")) {
+            Span axes, extra;
+            split_word(t, rest, &axes, &extra);
+            u32 dims = 0;
+            bool ok = axes.len > 0;
+            for (u32 i = 0; i < axes.len; ++i) {
+                u8 ch = t[axes.off + i];
+                if (ch >= 'A' && ch <= 'Z')
+                    ch = ch - 'A' + 'a';
+                if (ch == 'x')
+                    dims = dims > 1 ? dims : 1;
+                else if (ch == 'y')
+                    dims = dims > 2 ? dims : 2;
+                else if (ch == 'z')
+                    dims = 3;
+                else
+                    ok = false;
+            }
+            if (ok)
+                c.dims = dims;
+        } else if (span_eq(t, key, "cws") || span_eq(t, key, "reqd_work_group_size")) {
+            Span f[4];
+            u32 nf = split_fields_spans(t, rest, f, 4);
+            if (nf == 0 || nf > 3)
+                continue;
+            for (u32 i = 0; i < nf; ++i) {
+                i64 v;
+                if (!parse_int(t + f[i].off, f[i].len, &v) || v <= 0)
+                    break;
+                c.cws[i] = (u32)v;
+            }
+        } else if (span_eq(t, key, "useargs")) {
+            c.useargs = 1;
+        } else if (span_eq(t, key, "arg")) {
+            Span f[4];
+            u32 nf = split_fields_spans(t, rest, f, 4);
+            if (nf < 3)
+                continue;
+            KArg &a = c.args[c.nargs];
+            a.name = f[0];
+            u32 space = AS_NONE;
+            Span mt = f[2];
+            if (nf > 3) {
+                if (span_eq(t, f[3], "global"))
+                    space = AS_GLOBAL;
+                else if (span_eq(t, f[3], "local"))
+                    space = AS_LOCAL;
+                else if (span_eq(t, f[3], "constant"))
+                    space = AS_CONSTANT;
+            } else {
+                for (u32 i = 0; i < mt.len; ++i)
+                    if (t[mt.off + i] == '*') {
+                        space = AS_GLOBAL;
+                        break;
+                    }
+            }
+            a.type = type_from_arg_decl(t, mt, space);
+            a.implicit = (a.name.len >= 2 && t[a.name.off] == '_' && t[a.name.off + 1] == '.');
+            // canonical sanitized-name id
+            u32 id = c.nargs;
+            for (u32 j = 0; j < c.nargs; ++j)
+                if (sanitized_eq(t, c.args[j].name, a.name)) {
+                    id = c.args[j].name_id;
+                    break;
+                }
+            a.name_id = id;
+            K.arg_sname[c.nargs] = a.name;
+            c.nargs++;
+        }
+    }
+    return true;
+}
+
+// ============================================================ ABI map
+OD_INL void abi_add(KCtx &K, const AbiEntry &e) {
+    u32 w = 0;
+    for (u32 i = 0; i < K.nabi; ++i)
+        if (!(K.abi[i].offset == e.offset && K.abi[i].dwords == e.dwords))
+            K.abi[w++] = K.abi[i];
+    K.nabi = w;
+    K.abi[K.nabi++] = e;
+}
+
+// build_abi_map  abi_model.cpp:155-245 (no overrides)
+OD_INL bool build_abi(KCtx &K) {
+    K.abi = K.mem->get<AbiEntry>(8 + K.cfg.nargs);
+    if (!K.abi)
+        return false;
+    K.nabi = 0;
+    if (K.cfg.useargs) {
+        const u32 off[7] = {0x0, 0x8, 0x10, 0xc, 0x10, 0x14, 0x20010};
+        const u8 dw[7] = {2, 2, 2, 1, 1, 1, 1};
+        const u8 fn[7] = {F_GLOBAL_OFFSET, F_GLOBAL_OFFSET, F_GLOBAL_OFFSET, F_GLOBAL_SIZE,
+                          F_GLOBAL_SIZE, F_GLOBAL_SIZE, F_WORK_DIM};
+        const u8 dm[7] = {0, 1, 2, 0, 1, 2, 0};
+        for (int i = 0; i < 7; ++i) {
+            AbiEntry e;
+            e.offset = off[i];
+            e.dwords = dw[i];
+            e.has_builtin = 1;
+            e.fn = fn[i];
+            e.dim = dm[i];
+            e.arg_index = -1;
+            e.type = fn[i] == F_GLOBAL_OFFSET ? DT_U64 : DT_U32;
+            abi_add(K, e);
+        }
+    }
+    u32 offset = 0;
+    const u8 *t = K.in->t;
+    for (u32 i = 0; i < K.cfg.nargs; ++i) {
+        const KArg &a = K.cfg.args[i];
+        u32 sz = dt_byte_size(a.type);
+        if (sz < 4)
+            sz = 4;
+        offset = (offset + sz - 1) & ~(sz - 1);
+        AbiEntry e;
+        e.offset = offset;
+        e.dwords = (u8)(sz / 4 > 1 ? sz / 4 : 1);
+        e.has_builtin = 0;
+        e.fn = 0;
+        e.dim = 0;
+        e.arg_index = (i32)i;
+        e.type = a.type;
+        if (a.implicit && a.name.len == 17 && starts_with(t + a.name.off, a.name.len, "_.global_offset_")) {
+            u8 last = t[a.name.off + 16];
+            if (last >= '0' && last <= '2') {
+                e.has_builtin = 1;
+                e.fn = F_GLOBAL_OFFSET;
+                e.dim = last - '0';
+            }
+        }
+        if (e.dwords <= 2)
+            abi_add(K, e);
+        offset += sz;
+    }
+    return true;
+}
+
+OD_INL const AbiEntry *abi_find(const KCtx &K, u32 offset, u32 dwords) {
+    for (u32 i = 0; i < K.nabi; ++i)
+        if (K.abi[i].offset == offset && K.abi[i].dwords == dwords)
+            return &K.abi[i];
+    return nullptr;
+}
+
+OD_INL const AbiEntry *abi_find_dword(const KCtx &K, u32 offset, bool *second) {
+    *second = false;
+    for (u32 i = 0; i < K.nabi; ++i)
+        if (K.abi[i].offset == offset && K.abi[i].dwords == 1)
+            return &K.abi[i];
+    for (u32 i = 0; i < K.nabi; ++i)
+        if (K.abi[i].offset == offset && K.abi[i].dwords == 2)
+            return &K.abi[i];
+    for (u32 i = 0; i < K.nabi; ++i)
+        if (K.abi[i].dwords == 2 && K.abi[i].offset + 4 == offset) {
+            *second = true;
+            return &K.abi[i];
+        }
+    return nullptr;
+}
+
+// match_settings_load  builtin_detector.cpp:70-84
+OD_INL u32 match_settings_load(KCtx &K, u32 offset, u32 dwords) {
+    const AbiEntry *e = abi_find(K, offset, dwords);
+    if (!e)
+        return 0;
+    if (e->has_builtin)
+        return K.E.builtin(e->fn, e->dim, dwords == 2 ? DT_U64 : DT_U32);
+    if (e->arg_index >= 0 && (u32)e->arg_index < K.cfg.nargs)
+        return K.E.arg(K.cfg.args[e->arg_index].name_id, e->type);
+    return 0;
+}
+
+// ====================================================== instructions
+OD_INL void classify_exec(const KCtx &K, Ins &I) {
+    I.xkind = XK_NONE;
+    I.xmask = 0;
+    if ((I.flags & IF_PARSE_FAILED) || I.prefix != PX_S)
+        return;
+    const Opnd *o = K.in->ops + I.op_start;
+    u32 n = I.nops;
+    if (I.root == R_AND_SAVEEXEC && n >= 2 && o[0].kind == OK_SREG && o[0].count == 2) {
+        I.xkind = XK_SAVE;
+        I.xmask = o[0].r.a;
+        return;
+    }
+    bool dst_exec = n >= 1 && op_is_special(o[0], SP_EXEC);
+    if (!dst_exec)
+        return;
+    if (I.root == R_MOV && n >= 2 && op_is_sreg_pair(o[1])) {
+        I.xkind = XK_RESTORE;
+        I.xmask = o[1].r.a;
+        return;
+    }
+    if (I.root == R_OR && n >= 3) {
+        if (op_is_special(o[1], SP_EXEC) && op_is_sreg_pair(o[2])) {
+            I.xkind = XK_RESTORE;
+            I.xmask = o[2].r.a;
+            return;
+        }
+        if (op_is_special(o[2], SP_EXEC) && op_is_sreg_pair(o[1])) {
+            I.xkind = XK_RESTORE;
+            I.xmask = o[1].r.a;
+            return;
+        }
+    }
+    if ((I.root == R_ANDN2 || I.root == R_XOR) && n >= 3) {
+        if (op_is_sreg_pair(o[1]) && op_is_special(o[2], SP_EXEC)) {
+            I.xkind = XK_INVERT;
+            I.xmask = o[1].r.a;
+        } else if (op_is_sreg_pair(o[2]) && op_is_special(o[1], SP_EXEC)) {
+            I.xkind = XK_INVERT;
+            I.xmask = o[2].r.a;
+        }
+    }
+}
+
+// parse_text + attach_trailing_labels (asm_frontend.cpp:486-521,
+// decompiler.cpp:20-31)
+OD_INL bool collect_instructions(KCtx &K) {
+    const KIn &in = *K.in;
+    u32 nl = in.lend - in.lbeg;
+    K.ins = K.mem->get<Ins>(nl + 1);
+    u32 total_labels = 0;
+    for (u32 l = in.lbeg + 1; l < in.lend; ++l)
+        if (in.lines[l].role == LR_TEXT)
+            total_labels += in.lins[l].nlabels;
+    K.kl = K.mem->get<u32>(total_labels + 1);
+    if (!K.ins || !K.kl)
+        return false;
+    K.nins = 0;
+    K.nkl = 0;
+    u32 pend_b = 0;
+    u32 last_line = in.line_base + in.lbeg + 1; // section.line
+    for (u32 l = in.lbeg + 1; l < in.lend; ++l) {
+        if (in.lines[l].role != LR_TEXT)
+            continue;
+        const LineIns &L = in.lins[l];
+        for (u32 k = 0; k < L.nlabels; ++k)
+            K.kl[K.nkl++] = L.lab_start + k;
+        if (!(L.flags & IF_HAS_INS))
+            continue;
+        Ins &I = K.ins[K.nins++];
+        I.root = L.root;
+        I.prefix = L.prefix;
+        I.rflags = L.rflags;
+        I.sfx[0] = L.sfx[0];
+        I.sfx[1] = L.sfx[1];
+        I.nops = L.nops;
+        I.flags = L.flags;
+        I.op_start = L.op_start;
+        I.line = in.line_base + l + 1;
+        I.src.off = L.src_off;
+        I.src.len = L.src_len;
+        I.lab_b = pend_b;
+        I.lab_n = K.nkl - pend_b;
+        pend_b = K.nkl;
+        last_line = I.line;
+        classify_exec(K, I);
+    }
+    K.nins_real = K.nins;
+    if (K.nkl > pend_b) {
+        Ins &I = K.ins[K.nins++];
+        I.root = R_ENDPGM;
+        I.prefix = PX_S;
+        I.rflags = 0;
+        I.sfx[0] = I.sfx[1] = 0;
+        I.nops = 0;
+        I.flags = IF_HAS_INS | IF_SYNTH;
+        I.op_start = 0;
+        I.line = last_line;
+        I.src.off = 0;
+        I.src.len = 0;
+        I.lab_b = pend_b;
+        I.lab_n = K.nkl - pend_b;
+        I.xkind = XK_NONE;
+        I.xmask = 0;
+    }
+    return true;
+}
+
+// ============================================================== CFG
+OD_INL bool is_branch(const Ins &I) {
+    return I.prefix == PX_S && (I.root == R_BRANCH || (I.rflags & RF_CBRANCH));
+}
+OD_INL bool is_endpgm(const Ins &I) { return I.prefix == PX_S && I.root == R_ENDPGM; }
+
+OD_INL const Label &klabel(const KCtx &K, u32 kli) { return K.in->labs[K.kl[kli]]; }
+
+OD_INL void lmap_put(KCtx &K, u32 kli, u32 block) {
+    const Label &L = klabel(K, kli);
+    u32 i = (u32)(L.hash >> 32) & (K.lmap_cap - 1);
+    while (K.lmap[2 * i]) {
+        const Label &M = klabel(K, K.lmap[2 * i] - 1);
+        if (M.hash == L.hash && M.len == L.len && bytes_eq(K.in->t + M.off, K.in->t + L.off, L.len)) {
+            K.lmap[2 * i + 1] = block;
+            return;
+        }
+        i = (i + 1) & (K.lmap_cap - 1);
+    }
+    K.lmap[2 * i] = kli + 1;
+    K.lmap[2 * i + 1] = block;
+}
+
+OD_INL int lmap_get(const KCtx &K, Span name) {
+    u64 h = fnv1a64(K.in->t + name.off, name.len);
+    u32 i = (u32)(h >> 32) & (K.lmap_cap - 1);
+    while (K.lmap[2 * i]) {
+        const Label &M = klabel(K, K.lmap[2 * i] - 1);
+        if (M.hash == h && M.len == name.len &&
+            bytes_eq(K.in->t + M.off, K.in->t + name.off, name.len))
+            return (int)K.lmap[2 * i + 1];
+        i = (i + 1) & (K.lmap_cap - 1);
+    }
+    return -1;
+}
+
+OD_INL int resolve_target(KCtx &K, const Ins &I) {
+    if (I.nops == 0 || op_at(K, I, 0).kind != OK_SYMBOL) {
+        K.failed = true; // "branch without a label operand"
+        return -1;
+    }
+    const Opnd &o = op_at(K, I, 0);
+    int b = lmap_get(K, Span{o.r.a, o.r.b});
+    if (b < 0)
+        K.failed = true; // "branch to undefined label"
+    return b;
+}
+
+OD_INL void mark_reachable(KCtx &K) {
+    for (u32 b = 0; b < K.nblk; ++b)
+        K.blk[b].reachable = 0;
+    if (!K.nblk)
+        return;
+    u32 sp = 0;
+    K.work[sp++] = 0;
+    while (sp) {
+        u32 id = K.work[--sp];
+        Block &B = K.blk[id];
+        if (B.reachable)
+            continue;
+        B.reachable = 1;
+        for (u32 s = 0; s < B.nsucc; ++s)
+            K.work[sp++] = (u32)B.succ[s];
+    }
+}
+
+// build_cfg  cfg.cpp:64-156
+OD_INL bool build_cfg(KCtx &K) {
+    u32 n = K.nins;
+    K.blk_cap = n + 2;
+    K.blk = K.mem->get<Block>(K.blk_cap);
+    K.stamp = K.mem->get<u32>(K.blk_cap);
+    K.work = K.mem->get<u32>(2 * K.blk_cap + 4);
+    K.supp = K.mem->get<u8>(n + 1);
+    u32 lc = 16;
+    while (lc < 2 * (K.nkl + 1))
+        lc <<= 1;
+    K.lmap_cap = lc;
+    K.lmap = K.mem->get<u32>(2 * lc);
+    if (!K.blk || !K.stamp || !K.work || !K.supp || !K.lmap)
+        return false;
+    for (u32 i = 0; i < 2 * lc; ++i)
+        K.lmap[i] = 0;
+    for (u32 i = 0; i < n; ++i)
+        K.supp[i] = 0;
+    for (u32 i = 0; i < K.blk_cap; ++i)
+        K.stamp[i] = 0;
+    K.stamp_gen = 0;
+    K.nblk = 0;
+    if (n == 0) {
+        Block &B = K.blk[K.nblk++];
+        B.ib = B.ie = 0;
+        B.lab_b = B.lab_n = 0;
+        term_default(B.term);
+        B.term.kind = T_END;
+        B.nsucc = 0;
+        B.reachable = 1;
+        B.absorbed = 0;
+        B.xfront.kind = B.xback.kind = XK_NONE;
+        return true;
+    }
+    // leaders
+    for (u32 i = 0; i < n; ++i) {
+        const Ins &I = K.ins[i];
+        bool lead = i == 0 || I.lab_n > 0;
+        if (i > 0) {
+            const Ins &P = K.ins[i - 1];
+            if (is_branch(P) || is_endpgm(P))
+                lead = true;
+        }
+        if (lead) {
+            if (K.nblk)
+                K.blk[K.nblk - 1].ie = i;
+            Block &B = K.blk[K.nblk];
+            B.ib = i;
+            B.ie = n;
+            B.lab_b = I.lab_b;
+            B.lab_n = I.lab_n;
+            term_default(B.term);
+            B.nsucc = 0;
+            B.reachable = 1;
+            B.absorbed = 0;
+            B.xfront.kind = B.xback.kind = XK_NONE;
+            for (u32 k = 0; k < I.lab_n; ++k)
+                lmap_put(K, I.lab_b + k, K.nblk);
+            K.nblk++;
+        }
+    }
+    for (u32 bi = 0; bi < K.nblk && !K.failed; ++bi) {
+        Block &B = K.blk[bi];
+        const Ins &last = K.ins[B.ie - 1];
+        int next = bi + 1 < K.nblk ? (int)bi + 1 : -1;
+        Term &t = B.term;
+        t.line = last.line;
+        if (is_endpgm(last)) {
+            t.kind = T_END;
+        } else if (last.prefix == PX_S && last.root == R_BRANCH) {
+            t.kind = T_UNCOND;
+            t.taken = resolve_target(K, last);
+        } else if (last.prefix == PX_S && (last.rflags & RF_CBRANCH)) {
+            int cc = -1;
+            switch (last.root) {
+            case R_CBRANCH_SCC0: cc = C_SCC0; break;
+            case R_CBRANCH_SCC1: cc = C_SCC1; break;
+            case R_CBRANCH_VCCZ: cc = C_VCCZ; break;
+            case R_CBRANCH_VCCNZ: cc = C_VCCNZ; break;
+            case R_CBRANCH_EXECZ: cc = C_EXECZ; break;
+            case R_CBRANCH_EXECNZ: cc = C_EXECNZ; break;
+            default: break;
+            }
+            if (cc < 0 || next < 0) {
+                K.failed = true;
+                break;
+            }
+            t.kind = T_COND;
+            t.cc = (u8)cc;
+            t.taken = resolve_target(K, last);
+            t.not_taken = next;
+        } else if (next >= 0) {
+            t.kind = T_FALL;
+            t.taken = next;
+        } else {
+            t.kind = T_END;
+        }
+        if (t.kind == T_COND) {
+            B.succ[0] = t.taken;
+            B.succ[1] = t.not_taken;
+            B.nsucc = 2;
+        } else if (t.taken >= 0) {
+            B.succ[0] = t.taken;
+            B.nsucc = 1;
+        }
+    }
+    if (K.failed)
+        return true;
+    mark_reachable(K);
+    return true;
+}
+
+// annotate_exec for one block: first and last non-suppressed exec op.
+OD_INL void annotate_block(KCtx &K, u32 b) {
+    Block &B = K.blk[b];
+    B.xfront.kind = B.xback.kind = XK_NONE;
+    for (u32 i = B.ib; i < B.ie; ++i) {
+        if (K.supp[i])
+            continue;
+        const Ins &I = K.ins[i];
+        if (I.xkind == XK_NONE)
+            continue;
+        XOp x;
+        x.kind = I.xkind;
+        x.index = i - B.ib;
+        x.mask = I.xmask;
+        x.ins = i;
+        if (B.xfront.kind == XK_NONE)
+            B.xfront = x;
+        B.xback = x;
+    }
+}
+
+// split_block  structurizer.cpp:416-435
+OD_INL u32 split_block(KCtx &K, u32 id, u32 at) {
+    u32 nid = K.nblk++;
+    Block &B = K.blk[id];
+    Block &N = K.blk[nid];
+    N.ib = B.ib + at;
+    N.ie = B.ie;
+    N.lab_b = N.lab_n = 0;
+    N.term = B.term;
+    N.nsucc = B.nsucc;
+    N.succ[0] = B.succ[0];
+    N.succ[1] = B.succ[1];
+    N.reachable = 1; // BasicBlock default (reachability is not recomputed)
+    N.absorbed = 0;
+    N.xfront.kind = N.xback.kind = XK_NONE;
+    B.ie = B.ib + at;
+    term_default(B.term);
+    B.term.kind = T_FALL;
+    B.term.taken = (i32)nid;
+    B.term.line = K.ins[N.ib].line;
+    B.succ[0] = (i32)nid;
+    B.nsucc = 1;
+    return nid;
+}
+
+// canonicalize_exec_blocks run to its fixed point (structurizer.cpp:440-463,
+// 613-615).  The reference restarts its scan after every split; blocks
+// before the split point are already canonical and a split block becomes
+// canonical, so one forward pass over the growing block list performs the
+// identical split sequence.
+OD_INL void canonicalize(KCtx &K) {
+    for (u32 b = 0; b < K.nblk; ++b) {
+        Block &B = K.blk[b];
+        u32 size = B.ie - B.ib;
+        for (u32 i = B.ib; i < B.ie; ++i) {
+            if (K.supp[i])
+                continue;
+            const Ins &I = K.ins[i];
+            if (I.xkind == XK_NONE)
+                continue;
+            u32 index = i - B.ib;
+            if (I.xkind == XK_SAVE) {
+                bool tail = B.term.kind == T_COND && (B.term.cc == C_EXECZ || B.term.cc == C_EXECNZ);
+                u32 last = size - 1;
+                u32 want = tail ? last - 1 : last;
+                if (index < want) {
+                    split_block(K, b, index + 1);
+                    break;
+                }
+            } else if (index > 0) {
+                split_block(K, b, index);
+                break;
+            }
+        }
+    }
+    for (u32 b = 0; b < K.nblk; ++b)
+        annotate_block(K, b);
+}
+
+OD_INL bool first_exec_op_is(const KCtx &K, u32 b, u32 kind, u32 mask) {
+    const Block &B = K.blk[b];
+    if (B.xfront.kind == XK_NONE || B.ie == B.ib)
+        return false;
+    return B.xfront.kind == kind && B.xfront.mask == mask && B.xfront.index == 0;
+}
+
+// mask_stops  structurizer.cpp:482-507.  Returns the number of stops found
+// (saturating at 2) and the first in *stop.
+OD_INL u32 mask_stops(KCtx &K, const i32 *starts, u32 nstarts, u32 mask, i32 header, i32 *stop) {
+    u32 gen = ++K.stamp_gen;
+    u32 sp = 0;
+    u32 nstops = 0;
+    for (u32 s = 0; s < nstarts; ++s)
+        K.work[sp++] = (u32)starts[s];
+    while (sp) {
+        i32 id = (i32)K.work[--sp];
+        if (id < 0 || (u32)id >= K.nblk || K.stamp[id] == gen)
+            continue;
+        K.stamp[id] = gen;
+        const Block &B = K.blk[id];
+        if (id != header) {
+            if (first_exec_op_is(K, (u32)id, XK_INVERT, mask) ||
+                first_exec_op_is(K, (u32)id, XK_RESTORE, mask)) {
+                if (nstops == 0)
+                    *stop = id;
+                ++nstops;
+                continue;
+            }
+            if (B.xback.kind == XK_SAVE && B.xback.mask == mask)
+                continue;
+        }
+        for (u32 s = 0; s < B.nsucc; ++s)
+            K.work[sp++] = (u32)B.succ[s];
+    }
+    return nstops;
+}
+
+// retarget_preds  structurizer.cpp:512-525
+OD_INL void retarget_preds(KCtx &K, i32 from, i32 to, i32 keep) {
+    for (u32 p = 0; p < K.nblk; ++p) {
+        Block &P = K.blk[p];
+        bool is_pred = false;
+        for (u32 s = 0; s < P.nsucc; ++s)
+            if (P.succ[s] == from)
+                is_pred = true;
+        if (!is_pred || (i32)p == keep)
+            continue;
+        for (u32 s = 0; s < P.nsucc; ++s)
+            if (P.succ[s] == from)
+                P.succ[s] = to;
+        if (P.term.taken == from)
+            P.term.taken = to;
+        if (P.term.not_taken == from)
+            P.term.not_taken = to;
+    }
+}
+
+struct MaskPattern {
+    i32 header;
+    u32 mask;
+    u32 src_ins; // instruction holding the save (source operand = ops[1])
+    bool has_bypass;
+    i32 then_entry;
+    i32 bypass;
+};
+
+// apply_mask_pattern  structurizer.cpp:527-609
+OD_INL bool apply_mask_pattern(KCtx &K, const MaskPattern &pat, u32 *touched, u32 *ntouched) {
+    Block &h = K.blk[pat.header];
+    const u32 save_index = h.xback.index;
+    i32 stop = -1;
+    i32 starts[2] = {pat.then_entry, 0};
+    u32 ns = mask_stops(K, starts, 1, pat.mask, pat.header, &stop);
+    if (ns != 1)
+        return false; // "multiple join points" / "save without inversion or restore"
+    const i32 invert = first_exec_op_is(K, (u32)stop, XK_INVERT, pat.mask) ? stop : -1;
+    i32 then_entry = pat.then_entry, else_entry = -1, join = -1;
+    *ntouched = 0;
+    if (invert >= 0) {
+        Block &ib = K.blk[invert];
+        const bool invert_only = (ib.ie - ib.ib) <= 2 && ib.term.kind == T_COND && ib.term.cc == C_EXECZ;
+        if (pat.has_bypass && pat.bypass != invert)
+            return false;
+        if (invert_only) {
+            else_entry = ib.term.not_taken;
+            join = ib.term.taken;
+            K.supp[ib.ib] = 1;
+            if (ib.ie - ib.ib > 1)
+                K.supp[ib.ib + 1] = 1;
+            retarget_preds(K, invert, join, pat.header);
+            ib.absorbed = 1;
+            ib.nsucc = 0;
+        } else {
+            i32 rstop = -1;
+            u32 nr = mask_stops(K, ib.succ, ib.nsucc, pat.mask, invert, &rstop);
+            if (nr != 1 || !first_exec_op_is(K, (u32)rstop, XK_RESTORE, pat.mask))
+                return false; // "mask inversion without a matching restore"
+            else_entry = invert;
+            join = rstop;
+            K.supp[ib.ib] = 1;
+            retarget_preds(K, invert, join, pat.header);
+        }
+        touched[(*ntouched)++] = (u32)invert;
+    } else {
+        if (pat.has_bypass && pat.bypass != stop)
+            return false;
+        join = stop;
+    }
+    if (join >= 0) {
+        Block &jb = K.blk[join];
+        if (first_exec_op_is(K, (u32)join, XK_RESTORE, pat.mask))
+            K.supp[jb.ib] = 1;
+        touched[(*ntouched)++] = (u32)join;
+    }
+    K.supp[h.ib + save_index] = 1;
+    h.term.kind = T_COND;
+    h.term.cc = C_MASKED;
+    h.term.mask_source = op_at(K, K.ins[pat.src_ins], 1);
+    h.term.not_taken = then_entry;
+    h.term.taken = else_entry >= 0 ? else_entry : join;
+    h.succ[0] = h.term.taken;
+    h.succ[1] = h.term.not_taken;
+    h.nsucc = 2;
+    touched[(*ntouched)++] = (u32)pat.header;
+    mark_reachable(K);
+    return true;
+}
+
+// normalize_if_else  structurizer.cpp:613-654
+OD_INL void normalize(KCtx &K) {
+    canonicalize(K);
+    const u32 nb = K.nblk;
+    for (u32 scan = 0; scan < nb; ++scan) {
+        Block &b = K.blk[scan];
+        if (!b.reachable || b.xback.kind == XK_NONE)
+            continue;
+        const XOp op = b.xback;
+        if (op.kind != XK_SAVE || K.supp[b.ib + op.index])
+            continue;
+        MaskPattern pat;
+        pat.header = (i32)scan;
+        pat.mask = op.mask;
+        pat.src_ins = op.ins;
+        pat.has_bypass = false;
+        pat.bypass = -1;
+        if (b.term.kind == T_COND && b.term.cc == C_EXECZ) {
+            pat.has_bypass = true;
+            pat.then_entry = b.term.not_taken;
+            pat.bypass = b.term.taken;
+            if (b.ie > b.ib)
+                K.supp[b.ie - 1] = 1;
+        } else if (b.term.kind == T_FALL) {
+            pat.then_entry = b.term.taken;
+        } else {
+            continue;
+        }
+        u32 touched[4];
+        u32 nt = 0;
+        if (apply_mask_pattern(K, pat, touched, &nt)) {
+            for (u32 k = 0; k < nt; ++k)
+                annotate_block(K, touched[k]);
+        } else if (pat.has_bypass) {
+            Block &hb = K.blk[pat.header];
+            K.supp[hb.ie - 1] = 0;
+        }
+    }
+}
+
+// ========================================================== regions
+OD_INL i32 entry_block(const KCtx &K, u32 r) {
+    while (K.rg[r].kind != RK_BLOCK)
+        r = K.child[K.rg[r].ch_b];
+    return K.rg[r].block_id;
+}
+
+OD_INL i32 exit_block(const KCtx &K, u32 r) {
+    for (;;) {
+        const Region &R = K.rg[r];
+        switch (R.kind) {
+        case RK_BLOCK: return R.block_id;
+        case RK_LINEAR: r = K.child[R.ch_b + R.ch_n - 1]; break;
+        default:
+            if (!R.join_absorbed)
+                return -1;
+            r = K.child[R.ch_b + R.ch_n - 1];
+            break;
+        }
+    }
+}
+
+OD_INL u32 make_region(KCtx &K, u8 kind) {
+    u32 id = ++K.nrg;
+    Region &R = K.rg[id];
+    R.kind = kind;
+    R.join_absorbed = 0;
+    R.cc = C_SCC1;
+    R.then_is_taken = 0;
+    R.block_id = -1;
+    R.join_block = -1;
+    R.has_term = 0;
+    R.mask_source.kind = OK_ANNOT;
+    R.mask_source.special = SP_EXEC;
+    R.mask_source.pad = 0;
+    R.mask_source.count = 1;
+    R.mask_source.value = 0;
+    R.ch_b = K.nchild;
+    R.ch_n = 0;
+    R.nsucc = 0;
+    return id;
+}
+
+OD_INL void rebuild_region_preds(KCtx &K) {
+    for (u32 i = 0; i < K.nlive; ++i)
+        K.pred_n[K.live[i]] = 0;
+    for (u32 i = 0; i < K.nlive; ++i) {
+        const Region &R = K.rg[K.live[i]];
+        for (u32 s = 0; s < R.nsucc; ++s)
+            K.pred_n[R.succ[s]]++;
+    }
+    u32 acc = 0;
+    for (u32 i = 0; i < K.nlive; ++i) {
+        u32 r = K.live[i];
+        K.pred_b[r] = acc;
+        acc += K.pred_n[r];
+        K.pred_n[r] = 0;
+    }
+    for (u32 i = 0; i < K.nlive; ++i) {
+        u32 r = K.live[i];
+        const Region &R = K.rg[r];
+        for (u32 s = 0; s < R.nsucc; ++s) {
+            u32 t = (u32)R.succ[s];
+            K.pred_l[K.pred_b[t] + K.pred_n[t]++] = r;
+        }
+    }
+}
+
+OD_INL void region_add_edge(KCtx &K, u32 from, u32 to) {
+    Region &R = K.rg[from];
+    for (u32 s = 0; s < R.nsucc; ++s)
+        if ((u32)R.succ[s] == to)
+            return;
+    R.succ[R.nsucc++] = (i32)to;
+}
+
+// RegionGraph::from_cfg  structurizer.cpp:88-111
+OD_INL bool build_regions(KCtx &K) {
+    u32 cap = 2 * K.nblk + 4;
+    K.rg_cap = cap;
+    K.rg = K.mem->get<Region>(cap + 1);
+    K.child_cap = 4 * cap + 8;
+    K.child = K.mem->get<u32>(K.child_cap);
+    K.live = K.mem->get<u32>(cap + 1);
+    K.pred_b = K.mem->get<u32>(cap + 1);
+    K.pred_n = K.mem->get<u32>(cap + 1);
+    K.pred_l = K.mem->get<u32>(2 * cap + 4);
+    K.rstamp = K.mem->get<u32>(cap + 1);
+    K.rpo = K.mem->get<u32>(cap + 1);
+    K.dfs = K.mem->get<u32>(2 * cap + 4);
+    u32 *by_block = K.mem->get<u32>(K.nblk + 1);
+    if (!K.rg || !K.child || !K.live || !K.pred_b || !K.pred_n || !K.pred_l || !K.rstamp ||
+        !K.rpo || !K.dfs || !by_block)
+        return false;
+    for (u32 i = 0; i <= cap; ++i)
+        K.rstamp[i] = 0;
+    K.rstamp_gen = 0;
+    K.nrg = 0;
+    K.nchild = 0;
+    K.nlive = 0;
+    K.entry_r = -1;
+    for (u32 b = 0; b < K.nblk; ++b) {
+        by_block[b] = 0;
+        const Block &B = K.blk[b];
+        if (!B.reachable || B.absorbed)
+            continue;
+        u32 r = make_region(K, RK_BLOCK);
+        K.rg[r].block_id = (i32)b;
+        K.live[K.nlive++] = r;
+        if (K.entry_r < 0)
+            K.entry_r = (i32)r;
+        by_block[b] = r;
+        if (b == 0)
+            K.entry_r = (i32)r;
+    }
+    for (u32 b = 0; b < K.nblk; ++b) {
+        if (!by_block[b])
+            continue;
+        const Block &B = K.blk[b];
+        for (u32 s = 0; s < B.nsucc; ++s) {
+            u32 to = by_block[B.succ[s]];
+            if (to)
+                region_add_edge(K, by_block[b], to);
+        }
+    }
+    rebuild_region_preds(K);
+    return true;
+}
+
+OD_INL bool single_pred_is(const KCtx &K, u32 node, u32 pred) {
+    return K.pred_n[node] == 1 && K.pred_l[K.pred_b[node]] == pred;
+}
+
+// RegionGraph::replace  structurizer.cpp:141-185
+OD_INL void region_replace(KCtx &K, const u32 *old, u32 nold, u32 merged) {
+    u32 gen = ++K.rstamp_gen;
+    for (u32 i = 0; i < nold; ++i)
+        K.rstamp[old[i]] = gen;
+    Region &M = K.rg[merged];
+    M.nsucc = 0;
+    for (u32 i = 0; i < nold; ++i) {
+        const Region &O = K.rg[old[i]];
+        for (u32 s = 0; s < O.nsucc; ++s) {
+            u32 t = (u32)O.succ[s] == old[0] ? merged : (u32)O.succ[s];
+            if (t != merged && K.rstamp[t] == gen)
+                continue;
+            bool dup = false;
+            for (u32 k = 0; k < M.nsucc; ++k)
+                if ((u32)M.succ[k] == t)
+                    dup = true;
+            if (!dup && M.nsucc < 2)
+                M.succ[M.nsucc++] = (i32)t;
+        }
+    }
+    u32 w = 0;
+    for (u32 i = 0; i < K.nlive; ++i)
+        if (K.rstamp[K.live[i]] != gen)
+            K.live[w++] = K.live[i];
+    K.live[w++] = merged;
+    K.nlive = w;
+    for (u32 i = 0; i + 1 < K.nlive; ++i) {
+        Region &R = K.rg[K.live[i]];
+        i32 out[2];
+        u32 no = 0;
+        for (u32 s = 0; s < R.nsucc; ++s) {
+            u32 t = K.rstamp[R.succ[s]] == gen ? merged : (u32)R.succ[s];
+            bool dup = false;
+            for (u32 k = 0; k < no; ++k)
+                if ((u32)out[k] == t)
+                    dup = true;
+            if (!dup)
+                out[no++] = (i32)t;
+        }
+        R.nsucc = no;
+        for (u32 k = 0; k < no; ++k)
+            R.succ[k] = out[k];
+    }
+    rebuild_region_preds(K);
+    if (K.entry_r >= 0 && K.rstamp[K.entry_r] == gen)
+        K.entry_r = (i32)merged;
+}
+
+OD_INL const Term *header_term(const KCtx &K, u32 r, bool *usable) {
+    i32 ex = exit_block(K, r);
+    const Term *t = ex >= 0 ? &K.blk[ex].term : nullptr;
+    if (!t) {
+        *usable = true;
+        return nullptr;
+    }
+    *usable = t->kind == T_COND && t->cc != C_EXECZ && t->cc != C_EXECNZ;
+    return t;
+}
+
+OD_INL void set_cond(KCtx &K, u32 m, const Term *term, bool then_is_taken) {
+    Region &M = K.rg[m];
+    if (term) {
+        M.cc = term->cc;
+        M.mask_source = term->mask_source;
+        M.has_term = 1;
+    }
+    M.then_is_taken = then_is_taken ? 1 : 0;
+}
+
+OD_INL void push_children(KCtx &K, u32 m, const u32 *c, u32 n) {
+    Region &M = K.rg[m];
+    M.ch_b = K.nchild;
+    for (u32 i = 0; i < n; ++i)
+        K.child[K.nchild++] = c[i];
+    M.ch_n = n;
+}
+
+// match_if_else  structurizer.cpp:230-274
+OD_INL u32 match_if_else(KCtx &K, u32 r) {
+    const Region &R = K.rg[r];
+    if (R.nsucc != 2 || R.succ[0] == R.succ[1])
+        return 0;
+    bool usable;
+    const Term *term = header_term(K, r, &usable);
+    if (!usable)
+        return 0;
+    u32 a = (u32)R.succ[0], b = (u32)R.succ[1];
+    if (!single_pred_is(K, a, r) || !single_pred_is(K, b, r))
+        return 0;
+    const Region &A = K.rg[a], &B = K.rg[b];
+    if (A.nsucc != 1 || B.nsucc != 1 || A.succ[0] != B.succ[0])
+        return 0;
+    u32 j = (u32)A.succ[0];
+    if (j == r)
+        return 0;
+    u32 then_r = a, else_r = b;
+    if (term && term->kind == T_COND) {
+        if (entry_block(K, a) == term->taken) {
+            then_r = b;
+            else_r = a;
+        }
+    }
+    const bool absorb = K.pred_n[j] == 2;
+    if (K.nchild + 4 > K.child_cap || K.nrg + 1 > K.rg_cap) {
+        K.oom = true;
+        return 0;
+    }
+    u32 m = make_region(K, RK_IFELSE);
+    set_cond(K, m, term, false);
+    K.rg[m].join_block = entry_block(K, j);
+    u32 ch[4] = {r, then_r, else_r, j};
+    u32 n = absorb ? 4 : 3;
+    push_children(K, m, ch, n);
+    K.rg[m].join_absorbed = absorb ? 1 : 0;
+    region_replace(K, ch, n, m);
+    return m;
+}
+
+// match_if  structurizer.cpp:276-323
+OD_INL u32 match_if(KCtx &K, u32 r) {
+    const Region &R = K.rg[r];
+    if (R.nsucc != 2 || R.succ[0] == R.succ[1])
+        return 0;
+    bool usable;
+    const Term *term = header_term(K, r, &usable);
+    if (!usable)
+        return 0;
+    u32 then_r = 0;
+    u32 j = 0;
+    for (u32 k = 0; k < 2; ++k) {
+        u32 cand = (u32)R.succ[k];
+        u32 other = (u32)R.succ[1 - k];
+        if (!single_pred_is(K, cand, r))
+            continue;
+        const Region &C = K.rg[cand];
+        if (C.nsucc == 1 && (u32)C.succ[0] == other && other != r) {
+            then_r = cand;
+            j = other;
+            break;
+        }
+    }
+    if (!then_r)
+        return 0;
+    bool then_is_taken = false;
+    if (term && term->kind == T_COND)
+        then_is_taken = entry_block(K, then_r) == term->taken;
+    const bool absorb = K.pred_n[j] == 2;
+    if (K.nchild + 3 > K.child_cap || K.nrg + 1 > K.rg_cap) {
+        K.oom = true;
+        return 0;
+    }
+    u32 m = make_region(K, RK_IFTHEN);
+    set_cond(K, m, term, then_is_taken);
+    K.rg[m].join_block = entry_block(K, j);
+    u32 ch[3] = {r, then_r, j};
+    u32 n = absorb ? 3 : 2;
+    push_children(K, m, ch, n);
+    K.rg[m].join_absorbed = absorb ? 1 : 0;
+    region_replace(K, ch, n, m);
+    return m;
+}
+
+// match_linear  structurizer.cpp:325-352
+OD_INL u32 match_linear(KCtx &K, u32 r) {
+    u32 cb = K.nchild; // build the chain directly in the child pool
+    u32 n = 0;
+    if (cb + 1 > K.child_cap) {
+        K.oom = true;
+        return 0;
+    }
+    K.child[cb + n++] = r;
+    u32 cur = r;
+    for (;;) {
+        const Region &C = K.rg[cur];
+        if (C.nsucc != 1)
+            break;
+        u32 next = (u32)C.succ[0];
+        if (next == r || !single_pred_is(K, next, cur))
+            break;
+        if (K.rg[next].nsucc > 1)
+            break;
+        if (cb + n + 1 > K.child_cap) {
+            K.oom = true;
+            return 0;
+        }
+        K.child[cb + n++] = next;
+        cur = next;
+    }
+    if (n < 2)
+        return 0;
+    if (K.nrg + 1 > K.rg_cap) {
+        K.oom = true;
+        return 0;
+    }
+    u32 m = make_region(K, RK_LINEAR);
+    K.rg[m].ch_b = cb;
+    K.rg[m].ch_n = n;
+    K.nchild = cb + n;
+    region_replace(K, K.child + cb, n, m);
+    return m;
+}
+
+// RegionGraph::rpo  structurizer.cpp:113-139
+OD_INL u32 region_rpo(KCtx &K) {
+    if (K.entry_r < 0)
+        return 0;
+    u32 gen = ++K.rstamp_gen;
+    u32 sp = 0, npost = 0;
+    K.dfs[2 * sp] = (u32)K.entry_r;
+    K.dfs[2 * sp + 1] = 0;
+    ++sp;
+    K.rstamp[K.entry_r] = gen;
+    while (sp) {
+        u32 node = K.dfs[2 * (sp - 1)];
+        u32 &idx = K.dfs[2 * (sp - 1) + 1];
+        const Region &R = K.rg[node];
+        if (idx < R.nsucc) {
+            u32 s = (u32)R.succ[idx++];
+            if (K.rstamp[s] != gen) {
+                K.rstamp[s] = gen;
+                K.dfs[2 * sp] = s;
+                K.dfs[2 * sp + 1] = 0;
+                ++sp;
+            }
+        } else {
+            K.rpo[npost++] = node;
+            --sp;
+        }
+    }
+    // reverse in place
+    for (u32 i = 0; i < npost / 2; ++i) {
+        u32 x = K.rpo[i];
+        K.rpo[i] = K.rpo[npost - 1 - i];
+        K.rpo[npost - 1 - i] = x;
+    }
+    return npost;
+}
+
+// reduce  structurizer.cpp:354-403
+OD_INL void reduce(KCtx &K) {
+    bool progress = true;
+    while (progress && K.nlive > 1 && !K.oom) {
+        progress = false;
+        u32 n = region_rpo(K);
+        for (u32 i = 0; i < n; ++i) {
+            u32 r = K.rpo[i];
+            u32 m = match_if_else(K, r);
+            if (!m)
+                m = match_if(K, r);
+            if (!m)
+                m = match_linear(K, r);
+            if (!m)
+                continue;
+            progress = true;
+            break;
+        }
+    }
+    K.reduced = K.nlive == 1;
+    K.root_r = K.reduced ? K.live[0] : 0;
+}
+
+// ========================================================== liveness
+OD_INL void lv_mark(u32 *set, u32 id) {
+    if (id < kNumRegIds)
+        set[id >> 5] |= 1u << (id & 31);
+}
+
+// add_operand_regs  cfg.cpp:230-265
+OD_INL void add_operand_regs(const Opnd &op, u32 *set) {
+    switch (op.kind) {
+    case OK_SREG:
+        for (u32 i = 0; i < op.count && op.r.a + i < kNumRegIds; ++i)
+            lv_mark(set, op.r.a + i);
+        break;
+    case OK_VREG:
+        for (u32 i = 0; i < op.count && kRegIdVgpr0 + op.r.a + i < kNumRegIds; ++i)
+            lv_mark(set, kRegIdVgpr0 + op.r.a + i);
+        break;
+    case OK_SPECIAL:
+        switch (op.special) {
+        case SP_EXEC:
+            lv_mark(set, kRegIdExecLo);
+            lv_mark(set, kRegIdExecHi);
+            break;
+        case SP_EXEC_LO: lv_mark(set, kRegIdExecLo); break;
+        case SP_EXEC_HI: lv_mark(set, kRegIdExecHi); break;
+        case SP_VCC:
+            lv_mark(set, kRegIdVccLo);
+            lv_mark(set, kRegIdVccHi);
+            break;
+        case SP_VCC_LO: lv_mark(set, kRegIdVccLo); break;
+        case SP_VCC_HI: lv_mark(set, kRegIdVccHi); break;
+        case SP_SCC: lv_mark(set, kRegIdScc); break;
+        case SP_M0: lv_mark(set, kRegIdM0); break;
+        }
+        break;
+    default:
+        break;
+    }
+}
+
+// instruction_use_def  cfg.cpp:272-352
+OD_INL void instruction_use_def(const KCtx &K, const Ins &I, u32 *use, u32 *def) {
+    const Opnd *o = K.in->ops + I.op_start;
+    const u32 n = (I.flags & IF_SYNTH) ? 0 : I.nops;
+    if (I.flags & IF_PARSE_FAILED) {
+        for (u32 k = 0; k < n; ++k)
+            add_operand_regs(o[k], use);
+        return;
+    }
+    const u32 root = I.root;
+    const u32 px = I.prefix;
+    if (px == PX_S && (root == R_WAITCNT || root == R_NOP || root == R_ENDPGM || root == R_BARRIER))
+        return;
+    if (px == PX_S && root == R_BRANCH)
+        return;
+    if (px == PX_S && (I.rflags & RF_CBRANCH)) {
+        if (root == R_CBRANCH_SCC0 || root == R_CBRANCH_SCC1) {
+            lv_mark(use, kRegIdScc);
+        } else if (root == R_CBRANCH_VCCZ || root == R_CBRANCH_VCCNZ) {
+            lv_mark(use, kRegIdVccLo);
+            lv_mark(use, kRegIdVccHi);
+        } else {
+            lv_mark(use, kRegIdExecLo);
+            lv_mark(use, kRegIdExecHi);
+        }
+        return;
+    }
+    if (px == PX_FLAT && (I.rflags & RF_STORE)) {
+        for (u32 k = 0; k < n; ++k)
+            add_operand_regs(o[k], use);
+        return;
+    }
+    if (px == PX_S && (I.rflags & RF_CMP)) {
+        for (u32 k = 0; k < n; ++k)
+            add_operand_regs(o[k], use);
+        lv_mark(def, kRegIdScc);
+        return;
+    }
+    if (px == PX_S && root == R_AND_SAVEEXEC && n > 0) {
+        add_operand_regs(o[0], def);
+        for (u32 k = 1; k < n; ++k)
+            add_operand_regs(o[k], use);
+        lv_mark(use, kRegIdExecLo);
+        lv_mark(use, kRegIdExecHi);
+        lv_mark(def, kRegIdExecLo);
+        lv_mark(def, kRegIdExecHi);
+        return;
+    }
+    u32 ndefs = 1;
+    if (px == PX_V && (root == R_ADD || root == R_SUB || root == R_SUBREV || root == R_ADDC) &&
+        n >= 2 && (op_is_special(o[1], SP_VCC) || op_is_sreg_pair(o[1])))
+        ndefs = 2;
+    const bool reads_dst = (px == PX_S && (root == R_ADDK || root == R_MULK)) || (px == PX_V && root == R_MAC);
+    for (u32 k = 0; k < n; ++k) {
+        if (k < ndefs) {
+            add_operand_regs(o[k], def);
+            if (reads_dst && k == 0)
+                add_operand_regs(o[k], use);
+        } else {
+            add_operand_regs(o[k], use);
+        }
+    }
+    if (px == PX_S && n >= 1 &&
+        (root == R_ADD || root == R_SUB || root == R_ADDK || root == R_MULK || root == R_AND ||
+         root == R_OR || root == R_XOR || root == R_ANDN2 || root == R_LSHL || root == R_LSHR ||
+         root == R_ASHR))
+        lv_mark(def, kRegIdScc);
+}
+
+// live_in_sets  cfg.cpp:356-398 (word-parallel; the least fixpoint is
+// unique, so iteration order does not matter)
+OD_INL bool liveness(KCtx &K) {
+    const u32 nb = K.nblk;
+    u32 *use = K.mem->get<u32>((u64)nb * kLiveWords);
+    u32 *def = K.mem->get<u32>((u64)nb * kLiveWords);
+    K.live_in = K.mem->get<u32>((u64)nb * kLiveWords);
+    if (!use || !def || !K.live_in)
+        return false;
+    for (u32 b = 0; b < nb; ++b) {
+        u32 *U = use + b * kLiveWords, *D = def + b * kLiveWords;
+        for (u32 w = 0; w < kLiveWords; ++w) {
+            U[w] = 0;
+            D[w] = 0;
+            K.live_in[b * kLiveWords + w] = 0;
+        }
+        const Block &B = K.blk[b];
+        for (u32 i = B.ib; i < B.ie; ++i) {
+            if (K.supp[i])
+                continue;
+            u32 iu[kLiveWords], id[kLiveWords];
+            for (u32 w = 0; w < kLiveWords; ++w)
+                iu[w] = id[w] = 0;
+            instruction_use_def(K, K.ins[i], iu, id);
+            for (u32 w = 0; w < kLiveWords; ++w) {
+                U[w] |= iu[w] & ~D[w];
+                D[w] |= id[w];
+            }
+        }
+    }
+    bool changed = true;
+    while (changed) {
+        changed = false;
+        for (u32 bi = nb; bi-- > 0;) {
+            const Block &B = K.blk[bi];
+            u32 *L = K.live_in + bi * kLiveWords;
+            for (u32 w = 0; w < kLiveWords; ++w) {
+                u32 out = 0;
+                for (u32 s = 0; s < B.nsucc; ++s)
+                    out |= K.live_in[(u32)B.succ[s] * kLiveWords + w];
+                u32 in = use[bi * kLiveWords + w] | (out & ~def[bi * kLiveWords + w]);
+                if (in != L[w]) {
+                    L[w] = in;
+                    changed = true;
+                }
+            }
+        }
+    }
+    return true;
+}
+
+OD_INL bool lv_test(const u32 *set, u32 id) { return (set[id >> 5] >> (id & 31)) & 1; }
+
+} // namespace od
+
+#include "od_lower.cuh"

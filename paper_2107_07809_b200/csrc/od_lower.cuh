@@ -1,0 +1,1490 @@
+// ocldec-b200: symbolic lowering (sym_state.cpp, lower.cpp), decl hoisting
+// (decompiler.cpp:37-53) and kernel emission (codegen.cpp:358-467).
+//
+// RegisterFile copies at if-splits (lower.cpp:143-147) are replaced by an
+// undo log: the then arm runs in place, its touched slots are saved as a
+// sorted delta and rolled back, the else arm runs, and the merge visits only
+// the union of touched slots in ascending register id (the order of
+// merge_at_join's 0..365 loop, sym_state.cpp:876).
+#pragma once
+
+namespace od {
+
+// ------------------------------------------------------- register file
+OD_INL u32 dense_of_phys(u32 p) {
+    if (p < 360)
+        return p;
+    switch (p) {
+    case 360: return kRegIdExecLo;
+    case 361: return kRegIdVccLo;
+    case 362: return kRegIdScc;
+    default: return kRegIdM0;
+    }
+}
+
+OD_INL void log_slot(KCtx &K, u32 p) {
+    if (!K.log_depth)
+        return;
+    if (K.nlog >= K.log_cap) {
+        K.oom = true;
+        return;
+    }
+    UndoRec &u = K.log[K.nlog++];
+    const Slot &s = K.regs[p];
+    u.phys = p;
+    u.version = s.version;
+    u.expr = s.expr;
+    u.type = s.type;
+    u.integ = s.integ;
+}
+
+OD_INL void undo_to(KCtx &K, u32 pos) {
+    while (K.nlog > pos) {
+        const UndoRec &u = K.log[--K.nlog];
+        Slot &s = K.regs[u.phys];
+        s.version = u.version;
+        s.expr = u.expr;
+        s.type = u.type;
+        s.integ = (u8)u.integ;
+    }
+}
+
+OD_INL void record_fresh(KCtx &K, u32 cls, u32 num, DT t) {
+    if (K.nfresh >= K.fresh_cap) {
+        K.oom = true;
+        return;
+    }
+    Fresh &f = K.fresh[K.nfresh++];
+    f.cls = cls;
+    f.num = num;
+    f.type = t;
+}
+
+// bind_fresh  sym_state.cpp:63-78
+OD_INL u32 bind_fresh(KCtx &K, u32 p, DT t = DT_B32) {
+    Slot &s = K.regs[p];
+    if (!s.expr) {
+        log_slot(K, p);
+        if (dt_is_unknown(s.type))
+            s.type = t;
+        s.expr = K.E.var(p, s.version, s.type);
+        s.integ = IN_ENTIRE;
+        record_fresh(K, p, s.version, s.type);
+        K.pool.insert(p, s.version);
+    }
+    return s.expr;
+}
+
+// read_slot32  sym_state.cpp:82-94
+OD_INL u32 read_slot32(KCtx &K, u32 id) {
+    u32 p = phys_of(id);
+    bind_fresh(K, p);
+    const Slot &s = K.regs[p];
+    if (s.integ == IN_LOW)
+        return K.E.unary(U_LO32, s.expr, DT_B32);
+    if (s.integ == IN_HIGH)
+        return K.E.unary(U_HI32, s.expr, DT_B32);
+    return s.expr;
+}
+
+// concat64  sym_state.cpp:96-105
+OD_INL u32 concat64(KCtx &K, u32 lo, u32 hi) {
+    EArena &E = K.E;
+    if (E.is_const_v(hi, 0))
+        return E.unary(U_CAST, lo, DT_U64);
+    if (lo && hi && E.n[lo].kind == E_UNARY && E.n[lo].op == U_LO32 && E.n[hi].kind == E_UNARY &&
+        E.n[hi].op == U_HI32 && expr_equal(E, E.n[lo].a, E.n[hi].a, K.eqst))
+        return E.n[lo].a;
+    return E.binary(O_CONCAT64, lo, hi, DT_B64);
+}
+
+// read_pair_ids  sym_state.cpp:107-114.  The two read_slot32 calls are
+// arguments of one call; GCC (the oracle's compiler) evaluates them right to
+// left, which fixes the order fresh variables are recorded in.
+OD_INL u32 read_pair_ids(KCtx &K, u32 lo_id) {
+    const Slot &lo = K.regs[phys_of(lo_id)];
+    const Slot &hi = K.regs[phys_of(lo_id + 1)];
+    if (lo.expr && lo.expr == hi.expr && lo.integ == IN_LOW && hi.integ == IN_HIGH)
+        return lo.expr;
+    u32 h = read_slot32(K, lo_id + 1);
+    u32 l = read_slot32(K, lo_id);
+    return concat64(K, l, h);
+}
+
+// dissolve_pair  sym_state.cpp:118-135
+OD_INL void dissolve_pair(KCtx &K, u32 id) {
+    u32 p = phys_of(id);
+    Slot &s = K.regs[p];
+    if (s.integ == IN_ENTIRE || !s.expr)
+        return;
+    const bool is_low = s.integ == IN_LOW;
+    if (id >= kRegIdExecLo) {
+        log_slot(K, p);
+        s.integ = IN_ENTIRE;
+        return;
+    }
+    u32 pid = is_low ? id + 1 : id - 1;
+    if (pid >= kRegIdExecLo) { // out of the reference's std::array range
+        K.oom = true;
+        return;
+    }
+    Slot &q = K.regs[pid];
+    if (q.expr == s.expr) {
+        log_slot(K, pid);
+        q.expr = K.E.unary(is_low ? U_HI32 : U_LO32, s.expr, DT_B32);
+        q.integ = IN_ENTIRE;
+        q.type = DT_B32;
+    }
+    log_slot(K, p);
+    s.integ = IN_ENTIRE;
+}
+
+OD_INL void write_slot32(KCtx &K, u32 id, u32 value, DT t) {
+    if (id >= kNumRegIds) {
+        K.oom = true;
+        return;
+    }
+    dissolve_pair(K, id);
+    u32 p = phys_of(id);
+    log_slot(K, p);
+    Slot &s = K.regs[p];
+    s.version += 1;
+    s.expr = value;
+    s.type = t;
+    s.integ = IN_ENTIRE;
+}
+
+OD_INL void write_pair_ids(KCtx &K, u32 lo_id, u32 value, DT t) {
+    if (lo_id >= kRegIdExecLo) {
+        if (lo_id >= kNumRegIds) {
+            K.oom = true;
+            return;
+        }
+        u32 p = phys_of(lo_id);
+        log_slot(K, p);
+        Slot &s = K.regs[p];
+        s.version += 1;
+        s.expr = value;
+        s.type = t;
+        s.integ = IN_ENTIRE;
+        return;
+    }
+    if (lo_id + 1 >= kRegIdExecLo) {
+        K.oom = true;
+        return;
+    }
+    dissolve_pair(K, lo_id);
+    dissolve_pair(K, lo_id + 1);
+    log_slot(K, lo_id);
+    log_slot(K, lo_id + 1);
+    Slot &lo = K.regs[lo_id];
+    Slot &hi = K.regs[lo_id + 1];
+    lo.version += 1;
+    hi.version += 1;
+    lo.expr = value;
+    hi.expr = value;
+    lo.type = t;
+    hi.type = t;
+    lo.integ = IN_LOW;
+    hi.integ = IN_HIGH;
+}
+
+// invalidate_slot  sym_state.cpp:169-180
+OD_INL void invalidate_slot(KCtx &K, u32 id, u32 count) {
+    for (u32 i = 0; i < count; ++i) {
+        if (id + i >= kNumRegIds) {
+            K.oom = true; // std::array::at would throw in the reference
+            return;
+        }
+        dissolve_pair(K, id + i);
+        u32 p = phys_of(id + i);
+        log_slot(K, p);
+        Slot &s = K.regs[p];
+        s.version += 1;
+        s.expr = 0;
+        s.type = DT_UNKNOWN;
+        s.integ = IN_ENTIRE;
+        if (id + i >= kRegIdExecLo)
+            break;
+    }
+}
+
+OD_INL u32 operand_reg_id(const Opnd &o) {
+    switch (o.kind) {
+    case OK_SREG: return o.r.a;
+    case OK_VREG: return kRegIdVgpr0 + o.r.a;
+    case OK_SPECIAL:
+        switch (o.special) {
+        case SP_EXEC:
+        case SP_EXEC_LO: return kRegIdExecLo;
+        case SP_EXEC_HI: return kRegIdExecHi;
+        case SP_VCC:
+        case SP_VCC_LO: return kRegIdVccLo;
+        case SP_VCC_HI: return kRegIdVccHi;
+        case SP_SCC: return kRegIdScc;
+        default: return kRegIdM0;
+        }
+    default: return kNumRegIds;
+    }
+}
+
+OD_INL u32 read_pair(KCtx &K, const Opnd &o);
+
+// read_operand  sym_state.cpp:205-227
+OD_INL u32 read_operand(KCtx &K, const Opnd &o) {
+    switch (o.kind) {
+    case OK_LITERAL: return K.E.constant((u64)o.value & 0xffffffffull, DT_B32);
+    case OK_SREG:
+    case OK_VREG: {
+        if (o.count >= 2)
+            return read_pair(K, o);
+        u32 id = operand_reg_id(o);
+        if (id >= kNumRegIds) {
+            K.oom = true;
+            return 0;
+        }
+        return read_slot32(K, id);
+    }
+    case OK_SPECIAL: {
+        u32 id = operand_reg_id(o);
+        DT t = (o.special == SP_EXEC || o.special == SP_VCC) ? DT_B64 : DT_B32;
+        return bind_fresh(K, phys_of(id), t);
+    }
+    default: return 0;
+    }
+}
+
+// read_pair  sym_state.cpp:229-240
+OD_INL u32 read_pair(KCtx &K, const Opnd &o) {
+    if (o.kind == OK_LITERAL)
+        return K.E.constant((u64)o.value, DT_B64);
+    if (o.kind == OK_SPECIAL)
+        return read_operand(K, o);
+    if (o.kind == OK_SREG || o.kind == OK_VREG) {
+        u32 id = operand_reg_id(o);
+        if (id + 1 >= kNumRegIds) {
+            K.oom = true;
+            return 0;
+        }
+        if (o.count < 2)
+            return read_slot32(K, id);
+        return read_pair_ids(K, id);
+    }
+    return 0;
+}
+
+// ------------------------------------------------------- statements
+OD_INL u32 new_stmt(KCtx &K, u8 kind) {
+    if (K.nst >= K.st_cap) {
+        K.oom = true;
+        return 0; // stmt 0 is a scratch sink
+    }
+    u32 i = K.nst++;
+    Stmt &s = K.st[i];
+    s.kind = kind;
+    s.pad = 0;
+    s.cls = 0;
+    s.next = 0;
+    s.a = s.b = s.c = s.d = 0;
+    return i;
+}
+
+OD_INL u32 new_list(KCtx &K) {
+    if (K.nlists >= K.lists_cap) {
+        K.oom = true;
+        return 0;
+    }
+    u32 i = K.nlists++;
+    K.lists[i].head = K.lists[i].tail = 0;
+    return i;
+}
+
+OD_INL void list_append(KCtx &K, u32 l, u32 s) {
+    if (!s)
+        return;
+    SList &L = K.lists[l];
+    if (L.tail)
+        K.st[L.tail].next = s;
+    else
+        L.head = s;
+    L.tail = s;
+}
+
+OD_INL u32 fold(KCtx &K, u32 e) { return fold_expr(K.E, e, K.cfg, K.fs); }
+
+// ------------------------------------------------------------ stepper
+struct Step {
+    KCtx &K;
+    const Ins &I;
+    u32 out; // statement list
+
+    OD_INL const Opnd &op(u32 k) const { return op_at(K, I, k); }
+    OD_INL u32 n() const { return (I.flags & IF_SYNTH) ? 0 : I.nops; }
+    OD_INL u32 read(const Opnd &o) { return read_operand(K, o); }
+    OD_INL u32 read64(const Opnd &o) { return read_pair(K, o); }
+    OD_INL DT ty(u32 e) const { return K.E.n[e].type; }
+
+    OD_INL void write(const Opnd &o, u32 value, DT t) {
+        u32 id = operand_reg_id(o);
+        if (id >= kNumRegIds)
+            return;
+        const bool pair = o.count >= 2 || (o.kind == OK_SPECIAL && (o.special == SP_EXEC || o.special == SP_VCC));
+        if (pair)
+            write_pair_ids(K, id, value, t);
+        else
+            write_slot32(K, id, value, t);
+    }
+
+    // Stepper::fallback  sym_state.cpp:273-288
+    OD_INL void fallback() {
+        u32 s = new_stmt(K, SK_RAW);
+        K.st[s].a = I.src.off;
+        K.st[s].b = I.src.len;
+        list_append(K, out, s);
+        K.fallbacks++;
+        u32 nn = (I.flags & IF_PARSE_FAILED) ? 0 : n();
+        for (u32 k = 0; k < nn; ++k) {
+            u32 id = operand_reg_id(op(k));
+            if (id < kNumRegIds) {
+                invalidate_slot(K, id, op(k).count);
+                break;
+            }
+        }
+        K.pend.valid = 0;
+        K.pend.base64 = K.pend.addend = 0;
+        K.pend.lo_vgpr = K.pend.lo_version = 0;
+    }
+
+    // Stepper::coerce  sym_state.cpp:300-310
+    OD_INL u32 coerce(u32 e, DT want) {
+        if (!e)
+            return e;
+        DT et = ty(e);
+        if (dt_base(et) == dt_base(want) && dt_bits(et) == dt_bits(want))
+            return e;
+        if (K.E.is_const(e))
+            return K.E.constant(K.E.cval(e), want);
+        if (dt_is_float(want) != dt_is_float(et))
+            return K.E.unary(U_CAST, e, want);
+        return e;
+    }
+
+    OD_INL void push_store(u32 addr, u32 value, DT et) {
+        u32 s = new_stmt(K, SK_STORE);
+        // lower_block folds store address and value (lower.cpp:37-39)
+        u32 fa = fold(K, addr);
+        u32 fv = fold(K, value);
+        K.st[s].a = fa;
+        K.st[s].b = fv;
+        K.st[s].c = et;
+        list_append(K, out, s);
+    }
+
+    // do_scalar_load  sym_state.cpp:348-405
+    OD_INL void scalar_load(u32 dwords) {
+        if (n() < 2 || !op_is_sreg(op(0)))
+            return fallback();
+        const Opnd &dst = op(0);
+        const Opnd &base_op = op(1);
+        u64 offset = 0;
+        if (n() >= 3 && op(2).kind == OK_LITERAL)
+            offset = (u64)op(2).value;
+        u32 base = read64(base_op);
+        if (base && K.E.n[base].kind == E_KBASE) {
+            if (dwords <= 2) {
+                u32 v = match_settings_load(K, (u32)offset, dwords);
+                if (v) {
+                    if (dwords == 2)
+                        write_pair_ids(K, dst.r.a, v, ty(v));
+                    else
+                        write_slot32(K, dst.r.a, v, ty(v));
+                    return;
+                }
+            }
+            bool all_known = true;
+            for (u32 i = 0; i < dwords && all_known; ++i) {
+                bool second;
+                all_known = abi_find_dword(K, (u32)offset + 4 * i, &second) != nullptr;
+            }
+            if (all_known) {
+                for (u32 i = 0; i < dwords;) {
+                    bool second;
+                    const AbiEntry *e = abi_find_dword(K, (u32)offset + 4 * i, &second);
+                    u32 v = match_settings_load(K, e->offset, e->dwords);
+                    if (e->dwords == 2 && !second && i + 1 < dwords) {
+                        write_pair_ids(K, dst.r.a + i, v, v ? ty(v) : DT_UNKNOWN);
+                        i += 2;
+                    } else {
+                        u32 half = e->dwords == 2 ? K.E.unary(second ? U_HI32 : U_LO32, v, DT_B32) : v;
+                        write_slot32(K, dst.r.a + i, half, half ? ty(half) : DT_UNKNOWN);
+                        i += 1;
+                    }
+                }
+                return;
+            }
+            // warning: scalar load from unmapped settings offset
+        }
+        for (u32 i = 0; i < dwords; ++i) {
+            u32 addr = K.E.binary(O_ADD, base, K.E.constant(offset + 4 * i, DT_U64), DT_U64);
+            u32 v = K.E.deref(addr, DT_B32, AS_GLOBAL);
+            write_slot32(K, dst.r.a + i, v, ty(v));
+        }
+    }
+
+    // do_compare  sym_state.cpp:407-460
+    OD_INL bool compare(bool vector_side) {
+        DT ct = suffix_type0(I, DT_I32);
+        const bool uns = dt_base(ct) == B_UNSIGNED;
+        u32 cop;
+        switch (I.root) {
+        case R_CMP_EQ: cop = O_CMPEQ; break;
+        case R_CMP_NE:
+        case R_CMP_LG:
+        case R_CMP_NEQ: cop = O_CMPNE; break;
+        case R_CMP_LT: cop = uns ? O_CMPLTU : O_CMPLT; break;
+        case R_CMP_LE: cop = uns ? O_CMPLEU : O_CMPLE; break;
+        case R_CMP_GT: cop = uns ? O_CMPGTU : O_CMPGT; break;
+        case R_CMP_GE: cop = uns ? O_CMPGEU : O_CMPGE; break;
+        default: return false;
+        }
+        u32 fs = vector_side ? 1 : 0;
+        if (n() < fs + 2)
+            return false;
+        u32 a = read(op(fs));
+        u32 b = read(op(fs + 1));
+        if (dt_is_float(ct)) {
+            a = coerce(a, ct);
+            b = coerce(b, ct);
+        } else if (a && K.E.is_const(a)) {
+            a = K.E.constant(K.E.cval(a), ct);
+        }
+        if (!dt_is_float(ct) && b && K.E.is_const(b))
+            b = K.E.constant(K.E.cval(b), ct);
+        u32 cmp = K.E.binary(cop, a, b, DT_I32);
+        if (vector_side) {
+            write(op(0), cmp, DT_B64);
+        } else {
+            log_slot(K, 362);
+            Slot &scc = K.regs[362];
+            scc.version += 1;
+            scc.expr = cmp;
+            scc.type = DT_I32;
+            scc.integ = IN_ENTIRE;
+        }
+        return true;
+    }
+
+    // handle_scalar  sym_state.cpp:462-555
+    OD_INL bool scalar() {
+        const u32 r = I.root;
+        const u32 nn = n();
+        if (nn > 0 && op(0).kind == OK_SPECIAL &&
+            (op(0).special == SP_EXEC || op(0).special == SP_EXEC_LO || op(0).special == SP_EXEC_HI))
+            return false;
+        if (r == R_LOAD_DWORD) return scalar_load(1), true;
+        if (r == R_LOAD_DWORDX2) return scalar_load(2), true;
+        if (r == R_LOAD_DWORDX4) return scalar_load(4), true;
+        if (r == R_MOV && nn >= 2) {
+            DT t = suffix_type0(I, DT_B32);
+            u32 v = dt_bits(t) == 64 ? read64(op(1)) : read(op(1));
+            write(op(0), v, v ? ty(v) : DT_UNKNOWN);
+            return true;
+        }
+        if ((r == R_ADD || r == R_SUB || r == R_MUL || r == R_ADDK || r == R_MULK) && nn >= 2) {
+            const bool k = r == R_ADDK || r == R_MULK;
+            if (!k && nn < 3)
+                return false;
+            DT t = suffix_type0(I, DT_I32);
+            u32 a = coerce(read(op(k ? 0 : 1)), t);
+            u32 b = coerce(read(op(k ? 1 : 2)), t);
+            u32 o = O_ADD;
+            if (r == R_SUB)
+                o = O_SUB;
+            else if (r == R_MUL || r == R_MULK)
+                o = O_MUL;
+            write(op(0), K.E.binary(o, a, b, t), t);
+            invalidate_slot(K, kRegIdScc, 1);
+            return true;
+        }
+        if ((r == R_AND || r == R_OR || r == R_XOR || r == R_ANDN2) && nn >= 3) {
+            DT t = suffix_type0(I, DT_B32);
+            const bool wide = dt_bits(t) == 64;
+            u32 a = wide ? read64(op(1)) : read(op(1));
+            u32 b = wide ? read64(op(2)) : read(op(2));
+            u32 v;
+            if (r == R_ANDN2)
+                v = K.E.binary(O_AND, a, K.E.unary(U_BITNOT, b, t), t);
+            else if (r == R_AND)
+                v = K.E.binary(O_AND, a, b, t);
+            else if (r == R_OR)
+                v = K.E.binary(O_OR, a, b, t);
+            else
+                v = K.E.binary(O_XOR, a, b, t);
+            write(op(0), v, t);
+            invalidate_slot(K, kRegIdScc, 1);
+            return true;
+        }
+        if ((r == R_LSHL || r == R_LSHR || r == R_ASHR) && nn >= 3) {
+            DT t = suffix_type0(I, DT_B32);
+            const bool wide = dt_bits(t) == 64;
+            u32 a = wide ? read64(op(1)) : read(op(1));
+            u32 b = read(op(2));
+            u32 o = r == R_LSHL ? O_SHL : (r == R_LSHR ? O_LSHR : O_ASHR);
+            write(op(0), K.E.binary(o, a, b, t), t);
+            invalidate_slot(K, kRegIdScc, 1);
+            return true;
+        }
+        if (I.rflags & RF_CMP)
+            return compare(false);
+        if (r == R_AND_SAVEEXEC)
+            return false;
+        if (r == R_WAITCNT || r == R_NOP || r == R_ENDPGM || r == R_BRANCH || (I.rflags & RF_CBRANCH))
+            return true;
+        return false;
+    }
+
+    OD_INL u32 mask24(u32 e) {
+        return K.E.binary(O_AND, e, K.E.constant(0xffffff, DT_U32), DT_U32);
+    }
+
+    // src24_kind  sym_state.cpp:563-568: 0 none, 1 unsigned, 2 signed
+    OD_INL u32 src24() const {
+        for (u32 k = 0; k < 2; ++k) {
+            u32 s = I.sfx[k];
+            if (!s)
+                break;
+            if (sfx_bits(s) == 24)
+                return sfx_base(s) == SB_I ? 2 : 1;
+        }
+        return 0;
+    }
+
+    // handle_vector  sym_state.cpp:577-769
+    OD_INL bool vector() {
+        const u32 r = I.root;
+        const u32 nn = n();
+        if (r == R_MOV && nn >= 2) {
+            u32 v = read(op(1));
+            write(op(0), v, v ? ty(v) : DT_B32);
+            return true;
+        }
+        if (!(I.flags & IF_PARSE_FAILED) && r == R_CNDMASK && nn >= 4 && op_is_vreg(op(0))) {
+            u32 cond = read(op(3));
+            u32 a = read(op(1));
+            u32 b = read(op(2));
+            DT t = b ? ty(b) : DT_B32;
+            write(op(0), K.E.ternary(cond, b, a, t), t);
+            return true;
+        }
+        if ((r == R_ADD || r == R_SUB || r == R_SUBREV) && nn >= 3) {
+            u32 src0 = 1;
+            bool carry = false;
+            if (op_is_special(op(1), SP_VCC) || op_is_sreg_pair(op(1))) {
+                src0 = 2;
+                carry = true;
+            }
+            if (nn < src0 + 2)
+                return false;
+            DT t = suffix_type0(I, DT_U32);
+            u32 a = coerce(read(op(src0)), t);
+            u32 b = coerce(read(op(src0 + 1)), t);
+            if (r == R_SUBREV) {
+                u32 x = a;
+                a = b;
+                b = x;
+            }
+            u32 o = r == R_ADD ? O_ADD : O_SUB;
+            u32 value = K.E.binary(o, a, b, t);
+            Pending pd;
+            pd.valid = 0;
+            pd.lo_vgpr = pd.lo_version = 0;
+            pd.base64 = pd.addend = 0;
+            if (r == R_ADD && carry && op_is_vreg(op(0))) {
+                u32 lo = 0, other = 0;
+                if (a && K.E.n[a].kind == E_UNARY && K.E.n[a].op == U_LO32) {
+                    lo = a;
+                    other = b;
+                } else if (b && K.E.n[b].kind == E_UNARY && K.E.n[b].op == U_LO32) {
+                    lo = b;
+                    other = a;
+                }
+                if (lo) {
+                    pd.valid = 1;
+                    pd.lo_vgpr = op(0).r.a;
+                    pd.base64 = K.E.n[lo].a;
+                    pd.addend = other;
+                }
+            }
+            write(op(0), value, t);
+            if (carry)
+                invalidate_slot(K, operand_reg_id(op(1)), op(1).count);
+            K.pend = pd;
+            if (pd.valid)
+                K.pend.lo_version = K.regs[kRegIdVgpr0 + pd.lo_vgpr].version;
+            return true;
+        }
+        if (r == R_ADDC && nn >= 5) {
+            const Pending pd = K.pend;
+            K.pend.valid = 0;
+            K.pend.base64 = K.pend.addend = 0;
+            K.pend.lo_vgpr = K.pend.lo_version = 0;
+            DT t = suffix_type0(I, DT_U32);
+            u32 x = read(op(2));
+            u32 y = read(op(3));
+            const bool cin_vcc = op_is_special(op(4), SP_VCC);
+            if (pd.valid && cin_vcc && op_is_vreg(op(0)) && op(0).r.a == pd.lo_vgpr + 1 &&
+                K.regs[kRegIdVgpr0 + pd.lo_vgpr].version == pd.lo_version) {
+                u32 hi = 0, zero = 0;
+                if (x && K.E.n[x].kind == E_UNARY && K.E.n[x].op == U_HI32 &&
+                    expr_equal(K.E, K.E.n[x].a, pd.base64, K.eqst)) {
+                    hi = x;
+                    zero = y;
+                } else if (y && K.E.n[y].kind == E_UNARY && K.E.n[y].op == U_HI32 &&
+                           expr_equal(K.E, K.E.n[y].a, pd.base64, K.eqst)) {
+                    hi = y;
+                    zero = x;
+                }
+                if (hi && zero && K.E.is_const_v(zero, 0)) {
+                    u32 add64 = K.E.unary(U_CAST, pd.addend, DT_U64);
+                    u32 joint = K.E.binary(O_ADD, pd.base64, add64, DT_U64);
+                    u32 lo_id = kRegIdVgpr0 + pd.lo_vgpr;
+                    if (lo_id + 1 >= kRegIdExecLo) {
+                        K.oom = true;
+                        return true;
+                    }
+                    log_slot(K, lo_id);
+                    Slot &lo = K.regs[lo_id];
+                    lo.expr = joint;
+                    lo.integ = IN_LOW;
+                    lo.type = DT_U64;
+                    log_slot(K, lo_id + 1);
+                    Slot &hs = K.regs[lo_id + 1];
+                    hs.version += 1;
+                    hs.expr = joint;
+                    hs.integ = IN_HIGH;
+                    hs.type = DT_U64;
+                    invalidate_slot(K, operand_reg_id(op(1)), op(1).count);
+                    return true;
+                }
+            }
+            // warning: v_addc_u32 outside the 64-bit add idiom
+            u32 v = K.E.binary(O_ADD, coerce(x, t), coerce(y, t), t);
+            write(op(0), v, t);
+            invalidate_slot(K, operand_reg_id(op(1)), op(1).count);
+            return true;
+        }
+        if ((r == R_MUL || r == R_MUL_LO || r == R_MUL_HI) && nn >= 3) {
+            const u32 narrow = src24();
+            if (narrow == 2)
+                return false;
+            DT t = suffix_type0(I, DT_U32);
+            u32 a = coerce(read(op(1)), t);
+            u32 b = coerce(read(op(2)), t);
+            if (narrow == 1) {
+                a = mask24(a);
+                b = mask24(b);
+            }
+            u32 o = O_MUL;
+            if (r == R_MUL_HI)
+                o = dt_is_signed(t) ? O_MULHIS : O_MULHI;
+            write(op(0), K.E.binary(o, a, b, t), t);
+            return true;
+        }
+        if (r == R_MAC && nn >= 3) {
+            DT t = suffix_type0(I, DT_F32);
+            u32 a = coerce(read(op(1)), t);
+            u32 b = coerce(read(op(2)), t);
+            u32 d = coerce(read(op(0)), t);
+            u32 v = K.E.binary(O_ADD, K.E.binary(O_MUL, a, b, t), d, t);
+            write(op(0), v, t);
+            return true;
+        }
+        if (r == R_MAD && nn >= 4) {
+            const u32 narrow = src24();
+            if (narrow == 2)
+                return false;
+            DT t = suffix_type0(I, DT_F32);
+            u32 a = coerce(read(op(1)), t);
+            u32 b = coerce(read(op(2)), t);
+            u32 c = coerce(read(op(3)), t);
+            if (narrow == 1) {
+                a = mask24(a);
+                b = mask24(b);
+            }
+            u32 v = K.E.binary(O_ADD, K.E.binary(O_MUL, a, b, t), c, t);
+            write(op(0), v, t);
+            return true;
+        }
+        if ((r == R_LSHLREV || r == R_LSHRREV || r == R_ASHRREV || r == R_LSHL || r == R_LSHR ||
+             r == R_ASHR) &&
+            nn >= 3) {
+            const bool rev = r == R_LSHLREV || r == R_LSHRREV || r == R_ASHRREV;
+            u32 shift = read(op(rev ? 1 : 2));
+            u32 value = read(op(rev ? 2 : 1));
+            DT t = (r == R_ASHR || r == R_ASHRREV) ? DT_I32 : suffix_type0(I, DT_B32);
+            u32 o = O_SHL;
+            if (I.rflags & RF_LSHR)
+                o = O_LSHR;
+            else if (I.rflags & RF_ASHR)
+                o = O_ASHR;
+            write(op(0), K.E.binary(o, coerce(value, t), shift, t), t);
+            return true;
+        }
+        if ((r == R_AND || r == R_OR || r == R_XOR) && nn >= 3) {
+            DT t = suffix_type0(I, DT_B32);
+            u32 a = coerce(read(op(1)), t);
+            u32 b = coerce(read(op(2)), t);
+            u32 o = r == R_AND ? O_AND : r == R_OR ? O_OR : O_XOR;
+            write(op(0), K.E.binary(o, a, b, t), t);
+            return true;
+        }
+        if (I.rflags & RF_CMP)
+            return compare(true);
+        return false;
+    }
+
+    // pointer_base  sym_state.cpp:323-340 (pre-order, left first)
+    OD_INL DT pointee_of(u32 addr) {
+        U32Stack &st = K.eqst;
+        u32 base = st.top;
+        st.push(addr);
+        u32 hit = 0;
+        while (st.top > base && !st.oom) {
+            u32 e = st.pop();
+            if (!e)
+                continue;
+            const ENode &x = K.E.n[e];
+            if (x.kind == E_ARG && dt_is_pointer(x.type)) {
+                hit = e;
+                break;
+            }
+            if (x.kind == E_BINARY && x.op == O_ADD) {
+                st.push(x.b);
+                st.push(x.a);
+            } else if (x.kind == E_UNARY && x.op == U_CAST) {
+                st.push(x.a);
+            }
+        }
+        st.top = base;
+        return hit ? dt_pointee(K.E.n[hit].type) : DT_B32;
+    }
+
+    // do_flat_load  sym_state.cpp:771-792
+    OD_INL void flat_load(u32 dwords) {
+        if (n() < 2)
+            return fallback();
+        const Opnd &dst = op(0);
+        u32 addr = read64(op(1));
+        DT elem = pointee_of(addr);
+        if (dwords == 2 && dt_byte_size(elem) == 8) {
+            u32 v = K.E.deref(addr, elem, AS_GLOBAL);
+            write_pair_ids(K, kRegIdVgpr0 + dst.r.a, v, elem);
+            return;
+        }
+        DT e32 = dt_byte_size(elem) == 4 ? elem : DT_B32;
+        for (u32 i = 0; i < dwords; ++i) {
+            u32 a = i == 0 ? addr : K.E.binary(O_ADD, addr, K.E.constant(4 * i, DT_U64), DT_U64);
+            u32 v = K.E.deref(a, e32, AS_GLOBAL);
+            write_slot32(K, kRegIdVgpr0 + dst.r.a + i, v, e32);
+        }
+    }
+
+    // do_flat_store  sym_state.cpp:794-827
+    OD_INL void flat_store(u32 dwords) {
+        if (n() < 2)
+            return fallback();
+        u32 addr = read64(op(0));
+        const Opnd data = op(1);
+        DT elem = pointee_of(addr);
+        if (dwords == 2 && dt_byte_size(elem) == 8 && data.count >= 2) {
+            push_store(addr, read64(data), elem);
+            return;
+        }
+        DT e32 = dt_byte_size(elem) == 4 ? elem : DT_B32;
+        for (u32 i = 0; i < dwords; ++i) {
+            u32 a = i == 0 ? addr : K.E.binary(O_ADD, addr, K.E.constant(4 * i, DT_U64), DT_U64);
+            Opnd piece = data;
+            if (piece.kind == OK_SREG || piece.kind == OK_VREG)
+                piece.r.a = data.r.a + i;
+            piece.count = 1;
+            push_store(a, read(piece), e32);
+        }
+    }
+
+    OD_INL bool flat() {
+        switch (I.root) {
+        case R_LOAD_DWORD: return flat_load(1), true;
+        case R_LOAD_DWORDX2: return flat_load(2), true;
+        case R_STORE_DWORD: return flat_store(1), true;
+        case R_STORE_DWORDX2: return flat_store(2), true;
+        default: return false;
+        }
+    }
+
+    // step  sym_state.cpp:840-864
+    OD_INL void run() {
+        if (I.flags & IF_PARSE_FAILED) {
+            fallback();
+            return;
+        }
+        bool handled = false;
+        if (I.prefix == PX_S)
+            handled = scalar();
+        else if (I.prefix == PX_V)
+            handled = vector();
+        else if (I.prefix == PX_FLAT)
+            handled = flat();
+        if (!handled)
+            fallback();
+        if (!(I.prefix == PX_V && (I.root == R_ADD || I.root == R_ADDC))) {
+            K.pend.valid = 0;
+            K.pend.base64 = K.pend.addend = 0;
+            K.pend.lo_vgpr = K.pend.lo_version = 0;
+        }
+    }
+};
+
+// lower_block  lower.cpp:29-49
+OD_INL void lower_block(KCtx &K, u32 b, u32 out) {
+    const Block &B = K.blk[b];
+    for (u32 i = B.ib; i < B.ie && !K.oom && !K.E.oom; ++i) {
+        if (K.supp[i])
+            continue;
+        Step s{K, K.ins[i], out};
+        s.run();
+    }
+}
+
+// taken_cond  lower.cpp:53-87
+OD_INL u32 taken_cond(KCtx &K, u32 cc, const Opnd &ms) {
+    switch (cc) {
+    case C_SCC0:
+    case C_SCC1: {
+        u32 e = K.regs[362].expr;
+        if (!e)
+            e = bind_fresh(K, 362, DT_B32);
+        return cc == C_SCC1 ? e : negate_condition(K.E, e);
+    }
+    case C_VCCZ:
+    case C_VCCNZ: {
+        u32 e = bind_fresh(K, 361, DT_B64);
+        return cc == C_VCCNZ ? e : negate_condition(K.E, e);
+    }
+    case C_MASKED: {
+        u32 src = (ms.count >= 2 || ms.kind == OK_SPECIAL) ? read_pair(K, ms) : read_operand(K, ms);
+        return negate_condition(K.E, src);
+    }
+    default: return 0;
+    }
+}
+
+OD_INL void initial_register_state(KCtx &K) {
+    for (u32 p = 0; p < kPhysSlots; ++p) {
+        Slot &s = K.regs[p];
+        s.version = 0;
+        s.expr = 0;
+        s.type = DT_UNKNOWN;
+        s.integ = IN_ENTIRE;
+    }
+    K.pend.valid = 0;
+    K.pend.base64 = K.pend.addend = 0;
+    K.pend.lo_vgpr = K.pend.lo_version = 0;
+}
+
+// initial_register_state  abi_model.cpp:253-281
+OD_INL void abi_entry_state(KCtx &K) {
+    initial_register_state(K);
+    u32 base = K.E.kbase();
+    K.regs[4].expr = base;
+    K.regs[4].integ = IN_LOW;
+    K.regs[4].type = DT_U64;
+    K.regs[5].expr = base;
+    K.regs[5].integ = IN_HIGH;
+    K.regs[5].type = DT_U64;
+    for (u32 d = 0; d < K.cfg.dims; ++d) {
+        K.regs[kRegIdVgpr0 + d].expr = K.E.builtin(F_LOCAL_ID, d, DT_U32);
+        K.regs[kRegIdVgpr0 + d].type = DT_U32;
+        K.regs[6 + d].expr = K.E.builtin(F_GROUP_ID, d, DT_U32);
+        K.regs[6 + d].type = DT_U32;
+    }
+    K.regs[360].expr = K.E.constant(~0ull, DT_B64);
+    K.regs[360].type = DT_B64;
+}
+
+// Collects the slots touched since log position p0 as a sorted delta on the
+// delta stack; returns (start, count).
+OD_INL void collect_delta(KCtx &K, u32 p0, u32 *start, u32 *count) {
+    u32 bm[kLiveWords];
+    for (u32 w = 0; w < kLiveWords; ++w)
+        bm[w] = 0;
+    for (u32 i = p0; i < K.nlog; ++i) {
+        u32 p = K.log[i].phys;
+        bm[p >> 5] |= 1u << (p & 31);
+    }
+    *start = K.ndstk;
+    for (u32 w = 0; w < kLiveWords; ++w) {
+        u32 m = bm[w];
+        while (m) {
+            u32 bit = __builtin_ctz(m);
+            m &= m - 1;
+            u32 p = w * 32 + bit;
+            if (K.ndstk >= K.dstk_cap) {
+                K.oom = true;
+                *count = K.ndstk - *start;
+                return;
+            }
+            K.dstk_id[K.ndstk] = p;
+            K.dstk[K.ndstk] = K.regs[p];
+            K.ndstk++;
+        }
+    }
+    *count = K.ndstk - *start;
+}
+
+OD_INL u32 half_view(KCtx &K, const Slot &s) {
+    if (s.integ == IN_LOW)
+        return K.E.unary(U_LO32, s.expr, DT_B32);
+    if (s.integ == IN_HIGH)
+        return K.E.unary(U_HI32, s.expr, DT_B32);
+    return s.expr;
+}
+
+// merge_at_join (sym_state.cpp:866-957) + emit_join (lower.cpp:89-121) for
+// the union of touched slots.  regs must hold the split state S0.
+OD_INL void merge_join(KCtx &K, const Frame &F, u32 td, u32 tn, u32 ed, u32 en, bool has_else,
+                       const u32 *live) {
+    u32 i = 0, j = 0;
+    while (i < tn || j < en) {
+        u32 pt = i < tn ? K.dstk_id[td + i] : 0xffffffffu;
+        u32 pe = j < en ? K.dstk_id[ed + j] : 0xffffffffu;
+        u32 p = pt < pe ? pt : pe;
+        Slot a = K.regs[p], b = K.regs[p];
+        if (pt == p) {
+            a = K.dstk[td + i];
+            ++i;
+        }
+        if (pe == p) {
+            b = K.dstk[ed + j];
+            ++j;
+        }
+        Slot m = a; // merged starts as the then state
+        if (p == 360) {
+            // exec halves are skipped: the then side passes through
+        } else if (a.version == b.version &&
+                   (!a.expr || !b.expr || expr_equal(K.E, a.expr, b.expr, K.eqst))) {
+            if (!a.expr && b.expr)
+                m = b;
+        } else {
+            u32 top = a.version > b.version ? a.version : b.version;
+            u32 id = dense_of_phys(p);
+            if (!lv_test(live, id)) {
+                m.version = top;
+                m.expr = 0;
+                m.type = DT_UNKNOWN;
+                m.integ = IN_ENTIRE;
+            } else {
+                u32 tv, ev;
+                if (p >= 361) { // vcc, scc, m0: raw slot expressions
+                    tv = a.expr;
+                    ev = b.expr;
+                } else {
+                    tv = a.expr ? half_view(K, a) : 0;
+                    ev = b.expr ? half_view(K, b) : 0;
+                }
+                DT vt = DT_B32;
+                if (tv && ev)
+                    vt = dt_unify(K.E.n[tv].type, K.E.n[ev].type);
+                else if (tv)
+                    vt = K.E.n[tv].type;
+                else if (ev)
+                    vt = K.E.n[ev].type;
+                if (dt_is_unknown(vt) || dt_is_pointer(vt))
+                    vt = dt_bits(vt) == 64 ? DT_B64 : DT_B32;
+                u32 serial = top + 1;
+                while (!K.pool.insert(p, serial))
+                    ++serial;
+                // emit_join for this fixup
+                u32 d = new_stmt(K, SK_DECL);
+                K.st[d].cls = (u16)p;
+                K.st[d].a = serial;
+                K.st[d].c = vt;
+                if (!has_else && ev)
+                    K.st[d].b = fold(K, ev);
+                list_append(K, F.out, d);
+                if (tv) {
+                    u32 s = new_stmt(K, SK_ASSIGN);
+                    K.st[s].cls = (u16)p;
+                    K.st[s].a = serial;
+                    K.st[s].b = fold(K, tv);
+                    list_append(K, F.then_l, s);
+                }
+                if (has_else && ev) {
+                    u32 s = new_stmt(K, SK_ASSIGN);
+                    K.st[s].cls = (u16)p;
+                    K.st[s].a = serial;
+                    K.st[s].b = fold(K, ev);
+                    list_append(K, F.else_l, s);
+                }
+                m.version = top + 1;
+                m.expr = K.E.var(p, serial, vt);
+                m.type = vt;
+                m.integ = IN_ENTIRE;
+            }
+        }
+        log_slot(K, p);
+        K.regs[p] = m;
+    }
+}
+
+OD_INL u32 push_frame(KCtx &K, u32 region, u32 out) {
+    if (K.nframes >= K.frames_cap) {
+        K.oom = true;
+        return 0;
+    }
+    Frame &F = K.frames[K.nframes++];
+    F.region = region;
+    F.phase = 0;
+    F.out = out;
+    F.then_l = F.else_l = 0;
+    F.cond = 0;
+    F.child = 0;
+    F.then_d = F.then_n = 0;
+    return 1;
+}
+
+// lower_region  lower.cpp:123-172, iterative.
+OD_INL void lower_structured(KCtx &K, u32 root, u32 out) {
+    abi_entry_state(K);
+    K.nframes = 0;
+    push_frame(K, root, out);
+    while (K.nframes && !K.oom && !K.E.oom) {
+        Frame &F = K.frames[K.nframes - 1];
+        const Region &R = K.rg[F.region];
+        if (R.kind == RK_BLOCK) {
+            u32 o = F.out;
+            K.nframes--;
+            lower_block(K, (u32)R.block_id, o);
+            continue;
+        }
+        if (R.kind == RK_LINEAR) {
+            if (F.child < R.ch_n) {
+                u32 c = K.child[R.ch_b + F.child++];
+                push_frame(K, c, F.out);
+            } else {
+                K.nframes--;
+            }
+            continue;
+        }
+        const bool has_else = R.kind == RK_IFELSE;
+        if (F.phase == 0) {
+            F.phase = 1;
+            push_frame(K, K.child[R.ch_b], F.out);
+            continue;
+        }
+        if (F.phase == 1) {
+            u32 taken = taken_cond(K, R.cc, R.mask_source);
+            u32 cond = R.then_is_taken ? taken : negate_condition(K.E, taken);
+            F.cond = fold(K, cond);
+            F.log_p0 = K.nlog;
+            F.pend = K.pend;
+            F.dstk_p0 = K.ndstk;
+            F.then_l = new_list(K);
+            F.else_l = new_list(K);
+            K.log_depth++;
+            F.phase = 2;
+            push_frame(K, K.child[R.ch_b + 1], F.then_l);
+            continue;
+        }
+        if (F.phase == 2) {
+            collect_delta(K, F.log_p0, &F.then_d, &F.then_n);
+            undo_to(K, F.log_p0);
+            K.pend = F.pend;
+            F.phase = 3;
+            if (has_else) {
+                push_frame(K, K.child[R.ch_b + 2], F.else_l);
+                continue;
+            }
+        }
+        // phase 3: both arms lowered
+        u32 ed, en;
+        collect_delta(K, F.log_p0, &ed, &en);
+        undo_to(K, F.log_p0);
+        K.log_depth--;
+        const u32 *live = K.live_in + (u32)R.join_block * kLiveWords;
+        merge_join(K, F, F.then_d, F.then_n, ed, en, has_else, live);
+        K.pend.valid = 0;
+        K.pend.base64 = K.pend.addend = 0;
+        K.pend.lo_vgpr = K.pend.lo_version = 0;
+        u32 s = new_stmt(K, SK_IF);
+        K.st[s].a = F.cond;
+        K.st[s].b = K.lists[F.then_l].head;
+        K.st[s].c = K.lists[F.else_l].head;
+        list_append(K, F.out, s);
+        K.ndstk = F.dstk_p0;
+        u32 out2 = F.out;
+        u32 join = R.join_absorbed ? K.child[R.ch_b + R.ch_n - 1] : 0;
+        K.nframes--;
+        if (join)
+            push_frame(K, join, out2);
+    }
+}
+
+// lower_goto_form  lower.cpp:187-250
+OD_INL void lower_goto(KCtx &K, u32 out) {
+    for (u32 k = 0; k < K.nblk && !K.oom && !K.E.oom; ++k) {
+        u32 id = k;
+        if (k > 0 && (!K.blk[id].reachable || K.blk[id].absorbed))
+            continue;
+        const Block &B = K.blk[id];
+        u32 l = new_stmt(K, SK_LABEL);
+        K.st[l].a = id;
+        list_append(K, out, l);
+        if (id == 0)
+            abi_entry_state(K);
+        else
+            initial_register_state(K);
+        lower_block(K, id, out);
+        const Term &t = B.term;
+        if (t.kind == T_FALL || t.kind == T_UNCOND) {
+            u32 g = new_stmt(K, SK_GOTO);
+            K.st[g].c = (u32)t.taken;
+            list_append(K, out, g);
+        } else if (t.kind == T_COND) {
+            u32 cond = taken_cond(K, t.cc, t.mask_source);
+            if (!cond) {
+                const Ins &last = K.ins[B.ie - 1];
+                u32 r = new_stmt(K, SK_RAW);
+                K.st[r].a = last.src.off;
+                K.st[r].b = last.src.len;
+                list_append(K, out, r);
+                K.fallbacks++;
+            } else {
+                u32 g = new_stmt(K, SK_GOTO);
+                K.st[g].a = fold(K, cond);
+                K.st[g].c = (u32)t.taken;
+                list_append(K, out, g);
+            }
+            u32 g2 = new_stmt(K, SK_GOTO);
+            K.st[g2].c = (u32)(t.not_taken >= 0 ? t.not_taken : t.taken);
+            list_append(K, out, g2);
+        }
+    }
+}
+
+// ------------------------------------------------------------ emission
+OD_INL void put_block_label(KCtx &K, Writer &w, u32 b) {
+    const Block &B = K.blk[b];
+    if (B.lab_n) {
+        const Label &L = klabel(K, B.lab_b);
+        w.putn(K.in->t + L.off, L.len);
+    } else {
+        w.puts("bb");
+        w.put_u64(b);
+    }
+}
+
+// emit_statement  codegen.cpp:393-442 (one statement, no If bodies)
+OD_INL void emit_simple(KCtx &K, Writer &w, const Stmt &s, u32 depth) {
+    RenderCtx &rc = K.rc;
+    u32 mark = K.E.top; // scratch nodes from render_indexed are discarded
+    switch (s.kind) {
+    case SK_ASSIGN:
+        w.spaces(depth * 4);
+        put_var_name(w, s.cls, s.a);
+        w.puts(" = ");
+        render_expr(w, rc, s.b, 0);
+        w.puts(";\n");
+        break;
+    case SK_DECL:
+        w.spaces(depth * 4);
+        render_type(w, dt_with_space(s.c, AS_NONE));
+        w.put(' ');
+        put_var_name(w, s.cls, s.a);
+        if (s.b) {
+            w.puts(" = ");
+            render_expr(w, rc, s.b, 0);
+        }
+        w.puts(";\n");
+        break;
+    case SK_STORE: {
+        w.spaces(depth * 4);
+        u32 target = K.E.deref(s.a, s.c, AS_GLOBAL);
+        render_expr(w, rc, target, 0);
+        w.puts(" = ");
+        u32 v = s.b;
+        if (v && is_bit_reinterpret(K.E.n[v].type, s.c)) {
+            w.puts(cast_name(s.c));
+            w.put('(');
+            render_expr(w, rc, v, 0);
+            w.put(')');
+        } else {
+            render_expr(w, rc, v, 0);
+        }
+        w.puts(";\n");
+        break;
+    }
+    case SK_RAW: {
+        w.spaces(depth * 4);
+        w.puts("__asm volatile (\"");
+        const u8 *p = K.in->t + s.a;
+        u32 b = 0, e = s.b;
+        while (b < e && (p[b] == ' ' || p[b] == '\t'))
+            ++b;
+        while (e > b && (p[e - 1] == ' ' || p[e - 1] == '\t'))
+            --e;
+        w.putn(p + b, e - b);
+        w.puts("\");\n");
+        break;
+    }
+    case SK_LABEL:
+        put_block_label(K, w, s.a);
+        w.puts(":;\n");
+        break;
+    case SK_GOTO:
+        w.spaces(depth * 4);
+        if (s.a) {
+            w.puts("if (");
+            render_expr(w, rc, s.a, 0);
+            w.puts(") goto ");
+        } else {
+            w.puts("goto ");
+        }
+        put_block_label(K, w, s.c);
+        w.puts(";\n");
+        break;
+    default: break;
+    }
+    K.E.top = mark;
+}
+
+// emit_body  codegen.cpp:378-381, iterative over nested If bodies.
+OD_INL void emit_list(KCtx &K, Writer &w, u32 head, u32 depth, u32 *stk, u32 stk_cap) {
+    // stack entries: (stmt, depth, state) triples
+    u32 sp = 0;
+    stk[0] = head;
+    stk[1] = depth;
+    stk[2] = 0;
+    sp = 1;
+    while (sp) {
+        u32 *e = stk + 3 * (sp - 1);
+        u32 s = e[0];
+        if (!s) {
+            --sp;
+            continue;
+        }
+        const Stmt &S = K.st[s];
+        u32 dp = e[1];
+        if (S.kind != SK_IF) {
+            emit_simple(K, w, S, dp);
+            e[0] = S.next;
+            continue;
+        }
+        if (e[2] == 0) {
+            w.spaces(dp * 4);
+            w.puts("if (");
+            u32 mark = K.E.top;
+            render_expr(w, K.rc, S.a, 0);
+            K.E.top = mark;
+            w.puts(") {\n");
+            e[2] = 1;
+            if (3 * (sp + 1) > stk_cap) {
+                K.oom = true;
+                return;
+            }
+            u32 *n = stk + 3 * sp;
+            n[0] = S.b;
+            n[1] = dp + 1;
+            n[2] = 0;
+            ++sp;
+            continue;
+        }
+        if (e[2] == 1 && S.c) {
+            w.spaces(dp * 4);
+            w.puts("} else {\n");
+            e[2] = 2;
+            if (3 * (sp + 1) > stk_cap) {
+                K.oom = true;
+                return;
+            }
+            u32 *n = stk + 3 * sp;
+            n[0] = S.c;
+            n[1] = dp + 1;
+            n[2] = 0;
+            ++sp;
+            continue;
+        }
+        w.spaces(dp * 4);
+        w.puts("}\n");
+        e[0] = S.next;
+        e[2] = 0;
+    }
+}
+
+// ------------------------------------------------------------ driver
+// decompile_section  decompiler.cpp:55-101 for one kernel.  Returns the
+// status; on KS_OK the OpenCL source is in w.
+OD_INL KOut decompile_kernel(const KIn &in, Bump &mem, const u8 **src) {
+    KOut out;
+    out.status = KS_OK;
+    out.structured = 0;
+    out.fallbacks = 0;
+    out.ninstr = 0;
+    out.out_len = 0;
+    KCtx K;
+    memset(&K, 0, sizeof(K));
+    K.in = &in;
+    K.mem = &mem;
+#define OD_CHECK(x)                                                                                \
+    do {                                                                                           \
+        if (!(x) || mem.oom) {                                                                     \
+            out.status = KS_OOM;                                                                   \
+            return out;                                                                            \
+        }                                                                                          \
+    } while (0)
+    OD_CHECK(parse_config(K));
+    OD_CHECK(collect_instructions(K));
+    out.ninstr = K.nins_real;
+    OD_CHECK(build_abi(K));
+    OD_CHECK(build_cfg(K));
+    if (K.failed) {
+        out.status = KS_FAILED;
+        return out;
+    }
+    normalize(K);
+    OD_CHECK(build_regions(K));
+    reduce(K);
+    if (K.oom) {
+        out.status = KS_OOM;
+        return out;
+    }
+    out.structured = K.reduced ? 1 : 0;
+    OD_CHECK(liveness(K));
+
+    // Carve the remaining arena into the dynamic pools.
+    K.regs = mem.get<Slot>(kPhysSlots);
+    OD_CHECK(K.regs);
+    u64 rem = mem.cap > mem.top ? mem.cap - mem.top : 0;
+    u64 unit = rem / 64;
+    K.E.cap = (u32)((unit * 22) / sizeof(ENode));
+    K.E.n = mem.get<ENode>(K.E.cap);
+    K.st_cap = (u32)((unit * 5) / sizeof(Stmt));
+    K.st = mem.get<Stmt>(K.st_cap);
+    K.lists_cap = 2 * K.nrg + 4;
+    K.lists = mem.get<SList>(K.lists_cap);
+    K.frames_cap = 2 * K.nrg + 8;
+    K.frames = mem.get<Frame>(K.frames_cap);
+    K.log_cap = (u32)((unit * 5) / sizeof(UndoRec));
+    K.log = mem.get<UndoRec>(K.log_cap);
+    K.dstk_cap = (u32)((unit * 4) / (sizeof(Slot) + 4));
+    K.dstk = mem.get<Slot>(K.dstk_cap);
+    K.dstk_id = mem.get<u32>(K.dstk_cap);
+    K.fresh_cap = (u32)((unit * 2) / sizeof(Fresh));
+    K.fresh = mem.get<Fresh>(K.fresh_cap);
+    {
+        u64 pc = 1024;
+        while (pc * 2 * 8 <= unit * 4)
+            pc *= 2;
+        K.pool.cap = (u32)pc;
+        K.pool.keys = mem.get<u64>(pc);
+        K.pool.count = 0;
+        K.pool.oom = false;
+    }
+    u32 scap = (u32)((unit * 2) / 4);
+    K.fs.st.p = mem.get<u32>(scap);
+    K.fs.st.cap = scap;
+    K.fs.terms.p = mem.get<u32>(scap);
+    K.fs.terms.cap = scap;
+    K.eqst.p = mem.get<u32>(scap);
+    K.eqst.cap = scap;
+    u32 tcap = (u32)((unit * 2) / 8);
+    K.rc.ts.p = mem.get<u64>(tcap);
+    K.rc.ts.cap = tcap;
+    u32 ecap = 3 * (K.nrg + 8);
+    u32 *estk = mem.get<u32>(ecap);
+    Writer w;
+    w.cap = (u32)(unit * 14 > 0xffffffffull ? 0xffffffffull : unit * 14);
+    w.p = mem.get<u8>(w.cap);
+    w.n = 0;
+    w.overflow = false;
+    *src = w.p;
+    OD_CHECK(K.E.n && K.st && K.lists && K.frames && K.log && K.dstk && K.dstk_id && K.fresh &&
+             K.pool.keys && K.fs.st.p && K.fs.terms.p && K.eqst.p && K.rc.ts.p && estk && w.p);
+    for (u32 i = 0; i < K.pool.cap; ++i)
+        K.pool.keys[i] = 0;
+    memset(&K.E.n[0], 0, sizeof(ENode));
+    K.E.top = 1; // node 0 = null
+    K.E.oom = false;
+    K.nst = 1;   // stmt 0 = sink
+    K.st[0].kind = SK_RAW;
+    K.st[0].next = 0;
+    K.nlists = 0;
+    u32 body = new_list(K);
+    K.rc.E = &K.E;
+    K.rc.cfg = &K.cfg;
+    K.rc.text = in.t;
+    K.rc.arg_sname = K.arg_sname;
+    K.rc.fs = K.fs;
+
+    if (K.reduced)
+        lower_structured(K, K.root_r, body);
+    else
+        lower_goto(K, body);
+    if (K.oom || K.E.oom || K.pool.oom || K.eqst.oom || K.fs.st.oom || K.fs.terms.oom) {
+        out.status = KS_OOM;
+        return out;
+    }
+    out.fallbacks = K.fallbacks;
+
+    // hoist_fresh_decls: first occurrence per name, in record order.
+    for (u32 i = 0; i < K.pool.cap; ++i)
+        K.pool.keys[i] = 0;
+    K.pool.count = 0;
+    u32 hoist = new_list(K);
+    for (u32 i = 0; i < K.nfresh; ++i) {
+        const Fresh &f = K.fresh[i];
+        if (!K.pool.insert(f.cls, f.num))
+            continue;
+        u32 d = new_stmt(K, SK_DECL);
+        K.st[d].cls = (u16)f.cls;
+        K.st[d].a = f.num;
+        K.st[d].c = f.type;
+        list_append(K, hoist, d);
+    }
+    if (K.oom || K.pool.oom) {
+        out.status = KS_OOM;
+        return out;
+    }
+
+    // emit_kernel  codegen.cpp:446-467
+    K.rc.fs = K.fs;
+    const u8 *t = in.t;
+    w.puts("__kernel void ");
+    w.putn(t + K.cfg.name.off, K.cfg.name.len);
+    w.put('(');
+    bool first = true;
+    for (u32 i = 0; i < K.cfg.nargs; ++i) {
+        const KArg &a = K.cfg.args[i];
+        if (a.implicit)
+            continue;
+        if (!first)
+            w.puts(", ");
+        first = false;
+        render_type(w, a.type);
+        if (!type_ends_star(a.type))
+            w.put(' ');
+        w.putn(t + a.name.off, a.name.len);
+    }
+    w.puts(") {\n");
+    emit_list(K, w, K.lists[hoist].head, 1, estk, ecap);
+    emit_list(K, w, K.lists[body].head, 1, estk, ecap);
+    w.puts("}\n");
+    if (K.oom || K.E.oom || K.rc.ts.oom || w.overflow || K.rc.fs.terms.oom || K.rc.fs.st.oom) {
+        out.status = KS_OOM;
+        return out;
+    }
+    out.out_len = w.n;
+    return out;
+#undef OD_CHECK
+}
+
+} // namespace od

@@ -1,0 +1,56 @@
+"""Developer diff: tools/devhost (device pipeline compiled for host) vs the
+oracle on the reference corpus, nests and synthetic listings.  Not a test."""
+import subprocess
+import sys
+
+sys.path.insert(0, ".")
+from oracle import oracle as O  # noqa: E402
+
+
+def dev(listing: bytes, extra=()):
+    p = subprocess.run(["build/devhost", *extra], input=listing, capture_output=True, timeout=60)
+    if p.returncode != 0:
+        return None, p.stderr.decode()[-2000:]
+    out = p.stdout
+    i = out.rindex(b"\nC ") + 1 if not out.startswith(b"C ") else 0
+    # parse trailing C record
+    nl = out.index(b"\n", i)
+    n = int(out[i + 2:nl])
+    return out[nl + 1:nl + 1 + n], out[:i]
+
+
+def check(name, listing, verbose=True, extra=()):
+    ref = O.decompile(listing, fold_local_size="--fold-local-size" in extra)
+    got, meta = dev(listing, extra)
+    if got is None:
+        print(f"CRASH {name}: {meta}")
+        return False
+    if got != ref.combined:
+        if verbose:
+            print(f"DIFF {name}")
+            print("--- ref\n" + ref.combined.decode(errors="replace"))
+            print("--- got\n" + got.decode(errors="replace"))
+        return False
+    return True
+
+
+if __name__ == "__main__":
+    ok = bad = 0
+    if check("copy.asm", open("/root/reference/proj/tests/data/copy.asm", "rb").read()):
+        ok += 1
+    else:
+        bad += 1
+    for nm, ls, _, _ in O.corpus():
+        if check(nm.decode(), ls):
+            ok += 1
+        else:
+            bad += 1
+    shown = 0
+    for seed in range(1, int(sys.argv[1]) if len(sys.argv) > 1 else 200):
+        r = check(f"nest{seed}", O.make_nest(seed), verbose=shown < 3)
+        if r:
+            ok += 1
+        else:
+            bad += 1
+            shown += 1
+    print("ok", ok, "bad", bad)

@@ -1,0 +1,171 @@
+// Developer harness (NOT part of the shipped library, never used by tests or
+// bench): compiles the device pipeline headers for the host so the per-kernel
+// algorithm can be diffed against the oracle in this GPU-less container.
+// The shipped path is paper_2107_07809_b200/csrc/ocldec_b200.cu on sm_100a.
+//
+//   g++ -O2 -std=c++17 -o build/devhost tools/devhost.cpp
+//   build/devhost < listing.s
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "../paper_2107_07809_b200/csrc/od_kernel.cuh"
+
+using namespace od;
+
+int main(int argc, char **argv) {
+    std::string in;
+    {
+        char buf[1 << 16];
+        size_t n;
+        while ((n = fread(buf, 1, sizeof buf, stdin)) > 0)
+            in.append(buf, n);
+    }
+    std::vector<u8> t(in.begin(), in.end());
+    const u32 corpus_len = (u32)t.size();
+    // P1a lines
+    std::vector<u32> starts;
+    {
+        u32 s = 0;
+        for (u32 i = 0; i < corpus_len; ++i)
+            if (t[i] == '\n') {
+                starts.push_back(s);
+                s = i + 1;
+            }
+        if (s < corpus_len)
+            starts.push_back(s);
+    }
+    u32 nl = (u32)starts.size();
+    std::vector<LineRec> lines(nl);
+    std::vector<u8> aux;
+    for (u32 l = 0; l < nl; ++l) {
+        u32 b = starts[l];
+        u32 e = l + 1 < nl ? starts[l + 1] - 1 : corpus_len;
+        if (l + 1 >= nl && e > b && t[e - 1] == '\n')
+            --e;
+        bool cx;
+        u32 cut = strip_scan(t.data() + b, e - b, &cx);
+        LineRec &L = lines[l];
+        memset(&L, 0, sizeof L);
+        if (!cx) {
+            L.off = b;
+            L.len = rtrim_len(t.data() + b, cut);
+        } else {
+            std::vector<u8> tmp(e - b + 1);
+            u32 k = strip_materialize(t.data() + b, e - b, tmp.data());
+            k = rtrim_len(tmp.data(), k);
+            L.off = corpus_len + (u32)aux.size();
+            L.len = k;
+            aux.insert(aux.end(), tmp.begin(), tmp.begin() + k);
+            L.complex = 1;
+        }
+    }
+    t.insert(t.end(), aux.begin(), aux.end());
+    for (u32 l = 0; l < nl; ++l)
+        lines[l].kind = classify_content(t.data(), Span{lines[l].off, lines[l].len});
+    // section scan
+    std::vector<u32> kstart;
+    int err_line = -1;
+    {
+        bool in_kernel = false;
+        int mode = 0; // 0 preamble 1 config 2 text
+        for (u32 l = 0; l < nl; ++l) {
+            LineRec &L = lines[l];
+            L.role = LR_NONE;
+            switch (L.kind) {
+            case LK_BLANK: break;
+            case LK_KERNEL_NONAME: err_line = (int)l; break;
+            case LK_KERNEL:
+                kstart.push_back(l);
+                in_kernel = true;
+                mode = 0;
+                break;
+            case LK_DIR_CONFIG:
+            case LK_DIR_TEXT:
+                if (!in_kernel)
+                    err_line = (int)l;
+                mode = L.kind == LK_DIR_CONFIG ? 1 : 2;
+                break;
+            default:
+                if (in_kernel)
+                    L.role = mode == 2 ? LR_TEXT : LR_CONFIG;
+            }
+            if (err_line >= 0)
+                break;
+        }
+    }
+    if (err_line >= 0) {
+        printf("E %d\nC 0\n", err_line + 1);
+        return 0;
+    }
+    RootTable rt;
+    build_root_table(&rt);
+    std::vector<LineIns> lins(nl);
+    std::vector<Opnd> ops;
+    std::vector<Label> labs;
+    for (u32 l = 0; l < nl; ++l) {
+        if (lines[l].role != LR_TEXT)
+            continue;
+        LineIns tmp;
+        decode_line(t.data(), Span{lines[l].off, lines[l].len}, &rt, &tmp, nullptr, nullptr);
+        u32 o0 = (u32)ops.size(), l0 = (u32)labs.size();
+        ops.resize(o0 + tmp.nops + 1);
+        labs.resize(l0 + tmp.nlabels + 1);
+        decode_line(t.data(), Span{lines[l].off, lines[l].len}, &rt, &lins[l], ops.data() + o0,
+                    labs.data() + l0);
+        lins[l].op_start = o0;
+        lins[l].lab_start = l0;
+        ops.resize(o0 + lins[l].nops);
+        labs.resize(l0 + lins[l].nlabels);
+    }
+    std::string combined, per;
+    for (size_t k = 0; k < kstart.size(); ++k) {
+        KIn kin;
+        kin.t = t.data();
+        kin.lines = lines.data();
+        kin.lins = lins.data();
+        kin.ops = ops.data();
+        kin.labs = labs.data();
+        kin.lbeg = kstart[k];
+        kin.lend = k + 1 < kstart.size() ? kstart[k + 1] : nl;
+        kin.line_base = 0;
+        kin.fold_local_size = argc > 1 && std::string(argv[1]) == "--fold-local-size";
+        u64 cap = 1 << 20;
+        KOut ko;
+        const u8 *src = nullptr;
+        std::vector<u8> arena;
+        for (;;) {
+            arena.assign(cap, 0);
+            Bump mem{arena.data(), 0, cap, false};
+            ko = decompile_kernel(kin, mem, &src);
+            if (ko.status != KS_OOM || cap > (1ull << 31))
+                break;
+            cap *= 4;
+        }
+        Span nm;
+        {
+            Span w, rest, extra;
+            split_word(t.data(), Span{lines[kin.lbeg].off, lines[kin.lbeg].len}, &w, &rest);
+            split_word(t.data(), rest, &nm, &extra);
+        }
+        std::string name((const char *)t.data() + nm.off, nm.len);
+        std::string s;
+        if (ko.status == KS_OK)
+            s.assign((const char *)src, ko.out_len);
+        per += "K " + std::to_string(ko.status == KS_FAILED ? 1 : 0) + " " +
+               std::to_string(ko.structured) + " " + std::to_string(ko.fallbacks) + " " +
+               std::to_string(name.size()) + " " + std::to_string(s.size()) + "\n" + name + s;
+        if (ko.status == KS_OOM)
+            fprintf(stderr, "kernel %zu: OOM\n", k);
+        if (!s.empty()) {
+            if (!combined.empty())
+                combined += "\n";
+            combined += s;
+        }
+    }
+    fwrite(per.data(), 1, per.size(), stdout);
+    printf("C %zu\n", combined.size());
+    fwrite(combined.data(), 1, combined.size(), stdout);
+    return 0;
+}
