@@ -54,3 +54,22 @@ if __name__ == "__main__":
             bad += 1
             shown += 1
     print("ok", ok, "bad", bad)
+
+
+def gen(shape, stress, seed, k0, n):
+    return subprocess.run(["build/devgen", str(shape), str(stress), str(seed), str(k0), str(n)],
+                          capture_output=True, check=True).stdout
+
+
+def split_kernels(listing: bytes):
+    parts = listing.split(b".kernel ")
+    return [b".kernel " + p for p in parts[1:]]
+
+
+def gencmp(shape, stress, seed, n, per=1):
+    bad = 0
+    for k0 in range(0, n, per):
+        ls = gen(shape, stress, seed, k0, per)
+        if not check(f"gen{shape}/{stress}/{k0}", ls, verbose=bad < 2):
+            bad += 1
+    return bad
