@@ -1,0 +1,129 @@
+/* ocldec-b200: C ABI of the B200-native batch GCN -> OpenCL decompiler.
+ *
+ * Drop-in boundary for the reference's pipeline front door
+ *   ocldec::decompile_listing(const std::string&, const DecompileOptions&)
+ *       /root/reference/proj/core/include/ocldec/decompiler.hpp:62
+ * and its result types
+ *   DecompileOptions      decompiler.hpp:29-35   -> ocldec_b200_options
+ *   DecompiledKernel      decompiler.hpp:39-52   -> ocldec_b200_kernel
+ *   DecompileResult       decompiler.hpp:54-60   -> ocldec_b200_result
+ *   combined_source()     decompiler.cpp:105-115 -> ocldec_b200_result.combined
+ *
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary.
+ * All decompilation runs on the GPU (sm_100a); there is no CPU path.  Every
+ * entry point returns 0 on success and a negative code on API misuse or CUDA
+ * failure (ocldec_b200_last_error() has the message).  Data errors (a kernel
+ * that fails to parse, a listing-level split error) are reported in the
+ * result exactly as the reference reports them, never as a return code.
+ */
+#ifndef OCLDEC_B200_H
+#define OCLDEC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OCLDEC_B200_ABI_VERSION 1
+
+/* DecompileOptions (decompiler.hpp:29-35).  abi_overrides and the DOT dumps
+ * are not supported by this version (fields reserved). */
+typedef struct ocldec_b200_options {
+    int fold_local_size;     /* FoldOptions::fold_local_size (sym_state.hpp:27-29) */
+    const char *only_kernel; /* restrict to one kernel by name, NULL = all        */
+    int device;              /* CUDA device ordinal                               */
+    size_t arena_bytes;      /* per-thread working arena, 0 = default             */
+} ocldec_b200_options;
+
+/* DecompiledKernel (decompiler.hpp:39-52): the printed source and flags. */
+typedef struct ocldec_b200_kernel {
+    uint64_t name_off, name_len;  /* into ocldec_b200_result.names  */
+    uint64_t src_off, src_len;    /* into ocldec_b200_result.combined (0 len when failed) */
+    int32_t failed;               /* hard parse error; source empty */
+    int32_t structured;           /* false: goto residue was needed */
+    int32_t fallback_count;       /* LoweredBody::fallback_count    */
+    uint32_t instructions;        /* parse_text instruction count    */
+} ocldec_b200_kernel;
+
+typedef struct ocldec_b200_result {
+    uint64_t nkernels;
+    ocldec_b200_kernel *kernels;
+    char *names;                  /* kernel names, concatenated */
+    char *combined;               /* combined_source(): sources joined by "\n" */
+    uint64_t combined_len;
+    int32_t split_error_line;     /* >0: split_kernels ParseError at this line (zero kernels) */
+    int32_t split_error_kind;     /* 1 nameless .kernel, 2 .config outside, 3 .text outside */
+    uint64_t instructions;        /* total parse_text instructions */
+    double device_ms;             /* device time of the pipeline (CUDA events) */
+} ocldec_b200_result;
+
+/* decompile_listing: host buffer in, host result out (H2D/D2H inside). */
+int ocldec_b200_decompile(const char *listing, size_t len, const ocldec_b200_options *opts,
+                          ocldec_b200_result **out);
+void ocldec_b200_free(ocldec_b200_result *res);
+const char *ocldec_b200_last_error(void);
+int ocldec_b200_version(void);
+
+/* ---------------------------------------------------------------- batch
+ * Session API for HBM-resident corpora (bench and multi-GPU shards).  A
+ * session owns device buffers on one device and one stream; calls on one
+ * session are serialized by the caller. */
+typedef struct ocldec_b200_session ocldec_b200_session;
+
+ocldec_b200_session *ocldec_b200_session_create(int device, size_t arena_bytes);
+void ocldec_b200_session_destroy(ocldec_b200_session *s);
+/* The stream all session work is issued on (a cudaStream_t). */
+void *ocldec_b200_session_stream(ocldec_b200_session *s);
+
+/* Decompiles a device-resident listing d_listing[0, len) whose kernel sections
+ * start at the byte offsets chunk_starts[0..nchunks) (each a ".kernel" line;
+ * chunk_starts[0] == 0).  Output stays on the device: *d_out / *out_len.
+ * Asynchronous on the session stream unless sync != 0.  Per-call counters
+ * are returned through ocldec_b200_session_stats. */
+int ocldec_b200_session_run(ocldec_b200_session *s, const void *d_listing, size_t len,
+                            const uint64_t *chunk_starts, size_t nchunks, int fold_local_size,
+                            int sync);
+/* Host-buffer batch call on a session (the e2e path): H2D of the listing,
+ * the device pipeline, D2H of combined_source into host_out (capacity
+ * out_cap).  *out_len always receives the output size; returns -2 when
+ * host_out is too small.  Pinned host buffers make both copies DMA. */
+int ocldec_b200_session_run_host(ocldec_b200_session *s, const char *listing, size_t len,
+                                 int fold_local_size, char *host_out, uint64_t out_cap,
+                                 uint64_t *out_len);
+typedef struct ocldec_b200_stats {
+    uint64_t kernels, instructions, lines, in_bytes, out_bytes, failed, goto_form, fallbacks;
+    uint64_t retried; /* kernels re-run with a larger arena */
+    uint64_t decompile_launches, total_launches;
+    double ms_parse, ms_decompile, ms_emit; /* last run, per pass (events) */
+} ocldec_b200_stats;
+int ocldec_b200_session_stats(ocldec_b200_session *s, ocldec_b200_stats *st);
+/* Device pointer + length of the last run's combined output. */
+int ocldec_b200_session_output(ocldec_b200_session *s, const void **d_out, uint64_t *len);
+/* Copies per-kernel (source offset, length, flags) of the last run to host arrays
+ * of size >= kernels: off/len in the combined output, flags bit0 failed,
+ * bit1 structured; fallbacks per kernel. */
+int ocldec_b200_session_kernels(ocldec_b200_session *s, uint64_t *off, uint64_t *len,
+                                uint32_t *flags, uint32_t *fallbacks);
+
+/* ------------------------------------------------------ synthetic corpora
+ * Counter-based generator; kernel k is a pure function of
+ * (shape, stress, seed, k), identical on host and device. */
+/* Host: writes kernels [k0, k0+count) into buf (cap bytes); offsets gets
+ * count+1 byte offsets; returns bytes written or a negative error
+ * (-2 = buffer too small; *needed gets the size). */
+int64_t ocldec_b200_gen_host(int shape, int stress, uint64_t seed, uint64_t k0, uint64_t count,
+                             char *buf, uint64_t cap, uint64_t *offsets, uint64_t *instructions,
+                             uint64_t *needed);
+/* Device: generates kernels [k0, k0+count) into a session-owned device buffer;
+ * returns its pointer, length, and per-kernel offsets (device). */
+int ocldec_b200_gen_device(ocldec_b200_session *s, int shape, int stress, uint64_t seed,
+                           uint64_t k0, uint64_t count, const void **d_buf, uint64_t *len,
+                           const uint64_t **d_offsets, uint64_t *instructions);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OCLDEC_B200_H */

@@ -1,0 +1,219 @@
+"""ocldec-b200: B200-native batch decompiler of AMD GCN listings to OpenCL C.
+
+Host-side mirror of the reference's front door (``ocldec::decompile_listing``,
+/root/reference/proj/core/include/ocldec/decompiler.hpp:29-62): same names,
+argument meaning and error behaviour.  Every call runs the sm_100a pipeline
+through the C ABI in ``include/ocldec_b200.h``; there is no CPU path.
+
+    >>> from paper_2107_07809_b200 import decompile_listing
+    >>> res = decompile_listing(open("copy.asm").read())
+    >>> print(res.combined_source())
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Union
+
+from . import _lib
+
+__all__ = ["DecompileOptions", "DecompiledKernel", "Diagnostic", "DecompileResult",
+           "decompile_listing", "generate_corpus", "Session", "SHAPES"]
+
+# Synthetic corpus shapes (BASELINE.json configs).
+SHAPES = {"C1": 1, "C2": 2, "C3": 3, "C4": 4, "C5": 5}
+
+
+@dataclass
+class DecompileOptions:
+    """DecompileOptions (decompiler.hpp:29-35).  abi_overrides and the DOT
+    dumps are not supported by this version."""
+    fold_local_size: bool = False           # FoldOptions (sym_state.hpp:27-29)
+    only_kernel: Optional[str] = None       # restrict to one kernel by name
+    device: int = 0
+    arena_bytes: int = 0                    # per-thread arena, 0 = default
+
+
+@dataclass
+class Diagnostic:
+    """Diagnostic (diagnostics.hpp:20-27).  severity: 0 note, 1 warning, 2 error."""
+    severity: int
+    line: int
+    message: str
+
+    def render(self, file: str) -> str:
+        sev = ("note", "warning", "error")[self.severity]
+        return f"{file}:{self.line}: {sev}: {self.message}"
+
+
+@dataclass
+class DecompiledKernel:
+    """DecompiledKernel (decompiler.hpp:39-52): printed source and flags."""
+    name: str
+    source: str
+    structured: bool
+    failed: bool
+    fallback_count: int
+    instructions: int
+
+
+@dataclass
+class DecompileResult:
+    """DecompileResult (decompiler.hpp:54-60)."""
+    kernels: List[DecompiledKernel] = field(default_factory=list)
+    diagnostics: List[Diagnostic] = field(default_factory=list)
+    combined: bytes = b""
+    device_ms: float = 0.0
+
+    def combined_source(self) -> str:
+        """decompiler.cpp:105-115: non-empty sources joined by newlines."""
+        return self.combined.decode("utf-8", errors="surrogateescape")
+
+
+_SPLIT_MESSAGES = {1: ".kernel directive without a name",
+                   2: ".config outside of a .kernel section",
+                   3: ".text outside of a .kernel section"}
+
+
+def decompile_listing(listing: Union[str, bytes], opts: Optional[DecompileOptions] = None) -> DecompileResult:
+    """ocldec::decompile_listing (decompiler.cpp:117-133) on the GPU.
+
+    A split_kernels ParseError yields zero kernels and one error diagnostic,
+    as in the reference (decompiler.cpp:120-125); a kernel-level ParseError
+    marks that kernel ``failed`` with empty source (decompiler.cpp:95-99).
+    """
+    L = _lib.load()
+    if isinstance(listing, str):
+        listing = listing.encode("utf-8", errors="surrogateescape")
+    opts = opts or DecompileOptions()
+    o = _lib.Options(int(opts.fold_local_size),
+                     opts.only_kernel.encode() if opts.only_kernel is not None else None,
+                     opts.device, opts.arena_bytes)
+    out = ctypes.POINTER(_lib.Result)()
+    rc = L.ocldec_b200_decompile(listing, len(listing), ctypes.byref(o), ctypes.byref(out))
+    if rc != 0:
+        raise RuntimeError(f"ocldec_b200_decompile failed ({rc}): {_lib.last_error()}")
+    try:
+        r = out.contents
+        res = DecompileResult(device_ms=r.device_ms)
+        combined = ctypes.string_at(r.combined, r.combined_len) if r.combined_len else b""
+        names = ctypes.string_at(r.names) if r.names else b""
+        res.combined = combined
+        for i in range(r.nkernels):
+            k = r.kernels[i]
+            src = combined[k.src_off:k.src_off + k.src_len] if k.src_len else b""
+            res.kernels.append(DecompiledKernel(
+                name=names[k.name_off:k.name_off + k.name_len].decode(errors="surrogateescape"),
+                source=src.decode("utf-8", errors="surrogateescape"),
+                structured=bool(k.structured), failed=bool(k.failed),
+                fallback_count=k.fallback_count, instructions=k.instructions))
+        if r.split_error_line > 0:
+            res.diagnostics.append(Diagnostic(2, r.split_error_line,
+                                              _SPLIT_MESSAGES.get(r.split_error_kind, "parse error")))
+        return res
+    finally:
+        L.ocldec_b200_free(out)
+
+
+def generate_corpus(shape: Union[int, str], count: int, seed: int = 1, k0: int = 0, stress: bool = False):
+    """Host generation of the synthetic corpus (od_gen.cuh; identical bytes to
+    the device generator).  Returns (listing bytes, per-kernel offsets list,
+    instruction count)."""
+    import numpy as np
+    L = _lib.load()
+    shape = SHAPES.get(shape, shape) if isinstance(shape, str) else shape
+    offs = np.zeros(count + 1, dtype=np.uint64)
+    ni = ctypes.c_uint64()
+    need = ctypes.c_uint64()
+    L.ocldec_b200_gen_host(shape, int(stress), seed, k0, count, None, 0, offs.ctypes.data,
+                           ctypes.byref(ni), ctypes.byref(need))
+    buf = ctypes.create_string_buffer(int(need.value) + 1)
+    n = L.ocldec_b200_gen_host(shape, int(stress), seed, k0, count, buf, need.value + 1, offs.ctypes.data,
+                               ctypes.byref(ni), ctypes.byref(need))
+    if n < 0:
+        raise RuntimeError("corpus generation failed")
+    return buf.raw[:n], offs, int(ni.value)
+
+
+class Session:
+    """HBM-resident batch runs (bench, multi-GPU shards): ocldec_b200_session_*."""
+
+    def __init__(self, device: int = 0, arena_bytes: int = 0):
+        self._L = _lib.load()
+        self._s = self._L.ocldec_b200_session_create(device, arena_bytes)
+        if not self._s:
+            raise RuntimeError(f"session create failed: {_lib.last_error()}")
+        self.device = device
+
+    def close(self):
+        if self._s:
+            self._L.ocldec_b200_session_destroy(self._s)
+            self._s = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream_ptr(self) -> int:
+        return self._L.ocldec_b200_session_stream(self._s) or 0
+
+    def generate(self, shape: Union[int, str], count: int, seed: int = 1, k0: int = 0, stress: bool = False):
+        """Device generation; returns (device ptr, length, device offsets ptr, instructions)."""
+        shape = SHAPES.get(shape, shape) if isinstance(shape, str) else shape
+        buf, ln, offs, ni = ctypes.c_void_p(), ctypes.c_uint64(), ctypes.c_void_p(), ctypes.c_uint64()
+        rc = self._L.ocldec_b200_gen_device(self._s, shape, int(stress), seed, k0, count, ctypes.byref(buf),
+                                            ctypes.byref(ln), ctypes.byref(offs), ctypes.byref(ni))
+        if rc:
+            raise RuntimeError(f"gen_device failed: {_lib.last_error()}")
+        return buf.value, ln.value, offs.value, ni.value
+
+    def run(self, d_listing: int, length: int, chunk_starts: Sequence[int], fold_local_size: bool = False,
+            sync: bool = True):
+        import numpy as np
+        cs = np.ascontiguousarray(np.asarray(chunk_starts, dtype=np.uint64))
+        rc = self._L.ocldec_b200_session_run(self._s, d_listing, length,
+                                             cs.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), len(cs),
+                                             int(fold_local_size), int(sync))
+        if rc:
+            raise RuntimeError(f"session_run failed ({rc}): {_lib.last_error()}")
+
+    def run_host(self, host_ptr: int, length: int, out_ptr: int, out_cap: int, fold_local_size: bool = False) -> int:
+        """Host buffers in and out (ocldec_b200_session_run_host); returns output length."""
+        n = ctypes.c_uint64()
+        rc = self._L.ocldec_b200_session_run_host(self._s, host_ptr, length, int(fold_local_size), out_ptr,
+                                                  out_cap, ctypes.byref(n))
+        if rc:
+            raise RuntimeError(f"session_run_host failed ({rc}): {_lib.last_error()}")
+        return n.value
+
+    def stats(self) -> dict:
+        st = _lib.Stats()
+        self._L.ocldec_b200_session_stats(self._s, ctypes.byref(st))
+        return {n: getattr(st, n) for n, _ in _lib.Stats._fields_}
+
+    def output(self):
+        p, n = ctypes.c_void_p(), ctypes.c_uint64()
+        self._L.ocldec_b200_session_output(self._s, ctypes.byref(p), ctypes.byref(n))
+        return p.value, n.value
+
+    def output_bytes(self) -> bytes:
+        """D2H copy of the last run's combined output (via torch for the copy)."""
+        import torch
+        p, n = self.output()
+        if n == 0:
+            return b""
+        host = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        _cudart_memcpy(host.data_ptr(), p, n)
+        return host.numpy().tobytes()
+
+
+def _cudart_memcpy(dst: int, src: int, n: int):
+    import torch
+    # cudaMemcpy through torch's CUDA runtime binding (device -> pinned host)
+    from torch.cuda import cudart
+    err = cudart().cudaMemcpy(dst, src, n, 2)  # cudaMemcpyDeviceToHost
+    if err != 0 and int(err) != 0:
+        raise RuntimeError(f"cudaMemcpy failed: {err}")

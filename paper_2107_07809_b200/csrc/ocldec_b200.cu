@@ -1,0 +1,1251 @@
+// ocldec-b200: device passes, host orchestration and the C ABI
+// (include/ocldec_b200.h).  sm_100a only.
+//
+// Pass plan per chunk of the listing:
+//   P1a k_nl_count/k_nl_write  16-byte vector loads, block scan of newline
+//                              flags -> newline positions
+//   P1b k_classify             thread per line: comment strip, trim, first word
+//   P1c section scan           (kernel count, last directive) pair scan -> line roles
+//   P1d k_decode (x2)          thread per text line: labels, perfect-hash
+//                              mnemonic, operands (sizing pass, scan, fill pass)
+//   P2-P4a k_decompile         persistent threads, one .kernel section each:
+//                              config/ABI, CFG, exec-mask normalization, region
+//                              reduction, liveness, lowering, emission
+//   P4b k_gather               scan of output lengths, warp-per-kernel scatter
+//                              into the combined_source buffer
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ocldec_b200.h"
+#include "od_gen.cuh"
+#include "od_kernel.cuh"
+#include "od_scan.cuh"
+
+using namespace od;
+
+namespace {
+
+thread_local std::string g_err;
+
+#define CK(x)                                                                                      \
+    do {                                                                                           \
+        cudaError_t e_ = (x);                                                                      \
+        if (e_ != cudaSuccess) {                                                                   \
+            g_err = std::string(#x) + ": " + cudaGetErrorString(e_);                               \
+            return -3;                                                                             \
+        }                                                                                          \
+    } while (0)
+
+constexpr u32 kTileThreads = 256;
+constexpr u32 kTileVecs = 4;                                  // uint4 per thread per tile
+constexpr u32 kTileBytes = kTileThreads * kTileVecs * 16;     // 16 KiB
+
+// ------------------------------------------------------------------ P1a
+// Newline count per 16 KiB tile.  The chunk may start unaligned: the tile
+// grid covers [base - mis, base + len) and masks bytes outside.
+__global__ void k_nl_count(const u8 *__restrict__ base, u64 len, u32 mis, u32 *tile_cnt) {
+    const u8 *p0 = base - mis;
+    const u64 tile0 = (u64)blockIdx.x * kTileBytes;
+    u32 c = 0;
+#pragma unroll
+    for (u32 j = 0; j < kTileVecs; ++j) {
+        u64 o = tile0 + ((u64)j * kTileThreads + threadIdx.x) * 16;
+        if (o >= len + mis)
+            continue;
+        uint4 v = *reinterpret_cast<const uint4 *>(p0 + o);
+        u32 w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                u64 pos = o + q * 4 + b;
+                u8 ch = (u8)(w[q] >> (8 * b));
+                if (ch == '\n' && pos >= mis && pos < len + mis)
+                    ++c;
+            }
+        }
+    }
+    // block reduce
+    c = __reduce_add_sync(0xffffffffu, c);
+    __shared__ u32 sm[kTileThreads / 32];
+    if ((threadIdx.x & 31) == 0)
+        sm[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        u32 v = threadIdx.x < kTileThreads / 32 ? sm[threadIdx.x] : 0;
+        v = __reduce_add_sync(0xffffffffu, v);
+        if (threadIdx.x == 0)
+            tile_cnt[blockIdx.x] = v;
+    }
+}
+
+// Writes the chunk-relative position of every newline, in order.
+__global__ void k_nl_write(const u8 *__restrict__ base, u64 len, u32 mis, const u32 *tile_off,
+                           u32 *nlpos) {
+    const u8 *p0 = base - mis;
+    const u64 tile0 = (u64)blockIdx.x * kTileBytes;
+    __shared__ SU32 sm[32];
+    u32 run = tile_off[blockIdx.x];
+    for (u32 j = 0; j < kTileVecs; ++j) {
+        u64 o = tile0 + ((u64)j * kTileThreads + threadIdx.x) * 16;
+        u32 bits = 0; // newline bitmap of my 16 bytes
+        if (o < len + mis) {
+            uint4 v = *reinterpret_cast<const uint4 *>(p0 + o);
+            u32 w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    u64 pos = o + q * 4 + b;
+                    u8 ch = (u8)(w[q] >> (8 * b));
+                    if (ch == '\n' && pos >= mis && pos < len + mis)
+                        bits |= 1u << (q * 4 + b);
+                }
+        }
+        SU32 agg;
+        SU32 ex = block_exclusive(SU32{(u32)__popc(bits)}, SU32{0}, AddU32{}, sm, &agg);
+        u32 k = run + ex.v;
+        while (bits) {
+            u32 b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            nlpos[k++] = (u32)(o + b - mis);
+        }
+        run += agg.v;
+    }
+}
+
+// ------------------------------------------------------------------ P1b
+// Thread per line: comment strip + rtrim + first-word kind.
+__global__ void k_classify(const u8 *__restrict__ t, u64 len, const u32 *__restrict__ nlpos,
+                           u32 nlf, u32 nlines, LineRec *lines, u32 *complex_bytes) {
+    u32 l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= nlines)
+        return;
+    u32 b = l == 0 ? 0 : nlpos[l - 1] + 1;
+    u32 e = l < nlf ? nlpos[l] : (u32)len;
+    bool cx;
+    u32 cut = strip_scan(t + b, e - b, &cx);
+    LineRec r;
+    r.off = b;
+    r.complex = cx;
+    r.role = LR_NONE;
+    r.pad = 0;
+    r.aux = 0;
+    if (!cx) {
+        r.len = rtrim_len(t + b, cut);
+        r.kind = classify_content(t, Span{r.off, r.len});
+    } else {
+        r.len = e - b; // raw span, materialized later
+        r.kind = LK_BLANK;
+        atomicAdd(complex_bytes, e - b);
+    }
+    lines[l] = r;
+}
+
+// Complex lines (with a terminated /* */ mid-line) are materialized into the
+// aux area after the chunk, then classified.
+__global__ void k_materialize(u8 *t, u32 aux_base, u32 nlines, LineRec *lines, u32 *aux_top) {
+    u32 l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= nlines || !lines[l].complex)
+        return;
+    LineRec r = lines[l];
+    u32 n = strip_materialize(t + r.off, r.len, nullptr);
+    u32 dst = aux_base + atomicAdd(aux_top, n);
+    strip_materialize(t + r.off, r.len, t + dst);
+    r.off = dst;
+    r.len = rtrim_len(t + dst, n);
+    r.kind = classify_content(t, Span{r.off, r.len});
+    lines[l] = r;
+}
+
+// ------------------------------------------------------------------ P1c
+struct SecLoad {
+    const LineRec *lines;
+    __device__ SecVal operator()(u64 i) const {
+        u8 k = lines[i].kind;
+        SecVal v;
+        v.cnt = k == LK_KERNEL ? 1 : 0;
+        v.last = (k == LK_KERNEL || k == LK_DIR_CONFIG || k == LK_DIR_TEXT) ? (i32)i : -1;
+        return v;
+    }
+};
+struct SecStore {
+    LineRec *lines;
+    u32 *kstart;
+    u32 *err; // min error line (0xffffffff none) and kind
+    __device__ void operator()(u64 i, SecVal ex, SecVal v) const {
+        LineRec &L = lines[i];
+        u8 k = L.kind;
+        if (k == LK_KERNEL) {
+            kstart[ex.cnt] = (u32)i;
+            return;
+        }
+        if (k == LK_KERNEL_NONAME) {
+            atomicMin(err, (u32)i);
+            return;
+        }
+        if (k == LK_DIR_CONFIG || k == LK_DIR_TEXT) {
+            if (ex.cnt == 0)
+                atomicMin(err, (u32)i);
+            return;
+        }
+        if (k != LK_OTHER || ex.cnt == 0)
+            return;
+        u8 mode_kind = lines[ex.last].kind; // last directive before (>= the .kernel line)
+        L.role = mode_kind == LK_DIR_TEXT ? LR_TEXT : LR_CONFIG;
+    }
+};
+
+// ------------------------------------------------------------------ P1d
+__device__ RootTable d_roots;
+
+__global__ void k_init_roots() {
+    if (threadIdx.x == 0 && blockIdx.x == 0)
+        build_root_table(&d_roots);
+}
+
+// mode 0: sizing (writes per-line operand/label counts); mode 1: fill.
+__global__ void k_decode(const u8 *__restrict__ t, u32 nlines, const LineRec *__restrict__ lines,
+                         LineIns *lins, u32 *ops_cnt, u32 *labs_cnt, const u32 *ops_off,
+                         const u32 *labs_off, Opnd *ops, Label *labs, int mode) {
+    __shared__ RootTable rt;
+    for (u32 i = threadIdx.x; i < sizeof(RootTable) / 4; i += blockDim.x)
+        reinterpret_cast<u32 *>(&rt)[i] = reinterpret_cast<const u32 *>(&d_roots)[i];
+    __syncthreads();
+    u32 l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= nlines)
+        return;
+    const LineRec L = lines[l];
+    if (L.role != LR_TEXT) {
+        if (mode == 0) {
+            ops_cnt[l] = 0;
+            labs_cnt[l] = 0;
+        }
+        return;
+    }
+    LineIns li;
+    if (mode == 0) {
+        decode_line(t, Span{L.off, L.len}, &rt, &li, nullptr, nullptr);
+        ops_cnt[l] = li.nops;
+        labs_cnt[l] = li.nlabels;
+    } else {
+        u32 oo = ops_off[l], lo = labs_off[l];
+        decode_line(t, Span{L.off, L.len}, &rt, &li, ops + oo, labs + lo);
+        li.op_start = oo;
+        li.lab_start = lo;
+        lins[l] = li;
+    }
+}
+
+// ------------------------------------------------------------------ P2-P4a
+struct KRes {
+    u32 status;     // KStatus, KS_SKIP = 4 for only_kernel filtering, 5 = staging full
+    u32 structured;
+    u32 fallbacks;
+    u32 ninstr;
+    u64 stage_off;
+    u32 out_len;
+    u32 name_off;   // kernel name span (chunk-relative; >= chunk len: aux area)
+    u32 name_len;
+    u32 pad[3];
+};
+enum : u32 { KS_SKIP = 4, KS_STAGE_FULL = 5 };
+
+struct DecompArgs {
+    const u8 *t;
+    const LineRec *lines;
+    const LineIns *lins;
+    const Opnd *ops;
+    const Label *labs;
+    const u32 *kstart;
+    u32 nk, nlines, line_base, fold_local_size;
+    const u32 *list; // kernels to (re)run; null = all
+    u32 count;
+    u32 *next;
+    u8 *arena;
+    u64 arena_bytes;
+    u8 *stage;
+    u64 stage_cap;
+    unsigned long long *stage_top;
+    KRes *res;
+    const u8 *only;  // only_kernel name (device) or null
+    u32 only_len;
+};
+
+__global__ void __launch_bounds__(64) k_decompile(DecompArgs a) {
+    const u64 tid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    u8 *arena = a.arena + tid * a.arena_bytes;
+    for (;;) {
+        u32 i = atomicAdd(a.next, 1u);
+        if (i >= a.count)
+            break;
+        u32 k = a.list ? a.list[i] : i;
+        KIn in;
+        in.t = a.t;
+        in.lines = a.lines;
+        in.lins = a.lins;
+        in.ops = a.ops;
+        in.labs = a.labs;
+        in.lbeg = a.kstart[k];
+        in.lend = k + 1 < a.nk ? a.kstart[k + 1] : a.nlines;
+        in.line_base = a.line_base;
+        in.fold_local_size = a.fold_local_size;
+        KRes r;
+        r.pad[0] = r.pad[1] = r.pad[2] = 0;
+        r.stage_off = 0;
+        r.out_len = 0;
+        r.structured = r.fallbacks = r.ninstr = 0;
+        Span nm;
+        {
+            Span w, rest, extra;
+            const LineRec &L = a.lines[in.lbeg];
+            split_word(a.t, Span{L.off, L.len}, &w, &rest);
+            split_word(a.t, rest, &nm, &extra);
+        }
+        r.name_off = nm.off;
+        r.name_len = nm.len;
+        if (a.only) {
+            if (nm.len != a.only_len || !bytes_eq(a.t + nm.off, a.only, nm.len)) {
+                r.status = KS_SKIP;
+                a.res[k] = r;
+                continue;
+            }
+        }
+        Bump mem{arena, 0, a.arena_bytes, false};
+        const u8 *src = nullptr;
+        KOut o = decompile_kernel(in, mem, &src);
+        r.status = o.status;
+        r.structured = o.structured;
+        r.fallbacks = o.fallbacks;
+        r.ninstr = o.ninstr;
+        if (o.status == KS_OK && o.out_len) {
+            u64 padded = (o.out_len + 15ull) & ~15ull;
+            u64 off = atomicAdd(a.stage_top, (unsigned long long)padded);
+            if (off + padded > a.stage_cap) {
+                r.status = KS_STAGE_FULL;
+            } else {
+                const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+                uint4 *d4 = reinterpret_cast<uint4 *>(a.stage + off);
+                for (u64 q = 0; q < padded / 16; ++q)
+                    d4[q] = s4[q];
+                r.stage_off = off;
+                r.out_len = o.out_len;
+            }
+        }
+        a.res[k] = r;
+    }
+}
+
+// ------------------------------------------------------------------ P4b
+struct OutLenLoad {
+    const KRes *res;
+    __device__ SU32 operator()(u64 i) const {
+        u32 n = res[i].status == KS_OK ? res[i].out_len : 0;
+        return SU32{n ? n + 1 : 0};
+    }
+};
+struct OutOffStore {
+    u64 *off;
+    __device__ void operator()(u64 i, SU32 ex, SU32) const { off[i] = ex.v; }
+};
+
+// Warp per kernel: staging -> combined output (+ the "\n" separator that
+// combined_source puts between non-empty sources).
+__global__ void k_gather(const KRes *__restrict__ res, const u64 *__restrict__ off, u32 nk,
+                         const u8 *__restrict__ stage, u8 *out, u64 out_base, u64 total) {
+    u32 warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    u32 lane = threadIdx.x & 31;
+    if (warp >= nk)
+        return;
+    const KRes r = res[warp];
+    if (r.status != KS_OK || !r.out_len)
+        return;
+    const u8 *s = stage + r.stage_off;
+    u8 *d = out + out_base + off[warp];
+    for (u32 i = lane; i < r.out_len; i += 32)
+        d[i] = s[i];
+    if (lane == 0 && out_base + off[warp] + r.out_len < total)
+        d[r.out_len] = '\n';
+}
+
+// ------------------------------------------------------------------ generator
+struct GenArgs {
+    GenCfg cfg;
+    u64 k0, count;
+    u64 *len;   // per kernel length (sizing) -> offsets after scan
+    u32 *ninstr;
+    u8 *buf;
+};
+
+__global__ void k_gen(GenArgs a, int mode) {
+    u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.count)
+        return;
+    Writer w;
+    if (mode == 0) {
+        w.p = nullptr;
+        w.n = 0;
+        w.cap = 0;
+        w.overflow = false;
+        u32 ni = gen_kernel(a.cfg, a.k0 + i, &w);
+        a.len[i] = w.n;
+        a.ninstr[i] = ni;
+    } else {
+        u64 off = a.len[i];
+        w.p = a.buf + off;
+        w.n = 0;
+        w.cap = 0xffffffffu;
+        w.overflow = false;
+        gen_kernel(a.cfg, a.k0 + i, &w);
+    }
+}
+
+struct U64Val {
+    u64 v;
+    __device__ static U64Val shfl_up(U64Val x, int d) { return U64Val{__shfl_up_sync(0xffffffffu, x.v, d)}; }
+};
+struct AddU64 {
+    __device__ U64Val operator()(U64Val a, U64Val b) const { return U64Val{a.v + b.v}; }
+};
+struct U64Load {
+    const u64 *p;
+    __device__ U64Val operator()(u64 i) const { return U64Val{p[i]}; }
+};
+struct U64Store {
+    u64 *p;
+    __device__ void operator()(u64 i, U64Val ex, U64Val) const { p[i] = ex.v; }
+};
+struct U32Load {
+    const u32 *p;
+    __device__ SU32 operator()(u64 i) const { return SU32{p[i]}; }
+};
+struct U32Store {
+    u32 *p;
+    __device__ void operator()(u64 i, SU32 ex, SU32) const { p[i] = ex.v; }
+};
+struct U32SumLoad64 {
+    const u32 *p;
+    __device__ U64Val operator()(u64 i) const { return U64Val{p[i]}; }
+};
+
+// ================================================================== host side
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+};
+
+int ensure(DevBuf &b, size_t bytes) {
+    if (bytes <= b.cap && b.p)
+        return 0;
+    if (b.p)
+        cudaFree(b.p);
+    size_t want = std::max(bytes + 256, b.cap + b.cap / 2);
+    b.p = nullptr;
+    b.cap = 0;
+    CK(cudaMalloc(&b.p, want));
+    b.cap = want;
+    return 0;
+}
+
+// Grows b to at least bytes, preserving the first keep bytes.
+int ensure_keep(DevBuf &b, size_t bytes, size_t keep, cudaStream_t st) {
+    if (bytes <= b.cap && b.p)
+        return 0;
+    size_t want = std::max(bytes + 256, b.cap + b.cap / 2);
+    void *np = nullptr;
+    CK(cudaMalloc(&np, want));
+    if (b.p && keep) {
+        CK(cudaMemcpyAsync(np, b.p, std::min(keep, b.cap), cudaMemcpyDeviceToDevice, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    if (b.p)
+        cudaFree(b.p);
+    b.p = np;
+    b.cap = want;
+    return 0;
+}
+
+template <class T> T *P(DevBuf &b) { return reinterpret_cast<T *>(b.p); }
+
+} // namespace
+
+struct ocldec_b200_session {
+    int device = 0;
+    int nsm = 148;
+    cudaStream_t stream = nullptr;
+    size_t arena_bytes = 0;
+    u32 threads = 0; // persistent decompile threads
+    DevBuf text, tiles, tiles_off, nlpos, lines, lins, ops_cnt, labs_cnt, ops_off, labs_off, ops,
+        labs, kstart, scan_tmp, scan_tot, counters, arena, stage, res, outoff, out, only, retry,
+        gen_len, gen_ninstr, gen_buf, gen_off, kmeta;
+    u64 out_len = 0;
+    u64 nk_total = 0;
+    u32 only_len = 0;
+    bool only_set = false;
+    ocldec_b200_stats stats{};
+    cudaEvent_t ev[8];
+    std::vector<KRes> host_res;      // last run, all chunks
+    std::vector<u64> host_kernel_off;
+    std::vector<u32> host_name_line; // chunk-relative .kernel line (host path names)
+};
+
+namespace {
+
+// Generic exclusive scan launcher.
+template <class T, class Op, class Load, class Store>
+int scan_exclusive(ocldec_b200_session *s, u64 n, T ident, Op op, Load load, Store store, T *d_total) {
+    if (n == 0)
+        return 0;
+    u64 per = (u64)kScanThreads * kScanItems;
+    u64 nb = (n + per - 1) / per;
+    if (ensure(s->scan_tmp, nb * sizeof(T)))
+        return -3;
+    T *agg = P<T>(s->scan_tmp);
+    k_scan_reduce<<<(u32)nb, kScanThreads, 0, s->stream>>>(n, ident, op, load, agg);
+    k_scan_blocks<<<1, kScanThreads, 0, s->stream>>>(nb, ident, op, agg, d_total);
+    k_scan_apply<<<(u32)nb, kScanThreads, 0, s->stream>>>(n, ident, op, load, store, agg);
+    s->stats.total_launches += 3;
+    CK(cudaGetLastError());
+    return 0;
+}
+
+int d2h_sync(ocldec_b200_session *s, void *h, const void *d, size_t n) {
+    CK(cudaMemcpyAsync(h, d, n, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    return 0;
+}
+
+struct ChunkOut {
+    u32 nk;
+    u32 nlines;
+    u32 err_line; // 0xffffffff none (chunk-relative)
+    u32 err_kind;
+    u64 out_bytes;
+};
+
+// Runs P1-P4 on one chunk t[0, len) (device).  can_extend: t is the
+// session's text buffer with room for the aux area.  Outputs are appended to
+// s->out at out_base; per-kernel results are appended to s->host_res.
+int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32 line_base,
+              int fold_local_size, u64 out_base, bool prev_nonempty, ChunkOut *co) {
+    cudaStream_t st = s->stream;
+    co->nk = 0;
+    co->nlines = 0;
+    co->err_line = 0xffffffffu;
+    co->err_kind = 0;
+    co->out_bytes = 0;
+    if (len == 0)
+        return 0;
+    if (len >= 0xf0000000ull) {
+        g_err = "chunk larger than 3.75 GiB";
+        return -1;
+    }
+    const u32 mis = (u32)((uintptr_t)t & 15);
+    const u64 span = len + mis;
+    const u32 ntiles = (u32)((span + kTileBytes - 1) / kTileBytes);
+    if (ensure(s->tiles, (ntiles + 1) * 4ull) || ensure(s->tiles_off, (ntiles + 1) * 4ull) ||
+        ensure(s->counters, 64))
+        return -3;
+    u32 *cnt = P<u32>(s->counters);
+    CK(cudaMemsetAsync(cnt, 0, 64, st));
+    CK(cudaEventRecord(s->ev[0], st));
+    k_nl_count<<<ntiles, kTileThreads, 0, st>>>(t, len, mis, P<u32>(s->tiles));
+    if (scan_exclusive(s, ntiles, SU32{0}, AddU32{}, U32Load{P<u32>(s->tiles)},
+                       U32Store{P<u32>(s->tiles_off)}, reinterpret_cast<SU32 *>(cnt)))
+        return -3;
+    u32 nlf = 0;
+    if (d2h_sync(s, &nlf, cnt, 4))
+        return -3;
+    // last character: a final line without '\n' still counts
+    u8 last = 0;
+    if (d2h_sync(s, &last, t + len - 1, 1))
+        return -3;
+    const u32 nlines = nlf + (last != '\n' ? 1 : 0);
+    co->nlines = nlines;
+    if (ensure(s->nlpos, (nlf + 1) * 4ull) || ensure(s->lines, (u64)(nlines + 1) * sizeof(LineRec)))
+        return -3;
+    k_nl_write<<<ntiles, kTileThreads, 0, st>>>(t, len, mis, P<u32>(s->tiles_off), P<u32>(s->nlpos));
+    const u32 lb = 256, lg = (nlines + lb - 1) / lb;
+    k_classify<<<lg, lb, 0, st>>>(t, len, P<u32>(s->nlpos), nlf, nlines, P<LineRec>(s->lines), cnt + 1);
+    s->stats.total_launches += 3;
+    CK(cudaGetLastError());
+    u32 cbytes = 0;
+    if (d2h_sync(s, &cbytes, cnt + 1, 4))
+        return -3;
+    if (cbytes) {
+        if (!can_extend) {
+            // copy the chunk into the session buffer (with aux room) and redo
+            if (ensure(s->text, len + cbytes + 64))
+                return -3;
+            CK(cudaMemcpyAsync(s->text.p, t, len, cudaMemcpyDeviceToDevice, st));
+            return run_chunk(s, P<u8>(s->text), len, true, line_base, fold_local_size, out_base,
+                             prev_nonempty, co);
+        }
+        k_materialize<<<lg, lb, 0, st>>>(const_cast<u8 *>(t), (u32)len, nlines, P<LineRec>(s->lines),
+                                         cnt + 2);
+        s->stats.total_launches++;
+    }
+    // P1c section scan
+    if (ensure(s->kstart, (nlines + 1) * 4ull))
+        return -3;
+    CK(cudaMemsetAsync(cnt + 4, 0xff, 4, st));
+    if (scan_exclusive(s, nlines, SecVal{0, -1}, SecOp{}, SecLoad{P<LineRec>(s->lines)},
+                       SecStore{P<LineRec>(s->lines), P<u32>(s->kstart), cnt + 4},
+                       reinterpret_cast<SecVal *>(cnt + 6)))
+        return -3;
+    u32 sec[4];
+    if (d2h_sync(s, sec, cnt + 4, 16))
+        return -3;
+    const u32 err = sec[0];
+    const u32 nk = sec[2];
+    if (err != 0xffffffffu) {
+        co->err_line = err;
+        LineRec lr;
+        if (d2h_sync(s, &lr, P<LineRec>(s->lines) + err, sizeof lr))
+            return -3;
+        co->err_kind = lr.kind == LK_KERNEL_NONAME ? 1 : lr.kind == LK_DIR_CONFIG ? 2 : 3;
+        return 0;
+    }
+    co->nk = nk;
+    if (nk == 0)
+        return 0;
+    CK(cudaEventRecord(s->ev[1], st));
+    // P1d decode: sizing, scans, fill
+    if (ensure(s->lins, (u64)(nlines + 1) * sizeof(LineIns)) || ensure(s->ops_cnt, (nlines + 1) * 4ull) ||
+        ensure(s->labs_cnt, (nlines + 1) * 4ull) || ensure(s->ops_off, (nlines + 1) * 4ull) ||
+        ensure(s->labs_off, (nlines + 1) * 4ull))
+        return -3;
+    k_decode<<<lg, lb, 0, st>>>(t, nlines, P<LineRec>(s->lines), P<LineIns>(s->lins), P<u32>(s->ops_cnt),
+                                P<u32>(s->labs_cnt), nullptr, nullptr, nullptr, nullptr, 0);
+    s->stats.total_launches++;
+    if (scan_exclusive(s, nlines, SU32{0}, AddU32{}, U32Load{P<u32>(s->ops_cnt)},
+                       U32Store{P<u32>(s->ops_off)}, reinterpret_cast<SU32 *>(cnt + 8)) ||
+        scan_exclusive(s, nlines, SU32{0}, AddU32{}, U32Load{P<u32>(s->labs_cnt)},
+                       U32Store{P<u32>(s->labs_off)}, reinterpret_cast<SU32 *>(cnt + 9)))
+        return -3;
+    u32 pools[2];
+    if (d2h_sync(s, pools, cnt + 8, 8))
+        return -3;
+    if (ensure(s->ops, (pools[0] + 1ull) * sizeof(Opnd)) || ensure(s->labs, (pools[1] + 1ull) * sizeof(Label)))
+        return -3;
+    k_decode<<<lg, lb, 0, st>>>(t, nlines, P<LineRec>(s->lines), P<LineIns>(s->lins), nullptr, nullptr,
+                                P<u32>(s->ops_off), P<u32>(s->labs_off), P<Opnd>(s->ops), P<Label>(s->labs), 1);
+    s->stats.total_launches++;
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(s->ev[2], st));
+
+    // P2-P4a decompile, with retries for kernels that outgrew the arena
+    if (ensure(s->res, (u64)nk * sizeof(KRes)) || ensure(s->retry, (u64)nk * 4) ||
+        ensure(s->outoff, (u64)(nk + 1) * 8))
+        return -3;
+    u64 stage_cap = std::max<u64>(len + (64ull << 20), 2 * len);
+    if (ensure(s->stage, stage_cap))
+        return -3;
+    stage_cap = s->stage.cap;
+    DecompArgs a;
+    a.t = t;
+    a.lines = P<LineRec>(s->lines);
+    a.lins = P<LineIns>(s->lins);
+    a.ops = P<Opnd>(s->ops);
+    a.labs = P<Label>(s->labs);
+    a.kstart = P<u32>(s->kstart);
+    a.nk = nk;
+    a.nlines = nlines;
+    a.line_base = line_base;
+    a.fold_local_size = (u32)fold_local_size;
+    a.list = nullptr;
+    a.count = nk;
+    a.next = cnt + 12;
+    a.arena = P<u8>(s->arena);
+    a.arena_bytes = s->arena_bytes;
+    a.stage = P<u8>(s->stage);
+    a.stage_cap = stage_cap;
+    a.stage_top = reinterpret_cast<unsigned long long *>(cnt + 14);
+    a.res = P<KRes>(s->res);
+    a.only = s->only_set ? P<u8>(s->only) : nullptr;
+    a.only_len = s->only_len;
+    CK(cudaMemsetAsync(cnt + 12, 0, 16, st));
+    {
+        u64 nthr = std::min<u64>(s->threads, ((u64)nk + 63) / 64 * 64);
+        if (ensure(s->arena, nthr * s->arena_bytes))
+            return -3;
+        a.arena = P<u8>(s->arena);
+        u32 blocks = (u32)((nthr + 63) / 64);
+        k_decompile<<<blocks, 64, 0, st>>>(a);
+        s->stats.decompile_launches++;
+        s->stats.total_launches++;
+        CK(cudaGetLastError());
+    }
+    // retry loop on the host-visible result statuses
+    std::vector<KRes> hr(nk);
+    u64 arena_b = s->arena_bytes;
+    for (int attempt = 0; attempt < 8; ++attempt) {
+        if (d2h_sync(s, hr.data(), a.res, (u64)nk * sizeof(KRes)))
+            return -3;
+        std::vector<u32> redo;
+        bool stage_full = false;
+        for (u32 k = 0; k < nk; ++k)
+            if (hr[k].status == KS_OOM || hr[k].status == KS_STAGE_FULL) {
+                redo.push_back(k);
+                stage_full |= hr[k].status == KS_STAGE_FULL;
+            }
+        if (redo.empty())
+            break;
+        s->stats.retried += redo.size();
+        if (stage_full) {
+            u64 top = 0;
+            if (d2h_sync(s, &top, a.stage_top, 8))
+                return -3;
+            // keep existing staged bytes: grow into a fresh buffer
+            DevBuf nb;
+            u64 want = std::max<u64>(top * 2, s->stage.cap * 2);
+            CK(cudaMalloc(&nb.p, want));
+            nb.cap = want;
+            CK(cudaMemcpyAsync(nb.p, s->stage.p, std::min<u64>(top, s->stage.cap), cudaMemcpyDeviceToDevice, st));
+            CK(cudaStreamSynchronize(st));
+            cudaFree(s->stage.p);
+            s->stage = nb;
+            a.stage = P<u8>(s->stage);
+            a.stage_cap = s->stage.cap;
+            // stage_top already beyond the old cap for failed kernels: clamp
+            u64 clamp = std::min<u64>(top, a.stage_cap);
+            CK(cudaMemcpyAsync(a.stage_top, &clamp, 8, cudaMemcpyHostToDevice, st));
+        }
+        bool oom = false;
+        for (u32 k : redo)
+            oom |= hr[k].status == KS_OOM;
+        if (oom)
+            arena_b *= 4;
+        u64 threads = std::max<u64>(s->arena.cap / arena_b, 1);
+        threads = std::min<u64>(threads, redo.size());
+        if (threads * arena_b > s->arena.cap) {
+            if (arena_b > (16ull << 30)) {
+                g_err = "kernel too large for the decompile arena";
+                return -1;
+            }
+            if (ensure(s->arena, threads * arena_b))
+                return -3;
+            a.arena = P<u8>(s->arena);
+        }
+        CK(cudaMemcpyAsync(P<u32>(s->retry), redo.data(), redo.size() * 4, cudaMemcpyHostToDevice, st));
+        a.list = P<u32>(s->retry);
+        a.count = (u32)redo.size();
+        a.arena_bytes = arena_b;
+        CK(cudaMemsetAsync(cnt + 12, 0, 4, st));
+        k_decompile<<<(u32)((threads + 63) / 64), 64, 0, st>>>(a);
+        s->stats.decompile_launches++;
+        s->stats.total_launches++;
+        CK(cudaGetLastError());
+    }
+    CK(cudaEventRecord(s->ev[3], st));
+    // P4b offsets + gather
+    if (scan_exclusive(s, nk, SU32{0}, AddU32{}, OutLenLoad{a.res}, OutOffStore{P<u64>(s->outoff)},
+                       reinterpret_cast<SU32 *>(cnt + 10)))
+        return -3;
+    u32 tot = 0;
+    if (d2h_sync(s, &tot, cnt + 10, 4))
+        return -3;
+    // tot = sum(len + 1) over non-empty; the last separator is dropped
+    u64 chunk_bytes = tot ? tot - 1 : 0;
+    u64 base = out_base;
+    if (tot && prev_nonempty) {
+        // separator between the previous chunk's last source and ours
+        u8 nl = '\n';
+        if (ensure_keep(s->out, out_base + 1 + chunk_bytes + 16, out_base, st))
+            return -3;
+        CK(cudaMemcpyAsync(P<u8>(s->out) + out_base, &nl, 1, cudaMemcpyHostToDevice, st));
+        base += 1;
+    }
+    if (ensure_keep(s->out, base + chunk_bytes + 16, base, st))
+        return -3;
+    k_gather<<<(nk * 32 + 255) / 256, 256, 0, st>>>(a.res, P<u64>(s->outoff), nk, P<u8>(s->stage),
+                                                     P<u8>(s->out), base, base + chunk_bytes);
+    s->stats.total_launches++;
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(s->ev[4], st));
+    co->out_bytes = (base - out_base) + chunk_bytes;
+    // keep per-kernel results for the host API
+    if (d2h_sync(s, hr.data(), a.res, (u64)nk * sizeof(KRes)))
+        return -3;
+    std::vector<u64> offs(nk);
+    if (d2h_sync(s, offs.data(), s->outoff.p, (u64)nk * 8))
+        return -3;
+    std::vector<u32> ks(nk);
+    if (d2h_sync(s, ks.data(), s->kstart.p, (u64)nk * 4))
+        return -3;
+    for (u32 k = 0; k < nk; ++k) {
+        s->host_res.push_back(hr[k]);
+        s->host_kernel_off.push_back(base + offs[k]);
+        s->host_name_line.push_back(ks[k]);
+        s->stats.instructions += hr[k].ninstr;
+        s->stats.failed += hr[k].status == KS_FAILED;
+        s->stats.goto_form += hr[k].status == KS_OK && !hr[k].structured;
+        s->stats.fallbacks += hr[k].fallbacks;
+    }
+    float ms = 0;
+    cudaEventElapsedTime(&ms, s->ev[0], s->ev[2]);
+    s->stats.ms_parse += ms;
+    cudaEventElapsedTime(&ms, s->ev[2], s->ev[3]);
+    s->stats.ms_decompile += ms;
+    cudaEventElapsedTime(&ms, s->ev[3], s->ev[4]);
+    s->stats.ms_emit += ms;
+    return 0;
+}
+
+int session_init(ocldec_b200_session *s, int device, size_t arena_bytes) {
+    s->device = device;
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    s->nsm = prop.multiProcessorCount;
+    CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    for (auto &e : s->ev)
+        CK(cudaEventCreate(&e));
+    s->arena_bytes = arena_bytes ? arena_bytes : (size_t)1 << 20;
+    // one resident wave: 4 blocks x 64 threads per SM
+    s->threads = (u32)s->nsm * 4 * 64;
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    size_t want = (size_t)s->threads * s->arena_bytes;
+    if (want > free_b / 3)
+        s->threads = (u32)std::max<size_t>(64, (free_b / 3) / s->arena_bytes / 64 * 64);
+    // the stack holds the per-thread pipeline context
+    CK(cudaDeviceSetLimit(cudaLimitStackSize, 16 * 1024));
+    k_init_roots<<<1, 1, 0, s->stream>>>();
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s->stream));
+    return 0;
+}
+
+void reset_stats(ocldec_b200_session *s) {
+    s->stats = ocldec_b200_stats{};
+    s->host_res.clear();
+    s->host_kernel_off.clear();
+    s->host_name_line.clear();
+    s->out_len = 0;
+}
+
+// Splits a host listing into chunks of < ~1 GiB at ".kernel" line starts.
+std::vector<u64> host_chunks(const char *p, size_t len, size_t target) {
+    std::vector<u64> starts{0};
+    size_t next = target;
+    while (next < len) {
+        // find a line whose first word is exactly ".kernel"
+        size_t i = next;
+        bool found = false;
+        while (i < len) {
+            const void *nlp = memchr(p + i, '\n', len - i);
+            if (!nlp)
+                break;
+            size_t ls = (const char *)nlp - p + 1;
+            size_t j = ls;
+            while (j < len && (p[j] == ' ' || p[j] == '\t'))
+                ++j;
+            if (j + 7 <= len && memcmp(p + j, ".kernel", 7) == 0 &&
+                (j + 7 == len || p[j + 7] == ' ' || p[j + 7] == '\t' || p[j + 7] == '\n' || p[j + 7] == '\r')) {
+                starts.push_back(ls);
+                found = true;
+                break;
+            }
+            i = ls;
+        }
+        if (!found)
+            break;
+        next = starts.back() + target;
+    }
+    return starts;
+}
+
+
+struct HostRun {
+    u64 out_bytes = 0;
+    int32_t split_error_line = 0, split_error_kind = 0;
+    double device_ms = 0;
+    std::vector<std::string> names;
+};
+
+std::mutex g_cache_mu;
+std::map<std::pair<int, size_t>, ocldec_b200_session *> g_cache;
+
+size_t chunk_target() {
+    const char *e = getenv("OCLDEC_B200_CHUNK_BYTES");
+    if (e && *e) {
+        size_t v = strtoull(e, nullptr, 0);
+        if (v >= 1)
+            return v;
+    }
+    return (size_t)1 << 30;
+}
+
+// decompile_listing over a host buffer: chunking at .kernel lines, H2D of
+// each chunk, the device pipeline, names back to the host.  Output stays in
+// s->out[0, out_bytes).
+int run_host_listing(ocldec_b200_session *s, const char *listing, size_t len, int fold_local_size,
+                     const char *only_kernel, HostRun *hr) {
+    reset_stats(s);
+    s->stats.in_bytes = len;
+    s->only_len = 0;
+    if (only_kernel) {
+        u32 ol = (u32)strlen(only_kernel);
+        if (ensure(s->only, ol + 8))
+            return -3;
+        CK(cudaMemcpy(s->only.p, only_kernel, ol, cudaMemcpyHostToDevice));
+        s->only_len = ol;
+        s->only_set = true;
+    } else {
+        s->only_set = false;
+    }
+    std::vector<u64> starts = host_chunks(listing, len, chunk_target());
+    u64 out_pos = 0;
+    u32 line_base = 0;
+    bool nonempty = false;
+    cudaEvent_t e0 = s->ev[5], e1 = s->ev[6];
+    CK(cudaEventRecord(e0, s->stream));
+    for (size_t c = 0; c < starts.size(); ++c) {
+        u64 b = starts[c];
+        u64 e = c + 1 < starts.size() ? starts[c + 1] : len;
+        u64 n = e - b;
+        if (ensure(s->text, 2 * n + 4096))
+            return -3;
+        if (n)
+            CK(cudaMemcpyAsync(s->text.p, listing + b, n, cudaMemcpyHostToDevice, s->stream));
+        ChunkOut co;
+        size_t before = s->host_res.size();
+        int rc = run_chunk(s, P<u8>(s->text), n, true, line_base, fold_local_size, out_pos, nonempty, &co);
+        if (rc)
+            return rc;
+        if (co.err_line != 0xffffffffu) {
+            hr->split_error_line = (int32_t)(line_base + co.err_line + 1);
+            hr->split_error_kind = (int32_t)co.err_kind;
+            s->host_res.clear();
+            s->host_kernel_off.clear();
+            hr->names.clear();
+            out_pos = 0;
+            break;
+        }
+        for (size_t k = before; k < s->host_res.size(); ++k) {
+            const KRes &r = s->host_res[k];
+            std::string nm;
+            if (r.name_off + (u64)r.name_len <= n) {
+                nm.assign(listing + b + r.name_off, r.name_len);
+            } else {
+                nm.resize(r.name_len);
+                if (r.name_len)
+                    CK(cudaMemcpy(&nm[0], P<u8>(s->text) + r.name_off, r.name_len, cudaMemcpyDeviceToHost));
+            }
+            hr->names.push_back(nm);
+        }
+        out_pos += co.out_bytes;
+        nonempty = nonempty || co.out_bytes > 0;
+        line_base += co.nlines;
+        s->stats.lines += co.nlines;
+        s->stats.kernels += co.nk;
+    }
+    CK(cudaEventRecord(e1, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    hr->device_ms = ms;
+    hr->out_bytes = out_pos;
+    s->out_len = out_pos;
+    s->stats.out_bytes = out_pos;
+    return 0;
+}
+
+} // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+const char *ocldec_b200_last_error(void) { return g_err.c_str(); }
+int ocldec_b200_version(void) { return OCLDEC_B200_ABI_VERSION; }
+
+ocldec_b200_session *ocldec_b200_session_create(int device, size_t arena_bytes) {
+    auto *s = new ocldec_b200_session();
+    if (session_init(s, device, arena_bytes)) {
+        delete s;
+        return nullptr;
+    }
+    return s;
+}
+
+void ocldec_b200_session_destroy(ocldec_b200_session *s) {
+    if (!s)
+        return;
+    cudaSetDevice(s->device);
+    DevBuf *bufs[] = {&s->text, &s->tiles, &s->tiles_off, &s->nlpos, &s->lines, &s->lins, &s->ops_cnt,
+                      &s->labs_cnt, &s->ops_off, &s->labs_off, &s->ops, &s->labs, &s->kstart,
+                      &s->scan_tmp, &s->scan_tot, &s->counters, &s->arena, &s->stage, &s->res,
+                      &s->outoff, &s->out, &s->only, &s->retry, &s->gen_len, &s->gen_ninstr,
+                      &s->gen_buf, &s->gen_off, &s->kmeta};
+    for (DevBuf *b : bufs)
+        if (b->p)
+            cudaFree(b->p);
+    for (auto &e : s->ev)
+        cudaEventDestroy(e);
+    if (s->stream)
+        cudaStreamDestroy(s->stream);
+    delete s;
+}
+
+void *ocldec_b200_session_stream(ocldec_b200_session *s) { return s ? (void *)s->stream : nullptr; }
+
+int ocldec_b200_session_run(ocldec_b200_session *s, const void *d_listing, size_t len,
+                            const uint64_t *chunk_starts, size_t nchunks, int fold_local_size, int sync) {
+    if (!s || (!d_listing && len)) {
+        g_err = "bad arguments";
+        return -1;
+    }
+    CK(cudaSetDevice(s->device));
+    reset_stats(s);
+    s->only_set = false;
+    s->stats.in_bytes = len;
+    u64 out_pos = 0;
+    u32 line_base = 0;
+    bool nonempty = false;
+    const u8 *base = static_cast<const u8 *>(d_listing);
+    if (nchunks == 0) {
+        static const uint64_t zero = 0;
+        chunk_starts = &zero;
+        nchunks = 1;
+    }
+    for (size_t c = 0; c < nchunks; ++c) {
+        u64 b = chunk_starts[c];
+        u64 e = c + 1 < nchunks ? chunk_starts[c + 1] : len;
+        ChunkOut co;
+        int rc = run_chunk(s, base + b, e - b, false, line_base, fold_local_size, out_pos, nonempty, &co);
+        if (rc)
+            return rc;
+        if (co.err_line != 0xffffffffu) {
+            g_err = "split_kernels error";
+            s->stats.lines += co.nlines;
+            return -4;
+        }
+        out_pos += co.out_bytes;
+        nonempty = nonempty || co.out_bytes > 0;
+        // next chunk's first line number: lines so far (chunk ends right after a '\n')
+        line_base += co.nlines;
+        s->stats.lines += co.nlines;
+        s->stats.kernels += co.nk;
+    }
+    s->out_len = out_pos;
+    s->stats.out_bytes = out_pos;
+    if (sync)
+        CK(cudaStreamSynchronize(s->stream));
+    return 0;
+}
+
+int ocldec_b200_session_stats(ocldec_b200_session *s, ocldec_b200_stats *st) {
+    if (!s || !st)
+        return -1;
+    *st = s->stats;
+    return 0;
+}
+
+int ocldec_b200_session_output(ocldec_b200_session *s, const void **d_out, uint64_t *len) {
+    if (!s)
+        return -1;
+    *d_out = s->out.p;
+    *len = s->out_len;
+    return 0;
+}
+
+int ocldec_b200_session_kernels(ocldec_b200_session *s, uint64_t *off, uint64_t *len, uint32_t *flags,
+                                uint32_t *fallbacks) {
+    if (!s)
+        return -1;
+    for (size_t k = 0; k < s->host_res.size(); ++k) {
+        const KRes &r = s->host_res[k];
+        if (off)
+            off[k] = s->host_kernel_off[k];
+        if (len)
+            len[k] = r.status == KS_OK ? r.out_len : 0;
+        if (flags)
+            flags[k] = (r.status == KS_FAILED ? 1u : 0u) | (r.structured ? 2u : 0u) |
+                       (r.status == KS_SKIP ? 4u : 0u);
+        if (fallbacks)
+            fallbacks[k] = r.fallbacks;
+    }
+    return 0;
+}
+
+int ocldec_b200_decompile(const char *listing, size_t len, const ocldec_b200_options *opts,
+                          ocldec_b200_result **out) {
+    if (!out || (!listing && len)) {
+        g_err = "bad arguments";
+        return -1;
+    }
+    *out = nullptr;
+    ocldec_b200_options o{};
+    if (opts)
+        o = *opts;
+    std::lock_guard<std::mutex> lock(g_cache_mu);
+    ocldec_b200_session *&s = g_cache[{o.device, o.arena_bytes}];
+    if (!s)
+        s = ocldec_b200_session_create(o.device, o.arena_bytes);
+    if (!s)
+        return -3;
+    CK(cudaSetDevice(s->device));
+    HostRun hr;
+    int rc = run_host_listing(s, listing, len, o.fold_local_size, o.only_kernel, &hr);
+    if (rc)
+        return rc;
+    auto *res = static_cast<ocldec_b200_result *>(calloc(1, sizeof(ocldec_b200_result)));
+    res->split_error_line = hr.split_error_line;
+    res->split_error_kind = hr.split_error_kind;
+    res->device_ms = hr.device_ms;
+    const u64 out_pos = hr.out_bytes;
+    res->combined = static_cast<char *>(malloc(out_pos + 1));
+    if (out_pos) {
+        CK(cudaMemcpyAsync(res->combined, s->out.p, out_pos, cudaMemcpyDeviceToHost, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+    }
+    res->combined[out_pos] = 0;
+    res->combined_len = out_pos;
+    size_t nk = s->host_res.size();
+    res->kernels = static_cast<ocldec_b200_kernel *>(calloc(nk + 1, sizeof(ocldec_b200_kernel)));
+    std::string nm;
+    u64 nkept = 0;
+    for (size_t k = 0; k < nk; ++k) {
+        const KRes &r = s->host_res[k];
+        if (r.status == KS_SKIP)
+            continue;
+        ocldec_b200_kernel &K = res->kernels[nkept++];
+        K.name_off = nm.size();
+        K.name_len = hr.names[k].size();
+        nm += hr.names[k];
+        K.src_off = s->host_kernel_off[k];
+        K.src_len = r.status == KS_OK ? r.out_len : 0;
+        K.failed = r.status == KS_FAILED;
+        K.structured = r.structured;
+        K.fallback_count = (int32_t)r.fallbacks;
+        K.instructions = r.ninstr;
+        res->instructions += r.ninstr;
+    }
+    res->nkernels = nkept;
+    res->names = static_cast<char *>(malloc(nm.size() + 1));
+    memcpy(res->names, nm.data(), nm.size());
+    res->names[nm.size()] = 0;
+    *out = res;
+    return 0;
+}
+
+int ocldec_b200_session_run_host(ocldec_b200_session *s, const char *listing, size_t len,
+                                 int fold_local_size, char *host_out, uint64_t out_cap,
+                                 uint64_t *out_len) {
+    if (!s || (!listing && len) || !out_len) {
+        g_err = "bad arguments";
+        return -1;
+    }
+    CK(cudaSetDevice(s->device));
+    HostRun hr;
+    int rc = run_host_listing(s, listing, len, fold_local_size, nullptr, &hr);
+    if (rc)
+        return rc;
+    *out_len = hr.out_bytes;
+    if (hr.out_bytes > out_cap || !host_out) {
+        g_err = "output buffer too small";
+        return -2;
+    }
+    if (hr.out_bytes) {
+        CK(cudaMemcpyAsync(host_out, s->out.p, hr.out_bytes, cudaMemcpyDeviceToHost, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+    }
+    return 0;
+}
+
+void ocldec_b200_free(ocldec_b200_result *res) {
+    if (!res)
+        return;
+    free(res->kernels);
+    free(res->names);
+    free(res->combined);
+    free(res);
+}
+
+int64_t ocldec_b200_gen_host(int shape, int stress, uint64_t seed, uint64_t k0, uint64_t count, char *buf,
+                             uint64_t cap, uint64_t *offsets, uint64_t *instructions, uint64_t *needed) {
+    GenCfg g{(u32)shape, (u32)stress, seed};
+    u64 total = 0, ni = 0;
+    for (u64 i = 0; i < count; ++i) {
+        Writer w{nullptr, 0, 0, false};
+        ni += gen_kernel(g, k0 + i, &w);
+        if (offsets)
+            offsets[i] = total;
+        total += w.n;
+    }
+    if (offsets)
+        offsets[count] = total;
+    if (needed)
+        *needed = total;
+    if (instructions)
+        *instructions = ni;
+    if (!buf)
+        return (int64_t)total;
+    if (total > cap)
+        return -2;
+    for (u64 i = 0; i < count; ++i) {
+        u64 off = offsets ? offsets[i] : 0;
+        Writer w{reinterpret_cast<u8 *>(buf) + off, 0, 0xffffffffu, false};
+        gen_kernel(g, k0 + i, &w);
+    }
+    return (int64_t)total;
+}
+
+int ocldec_b200_gen_device(ocldec_b200_session *s, int shape, int stress, uint64_t seed, uint64_t k0,
+                           uint64_t count, const void **d_buf, uint64_t *len, const uint64_t **d_offsets,
+                           uint64_t *instructions) {
+    if (!s)
+        return -1;
+    CK(cudaSetDevice(s->device));
+    if (ensure(s->gen_len, (count + 1) * 8) || ensure(s->gen_ninstr, (count + 1) * 4) ||
+        ensure(s->gen_off, (count + 1) * 8) || ensure(s->counters, 64))
+        return -3;
+    GenArgs a;
+    a.cfg = GenCfg{(u32)shape, (u32)stress, seed};
+    a.k0 = k0;
+    a.count = count;
+    a.len = P<u64>(s->gen_len);
+    a.ninstr = P<u32>(s->gen_ninstr);
+    a.buf = nullptr;
+    CK(cudaMemsetAsync(a.len + count, 0, 8, s->stream));
+    k_gen<<<(u32)((count + 127) / 128), 128, 0, s->stream>>>(a, 0);
+    CK(cudaGetLastError());
+    // offsets = exclusive scan of lengths (count + 1 entries, last = total)
+    if (scan_exclusive(s, count + 1, U64Val{0}, AddU64{}, U64Load{a.len}, U64Store{P<u64>(s->gen_off)},
+                       reinterpret_cast<U64Val *>(P<u32>(s->counters) + 8)))
+        return -3;
+    u64 total = 0;
+    if (d2h_sync(s, &total, P<u64>(s->gen_off) + count, 8))
+        return -3;
+    // instruction total
+    if (scan_exclusive(s, count, U64Val{0}, AddU64{}, U32SumLoad64{a.ninstr}, U64Store{a.len},
+                       reinterpret_cast<U64Val *>(P<u32>(s->counters) + 12)))
+        return -3;
+    u64 ni = 0;
+    if (d2h_sync(s, &ni, P<u32>(s->counters) + 12, 8))
+        return -3;
+    if (ensure(s->gen_buf, total + 64))
+        return -3;
+    a.len = P<u64>(s->gen_off);
+    a.buf = P<u8>(s->gen_buf);
+    k_gen<<<(u32)((count + 127) / 128), 128, 0, s->stream>>>(a, 1);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s->stream));
+    *d_buf = s->gen_buf.p;
+    *len = total;
+    *d_offsets = P<u64>(s->gen_off);
+    if (instructions)
+        *instructions = ni;
+    return 0;
+}
+
+} // extern "C"

@@ -14,10 +14,12 @@
 
 #if defined(__CUDACC__)
 #define OD_HD __host__ __device__
-#define OD_INL __host__ __device__ __forceinline__
+#define OD_INL __host__ __device__ inline
+#define OD_NOINL __host__ __device__ __noinline__
 #else
 #define OD_HD
 #define OD_INL inline
+#define OD_NOINL inline
 #define __host__
 #define __device__
 #endif
@@ -120,6 +122,14 @@ OD_INL DT dt_from_suffix(u32 s) {
     case SB_F: return dt_make(B_FLOAT, sfx_bits(s));
     default: return dt_make(B_BINARY, sfx_bits(s));
     }
+}
+
+OD_INL u32 ctz32(u32 m) {
+#ifdef __CUDA_ARCH__
+    return (u32)__ffs((int)m) - 1;
+#else
+    return (u32)__builtin_ctz(m);
+#endif
 }
 
 // ------------------------------------------------------------- characters

@@ -58,7 +58,7 @@ struct EArena {
     OD_INL bool is_const_v(u32 i, u64 v) const { return is_const(i) && cval(i) == v; }
 
     // Expr::constant  expr.cpp:40-44
-    OD_INL u32 constant(u64 v, DT t) {
+    OD_NOINL u32 constant(u64 v, DT t) {
         u32 bits = dt_bits(t) ? dt_bits(t) : 64;
         u64 mask = bits >= 64 ? ~0ull : ((1ull << bits) - 1);
         v &= mask;
@@ -76,7 +76,7 @@ struct EArena {
         e.memo = 0;
         return i;
     }
-    OD_INL u32 leaf(u8 kind, u8 op, u16 x, DT t, u32 a) {
+    OD_NOINL u32 leaf(u8 kind, u8 op, u16 x, DT t, u32 a) {
         u32 i = alloc();
         if (!i)
             return 0;
@@ -97,7 +97,7 @@ struct EArena {
     OD_INL u32 var(u32 cls, u32 num, DT t) { return leaf(E_VAR, 0, (u16)cls, t, num); }
 
     // Expr::unary  expr.cpp:71-93
-    OD_INL u32 unary(u32 op, u32 a, DT t) {
+    OD_NOINL u32 unary(u32 op, u32 a, DT t) {
         if (a) {
             const ENode &x = n[a];
             if (op == U_LO32 && x.kind == E_BINARY && x.op == O_CONCAT64)
@@ -131,7 +131,7 @@ struct EArena {
     }
 
     // Expr::binary  expr.cpp:95-132
-    OD_INL u32 binary(u32 op, u32 a, u32 b, DT t) {
+    OD_NOINL u32 binary(u32 op, u32 a, u32 b, DT t) {
         if (a && b && is_const(a) && is_const(b) && !dt_is_float(t) && dt_bits(t) <= 32) {
             u32 x = (u32)cval(a), y = (u32)cval(b);
             bool folded = true;
@@ -178,7 +178,7 @@ struct EArena {
     }
 
     // Expr::ternary  expr.cpp:134-140
-    OD_INL u32 ternary(u32 cond, u32 a, u32 b, DT t) {
+    OD_NOINL u32 ternary(u32 cond, u32 a, u32 b, DT t) {
         if (cond && is_const(cond))
             return cval(cond) ? a : b;
         u32 i = alloc();
@@ -197,7 +197,7 @@ struct EArena {
     }
 
     // Expr::deref  expr.cpp:142-148
-    OD_INL u32 deref(u32 addr, DT pointee, u32 space) {
+    OD_NOINL u32 deref(u32 addr, DT pointee, u32 space) {
         u32 i = alloc();
         if (!i)
             return 0;
@@ -232,7 +232,7 @@ struct U32Stack {
 };
 
 // expr_equal  expr.cpp:152-177 (iterative; pointer equality short-cuts)
-OD_INL bool expr_equal(const EArena &E, u32 a, u32 b, U32Stack &st) {
+OD_NOINL bool expr_equal(const EArena &E, u32 a, u32 b, U32Stack &st) {
     u32 base = st.top;
     st.push(a);
     st.push(b);
@@ -308,7 +308,7 @@ OD_INL bool expr_equal(const EArena &E, u32 a, u32 b, U32Stack &st) {
 }
 
 // negate_condition  expr.cpp:206-228
-OD_INL u32 negate_condition(EArena &E, u32 e) {
+OD_NOINL u32 negate_condition(EArena &E, u32 e) {
     if (e && E.n[e].kind == E_BINARY) {
         u32 op = E.n[e].op, f = op;
         switch (op) {
@@ -336,7 +336,7 @@ OD_INL u32 negate_condition(EArena &E, u32 e) {
 
 // collect_add_terms  expr.cpp:179-186: appends the in-order leaves of the
 // Add tree rooted at e to out (left to right).
-OD_INL void collect_add_terms(const EArena &E, u32 e, U32Stack &st, U32Stack &out) {
+OD_NOINL void collect_add_terms(const EArena &E, u32 e, U32Stack &st, U32Stack &out) {
     u32 base = st.top;
     st.push(e);
     while (st.top > base && !st.oom) {

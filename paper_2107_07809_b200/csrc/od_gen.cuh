@@ -757,7 +757,7 @@ OD_INL u32 gen_target(Gen &g, u32 shape) {
 
 // Writes kernel k of the corpus into *w (w->cap == 0: sizing only).
 // Returns the number of instruction lines emitted.
-OD_INL u32 gen_kernel(const GenCfg &cfg, u64 k, Writer *w) {
+OD_NOINL u32 gen_kernel(const GenCfg &cfg, u64 k, Writer *w) {
     Gen g;
     g.w = w;
     g.st = splitmix64(cfg.seed ^ (k * 0x9e3779b97f4a7c15ull + 0x2107078090ull));

@@ -411,7 +411,7 @@ OD_INL bool sanitized_eq(const u8 *t, Span a, Span b) {
 }
 
 // parse_config  asm_frontend.cpp:283-373 (diagnostics are not materialized)
-OD_INL bool parse_config(KCtx &K) {
+OD_NOINL bool parse_config(KCtx &K) {
     const KIn &in = *K.in;
     const u8 *t = in.t;
     KConfig &c = K.cfg;
@@ -531,7 +531,7 @@ OD_INL void abi_add(KCtx &K, const AbiEntry &e) {
 }
 
 // build_abi_map  abi_model.cpp:155-245 (no overrides)
-OD_INL bool build_abi(KCtx &K) {
+OD_NOINL bool build_abi(KCtx &K) {
     K.abi = K.mem->get<AbiEntry>(8 + K.cfg.nargs);
     if (!K.abi)
         return false;
@@ -621,7 +621,7 @@ OD_INL u32 match_settings_load(KCtx &K, u32 offset, u32 dwords) {
 }
 
 // ====================================================== instructions
-OD_INL void classify_exec(const KCtx &K, Ins &I) {
+OD_NOINL void classify_exec(const KCtx &K, Ins &I) {
     I.xkind = XK_NONE;
     I.xmask = 0;
     if ((I.flags & IF_PARSE_FAILED) || I.prefix != PX_S)
@@ -666,7 +666,7 @@ OD_INL void classify_exec(const KCtx &K, Ins &I) {
 
 // parse_text + attach_trailing_labels (asm_frontend.cpp:486-521,
 // decompiler.cpp:20-31)
-OD_INL bool collect_instructions(KCtx &K) {
+OD_NOINL bool collect_instructions(KCtx &K) {
     const KIn &in = *K.in;
     u32 nl = in.lend - in.lbeg;
     K.ins = K.mem->get<Ins>(nl + 1);
@@ -776,7 +776,7 @@ OD_INL int resolve_target(KCtx &K, const Ins &I) {
     return b;
 }
 
-OD_INL void mark_reachable(KCtx &K) {
+OD_NOINL void mark_reachable(KCtx &K) {
     for (u32 b = 0; b < K.nblk; ++b)
         K.blk[b].reachable = 0;
     if (!K.nblk)
@@ -795,7 +795,7 @@ OD_INL void mark_reachable(KCtx &K) {
 }
 
 // build_cfg  cfg.cpp:64-156
-OD_INL bool build_cfg(KCtx &K) {
+OD_NOINL bool build_cfg(KCtx &K) {
     u32 n = K.nins;
     K.blk_cap = n + 2;
     K.blk = K.mem->get<Block>(K.blk_cap);
@@ -908,7 +908,7 @@ OD_INL bool build_cfg(KCtx &K) {
 }
 
 // annotate_exec for one block: first and last non-suppressed exec op.
-OD_INL void annotate_block(KCtx &K, u32 b) {
+OD_NOINL void annotate_block(KCtx &K, u32 b) {
     Block &B = K.blk[b];
     B.xfront.kind = B.xback.kind = XK_NONE;
     for (u32 i = B.ib; i < B.ie; ++i) {
@@ -929,7 +929,7 @@ OD_INL void annotate_block(KCtx &K, u32 b) {
 }
 
 // split_block  structurizer.cpp:416-435
-OD_INL u32 split_block(KCtx &K, u32 id, u32 at) {
+OD_NOINL u32 split_block(KCtx &K, u32 id, u32 at) {
     u32 nid = K.nblk++;
     Block &B = K.blk[id];
     Block &N = K.blk[nid];
@@ -958,7 +958,7 @@ OD_INL u32 split_block(KCtx &K, u32 id, u32 at) {
 // before the split point are already canonical and a split block becomes
 // canonical, so one forward pass over the growing block list performs the
 // identical split sequence.
-OD_INL void canonicalize(KCtx &K) {
+OD_NOINL void canonicalize(KCtx &K) {
     for (u32 b = 0; b < K.nblk; ++b) {
         Block &B = K.blk[b];
         u32 size = B.ie - B.ib;
@@ -996,7 +996,7 @@ OD_INL bool first_exec_op_is(const KCtx &K, u32 b, u32 kind, u32 mask) {
 
 // mask_stops  structurizer.cpp:482-507.  Returns the number of stops found
 // (saturating at 2) and the first in *stop.
-OD_INL u32 mask_stops(KCtx &K, const i32 *starts, u32 nstarts, u32 mask, i32 header, i32 *stop) {
+OD_NOINL u32 mask_stops(KCtx &K, const i32 *starts, u32 nstarts, u32 mask, i32 header, i32 *stop) {
     u32 gen = ++K.stamp_gen;
     u32 sp = 0;
     u32 nstops = 0;
@@ -1026,7 +1026,7 @@ OD_INL u32 mask_stops(KCtx &K, const i32 *starts, u32 nstarts, u32 mask, i32 hea
 }
 
 // retarget_preds  structurizer.cpp:512-525
-OD_INL void retarget_preds(KCtx &K, i32 from, i32 to, i32 keep) {
+OD_NOINL void retarget_preds(KCtx &K, i32 from, i32 to, i32 keep) {
     for (u32 p = 0; p < K.nblk; ++p) {
         Block &P = K.blk[p];
         bool is_pred = false;
@@ -1055,7 +1055,7 @@ struct MaskPattern {
 };
 
 // apply_mask_pattern  structurizer.cpp:527-609
-OD_INL bool apply_mask_pattern(KCtx &K, const MaskPattern &pat, u32 *touched, u32 *ntouched) {
+OD_NOINL bool apply_mask_pattern(KCtx &K, const MaskPattern &pat, u32 *touched, u32 *ntouched) {
     Block &h = K.blk[pat.header];
     const u32 save_index = h.xback.index;
     i32 stop = -1;
@@ -1117,7 +1117,7 @@ OD_INL bool apply_mask_pattern(KCtx &K, const MaskPattern &pat, u32 *touched, u3
 }
 
 // normalize_if_else  structurizer.cpp:613-654
-OD_INL void normalize(KCtx &K) {
+OD_NOINL void normalize(KCtx &K) {
     canonicalize(K);
     const u32 nb = K.nblk;
     for (u32 scan = 0; scan < nb; ++scan) {
@@ -1199,7 +1199,7 @@ OD_INL u32 make_region(KCtx &K, u8 kind) {
     return id;
 }
 
-OD_INL void rebuild_region_preds(KCtx &K) {
+OD_NOINL void rebuild_region_preds(KCtx &K) {
     for (u32 i = 0; i < K.nlive; ++i)
         K.pred_n[K.live[i]] = 0;
     for (u32 i = 0; i < K.nlive; ++i) {
@@ -1233,7 +1233,7 @@ OD_INL void region_add_edge(KCtx &K, u32 from, u32 to) {
 }
 
 // RegionGraph::from_cfg  structurizer.cpp:88-111
-OD_INL bool build_regions(KCtx &K) {
+OD_NOINL bool build_regions(KCtx &K) {
     u32 cap = 2 * K.nblk + 4;
     K.rg_cap = cap;
     K.rg = K.mem->get<Region>(cap + 1);
@@ -1290,7 +1290,7 @@ OD_INL bool single_pred_is(const KCtx &K, u32 node, u32 pred) {
 }
 
 // RegionGraph::replace  structurizer.cpp:141-185
-OD_INL void region_replace(KCtx &K, const u32 *old, u32 nold, u32 merged) {
+OD_NOINL void region_replace(KCtx &K, const u32 *old, u32 nold, u32 merged) {
     u32 gen = ++K.rstamp_gen;
     for (u32 i = 0; i < nold; ++i)
         K.rstamp[old[i]] = gen;
@@ -1368,7 +1368,7 @@ OD_INL void push_children(KCtx &K, u32 m, const u32 *c, u32 n) {
 }
 
 // match_if_else  structurizer.cpp:230-274
-OD_INL u32 match_if_else(KCtx &K, u32 r) {
+OD_NOINL u32 match_if_else(KCtx &K, u32 r) {
     const Region &R = K.rg[r];
     if (R.nsucc != 2 || R.succ[0] == R.succ[1])
         return 0;
@@ -1409,7 +1409,7 @@ OD_INL u32 match_if_else(KCtx &K, u32 r) {
 }
 
 // match_if  structurizer.cpp:276-323
-OD_INL u32 match_if(KCtx &K, u32 r) {
+OD_NOINL u32 match_if(KCtx &K, u32 r) {
     const Region &R = K.rg[r];
     if (R.nsucc != 2 || R.succ[0] == R.succ[1])
         return 0;
@@ -1453,7 +1453,7 @@ OD_INL u32 match_if(KCtx &K, u32 r) {
 }
 
 // match_linear  structurizer.cpp:325-352
-OD_INL u32 match_linear(KCtx &K, u32 r) {
+OD_NOINL u32 match_linear(KCtx &K, u32 r) {
     u32 cb = K.nchild; // build the chain directly in the child pool
     u32 n = 0;
     if (cb + 1 > K.child_cap) {
@@ -1493,7 +1493,7 @@ OD_INL u32 match_linear(KCtx &K, u32 r) {
 }
 
 // RegionGraph::rpo  structurizer.cpp:113-139
-OD_INL u32 region_rpo(KCtx &K) {
+OD_NOINL u32 region_rpo(KCtx &K) {
     if (K.entry_r < 0)
         return 0;
     u32 gen = ++K.rstamp_gen;
@@ -1529,7 +1529,7 @@ OD_INL u32 region_rpo(KCtx &K) {
 }
 
 // reduce  structurizer.cpp:354-403
-OD_INL void reduce(KCtx &K) {
+OD_NOINL void reduce(KCtx &K) {
     bool progress = true;
     while (progress && K.nlive > 1 && !K.oom) {
         progress = false;
@@ -1592,7 +1592,7 @@ OD_INL void add_operand_regs(const Opnd &op, u32 *set) {
 }
 
 // instruction_use_def  cfg.cpp:272-352
-OD_INL void instruction_use_def(const KCtx &K, const Ins &I, u32 *use, u32 *def) {
+OD_NOINL void instruction_use_def(const KCtx &K, const Ins &I, u32 *use, u32 *def) {
     const Opnd *o = K.in->ops + I.op_start;
     const u32 n = (I.flags & IF_SYNTH) ? 0 : I.nops;
     if (I.flags & IF_PARSE_FAILED) {
@@ -1662,7 +1662,7 @@ OD_INL void instruction_use_def(const KCtx &K, const Ins &I, u32 *use, u32 *def)
 
 // live_in_sets  cfg.cpp:356-398 (word-parallel; the least fixpoint is
 // unique, so iteration order does not matter)
-OD_INL bool liveness(KCtx &K) {
+OD_NOINL bool liveness(KCtx &K) {
     const u32 nb = K.nblk;
     u32 *use = K.mem->get<u32>((u64)nb * kLiveWords);
     u32 *def = K.mem->get<u32>((u64)nb * kLiveWords);

@@ -61,7 +61,7 @@ OD_INL void record_fresh(KCtx &K, u32 cls, u32 num, DT t) {
 }
 
 // bind_fresh  sym_state.cpp:63-78
-OD_INL u32 bind_fresh(KCtx &K, u32 p, DT t = DT_B32) {
+OD_NOINL u32 bind_fresh(KCtx &K, u32 p, DT t = DT_B32) {
     Slot &s = K.regs[p];
     if (!s.expr) {
         log_slot(K, p);
@@ -88,7 +88,7 @@ OD_INL u32 read_slot32(KCtx &K, u32 id) {
 }
 
 // concat64  sym_state.cpp:96-105
-OD_INL u32 concat64(KCtx &K, u32 lo, u32 hi) {
+OD_NOINL u32 concat64(KCtx &K, u32 lo, u32 hi) {
     EArena &E = K.E;
     if (E.is_const_v(hi, 0))
         return E.unary(U_CAST, lo, DT_U64);
@@ -101,7 +101,7 @@ OD_INL u32 concat64(KCtx &K, u32 lo, u32 hi) {
 // read_pair_ids  sym_state.cpp:107-114.  The two read_slot32 calls are
 // arguments of one call; GCC (the oracle's compiler) evaluates them right to
 // left, which fixes the order fresh variables are recorded in.
-OD_INL u32 read_pair_ids(KCtx &K, u32 lo_id) {
+OD_NOINL u32 read_pair_ids(KCtx &K, u32 lo_id) {
     const Slot &lo = K.regs[phys_of(lo_id)];
     const Slot &hi = K.regs[phys_of(lo_id + 1)];
     if (lo.expr && lo.expr == hi.expr && lo.integ == IN_LOW && hi.integ == IN_HIGH)
@@ -112,7 +112,7 @@ OD_INL u32 read_pair_ids(KCtx &K, u32 lo_id) {
 }
 
 // dissolve_pair  sym_state.cpp:118-135
-OD_INL void dissolve_pair(KCtx &K, u32 id) {
+OD_NOINL void dissolve_pair(KCtx &K, u32 id) {
     u32 p = phys_of(id);
     Slot &s = K.regs[p];
     if (s.integ == IN_ENTIRE || !s.expr)
@@ -139,7 +139,7 @@ OD_INL void dissolve_pair(KCtx &K, u32 id) {
     s.integ = IN_ENTIRE;
 }
 
-OD_INL void write_slot32(KCtx &K, u32 id, u32 value, DT t) {
+OD_NOINL void write_slot32(KCtx &K, u32 id, u32 value, DT t) {
     if (id >= kNumRegIds) {
         K.oom = true;
         return;
@@ -154,7 +154,7 @@ OD_INL void write_slot32(KCtx &K, u32 id, u32 value, DT t) {
     s.integ = IN_ENTIRE;
 }
 
-OD_INL void write_pair_ids(KCtx &K, u32 lo_id, u32 value, DT t) {
+OD_NOINL void write_pair_ids(KCtx &K, u32 lo_id, u32 value, DT t) {
     if (lo_id >= kRegIdExecLo) {
         if (lo_id >= kNumRegIds) {
             K.oom = true;
@@ -190,7 +190,7 @@ OD_INL void write_pair_ids(KCtx &K, u32 lo_id, u32 value, DT t) {
 }
 
 // invalidate_slot  sym_state.cpp:169-180
-OD_INL void invalidate_slot(KCtx &K, u32 id, u32 count) {
+OD_NOINL void invalidate_slot(KCtx &K, u32 id, u32 count) {
     for (u32 i = 0; i < count; ++i) {
         if (id + i >= kNumRegIds) {
             K.oom = true; // std::array::at would throw in the reference
@@ -228,10 +228,10 @@ OD_INL u32 operand_reg_id(const Opnd &o) {
     }
 }
 
-OD_INL u32 read_pair(KCtx &K, const Opnd &o);
+OD_NOINL u32 read_pair(KCtx &K, const Opnd &o);
 
 // read_operand  sym_state.cpp:205-227
-OD_INL u32 read_operand(KCtx &K, const Opnd &o) {
+OD_NOINL u32 read_operand(KCtx &K, const Opnd &o) {
     switch (o.kind) {
     case OK_LITERAL: return K.E.constant((u64)o.value & 0xffffffffull, DT_B32);
     case OK_SREG:
@@ -336,7 +336,7 @@ struct Step {
     }
 
     // Stepper::fallback  sym_state.cpp:273-288
-    OD_INL void fallback() {
+    OD_NOINL void fallback() {
         u32 s = new_stmt(K, SK_RAW);
         K.st[s].a = I.src.off;
         K.st[s].b = I.src.len;
@@ -369,7 +369,7 @@ struct Step {
         return e;
     }
 
-    OD_INL void push_store(u32 addr, u32 value, DT et) {
+    OD_NOINL void push_store(u32 addr, u32 value, DT et) {
         u32 s = new_stmt(K, SK_STORE);
         // lower_block folds store address and value (lower.cpp:37-39)
         u32 fa = fold(K, addr);
@@ -381,7 +381,7 @@ struct Step {
     }
 
     // do_scalar_load  sym_state.cpp:348-405
-    OD_INL void scalar_load(u32 dwords) {
+    OD_NOINL void scalar_load(u32 dwords) {
         if (n() < 2 || !op_is_sreg(op(0)))
             return fallback();
         const Opnd &dst = op(0);
@@ -432,7 +432,7 @@ struct Step {
     }
 
     // do_compare  sym_state.cpp:407-460
-    OD_INL bool compare(bool vector_side) {
+    OD_NOINL bool compare(bool vector_side) {
         DT ct = suffix_type0(I, DT_I32);
         const bool uns = dt_base(ct) == B_UNSIGNED;
         u32 cop;
@@ -475,7 +475,7 @@ struct Step {
     }
 
     // handle_scalar  sym_state.cpp:462-555
-    OD_INL bool scalar() {
+    OD_NOINL bool scalar() {
         const u32 r = I.root;
         const u32 nn = n();
         if (nn > 0 && op(0).kind == OK_SPECIAL &&
@@ -560,7 +560,7 @@ struct Step {
     }
 
     // handle_vector  sym_state.cpp:577-769
-    OD_INL bool vector() {
+    OD_NOINL bool vector() {
         const u32 r = I.root;
         const u32 nn = n();
         if (r == R_MOV && nn >= 2) {
@@ -744,7 +744,7 @@ struct Step {
     }
 
     // pointer_base  sym_state.cpp:323-340 (pre-order, left first)
-    OD_INL DT pointee_of(u32 addr) {
+    OD_NOINL DT pointee_of(u32 addr) {
         U32Stack &st = K.eqst;
         u32 base = st.top;
         st.push(addr);
@@ -770,7 +770,7 @@ struct Step {
     }
 
     // do_flat_load  sym_state.cpp:771-792
-    OD_INL void flat_load(u32 dwords) {
+    OD_NOINL void flat_load(u32 dwords) {
         if (n() < 2)
             return fallback();
         const Opnd &dst = op(0);
@@ -790,7 +790,7 @@ struct Step {
     }
 
     // do_flat_store  sym_state.cpp:794-827
-    OD_INL void flat_store(u32 dwords) {
+    OD_NOINL void flat_store(u32 dwords) {
         if (n() < 2)
             return fallback();
         u32 addr = read64(op(0));
@@ -811,7 +811,7 @@ struct Step {
         }
     }
 
-    OD_INL bool flat() {
+    OD_NOINL bool flat() {
         switch (I.root) {
         case R_LOAD_DWORD: return flat_load(1), true;
         case R_LOAD_DWORDX2: return flat_load(2), true;
@@ -822,7 +822,7 @@ struct Step {
     }
 
     // step  sym_state.cpp:840-864
-    OD_INL void run() {
+    OD_NOINL void run() {
         if (I.flags & IF_PARSE_FAILED) {
             fallback();
             return;
@@ -845,7 +845,7 @@ struct Step {
 };
 
 // lower_block  lower.cpp:29-49
-OD_INL void lower_block(KCtx &K, u32 b, u32 out) {
+OD_NOINL void lower_block(KCtx &K, u32 b, u32 out) {
     const Block &B = K.blk[b];
     for (u32 i = B.ib; i < B.ie && !K.oom && !K.E.oom; ++i) {
         if (K.supp[i])
@@ -856,7 +856,7 @@ OD_INL void lower_block(KCtx &K, u32 b, u32 out) {
 }
 
 // taken_cond  lower.cpp:53-87
-OD_INL u32 taken_cond(KCtx &K, u32 cc, const Opnd &ms) {
+OD_NOINL u32 taken_cond(KCtx &K, u32 cc, const Opnd &ms) {
     switch (cc) {
     case C_SCC0:
     case C_SCC1: {
@@ -892,7 +892,7 @@ OD_INL void initial_register_state(KCtx &K) {
 }
 
 // initial_register_state  abi_model.cpp:253-281
-OD_INL void abi_entry_state(KCtx &K) {
+OD_NOINL void abi_entry_state(KCtx &K) {
     initial_register_state(K);
     u32 base = K.E.kbase();
     K.regs[4].expr = base;
@@ -913,7 +913,7 @@ OD_INL void abi_entry_state(KCtx &K) {
 
 // Collects the slots touched since log position p0 as a sorted delta on the
 // delta stack; returns (start, count).
-OD_INL void collect_delta(KCtx &K, u32 p0, u32 *start, u32 *count) {
+OD_NOINL void collect_delta(KCtx &K, u32 p0, u32 *start, u32 *count) {
     u32 bm[kLiveWords];
     for (u32 w = 0; w < kLiveWords; ++w)
         bm[w] = 0;
@@ -925,7 +925,7 @@ OD_INL void collect_delta(KCtx &K, u32 p0, u32 *start, u32 *count) {
     for (u32 w = 0; w < kLiveWords; ++w) {
         u32 m = bm[w];
         while (m) {
-            u32 bit = __builtin_ctz(m);
+            u32 bit = ctz32(m);
             m &= m - 1;
             u32 p = w * 32 + bit;
             if (K.ndstk >= K.dstk_cap) {
@@ -951,7 +951,7 @@ OD_INL u32 half_view(KCtx &K, const Slot &s) {
 
 // merge_at_join (sym_state.cpp:866-957) + emit_join (lower.cpp:89-121) for
 // the union of touched slots.  regs must hold the split state S0.
-OD_INL void merge_join(KCtx &K, const Frame &F, u32 td, u32 tn, u32 ed, u32 en, bool has_else,
+OD_NOINL void merge_join(KCtx &K, const Frame &F, u32 td, u32 tn, u32 ed, u32 en, bool has_else,
                        const u32 *live) {
     u32 i = 0, j = 0;
     while (i < tn || j < en) {
@@ -1053,7 +1053,7 @@ OD_INL u32 push_frame(KCtx &K, u32 region, u32 out) {
 }
 
 // lower_region  lower.cpp:123-172, iterative.
-OD_INL void lower_structured(KCtx &K, u32 root, u32 out) {
+OD_NOINL void lower_structured(KCtx &K, u32 root, u32 out) {
     abi_entry_state(K);
     K.nframes = 0;
     push_frame(K, root, out);
@@ -1130,7 +1130,7 @@ OD_INL void lower_structured(KCtx &K, u32 root, u32 out) {
 }
 
 // lower_goto_form  lower.cpp:187-250
-OD_INL void lower_goto(KCtx &K, u32 out) {
+OD_NOINL void lower_goto(KCtx &K, u32 out) {
     for (u32 k = 0; k < K.nblk && !K.oom && !K.E.oom; ++k) {
         u32 id = k;
         if (k > 0 && (!K.blk[id].reachable || K.blk[id].absorbed))
@@ -1184,7 +1184,7 @@ OD_INL void put_block_label(KCtx &K, Writer &w, u32 b) {
 }
 
 // emit_statement  codegen.cpp:393-442 (one statement, no If bodies)
-OD_INL void emit_simple(KCtx &K, Writer &w, const Stmt &s, u32 depth) {
+OD_NOINL void emit_simple(KCtx &K, Writer &w, const Stmt &s, u32 depth) {
     RenderCtx &rc = K.rc;
     u32 mark = K.E.top; // scratch nodes from render_indexed are discarded
     switch (s.kind) {
@@ -1258,7 +1258,7 @@ OD_INL void emit_simple(KCtx &K, Writer &w, const Stmt &s, u32 depth) {
 }
 
 // emit_body  codegen.cpp:378-381, iterative over nested If bodies.
-OD_INL void emit_list(KCtx &K, Writer &w, u32 head, u32 depth, u32 *stk, u32 stk_cap) {
+OD_NOINL void emit_list(KCtx &K, Writer &w, u32 head, u32 depth, u32 *stk, u32 stk_cap) {
     // stack entries: (stmt, depth, state) triples
     u32 sp = 0;
     stk[0] = head;
@@ -1323,7 +1323,7 @@ OD_INL void emit_list(KCtx &K, Writer &w, u32 head, u32 depth, u32 *stk, u32 stk
 // ------------------------------------------------------------ driver
 // decompile_section  decompiler.cpp:55-101 for one kernel.  Returns the
 // status; on KS_OK the OpenCL source is in w.
-OD_INL KOut decompile_kernel(const KIn &in, Bump &mem, const u8 **src) {
+OD_NOINL KOut decompile_kernel(const KIn &in, Bump &mem, const u8 **src) {
     KOut out;
     out.status = KS_OK;
     out.structured = 0;

@@ -63,7 +63,7 @@ struct Label {
 // strip_comments (asm_frontend.cpp:44-66).  Returns the cut position for
 // the simple case; *complex is set when a terminated /* */ must be removed
 // from the middle (the content is then not a single span).
-OD_INL u32 strip_scan(const u8 *p, u32 n, bool *complex) {
+OD_NOINL u32 strip_scan(const u8 *p, u32 n, bool *complex) {
     bool inq = false;
     *complex = false;
     for (u32 i = 0; i < n; ++i) {
@@ -93,7 +93,7 @@ OD_INL u32 strip_scan(const u8 *p, u32 n, bool *complex) {
 }
 
 // Materializes strip_comments(line) into out (when non-null); returns length.
-OD_INL u32 strip_materialize(const u8 *p, u32 n, u8 *out) {
+OD_NOINL u32 strip_materialize(const u8 *p, u32 n, u8 *out) {
     bool inq = false;
     u32 k = 0;
     for (u32 i = 0; i < n; ++i) {
@@ -148,7 +148,7 @@ OD_INL void split_word(const u8 *t, Span s, Span *word, Span *rest) {
 
 // Kind of a non-blank content line (split_kernels' first-word dispatch,
 // asm_frontend.cpp:235-262).
-OD_INL u8 classify_content(const u8 *t, Span c) {
+OD_NOINL u8 classify_content(const u8 *t, Span c) {
     if (c.len == 0)
         return LK_BLANK;
     Span w, rest;
@@ -184,7 +184,7 @@ OD_INL u32 root_hash_slot(const u8 *p, u32 n) {
 
 // Fills the perfect-hash table (host or device; 128 slots, collision-free
 // for the dispatch set by construction of the seed).
-OD_INL void build_root_table(RootTable *rt) {
+OD_NOINL void build_root_table(RootTable *rt) {
     const char *names[R_COUNT] = {OD_ROOT_STRINGS};
     for (u32 i = 0; i < 128; ++i)
         rt->slot[i] = 0;
@@ -240,7 +240,7 @@ struct Mnem {
 };
 
 // decompose_mnemonic  asm_frontend.cpp:375-423
-OD_INL Mnem decompose(const u8 *t, Span m, const RootTable *rt) {
+OD_NOINL Mnem decompose(const u8 *t, Span m, const RootTable *rt) {
     Mnem r;
     r.prefix = PX_OTHER;
     r.rflags = 0;
@@ -331,7 +331,7 @@ OD_INL Mnem decompose(const u8 *t, Span m, const RootTable *rt) {
 
 // ------------------------------------------------------- operand parsing
 // Result of one token: 0 ok, 1 parse error (ParseError thrown in ref).
-OD_INL int parse_register(const u8 *t, Span tok, Opnd *op, bool *is_reg) {
+OD_NOINL int parse_register(const u8 *t, Span tok, Opnd *op, bool *is_reg) {
     *is_reg = false;
     const u8 *p = t + tok.off;
     u32 n = tok.len;
@@ -383,7 +383,7 @@ OD_INL int parse_register(const u8 *t, Span tok, Opnd *op, bool *is_reg) {
 }
 
 // parse_operand  asm_frontend.cpp:188-216
-OD_INL int parse_operand(const u8 *t, Span tok, Opnd *op) {
+OD_NOINL int parse_operand(const u8 *t, Span tok, Opnd *op) {
     const u8 *p = t + tok.off;
     u32 n = tok.len;
     int sp = -1;
@@ -443,7 +443,7 @@ OD_INL int parse_operand(const u8 *t, Span tok, Opnd *op) {
 // plus parse_instruction (:439-484).  When ops/labs are null only the
 // counts are produced (sizing pass).  Returns 1 when an operand ParseError
 // demoted the instruction to parse_failed.
-OD_INL int decode_line(const u8 *t, Span content, const RootTable *rt, LineIns *out, Opnd *ops,
+OD_NOINL int decode_line(const u8 *t, Span content, const RootTable *rt, LineIns *out, Opnd *ops,
                        Label *labs) {
     u32 b = content.off, e = content.off + content.len;
     while (b < e && c_space(t[b]))

@@ -47,7 +47,7 @@ OD_INL u32 cfg_local_size(const KConfig &c, int dim) {
 }
 
 // match_group_product  builtin_detector.cpp:39-59
-OD_INL bool match_group_product(const EArena &E, u32 e, const KConfig &cfg, u32 dim) {
+OD_NOINL bool match_group_product(const EArena &E, u32 e, const KConfig &cfg, u32 dim) {
     u32 cws = cfg_local_size(cfg, (int)dim);
     if (cws == 1 && match_builtin(E, e, F_GROUP_ID, dim))
         return true;
@@ -70,7 +70,7 @@ OD_INL bool match_group_product(const EArena &E, u32 e, const KConfig &cfg, u32 
 }
 
 // fold_global_id  builtin_detector.cpp:86-124
-OD_INL u32 fold_global_id(EArena &E, u32 e, const KConfig &cfg, FoldScratch &s) {
+OD_NOINL u32 fold_global_id(EArena &E, u32 e, const KConfig &cfg, FoldScratch &s) {
     if (!e || E.n[e].kind != E_BINARY || E.n[e].op != O_ADD || dt_bits(E.n[e].type) != 32)
         return 0;
     u32 tb = s.terms.top;
@@ -108,7 +108,7 @@ OD_INL u32 fold_global_id(EArena &E, u32 e, const KConfig &cfg, FoldScratch &s) 
 }
 
 // fold_num_groups  builtin_detector.cpp:126-143
-OD_INL u32 fold_num_groups(EArena &E, u32 e, const KConfig &cfg) {
+OD_NOINL u32 fold_num_groups(EArena &E, u32 e, const KConfig &cfg) {
     if (!e || E.n[e].kind != E_BINARY)
         return 0;
     const ENode x = E.n[e];
@@ -129,7 +129,7 @@ OD_INL u32 fold_num_groups(EArena &E, u32 e, const KConfig &cfg) {
 }
 
 // fold_local_size  builtin_detector.cpp:145-169
-OD_INL u32 fold_local_size(EArena &E, u32 e, const KConfig &cfg) {
+OD_NOINL u32 fold_local_size(EArena &E, u32 e, const KConfig &cfg) {
     if (!e || E.n[e].kind != E_BINARY || E.n[e].op != O_MUL)
         return 0;
     const ENode x = E.n[e];
@@ -157,7 +157,7 @@ enum : u32 { kMemoNull = 0xffffffffu };
 
 // fold_expr  builtin_detector.cpp:171-209.  Pure in its argument, so the
 // result is memoized per node (the reference re-walks shared sub-DAGs).
-OD_INL u32 fold_expr(EArena &E, u32 root, const KConfig &cfg, FoldScratch &s) {
+OD_NOINL u32 fold_expr(EArena &E, u32 root, const KConfig &cfg, FoldScratch &s) {
     if (!root)
         return 0;
     if (E.n[root].memo)
@@ -259,7 +259,7 @@ OD_INL void render_space_prefix(Writer &w, u32 space) {
 
 // Pointer types recurse on pointee(): each level prints the space prefix,
 // then the pointee, ' ', and its own depth in stars.
-OD_INL void render_type(Writer &w, DT t) {
+OD_NOINL void render_type(Writer &w, DT t) {
     u32 d = dt_depth(t);
     if (d == 0) {
         render_scalar_type(w, t);
@@ -321,7 +321,7 @@ OD_INL void put_var_name(Writer &w, u32 cls, u32 num) {
 }
 
 // render_const  codegen.cpp:106-136
-OD_INL void render_const(Writer &w, const EArena &E, u32 e) {
+OD_NOINL void render_const(Writer &w, const EArena &E, u32 e) {
     DT t = E.n[e].type;
     u64 v = E.cval(e);
     if (dt_is_float(t) && dt_bits(t) == 32) {
@@ -510,7 +510,7 @@ OD_INL u32 unscale_term(EArena &E, u32 term, u32 size) {
 // render_indexed  codegen.cpp:202-234: returns true and pushes the tasks
 // for "name[index]" when the address splits into pointer-arg base + scaled
 // index terms.
-OD_INL bool render_indexed(Writer &w, RenderCtx &rc, u32 addr, DT elem) {
+OD_NOINL bool render_indexed(Writer &w, RenderCtx &rc, u32 addr, DT elem) {
     EArena &E = *rc.E;
     U32Stack &terms = rc.fs.terms;
     u32 tb = terms.top;
@@ -556,7 +556,7 @@ OD_INL bool render_indexed(Writer &w, RenderCtx &rc, u32 addr, DT elem) {
     return ok;
 }
 
-OD_INL void render_deref(Writer &w, RenderCtx &rc, u32 addr, DT elem) {
+OD_NOINL void render_deref(Writer &w, RenderCtx &rc, u32 addr, DT elem) {
     if (render_indexed(w, rc, addr, elem))
         return;
     w.puts("*((");
@@ -573,7 +573,7 @@ OD_INL void render_deref(Writer &w, RenderCtx &rc, u32 addr, DT elem) {
 }
 
 // render(e, min_prec)  codegen.cpp:260-352, streamed through the task stack.
-OD_INL void render_expr(Writer &w, RenderCtx &rc, u32 root, int min_prec = 0) {
+OD_NOINL void render_expr(Writer &w, RenderCtx &rc, u32 root, int min_prec = 0) {
     EArena &E = *rc.E;
     TaskStack &ts = rc.ts;
     u32 base = ts.top;

@@ -1,0 +1,165 @@
+"""GPU parity tests: the sm_100a pipeline, called through the C ABI, must
+produce byte-identical combined_source (and identical per-kernel flags) to
+the reference on the same inputs (bit-exact: the path is integer/byte work).
+
+Checked against: the reference's CLI golden pair, the committed corpus /
+nest / edge fixtures, the live oracle (oracle/_ref, the reference compiled
+from its sources) on generated corpora of every shape, and — at sizes the
+oracle cannot finish — size-independent properties (determinism, chunking
+invariance, host/device generator identity, per-kernel independence).
+"""
+import hashlib
+import json
+import os
+
+import pytest
+
+import paper_2107_07809_b200 as P
+from oracle import oracle as O
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+pytestmark = pytest.mark.gpu
+
+
+def _jsonl(name):
+    with open(os.path.join(GOLDEN, name)) as f:
+        return [json.loads(line) for line in f]
+
+
+def _flags(res):
+    return [(k.name, k.failed, k.structured, k.fallback_count) for k in res.kernels]
+
+
+def test_copy_golden():
+    listing = open(os.path.join(GOLDEN, "copy.asm"), "rb").read()
+    res = P.decompile_listing(listing)
+    assert res.combined == open(os.path.join(GOLDEN, "copy.cl"), "rb").read()
+    assert _flags(res) == [("copy", False, True, 0)]
+    assert res.kernels[0].instructions == 12
+
+
+def test_reference_corpus():
+    for rec in _jsonl("corpus.jsonl"):
+        res = P.decompile_listing(rec["listing"])
+        assert res.combined_source() == rec["combined"], rec["name"]
+        k = rec["kernels"][0]
+        assert _flags(res) == [(k["name"], k["failed"], k["structured"], k["fallbacks"])], rec["name"]
+        assert res.kernels[0].fallback_count == rec["expected_fallbacks"]
+
+
+def test_reference_corpus_as_one_listing():
+    recs = _jsonl("corpus.jsonl")
+    listing = "".join(r["listing"] for r in recs)
+    res = P.decompile_listing(listing)
+    if O.available():
+        assert res.combined == O.decompile(listing.encode()).combined
+    assert res.combined_source() == "\n".join(r["combined"] for r in recs)
+
+
+def test_nest_fixtures():
+    recs = _jsonl("nests.jsonl")
+    listing = "".join(r["listing"] for r in recs)
+    res = P.decompile_listing(listing)
+    assert res.combined_source() == "\n".join(r["combined"] for r in recs)
+    assert all(k.structured for k in res.kernels)
+
+
+@pytest.mark.skipif(not O.available(), reason="oracle not built")
+def test_1000_nests_vs_oracle():
+    listing = b"".join(O.make_nest(s) for s in range(1, 1001))
+    res = P.decompile_listing(listing)
+    ref = O.decompile(listing)
+    assert res.combined == ref.combined
+    assert [(k.failed, k.structured, k.fallback_count) for k in res.kernels] == \
+           [(k.failed, k.structured, k.fallback_count) for k in ref.kernels]
+
+
+def test_edge_cases():
+    for rec in _jsonl("edge.jsonl"):
+        res = P.decompile_listing(rec["listing"].encode("utf-8", "surrogateescape"),
+                                  P.DecompileOptions(fold_local_size=rec["fold_local_size"],
+                                                     only_kernel=rec["only_kernel"]))
+        assert res.combined_source() == rec["combined"], rec["name"]
+        want = [(k["name"], k["failed"], k["structured"], k["fallbacks"]) for k in rec["kernels"]]
+        assert _flags(res) == want, rec["name"]
+        errs = [d for d in rec["diagnostics"] if d[0] == 2 and not rec["kernels"]]
+        if errs:  # split_kernels errors: zero kernels + one error at that line
+            assert [(d.severity, d.line, d.message) for d in res.diagnostics] == [tuple(errs[0])]
+
+
+@pytest.mark.parametrize("g", json.load(open(os.path.join(GOLDEN, "gen.json"))),
+                         ids=lambda g: f"C{g['shape']}s{g['stress']}")
+def test_generated_fixture_hashes(g):
+    listing, _, ni = P.generate_corpus(g["shape"], g["count"], seed=g["seed"], stress=bool(g["stress"]))
+    assert hashlib.sha256(listing).hexdigest() == g["listing_sha256"]
+    res = P.decompile_listing(listing)
+    assert hashlib.sha256(res.combined).hexdigest() == g["combined_sha256"]
+    assert len(res.combined) == g["combined_len"]
+    assert sum(k.failed for k in res.kernels) == g["failed"]
+    assert sum(k.fallback_count for k in res.kernels) == g["fallbacks"]
+    assert sum(k.instructions for k in res.kernels) == ni
+
+
+@pytest.mark.skipif(not O.available(), reason="oracle not built")
+@pytest.mark.parametrize("shape,stress,count", [("C1", 1, 300), ("C2", 0, 200), ("C2", 1, 200),
+                                                ("C3", 0, 1000), ("C3", 1, 1000), ("C4", 0, 150),
+                                                ("C4", 1, 150)])
+def test_generated_vs_oracle(shape, stress, count):
+    listing, offs, _ = P.generate_corpus(shape, count, seed=1234 + count, stress=bool(stress))
+    res = P.decompile_listing(listing)
+    ref = O.decompile(listing)
+    assert res.combined == ref.combined
+    assert [(k.failed, k.structured, k.fallback_count) for k in res.kernels] == \
+           [(k.failed, k.structured, k.fallback_count) for k in ref.kernels]
+
+
+@pytest.mark.skipif(not O.available(), reason="oracle not built")
+def test_long_kernels_sample_vs_oracle():
+    listing, offs, ni = P.generate_corpus("C5", 3, seed=0x210707809C5, k0=1000)
+    res = P.decompile_listing(listing)
+    assert res.combined == O.decompile(listing).combined
+    assert ni > 20000
+
+
+def test_session_device_generation_matches_host():
+    s = P.Session(0)
+    try:
+        for shape in ("C2", "C3"):
+            d_buf, n, d_offs, ni = s.generate(shape, 64, seed=77)
+            host, offs, hni = P.generate_corpus(shape, 64, seed=77)
+            assert n == len(host) and ni == hni
+            s.run(d_buf, n, [0])
+            dev_out = s.output_bytes()
+            assert dev_out == P.decompile_listing(host).combined
+    finally:
+        s.close()
+
+
+def test_chunked_run_matches_single_chunk():
+    """Chunking at .kernel boundaries is invisible in the output."""
+    s = P.Session(0)
+    try:
+        d_buf, n, d_offs, ni = s.generate("C3", 200, seed=5, stress=False)
+        host, offs, _ = P.generate_corpus("C3", 200, seed=5)
+        s.run(d_buf, n, [0])
+        one = s.output_bytes()
+        s.run(d_buf, n, [int(offs[k]) for k in (0, 1, 17, 99, 150, 199)])
+        many = s.output_bytes()
+        st = s.stats()
+        assert one == many and st["kernels"] == 200
+    finally:
+        s.close()
+
+
+def test_small_arena_retry_path():
+    """Kernels that outgrow the per-thread arena are re-run with a larger one."""
+    listing, _, _ = P.generate_corpus("C4", 40, seed=3)
+    a = P.decompile_listing(listing, P.DecompileOptions(arena_bytes=64 << 10))
+    b = P.decompile_listing(listing)
+    assert a.combined == b.combined
+
+
+def test_empty_and_preamble_only():
+    assert P.decompile_listing("").kernels == []
+    r = P.decompile_listing(".amdcl2\n.gpu Fiji\n")
+    assert r.kernels == [] and r.combined == b"" and r.diagnostics == []
