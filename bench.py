@@ -28,7 +28,7 @@ sys.path.insert(0, ROOT)
 
 SEEDS = {"C1": 1, "C2": 0x210707809C2, "C3": 0x210707809C3, "C4": 0x210707809C4, "C5": 0x210707809C5}
 DEFAULT_KERNELS = {"C1": 1, "C2": 10_000, "C3": 10_000, "C4": 1_000_000, "C5": 1_000}
-CHUNK_BYTES = 1 << 30
+CHUNK_BYTES = 5 << 29  # 2.5 GiB chunks at .kernel boundaries
 METRIC = "GCN instructions decompiled/sec (device-timed) at 1/2/4/8 B200 vs host CPU"
 
 
@@ -204,8 +204,7 @@ def main():
     offs = torch.empty(nk + 1, dtype=torch.int64, device="cuda")
     host_offs = np.empty(nk + 1, dtype=np.uint64)
     # device offsets -> host (chunk boundaries at .kernel starts every ~1 GiB)
-    from torch.cuda import cudart
-    cudart().cudaMemcpy(host_offs.ctypes.data, d_offs, (nk + 1) * 8, 2)
+    P.copy(host_offs.ctypes.data, d_offs, (nk + 1) * 8)
     starts = chunk_starts_from(host_offs)
 
     def step():
@@ -254,7 +253,7 @@ def main():
     if not args.no_e2e:
         try:
             host_in = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
-            cudart().cudaMemcpy(host_in.data_ptr(), d_buf, nbytes, 2)
+            P.copy(host_in.data_ptr(), d_buf, nbytes)
             out_cap = int(out_b * 1.1) + (1 << 20)
             host_out = torch.empty(out_cap, dtype=torch.uint8, pin_memory=True)
             e_steps = max(1, min(args.steps, 3))

@@ -34,7 +34,7 @@ typedef struct ocldec_b200_options {
     int fold_local_size;     /* FoldOptions::fold_local_size (sym_state.hpp:27-29) */
     const char *only_kernel; /* restrict to one kernel by name, NULL = all        */
     int device;              /* CUDA device ordinal                               */
-    size_t arena_bytes;      /* per-thread working arena, 0 = default             */
+    size_t arena_bytes;      /* decompile arena pool per wave, 0 = default         */
 } ocldec_b200_options;
 
 /* DecompiledKernel (decompiler.hpp:39-52): the printed source and flags. */
@@ -97,6 +97,7 @@ typedef struct ocldec_b200_stats {
     uint64_t retried; /* kernels re-run with a larger arena */
     uint64_t decompile_launches, total_launches;
     double ms_parse, ms_decompile, ms_emit; /* last run, per pass (events) */
+    uint64_t prof_cycles[16]; /* OCLDEC_B200_PROF=1: SM cycles per decompile phase (cumulative) */
 } ocldec_b200_stats;
 int ocldec_b200_session_stats(ocldec_b200_session *s, ocldec_b200_stats *st);
 /* Device pointer + length of the last run's combined output. */
@@ -106,6 +107,10 @@ int ocldec_b200_session_output(ocldec_b200_session *s, const void **d_out, uint6
  * bit1 structured; fallbacks per kernel. */
 int ocldec_b200_session_kernels(ocldec_b200_session *s, uint64_t *off, uint64_t *len,
                                 uint32_t *flags, uint32_t *fallbacks);
+
+/* cudaMemcpy(dst, src, n, cudaMemcpyDefault): host<->device staging helper
+ * for callers without their own CUDA runtime binding. */
+int ocldec_b200_copy(void *dst, const void *src, uint64_t n);
 
 /* ------------------------------------------------------ synthetic corpora
  * Counter-based generator; kernel k is a pure function of

@@ -192,7 +192,9 @@ class Session:
     def stats(self) -> dict:
         st = _lib.Stats()
         self._L.ocldec_b200_session_stats(self._s, ctypes.byref(st))
-        return {n: getattr(st, n) for n, _ in _lib.Stats._fields_}
+        d = {n: getattr(st, n) for n, _ in _lib.Stats._fields_}
+        d["prof_cycles"] = list(d["prof_cycles"])
+        return d
 
     def output(self):
         p, n = ctypes.c_void_p(), ctypes.c_uint64()
@@ -211,9 +213,11 @@ class Session:
 
 
 def _cudart_memcpy(dst: int, src: int, n: int):
-    import torch
-    # cudaMemcpy through torch's CUDA runtime binding (device -> pinned host)
-    from torch.cuda import cudart
-    err = cudart().cudaMemcpy(dst, src, n, 2)  # cudaMemcpyDeviceToHost
-    if err != 0 and int(err) != 0:
-        raise RuntimeError(f"cudaMemcpy failed: {err}")
+    """cudaMemcpyDefault through the library (UVA: either direction)."""
+    rc = _lib.load().ocldec_b200_copy(dst, src, n)
+    if rc:
+        raise RuntimeError(f"copy failed: {_lib.last_error()}")
+
+
+def copy(dst: int, src: int, n: int):
+    _cudart_memcpy(dst, src, n)

@@ -37,7 +37,8 @@ class Stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in (
         "kernels", "instructions", "lines", "in_bytes", "out_bytes", "failed", "goto_form",
         "fallbacks", "retried", "decompile_launches", "total_launches")] + [
-        ("ms_parse", ctypes.c_double), ("ms_decompile", ctypes.c_double), ("ms_emit", ctypes.c_double)]
+        ("ms_parse", ctypes.c_double), ("ms_decompile", ctypes.c_double), ("ms_emit", ctypes.c_double),
+        ("prof_cycles", ctypes.c_uint64 * 16)]
 
 
 EXPORTS = [
@@ -45,7 +46,7 @@ EXPORTS = [
     "ocldec_b200_session_create", "ocldec_b200_session_destroy", "ocldec_b200_session_stream",
     "ocldec_b200_session_run", "ocldec_b200_session_stats", "ocldec_b200_session_output",
     "ocldec_b200_session_kernels", "ocldec_b200_gen_host", "ocldec_b200_gen_device",
-    "ocldec_b200_session_run_host",
+    "ocldec_b200_session_run_host", "ocldec_b200_copy",
 ]
 
 _lib = None
@@ -77,6 +78,8 @@ def load():
     L.ocldec_b200_session_run.restype = i32
     L.ocldec_b200_session_run_host.argtypes = [vp, vp, ctypes.c_size_t, i32, vp, u64, ctypes.POINTER(u64)]
     L.ocldec_b200_session_run_host.restype = i32
+    L.ocldec_b200_copy.argtypes = [vp, vp, u64]
+    L.ocldec_b200_copy.restype = i32
     L.ocldec_b200_session_stats.argtypes = [vp, ctypes.POINTER(Stats)]
     L.ocldec_b200_session_output.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(u64)]
     L.ocldec_b200_session_kernels.argtypes = [vp, vp, vp, vp, vp]

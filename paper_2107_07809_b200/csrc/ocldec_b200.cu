@@ -8,9 +8,10 @@
 //   P1c section scan           (kernel count, last directive) pair scan -> line roles
 //   P1d k_decode (x2)          thread per text line: labels, perfect-hash
 //                              mnemonic, operands (sizing pass, scan, fill pass)
-//   P2-P4a k_decompile         persistent threads, one .kernel section each:
-//                              config/ABI, CFG, exec-mask normalization, region
-//                              reduction, liveness, lowering, emission
+//   P2-P4a k_decompile         thread per .kernel section, size-sorted waves with
+//                              exact per-kernel arenas: config/ABI, CFG,
+//                              exec-mask normalization, region reduction,
+//                              liveness, lowering, emission
 //   P4b k_gather               scan of output lengths, warp-per-kernel scatter
 //                              into the combined_source buffer
 #include <cuda_runtime.h>
@@ -233,12 +234,13 @@ __global__ void k_decode(const u8 *__restrict__ t, u32 nlines, const LineRec *__
     }
     LineIns li;
     if (mode == 0) {
-        decode_line(t, Span{L.off, L.len}, &rt, &li, nullptr, nullptr);
+        decode_line(t, Span{L.off, L.len}, &rt, &li, nullptr, 0, nullptr);
         ops_cnt[l] = li.nops;
         labs_cnt[l] = li.nlabels;
     } else {
         u32 oo = ops_off[l], lo = labs_off[l];
-        decode_line(t, Span{L.off, L.len}, &rt, &li, ops + oo, labs + lo);
+        const u32 cap = (l + 1 < nlines ? ops_off[l + 1] : 0xffffffffu) - oo;
+        decode_line(t, Span{L.off, L.len}, &rt, &li, ops + oo, cap, labs + lo);
         li.op_start = oo;
         li.lab_start = lo;
         lins[l] = li;
@@ -267,81 +269,112 @@ struct DecompArgs {
     const Label *labs;
     const u32 *kstart;
     u32 nk, nlines, line_base, fold_local_size;
-    const u32 *list; // kernels to (re)run; null = all
-    u32 count;
-    u32 *next;
+    const u32 *order;   // kernels of this wave (size-sorted)
+    const u64 *boff;    // arena offsets (exclusive scan of budgets, per order slot)
+    u64 boff0;          // boff of the first slot of the wave
+    u32 count;          // kernels in the wave
+    u32 scale;
     u8 *arena;
-    u64 arena_bytes;
     u8 *stage;
     u64 stage_cap;
     unsigned long long *stage_top;
     KRes *res;
     const u8 *only;  // only_kernel name (device) or null
     u32 only_len;
+    u64 *prof;
 };
 
-__global__ void __launch_bounds__(64) k_decompile(DecompArgs a) {
-    const u64 tid = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-    u8 *arena = a.arena + tid * a.arena_bytes;
-    for (;;) {
-        u32 i = atomicAdd(a.next, 1u);
-        if (i >= a.count)
-            break;
-        u32 k = a.list ? a.list[i] : i;
-        KIn in;
-        in.t = a.t;
-        in.lines = a.lines;
-        in.lins = a.lins;
-        in.ops = a.ops;
-        in.labs = a.labs;
-        in.lbeg = a.kstart[k];
-        in.lend = k + 1 < a.nk ? a.kstart[k + 1] : a.nlines;
-        in.line_base = a.line_base;
-        in.fold_local_size = a.fold_local_size;
-        KRes r;
-        r.pad[0] = r.pad[1] = r.pad[2] = 0;
-        r.stage_off = 0;
-        r.out_len = 0;
-        r.structured = r.fallbacks = r.ninstr = 0;
-        Span nm;
-        {
-            Span w, rest, extra;
-            const LineRec &L = a.lines[in.lbeg];
-            split_word(a.t, Span{L.off, L.len}, &w, &rest);
-            split_word(a.t, rest, &nm, &extra);
-        }
-        r.name_off = nm.off;
-        r.name_len = nm.len;
-        if (a.only) {
-            if (nm.len != a.only_len || !bytes_eq(a.t + nm.off, a.only, nm.len)) {
-                r.status = KS_SKIP;
-                a.res[k] = r;
-                continue;
-            }
-        }
-        Bump mem{arena, 0, a.arena_bytes, false};
-        const u8 *src = nullptr;
-        KOut o = decompile_kernel(in, mem, &src);
-        r.status = o.status;
-        r.structured = o.structured;
-        r.fallbacks = o.fallbacks;
-        r.ninstr = o.ninstr;
-        if (o.status == KS_OK && o.out_len) {
-            u64 padded = (o.out_len + 15ull) & ~15ull;
-            u64 off = atomicAdd(a.stage_top, (unsigned long long)padded);
-            if (off + padded > a.stage_cap) {
-                r.status = KS_STAGE_FULL;
-            } else {
-                const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
-                uint4 *d4 = reinterpret_cast<uint4 *>(a.stage + off);
-                for (u64 q = 0; q < padded / 16; ++q)
-                    d4[q] = s4[q];
-                r.stage_off = off;
-                r.out_len = o.out_len;
-            }
-        }
-        a.res[k] = r;
+// Thread per kernel, kernels size-sorted (largest first) so warps are
+// uniform and the block scheduler packs big kernels first; each kernel gets
+// an exact arena slice sized by arena_budget(lines).
+__global__ void __launch_bounds__(128) k_decompile(DecompArgs a) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.count)
+        return;
+    const u32 k = a.order[i];
+    KIn in;
+    in.t = a.t;
+    in.lines = a.lines;
+    in.lins = a.lins;
+    in.ops = a.ops;
+    in.labs = a.labs;
+    in.lbeg = a.kstart[k];
+    in.lend = k + 1 < a.nk ? a.kstart[k + 1] : a.nlines;
+    in.line_base = a.line_base;
+    in.fold_local_size = a.fold_local_size;
+    in.scale = a.scale;
+    in.prof = a.prof;
+    KRes r;
+    r.pad[0] = r.pad[1] = r.pad[2] = 0;
+    r.stage_off = 0;
+    r.out_len = 0;
+    r.structured = r.fallbacks = r.ninstr = 0;
+    Span nm;
+    {
+        Span w, rest, extra;
+        const LineRec &L = a.lines[in.lbeg];
+        split_word(a.t, Span{L.off, L.len}, &w, &rest);
+        split_word(a.t, rest, &nm, &extra);
     }
+    r.name_off = nm.off;
+    r.name_len = nm.len;
+    if (a.only && (nm.len != a.only_len || !bytes_eq(a.t + nm.off, a.only, nm.len))) {
+        r.status = KS_SKIP;
+        a.res[k] = r;
+        return;
+    }
+    const u64 off = a.boff[i] - a.boff0;
+    Bump mem{a.arena + off, 0, a.boff[i + 1] - a.boff[i], false};
+    const u8 *src = nullptr;
+    KOut o = decompile_kernel(in, mem, &src);
+    r.status = o.status;
+    r.structured = o.structured;
+    r.fallbacks = o.fallbacks;
+    r.ninstr = o.ninstr;
+    if (o.status == KS_OK && o.out_len) {
+        u64 padded = (o.out_len + 15ull) & ~15ull;
+        u64 so = atomicAdd(a.stage_top, (unsigned long long)padded);
+        if (so + padded > a.stage_cap) {
+            r.status = KS_STAGE_FULL;
+        } else {
+            const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+            uint4 *d4 = reinterpret_cast<uint4 *>(a.stage + so);
+            for (u64 q = 0; q < padded / 16; ++q)
+                d4[q] = s4[q];
+            r.stage_off = so;
+            r.out_len = o.out_len;
+        }
+    }
+    a.res[k] = r;
+}
+
+// Per-kernel size key and arena budget.
+__global__ void k_ksize(const u32 *kstart, u32 nk, u32 nlines, u32 scale, u32 *key, u64 *budget) {
+    u32 k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nk)
+        return;
+    u32 n = (k + 1 < nk ? kstart[k + 1] : nlines) - kstart[k];
+    key[k] = n;
+    budget[k] = arena_budget(n, scale);
+}
+
+// Counting sort by descending size: histogram, scan, scatter.
+constexpr u32 kSizeBuckets = 1u << 16;
+__device__ __forceinline__ u32 size_bucket(u32 n) {
+    return kSizeBuckets - 1 - (n < kSizeBuckets - 1 ? n : kSizeBuckets - 1);
+}
+__global__ void k_hist(const u32 *key, u32 nk, u32 *hist) {
+    u32 k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < nk)
+        atomicAdd(&hist[size_bucket(key[k])], 1u);
+}
+__global__ void k_scatter(const u32 *key, u32 nk, u32 *cursor, u32 *order, const u64 *budget, u64 *sbudget) {
+    u32 k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nk)
+        return;
+    u32 pos = atomicAdd(&cursor[size_bucket(key[k])], 1u);
+    order[pos] = k;
+    sbudget[pos] = budget[k];
 }
 
 // ------------------------------------------------------------------ P4b
@@ -482,10 +515,11 @@ struct ocldec_b200_session {
     int nsm = 148;
     cudaStream_t stream = nullptr;
     size_t arena_bytes = 0;
-    u32 threads = 0; // persistent decompile threads
     DevBuf text, tiles, tiles_off, nlpos, lines, lins, ops_cnt, labs_cnt, ops_off, labs_off, ops,
         labs, kstart, scan_tmp, scan_tot, counters, arena, stage, res, outoff, out, only, retry,
-        gen_len, gen_ninstr, gen_buf, gen_off, kmeta;
+        gen_len, gen_ninstr, gen_buf, gen_off, kmeta, order, budget, sbudget, boff, hist, prof;
+    u64 pool_bytes = 0;  // arena pool per decompile wave
+    bool prof_on = false;
     u64 out_len = 0;
     u64 nk_total = 0;
     u32 only_len = 0;
@@ -581,6 +615,10 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     if (d2h_sync(s, &cbytes, cnt + 1, 4))
         return -3;
     if (cbytes) {
+        if (len + (u64)cbytes >= 0xffff0000ull) {
+            g_err = "chunk plus comment-stripped lines exceed 4 GiB";
+            return -1;
+        }
         if (!can_extend) {
             // copy the chunk into the session buffer (with aux room) and redo
             if (ensure(s->text, len + cbytes + 64))
@@ -642,14 +680,16 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     CK(cudaGetLastError());
     CK(cudaEventRecord(s->ev[2], st));
 
-    // P2-P4a decompile, with retries for kernels that outgrew the arena
-    if (ensure(s->res, (u64)nk * sizeof(KRes)) || ensure(s->retry, (u64)nk * 4) ||
-        ensure(s->outoff, (u64)(nk + 1) * 8))
+    // P2-P4a decompile: size-sorted waves, exact per-kernel arenas, retries
+    if (ensure(s->res, (u64)nk * sizeof(KRes)) || ensure(s->outoff, (u64)(nk + 1) * 8) ||
+        ensure(s->kmeta, (u64)nk * 4 + 16) || ensure(s->order, (u64)nk * 4 + 16) ||
+        ensure(s->budget, (u64)(nk + 1) * 8) || ensure(s->sbudget, (u64)(nk + 1) * 8) ||
+        ensure(s->boff, (u64)(nk + 2) * 8) || ensure(s->hist, (u64)kSizeBuckets * 4))
         return -3;
     u64 stage_cap = std::max<u64>(len + (64ull << 20), 2 * len);
     if (ensure(s->stage, stage_cap))
         return -3;
-    stage_cap = s->stage.cap;
+    CK(cudaMemsetAsync(cnt + 14, 0, 8, st));
     DecompArgs a;
     a.t = t;
     a.lines = P<LineRec>(s->lines);
@@ -661,33 +701,72 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     a.nlines = nlines;
     a.line_base = line_base;
     a.fold_local_size = (u32)fold_local_size;
-    a.list = nullptr;
-    a.count = nk;
-    a.next = cnt + 12;
-    a.arena = P<u8>(s->arena);
-    a.arena_bytes = s->arena_bytes;
     a.stage = P<u8>(s->stage);
-    a.stage_cap = stage_cap;
+    a.stage_cap = s->stage.cap;
     a.stage_top = reinterpret_cast<unsigned long long *>(cnt + 14);
     a.res = P<KRes>(s->res);
     a.only = s->only_set ? P<u8>(s->only) : nullptr;
     a.only_len = s->only_len;
-    CK(cudaMemsetAsync(cnt + 12, 0, 16, st));
-    {
-        u64 nthr = std::min<u64>(s->threads, ((u64)nk + 63) / 64 * 64);
-        if (ensure(s->arena, nthr * s->arena_bytes))
-            return -3;
-        a.arena = P<u8>(s->arena);
-        u32 blocks = (u32)((nthr + 63) / 64);
-        k_decompile<<<blocks, 64, 0, st>>>(a);
-        s->stats.decompile_launches++;
-        s->stats.total_launches++;
-        CK(cudaGetLastError());
-    }
-    // retry loop on the host-visible result statuses
+    a.prof = s->prof_on ? P<u64>(s->prof) : nullptr;
+    const u32 kb = 256, kg = (nk + kb - 1) / kb;
+    u32 *key = P<u32>(s->kmeta);
+    k_ksize<<<kg, kb, 0, st>>>(P<u32>(s->kstart), nk, nlines, 1, key, P<u64>(s->budget));
+    CK(cudaMemsetAsync(s->hist.p, 0, kSizeBuckets * 4ull, st));
+    k_hist<<<kg, kb, 0, st>>>(key, nk, P<u32>(s->hist));
+    if (scan_exclusive(s, kSizeBuckets, SU32{0}, AddU32{}, U32Load{P<u32>(s->hist)},
+                       U32Store{P<u32>(s->hist)}, reinterpret_cast<SU32 *>(cnt + 11)))
+        return -3;
+    k_scatter<<<kg, kb, 0, st>>>(key, nk, P<u32>(s->hist), P<u32>(s->order), P<u64>(s->budget),
+                                 P<u64>(s->sbudget));
+    CK(cudaMemsetAsync(P<u64>(s->sbudget) + nk, 0, 8, st));
+    if (scan_exclusive(s, nk + 1, U64Val{0}, AddU64{}, U64Load{P<u64>(s->sbudget)},
+                       U64Store{P<u64>(s->boff)}, reinterpret_cast<U64Val *>(P<u64>(s->budget) + nk)))
+        return -3;
+    s->stats.total_launches += 4;
+    std::vector<u64> boff(nk + 1);
+    if (d2h_sync(s, boff.data(), s->boff.p, (u64)(nk + 1) * 8))
+        return -3;
+    // waves: as many size-sorted kernels as the arena pool holds
+    auto launch_waves = [&](const u64 *h_boff, const u32 *d_order, const u64 *d_boff, u32 count,
+                            u32 scale) -> int {
+        u32 w0 = 0;
+        while (w0 < count) {
+            u64 need1 = h_boff[w0 + 1] - h_boff[w0];
+            if (ensure(s->arena, std::max<u64>(need1, std::min<u64>(s->pool_bytes, h_boff[count] - h_boff[w0]))))
+                return -3;
+            u64 cap = s->arena.cap;
+            u32 w1 = w0 + 1;
+            // largest w1 with boff[w1] - boff[w0] <= cap
+            u32 lo = w0 + 1, hi = count;
+            while (lo < hi) {
+                u32 mid = lo + (hi - lo + 1) / 2;
+                if (h_boff[mid] - h_boff[w0] <= cap)
+                    lo = mid;
+                else
+                    hi = mid - 1;
+            }
+            w1 = lo;
+            a.order = d_order + w0;
+            a.boff = d_boff + w0;
+            a.boff0 = h_boff[w0];
+            a.count = w1 - w0;
+            a.scale = scale;
+            a.arena = P<u8>(s->arena);
+            k_decompile<<<(a.count + 127) / 128, 128, 0, st>>>(a);
+            s->stats.decompile_launches++;
+            s->stats.total_launches++;
+            CK(cudaGetLastError());
+            w0 = w1;
+        }
+        return 0;
+    };
+    if (launch_waves(boff.data(), P<u32>(s->order), P<u64>(s->boff), nk, 1))
+        return -3;
+    // retries: kernels that outgrew their pools (or the staging buffer)
     std::vector<KRes> hr(nk);
-    u64 arena_b = s->arena_bytes;
-    for (int attempt = 0; attempt < 8; ++attempt) {
+    u32 scale = 1;
+    std::vector<u32> keys;
+    for (int attempt = 0; attempt < 6; ++attempt) {
         if (d2h_sync(s, hr.data(), a.res, (u64)nk * sizeof(KRes)))
             return -3;
         std::vector<u32> redo;
@@ -704,7 +783,6 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
             u64 top = 0;
             if (d2h_sync(s, &top, a.stage_top, 8))
                 return -3;
-            // keep existing staged bytes: grow into a fresh buffer
             DevBuf nb;
             u64 want = std::max<u64>(top * 2, s->stage.cap * 2);
             CK(cudaMalloc(&nb.p, want));
@@ -715,35 +793,25 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
             s->stage = nb;
             a.stage = P<u8>(s->stage);
             a.stage_cap = s->stage.cap;
-            // stage_top already beyond the old cap for failed kernels: clamp
-            u64 clamp = std::min<u64>(top, a.stage_cap);
-            CK(cudaMemcpyAsync(a.stage_top, &clamp, 8, cudaMemcpyHostToDevice, st));
         }
         bool oom = false;
         for (u32 k : redo)
             oom |= hr[k].status == KS_OOM;
         if (oom)
-            arena_b *= 4;
-        u64 threads = std::max<u64>(s->arena.cap / arena_b, 1);
-        threads = std::min<u64>(threads, redo.size());
-        if (threads * arena_b > s->arena.cap) {
-            if (arena_b > (16ull << 30)) {
-                g_err = "kernel too large for the decompile arena";
-                return -1;
-            }
-            if (ensure(s->arena, threads * arena_b))
+            scale *= 4;
+        if (keys.empty()) {
+            keys.resize(nk);
+            if (d2h_sync(s, keys.data(), key, (u64)nk * 4))
                 return -3;
-            a.arena = P<u8>(s->arena);
         }
-        CK(cudaMemcpyAsync(P<u32>(s->retry), redo.data(), redo.size() * 4, cudaMemcpyHostToDevice, st));
-        a.list = P<u32>(s->retry);
-        a.count = (u32)redo.size();
-        a.arena_bytes = arena_b;
-        CK(cudaMemsetAsync(cnt + 12, 0, 4, st));
-        k_decompile<<<(u32)((threads + 63) / 64), 64, 0, st>>>(a);
-        s->stats.decompile_launches++;
-        s->stats.total_launches++;
-        CK(cudaGetLastError());
+        std::vector<u64> rb(redo.size() + 1, 0);
+        for (size_t i = 0; i < redo.size(); ++i)
+            rb[i + 1] = rb[i] + arena_budget(keys[redo[i]], scale);
+        CK(cudaMemcpyAsync(P<u32>(s->order), redo.data(), redo.size() * 4, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(P<u64>(s->boff), rb.data(), rb.size() * 8, cudaMemcpyHostToDevice, st));
+        if (launch_waves(rb.data(), P<u32>(s->order), P<u64>(s->boff), (u32)redo.size(), scale))
+            return -3;
+        CK(cudaStreamSynchronize(st));
     }
     CK(cudaEventRecord(s->ev[3], st));
     // P4b offsets + gather
@@ -809,14 +877,17 @@ int session_init(ocldec_b200_session *s, int device, size_t arena_bytes) {
     CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
     for (auto &e : s->ev)
         CK(cudaEventCreate(&e));
-    s->arena_bytes = arena_bytes ? arena_bytes : (size_t)1 << 20;
-    // one resident wave: 4 blocks x 64 threads per SM
-    s->threads = (u32)s->nsm * 4 * 64;
+    // arena pool for one decompile wave (per-kernel slices sized by arena_budget)
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
-    size_t want = (size_t)s->threads * s->arena_bytes;
-    if (want > free_b / 3)
-        s->threads = (u32)std::max<size_t>(64, (free_b / 3) / s->arena_bytes / 64 * 64);
+    s->pool_bytes = arena_bytes ? arena_bytes : std::min<size_t>(free_b * 2 / 5, (size_t)64 << 30);
+    s->arena_bytes = s->pool_bytes;
+    const char *pe = getenv("OCLDEC_B200_PROF");
+    s->prof_on = pe && *pe && *pe != '0';
+    if (ensure(s->prof, 16 * 8))
+        return -3;
+    CK(cudaMemset(s->prof.p, 0, 16 * 8));
+    CK(cudaFuncSetAttribute(k_decompile, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
     // the stack holds the per-thread pipeline context
     CK(cudaDeviceSetLimit(cudaLimitStackSize, 16 * 1024));
     k_init_roots<<<1, 1, 0, s->stream>>>();
@@ -827,6 +898,8 @@ int session_init(ocldec_b200_session *s, int device, size_t arena_bytes) {
 
 void reset_stats(ocldec_b200_session *s) {
     s->stats = ocldec_b200_stats{};
+    if (s->prof_on && s->prof.p)
+        cudaMemsetAsync(s->prof.p, 0, 16 * 8, s->stream);
     s->host_res.clear();
     s->host_kernel_off.clear();
     s->host_name_line.clear();
@@ -882,7 +955,7 @@ size_t chunk_target() {
         if (v >= 1)
             return v;
     }
-    return (size_t)1 << 30;
+    return (size_t)5 << 29; // 2.5 GiB: chunk + aux area stay in u32 offsets
 }
 
 // decompile_listing over a host buffer: chunking at .kernel lines, H2D of
@@ -985,7 +1058,8 @@ void ocldec_b200_session_destroy(ocldec_b200_session *s) {
                       &s->labs_cnt, &s->ops_off, &s->labs_off, &s->ops, &s->labs, &s->kstart,
                       &s->scan_tmp, &s->scan_tot, &s->counters, &s->arena, &s->stage, &s->res,
                       &s->outoff, &s->out, &s->only, &s->retry, &s->gen_len, &s->gen_ninstr,
-                      &s->gen_buf, &s->gen_off, &s->kmeta};
+                      &s->gen_buf, &s->gen_off, &s->kmeta, &s->order, &s->budget, &s->sbudget,
+                      &s->boff, &s->hist, &s->prof};
     for (DevBuf *b : bufs)
         if (b->p)
             cudaFree(b->p);
@@ -1043,9 +1117,16 @@ int ocldec_b200_session_run(ocldec_b200_session *s, const void *d_listing, size_
     return 0;
 }
 
+int ocldec_b200_copy(void *dst, const void *src, uint64_t n) {
+    CK(cudaMemcpy(dst, src, n, cudaMemcpyDefault));
+    return 0;
+}
+
 int ocldec_b200_session_stats(ocldec_b200_session *s, ocldec_b200_stats *st) {
     if (!s || !st)
         return -1;
+    if (s->prof_on)
+        CK(cudaMemcpy(s->stats.prof_cycles, s->prof.p, sizeof(s->stats.prof_cycles), cudaMemcpyDeviceToHost));
     *st = s->stats;
     return 0;
 }

@@ -219,13 +219,16 @@ OD_INL bool is_cmp(u32 op) { return op >= O_CMPEQ && op <= O_CMPGEU; }
 // Scratch stack of u32 carved from the arena (explicit recursion stacks).
 struct U32Stack {
     u32 *p;
-    u32 top, cap;
+    u32 top, cap, hw;
     bool oom;
     OD_INL void push(u32 v) {
-        if (top < cap)
+        if (top < cap) {
             p[top++] = v;
-        else
+            if (top > hw)
+                hw = top;
+        } else {
             oom = true;
+        }
     }
     OD_INL u32 pop() { return p[--top]; }
     OD_INL bool empty() const { return top == 0; }

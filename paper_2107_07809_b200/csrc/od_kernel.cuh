@@ -51,6 +51,8 @@ struct KIn {
     u32 lbeg, lend;       // [.kernel line, next .kernel line) (chunk-relative)
     u32 line_base;        // global 1-based line number of chunk line 0 is line_base + 1
     u32 fold_local_size;
+    u32 scale;            // pool capacity multiplier (retries)
+    u64 *prof;            // optional per-phase cycle counters
 };
 
 struct KOut {
@@ -59,6 +61,9 @@ struct KOut {
     u32 fallbacks;
     u32 ninstr;      // parse_text instructions (synthetic s_endpgm excluded)
     u32 out_len;     // bytes of source written to the writer
+    // high-water marks (arena budgeting)
+    u32 u_fixed;     // bytes before the dynamic pools
+    u32 u_nodes, u_stmts, u_log, u_dstk, u_fresh, u_names, u_stack, u_tasks, u_regions;
 };
 
 // -------------------------------------------------------- instructions
@@ -293,7 +298,7 @@ struct KCtx {
     U32Stack eqst;
     Slot *regs;   // kPhysSlots
     UndoRec *log;
-    u32 nlog, log_cap;
+    u32 nlog, log_cap, log_hw;
     u32 log_depth; // > 0 while inside an if arm
     Pending pend;
     Stmt *st;
@@ -308,7 +313,8 @@ struct KCtx {
     u32 nframes, frames_cap;
     Slot *dstk;   // delta stack (values)
     u32 *dstk_id; // delta stack (phys ids)
-    u32 ndstk, dstk_cap;
+    u32 ndstk, dstk_cap, dstk_hw;
+    u32 stack_hw;
 
     // rendering
     RenderCtx rc;

@@ -30,6 +30,8 @@ OD_INL void log_slot(KCtx &K, u32 p) {
         return;
     }
     UndoRec &u = K.log[K.nlog++];
+    if (K.nlog > K.log_hw)
+        K.log_hw = K.nlog;
     const Slot &s = K.regs[p];
     u.phys = p;
     u.version = s.version;
@@ -936,6 +938,8 @@ OD_NOINL void collect_delta(KCtx &K, u32 p0, u32 *start, u32 *count) {
             K.dstk_id[K.ndstk] = p;
             K.dstk[K.ndstk] = K.regs[p];
             K.ndstk++;
+            if (K.ndstk > K.dstk_hw)
+                K.dstk_hw = K.ndstk;
         }
     }
     *count = K.ndstk - *start;
@@ -1320,16 +1324,89 @@ OD_NOINL void emit_list(KCtx &K, Writer &w, u32 head, u32 depth, u32 *stk, u32 s
     }
 }
 
+// ------------------------------------------------------------ budgets
+// Capacities of the dynamic pools for a kernel section of n lines, scaled by
+// s on retry.  Measured high-water marks per line on the synthetic shapes
+// (tools/devhost OD_USAGE): nodes <= 3, stmts <= 0.6, log <= 0.6,
+// deltas <= 0.3, fresh <= 0.34, output <= 30 bytes.
+struct PoolCaps {
+    u32 nodes, stmts, log, dstk, fresh, names, stack, tasks, out;
+};
+
+OD_INL PoolCaps pool_caps(u32 n, u32 s) {
+    PoolCaps c;
+    c.nodes = s * (4 * n + 1024);
+    c.stmts = s * (n + 256);
+    c.log = s * (2 * n + 1024);
+    c.dstk = s * (n + 1024);
+    c.fresh = s * (n / 2 + 256);
+    u32 want = 2 * (c.fresh + c.log / 2);
+    u32 pw = 1024;
+    while (pw < want)
+        pw <<= 1;
+    c.names = pw;
+    c.stack = s * (n + 256);
+    c.tasks = s * (n + 256);
+    u64 out = (u64)s * (48ull * n + 8192);
+    c.out = out > 0xfffff000ull ? 0xfffff000u : (u32)out;
+    return c;
+}
+
+// Upper bound of the arena decompile_kernel needs for n lines at scale s
+// (every allocation it makes, with worst-case counts: one block per
+// instruction, two regions per block, two labels per line).
+OD_INL u64 arena_budget(u32 n, u32 s) {
+    const u64 b = n + 2;          // blocks
+    const u64 r = 2 * b + 6;      // regions
+    u64 t = 0;
+    t += (n + 1) * (sizeof(KArg) + sizeof(Span));            // config
+    t += (n + 2) * sizeof(Ins) + (2 * n + 2) * 4;            // instructions, labels
+    t += (n + 9) * sizeof(AbiEntry);                         // ABI map
+    t += b * (sizeof(Block) + 4 + 8 + 1) + 16;               // blocks, stamps, work, supp
+    u64 lc = 16;
+    while (lc < 2 * (2 * (u64)n + 2))
+        lc <<= 1;
+    t += 2 * lc * 4;                                         // label map
+    t += (r + 1) * (sizeof(Region) + 6 * 4) + (4 * r + 8) * 4 + 2 * (2 * r + 4) * 4 + (b + 1) * 4;
+    t += 3 * b * kLiveWords * 4;                             // liveness
+    t += kPhysSlots * sizeof(Slot);
+    const PoolCaps c = pool_caps(n, s);
+    t += (u64)c.nodes * sizeof(ENode) + (u64)c.stmts * sizeof(Stmt) + (2 * r + 4) * sizeof(SList) +
+         (2 * r + 8) * sizeof(Frame) + (u64)c.log * sizeof(UndoRec) + (u64)c.dstk * (sizeof(Slot) + 4) +
+         (u64)c.fresh * sizeof(Fresh) + (u64)c.names * 8 + 3ull * c.stack * 4 + (u64)c.tasks * 8 +
+         3 * (r + 8) * 4 + c.out;
+    t += 64 * 16; // per-allocation alignment
+    return (t + 255) & ~255ull;
+}
+
 // ------------------------------------------------------------ driver
 // decompile_section  decompiler.cpp:55-101 for one kernel.  Returns the
 // status; on KS_OK the OpenCL source is in w.
+#ifdef __CUDA_ARCH__
+#define OD_CLK() clock64()
+#define OD_PROF(i, t0)                                                                             \
+    do {                                                                                           \
+        if (in.prof) {                                                                             \
+            long long t1_ = clock64();                                                             \
+            atomicAdd((unsigned long long *)&in.prof[i], (unsigned long long)(t1_ - t0));          \
+            t0 = t1_;                                                                              \
+        }                                                                                          \
+    } while (0)
+#else
+#define OD_CLK() 0
+#define OD_PROF(i, t0) (void)t0
+#endif
+
 OD_NOINL KOut decompile_kernel(const KIn &in, Bump &mem, const u8 **src) {
+    long long tp = OD_CLK();
     KOut out;
     out.status = KS_OK;
     out.structured = 0;
     out.fallbacks = 0;
     out.ninstr = 0;
     out.out_len = 0;
+    out.u_fixed = out.u_nodes = out.u_stmts = out.u_log = out.u_dstk = out.u_fresh = 0;
+    out.u_names = out.u_stack = out.u_tasks = out.u_regions = 0;
     KCtx K;
     memset(&K, 0, sizeof(K));
     K.in = &in;
@@ -1345,64 +1422,65 @@ OD_NOINL KOut decompile_kernel(const KIn &in, Bump &mem, const u8 **src) {
     OD_CHECK(collect_instructions(K));
     out.ninstr = K.nins_real;
     OD_CHECK(build_abi(K));
+    OD_PROF(0, tp);
     OD_CHECK(build_cfg(K));
     if (K.failed) {
         out.status = KS_FAILED;
         return out;
     }
+    OD_PROF(1, tp);
     normalize(K);
+    OD_PROF(2, tp);
     OD_CHECK(build_regions(K));
     reduce(K);
     if (K.oom) {
         out.status = KS_OOM;
         return out;
     }
+    OD_PROF(3, tp);
     out.structured = K.reduced ? 1 : 0;
     OD_CHECK(liveness(K));
+    OD_PROF(4, tp);
 
     // Carve the remaining arena into the dynamic pools.
+    out.u_fixed = (u32)mem.top;
+    out.u_regions = K.nrg;
     K.regs = mem.get<Slot>(kPhysSlots);
     OD_CHECK(K.regs);
-    u64 rem = mem.cap > mem.top ? mem.cap - mem.top : 0;
-    u64 unit = rem / 64;
-    K.E.cap = (u32)((unit * 22) / sizeof(ENode));
+    const PoolCaps pc = pool_caps(in.lend - in.lbeg, in.scale ? in.scale : 1);
+    K.E.cap = pc.nodes;
     K.E.n = mem.get<ENode>(K.E.cap);
-    K.st_cap = (u32)((unit * 5) / sizeof(Stmt));
+    K.st_cap = pc.stmts;
     K.st = mem.get<Stmt>(K.st_cap);
     K.lists_cap = 2 * K.nrg + 4;
     K.lists = mem.get<SList>(K.lists_cap);
     K.frames_cap = 2 * K.nrg + 8;
     K.frames = mem.get<Frame>(K.frames_cap);
-    K.log_cap = (u32)((unit * 5) / sizeof(UndoRec));
+    K.log_cap = pc.log;
     K.log = mem.get<UndoRec>(K.log_cap);
-    K.dstk_cap = (u32)((unit * 4) / (sizeof(Slot) + 4));
+    K.dstk_cap = pc.dstk;
     K.dstk = mem.get<Slot>(K.dstk_cap);
     K.dstk_id = mem.get<u32>(K.dstk_cap);
-    K.fresh_cap = (u32)((unit * 2) / sizeof(Fresh));
+    K.fresh_cap = pc.fresh;
     K.fresh = mem.get<Fresh>(K.fresh_cap);
-    {
-        u64 pc = 1024;
-        while (pc * 2 * 8 <= unit * 4)
-            pc *= 2;
-        K.pool.cap = (u32)pc;
-        K.pool.keys = mem.get<u64>(pc);
-        K.pool.count = 0;
-        K.pool.oom = false;
-    }
-    u32 scap = (u32)((unit * 2) / 4);
+    K.pool.cap = pc.names;
+    K.pool.keys = mem.get<u64>(pc.names);
+    K.pool.count = 0;
+    K.pool.oom = false;
+    const u32 scap = pc.stack;
     K.fs.st.p = mem.get<u32>(scap);
     K.fs.st.cap = scap;
     K.fs.terms.p = mem.get<u32>(scap);
     K.fs.terms.cap = scap;
     K.eqst.p = mem.get<u32>(scap);
     K.eqst.cap = scap;
-    u32 tcap = (u32)((unit * 2) / 8);
+    const u32 tcap = pc.tasks;
     K.rc.ts.p = mem.get<u64>(tcap);
     K.rc.ts.cap = tcap;
     u32 ecap = 3 * (K.nrg + 8);
     u32 *estk = mem.get<u32>(ecap);
     Writer w;
-    w.cap = (u32)(unit * 14 > 0xffffffffull ? 0xffffffffull : unit * 14);
+    w.cap = pc.out;
     w.p = mem.get<u8>(w.cap);
     w.n = 0;
     w.overflow = false;
@@ -1425,10 +1503,12 @@ OD_NOINL KOut decompile_kernel(const KIn &in, Bump &mem, const u8 **src) {
     K.rc.arg_sname = K.arg_sname;
     K.rc.fs = K.fs;
 
+    OD_PROF(5, tp);
     if (K.reduced)
         lower_structured(K, K.root_r, body);
     else
         lower_goto(K, body);
+    OD_PROF(6, tp);
     if (K.oom || K.E.oom || K.pool.oom || K.eqst.oom || K.fs.st.oom || K.fs.terms.oom) {
         out.status = KS_OOM;
         return out;
@@ -1482,7 +1562,23 @@ OD_NOINL KOut decompile_kernel(const KIn &in, Bump &mem, const u8 **src) {
         out.status = KS_OOM;
         return out;
     }
+    OD_PROF(7, tp);
     out.out_len = w.n;
+    out.u_nodes = K.E.top;
+    out.u_stmts = K.nst;
+    out.u_log = K.log_hw;
+    out.u_dstk = K.dstk_hw;
+    out.u_fresh = K.nfresh;
+    out.u_names = K.pool.count;
+    {
+        u32 h = K.fs.st.hw;
+        if (K.fs.terms.hw > h) h = K.fs.terms.hw;
+        if (K.eqst.hw > h) h = K.eqst.hw;
+        if (K.rc.fs.st.hw > h) h = K.rc.fs.st.hw;
+        if (K.rc.fs.terms.hw > h) h = K.rc.fs.terms.hw;
+        out.u_stack = h;
+    }
+    out.u_tasks = K.rc.ts.hw;
     return out;
 #undef OD_CHECK
 }

@@ -444,7 +444,7 @@ OD_NOINL int parse_operand(const u8 *t, Span tok, Opnd *op) {
 // counts are produced (sizing pass).  Returns 1 when an operand ParseError
 // demoted the instruction to parse_failed.
 OD_NOINL int decode_line(const u8 *t, Span content, const RootTable *rt, LineIns *out, Opnd *ops,
-                       Label *labs) {
+                         u32 ops_cap, Label *labs) {
     u32 b = content.off, e = content.off + content.len;
     while (b < e && c_space(t[b]))
         ++b;
@@ -489,7 +489,7 @@ OD_NOINL int decode_line(const u8 *t, Span content, const RootTable *rt, LineIns
 
     if (span_eq(t, word, "s_waitcnt")) {
         if (rest.len) {
-            if (ops) {
+            if (ops && ops_cap > 0) {
                 ops[0].kind = OK_ANNOT;
                 ops[0].special = 0;
                 ops[0].count = 1;
@@ -550,7 +550,7 @@ OD_NOINL int decode_line(const u8 *t, Span content, const RootTable *rt, LineIns
             }
             if (!first_tok && tmp.kind == OK_SYMBOL)
                 tmp.kind = OK_ANNOT;
-            if (ops)
+            if (ops && nops < ops_cap) // a later ParseError leaves the sized slot empty
                 ops[nops] = tmp;
             ++nops;
             first_tok = false;

@@ -444,13 +444,16 @@ OD_INL const char *rstr(u32 id) {
 
 struct TaskStack {
     u64 *p;
-    u32 top, cap;
+    u32 top, cap, hw;
     bool oom;
     OD_INL void push(u32 kind, u32 arg, u32 node) {
-        if (top < cap)
+        if (top < cap) {
             p[top++] = (u64)kind | ((u64)arg << 8) | ((u64)node << 32);
-        else
+            if (top > hw)
+                hw = top;
+        } else {
             oom = true;
+        }
     }
 };
 

@@ -108,12 +108,12 @@ int main(int argc, char **argv) {
         if (lines[l].role != LR_TEXT)
             continue;
         LineIns tmp;
-        decode_line(t.data(), Span{lines[l].off, lines[l].len}, &rt, &tmp, nullptr, nullptr);
+        decode_line(t.data(), Span{lines[l].off, lines[l].len}, &rt, &tmp, nullptr, 0, nullptr);
         u32 o0 = (u32)ops.size(), l0 = (u32)labs.size();
         ops.resize(o0 + tmp.nops + 1);
         labs.resize(l0 + tmp.nlabels + 1);
         decode_line(t.data(), Span{lines[l].off, lines[l].len}, &rt, &lins[l], ops.data() + o0,
-                    labs.data() + l0);
+                    tmp.nops, labs.data() + l0);
         lins[l].op_start = o0;
         lins[l].lab_start = l0;
         ops.resize(o0 + lins[l].nops);
@@ -131,17 +131,19 @@ int main(int argc, char **argv) {
         kin.lend = k + 1 < kstart.size() ? kstart[k + 1] : nl;
         kin.line_base = 0;
         kin.fold_local_size = argc > 1 && std::string(argv[1]) == "--fold-local-size";
-        u64 cap = 1 << 20;
+        kin.prof = nullptr;
         KOut ko;
         const u8 *src = nullptr;
         std::vector<u8> arena;
-        for (;;) {
+        for (kin.scale = 1;; kin.scale *= 4) {
+            u64 cap = arena_budget(kin.lend - kin.lbeg, kin.scale);
             arena.assign(cap, 0);
             Bump mem{arena.data(), 0, cap, false};
             ko = decompile_kernel(kin, mem, &src);
-            if (ko.status != KS_OOM || cap > (1ull << 31))
+            if (ko.status != KS_OOM || kin.scale > 1024)
                 break;
-            cap *= 4;
+            if (getenv("OD_USAGE"))
+                fprintf(stderr, "retry kernel %zu scale %u\n", k, kin.scale * 4);
         }
         Span nm;
         {
@@ -158,6 +160,10 @@ int main(int argc, char **argv) {
                std::to_string(name.size()) + " " + std::to_string(s.size()) + "\n" + name + s;
         if (ko.status == KS_OOM)
             fprintf(stderr, "kernel %zu: OOM\n", k);
+        if (getenv("OD_USAGE"))
+            fprintf(stderr, "U %u %u %u %u %u %u %u %u %u %u %u %u\n", kin.lend - kin.lbeg, ko.ninstr,
+                    ko.u_fixed, ko.u_nodes, ko.u_stmts, ko.u_log, ko.u_dstk, ko.u_fresh, ko.u_names,
+                    ko.u_stack, ko.u_tasks, ko.out_len);
         if (!s.empty()) {
             if (!combined.empty())
                 combined += "\n";
