@@ -282,13 +282,17 @@ struct DecompArgs {
     const u8 *only;  // only_kernel name (device) or null
     u32 only_len;
     u64 *prof;
+    u32 lanes_per; // lanes per kernel: 32 / kernels-per-warp
 };
 
-// Thread per kernel, kernels size-sorted (largest first) so warps are
-// uniform and the block scheduler packs big kernels first; each kernel gets
-// an exact arena slice sized by arena_budget(lines).
+// kpw kernels per warp (lane 0 of each 32/kpw-lane group works), kernels
+// size-sorted (largest first) so the block scheduler starts big kernels
+// first; each kernel gets an exact arena slice sized by arena_budget(lines).
 __global__ void __launch_bounds__(128) k_decompile(DecompArgs a) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    const u32 g = blockIdx.x * blockDim.x + threadIdx.x;
+    if ((threadIdx.x & 31) % a.lanes_per)
+        return;
+    const u32 i = g / a.lanes_per;
     if (i >= a.count)
         return;
     const u32 k = a.order[i];
@@ -520,6 +524,7 @@ struct ocldec_b200_session {
         gen_len, gen_ninstr, gen_buf, gen_off, kmeta, order, budget, sbudget, boff, hist, prof;
     u64 pool_bytes = 0;  // arena pool per decompile wave
     bool prof_on = false;
+    u32 lanes_per = 32; // 32 / kernels per warp
     u64 out_len = 0;
     u64 nk_total = 0;
     u32 only_len = 0;
@@ -752,7 +757,8 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
             a.count = w1 - w0;
             a.scale = scale;
             a.arena = P<u8>(s->arena);
-            k_decompile<<<(a.count + 127) / 128, 128, 0, st>>>(a);
+            a.lanes_per = s->lanes_per;
+            k_decompile<<<(u32)(((u64)a.count * s->lanes_per + 127) / 128), 128, 0, st>>>(a);
             s->stats.decompile_launches++;
             s->stats.total_launches++;
             CK(cudaGetLastError());
@@ -884,6 +890,11 @@ int session_init(ocldec_b200_session *s, int device, size_t arena_bytes) {
     s->arena_bytes = s->pool_bytes;
     const char *pe = getenv("OCLDEC_B200_PROF");
     s->prof_on = pe && *pe && *pe != '0';
+    const char *kp = getenv("OCLDEC_B200_KPW");
+    u32 kpw = kp && *kp ? (u32)atoi(kp) : 1;
+    if (kpw != 1 && kpw != 2 && kpw != 4 && kpw != 8 && kpw != 16 && kpw != 32)
+        kpw = 1;
+    s->lanes_per = 32 / kpw;
     if (ensure(s->prof, 16 * 8))
         return -3;
     CK(cudaMemset(s->prof.p, 0, 16 * 8));

@@ -5,6 +5,7 @@
 //
 //   g++ -O2 -std=c++17 -o build/devhost tools/devhost.cpp
 //   build/devhost < listing.s
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -139,7 +140,11 @@ int main(int argc, char **argv) {
             u64 cap = arena_budget(kin.lend - kin.lbeg, kin.scale);
             arena.assign(cap, 0);
             Bump mem{arena.data(), 0, cap, false};
+            auto t0 = std::chrono::steady_clock::now();
             ko = decompile_kernel(kin, mem, &src);
+            if (getenv("OD_TIME"))
+                fprintf(stderr, "T %zu %u %.1f\n", k, ko.ninstr,
+                        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
             if (ko.status != KS_OOM || kin.scale > 1024)
                 break;
             if (getenv("OD_USAGE"))
