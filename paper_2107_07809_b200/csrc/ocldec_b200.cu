@@ -8,7 +8,7 @@
 //   P1c section scan           (kernel count, last directive) pair scan -> line roles
 //   P1d k_decode (x2)          thread per text line: labels, perfect-hash
 //                              mnemonic, operands (sizing pass, scan, fill pass)
-//   P2-P4a k_decompile         thread per .kernel section, size-sorted waves with
+//   P2-P4a k_front/k_lower/k_emit  thread per .kernel section, size-sorted waves with
 //                              exact per-kernel arenas: config/ABI, CFG,
 //                              exec-mask normalization, region reduction,
 //                              liveness, lowering, emission
@@ -285,18 +285,44 @@ struct DecompArgs {
     u32 lanes_per; // lanes per kernel: 32 / kernels-per-warp
 };
 
-// kpw kernels per warp (lane 0 of each 32/kpw-lane group works), kernels
+// Three launches per wave, one per pipeline phase (od_lower.cuh dk_front /
+// dk_lower / dk_emit): every warp on an SM runs the same phase's code.  kpw
+// kernels per warp (lane 0 of each 32/kpw-lane group works), kernels
 // size-sorted (largest first) so the block scheduler starts big kernels
-// first; each kernel gets an exact arena slice sized by arena_budget(lines).
-__global__ void __launch_bounds__(128) k_decompile(DecompArgs a) {
+// first; each kernel gets an exact arena slice sized by kernel_budget(lines),
+// whose base holds its KState (in HBM, so its self-references stay valid
+// across the launches).
+struct Slot0 {
+    u32 k;
+    u8 *base;
+};
+__device__ __forceinline__ bool dk_slot(const DecompArgs &a, Slot0 *o) {
     const u32 g = blockIdx.x * blockDim.x + threadIdx.x;
     if ((threadIdx.x & 31) % a.lanes_per)
-        return;
+        return false;
     const u32 i = g / a.lanes_per;
     if (i >= a.count)
+        return false;
+    o->k = a.order[i];
+    o->base = a.arena + (a.boff[i] - a.boff0);
+    return true;
+}
+
+__global__ void __launch_bounds__(128) k_front(DecompArgs a) {
+    Slot0 sl;
+    if (!dk_slot(a, &sl))
         return;
-    const u32 k = a.order[i];
-    KIn in;
+    const u32 k = sl.k;
+    const u32 i = (blockIdx.x * blockDim.x + threadIdx.x) / a.lanes_per;
+    KState *g = reinterpret_cast<KState *>(sl.base);
+    const u64 kb = (sizeof(KState) + 255) & ~255ull;
+    // Field-wise setup of the state in HBM.  (nvcc 12.9 miscompiled an
+    // aggregate copy of a locally built KIn here into a copy of the first
+    // bytes of the kernel parameters.)
+    static_assert(sizeof(KState) % 8 == 0, "KState is zeroed in u64 words");
+    for (u32 q = 0; q < sizeof(KState) / 8; ++q)
+        reinterpret_cast<u64 *>(g)[q] = 0;
+    KIn &in = g->in;
     in.t = a.t;
     in.lines = a.lines;
     in.lins = a.lins;
@@ -308,11 +334,12 @@ __global__ void __launch_bounds__(128) k_decompile(DecompArgs a) {
     in.fold_local_size = a.fold_local_size;
     in.scale = a.scale;
     in.prof = a.prof;
-    KRes r;
-    r.pad[0] = r.pad[1] = r.pad[2] = 0;
-    r.stage_off = 0;
-    r.out_len = 0;
-    r.structured = r.fallbacks = r.ninstr = 0;
+    g->mem.base = sl.base + kb;
+    g->mem.top = 0;
+    g->mem.cap = a.boff[i + 1] - a.boff[i] - kb;
+    g->mem.oom = false;
+    g->out.status = KS_OK;
+    kstate_fix(*g);
     Span nm;
     {
         Span w, rest, extra;
@@ -320,21 +347,56 @@ __global__ void __launch_bounds__(128) k_decompile(DecompArgs a) {
         split_word(a.t, Span{L.off, L.len}, &w, &rest);
         split_word(a.t, rest, &nm, &extra);
     }
-    r.name_off = nm.off;
-    r.name_len = nm.len;
     if (a.only && (nm.len != a.only_len || !bytes_eq(a.t + nm.off, a.only, nm.len))) {
-        r.status = KS_SKIP;
-        a.res[k] = r;
-        return;
+        g->out.status = KS_SKIP;
+        g->done = 1;
+    } else {
+#ifdef OD_DEBUG_FRONT
+        printf("k=%u g=%p K.in=%p &g->in=%p g->in.t=%p g->in.lines=%p lbeg=%u lend=%u mem.base=%p cap=%llu\n",
+               k, g, g->K.in, &g->in, g->in.t, g->in.lines, g->in.lbeg, g->in.lend, g->mem.base,
+               (unsigned long long)g->mem.cap);
+#endif
+        dk_front(*g);
     }
-    const u64 off = a.boff[i] - a.boff0;
-    Bump mem{a.arena + off, 0, a.boff[i + 1] - a.boff[i], false};
+}
+
+__global__ void __launch_bounds__(128) k_lower(DecompArgs a) {
+    Slot0 sl;
+    if (!dk_slot(a, &sl))
+        return;
+    KState *g = reinterpret_cast<KState *>(sl.base);
+    if (!g->done)
+        dk_lower(*g);
+}
+
+__global__ void __launch_bounds__(128) k_emit(DecompArgs a) {
+    Slot0 sl;
+    if (!dk_slot(a, &sl))
+        return;
+    KState *g = reinterpret_cast<KState *>(sl.base);
+    KOut o;
     const u8 *src = nullptr;
-    KOut o = decompile_kernel(in, mem, &src);
+    if (!g->done)
+        dk_emit(*g);
+    o = g->out;
+    src = g->w.p;
+    const u32 k = sl.k;
+    KRes r;
+    r.pad[0] = r.pad[1] = r.pad[2] = 0;
+    r.stage_off = 0;
+    r.out_len = 0;
     r.status = o.status;
     r.structured = o.structured;
     r.fallbacks = o.fallbacks;
     r.ninstr = o.ninstr;
+    {
+        Span nm, w, rest, extra;
+        const LineRec &L = a.lines[a.kstart[k]];
+        split_word(a.t, Span{L.off, L.len}, &w, &rest);
+        split_word(a.t, rest, &nm, &extra);
+        r.name_off = nm.off;
+        r.name_len = nm.len;
+    }
     if (o.status == KS_OK && o.out_len) {
         u64 padded = (o.out_len + 15ull) & ~15ull;
         u64 so = atomicAdd(a.stage_top, (unsigned long long)padded);
@@ -359,7 +421,7 @@ __global__ void k_ksize(const u32 *kstart, u32 nk, u32 nlines, u32 scale, u32 *k
         return;
     u32 n = (k + 1 < nk ? kstart[k + 1] : nlines) - kstart[k];
     key[k] = n;
-    budget[k] = arena_budget(n, scale);
+    budget[k] = kernel_budget(n, scale);
 }
 
 // Counting sort by descending size: histogram, scan, scatter.
@@ -758,9 +820,12 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
             a.scale = scale;
             a.arena = P<u8>(s->arena);
             a.lanes_per = s->lanes_per;
-            k_decompile<<<(u32)(((u64)a.count * s->lanes_per + 127) / 128), 128, 0, st>>>(a);
-            s->stats.decompile_launches++;
-            s->stats.total_launches++;
+            const u32 grid = (u32)(((u64)a.count * s->lanes_per + 127) / 128);
+            k_front<<<grid, 128, 0, st>>>(a);
+            k_lower<<<grid, 128, 0, st>>>(a);
+            k_emit<<<grid, 128, 0, st>>>(a);
+            s->stats.decompile_launches += 3;
+            s->stats.total_launches += 3;
             CK(cudaGetLastError());
             w0 = w1;
         }
@@ -812,7 +877,7 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
         }
         std::vector<u64> rb(redo.size() + 1, 0);
         for (size_t i = 0; i < redo.size(); ++i)
-            rb[i + 1] = rb[i] + arena_budget(keys[redo[i]], scale);
+            rb[i + 1] = rb[i] + kernel_budget(keys[redo[i]], scale);
         CK(cudaMemcpyAsync(P<u32>(s->order), redo.data(), redo.size() * 4, cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(P<u64>(s->boff), rb.data(), rb.size() * 8, cudaMemcpyHostToDevice, st));
         if (launch_waves(rb.data(), P<u32>(s->order), P<u64>(s->boff), (u32)redo.size(), scale))
@@ -898,7 +963,9 @@ int session_init(ocldec_b200_session *s, int device, size_t arena_bytes) {
     if (ensure(s->prof, 16 * 8))
         return -3;
     CK(cudaMemset(s->prof.p, 0, 16 * 8));
-    CK(cudaFuncSetAttribute(k_decompile, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    CK(cudaFuncSetAttribute(k_front, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    CK(cudaFuncSetAttribute(k_lower, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    CK(cudaFuncSetAttribute(k_emit, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
     // the stack holds the per-thread pipeline context
     CK(cudaDeviceSetLimit(cudaLimitStackSize, 16 * 1024));
     k_init_roots<<<1, 1, 0, s->stream>>>();

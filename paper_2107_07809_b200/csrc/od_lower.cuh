@@ -1380,8 +1380,15 @@ OD_INL u64 arena_budget(u32 n, u32 s) {
 }
 
 // ------------------------------------------------------------ driver
-// decompile_section  decompiler.cpp:55-101 for one kernel.  Returns the
-// status; on KS_OK the OpenCL source is in w.
+// decompile_section (decompiler.cpp:55-101) for one kernel, split into three
+// phases so each device launch runs one phase's code (the instruction cache
+// holds one phase, not the whole pipeline):
+//   dk_front  parse_config .. liveness, pool carving
+//   dk_lower  lower_kernel + hoist_fresh_decls
+//   dk_emit   emit_kernel
+// The per-kernel state persists between launches in a KState at the base of
+// the kernel's arena slice; each phase copies it to local memory, re-points
+// the self-references (kstate_fix) and writes it back.
 #ifdef __CUDA_ARCH__
 #define OD_CLK() clock64()
 #define OD_PROF(i, t0)                                                                             \
@@ -1397,25 +1404,45 @@ OD_INL u64 arena_budget(u32 n, u32 s) {
 #define OD_PROF(i, t0) (void)t0
 #endif
 
-OD_NOINL KOut decompile_kernel(const KIn &in, Bump &mem, const u8 **src) {
-    long long tp = OD_CLK();
-    KOut out;
-    out.status = KS_OK;
-    out.structured = 0;
-    out.fallbacks = 0;
-    out.ninstr = 0;
-    out.out_len = 0;
-    out.u_fixed = out.u_nodes = out.u_stmts = out.u_log = out.u_dstk = out.u_fresh = 0;
-    out.u_names = out.u_stack = out.u_tasks = out.u_regions = 0;
+struct KState {
+    KIn in;
+    Bump mem;
     KCtx K;
-    memset(&K, 0, sizeof(K));
-    K.in = &in;
-    K.mem = &mem;
+    KOut out;
+    Writer w;
+    u32 *estk;
+    u32 ecap, body, hoist;
+    u32 done; // out.status is final
+};
+
+OD_INL void kstate_fix(KState &S) {
+    S.K.in = &S.in;
+    S.K.mem = &S.mem;
+    S.K.rc.E = &S.K.E;
+    S.K.rc.cfg = &S.K.cfg;
+}
+
+// Initializes S for one kernel; mem must be the kernel's whole arena slice.
+OD_INL void kstate_init(KState &S, const KIn &in, const Bump &mem) {
+    memset(&S, 0, sizeof(S));
+    S.in = in;
+    S.mem = mem;
+    S.out.status = KS_OK;
+    kstate_fix(S);
+}
+
+OD_NOINL void dk_front(KState &S) {
+    const KIn &in = S.in;
+    Bump &mem = S.mem;
+    KCtx &K = S.K;
+    KOut &out = S.out;
+    long long tp = OD_CLK();
 #define OD_CHECK(x)                                                                                \
     do {                                                                                           \
         if (!(x) || mem.oom) {                                                                     \
             out.status = KS_OOM;                                                                   \
-            return out;                                                                            \
+            S.done = 1;                                                                            \
+            return;                                                                                \
         }                                                                                          \
     } while (0)
     OD_CHECK(parse_config(K));
@@ -1426,7 +1453,8 @@ OD_NOINL KOut decompile_kernel(const KIn &in, Bump &mem, const u8 **src) {
     OD_CHECK(build_cfg(K));
     if (K.failed) {
         out.status = KS_FAILED;
-        return out;
+        S.done = 1;
+        return;
     }
     OD_PROF(1, tp);
     normalize(K);
@@ -1435,7 +1463,8 @@ OD_NOINL KOut decompile_kernel(const KIn &in, Bump &mem, const u8 **src) {
     reduce(K);
     if (K.oom) {
         out.status = KS_OOM;
-        return out;
+        S.done = 1;
+        return;
     }
     OD_PROF(3, tp);
     out.structured = K.reduced ? 1 : 0;
@@ -1477,16 +1506,15 @@ OD_NOINL KOut decompile_kernel(const KIn &in, Bump &mem, const u8 **src) {
     const u32 tcap = pc.tasks;
     K.rc.ts.p = mem.get<u64>(tcap);
     K.rc.ts.cap = tcap;
-    u32 ecap = 3 * (K.nrg + 8);
-    u32 *estk = mem.get<u32>(ecap);
-    Writer w;
+    S.ecap = 3 * (K.nrg + 8);
+    S.estk = mem.get<u32>(S.ecap);
+    Writer &w = S.w;
     w.cap = pc.out;
     w.p = mem.get<u8>(w.cap);
     w.n = 0;
     w.overflow = false;
-    *src = w.p;
     OD_CHECK(K.E.n && K.st && K.lists && K.frames && K.log && K.dstk && K.dstk_id && K.fresh &&
-             K.pool.keys && K.fs.st.p && K.fs.terms.p && K.eqst.p && K.rc.ts.p && estk && w.p);
+             K.pool.keys && K.fs.st.p && K.fs.terms.p && K.eqst.p && K.rc.ts.p && S.estk && w.p);
     for (u32 i = 0; i < K.pool.cap; ++i)
         K.pool.keys[i] = 0;
     memset(&K.E.n[0], 0, sizeof(ENode));
@@ -1496,22 +1524,28 @@ OD_NOINL KOut decompile_kernel(const KIn &in, Bump &mem, const u8 **src) {
     K.st[0].kind = SK_RAW;
     K.st[0].next = 0;
     K.nlists = 0;
-    u32 body = new_list(K);
-    K.rc.E = &K.E;
-    K.rc.cfg = &K.cfg;
+    S.body = new_list(K);
     K.rc.text = in.t;
     K.rc.arg_sname = K.arg_sname;
     K.rc.fs = K.fs;
-
     OD_PROF(5, tp);
+#undef OD_CHECK
+}
+
+OD_NOINL void dk_lower(KState &S) {
+    const KIn &in = S.in;
+    KCtx &K = S.K;
+    KOut &out = S.out;
+    long long tp = OD_CLK();
     if (K.reduced)
-        lower_structured(K, K.root_r, body);
+        lower_structured(K, K.root_r, S.body);
     else
-        lower_goto(K, body);
+        lower_goto(K, S.body);
     OD_PROF(6, tp);
     if (K.oom || K.E.oom || K.pool.oom || K.eqst.oom || K.fs.st.oom || K.fs.terms.oom) {
         out.status = KS_OOM;
-        return out;
+        S.done = 1;
+        return;
     }
     out.fallbacks = K.fallbacks;
 
@@ -1519,7 +1553,7 @@ OD_NOINL KOut decompile_kernel(const KIn &in, Bump &mem, const u8 **src) {
     for (u32 i = 0; i < K.pool.cap; ++i)
         K.pool.keys[i] = 0;
     K.pool.count = 0;
-    u32 hoist = new_list(K);
+    S.hoist = new_list(K);
     for (u32 i = 0; i < K.nfresh; ++i) {
         const Fresh &f = K.fresh[i];
         if (!K.pool.insert(f.cls, f.num))
@@ -1528,14 +1562,21 @@ OD_NOINL KOut decompile_kernel(const KIn &in, Bump &mem, const u8 **src) {
         K.st[d].cls = (u16)f.cls;
         K.st[d].a = f.num;
         K.st[d].c = f.type;
-        list_append(K, hoist, d);
+        list_append(K, S.hoist, d);
     }
     if (K.oom || K.pool.oom) {
         out.status = KS_OOM;
-        return out;
+        S.done = 1;
     }
+}
 
-    // emit_kernel  codegen.cpp:446-467
+// emit_kernel  codegen.cpp:446-467
+OD_NOINL void dk_emit(KState &S) {
+    const KIn &in = S.in;
+    KCtx &K = S.K;
+    KOut &out = S.out;
+    Writer &w = S.w;
+    long long tp = OD_CLK();
     K.rc.fs = K.fs;
     const u8 *t = in.t;
     w.puts("__kernel void ");
@@ -1555,12 +1596,13 @@ OD_NOINL KOut decompile_kernel(const KIn &in, Bump &mem, const u8 **src) {
         w.putn(t + a.name.off, a.name.len);
     }
     w.puts(") {\n");
-    emit_list(K, w, K.lists[hoist].head, 1, estk, ecap);
-    emit_list(K, w, K.lists[body].head, 1, estk, ecap);
+    emit_list(K, w, K.lists[S.hoist].head, 1, S.estk, S.ecap);
+    emit_list(K, w, K.lists[S.body].head, 1, S.estk, S.ecap);
     w.puts("}\n");
+    S.done = 1;
     if (K.oom || K.E.oom || K.rc.ts.oom || w.overflow || K.rc.fs.terms.oom || K.rc.fs.st.oom) {
         out.status = KS_OOM;
-        return out;
+        return;
     }
     OD_PROF(7, tp);
     out.out_len = w.n;
@@ -1579,8 +1621,32 @@ OD_NOINL KOut decompile_kernel(const KIn &in, Bump &mem, const u8 **src) {
         out.u_stack = h;
     }
     out.u_tasks = K.rc.ts.hw;
-    return out;
-#undef OD_CHECK
+}
+
+// Arena slice of a kernel of n lines at scale s on the device: the KState
+// plus everything dk_front/dk_lower/dk_emit allocate.
+OD_INL u64 kernel_budget(u32 n, u32 s) { return arena_budget(n, s) + ((sizeof(KState) + 255) & ~255ull); }
+
+// All three phases back to back (host harness and single-launch use).
+// Returns the status; on KS_OK the OpenCL source is at *src.
+OD_INL KOut decompile_kernel(const KIn &in, Bump &mem, const u8 **src) {
+    // The state moves between phases as it does between device launches,
+    // so a stale self-reference shows up here too.
+    KState A, B;
+    kstate_init(A, in, mem);
+    dk_front(A);
+    B = A;
+    memset(&A, 0xA5, sizeof(A));
+    kstate_fix(B);
+    if (!B.done)
+        dk_lower(B);
+    A = B;
+    memset(&B, 0x5A, sizeof(B));
+    kstate_fix(A);
+    if (!A.done)
+        dk_emit(A);
+    *src = A.w.p;
+    return A.out;
 }
 
 } // namespace od
