@@ -1,0 +1,122 @@
+// ocldec-b200: C++ front door with the reference's shape.
+//
+// Header-only shim over the C ABI (ocldec_b200.h) that mirrors
+//   ocldec::decompile_listing(const std::string&, const DecompileOptions&)
+//       /root/reference/proj/core/include/ocldec/decompiler.hpp:62
+// with the fields a caller of the reference consumes on this path:
+//   DecompiledKernel{name, source, structured, failed} (decompiler.hpp:39-52)
+//   LoweredBody::fallback_count                        (lower.hpp:23-41)
+//   DecompileResult::combined_source()                 (decompiler.cpp:105-115)
+//   DiagnosticSink entries for split errors            (decompiler.cpp:120-125)
+// Inspection fields (config, instructions, cfg, regions, body tree, DOT) are
+// not produced.  All work runs on the GPU; errors from the device runtime are
+// thrown as std::runtime_error (API misuse / CUDA failure only — data errors
+// come back in the result exactly as the reference reports them).
+#ifndef OCLDEC_B200_HPP
+#define OCLDEC_B200_HPP
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ocldec_b200.h"
+
+namespace ocldec_b200 {
+
+struct DecompileOptions {
+    bool fold_local_size = false; // FoldOptions::fold_local_size (sym_state.hpp:27-29)
+    std::string only_kernel;      // empty = all kernels (DecompileOptions::only_kernel)
+    int device = 0;
+};
+
+struct DecompiledKernel {
+    std::string name;
+    std::string source;
+    bool structured = false;
+    bool failed = false;
+    int fallback_count = 0;
+    unsigned instructions = 0;
+};
+
+// Diagnostic (diagnostics.hpp:20-27); render() matches diagnostics.cpp:22-26.
+struct Diagnostic {
+    enum Severity { Note = 0, Warning = 1, Error = 2 } severity = Error;
+    int line = 0;
+    std::string message;
+    std::string render(const std::string &file) const {
+        static const char *names[] = {"note", "warning", "error"};
+        return file + ":" + std::to_string(line) + ": " + names[severity] + ": " + message;
+    }
+};
+
+struct DecompileResult {
+    std::vector<DecompiledKernel> kernels;
+    std::vector<Diagnostic> diagnostics;
+    double device_ms = 0;
+    bool has_errors() const {
+        for (const auto &d : diagnostics)
+            if (d.severity == Diagnostic::Error)
+                return true;
+        return false;
+    }
+    // decompiler.cpp:105-115: non-empty sources joined by "\n".
+    std::string combined_source() const {
+        std::string out;
+        for (const auto &k : kernels) {
+            if (k.source.empty())
+                continue;
+            if (!out.empty())
+                out += "\n";
+            out += k.source;
+        }
+        return out;
+    }
+};
+
+inline const char *split_error_message(int kind) {
+    switch (kind) {
+    case 1: return ".kernel directive without a name";
+    case 2: return ".config outside of a .kernel section";
+    case 3: return ".text outside of a .kernel section";
+    default: return "parse error";
+    }
+}
+
+inline DecompileResult decompile_listing(const std::string &listing, const DecompileOptions &opts = {}) {
+    ocldec_b200_options o{};
+    o.fold_local_size = opts.fold_local_size ? 1 : 0;
+    o.only_kernel = opts.only_kernel.empty() ? nullptr : opts.only_kernel.c_str();
+    o.device = opts.device;
+    o.arena_bytes = 0;
+    ocldec_b200_result *r = nullptr;
+    int rc = ocldec_b200_decompile(listing.data(), listing.size(), &o, &r);
+    if (rc != 0)
+        throw std::runtime_error(std::string("ocldec_b200_decompile: ") + ocldec_b200_last_error());
+    DecompileResult res;
+    res.device_ms = r->device_ms;
+    for (uint64_t i = 0; i < r->nkernels; ++i) {
+        const ocldec_b200_kernel &k = r->kernels[i];
+        DecompiledKernel d;
+        d.name.assign(r->names + k.name_off, k.name_len);
+        if (k.src_len)
+            d.source.assign(r->combined + k.src_off, k.src_len);
+        d.structured = k.structured != 0;
+        d.failed = k.failed != 0;
+        d.fallback_count = k.fallback_count;
+        d.instructions = k.instructions;
+        res.kernels.push_back(std::move(d));
+    }
+    if (r->split_error_line > 0) {
+        Diagnostic dg;
+        dg.severity = Diagnostic::Error;
+        dg.line = r->split_error_line;
+        dg.message = split_error_message(r->split_error_kind);
+        res.diagnostics.push_back(dg);
+    }
+    ocldec_b200_free(r);
+    return res;
+}
+
+} // namespace ocldec_b200
+
+#endif // OCLDEC_B200_HPP

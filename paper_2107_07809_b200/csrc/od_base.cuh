@@ -315,15 +315,15 @@ struct Writer {
             overflow = true;
         ++n;
     }
-    OD_INL void puts(const char *s) {
+    OD_NOINL void puts(const char *s) {
         while (*s)
             put((u8)*s++);
     }
-    OD_INL void putn(const u8 *s, u32 len) {
+    OD_NOINL void putn(const u8 *s, u32 len) {
         for (u32 i = 0; i < len; ++i)
             put(s[i]);
     }
-    OD_INL void put_u64(u64 v) {
+    OD_NOINL void put_u64(u64 v) {
         char buf[24];
         int k = 0;
         do {
@@ -333,7 +333,7 @@ struct Writer {
         while (k)
             put((u8)buf[--k]);
     }
-    OD_INL void put_i64(i64 v) {
+    OD_NOINL void put_i64(i64 v) {
         if (v < 0) {
             put('-');
             put_u64(0ull - (u64)v);
@@ -341,7 +341,7 @@ struct Writer {
             put_u64((u64)v);
         }
     }
-    OD_INL void put_hex(u64 v) {
+    OD_NOINL void put_hex(u64 v) {
         char buf[20];
         int k = 0;
         do {
@@ -352,7 +352,7 @@ struct Writer {
         while (k)
             put((u8)buf[--k]);
     }
-    OD_INL void spaces(u32 k) {
+    OD_NOINL void spaces(u32 k) {
         for (u32 i = 0; i < k; ++i)
             put(' ');
     }

@@ -326,7 +326,7 @@ struct Step {
     OD_INL u32 read64(const Opnd &o) { return read_pair(K, o); }
     OD_INL DT ty(u32 e) const { return K.E.n[e].type; }
 
-    OD_INL void write(const Opnd &o, u32 value, DT t) {
+    OD_NOINL void write(const Opnd &o, u32 value, DT t) {
         u32 id = operand_reg_id(o);
         if (id >= kNumRegIds)
             return;
@@ -358,7 +358,7 @@ struct Step {
     }
 
     // Stepper::coerce  sym_state.cpp:300-310
-    OD_INL u32 coerce(u32 e, DT want) {
+    OD_NOINL u32 coerce(u32 e, DT want) {
         if (!e)
             return e;
         DT et = ty(e);

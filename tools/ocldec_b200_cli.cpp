@@ -1,0 +1,143 @@
+// ocldec-b200: command-line front end over the C ABI (include/ocldec_b200.hpp).
+//
+// Same flags, output file and exit codes as the reference CLI
+// (/root/reference/proj/tools/ocldec.cpp:81-177) for the options this path
+// supports:
+//   ocldec-b200 <input> [-o|--output FILE] [--kernel NAME] [--fold-local-size]
+// The output is combined_source() written atomically (temp file + rename,
+// ocldec.cpp:35-57) to FILE or <input stem>.cl (ocldec.cpp:59-66).
+// Diagnostics go to stderr as "file:line: severity: message"; exit status is 1
+// when no kernel was produced or any kernel failed, 0 otherwise.
+// --abi-map / --dump-cfg / --dump-regions are rejected (not supported).
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <iostream>
+#include <sstream>
+#include <string>
+
+#include "../include/ocldec_b200.hpp"
+
+namespace {
+
+bool read_file(const std::string &path, std::string &out, std::string &err) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) {
+        err = "cannot open '" + path + "' for reading";
+        return false;
+    }
+    std::ostringstream buf;
+    buf << in.rdbuf();
+    out = buf.str();
+    return true;
+}
+
+bool write_atomic(const std::string &path, const std::string &content, std::string &err) {
+    const std::string tmp = path + ".tmp";
+    FILE *f = std::fopen(tmp.c_str(), "wb");
+    if (!f) {
+        err = "cannot open '" + tmp + "' for writing";
+        return false;
+    }
+    bool ok = std::fwrite(content.data(), 1, content.size(), f) == content.size();
+    ok = (std::fclose(f) == 0) && ok;
+    if (!ok) {
+        err = "write to '" + tmp + "' failed";
+        std::remove(tmp.c_str());
+        return false;
+    }
+    if (std::rename(tmp.c_str(), path.c_str()) != 0) {
+        err = "cannot rename '" + tmp + "' to '" + path + "'";
+        std::remove(tmp.c_str());
+        return false;
+    }
+    return true;
+}
+
+std::string default_output(const std::string &input) {
+    std::string stem = input;
+    size_t slash = stem.find_last_of("/\\");
+    size_t dot = stem.find_last_of('.');
+    if (dot != std::string::npos && (slash == std::string::npos || dot > slash))
+        stem.resize(dot);
+    return stem + ".cl";
+}
+
+int usage(const char *argv0, int code) {
+    std::fprintf(code ? stderr : stdout,
+                 "Decompiles AMD GCN disassembly listings (CLRX syntax) to OpenCL C on the GPU\n"
+                 "Usage: %s input [-o OUTPUT] [--kernel NAME] [--fold-local-size] [--device N]\n",
+                 argv0);
+    return code;
+}
+
+} // namespace
+
+int main(int argc, char **argv) {
+    std::string input, output, only;
+    ocldec_b200::DecompileOptions opts;
+    for (int i = 1; i < argc; ++i) {
+        std::string a = argv[i];
+        if (a == "-h" || a == "--help")
+            return usage(argv[0], 0);
+        if (a == "--version") {
+            std::printf("ocldec-b200 (C ABI %d)\n", OCLDEC_B200_ABI_VERSION);
+            return 0;
+        }
+        if ((a == "-o" || a == "--output" || a == "--kernel" || a == "--device") && i + 1 < argc) {
+            std::string v = argv[++i];
+            if (a == "--kernel")
+                opts.only_kernel = v;
+            else if (a == "--device")
+                opts.device = std::atoi(v.c_str());
+            else
+                output = v;
+            continue;
+        }
+        if (a == "--fold-local-size") {
+            opts.fold_local_size = true;
+            continue;
+        }
+        if (a == "--abi-map" || a == "--dump-cfg" || a == "--dump-regions") {
+            std::cerr << "ocldec-b200: error: " << a << " is not supported by this build\n";
+            return 1;
+        }
+        if (!a.empty() && a[0] == '-')
+            return usage(argv[0], 1);
+        if (!input.empty())
+            return usage(argv[0], 1);
+        input = a;
+    }
+    if (input.empty())
+        return usage(argv[0], 1);
+
+    std::string err, listing;
+    if (!read_file(input, listing, err)) {
+        std::cerr << "ocldec-b200: error: " << err << "\n";
+        return 1;
+    }
+    ocldec_b200::DecompileResult result;
+    try {
+        result = ocldec_b200::decompile_listing(listing, opts);
+    } catch (const std::exception &e) {
+        std::cerr << "ocldec-b200: error: " << e.what() << "\n";
+        return 1;
+    }
+    for (const auto &d : result.diagnostics)
+        std::cerr << d.render(input) << "\n";
+    if (result.kernels.empty()) {
+        if (!result.has_errors())
+            std::cerr << input << ":0: error: no kernels found\n";
+        return 1;
+    }
+    bool any_failed = false;
+    for (const auto &k : result.kernels)
+        any_failed = any_failed || k.failed;
+    if (output.empty())
+        output = default_output(input);
+    if (!write_atomic(output, result.combined_source(), err)) {
+        std::cerr << "ocldec-b200: error: " << err << "\n";
+        return 1;
+    }
+    return any_failed ? 1 : 0;
+}
