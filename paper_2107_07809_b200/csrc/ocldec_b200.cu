@@ -586,7 +586,8 @@ struct ocldec_b200_session {
         gen_len, gen_ninstr, gen_buf, gen_off, kmeta, order, budget, sbudget, boff, hist, prof;
     u64 pool_bytes = 0;  // arena pool per decompile wave
     bool prof_on = false;
-    u32 lanes_per = 32; // 32 / kernels per warp
+    u32 lanes_front = 32, lanes_lower = 32, lanes_emit = 32; // 32 / kernels per warp, per phase
+    u32 smem_front = 0, smem_lower = 0, smem_emit = 0;        // occupancy limiters (dynamic smem)
     u64 out_len = 0;
     u64 nk_total = 0;
     u32 only_len = 0;
@@ -596,9 +597,35 @@ struct ocldec_b200_session {
     std::vector<KRes> host_res;      // last run, all chunks
     std::vector<u64> host_kernel_off;
     std::vector<u32> host_name_line; // chunk-relative .kernel line (host path names)
+    std::vector<cudaEvent_t> pev;    // phase-launch events (pool)
+    size_t pev_used = 0;
 };
 
 namespace {
+
+// Events bracketing each phase launch of a chunk (timed after the chunk syncs).
+int phase_event(ocldec_b200_session *s, cudaEvent_t *e) {
+    if (s->pev_used == s->pev.size()) {
+        cudaEvent_t n;
+        CK(cudaEventCreate(&n));
+        s->pev.push_back(n);
+    }
+    *e = s->pev[s->pev_used++];
+    return 0;
+}
+
+void sum_phase_events(ocldec_b200_session *s) {
+    for (size_t i = 0; i + 3 < s->pev_used; i += 4) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, s->pev[i], s->pev[i + 1]);
+        s->stats.ms_front += ms;
+        cudaEventElapsedTime(&ms, s->pev[i + 1], s->pev[i + 2]);
+        s->stats.ms_lower += ms;
+        cudaEventElapsedTime(&ms, s->pev[i + 2], s->pev[i + 3]);
+        s->stats.ms_render += ms;
+    }
+    s->pev_used = 0;
+}
 
 // Generic exclusive scan launcher.
 template <class T, class Op, class Load, class Store>
@@ -819,11 +846,21 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
             a.count = w1 - w0;
             a.scale = scale;
             a.arena = P<u8>(s->arena);
-            a.lanes_per = s->lanes_per;
-            const u32 grid = (u32)(((u64)a.count * s->lanes_per + 127) / 128);
-            k_front<<<grid, 128, 0, st>>>(a);
-            k_lower<<<grid, 128, 0, st>>>(a);
-            k_emit<<<grid, 128, 0, st>>>(a);
+            auto grid = [&](u32 lp) { return (u32)(((u64)a.count * lp + 127) / 128); };
+            cudaEvent_t pe[4];
+            for (auto &e : pe)
+                if (phase_event(s, &e))
+                    return -3;
+            CK(cudaEventRecord(pe[0], st));
+            a.lanes_per = s->lanes_front;
+            k_front<<<grid(a.lanes_per), 128, s->smem_front, st>>>(a);
+            CK(cudaEventRecord(pe[1], st));
+            a.lanes_per = s->lanes_lower;
+            k_lower<<<grid(a.lanes_per), 128, s->smem_lower, st>>>(a);
+            CK(cudaEventRecord(pe[2], st));
+            a.lanes_per = s->lanes_emit;
+            k_emit<<<grid(a.lanes_per), 128, s->smem_emit, st>>>(a);
+            CK(cudaEventRecord(pe[3], st));
             s->stats.decompile_launches += 3;
             s->stats.total_launches += 3;
             CK(cudaGetLastError());
@@ -936,6 +973,7 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     s->stats.ms_decompile += ms;
     cudaEventElapsedTime(&ms, s->ev[3], s->ev[4]);
     s->stats.ms_emit += ms;
+    sum_phase_events(s);
     return 0;
 }
 
@@ -955,11 +993,29 @@ int session_init(ocldec_b200_session *s, int device, size_t arena_bytes) {
     s->arena_bytes = s->pool_bytes;
     const char *pe = getenv("OCLDEC_B200_PROF");
     s->prof_on = pe && *pe && *pe != '0';
-    const char *kp = getenv("OCLDEC_B200_KPW");
-    u32 kpw = kp && *kp ? (u32)atoi(kp) : 1;
-    if (kpw != 1 && kpw != 2 && kpw != 4 && kpw != 8 && kpw != 16 && kpw != 32)
-        kpw = 1;
-    s->lanes_per = 32 / kpw;
+    // kernels per warp per phase (1, 2, 4, 8, 16 or 32); OCLDEC_B200_KPW sets all
+    auto kpw_env = [](const char *name, u32 dflt) {
+        const char *kp = getenv(name);
+        u32 k = kp && *kp ? (u32)atoi(kp) : dflt;
+        return (k == 1 || k == 2 || k == 4 || k == 8 || k == 16 || k == 32) ? k : dflt;
+    };
+    const u32 kall = kpw_env("OCLDEC_B200_KPW", 1);
+    s->lanes_front = 32 / kpw_env("OCLDEC_B200_KPW_FRONT", kall);
+    s->lanes_lower = 32 / kpw_env("OCLDEC_B200_KPW_LOWER", kall);
+    s->lanes_emit = 32 / kpw_env("OCLDEC_B200_KPW_EMIT", kall);
+    // OCLDEC_B200_OCC_{FRONT,LOWER,EMIT}=blocks per SM: caps occupancy with
+    // dynamic shared memory (tuning experiments; 0 = no cap)
+    auto occ_smem = [](const char *name) -> u32 {
+        const char *e = getenv(name);
+        u32 occ = e && *e ? (u32)atoi(e) : 0;
+        return occ ? (u32)((200u * 1024u) / occ) & ~1023u : 0u;
+    };
+    s->smem_front = occ_smem("OCLDEC_B200_OCC_FRONT");
+    s->smem_lower = occ_smem("OCLDEC_B200_OCC_LOWER");
+    s->smem_emit = occ_smem("OCLDEC_B200_OCC_EMIT");
+    CK(cudaFuncSetAttribute(k_front, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_lower, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     if (ensure(s->prof, 16 * 8))
         return -3;
     CK(cudaMemset(s->prof.p, 0, 16 * 8));
@@ -976,6 +1032,7 @@ int session_init(ocldec_b200_session *s, int device, size_t arena_bytes) {
 
 void reset_stats(ocldec_b200_session *s) {
     s->stats = ocldec_b200_stats{};
+    s->pev_used = 0;
     if (s->prof_on && s->prof.p)
         cudaMemsetAsync(s->prof.p, 0, 16 * 8, s->stream);
     s->host_res.clear();
@@ -1142,6 +1199,8 @@ void ocldec_b200_session_destroy(ocldec_b200_session *s) {
         if (b->p)
             cudaFree(b->p);
     for (auto &e : s->ev)
+        cudaEventDestroy(e);
+    for (auto &e : s->pev)
         cudaEventDestroy(e);
     if (s->stream)
         cudaStreamDestroy(s->stream);

@@ -19,9 +19,16 @@
 #else
 #define OD_HD
 #define OD_INL inline
+#ifdef OD_HOST_PROFILE
+#define OD_NOINL inline __attribute__((noinline))
+#else
 #define OD_NOINL inline
+#endif
 #define __host__
 #define __device__
+struct uint4 {
+    uint32_t x, y, z, w;
+};
 #endif
 
 namespace od {

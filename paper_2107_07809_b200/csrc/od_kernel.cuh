@@ -280,7 +280,7 @@ struct KCtx {
     u32 nchild, child_cap;
     u32 *live;   // live region list
     u32 nlive;
-    u32 *pred_b, *pred_n, *pred_l; // CSR preds per region
+    u32 *pred_n, *pred_x; // per region: live predecessor count and xor of their ids
     u32 *rstamp; // region stamps
     u32 rstamp_gen;
     u32 *rpo;    // rpo output
@@ -297,6 +297,7 @@ struct KCtx {
     FoldScratch fs;
     U32Stack eqst;
     Slot *regs;   // kPhysSlots
+    u32 dirty[kLiveWords]; // slots written since the last initial_register_state
     UndoRec *log;
     u32 nlog, log_cap, log_hw;
     u32 log_depth; // > 0 while inside an if arm
@@ -1205,28 +1206,28 @@ OD_INL u32 make_region(KCtx &K, u8 kind) {
     return id;
 }
 
+// Predecessors are kept as (count, xor of ids) per region: the matchers only
+// ask for the count and, when it is 1, for the single predecessor
+// (structurizer.cpp:230-352), and the xor of a one-element set is that
+// element.  Succ lists are duplicate-free, so each edge counts once.
+OD_INL void pred_add(KCtx &K, u32 t, u32 from) {
+    K.pred_n[t]++;
+    K.pred_x[t] ^= from;
+}
+OD_INL void pred_del(KCtx &K, u32 t, u32 from) {
+    K.pred_n[t]--;
+    K.pred_x[t] ^= from;
+}
+
 OD_NOINL void rebuild_region_preds(KCtx &K) {
-    for (u32 i = 0; i < K.nlive; ++i)
+    for (u32 i = 0; i < K.nlive; ++i) {
         K.pred_n[K.live[i]] = 0;
+        K.pred_x[K.live[i]] = 0;
+    }
     for (u32 i = 0; i < K.nlive; ++i) {
         const Region &R = K.rg[K.live[i]];
         for (u32 s = 0; s < R.nsucc; ++s)
-            K.pred_n[R.succ[s]]++;
-    }
-    u32 acc = 0;
-    for (u32 i = 0; i < K.nlive; ++i) {
-        u32 r = K.live[i];
-        K.pred_b[r] = acc;
-        acc += K.pred_n[r];
-        K.pred_n[r] = 0;
-    }
-    for (u32 i = 0; i < K.nlive; ++i) {
-        u32 r = K.live[i];
-        const Region &R = K.rg[r];
-        for (u32 s = 0; s < R.nsucc; ++s) {
-            u32 t = (u32)R.succ[s];
-            K.pred_l[K.pred_b[t] + K.pred_n[t]++] = r;
-        }
+            pred_add(K, (u32)R.succ[s], K.live[i]);
     }
 }
 
@@ -1246,14 +1247,13 @@ OD_NOINL bool build_regions(KCtx &K) {
     K.child_cap = 4 * cap + 8;
     K.child = K.mem->get<u32>(K.child_cap);
     K.live = K.mem->get<u32>(cap + 1);
-    K.pred_b = K.mem->get<u32>(cap + 1);
     K.pred_n = K.mem->get<u32>(cap + 1);
-    K.pred_l = K.mem->get<u32>(2 * cap + 4);
+    K.pred_x = K.mem->get<u32>(cap + 1);
     K.rstamp = K.mem->get<u32>(cap + 1);
     K.rpo = K.mem->get<u32>(cap + 1);
     K.dfs = K.mem->get<u32>(2 * cap + 4);
     u32 *by_block = K.mem->get<u32>(K.nblk + 1);
-    if (!K.rg || !K.child || !K.live || !K.pred_b || !K.pred_n || !K.pred_l || !K.rstamp ||
+    if (!K.rg || !K.child || !K.live || !K.pred_n || !K.pred_x || !K.rstamp ||
         !K.rpo || !K.dfs || !by_block)
         return false;
     for (u32 i = 0; i <= cap; ++i)
@@ -1292,7 +1292,7 @@ OD_NOINL bool build_regions(KCtx &K) {
 }
 
 OD_INL bool single_pred_is(const KCtx &K, u32 node, u32 pred) {
-    return K.pred_n[node] == 1 && K.pred_l[K.pred_b[node]] == pred;
+    return K.pred_n[node] == 1 && K.pred_x[node] == pred;
 }
 
 // RegionGraph::replace  structurizer.cpp:141-185
@@ -1302,9 +1302,12 @@ OD_NOINL void region_replace(KCtx &K, const u32 *old, u32 nold, u32 merged) {
         K.rstamp[old[i]] = gen;
     Region &M = K.rg[merged];
     M.nsucc = 0;
+    K.pred_n[merged] = 0;
+    K.pred_x[merged] = 0;
     for (u32 i = 0; i < nold; ++i) {
         const Region &O = K.rg[old[i]];
         for (u32 s = 0; s < O.nsucc; ++s) {
+            pred_del(K, (u32)O.succ[s], old[i]);
             u32 t = (u32)O.succ[s] == old[0] ? merged : (u32)O.succ[s];
             if (t != merged && K.rstamp[t] == gen)
                 continue;
@@ -1316,6 +1319,8 @@ OD_NOINL void region_replace(KCtx &K, const u32 *old, u32 nold, u32 merged) {
                 M.succ[M.nsucc++] = (i32)t;
         }
     }
+    for (u32 k = 0; k < M.nsucc; ++k)
+        pred_add(K, (u32)M.succ[k], merged);
     u32 w = 0;
     for (u32 i = 0; i < K.nlive; ++i)
         if (K.rstamp[K.live[i]] != gen)
@@ -1323,7 +1328,13 @@ OD_NOINL void region_replace(KCtx &K, const u32 *old, u32 nold, u32 merged) {
     K.live[w++] = merged;
     K.nlive = w;
     for (u32 i = 0; i + 1 < K.nlive; ++i) {
-        Region &R = K.rg[K.live[i]];
+        const u32 u = K.live[i];
+        Region &R = K.rg[u];
+        bool hit = false;
+        for (u32 s = 0; s < R.nsucc; ++s)
+            hit |= K.rstamp[R.succ[s]] == gen;
+        if (!hit)
+            continue;
         i32 out[2];
         u32 no = 0;
         for (u32 s = 0; s < R.nsucc; ++s) {
@@ -1335,11 +1346,15 @@ OD_NOINL void region_replace(KCtx &K, const u32 *old, u32 nold, u32 merged) {
             if (!dup)
                 out[no++] = (i32)t;
         }
+        // edges into the old regions die with them; u gains one edge into M
+        for (u32 s = 0; s < R.nsucc; ++s)
+            if (K.rstamp[R.succ[s]] == gen)
+                pred_del(K, (u32)R.succ[s], u);
+        pred_add(K, merged, u);
         R.nsucc = no;
         for (u32 k = 0; k < no; ++k)
             R.succ[k] = out[k];
     }
-    rebuild_region_preds(K);
     if (K.entry_r >= 0 && K.rstamp[K.entry_r] == gen)
         K.entry_r = (i32)merged;
 }
@@ -1558,38 +1573,63 @@ OD_NOINL void reduce(KCtx &K) {
 }
 
 // ========================================================== liveness
-OD_INL void lv_mark(u32 *set, u32 id) {
-    if (id < kNumRegIds)
-        set[id >> 5] |= 1u << (id & 31);
+// Per-block gen/kill accumulation (cfg.cpp:360-372): a use counts unless an
+// earlier instruction of the block defined the register; an instruction's
+// own defs are buffered and committed after it (use before def).
+struct LvSink {
+    u32 *U, *D;
+    u32 dd[kLiveWords];
+    u32 touched;
+};
+
+OD_INL void lv_mark(LvSink &S, u32 id, bool is_def) {
+    if (id >= kNumRegIds)
+        return;
+    const u32 w = id >> 5, bit = 1u << (id & 31);
+    if (is_def) {
+        S.dd[w] |= bit;
+        S.touched |= 1u << w;
+    } else if (!(S.D[w] & bit)) {
+        S.U[w] |= bit;
+    }
+}
+
+OD_INL void lv_commit(LvSink &S) {
+    while (S.touched) {
+        const u32 w = ctz32(S.touched);
+        S.touched &= S.touched - 1;
+        S.D[w] |= S.dd[w];
+        S.dd[w] = 0;
+    }
 }
 
 // add_operand_regs  cfg.cpp:230-265
-OD_INL void add_operand_regs(const Opnd &op, u32 *set) {
+OD_INL void add_operand_regs(const Opnd &op, LvSink &set, bool is_def) {
     switch (op.kind) {
     case OK_SREG:
         for (u32 i = 0; i < op.count && op.r.a + i < kNumRegIds; ++i)
-            lv_mark(set, op.r.a + i);
+            lv_mark(set, op.r.a + i, is_def);
         break;
     case OK_VREG:
         for (u32 i = 0; i < op.count && kRegIdVgpr0 + op.r.a + i < kNumRegIds; ++i)
-            lv_mark(set, kRegIdVgpr0 + op.r.a + i);
+            lv_mark(set, kRegIdVgpr0 + op.r.a + i, is_def);
         break;
     case OK_SPECIAL:
         switch (op.special) {
         case SP_EXEC:
-            lv_mark(set, kRegIdExecLo);
-            lv_mark(set, kRegIdExecHi);
+            lv_mark(set, kRegIdExecLo, is_def);
+            lv_mark(set, kRegIdExecHi, is_def);
             break;
-        case SP_EXEC_LO: lv_mark(set, kRegIdExecLo); break;
-        case SP_EXEC_HI: lv_mark(set, kRegIdExecHi); break;
+        case SP_EXEC_LO: lv_mark(set, kRegIdExecLo, is_def); break;
+        case SP_EXEC_HI: lv_mark(set, kRegIdExecHi, is_def); break;
         case SP_VCC:
-            lv_mark(set, kRegIdVccLo);
-            lv_mark(set, kRegIdVccHi);
+            lv_mark(set, kRegIdVccLo, is_def);
+            lv_mark(set, kRegIdVccHi, is_def);
             break;
-        case SP_VCC_LO: lv_mark(set, kRegIdVccLo); break;
-        case SP_VCC_HI: lv_mark(set, kRegIdVccHi); break;
-        case SP_SCC: lv_mark(set, kRegIdScc); break;
-        case SP_M0: lv_mark(set, kRegIdM0); break;
+        case SP_VCC_LO: lv_mark(set, kRegIdVccLo, is_def); break;
+        case SP_VCC_HI: lv_mark(set, kRegIdVccHi, is_def); break;
+        case SP_SCC: lv_mark(set, kRegIdScc, is_def); break;
+        case SP_M0: lv_mark(set, kRegIdM0, is_def); break;
         }
         break;
     default:
@@ -1598,12 +1638,12 @@ OD_INL void add_operand_regs(const Opnd &op, u32 *set) {
 }
 
 // instruction_use_def  cfg.cpp:272-352
-OD_NOINL void instruction_use_def(const KCtx &K, const Ins &I, u32 *use, u32 *def) {
+OD_NOINL void instruction_use_def(const KCtx &K, const Ins &I, LvSink &S) {
     const Opnd *o = K.in->ops + I.op_start;
     const u32 n = (I.flags & IF_SYNTH) ? 0 : I.nops;
     if (I.flags & IF_PARSE_FAILED) {
         for (u32 k = 0; k < n; ++k)
-            add_operand_regs(o[k], use);
+            add_operand_regs(o[k], S, false);
         return;
     }
     const u32 root = I.root;
@@ -1614,35 +1654,35 @@ OD_NOINL void instruction_use_def(const KCtx &K, const Ins &I, u32 *use, u32 *de
         return;
     if (px == PX_S && (I.rflags & RF_CBRANCH)) {
         if (root == R_CBRANCH_SCC0 || root == R_CBRANCH_SCC1) {
-            lv_mark(use, kRegIdScc);
+            lv_mark(S, kRegIdScc, false);
         } else if (root == R_CBRANCH_VCCZ || root == R_CBRANCH_VCCNZ) {
-            lv_mark(use, kRegIdVccLo);
-            lv_mark(use, kRegIdVccHi);
+            lv_mark(S, kRegIdVccLo, false);
+            lv_mark(S, kRegIdVccHi, false);
         } else {
-            lv_mark(use, kRegIdExecLo);
-            lv_mark(use, kRegIdExecHi);
+            lv_mark(S, kRegIdExecLo, false);
+            lv_mark(S, kRegIdExecHi, false);
         }
         return;
     }
     if (px == PX_FLAT && (I.rflags & RF_STORE)) {
         for (u32 k = 0; k < n; ++k)
-            add_operand_regs(o[k], use);
+            add_operand_regs(o[k], S, false);
         return;
     }
     if (px == PX_S && (I.rflags & RF_CMP)) {
         for (u32 k = 0; k < n; ++k)
-            add_operand_regs(o[k], use);
-        lv_mark(def, kRegIdScc);
+            add_operand_regs(o[k], S, false);
+        lv_mark(S, kRegIdScc, true);
         return;
     }
     if (px == PX_S && root == R_AND_SAVEEXEC && n > 0) {
-        add_operand_regs(o[0], def);
+        add_operand_regs(o[0], S, true);
         for (u32 k = 1; k < n; ++k)
-            add_operand_regs(o[k], use);
-        lv_mark(use, kRegIdExecLo);
-        lv_mark(use, kRegIdExecHi);
-        lv_mark(def, kRegIdExecLo);
-        lv_mark(def, kRegIdExecHi);
+            add_operand_regs(o[k], S, false);
+        lv_mark(S, kRegIdExecLo, false);
+        lv_mark(S, kRegIdExecHi, false);
+        lv_mark(S, kRegIdExecLo, true);
+        lv_mark(S, kRegIdExecHi, true);
         return;
     }
     u32 ndefs = 1;
@@ -1652,18 +1692,18 @@ OD_NOINL void instruction_use_def(const KCtx &K, const Ins &I, u32 *use, u32 *de
     const bool reads_dst = (px == PX_S && (root == R_ADDK || root == R_MULK)) || (px == PX_V && root == R_MAC);
     for (u32 k = 0; k < n; ++k) {
         if (k < ndefs) {
-            add_operand_regs(o[k], def);
+            add_operand_regs(o[k], S, true);
             if (reads_dst && k == 0)
-                add_operand_regs(o[k], use);
+                add_operand_regs(o[k], S, false);
         } else {
-            add_operand_regs(o[k], use);
+            add_operand_regs(o[k], S, false);
         }
     }
     if (px == PX_S && n >= 1 &&
         (root == R_ADD || root == R_SUB || root == R_ADDK || root == R_MULK || root == R_AND ||
          root == R_OR || root == R_XOR || root == R_ANDN2 || root == R_LSHL || root == R_LSHR ||
          root == R_ASHR))
-        lv_mark(def, kRegIdScc);
+        lv_mark(S, kRegIdScc, true);
 }
 
 // live_in_sets  cfg.cpp:356-398 (word-parallel; the least fixpoint is
@@ -1675,6 +1715,13 @@ OD_NOINL bool liveness(KCtx &K) {
     K.live_in = K.mem->get<u32>((u64)nb * kLiveWords);
     if (!use || !def || !K.live_in)
         return false;
+    u32 any[kLiveWords]; // union of the use sets
+    for (u32 w = 0; w < kLiveWords; ++w)
+        any[w] = 0;
+    LvSink S;
+    for (u32 w = 0; w < kLiveWords; ++w)
+        S.dd[w] = 0;
+    S.touched = 0;
     for (u32 b = 0; b < nb; ++b) {
         u32 *U = use + b * kLiveWords, *D = def + b * kLiveWords;
         for (u32 w = 0; w < kLiveWords; ++w) {
@@ -1682,27 +1729,33 @@ OD_NOINL bool liveness(KCtx &K) {
             D[w] = 0;
             K.live_in[b * kLiveWords + w] = 0;
         }
+        S.U = U;
+        S.D = D;
         const Block &B = K.blk[b];
         for (u32 i = B.ib; i < B.ie; ++i) {
             if (K.supp[i])
                 continue;
-            u32 iu[kLiveWords], id[kLiveWords];
-            for (u32 w = 0; w < kLiveWords; ++w)
-                iu[w] = id[w] = 0;
-            instruction_use_def(K, K.ins[i], iu, id);
-            for (u32 w = 0; w < kLiveWords; ++w) {
-                U[w] |= iu[w] & ~D[w];
-                D[w] |= id[w];
-            }
+            instruction_use_def(K, K.ins[i], S);
+            lv_commit(S);
         }
+        for (u32 w = 0; w < kLiveWords; ++w)
+            any[w] |= U[w];
     }
-    bool changed = true;
+    // Only words holding some use bit can ever become live (live_in is a
+    // subset of the union of the use sets), so the fixpoint runs over those.
+    u32 wl[kLiveWords];
+    u32 nw = 0;
+    for (u32 w = 0; w < kLiveWords; ++w)
+        if (any[w])
+            wl[nw++] = w;
+    bool changed = nw > 0;
     while (changed) {
         changed = false;
         for (u32 bi = nb; bi-- > 0;) {
             const Block &B = K.blk[bi];
             u32 *L = K.live_in + bi * kLiveWords;
-            for (u32 w = 0; w < kLiveWords; ++w) {
+            for (u32 k = 0; k < nw; ++k) {
+                const u32 w = wl[k];
                 u32 out = 0;
                 for (u32 s = 0; s < B.nsucc; ++s)
                     out |= K.live_in[(u32)B.succ[s] * kLiveWords + w];

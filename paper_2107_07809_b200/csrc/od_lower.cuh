@@ -23,6 +23,7 @@ OD_INL u32 dense_of_phys(u32 p) {
 }
 
 OD_INL void log_slot(KCtx &K, u32 p) {
+    K.dirty[p >> 5] |= 1u << (p & 31);
     if (!K.log_depth)
         return;
     if (K.nlog >= K.log_cap) {
@@ -313,6 +314,15 @@ OD_INL void list_append(KCtx &K, u32 l, u32 s) {
 }
 
 OD_INL u32 fold(KCtx &K, u32 e) { return fold_expr(K.E, e, K.cfg, K.fs); }
+
+// Clears a name set (16-byte stores; cap is a power of two >= 1024).
+OD_INL void name_set_clear(NameSet &ns) {
+    uint4 z = {0, 0, 0, 0};
+    uint4 *p = reinterpret_cast<uint4 *>(ns.keys);
+    for (u32 i = 0; i < ns.cap / 2; ++i)
+        p[i] = z;
+    ns.count = 0;
+}
 
 // ------------------------------------------------------------ stepper
 struct Step {
@@ -880,18 +890,40 @@ OD_NOINL u32 taken_cond(KCtx &K, u32 cc, const Opnd &ms) {
     }
 }
 
+OD_INL void reset_slot(Slot &s) {
+    s.version = 0;
+    s.expr = 0;
+    s.type = DT_UNKNOWN;
+    s.integ = IN_ENTIRE;
+}
+
+// Every slot to the RegisterFile default (once per kernel, at pool carving).
+OD_INL void full_register_init(KCtx &K) {
+    for (u32 p = 0; p < kPhysSlots; ++p)
+        reset_slot(K.regs[p]);
+    for (u32 w = 0; w < kLiveWords; ++w)
+        K.dirty[w] = 0;
+}
+
+// A default RegisterFile: only the slots written since the last reset (every
+// write goes through log_slot, which marks them) are cleared — lower_goto
+// restarts from this state at every block (lower.cpp:204-206).
 OD_INL void initial_register_state(KCtx &K) {
-    for (u32 p = 0; p < kPhysSlots; ++p) {
-        Slot &s = K.regs[p];
-        s.version = 0;
-        s.expr = 0;
-        s.type = DT_UNKNOWN;
-        s.integ = IN_ENTIRE;
+    for (u32 w = 0; w < kLiveWords; ++w) {
+        u32 m = K.dirty[w];
+        K.dirty[w] = 0;
+        while (m) {
+            u32 b = ctz32(m);
+            m &= m - 1;
+            reset_slot(K.regs[w * 32 + b]);
+        }
     }
     K.pend.valid = 0;
     K.pend.base64 = K.pend.addend = 0;
     K.pend.lo_vgpr = K.pend.lo_version = 0;
 }
+
+OD_INL void mark_dirty(KCtx &K, u32 p) { K.dirty[p >> 5] |= 1u << (p & 31); }
 
 // initial_register_state  abi_model.cpp:253-281
 OD_NOINL void abi_entry_state(KCtx &K) {
@@ -911,6 +943,13 @@ OD_NOINL void abi_entry_state(KCtx &K) {
     }
     K.regs[360].expr = K.E.constant(~0ull, DT_B64);
     K.regs[360].type = DT_B64;
+    mark_dirty(K, 4);
+    mark_dirty(K, 5);
+    mark_dirty(K, 360);
+    for (u32 d = 0; d < K.cfg.dims; ++d) {
+        mark_dirty(K, kRegIdVgpr0 + d);
+        mark_dirty(K, 6 + d);
+    }
 }
 
 // Collects the slots touched since log position p0 as a sorted delta on the
@@ -1476,6 +1515,7 @@ OD_NOINL void dk_front(KState &S) {
     out.u_regions = K.nrg;
     K.regs = mem.get<Slot>(kPhysSlots);
     OD_CHECK(K.regs);
+    full_register_init(K);
     const PoolCaps pc = pool_caps(in.lend - in.lbeg, in.scale ? in.scale : 1);
     K.E.cap = pc.nodes;
     K.E.n = mem.get<ENode>(K.E.cap);
@@ -1515,8 +1555,7 @@ OD_NOINL void dk_front(KState &S) {
     w.overflow = false;
     OD_CHECK(K.E.n && K.st && K.lists && K.frames && K.log && K.dstk && K.dstk_id && K.fresh &&
              K.pool.keys && K.fs.st.p && K.fs.terms.p && K.eqst.p && K.rc.ts.p && S.estk && w.p);
-    for (u32 i = 0; i < K.pool.cap; ++i)
-        K.pool.keys[i] = 0;
+    name_set_clear(K.pool);
     memset(&K.E.n[0], 0, sizeof(ENode));
     K.E.top = 1; // node 0 = null
     K.E.oom = false;
@@ -1550,8 +1589,7 @@ OD_NOINL void dk_lower(KState &S) {
     out.fallbacks = K.fallbacks;
 
     // hoist_fresh_decls: first occurrence per name, in record order.
-    for (u32 i = 0; i < K.pool.cap; ++i)
-        K.pool.keys[i] = 0;
+    name_set_clear(K.pool);
     K.pool.count = 0;
     S.hoist = new_list(K);
     for (u32 i = 0; i < K.nfresh; ++i) {

@@ -26,7 +26,7 @@ st = s.stats()
 names = ["config+abi", "cfg", "normalize", "regions+reduce", "liveness", "pools", "lowering", "emit"]
 tot = sum(st["prof_cycles"][:8]) or 1
 print(json.dumps({"cfg": cfg, "kernels": nk, "instr": ni, "wall_s": dt, "instr_per_s": ni / dt,
-                  "ms": {k: st[k] for k in ("ms_parse", "ms_decompile", "ms_emit")},
+                  "ms": {k: st[k] for k in ("ms_parse", "ms_decompile", "ms_emit", "ms_front", "ms_lower", "ms_render")},
                   "launches": st["decompile_launches"], "retried": st["retried"],
                   "phase_share": {names[i]: round(st["prof_cycles"][i] / tot, 4) for i in range(8)},
                   "cycles_per_instr": tot / ni}))
