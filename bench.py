@@ -226,7 +226,7 @@ def main():
     ms_dec = 0.0
     ms_parse = 0.0
     ms_emit = 0.0
-    ms_ph = {"k_front": 0.0, "k_lower": 0.0, "k_emit": 0.0}
+    ms_ph = {"k_front": 0.0, "k_lower": 0.0, "k_fold": 0.0, "k_emit": 0.0}
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
@@ -237,6 +237,7 @@ def main():
             ms_emit += st["ms_emit"]
             ms_ph["k_front"] += st["ms_front"]
             ms_ph["k_lower"] += st["ms_lower"]
+            ms_ph["k_fold"] += st["ms_fold"]
             ms_ph["k_emit"] += st["ms_render"]
         ev1.record(stream)
         torch.cuda.synchronize()

@@ -99,6 +99,7 @@ typedef struct ocldec_b200_stats {
     double ms_parse, ms_decompile, ms_emit; /* last run, per pass (events); emit = combined_source gather */
     uint64_t prof_cycles[16]; /* OCLDEC_B200_PROF=1: SM cycles per decompile phase (cumulative) */
     double ms_front, ms_lower, ms_render; /* decompile pass split by launch (k_front/k_lower/k_emit) */
+    double ms_fold;                       /* k_fold (fold_expr over the statements) */
 } ocldec_b200_stats;
 int ocldec_b200_session_stats(ocldec_b200_session *s, ocldec_b200_stats *st);
 /* Device pointer + length of the last run's combined output. */

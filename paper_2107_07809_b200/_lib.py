@@ -39,7 +39,8 @@ class Stats(ctypes.Structure):
         "fallbacks", "retried", "decompile_launches", "total_launches")] + [
         ("ms_parse", ctypes.c_double), ("ms_decompile", ctypes.c_double), ("ms_emit", ctypes.c_double),
         ("prof_cycles", ctypes.c_uint64 * 16),
-        ("ms_front", ctypes.c_double), ("ms_lower", ctypes.c_double), ("ms_render", ctypes.c_double)]
+        ("ms_front", ctypes.c_double), ("ms_lower", ctypes.c_double), ("ms_render", ctypes.c_double),
+        ("ms_fold", ctypes.c_double)]
 
 
 EXPORTS = [

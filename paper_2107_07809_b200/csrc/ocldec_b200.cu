@@ -8,7 +8,7 @@
 //   P1c section scan           (kernel count, last directive) pair scan -> line roles
 //   P1d k_decode (x2)          thread per text line: labels, perfect-hash
 //                              mnemonic, operands (sizing pass, scan, fill pass)
-//   P2-P4a k_front/k_lower/k_emit  thread per .kernel section, size-sorted waves with
+//   P2-P4a k_front/k_lower/k_fold/k_emit  thread per .kernel section, size-sorted waves with
 //                              exact per-kernel arenas: config/ABI, CFG,
 //                              exec-mask normalization, region reduction,
 //                              liveness, lowering, emission
@@ -369,6 +369,15 @@ __global__ void __launch_bounds__(128) k_lower(DecompArgs a) {
         dk_lower(*g);
 }
 
+__global__ void __launch_bounds__(128) k_fold(DecompArgs a) {
+    Slot0 sl;
+    if (!dk_slot(a, &sl))
+        return;
+    KState *g = reinterpret_cast<KState *>(sl.base);
+    if (!g->done)
+        dk_fold(*g);
+}
+
 __global__ void __launch_bounds__(128) k_emit(DecompArgs a) {
     Slot0 sl;
     if (!dk_slot(a, &sl))
@@ -615,13 +624,15 @@ int phase_event(ocldec_b200_session *s, cudaEvent_t *e) {
 }
 
 void sum_phase_events(ocldec_b200_session *s) {
-    for (size_t i = 0; i + 3 < s->pev_used; i += 4) {
+    for (size_t i = 0; i + 4 < s->pev_used; i += 5) {
         float ms = 0;
         cudaEventElapsedTime(&ms, s->pev[i], s->pev[i + 1]);
         s->stats.ms_front += ms;
         cudaEventElapsedTime(&ms, s->pev[i + 1], s->pev[i + 2]);
         s->stats.ms_lower += ms;
         cudaEventElapsedTime(&ms, s->pev[i + 2], s->pev[i + 3]);
+        s->stats.ms_fold += ms;
+        cudaEventElapsedTime(&ms, s->pev[i + 3], s->pev[i + 4]);
         s->stats.ms_render += ms;
     }
     s->pev_used = 0;
@@ -847,7 +858,7 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
             a.scale = scale;
             a.arena = P<u8>(s->arena);
             auto grid = [&](u32 lp) { return (u32)(((u64)a.count * lp + 127) / 128); };
-            cudaEvent_t pe[4];
+            cudaEvent_t pe[5];
             for (auto &e : pe)
                 if (phase_event(s, &e))
                     return -3;
@@ -858,11 +869,13 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
             a.lanes_per = s->lanes_lower;
             k_lower<<<grid(a.lanes_per), 128, s->smem_lower, st>>>(a);
             CK(cudaEventRecord(pe[2], st));
+            k_fold<<<grid(a.lanes_per), 128, s->smem_lower, st>>>(a);
+            CK(cudaEventRecord(pe[3], st));
             a.lanes_per = s->lanes_emit;
             k_emit<<<grid(a.lanes_per), 128, s->smem_emit, st>>>(a);
-            CK(cudaEventRecord(pe[3], st));
-            s->stats.decompile_launches += 3;
-            s->stats.total_launches += 3;
+            CK(cudaEventRecord(pe[4], st));
+            s->stats.decompile_launches += 4;
+            s->stats.total_launches += 4;
             CK(cudaGetLastError());
             w0 = w1;
         }
@@ -1022,6 +1035,8 @@ int session_init(ocldec_b200_session *s, int device, size_t arena_bytes) {
     CK(cudaFuncSetAttribute(k_front, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
     CK(cudaFuncSetAttribute(k_lower, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
     CK(cudaFuncSetAttribute(k_emit, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    CK(cudaFuncSetAttribute(k_fold, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    CK(cudaFuncSetAttribute(k_fold, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     // the stack holds the per-thread pipeline context
     CK(cudaDeviceSetLimit(cudaLimitStackSize, 16 * 1024));
     k_init_roots<<<1, 1, 0, s->stream>>>();

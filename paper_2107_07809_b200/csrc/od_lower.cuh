@@ -383,11 +383,10 @@ struct Step {
 
     OD_NOINL void push_store(u32 addr, u32 value, DT et) {
         u32 s = new_stmt(K, SK_STORE);
-        // lower_block folds store address and value (lower.cpp:37-39)
-        u32 fa = fold(K, addr);
-        u32 fv = fold(K, value);
-        K.st[s].a = fa;
-        K.st[s].b = fv;
+        // lower_block folds store address and value (lower.cpp:37-39); the
+        // fold runs in its own pass (dk_fold)
+        K.st[s].a = addr; // folded by dk_fold
+        K.st[s].b = value;
         K.st[s].c = et;
         list_append(K, out, s);
     }
@@ -1052,20 +1051,20 @@ OD_NOINL void merge_join(KCtx &K, const Frame &F, u32 td, u32 tn, u32 ed, u32 en
                 K.st[d].a = serial;
                 K.st[d].c = vt;
                 if (!has_else && ev)
-                    K.st[d].b = fold(K, ev);
+                    K.st[d].b = ev;
                 list_append(K, F.out, d);
                 if (tv) {
                     u32 s = new_stmt(K, SK_ASSIGN);
                     K.st[s].cls = (u16)p;
                     K.st[s].a = serial;
-                    K.st[s].b = fold(K, tv);
+                    K.st[s].b = tv;
                     list_append(K, F.then_l, s);
                 }
                 if (has_else && ev) {
                     u32 s = new_stmt(K, SK_ASSIGN);
                     K.st[s].cls = (u16)p;
                     K.st[s].a = serial;
-                    K.st[s].b = fold(K, ev);
+                    K.st[s].b = ev;
                     list_append(K, F.else_l, s);
                 }
                 m.version = top + 1;
@@ -1127,7 +1126,7 @@ OD_NOINL void lower_structured(KCtx &K, u32 root, u32 out) {
         if (F.phase == 1) {
             u32 taken = taken_cond(K, R.cc, R.mask_source);
             u32 cond = R.then_is_taken ? taken : negate_condition(K.E, taken);
-            F.cond = fold(K, cond);
+            F.cond = cond;
             F.log_p0 = K.nlog;
             F.pend = K.pend;
             F.dstk_p0 = K.ndstk;
@@ -1203,7 +1202,7 @@ OD_NOINL void lower_goto(KCtx &K, u32 out) {
                 K.fallbacks++;
             } else {
                 u32 g = new_stmt(K, SK_GOTO);
-                K.st[g].a = fold(K, cond);
+                K.st[g].a = cond;
                 K.st[g].c = (u32)t.taken;
                 list_append(K, out, g);
             }
@@ -1608,6 +1607,42 @@ OD_NOINL void dk_lower(KState &S) {
     }
 }
 
+// The fold_expr calls of lower_block / taken_cond / emit_join (lower.cpp:37-39,
+// 89-121, 139-141, 225-240) as one pass over the statement pool.  Folded
+// trees only ever land in statements (never in register slots, whose
+// identity read_pair_ids/dissolve_pair compare), and fold_expr is a pure
+// function of its subtree, so folding after lowering gives the same text.
+OD_NOINL void dk_fold(KState &S) {
+    const KIn &in = S.in;
+    KCtx &K = S.K;
+    long long tp = OD_CLK();
+    for (u32 i = 1; i < K.nst && !K.E.oom; ++i) {
+        Stmt &st = K.st[i];
+        switch (st.kind) {
+        case SK_STORE:
+            st.a = fold(K, st.a);
+            st.b = fold(K, st.b);
+            break;
+        case SK_DECL:
+        case SK_ASSIGN:
+            if (st.b)
+                st.b = fold(K, st.b);
+            break;
+        case SK_IF:
+        case SK_GOTO:
+            if (st.a)
+                st.a = fold(K, st.a);
+            break;
+        default: break;
+        }
+    }
+    OD_PROF(8, tp);
+    if (K.E.oom || K.fs.st.oom || K.fs.terms.oom) {
+        S.out.status = KS_OOM;
+        S.done = 1;
+    }
+}
+
 // emit_kernel  codegen.cpp:446-467
 OD_NOINL void dk_emit(KState &S) {
     const KIn &in = S.in;
@@ -1678,6 +1713,8 @@ OD_INL KOut decompile_kernel(const KIn &in, Bump &mem, const u8 **src) {
     kstate_fix(B);
     if (!B.done)
         dk_lower(B);
+    if (!B.done)
+        dk_fold(B);
     A = B;
     memset(&B, 0x5A, sizeof(B));
     kstate_fix(A);

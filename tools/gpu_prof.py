@@ -23,10 +23,10 @@ for i in range(2):
     s.run(d_buf, n, starts)
     dt = time.time() - t
 st = s.stats()
-names = ["config+abi", "cfg", "normalize", "regions+reduce", "liveness", "pools", "lowering", "emit"]
-tot = sum(st["prof_cycles"][:8]) or 1
+names = ["config+abi", "cfg", "normalize", "regions+reduce", "liveness", "pools", "lowering", "emit", "fold"]
+tot = sum(st["prof_cycles"][:9]) or 1
 print(json.dumps({"cfg": cfg, "kernels": nk, "instr": ni, "wall_s": dt, "instr_per_s": ni / dt,
-                  "ms": {k: st[k] for k in ("ms_parse", "ms_decompile", "ms_emit", "ms_front", "ms_lower", "ms_render")},
+                  "ms": {k: st[k] for k in ("ms_parse", "ms_decompile", "ms_emit", "ms_front", "ms_lower", "ms_fold", "ms_render")},
                   "launches": st["decompile_launches"], "retried": st["retried"],
-                  "phase_share": {names[i]: round(st["prof_cycles"][i] / tot, 4) for i in range(8)},
+                  "phase_share": {names[i]: round(st["prof_cycles"][i] / tot, 4) for i in range(9)},
                   "cycles_per_instr": tot / ni}))
