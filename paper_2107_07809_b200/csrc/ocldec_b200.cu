@@ -290,8 +290,7 @@ struct DecompArgs {
 // kernels per warp (lane 0 of each 32/kpw-lane group works), kernels
 // size-sorted (largest first) so the block scheduler starts big kernels
 // first; each kernel gets an exact arena slice sized by kernel_budget(lines),
-// whose base holds its KState (in HBM, so its self-references stay valid
-// across the launches).
+// whose base holds its KState between the launches.
 struct Slot0 {
     u32 k;
     u8 *base;
@@ -306,6 +305,25 @@ __device__ __forceinline__ bool dk_slot(const DecompArgs &a, Slot0 *o) {
     o->k = a.order[i];
     o->base = a.arena + (a.boff[i] - a.boff0);
     return true;
+}
+
+// The phase kernels run on a local (stack) copy of the KState: its hot
+// counters (arena tops, writer position, stack tops) then live in L1
+// write-back local memory instead of write-through global memory.  Copies
+// are word loops (an aggregate copy here was miscompiled by nvcc 12.9).
+__device__ __forceinline__ void kstate_load(KState &S, const KState *g) {
+    static_assert(sizeof(KState) % 8 == 0, "KState is copied in u64 words");
+    const u64 *src = reinterpret_cast<const u64 *>(g);
+    u64 *dst = reinterpret_cast<u64 *>(&S);
+    for (u32 q = 0; q < sizeof(KState) / 8; ++q)
+        dst[q] = src[q];
+    kstate_fix(S);
+}
+__device__ __forceinline__ void kstate_store(KState *g, const KState &S) {
+    const u64 *src = reinterpret_cast<const u64 *>(&S);
+    u64 *dst = reinterpret_cast<u64 *>(g);
+    for (u32 q = 0; q < sizeof(KState) / 8; ++q)
+        dst[q] = src[q];
 }
 
 __global__ void __launch_bounds__(128) k_front(DecompArgs a) {
@@ -356,7 +374,10 @@ __global__ void __launch_bounds__(128) k_front(DecompArgs a) {
                k, g, g->K.in, &g->in, g->in.t, g->in.lines, g->in.lbeg, g->in.lend, g->mem.base,
                (unsigned long long)g->mem.cap);
 #endif
-        dk_front(*g);
+        KState S;
+        kstate_load(S, g);
+        dk_front(S);
+        kstate_store(g, S);
     }
 }
 
@@ -365,8 +386,12 @@ __global__ void __launch_bounds__(128) k_lower(DecompArgs a) {
     if (!dk_slot(a, &sl))
         return;
     KState *g = reinterpret_cast<KState *>(sl.base);
-    if (!g->done)
-        dk_lower(*g);
+    if (g->done)
+        return;
+    KState S;
+    kstate_load(S, g);
+    dk_lower(S);
+    kstate_store(g, S);
 }
 
 __global__ void __launch_bounds__(128) k_fold(DecompArgs a) {
@@ -374,8 +399,12 @@ __global__ void __launch_bounds__(128) k_fold(DecompArgs a) {
     if (!dk_slot(a, &sl))
         return;
     KState *g = reinterpret_cast<KState *>(sl.base);
-    if (!g->done)
-        dk_fold(*g);
+    if (g->done)
+        return;
+    KState S;
+    kstate_load(S, g);
+    dk_fold(S);
+    kstate_store(g, S);
 }
 
 __global__ void __launch_bounds__(128) k_emit(DecompArgs a) {
@@ -385,10 +414,15 @@ __global__ void __launch_bounds__(128) k_emit(DecompArgs a) {
     KState *g = reinterpret_cast<KState *>(sl.base);
     KOut o;
     const u8 *src = nullptr;
-    if (!g->done)
-        dk_emit(*g);
-    o = g->out;
-    src = g->w.p;
+    if (!g->done) {
+        KState S;
+        kstate_load(S, g);
+        dk_emit(S);
+        o = S.out;
+        src = S.w.p;
+    } else {
+        o = g->out;
+    }
     const u32 k = sl.k;
     KRes r;
     r.pad[0] = r.pad[1] = r.pad[2] = 0;

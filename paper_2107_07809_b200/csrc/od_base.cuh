@@ -139,6 +139,16 @@ OD_INL u32 ctz32(u32 m) {
 #endif
 }
 
+OD_INL u32 ctz64(u64 m) {
+#ifdef __CUDA_ARCH__
+    return (u32)__ffsll((long long)m) - 1;
+#else
+    return (u32)__builtin_ctzll(m);
+#endif
+}
+
+constexpr u32 kNoRank = 0xffffffffu;
+
 // ------------------------------------------------------------- characters
 // <cctype> in the "C" locale, as the reference uses it.
 OD_INL bool c_space(u8 c) { return c == ' ' || (c >= 9 && c <= 13); }

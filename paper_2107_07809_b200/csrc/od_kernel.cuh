@@ -283,6 +283,12 @@ struct KCtx {
     u32 *pred_n, *pred_x; // per region: live predecessor count and xor of their ids
     u32 *rstamp; // region stamps
     u32 rstamp_gen;
+    u32 *dmark;  // dirty-neighbourhood stamps (region_replace)
+    u32 dmark_gen;
+    u32 *rank;   // region -> position in the reverse post-order (kNoRank: none)
+    u32 *at;     // position -> region (0: removed)
+    u64 *cand;   // positions still to try: present and not known to fail
+    u32 ncand_w;
     u32 *rpo;    // rpo output
     u32 *dfs;    // dfs stack (pairs)
     i32 entry_r;
@@ -1072,6 +1078,7 @@ OD_NOINL bool apply_mask_pattern(KCtx &K, const MaskPattern &pat, u32 *touched, 
         return false; // "multiple join points" / "save without inversion or restore"
     const i32 invert = first_exec_op_is(K, (u32)stop, XK_INVERT, pat.mask) ? stop : -1;
     i32 then_entry = pat.then_entry, else_entry = -1, join = -1;
+    bool reach_may_shrink = false;
     *ntouched = 0;
     if (invert >= 0) {
         Block &ib = K.blk[invert];
@@ -1087,6 +1094,7 @@ OD_NOINL bool apply_mask_pattern(KCtx &K, const MaskPattern &pat, u32 *touched, 
             retarget_preds(K, invert, join, pat.header);
             ib.absorbed = 1;
             ib.nsucc = 0;
+            reach_may_shrink = true;
         } else {
             i32 rstop = -1;
             u32 nr = mask_stops(K, ib.succ, ib.nsucc, pat.mask, invert, &rstop);
@@ -1119,7 +1127,26 @@ OD_NOINL bool apply_mask_pattern(KCtx &K, const MaskPattern &pat, u32 *touched, 
     h.succ[1] = h.term.not_taken;
     h.nsucc = 2;
     touched[(*ntouched)++] = (u32)pat.header;
-    mark_reachable(K);
+    // cfg.mark_reachable() (structurizer.cpp:606).  Every new edge targets a
+    // block the mask walk reached from the (reachable) header, so
+    // reachability can only shrink, and it can only shrink when the inverted
+    // block loses its out-edges (invert-only form); in the other forms the
+    // edge changes keep every block reachable, so the walk is skipped.
+    if (reach_may_shrink)
+        mark_reachable(K);
+#ifdef OD_HOST_CHECK
+    else {
+        for (u32 b = 0; b < K.nblk; ++b)
+            K.stamp[b] = K.blk[b].reachable;
+        mark_reachable(K);
+        for (u32 b = 0; b < K.nblk; ++b)
+            if (K.stamp[b] != K.blk[b].reachable)
+                abort();
+        K.stamp_gen = 0;
+        for (u32 b = 0; b < K.nblk; ++b)
+            K.stamp[b] = 0;
+    }
+#endif
     return true;
 }
 
@@ -1250,15 +1277,23 @@ OD_NOINL bool build_regions(KCtx &K) {
     K.pred_n = K.mem->get<u32>(cap + 1);
     K.pred_x = K.mem->get<u32>(cap + 1);
     K.rstamp = K.mem->get<u32>(cap + 1);
+    K.dmark = K.mem->get<u32>(cap + 1);
+    K.rank = K.mem->get<u32>(cap + 1);
+    K.at = K.mem->get<u32>(cap + 1);
+    K.cand = K.mem->get<u64>(cap / 64 + 2);
     K.rpo = K.mem->get<u32>(cap + 1);
     K.dfs = K.mem->get<u32>(2 * cap + 4);
     u32 *by_block = K.mem->get<u32>(K.nblk + 1);
     if (!K.rg || !K.child || !K.live || !K.pred_n || !K.pred_x || !K.rstamp ||
-        !K.rpo || !K.dfs || !by_block)
+        !K.rpo || !K.dfs || !by_block || !K.dmark || !K.rank || !K.at || !K.cand)
         return false;
-    for (u32 i = 0; i <= cap; ++i)
+    for (u32 i = 0; i <= cap; ++i) {
         K.rstamp[i] = 0;
+        K.dmark[i] = 0;
+        K.rank[i] = kNoRank;
+    }
     K.rstamp_gen = 0;
+    K.dmark_gen = 0;
     K.nrg = 0;
     K.nchild = 0;
     K.nlive = 0;
@@ -1295,9 +1330,21 @@ OD_INL bool single_pred_is(const KCtx &K, u32 node, u32 pred) {
     return K.pred_n[node] == 1 && K.pred_x[node] == pred;
 }
 
+OD_INL void cand_set(KCtx &K, u32 r) {
+    const u32 k = K.rank[r];
+    if (k != kNoRank)
+        K.cand[k >> 6] |= 1ull << (k & 63);
+}
+OD_INL void cand_clear(KCtx &K, u32 r) {
+    const u32 k = K.rank[r];
+    if (k != kNoRank)
+        K.cand[k >> 6] &= ~(1ull << (k & 63));
+}
+
 // RegionGraph::replace  structurizer.cpp:141-185
 OD_NOINL void region_replace(KCtx &K, const u32 *old, u32 nold, u32 merged) {
     u32 gen = ++K.rstamp_gen;
+    const u32 dg = ++K.dmark_gen;
     for (u32 i = 0; i < nold; ++i)
         K.rstamp[old[i]] = gen;
     Region &M = K.rg[merged];
@@ -1354,6 +1401,39 @@ OD_NOINL void region_replace(KCtx &K, const u32 *old, u32 nold, u32 merged) {
         R.nsucc = no;
         for (u32 k = 0; k < no; ++k)
             R.succ[k] = out[k];
+        K.dmark[u] = dg; // u is a predecessor of M: its succ list changed
+        cand_set(K, u);
+    }
+    // A cached matcher failure of r stays valid while r's succ list, and the
+    // pred counts / single pred / succ lists of r's successors, are unchanged
+    // (structurizer.cpp:230-352 read nothing else on the failing paths).
+    // Changed succ lists: M and its preds P; changed pred sets: M and
+    // succs(M).  So r is dirty iff r is M, in P, or has a successor in
+    // succs(M) or P.
+    // The reverse post-order after the merge is the old one with the
+    // absorbed regions dropped and M at the header's position: the absorbed
+    // regions are reachable only through the header, and the merged region
+    // has the single exit (or the join's exits, in order) the header's walk
+    // reached them through (structurizer.cpp:113-139 recomputes it instead).
+    const u32 hr = K.rank[old[0]];
+    for (u32 i = 0; i < nold; ++i) {
+        cand_clear(K, old[i]);
+        if (K.rank[old[i]] != kNoRank)
+            K.at[K.rank[old[i]]] = 0;
+        K.rank[old[i]] = kNoRank;
+    }
+    K.rank[merged] = hr;
+    if (hr != kNoRank)
+        K.at[hr] = merged;
+    cand_set(K, merged);
+    for (u32 k = 0; k < M.nsucc; ++k)
+        K.dmark[M.succ[k]] = dg;
+    for (u32 i = 0; i + 1 < K.nlive; ++i) {
+        const u32 u = K.live[i];
+        const Region &R = K.rg[u];
+        for (u32 s = 0; s < R.nsucc; ++s)
+            if (K.dmark[R.succ[s]] == dg)
+                cand_set(K, u);
     }
     if (K.entry_r >= 0 && K.rstamp[K.entry_r] == gen)
         K.entry_r = (i32)merged;
@@ -1549,24 +1629,38 @@ OD_NOINL u32 region_rpo(KCtx &K) {
     return npost;
 }
 
-// reduce  structurizer.cpp:354-403
+// reduce  structurizer.cpp:354-403.  The reference rescans a fresh reverse
+// post-order after every merge and takes the first region a matcher accepts.
+// Here the order is maintained across merges (region_replace) and a region
+// whose matchers failed is only retried once a merge touched its
+// neighbourhood, which selects the same region at every step.
 OD_NOINL void reduce(KCtx &K) {
-    bool progress = true;
-    while (progress && K.nlive > 1 && !K.oom) {
-        progress = false;
-        u32 n = region_rpo(K);
-        for (u32 i = 0; i < n; ++i) {
-            u32 r = K.rpo[i];
-            u32 m = match_if_else(K, r);
-            if (!m)
-                m = match_if(K, r);
-            if (!m)
-                m = match_linear(K, r);
-            if (!m)
-                continue;
-            progress = true;
-            break;
-        }
+    const u32 n = region_rpo(K);
+    K.ncand_w = n / 64 + 1;
+    for (u32 w = 0; w < K.ncand_w; ++w)
+        K.cand[w] = 0;
+    for (u32 i = 0; i < n; ++i) {
+        K.rank[K.rpo[i]] = i;
+        K.at[i] = K.rpo[i];
+        K.cand[i >> 6] |= 1ull << (i & 63);
+    }
+    while (K.nlive > 1 && !K.oom) {
+        u32 pos = kNoRank;
+        for (u32 w = 0; w < K.ncand_w; ++w)
+            if (K.cand[w]) {
+                pos = w * 64 + ctz64(K.cand[w]);
+                break;
+            }
+        if (pos == kNoRank)
+            break; // no progress: residue
+        const u32 r = K.at[pos];
+        u32 m = match_if_else(K, r);
+        if (!m)
+            m = match_if(K, r);
+        if (!m)
+            m = match_linear(K, r);
+        if (!m && !K.oom)
+            K.cand[pos >> 6] &= ~(1ull << (pos & 63)); // fails until its neighbourhood changes
     }
     K.reduced = K.nlive == 1;
     K.root_r = K.reduced ? K.live[0] : 0;

@@ -141,6 +141,14 @@ int main(int argc, char **argv) {
             arena.assign(cap, 0);
             Bump mem{arena.data(), 0, cap, false};
             auto t0 = std::chrono::steady_clock::now();
+            if (getenv("OD_TIME_FRONT")) {
+                KState F;
+                kstate_init(F, kin, mem);
+                dk_front(F);
+                fprintf(stderr, "F %zu %u %u %.1f\n", k, F.out.ninstr, F.K.nblk,
+                        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
+                t0 = std::chrono::steady_clock::now();
+            }
             ko = decompile_kernel(kin, mem, &src);
             if (getenv("OD_TIME"))
                 fprintf(stderr, "T %zu %u %.1f\n", k, ko.ninstr,
