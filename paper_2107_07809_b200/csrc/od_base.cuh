@@ -332,23 +332,39 @@ struct Writer {
             overflow = true;
         ++n;
     }
+    // The bulk writers keep the cursor in registers and check the capacity
+    // once per call (the writer itself lives in local memory).
     OD_NOINL void puts(const char *s) {
-        while (*s)
-            put((u8)*s++);
+        u32 len = 0;
+        while (s[len])
+            ++len;
+        putn(reinterpret_cast<const u8 *>(s), len);
     }
     OD_NOINL void putn(const u8 *s, u32 len) {
-        for (u32 i = 0; i < len; ++i)
-            put(s[i]);
+        const u32 k = n;
+        if (k + len <= cap) {
+            u8 *d = p + k;
+            for (u32 i = 0; i < len; ++i)
+                d[i] = s[i];
+        } else {
+            for (u32 i = 0; i < len; ++i)
+                if (k + i < cap)
+                    p[k + i] = s[i];
+            overflow = true;
+        }
+        n = k + len;
     }
     OD_NOINL void put_u64(u64 v) {
-        char buf[24];
-        int k = 0;
+        u8 buf[24];
+        u32 k = 0;
         do {
-            buf[k++] = char('0' + v % 10);
+            buf[k++] = u8('0' + v % 10);
             v /= 10;
         } while (v);
-        while (k)
-            put((u8)buf[--k]);
+        u8 out[24];
+        for (u32 i = 0; i < k; ++i)
+            out[i] = buf[k - 1 - i];
+        putn(out, k);
     }
     OD_NOINL void put_i64(i64 v) {
         if (v < 0) {
@@ -359,19 +375,31 @@ struct Writer {
         }
     }
     OD_NOINL void put_hex(u64 v) {
-        char buf[20];
-        int k = 0;
+        u8 buf[20];
+        u32 k = 0;
         do {
             u32 d = u32(v & 15);
-            buf[k++] = char(d < 10 ? '0' + d : 'a' + d - 10);
+            buf[k++] = u8(d < 10 ? '0' + d : 'a' + d - 10);
             v >>= 4;
         } while (v);
-        while (k)
-            put((u8)buf[--k]);
-    }
-    OD_NOINL void spaces(u32 k) {
+        u8 out[20];
         for (u32 i = 0; i < k; ++i)
-            put(' ');
+            out[i] = buf[k - 1 - i];
+        putn(out, k);
+    }
+    OD_NOINL void spaces(u32 len) {
+        const u32 k = n;
+        if (k + len <= cap) {
+            u8 *d = p + k;
+            for (u32 i = 0; i < len; ++i)
+                d[i] = ' ';
+        } else {
+            for (u32 i = 0; i < len; ++i)
+                if (k + i < cap)
+                    p[k + i] = ' ';
+            overflow = true;
+        }
+        n = k + len;
     }
 };
 
