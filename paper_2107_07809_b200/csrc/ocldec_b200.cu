@@ -283,6 +283,7 @@ struct DecompArgs {
     u32 only_len;
     u64 *prof;
     u32 lanes_per; // lanes per kernel: 32 / kernels-per-warp
+    const KSize *sizes; // per kernel (k_ksize)
 };
 
 // Three launches per wave, one per pipeline phase (od_lower.cuh dk_front /
@@ -352,6 +353,7 @@ __global__ void __launch_bounds__(128) k_front(DecompArgs a) {
     in.fold_local_size = a.fold_local_size;
     in.scale = a.scale;
     in.prof = a.prof;
+    in.nblk_cap = a.scale <= 1 ? a.sizes[k].nb : 0;
     g->mem.base = sl.base + kb;
     g->mem.top = 0;
     g->mem.cap = a.boff[i + 1] - a.boff[i] - kb;
@@ -457,14 +459,18 @@ __global__ void __launch_bounds__(128) k_emit(DecompArgs a) {
     a.res[k] = r;
 }
 
-// Per-kernel size key and arena budget.
-__global__ void k_ksize(const u32 *kstart, u32 nk, u32 nlines, u32 scale, u32 *key, u64 *budget) {
+// Per-kernel sizes (a pass over the kernel's decoded lines), size key and
+// arena budget.
+__global__ void k_ksize(const u32 *kstart, u32 nk, u32 nlines, const LineRec *lines, const LineIns *lins,
+                        const Opnd *ops, KSize *sizes, u32 *key, u64 *budget) {
     u32 k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= nk)
         return;
-    u32 n = (k + 1 < nk ? kstart[k + 1] : nlines) - kstart[k];
-    key[k] = n;
-    budget[k] = kernel_budget(n, scale);
+    const u32 b = kstart[k], e = k + 1 < nk ? kstart[k + 1] : nlines;
+    const KSize z = kernel_size(lines, lins, ops, b, e);
+    sizes[k] = z;
+    key[k] = z.n;
+    budget[k] = kernel_budget(z, 1);
 }
 
 // Counting sort by descending size: histogram, scan, scatter.
@@ -626,7 +632,7 @@ struct ocldec_b200_session {
     size_t arena_bytes = 0;
     DevBuf text, tiles, tiles_off, nlpos, lines, lins, ops_cnt, labs_cnt, ops_off, labs_off, ops,
         labs, kstart, scan_tmp, scan_tot, counters, arena, stage, res, outoff, out, only, retry,
-        gen_len, gen_ninstr, gen_buf, gen_off, kmeta, order, budget, sbudget, boff, hist, prof;
+        gen_len, gen_ninstr, gen_buf, gen_off, kmeta, order, budget, sbudget, boff, hist, prof, ksizes;
     u64 pool_bytes = 0;  // arena pool per decompile wave
     bool prof_on = false;
     u32 lanes_front = 32, lanes_lower = 32, lanes_emit = 32; // 32 / kernels per warp, per phase
@@ -849,7 +855,11 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     a.prof = s->prof_on ? P<u64>(s->prof) : nullptr;
     const u32 kb = 256, kg = (nk + kb - 1) / kb;
     u32 *key = P<u32>(s->kmeta);
-    k_ksize<<<kg, kb, 0, st>>>(P<u32>(s->kstart), nk, nlines, 1, key, P<u64>(s->budget));
+    if (ensure(s->ksizes, (u64)nk * sizeof(KSize) + 16))
+        return -3;
+    a.sizes = P<KSize>(s->ksizes);
+    k_ksize<<<kg, kb, 0, st>>>(P<u32>(s->kstart), nk, nlines, P<LineRec>(s->lines), P<LineIns>(s->lins),
+                               P<Opnd>(s->ops), P<KSize>(s->ksizes), key, P<u64>(s->budget));
     CK(cudaMemsetAsync(s->hist.p, 0, kSizeBuckets * 4ull, st));
     k_hist<<<kg, kb, 0, st>>>(key, nk, P<u32>(s->hist));
     if (scan_exclusive(s, kSizeBuckets, SU32{0}, AddU32{}, U32Load{P<u32>(s->hist)},
@@ -920,7 +930,7 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     // retries: kernels that outgrew their pools (or the staging buffer)
     std::vector<KRes> hr(nk);
     u32 scale = 1;
-    std::vector<u32> keys;
+    std::vector<KSize> zs;
     for (int attempt = 0; attempt < 6; ++attempt) {
         if (d2h_sync(s, hr.data(), a.res, (u64)nk * sizeof(KRes)))
             return -3;
@@ -954,14 +964,14 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
             oom |= hr[k].status == KS_OOM;
         if (oom)
             scale *= 4;
-        if (keys.empty()) {
-            keys.resize(nk);
-            if (d2h_sync(s, keys.data(), key, (u64)nk * 4))
+        if (zs.empty()) {
+            zs.resize(nk);
+            if (d2h_sync(s, zs.data(), a.sizes, (u64)nk * sizeof(KSize)))
                 return -3;
         }
         std::vector<u64> rb(redo.size() + 1, 0);
         for (size_t i = 0; i < redo.size(); ++i)
-            rb[i + 1] = rb[i] + kernel_budget(keys[redo[i]], scale);
+            rb[i + 1] = rb[i] + kernel_budget(zs[redo[i]], scale);
         CK(cudaMemcpyAsync(P<u32>(s->order), redo.data(), redo.size() * 4, cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(P<u64>(s->boff), rb.data(), rb.size() * 8, cudaMemcpyHostToDevice, st));
         if (launch_waves(rb.data(), P<u32>(s->order), P<u64>(s->boff), (u32)redo.size(), scale))
@@ -1243,7 +1253,7 @@ void ocldec_b200_session_destroy(ocldec_b200_session *s) {
                       &s->scan_tmp, &s->scan_tot, &s->counters, &s->arena, &s->stage, &s->res,
                       &s->outoff, &s->out, &s->only, &s->retry, &s->gen_len, &s->gen_ninstr,
                       &s->gen_buf, &s->gen_off, &s->kmeta, &s->order, &s->budget, &s->sbudget,
-                      &s->boff, &s->hist, &s->prof};
+                      &s->boff, &s->hist, &s->prof, &s->ksizes};
     for (DevBuf *b : bufs)
         if (b->p)
             cudaFree(b->p);

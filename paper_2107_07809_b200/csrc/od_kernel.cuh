@@ -52,6 +52,7 @@ struct KIn {
     u32 line_base;        // global 1-based line number of chunk line 0 is line_base + 1
     u32 fold_local_size;
     u32 scale;            // pool capacity multiplier (retries)
+    u32 nblk_cap;         // block capacity (KSize::nb; 0 = one per instruction)
     u64 *prof;            // optional per-phase cycle counters
 };
 
@@ -634,59 +635,102 @@ OD_INL u32 match_settings_load(KCtx &K, u32 offset, u32 dwords) {
 }
 
 // ====================================================== instructions
-OD_NOINL void classify_exec(const KCtx &K, Ins &I) {
-    I.xkind = XK_NONE;
-    I.xmask = 0;
-    if ((I.flags & IF_PARSE_FAILED) || I.prefix != PX_S)
-        return;
-    const Opnd *o = K.in->ops + I.op_start;
-    u32 n = I.nops;
-    if (I.root == R_AND_SAVEEXEC && n >= 2 && o[0].kind == OK_SREG && o[0].count == 2) {
-        I.xkind = XK_SAVE;
-        I.xmask = o[0].r.a;
-        return;
+// annotate_exec's per-instruction classification (cfg.cpp:158-226) from the
+// decoded fields; *mask gets the saved-mask SGPR.
+OD_INL u32 exec_kind_of(u32 root, u32 prefix, u32 flags, u32 n, const Opnd *o, u32 *mask) {
+    *mask = 0;
+    if ((flags & IF_PARSE_FAILED) || prefix != PX_S)
+        return XK_NONE;
+    if (root == R_AND_SAVEEXEC && n >= 2 && o[0].kind == OK_SREG && o[0].count == 2) {
+        *mask = o[0].r.a;
+        return XK_SAVE;
     }
     bool dst_exec = n >= 1 && op_is_special(o[0], SP_EXEC);
     if (!dst_exec)
-        return;
-    if (I.root == R_MOV && n >= 2 && op_is_sreg_pair(o[1])) {
-        I.xkind = XK_RESTORE;
-        I.xmask = o[1].r.a;
-        return;
+        return XK_NONE;
+    if (root == R_MOV && n >= 2 && op_is_sreg_pair(o[1])) {
+        *mask = o[1].r.a;
+        return XK_RESTORE;
     }
-    if (I.root == R_OR && n >= 3) {
+    if (root == R_OR && n >= 3) {
         if (op_is_special(o[1], SP_EXEC) && op_is_sreg_pair(o[2])) {
-            I.xkind = XK_RESTORE;
-            I.xmask = o[2].r.a;
-            return;
+            *mask = o[2].r.a;
+            return XK_RESTORE;
         }
         if (op_is_special(o[2], SP_EXEC) && op_is_sreg_pair(o[1])) {
-            I.xkind = XK_RESTORE;
-            I.xmask = o[1].r.a;
-            return;
+            *mask = o[1].r.a;
+            return XK_RESTORE;
         }
     }
-    if ((I.root == R_ANDN2 || I.root == R_XOR) && n >= 3) {
+    if ((root == R_ANDN2 || root == R_XOR) && n >= 3) {
         if (op_is_sreg_pair(o[1]) && op_is_special(o[2], SP_EXEC)) {
-            I.xkind = XK_INVERT;
-            I.xmask = o[1].r.a;
-        } else if (op_is_sreg_pair(o[2]) && op_is_special(o[1], SP_EXEC)) {
-            I.xkind = XK_INVERT;
-            I.xmask = o[2].r.a;
+            *mask = o[1].r.a;
+            return XK_INVERT;
+        }
+        if (op_is_sreg_pair(o[2]) && op_is_special(o[1], SP_EXEC)) {
+            *mask = o[2].r.a;
+            return XK_INVERT;
         }
     }
+    return XK_NONE;
+}
+
+OD_NOINL void classify_exec(const KCtx &K, Ins &I) {
+    u32 m;
+    I.xkind = (u8)exec_kind_of(I.root, I.prefix, I.flags, I.nops, K.in->ops + I.op_start, &m);
+    I.xmask = m;
+}
+
+// Per-kernel sizes that bound every allocation decompile_kernel makes
+// (kernel_budget): counted from the decoded lines before the wave layout.
+struct KSize {
+    u32 n;    // lines of the section (incl. the .kernel line)
+    u32 ncfg; // config lines
+    u32 nins; // instruction lines
+    u32 nlab; // labels
+    u32 nb;   // blocks: leaders (first, labelled, after a branch/endpgm) + exec-op splits + the synthetic end
+};
+
+OD_INL KSize kernel_size(const LineRec *lines, const LineIns *lins, const Opnd *ops, u32 lbeg, u32 lend) {
+    KSize z;
+    z.n = lend - lbeg;
+    z.ncfg = z.nins = z.nlab = 0;
+    u32 labelled = 0, enders = 0, xops = 0;
+    for (u32 l = lbeg + 1; l < lend; ++l) {
+        const u8 role = lines[l].role;
+        if (role == LR_CONFIG) {
+            ++z.ncfg;
+            continue;
+        }
+        if (role != LR_TEXT)
+            continue;
+        const LineIns &L = lins[l];
+        z.nlab += L.nlabels;
+        labelled += L.nlabels ? 1 : 0;
+        if (!(L.flags & IF_HAS_INS))
+            continue;
+        ++z.nins;
+        if (L.prefix == PX_S && (L.root == R_BRANCH || L.root == R_ENDPGM || (L.rflags & RF_CBRANCH)))
+            ++enders;
+        u32 m;
+        if (L.prefix == PX_S && exec_kind_of(L.root, L.prefix, L.flags, L.nops, ops + L.op_start, &m) != XK_NONE)
+            ++xops;
+    }
+    z.nb = 3 + labelled + enders + xops;
+    return z;
 }
 
 // parse_text + attach_trailing_labels (asm_frontend.cpp:486-521,
 // decompiler.cpp:20-31)
 OD_NOINL bool collect_instructions(KCtx &K) {
     const KIn &in = *K.in;
-    u32 nl = in.lend - in.lbeg;
-    K.ins = K.mem->get<Ins>(nl + 1);
-    u32 total_labels = 0;
+    u32 total_labels = 0, total_ins = 0;
     for (u32 l = in.lbeg + 1; l < in.lend; ++l)
-        if (in.lines[l].role == LR_TEXT)
+        if (in.lines[l].role == LR_TEXT) {
             total_labels += in.lins[l].nlabels;
+            total_ins += (in.lins[l].flags & IF_HAS_INS) ? 1 : 0;
+        }
+    K.ins = K.mem->get<Ins>(total_ins + 2); // + synthetic s_endpgm
     K.kl = K.mem->get<u32>(total_labels + 1);
     if (!K.ins || !K.kl)
         return false;
@@ -811,6 +855,8 @@ OD_NOINL void mark_reachable(KCtx &K) {
 OD_NOINL bool build_cfg(KCtx &K) {
     u32 n = K.nins;
     K.blk_cap = n + 2;
+    if (K.in->nblk_cap && K.in->nblk_cap < K.blk_cap)
+        K.blk_cap = K.in->nblk_cap;
     K.blk = K.mem->get<Block>(K.blk_cap);
     K.stamp = K.mem->get<u32>(K.blk_cap);
     K.work = K.mem->get<u32>(2 * K.blk_cap + 4);
@@ -852,6 +898,8 @@ OD_NOINL bool build_cfg(KCtx &K) {
                 lead = true;
         }
         if (lead) {
+            if (K.nblk >= K.blk_cap)
+                return false; // size bound too tight: KS_OOM, retried at the worst case
             if (K.nblk)
                 K.blk[K.nblk - 1].ie = i;
             Block &B = K.blk[K.nblk];
@@ -943,6 +991,10 @@ OD_NOINL void annotate_block(KCtx &K, u32 b) {
 
 // split_block  structurizer.cpp:416-435
 OD_NOINL u32 split_block(KCtx &K, u32 id, u32 at) {
+    if (K.nblk >= K.blk_cap) { // the size bound was too tight: retry at the worst case
+        K.oom = true;
+        return id;
+    }
     u32 nid = K.nblk++;
     Block &B = K.blk[id];
     Block &N = K.blk[nid];

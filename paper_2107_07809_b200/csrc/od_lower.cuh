@@ -1390,25 +1390,30 @@ OD_INL PoolCaps pool_caps(u32 n, u32 s) {
     return c;
 }
 
-// Upper bound of the arena decompile_kernel needs for n lines at scale s
-// (every allocation it makes, with worst-case counts: one block per
-// instruction, two regions per block, two labels per line).
-OD_INL u64 arena_budget(u32 n, u32 s) {
-    const u64 b = n + 2;          // blocks
-    const u64 r = 2 * b + 6;      // regions
+// Upper bound of the arena decompile_kernel needs for a kernel of sizes z at
+// scale s (every allocation it makes, in order; regions <= 2 * blocks + 4).
+// At s > 1 (a retry) the block bound falls back to one block per
+// instruction.
+OD_INL u64 arena_budget(const KSize &z, u32 s) {
+    const u64 ni = z.nins + 1;                                // + synthetic s_endpgm
+    u64 b = ni + 2;                                           // blocks (build_cfg's cap)
+    if (s <= 1 && z.nb < b)
+        b = z.nb;
+    const u64 r = 2 * b + 4;                                  // regions (build_regions' cap)
     u64 t = 0;
-    t += (n + 1) * (sizeof(KArg) + sizeof(Span));            // config
-    t += (n + 2) * sizeof(Ins) + (2 * n + 2) * 4;            // instructions, labels
-    t += (n + 9) * sizeof(AbiEntry);                         // ABI map
-    t += b * (sizeof(Block) + 4 + 8 + 1) + 16;               // blocks, stamps, work, supp
+    t += (z.ncfg + 1) * (sizeof(KArg) + sizeof(Span));       // config
+    t += (ni + 1) * sizeof(Ins) + (z.nlab + 1) * 4;           // instructions, labels
+    t += (8 + z.ncfg) * sizeof(AbiEntry);                     // ABI map
+    t += b * (sizeof(Block) + 4) + (2 * b + 4) * 4 + (ni + 1); // blocks, stamps, work, supp
     u64 lc = 16;
-    while (lc < 2 * (2 * (u64)n + 2))
+    while (lc < 2 * ((u64)z.nlab + 1))
         lc <<= 1;
-    t += 2 * lc * 4;                                         // label map
-    t += (r + 1) * (sizeof(Region) + 6 * 4) + (4 * r + 8) * 4 + 2 * (2 * r + 4) * 4 + (b + 1) * 4;
-    t += 3 * b * kLiveWords * 4;                             // liveness
+    t += 2 * lc * 4;                                          // label map
+    t += (r + 1) * sizeof(Region) + (4 * r + 8) * 4 + 8 * (r + 1) * 4 + (r / 64 + 2) * 8 +
+         (2 * r + 4) * 4 + (b + 1) * 4;                       // regions
+    t += 3 * b * kLiveWords * 4;                              // liveness
     t += kPhysSlots * sizeof(Slot);
-    const PoolCaps c = pool_caps(n, s);
+    const PoolCaps c = pool_caps(z.n, s);
     t += (u64)c.nodes * sizeof(ENode) + (u64)c.stmts * sizeof(Stmt) + (2 * r + 4) * sizeof(SList) +
          (2 * r + 8) * sizeof(Frame) + (u64)c.log * sizeof(UndoRec) + (u64)c.dstk * (sizeof(Slot) + 4) +
          (u64)c.fresh * sizeof(Fresh) + (u64)c.names * 8 + 3ull * c.stack * 4 + (u64)c.tasks * 8 +
@@ -1496,6 +1501,7 @@ OD_NOINL void dk_front(KState &S) {
     }
     OD_PROF(1, tp);
     normalize(K);
+    OD_CHECK(!K.oom);
     OD_PROF(2, tp);
     OD_CHECK(build_regions(K));
     reduce(K);
@@ -1698,7 +1704,7 @@ OD_NOINL void dk_emit(KState &S) {
 
 // Arena slice of a kernel of n lines at scale s on the device: the KState
 // plus everything dk_front/dk_lower/dk_emit allocate.
-OD_INL u64 kernel_budget(u32 n, u32 s) { return arena_budget(n, s) + ((sizeof(KState) + 255) & ~255ull); }
+OD_INL u64 kernel_budget(const KSize &z, u32 s) { return arena_budget(z, s) + ((sizeof(KState) + 255) & ~255ull); }
 
 // All three phases back to back (host harness and single-launch use).
 // Returns the status; on KS_OK the OpenCL source is at *src.

@@ -136,8 +136,10 @@ int main(int argc, char **argv) {
         KOut ko;
         const u8 *src = nullptr;
         std::vector<u8> arena;
+        const KSize z = kernel_size(lines.data(), lins.data(), ops.data(), kin.lbeg, kin.lend);
         for (kin.scale = 1;; kin.scale *= 4) {
-            u64 cap = arena_budget(kin.lend - kin.lbeg, kin.scale);
+            kin.nblk_cap = kin.scale <= 1 ? z.nb : 0;
+            u64 cap = arena_budget(z, kin.scale);
             arena.assign(cap, 0);
             Bump mem{arena.data(), 0, cap, false};
             auto t0 = std::chrono::steady_clock::now();
@@ -155,7 +157,7 @@ int main(int argc, char **argv) {
                         std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
             if (ko.status != KS_OOM || kin.scale > 1024)
                 break;
-            if (getenv("OD_USAGE"))
+            if (getenv("OD_USAGE") || getenv("OD_RETRY"))
                 fprintf(stderr, "retry kernel %zu scale %u\n", k, kin.scale * 4);
         }
         Span nm;

@@ -10,11 +10,22 @@ from collections import defaultdict
 CSRC = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2107_07809_b200", "csrc")
 starts = {}
 pat = re.compile(r"^\s*(?:OD_NOINL|OD_INL|__global__|__device__)[^(]*?\b(\w+)\s*\(")
+REV = os.environ.get("REV")  # read the sources at this git revision (the profiled build)
+
+
+def source_lines(f):
+    if REV:
+        import subprocess
+        return subprocess.run(["git", "show", f"{REV}:paper_2107_07809_b200/csrc/{f}"], capture_output=True,
+                              text=True, cwd=os.path.dirname(CSRC) + "/..").stdout.splitlines()
+    return open(os.path.join(CSRC, f)).read().splitlines()
+
+
 for f in os.listdir(CSRC):
     if not (f.endswith(".cuh") or f.endswith(".cu")):
         continue
     lst = []
-    for i, line in enumerate(open(os.path.join(CSRC, f)), 1):
+    for i, line in enumerate(source_lines(f), 1):
         m = pat.match(line)
         if m:
             lst.append((i, m.group(1)))
