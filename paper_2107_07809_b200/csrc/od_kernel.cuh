@@ -282,6 +282,9 @@ struct KCtx {
     u32 *live;   // live region list
     u32 nlive;
     u32 *pred_n, *pred_x; // per region: live predecessor count and xor of their ids
+    u32 *phead;           // per region: predecessor edge list (edge pool index, 0 = end)
+    u32 *enext, *efrom;   // edge pool
+    u32 etop, efree, ecap;
     u32 *rstamp; // region stamps
     u32 rstamp_gen;
     u32 *dmark;  // dirty-neighbourhood stamps (region_replace)
@@ -1292,16 +1295,42 @@ OD_INL u32 make_region(KCtx &K, u8 kind) {
 OD_INL void pred_add(KCtx &K, u32 t, u32 from) {
     K.pred_n[t]++;
     K.pred_x[t] ^= from;
+    u32 e = K.efree;
+    if (e)
+        K.efree = K.enext[e];
+    else if (K.etop < K.ecap)
+        e = K.etop++;
+    else {
+        K.oom = true;
+        return;
+    }
+    K.efrom[e] = from;
+    K.enext[e] = K.phead[t];
+    K.phead[t] = e;
 }
 OD_INL void pred_del(KCtx &K, u32 t, u32 from) {
     K.pred_n[t]--;
     K.pred_x[t] ^= from;
+    u32 *link = &K.phead[t];
+    while (*link) {
+        const u32 e = *link;
+        if (K.efrom[e] == from) {
+            *link = K.enext[e];
+            K.enext[e] = K.efree;
+            K.efree = e;
+            return;
+        }
+        link = &K.enext[e];
+    }
 }
 
 OD_NOINL void rebuild_region_preds(KCtx &K) {
+    K.etop = 1; // edge 0 = end of list
+    K.efree = 0;
     for (u32 i = 0; i < K.nlive; ++i) {
         K.pred_n[K.live[i]] = 0;
         K.pred_x[K.live[i]] = 0;
+        K.phead[K.live[i]] = 0;
     }
     for (u32 i = 0; i < K.nlive; ++i) {
         const Region &R = K.rg[K.live[i]];
@@ -1328,6 +1357,10 @@ OD_NOINL bool build_regions(KCtx &K) {
     K.live = K.mem->get<u32>(cap + 1);
     K.pred_n = K.mem->get<u32>(cap + 1);
     K.pred_x = K.mem->get<u32>(cap + 1);
+    K.phead = K.mem->get<u32>(cap + 1);
+    K.ecap = 2 * cap + 4;
+    K.enext = K.mem->get<u32>(K.ecap);
+    K.efrom = K.mem->get<u32>(K.ecap);
     K.rstamp = K.mem->get<u32>(cap + 1);
     K.dmark = K.mem->get<u32>(cap + 1);
     K.rank = K.mem->get<u32>(cap + 1);
@@ -1336,7 +1369,7 @@ OD_NOINL bool build_regions(KCtx &K) {
     K.rpo = K.mem->get<u32>(cap + 1);
     K.dfs = K.mem->get<u32>(2 * cap + 4);
     u32 *by_block = K.mem->get<u32>(K.nblk + 1);
-    if (!K.rg || !K.child || !K.live || !K.pred_n || !K.pred_x || !K.rstamp ||
+    if (!K.rg || !K.child || !K.live || !K.pred_n || !K.pred_x || !K.phead || !K.enext || !K.efrom || !K.rstamp ||
         !K.rpo || !K.dfs || !by_block || !K.dmark || !K.rank || !K.at || !K.cand)
         return false;
     for (u32 i = 0; i <= cap; ++i) {
@@ -1395,7 +1428,7 @@ OD_INL void cand_clear(KCtx &K, u32 r) {
 
 // RegionGraph::replace  structurizer.cpp:141-185
 OD_NOINL void region_replace(KCtx &K, const u32 *old, u32 nold, u32 merged) {
-    u32 gen = ++K.rstamp_gen;
+    const u32 gen = ++K.rstamp_gen;
     const u32 dg = ++K.dmark_gen;
     for (u32 i = 0; i < nold; ++i)
         K.rstamp[old[i]] = gen;
@@ -1403,11 +1436,16 @@ OD_NOINL void region_replace(KCtx &K, const u32 *old, u32 nold, u32 merged) {
     M.nsucc = 0;
     K.pred_n[merged] = 0;
     K.pred_x[merged] = 0;
+    K.phead[merged] = 0;
+    // M's successors: the old regions' exits in order (self edges to the
+    // header become M's self edge), at most two.
     for (u32 i = 0; i < nold; ++i) {
         const Region &O = K.rg[old[i]];
         for (u32 s = 0; s < O.nsucc; ++s) {
-            pred_del(K, (u32)O.succ[s], old[i]);
-            u32 t = (u32)O.succ[s] == old[0] ? merged : (u32)O.succ[s];
+            const u32 t0 = (u32)O.succ[s];
+            if (K.rstamp[t0] != gen)
+                pred_del(K, t0, old[i]);
+            u32 t = t0 == old[0] ? merged : t0;
             if (t != merged && K.rstamp[t] == gen)
                 continue;
             bool dup = false;
@@ -1420,48 +1458,45 @@ OD_NOINL void region_replace(KCtx &K, const u32 *old, u32 nold, u32 merged) {
     }
     for (u32 k = 0; k < M.nsucc; ++k)
         pred_add(K, (u32)M.succ[k], merged);
-    u32 w = 0;
-    for (u32 i = 0; i < K.nlive; ++i)
-        if (K.rstamp[K.live[i]] != gen)
-            K.live[w++] = K.live[i];
-    K.live[w++] = merged;
-    K.nlive = w;
-    for (u32 i = 0; i + 1 < K.nlive; ++i) {
-        const u32 u = K.live[i];
-        Region &R = K.rg[u];
-        bool hit = false;
-        for (u32 s = 0; s < R.nsucc; ++s)
-            hit |= K.rstamp[R.succ[s]] == gen;
-        if (!hit)
-            continue;
-        i32 out[2];
-        u32 no = 0;
-        for (u32 s = 0; s < R.nsucc; ++s) {
-            u32 t = K.rstamp[R.succ[s]] == gen ? merged : (u32)R.succ[s];
-            bool dup = false;
+    // Outside predecessors of the old regions now point at M (their succ
+    // lists keep their order; duplicates collapse).
+    for (u32 i = 0; i < nold; ++i) {
+        for (u32 e = K.phead[old[i]]; e; e = K.enext[e]) {
+            const u32 u = K.efrom[e];
+            if (K.rstamp[u] == gen || K.dmark[u] == dg)
+                continue;
+            Region &R = K.rg[u];
+            i32 out[2];
+            u32 no = 0;
+            for (u32 s = 0; s < R.nsucc; ++s) {
+                u32 t = K.rstamp[R.succ[s]] == gen ? merged : (u32)R.succ[s];
+                bool dup = false;
+                for (u32 k = 0; k < no; ++k)
+                    if ((u32)out[k] == t)
+                        dup = true;
+                if (!dup)
+                    out[no++] = (i32)t;
+            }
+            R.nsucc = no;
             for (u32 k = 0; k < no; ++k)
-                if ((u32)out[k] == t)
-                    dup = true;
-            if (!dup)
-                out[no++] = (i32)t;
+                R.succ[k] = out[k];
+            K.dmark[u] = dg; // u is a predecessor of M: its succ list changed
         }
-        // edges into the old regions die with them; u gains one edge into M
-        for (u32 s = 0; s < R.nsucc; ++s)
-            if (K.rstamp[R.succ[s]] == gen)
-                pred_del(K, (u32)R.succ[s], u);
-        pred_add(K, merged, u);
-        R.nsucc = no;
-        for (u32 k = 0; k < no; ++k)
-            R.succ[k] = out[k];
-        K.dmark[u] = dg; // u is a predecessor of M: its succ list changed
-        cand_set(K, u);
     }
-    // A cached matcher failure of r stays valid while r's succ list, and the
-    // pred counts / single pred / succ lists of r's successors, are unchanged
-    // (structurizer.cpp:230-352 read nothing else on the failing paths).
-    // Changed succ lists: M and its preds P; changed pred sets: M and
-    // succs(M).  So r is dirty iff r is M, in P, or has a successor in
-    // succs(M) or P.
+    // (pred lists of the old regions die with them; the marked ones gain M)
+    for (u32 i = 0; i < nold; ++i)
+        for (u32 e = K.phead[old[i]]; e; e = K.enext[e]) {
+            const u32 u = K.efrom[e];
+            if (K.dmark[u] == dg && K.rstamp[u] != gen) {
+                K.dmark[u] = dg + 1; // once per predecessor
+                pred_add(K, merged, u);
+            }
+        }
+    K.dmark_gen = dg + 1;
+    const u32 pg = dg + 1;   // P marked pg now
+    K.nlive -= nold - 1;
+    if (K.entry_r >= 0 && K.rstamp[K.entry_r] == gen)
+        K.entry_r = (i32)merged;
     // The reverse post-order after the merge is the old one with the
     // absorbed regions dropped and M at the header's position: the absorbed
     // regions are reachable only through the header, and the merged region
@@ -1477,18 +1512,23 @@ OD_NOINL void region_replace(KCtx &K, const u32 *old, u32 nold, u32 merged) {
     K.rank[merged] = hr;
     if (hr != kNoRank)
         K.at[hr] = merged;
+    // A cached matcher failure of r stays valid while r's succ list, and the
+    // pred counts / single pred / succ lists of r's successors, are unchanged
+    // (structurizer.cpp:230-352 read nothing else on the failing paths).
+    // Changed succ lists: M and its preds P; changed pred sets: M and
+    // succs(M).  So the dirty regions are M, P, and the predecessors of
+    // succs(M) and of P.
     cand_set(K, merged);
-    for (u32 k = 0; k < M.nsucc; ++k)
-        K.dmark[M.succ[k]] = dg;
-    for (u32 i = 0; i + 1 < K.nlive; ++i) {
-        const u32 u = K.live[i];
-        const Region &R = K.rg[u];
-        for (u32 s = 0; s < R.nsucc; ++s)
-            if (K.dmark[R.succ[s]] == dg)
-                cand_set(K, u);
+    for (u32 e = K.phead[merged]; e; e = K.enext[e]) {
+        const u32 u = K.efrom[e];
+        cand_set(K, u);
+        for (u32 f = K.phead[u]; f; f = K.enext[f])
+            cand_set(K, K.efrom[f]);
     }
-    if (K.entry_r >= 0 && K.rstamp[K.entry_r] == gen)
-        K.entry_r = (i32)merged;
+    for (u32 k = 0; k < M.nsucc; ++k)
+        for (u32 e = K.phead[M.succ[k]]; e; e = K.enext[e])
+            cand_set(K, K.efrom[e]);
+    (void)pg;
 }
 
 OD_INL const Term *header_term(const KCtx &K, u32 r, bool *usable) {
@@ -1715,7 +1755,7 @@ OD_NOINL void reduce(KCtx &K) {
             K.cand[pos >> 6] &= ~(1ull << (pos & 63)); // fails until its neighbourhood changes
     }
     K.reduced = K.nlive == 1;
-    K.root_r = K.reduced ? K.live[0] : 0;
+    K.root_r = K.reduced ? (u32)K.entry_r : 0; // the one live region holds the entry
 }
 
 // ========================================================== liveness

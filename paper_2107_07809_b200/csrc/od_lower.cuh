@@ -1409,8 +1409,8 @@ OD_INL u64 arena_budget(const KSize &z, u32 s) {
     while (lc < 2 * ((u64)z.nlab + 1))
         lc <<= 1;
     t += 2 * lc * 4;                                          // label map
-    t += (r + 1) * sizeof(Region) + (4 * r + 8) * 4 + 8 * (r + 1) * 4 + (r / 64 + 2) * 8 +
-         (2 * r + 4) * 4 + (b + 1) * 4;                       // regions
+    t += (r + 1) * sizeof(Region) + (4 * r + 8) * 4 + 9 * (r + 1) * 4 + (r / 64 + 2) * 8 +
+         (2 * r + 4) * 4 * 3 + (b + 1) * 4;                   // regions, pred edge lists
     t += 3 * b * kLiveWords * 4;                              // liveness
     t += kPhysSlots * sizeof(Slot);
     const PoolCaps c = pool_caps(z.n, s);
