@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libocldec_b200.so")
+# OCLDEC_B200_LIB selects an alternative in-tree build (tuning experiments).
+LIB_PATH = os.environ.get("OCLDEC_B200_LIB") or os.path.join(_HERE, "libocldec_b200.so")
 
 
 class Options(ctypes.Structure):

@@ -308,6 +308,20 @@ __device__ __forceinline__ bool dk_slot(const DecompArgs &a, Slot0 *o) {
     return true;
 }
 
+// Minimum resident blocks per SM for the phase kernels (register caps).
+#ifndef OD_MINB_FRONT
+#define OD_MINB_FRONT 10
+#endif
+#ifndef OD_MINB_LOWER
+#define OD_MINB_LOWER 16
+#endif
+#ifndef OD_MINB_FOLD
+#define OD_MINB_FOLD 12
+#endif
+#ifndef OD_MINB_EMIT
+#define OD_MINB_EMIT 16
+#endif
+
 // The phase kernels run on a local (stack) copy of the KState: its hot
 // counters (arena tops, writer position, stack tops) then live in L1
 // write-back local memory instead of write-through global memory.  Copies
@@ -327,7 +341,7 @@ __device__ __forceinline__ void kstate_store(KState *g, const KState &S) {
         dst[q] = src[q];
 }
 
-__global__ void __launch_bounds__(128) k_front(DecompArgs a) {
+__global__ void __launch_bounds__(128, OD_MINB_FRONT) k_front(DecompArgs a) {
     Slot0 sl;
     if (!dk_slot(a, &sl))
         return;
@@ -383,7 +397,7 @@ __global__ void __launch_bounds__(128) k_front(DecompArgs a) {
     }
 }
 
-__global__ void __launch_bounds__(128) k_lower(DecompArgs a) {
+__global__ void __launch_bounds__(128, OD_MINB_LOWER) k_lower(DecompArgs a) {
     Slot0 sl;
     if (!dk_slot(a, &sl))
         return;
@@ -396,7 +410,7 @@ __global__ void __launch_bounds__(128) k_lower(DecompArgs a) {
     kstate_store(g, S);
 }
 
-__global__ void __launch_bounds__(128) k_fold(DecompArgs a) {
+__global__ void __launch_bounds__(128, OD_MINB_FOLD) k_fold(DecompArgs a) {
     Slot0 sl;
     if (!dk_slot(a, &sl))
         return;
@@ -409,7 +423,7 @@ __global__ void __launch_bounds__(128) k_fold(DecompArgs a) {
     kstate_store(g, S);
 }
 
-__global__ void __launch_bounds__(128) k_emit(DecompArgs a) {
+__global__ void __launch_bounds__(128, OD_MINB_EMIT) k_emit(DecompArgs a) {
     Slot0 sl;
     if (!dk_slot(a, &sl))
         return;
