@@ -367,7 +367,13 @@ __global__ void __launch_bounds__(128, OD_MINB_FRONT) k_front(DecompArgs a) {
     in.fold_local_size = a.fold_local_size;
     in.scale = a.scale;
     in.prof = a.prof;
-    in.nblk_cap = a.scale <= 1 ? a.sizes[k].nb : 0;
+    {
+        const KSize z = a.sizes[k];
+        in.nblk_cap = a.scale <= 1 ? z.nb : 0;
+        in.ncfg = z.ncfg;
+        in.nins = z.nins;
+        in.nlab = z.nlab;
+    }
     g->mem.base = sl.base + kb;
     g->mem.top = 0;
     g->mem.cap = a.boff[i + 1] - a.boff[i] - kb;

@@ -334,6 +334,8 @@ struct Writer {
     }
     // The bulk writers keep the cursor in registers and check the capacity
     // once per call (the writer itself lives in local memory).
+    // string literal: length known at compile time
+    template <u32 N> OD_INL void lit(const char (&s)[N]) { putn(reinterpret_cast<const u8 *>(s), N - 1); }
     OD_NOINL void puts(const char *s) {
         u32 len = 0;
         while (s[len])

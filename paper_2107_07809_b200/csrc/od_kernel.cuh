@@ -53,6 +53,7 @@ struct KIn {
     u32 fold_local_size;
     u32 scale;            // pool capacity multiplier (retries)
     u32 nblk_cap;         // block capacity (KSize::nb; 0 = one per instruction)
+    u32 ncfg, nins, nlab; // KSize counts of the section (config lines, instructions, labels)
     u64 *prof;            // optional per-phase cycle counters
 };
 
@@ -445,10 +446,7 @@ OD_NOINL bool parse_config(KCtx &K) {
         split_word(t, rest, &nm, &extra);
         c.name = nm;
     }
-    u32 ncfg = 0;
-    for (u32 l = in.lbeg + 1; l < in.lend; ++l)
-        if (in.lines[l].role == LR_CONFIG)
-            ++ncfg;
+    const u32 ncfg = in.ncfg;
     c.args = K.mem->get<KArg>(ncfg + 1);
     K.arg_sname = K.mem->get<Span>(ncfg + 1);
     if (!c.args || !K.arg_sname)
@@ -727,29 +725,29 @@ OD_INL KSize kernel_size(const LineRec *lines, const LineIns *lins, const Opnd *
 // decompiler.cpp:20-31)
 OD_NOINL bool collect_instructions(KCtx &K) {
     const KIn &in = *K.in;
-    u32 total_labels = 0, total_ins = 0;
-    for (u32 l = in.lbeg + 1; l < in.lend; ++l)
-        if (in.lines[l].role == LR_TEXT) {
-            total_labels += in.lins[l].nlabels;
-            total_ins += (in.lins[l].flags & IF_HAS_INS) ? 1 : 0;
-        }
-    K.ins = K.mem->get<Ins>(total_ins + 2); // + synthetic s_endpgm
-    K.kl = K.mem->get<u32>(total_labels + 1);
+    K.ins = K.mem->get<Ins>(in.nins + 2); // + synthetic s_endpgm
+    K.kl = K.mem->get<u32>(in.nlab + 1);
     if (!K.ins || !K.kl)
         return false;
-    K.nins = 0;
-    K.nkl = 0;
-    u32 pend_b = 0;
-    u32 last_line = in.line_base + in.lbeg + 1; // section.line
-    for (u32 l = in.lbeg + 1; l < in.lend; ++l) {
-        if (in.lines[l].role != LR_TEXT)
+    // locals: the stores below go through generic pointers, which would
+    // otherwise force the KCtx fields to be reloaded every iteration
+    const LineRec *__restrict__ lines = in.lines;
+    const LineIns *__restrict__ lins = in.lins;
+    const Opnd *__restrict__ ops = in.ops;
+    Ins *__restrict__ ins = K.ins;
+    u32 *__restrict__ kl = K.kl;
+    const u32 lbeg = in.lbeg, lend = in.lend, line_base = in.line_base;
+    u32 ni = 0, nkl = 0, pend_b = 0;
+    u32 last_line = line_base + lbeg + 1; // section.line
+    for (u32 l = lbeg + 1; l < lend; ++l) {
+        if (lines[l].role != LR_TEXT)
             continue;
-        const LineIns &L = in.lins[l];
+        const LineIns L = lins[l];
         for (u32 k = 0; k < L.nlabels; ++k)
-            K.kl[K.nkl++] = L.lab_start + k;
+            kl[nkl++] = L.lab_start + k;
         if (!(L.flags & IF_HAS_INS))
             continue;
-        Ins &I = K.ins[K.nins++];
+        Ins I;
         I.root = L.root;
         I.prefix = L.prefix;
         I.rflags = L.rflags;
@@ -758,15 +756,21 @@ OD_NOINL bool collect_instructions(KCtx &K) {
         I.nops = L.nops;
         I.flags = L.flags;
         I.op_start = L.op_start;
-        I.line = in.line_base + l + 1;
+        I.line = line_base + l + 1;
         I.src.off = L.src_off;
         I.src.len = L.src_len;
         I.lab_b = pend_b;
-        I.lab_n = K.nkl - pend_b;
-        pend_b = K.nkl;
+        I.lab_n = nkl - pend_b;
+        u32 m = 0;
+        I.xkind = L.prefix == PX_S ? (u8)exec_kind_of(L.root, L.prefix, L.flags, L.nops, ops + L.op_start, &m)
+                                   : (u8)XK_NONE;
+        I.xmask = m;
+        ins[ni++] = I;
+        pend_b = nkl;
         last_line = I.line;
-        classify_exec(K, I);
     }
+    K.nins = ni;
+    K.nkl = nkl;
     K.nins_real = K.nins;
     if (K.nkl > pend_b) {
         Ins &I = K.ins[K.nins++];
@@ -1763,7 +1767,7 @@ OD_NOINL void reduce(KCtx &K) {
 // earlier instruction of the block defined the register; an instruction's
 // own defs are buffered and committed after it (use before def).
 struct LvSink {
-    u32 *U, *D;
+    u32 U[kLiveWords], D[kLiveWords]; // the block's gen / kill, accumulated locally
     u32 dd[kLiveWords];
     u32 touched;
 };
@@ -1908,24 +1912,29 @@ OD_NOINL bool liveness(KCtx &K) {
     for (u32 w = 0; w < kLiveWords; ++w)
         S.dd[w] = 0;
     S.touched = 0;
+    const Block *__restrict__ blk = K.blk;
+    const Ins *__restrict__ ins = K.ins;
+    const u8 *__restrict__ supp = K.supp;
+    u32 *__restrict__ live_in = K.live_in;
     for (u32 b = 0; b < nb; ++b) {
-        u32 *U = use + b * kLiveWords, *D = def + b * kLiveWords;
         for (u32 w = 0; w < kLiveWords; ++w) {
-            U[w] = 0;
-            D[w] = 0;
-            K.live_in[b * kLiveWords + w] = 0;
+            S.U[w] = 0;
+            S.D[w] = 0;
         }
-        S.U = U;
-        S.D = D;
-        const Block &B = K.blk[b];
-        for (u32 i = B.ib; i < B.ie; ++i) {
-            if (K.supp[i])
+        const u32 ib = blk[b].ib, ie = blk[b].ie;
+        for (u32 i = ib; i < ie; ++i) {
+            if (supp[i])
                 continue;
-            instruction_use_def(K, K.ins[i], S);
+            instruction_use_def(K, ins[i], S);
             lv_commit(S);
         }
-        for (u32 w = 0; w < kLiveWords; ++w)
-            any[w] |= U[w];
+        u32 *U = use + b * kLiveWords, *D = def + b * kLiveWords, *L = live_in + b * kLiveWords;
+        for (u32 w = 0; w < kLiveWords; ++w) {
+            U[w] = S.U[w];
+            D[w] = S.D[w];
+            L[w] = 0;
+            any[w] |= S.U[w];
+        }
     }
     // Only words holding some use bit can ever become live (live_in is a
     // subset of the union of the use sets), so the fixpoint runs over those.
@@ -1938,13 +1947,17 @@ OD_NOINL bool liveness(KCtx &K) {
     while (changed) {
         changed = false;
         for (u32 bi = nb; bi-- > 0;) {
-            const Block &B = K.blk[bi];
-            u32 *L = K.live_in + bi * kLiveWords;
+            const Block &B = blk[bi];
+            const u32 ns = B.nsucc;
+            const u32 s0 = ns > 0 ? (u32)B.succ[0] : 0, s1 = ns > 1 ? (u32)B.succ[1] : 0;
+            u32 *L = live_in + bi * kLiveWords;
             for (u32 k = 0; k < nw; ++k) {
                 const u32 w = wl[k];
                 u32 out = 0;
-                for (u32 s = 0; s < B.nsucc; ++s)
-                    out |= K.live_in[(u32)B.succ[s] * kLiveWords + w];
+                if (ns > 0)
+                    out |= live_in[s0 * kLiveWords + w];
+                if (ns > 1)
+                    out |= live_in[s1 * kLiveWords + w];
                 u32 in = use[bi * kLiveWords + w] | (out & ~def[bi * kLiveWords + w]);
                 if (in != L[w]) {
                     L[w] = in;

@@ -1220,7 +1220,7 @@ OD_INL void put_block_label(KCtx &K, Writer &w, u32 b) {
         const Label &L = klabel(K, B.lab_b);
         w.putn(K.in->t + L.off, L.len);
     } else {
-        w.puts("bb");
+        w.lit("bb");
         w.put_u64(b);
     }
 }
@@ -1233,9 +1233,9 @@ OD_NOINL void emit_simple(KCtx &K, Writer &w, const Stmt &s, u32 depth) {
     case SK_ASSIGN:
         w.spaces(depth * 4);
         put_var_name(w, s.cls, s.a);
-        w.puts(" = ");
+        w.lit(" = ");
         render_expr(w, rc, s.b, 0);
-        w.puts(";\n");
+        w.lit(";\n");
         break;
     case SK_DECL:
         w.spaces(depth * 4);
@@ -1243,16 +1243,16 @@ OD_NOINL void emit_simple(KCtx &K, Writer &w, const Stmt &s, u32 depth) {
         w.put(' ');
         put_var_name(w, s.cls, s.a);
         if (s.b) {
-            w.puts(" = ");
+            w.lit(" = ");
             render_expr(w, rc, s.b, 0);
         }
-        w.puts(";\n");
+        w.lit(";\n");
         break;
     case SK_STORE: {
         w.spaces(depth * 4);
         u32 target = K.E.deref(s.a, s.c, AS_GLOBAL);
         render_expr(w, rc, target, 0);
-        w.puts(" = ");
+        w.lit(" = ");
         u32 v = s.b;
         if (v && is_bit_reinterpret(K.E.n[v].type, s.c)) {
             w.puts(cast_name(s.c));
@@ -1262,12 +1262,12 @@ OD_NOINL void emit_simple(KCtx &K, Writer &w, const Stmt &s, u32 depth) {
         } else {
             render_expr(w, rc, v, 0);
         }
-        w.puts(";\n");
+        w.lit(";\n");
         break;
     }
     case SK_RAW: {
         w.spaces(depth * 4);
-        w.puts("__asm volatile (\"");
+        w.lit("__asm volatile (\"");
         const u8 *p = K.in->t + s.a;
         u32 b = 0, e = s.b;
         while (b < e && (p[b] == ' ' || p[b] == '\t'))
@@ -1275,24 +1275,24 @@ OD_NOINL void emit_simple(KCtx &K, Writer &w, const Stmt &s, u32 depth) {
         while (e > b && (p[e - 1] == ' ' || p[e - 1] == '\t'))
             --e;
         w.putn(p + b, e - b);
-        w.puts("\");\n");
+        w.lit("\");\n");
         break;
     }
     case SK_LABEL:
         put_block_label(K, w, s.a);
-        w.puts(":;\n");
+        w.lit(":;\n");
         break;
     case SK_GOTO:
         w.spaces(depth * 4);
         if (s.a) {
-            w.puts("if (");
+            w.lit("if (");
             render_expr(w, rc, s.a, 0);
-            w.puts(") goto ");
+            w.lit(") goto ");
         } else {
-            w.puts("goto ");
+            w.lit("goto ");
         }
         put_block_label(K, w, s.c);
-        w.puts(";\n");
+        w.lit(";\n");
         break;
     default: break;
     }
@@ -1323,11 +1323,11 @@ OD_NOINL void emit_list(KCtx &K, Writer &w, u32 head, u32 depth, u32 *stk, u32 s
         }
         if (e[2] == 0) {
             w.spaces(dp * 4);
-            w.puts("if (");
+            w.lit("if (");
             u32 mark = K.E.top;
             render_expr(w, K.rc, S.a, 0);
             K.E.top = mark;
-            w.puts(") {\n");
+            w.lit(") {\n");
             e[2] = 1;
             if (3 * (sp + 1) > stk_cap) {
                 K.oom = true;
@@ -1342,7 +1342,7 @@ OD_NOINL void emit_list(KCtx &K, Writer &w, u32 head, u32 depth, u32 *stk, u32 s
         }
         if (e[2] == 1 && S.c) {
             w.spaces(dp * 4);
-            w.puts("} else {\n");
+            w.lit("} else {\n");
             e[2] = 2;
             if (3 * (sp + 1) > stk_cap) {
                 K.oom = true;
@@ -1356,7 +1356,7 @@ OD_NOINL void emit_list(KCtx &K, Writer &w, u32 head, u32 depth, u32 *stk, u32 s
             continue;
         }
         w.spaces(dp * 4);
-        w.puts("}\n");
+        w.lit("}\n");
         e[0] = S.next;
         e[2] = 0;
     }
@@ -1658,7 +1658,7 @@ OD_NOINL void dk_emit(KState &S) {
     long long tp = OD_CLK();
     K.rc.fs = K.fs;
     const u8 *t = in.t;
-    w.puts("__kernel void ");
+    w.lit("__kernel void ");
     w.putn(t + K.cfg.name.off, K.cfg.name.len);
     w.put('(');
     bool first = true;
@@ -1667,17 +1667,17 @@ OD_NOINL void dk_emit(KState &S) {
         if (a.implicit)
             continue;
         if (!first)
-            w.puts(", ");
+            w.lit(", ");
         first = false;
         render_type(w, a.type);
         if (!type_ends_star(a.type))
             w.put(' ');
         w.putn(t + a.name.off, a.name.len);
     }
-    w.puts(") {\n");
+    w.lit(") {\n");
     emit_list(K, w, K.lists[S.hoist].head, 1, S.estk, S.ecap);
     emit_list(K, w, K.lists[S.body].head, 1, S.estk, S.ecap);
-    w.puts("}\n");
+    w.lit("}\n");
     S.done = 1;
     if (K.oom || K.E.oom || K.rc.ts.oom || w.overflow || K.rc.fs.terms.oom || K.rc.fs.st.oom) {
         out.status = KS_OOM;

@@ -236,7 +236,7 @@ OD_INL void render_scalar_type(Writer &w, DT t) {
     if (base == B_BINARY || base == B_UNKNOWN)
         base = B_UNSIGNED;
     switch (base) {
-    case B_VOID: w.puts("void"); return;
+    case B_VOID: w.lit("void"); return;
     case B_FLOAT: w.puts(bits == 64 ? "double" : "float"); return;
     case B_SIGNED:
         w.puts(bits == 8 ? "char" : bits == 16 ? "short" : bits == 64 ? "long" : "int");
@@ -249,10 +249,10 @@ OD_INL void render_scalar_type(Writer &w, DT t) {
 
 OD_INL void render_space_prefix(Writer &w, u32 space) {
     switch (space) {
-    case AS_GLOBAL: w.puts("__global "); break;
-    case AS_LOCAL: w.puts("__local "); break;
-    case AS_CONSTANT: w.puts("__constant "); break;
-    case AS_PRIVATE: w.puts("__private "); break;
+    case AS_GLOBAL: w.lit("__global "); break;
+    case AS_LOCAL: w.lit("__local "); break;
+    case AS_CONSTANT: w.lit("__constant "); break;
+    case AS_PRIVATE: w.lit("__private "); break;
     default: break;
     }
 }
@@ -304,13 +304,13 @@ OD_INL void put_reg_name(Writer &w, u32 cls) {
         w.put('v');
         w.put_u64(cls - 104);
     } else if (cls == 360) {
-        w.puts("exec");
+        w.lit("exec");
     } else if (cls == 361) {
-        w.puts("vcc");
+        w.lit("vcc");
     } else if (cls == 362) {
-        w.puts("scc");
+        w.lit("scc");
     } else {
-        w.puts("m0");
+        w.lit("m0");
     }
 }
 
@@ -330,12 +330,12 @@ OD_NOINL void render_const(Writer &w, const EArena &E, u32 e) {
         memcpy(&f, &bits, 4);
         if (isfinite(f) && f == floorf(f) && fabsf(f) < 1e6f) {
             w.put_i64((long long)f);
-            w.puts(".0f");
+            w.lit(".0f");
             return;
         }
-        w.puts("as_float(0x");
+        w.lit("as_float(0x");
         w.put_hex(bits);
-        w.puts("u)");
+        w.lit("u)");
         return;
     }
     if (dt_is_signed(t) && dt_bits(t) == 32 && (v >> 31) == 1) {
@@ -345,11 +345,11 @@ OD_NOINL void render_const(Writer &w, const EArena &E, u32 e) {
     if (v < 4096) {
         w.put_u64(v);
     } else {
-        w.puts("0x");
+        w.lit("0x");
         w.put_hex(v);
     }
     if (dt_bits(t) == 64 && v > 0xffffffffull)
-        w.puts("ul");
+        w.lit("ul");
 }
 
 enum { kPrimary = 16, kUnary = 14 };
@@ -562,15 +562,15 @@ OD_NOINL bool render_indexed(Writer &w, RenderCtx &rc, u32 addr, DT elem) {
 OD_NOINL void render_deref(Writer &w, RenderCtx &rc, u32 addr, DT elem) {
     if (render_indexed(w, rc, addr, elem))
         return;
-    w.puts("*((");
+    w.lit("*((");
     switch (dt_space(elem)) {
-    case AS_GLOBAL: w.puts("__global "); break;
-    case AS_LOCAL: w.puts("__local "); break;
-    case AS_CONSTANT: w.puts("__constant "); break;
+    case AS_GLOBAL: w.lit("__global "); break;
+    case AS_LOCAL: w.lit("__local "); break;
+    case AS_CONSTANT: w.lit("__constant "); break;
     default: break;
     }
     render_type(w, dt_with_space(elem, AS_NONE));
-    w.puts(" *)");
+    w.lit(" *)");
     rc.ts.push(RT_CHAR, ')', 0);
     rc.ts.push(RT_NODE, kUnary, addr);
 }
@@ -621,7 +621,7 @@ OD_NOINL void render_expr(Writer &w, RenderCtx &rc, u32 root, int min_prec = 0) 
         // RT_NODE
         int mp = (int)arg;
         if (!e) {
-            w.puts("0 /* missing */");
+            w.lit("0 /* missing */");
             continue;
         }
         const ENode x = E.n[e];
@@ -636,7 +636,7 @@ OD_NOINL void render_expr(Writer &w, RenderCtx &rc, u32 root, int min_prec = 0) 
             break;
         case E_ARG: put_arg_name(w, rc, x.a); break;
         case E_VAR: put_var_name(w, x.x, x.a); break;
-        case E_KBASE: w.puts("__settings_base"); break;
+        case E_KBASE: w.lit("__settings_base"); break;
         case E_UNARY:
             switch (x.op) {
             case U_LNOT:
@@ -652,11 +652,11 @@ OD_NOINL void render_expr(Writer &w, RenderCtx &rc, u32 root, int min_prec = 0) 
                 ts.push(RT_NODE, kUnary, x.a);
                 break;
             case U_LO32:
-                w.puts("(uint)");
+                w.lit("(uint)");
                 ts.push(RT_NODE, kUnary, x.a);
                 break;
             case U_HI32:
-                w.puts("(uint)(");
+                w.lit("(uint)(");
                 ts.push(RT_STR, S_SHR32, 0);
                 ts.push(RT_NODE, 11, x.a);
                 break;
@@ -677,7 +677,7 @@ OD_NOINL void render_expr(Writer &w, RenderCtx &rc, u32 root, int min_prec = 0) 
             break;
         case E_BINARY: {
             if (x.op == O_MULHI || x.op == O_MULHIS) {
-                w.puts("mul_hi(");
+                w.lit("mul_hi(");
                 ts.push(RT_CHAR, ')', 0);
                 ts.push(RT_SA, x.op, x.b);
                 ts.push(RT_STR, S_COMMA, 0);
@@ -685,7 +685,7 @@ OD_NOINL void render_expr(Writer &w, RenderCtx &rc, u32 root, int min_prec = 0) 
                 break;
             }
             if (x.op == O_CONCAT64) {
-                w.puts("upsample(");
+                w.lit("upsample(");
                 ts.push(RT_CHAR, ')', 0);
                 ts.push(RT_NODE, 0, x.a);
                 ts.push(RT_STR, S_COMMA, 0);

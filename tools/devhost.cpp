@@ -139,6 +139,9 @@ int main(int argc, char **argv) {
         const KSize z = kernel_size(lines.data(), lins.data(), ops.data(), kin.lbeg, kin.lend);
         for (kin.scale = 1;; kin.scale *= 4) {
             kin.nblk_cap = kin.scale <= 1 ? z.nb : 0;
+            kin.ncfg = z.ncfg;
+            kin.nins = z.nins;
+            kin.nlab = z.nlab;
             u64 cap = arena_budget(z, kin.scale);
             arena.assign(cap, 0);
             Bump mem{arena.data(), 0, cap, false};
