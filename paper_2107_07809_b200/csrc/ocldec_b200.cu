@@ -512,6 +512,17 @@ __global__ void k_scatter(const u32 *key, u32 nk, u32 *cursor, u32 *order, const
     sbudget[pos] = budget[k];
 }
 
+// Interleaves the size-sorted order (even positions first, then odd), so
+// contiguous waves get the same mix of kernel sizes.
+__global__ void k_interleave(const u32 *order, const u64 *sb, u32 n, u32 *order_out, u64 *sb_out) {
+    u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n)
+        return;
+    const u32 p = (i & 1) ? (n + 1) / 2 + i / 2 : i / 2;
+    order_out[p] = order[i];
+    sb_out[p] = sb[i];
+}
+
 // ------------------------------------------------------------------ P4b
 struct OutLenLoad {
     const KRes *res;
@@ -649,6 +660,7 @@ struct ocldec_b200_session {
     int device = 0;
     int nsm = 148;
     cudaStream_t stream = nullptr;
+    cudaStream_t stream2 = nullptr; // second decompile-wave stream
     size_t arena_bytes = 0;
     DevBuf text, tiles, tiles_off, nlpos, lines, lins, ops_cnt, labs_cnt, ops_off, labs_off, ops,
         labs, kstart, scan_tmp, scan_tot, counters, arena, stage, res, outoff, out, only, retry,
@@ -887,6 +899,12 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
         return -3;
     k_scatter<<<kg, kb, 0, st>>>(key, nk, P<u32>(s->hist), P<u32>(s->order), P<u64>(s->budget),
                                  P<u64>(s->sbudget));
+    if (nk >= 1024 && s->stream2) {
+        k_interleave<<<kg, kb, 0, st>>>(P<u32>(s->order), P<u64>(s->sbudget), nk, key, P<u64>(s->budget));
+        CK(cudaMemcpyAsync(s->order.p, key, (u64)nk * 4, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(s->sbudget.p, s->budget.p, (u64)nk * 8, cudaMemcpyDeviceToDevice, st));
+        s->stats.total_launches++;
+    }
     CK(cudaMemsetAsync(P<u64>(s->sbudget) + nk, 0, 8, st));
     if (scan_exclusive(s, nk + 1, U64Val{0}, AddU64{}, U64Load{P<u64>(s->sbudget)},
                        U64Store{P<u64>(s->boff)}, reinterpret_cast<U64Val *>(P<u64>(s->budget) + nk)))
@@ -896,15 +914,30 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     if (d2h_sync(s, boff.data(), s->boff.p, (u64)(nk + 1) * 8))
         return -3;
     // waves: as many size-sorted kernels as the arena pool holds
+    // Waves of size-sorted kernels, each as many as its arena region holds.
+    // Large launches alternate between two streams (each with half of the
+    // arena), so one wave's phase tails overlap the other wave's bulk.
     auto launch_waves = [&](const u64 *h_boff, const u32 *d_order, const u64 *d_boff, u32 count,
                             u32 scale) -> int {
-        u32 w0 = 0;
+        if (!count)
+            return 0;
+        const u64 total = h_boff[count] - h_boff[0];
+        u64 maxneed = 0;
+        for (u32 i = 0; i < count; ++i)
+            maxneed = std::max<u64>(maxneed, h_boff[i + 1] - h_boff[i]);
+        const bool two = count >= 1024 && s->stream2;
+        if (ensure(s->arena, std::max<u64>(two ? 2 * maxneed + 512 : maxneed, std::min<u64>(s->pool_bytes, total))))
+            return -3;
+        const u64 half = (s->arena.cap / 2) & ~255ull;
+        u64 cap = s->arena.cap;
+        if (two)
+            cap = std::min<u64>(half, std::max<u64>(maxneed, (total + 1) / 2 + maxneed / 2));
+        if (two) {
+            CK(cudaEventRecord(s->ev[7], st));
+            CK(cudaStreamWaitEvent(s->stream2, s->ev[7], 0));
+        }
+        u32 w0 = 0, wi = 0;
         while (w0 < count) {
-            u64 need1 = h_boff[w0 + 1] - h_boff[w0];
-            if (ensure(s->arena, std::max<u64>(need1, std::min<u64>(s->pool_bytes, h_boff[count] - h_boff[w0]))))
-                return -3;
-            u64 cap = s->arena.cap;
-            u32 w1 = w0 + 1;
             // largest w1 with boff[w1] - boff[w0] <= cap
             u32 lo = w0 + 1, hi = count;
             while (lo < hi) {
@@ -914,34 +947,41 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
                 else
                     hi = mid - 1;
             }
-            w1 = lo;
+            const u32 w1 = lo;
+            const bool second = two && (wi & 1);
+            cudaStream_t ws = second ? s->stream2 : st;
             a.order = d_order + w0;
             a.boff = d_boff + w0;
             a.boff0 = h_boff[w0];
             a.count = w1 - w0;
             a.scale = scale;
-            a.arena = P<u8>(s->arena);
+            a.arena = P<u8>(s->arena) + (second ? half : 0);
             auto grid = [&](u32 lp) { return (u32)(((u64)a.count * lp + 127) / 128); };
             cudaEvent_t pe[5];
             for (auto &e : pe)
                 if (phase_event(s, &e))
                     return -3;
-            CK(cudaEventRecord(pe[0], st));
+            CK(cudaEventRecord(pe[0], ws));
             a.lanes_per = s->lanes_front;
-            k_front<<<grid(a.lanes_per), 128, s->smem_front, st>>>(a);
-            CK(cudaEventRecord(pe[1], st));
+            k_front<<<grid(a.lanes_per), 128, s->smem_front, ws>>>(a);
+            CK(cudaEventRecord(pe[1], ws));
             a.lanes_per = s->lanes_lower;
-            k_lower<<<grid(a.lanes_per), 128, s->smem_lower, st>>>(a);
-            CK(cudaEventRecord(pe[2], st));
-            k_fold<<<grid(a.lanes_per), 128, s->smem_lower, st>>>(a);
-            CK(cudaEventRecord(pe[3], st));
+            k_lower<<<grid(a.lanes_per), 128, s->smem_lower, ws>>>(a);
+            CK(cudaEventRecord(pe[2], ws));
+            k_fold<<<grid(a.lanes_per), 128, s->smem_lower, ws>>>(a);
+            CK(cudaEventRecord(pe[3], ws));
             a.lanes_per = s->lanes_emit;
-            k_emit<<<grid(a.lanes_per), 128, s->smem_emit, st>>>(a);
-            CK(cudaEventRecord(pe[4], st));
+            k_emit<<<grid(a.lanes_per), 128, s->smem_emit, ws>>>(a);
+            CK(cudaEventRecord(pe[4], ws));
             s->stats.decompile_launches += 4;
             s->stats.total_launches += 4;
             CK(cudaGetLastError());
             w0 = w1;
+            ++wi;
+        }
+        if (two) {
+            CK(cudaEventRecord(s->ev[7], s->stream2));
+            CK(cudaStreamWaitEvent(st, s->ev[7], 0));
         }
         return 0;
     };
@@ -1061,6 +1101,13 @@ int session_init(ocldec_b200_session *s, int device, size_t arena_bytes) {
     CK(cudaGetDeviceProperties(&prop, device));
     s->nsm = prop.multiProcessorCount;
     CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    {
+        // Opt-in: overlapping waves mixes phase code on the SMs, which costs
+        // more instruction-cache misses than it hides tails (measured).
+        const char *ts = getenv("OCLDEC_B200_TWO_STREAMS");
+        if (ts && *ts == '1')
+            CK(cudaStreamCreateWithFlags(&s->stream2, cudaStreamNonBlocking));
+    }
     for (auto &e : s->ev)
         CK(cudaEventCreate(&e));
     // arena pool for one decompile wave (per-kernel slices sized by arena_budget)
@@ -1283,6 +1330,8 @@ void ocldec_b200_session_destroy(ocldec_b200_session *s) {
         cudaEventDestroy(e);
     if (s->stream)
         cudaStreamDestroy(s->stream);
+    if (s->stream2)
+        cudaStreamDestroy(s->stream2);
     delete s;
 }
 
