@@ -328,10 +328,12 @@ OD_INL void name_set_clear(NameSet &ns) {
 struct Step {
     KCtx &K;
     const Ins &I;
-    u32 out; // statement list
+    u32 out;        // statement list
+    const Opnd *o;  // the instruction's operands (K.in->ops + I.op_start)
+    u32 nn_;        // operand count (0 for the synthetic s_endpgm)
 
-    OD_INL const Opnd &op(u32 k) const { return op_at(K, I, k); }
-    OD_INL u32 n() const { return (I.flags & IF_SYNTH) ? 0 : I.nops; }
+    OD_INL const Opnd &op(u32 k) const { return o[k]; }
+    OD_INL u32 n() const { return nn_; }
     OD_INL u32 read(const Opnd &o) { return read_operand(K, o); }
     OD_INL u32 read64(const Opnd &o) { return read_pair(K, o); }
     OD_INL DT ty(u32 e) const { return K.E.n[e].type; }
@@ -861,7 +863,8 @@ OD_NOINL void lower_block(KCtx &K, u32 b, u32 out) {
     for (u32 i = B.ib; i < B.ie && !K.oom && !K.E.oom; ++i) {
         if (K.supp[i])
             continue;
-        Step s{K, K.ins[i], out};
+        const Ins &I = K.ins[i];
+        Step s{K, I, out, K.in->ops + I.op_start, (I.flags & IF_SYNTH) ? 0u : (u32)I.nops};
         s.run();
     }
 }
