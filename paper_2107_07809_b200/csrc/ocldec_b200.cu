@@ -308,6 +308,17 @@ __device__ __forceinline__ bool dk_slot(const DecompArgs &a, Slot0 *o) {
     return true;
 }
 
+// 1: a phase kernel runs on a local-memory copy of the KState; 0: in place in
+// HBM (measured per phase: lowering is faster in place, the others on the copy;
+// local memory interleaves words across the 32 lanes, so a lone active lane
+// spreads its state over 32x the L1 lines).
+#ifndef OD_LOCAL_STATE
+#define OD_LOCAL_STATE 1
+#endif
+#ifndef OD_LOCAL_LOWER
+#define OD_LOCAL_LOWER 0
+#endif
+
 // Minimum resident blocks per SM for the phase kernels (register caps).
 #ifndef OD_MINB_FRONT
 #define OD_MINB_FRONT 10
@@ -396,10 +407,14 @@ __global__ void __launch_bounds__(128, OD_MINB_FRONT) k_front(DecompArgs a) {
                k, g, g->K.in, &g->in, g->in.t, g->in.lines, g->in.lbeg, g->in.lend, g->mem.base,
                (unsigned long long)g->mem.cap);
 #endif
+#if OD_LOCAL_STATE
         KState S;
         kstate_load(S, g);
         dk_front(S);
         kstate_store(g, S);
+#else
+        dk_front(*g);
+#endif
     }
 }
 
@@ -410,10 +425,14 @@ __global__ void __launch_bounds__(128, OD_MINB_LOWER) k_lower(DecompArgs a) {
     KState *g = reinterpret_cast<KState *>(sl.base);
     if (g->done)
         return;
+#if OD_LOCAL_LOWER
     KState S;
     kstate_load(S, g);
     dk_lower(S);
     kstate_store(g, S);
+#else
+    dk_lower(*g);
+#endif
 }
 
 __global__ void __launch_bounds__(128, OD_MINB_FOLD) k_fold(DecompArgs a) {
@@ -423,10 +442,14 @@ __global__ void __launch_bounds__(128, OD_MINB_FOLD) k_fold(DecompArgs a) {
     KState *g = reinterpret_cast<KState *>(sl.base);
     if (g->done)
         return;
+#if OD_LOCAL_STATE
     KState S;
     kstate_load(S, g);
     dk_fold(S);
     kstate_store(g, S);
+#else
+    dk_fold(*g);
+#endif
 }
 
 __global__ void __launch_bounds__(128, OD_MINB_EMIT) k_emit(DecompArgs a) {
@@ -437,11 +460,17 @@ __global__ void __launch_bounds__(128, OD_MINB_EMIT) k_emit(DecompArgs a) {
     KOut o;
     const u8 *src = nullptr;
     if (!g->done) {
+#if OD_LOCAL_STATE
         KState S;
         kstate_load(S, g);
         dk_emit(S);
         o = S.out;
         src = S.w.p;
+#else
+        dk_emit(*g);
+        o = g->out;
+        src = g->w.p;
+#endif
     } else {
         o = g->out;
     }
