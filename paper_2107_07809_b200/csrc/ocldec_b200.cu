@@ -234,9 +234,10 @@ __global__ void k_decode(const u8 *__restrict__ t, u32 nlines, const LineRec *__
     }
     LineIns li;
     if (mode == 0) {
-        decode_line(t, Span{L.off, L.len}, &rt, &li, nullptr, 0, nullptr);
-        ops_cnt[l] = li.nops;
-        labs_cnt[l] = li.nlabels;
+        u32 no, nl;
+        count_line(t, Span{L.off, L.len}, &no, &nl);
+        ops_cnt[l] = no;
+        labs_cnt[l] = nl;
     } else {
         u32 oo = ops_off[l], lo = labs_off[l];
         const u32 cap = (l + 1 < nlines ? ops_off[l + 1] : 0xffffffffu) - oo;
@@ -413,6 +414,7 @@ __global__ void __launch_bounds__(128, OD_MINB_FRONT) k_front(DecompArgs a) {
         dk_front(S);
         kstate_store(g, S);
 #else
+        kstate_fix(*g);
         dk_front(*g);
 #endif
     }
@@ -431,6 +433,7 @@ __global__ void __launch_bounds__(128, OD_MINB_LOWER) k_lower(DecompArgs a) {
     dk_lower(S);
     kstate_store(g, S);
 #else
+    kstate_fix(*g); // the previous phase ran on a local copy: re-point into HBM
     dk_lower(*g);
 #endif
 }
@@ -448,6 +451,7 @@ __global__ void __launch_bounds__(128, OD_MINB_FOLD) k_fold(DecompArgs a) {
     dk_fold(S);
     kstate_store(g, S);
 #else
+    kstate_fix(*g);
     dk_fold(*g);
 #endif
 }
@@ -467,6 +471,7 @@ __global__ void __launch_bounds__(128, OD_MINB_EMIT) k_emit(DecompArgs a) {
         o = S.out;
         src = S.w.p;
 #else
+        kstate_fix(*g);
         dk_emit(*g);
         o = g->out;
         src = g->w.p;

@@ -163,3 +163,29 @@ def test_empty_and_preamble_only():
     assert P.decompile_listing("").kernels == []
     r = P.decompile_listing(".amdcl2\n.gpu Fiji\n")
     assert r.kernels == [] and r.combined == b"" and r.diagnostics == []
+
+
+@pytest.mark.skipif(not O.available(), reason="oracle not built")
+def test_larger_c4_sample_vs_oracle():
+    """A 1,500-kernel C4 sample (both size classes, straight and branching,
+    stress syntax) in one listing: one decompile wave with the size-sorted
+    interleaving, compared byte for byte with the reference."""
+    listing, offs, ni = P.generate_corpus("C4", 1500, seed=0x210707809C4 + 1, stress=True)
+    res = P.decompile_listing(listing)
+    ref = O.decompile(listing)
+    assert res.combined == ref.combined
+    assert [(k.failed, k.structured, k.fallback_count) for k in res.kernels] == \
+           [(k.failed, k.structured, k.fallback_count) for k in ref.kernels]
+
+
+@pytest.mark.skipif(not O.available(), reason="oracle not built")
+def test_host_chunking_vs_oracle(monkeypatch):
+    """The host path cuts the listing into chunks at .kernel lines
+    (OCLDEC_B200_CHUNK_BYTES); every chunk runs all phases, the state of a
+    kernel moves between phase launches, and the combined output must not
+    change."""
+    listing, offs, _ = P.generate_corpus("C3", 1200, seed=91, stress=True)
+    ref = O.decompile(listing).combined
+    monkeypatch.setenv("OCLDEC_B200_CHUNK_BYTES", str(len(listing) // 7))
+    res = P.decompile_listing(listing, P.DecompileOptions(arena_bytes=(96 << 20) + 4096))
+    assert res.combined == ref
