@@ -214,14 +214,46 @@ __global__ void k_init_roots() {
 }
 
 // mode 0: sizing (writes per-line operand/label counts); mode 1: fill.
-__global__ void k_decode(const u8 *__restrict__ t, u32 nlines, const LineRec *__restrict__ lines,
-                         LineIns *lins, u32 *ops_cnt, u32 *labs_cnt, const u32 *ops_off,
-                         const u32 *labs_off, Opnd *ops, Label *labs, int mode) {
+// The block's 256 lines are one contiguous span of the listing: it is staged
+// in shared memory (16-byte vector loads for the aligned interior) and every
+// thread decodes its line from there.  Lines whose content lives in the aux
+// area (comment-stripped copies) and oversized spans read the listing in HBM.
+constexpr u32 kDecodeStage = 16384;
+
+__global__ void __launch_bounds__(256) k_decode(const u8 *__restrict__ t, u64 len, const u32 *__restrict__ nlpos,
+                                                u32 nlf, u32 nlines, const LineRec *__restrict__ lines,
+                                                LineIns *lins, u32 *ops_cnt, u32 *labs_cnt, const u32 *ops_off,
+                                                const u32 *labs_off, Opnd *ops, Label *labs, int mode) {
     __shared__ RootTable rt;
+    __shared__ __align__(16) u8 stage[kDecodeStage];
     for (u32 i = threadIdx.x; i < sizeof(RootTable) / 4; i += blockDim.x)
         reinterpret_cast<u32 *>(&rt)[i] = reinterpret_cast<const u32 *>(&d_roots)[i];
+    // raw span of the block's lines
+    const u32 l0 = blockIdx.x * blockDim.x;
+    const u32 l1 = min(l0 + blockDim.x, nlines);
+    const u64 sb = l0 == 0 ? 0 : (u64)nlpos[l0 - 1] + 1;
+    const u64 se = l1 - 1 < nlf ? (u64)nlpos[l1 - 1] : len;
+    // stage [ab, se): ab = sb rounded down to a 16-byte boundary of the
+    // listing (never before the chunk start: the first block of a misaligned
+    // chunk stages bytewise)
+    const u32 lead = (u32)((uintptr_t)(t + sb) & 15);
+    const bool vec = sb >= lead;
+    const u64 ab = vec ? sb - lead : sb;
+    const bool staged = se - ab <= kDecodeStage;
+    if (staged) {
+        u64 done = ab;
+        if (vec) {
+            const u64 nv = (se - ab) / 16;
+            const uint4 *src = reinterpret_cast<const uint4 *>(t + ab);
+            for (u64 q = threadIdx.x; q < nv; q += blockDim.x)
+                reinterpret_cast<uint4 *>(stage)[q] = src[q];
+            done = ab + 16 * nv;
+        }
+        for (u64 o = done + threadIdx.x; o < se; o += blockDim.x)
+            stage[o - ab] = t[o];
+    }
     __syncthreads();
-    u32 l = blockIdx.x * blockDim.x + threadIdx.x;
+    const u32 l = l0 + threadIdx.x;
     if (l >= nlines)
         return;
     const LineRec L = lines[l];
@@ -232,16 +264,19 @@ __global__ void k_decode(const u8 *__restrict__ t, u32 nlines, const LineRec *__
         }
         return;
     }
+    // the decoder addresses the listing by chunk offsets: tb[off] == t[off]
+    const bool in_stage = staged && !L.complex && L.off >= sb && (u64)L.off + L.len <= se;
+    const u8 *tb = in_stage ? stage - ab : t;
     LineIns li;
     if (mode == 0) {
         u32 no, nl;
-        count_line(t, Span{L.off, L.len}, &no, &nl);
+        count_line(tb, Span{L.off, L.len}, &no, &nl);
         ops_cnt[l] = no;
         labs_cnt[l] = nl;
     } else {
         u32 oo = ops_off[l], lo = labs_off[l];
         const u32 cap = (l + 1 < nlines ? ops_off[l + 1] : 0xffffffffu) - oo;
-        decode_line(t, Span{L.off, L.len}, &rt, &li, ops + oo, cap, labs + lo);
+        decode_line(tb, Span{L.off, L.len}, &rt, &li, ops + oo, cap, labs + lo);
         li.op_start = oo;
         li.lab_start = lo;
         lins[l] = li;
@@ -872,8 +907,8 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
         ensure(s->labs_cnt, (nlines + 1) * 4ull) || ensure(s->ops_off, (nlines + 1) * 4ull) ||
         ensure(s->labs_off, (nlines + 1) * 4ull))
         return -3;
-    k_decode<<<lg, lb, 0, st>>>(t, nlines, P<LineRec>(s->lines), P<LineIns>(s->lins), P<u32>(s->ops_cnt),
-                                P<u32>(s->labs_cnt), nullptr, nullptr, nullptr, nullptr, 0);
+    k_decode<<<lg, lb, 0, st>>>(t, len, P<u32>(s->nlpos), nlf, nlines, P<LineRec>(s->lines), P<LineIns>(s->lins),
+                                P<u32>(s->ops_cnt), P<u32>(s->labs_cnt), nullptr, nullptr, nullptr, nullptr, 0);
     s->stats.total_launches++;
     if (scan_exclusive(s, nlines, SU32{0}, AddU32{}, U32Load{P<u32>(s->ops_cnt)},
                        U32Store{P<u32>(s->ops_off)}, reinterpret_cast<SU32 *>(cnt + 8)) ||
@@ -885,8 +920,9 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
         return -3;
     if (ensure(s->ops, (pools[0] + 1ull) * sizeof(Opnd)) || ensure(s->labs, (pools[1] + 1ull) * sizeof(Label)))
         return -3;
-    k_decode<<<lg, lb, 0, st>>>(t, nlines, P<LineRec>(s->lines), P<LineIns>(s->lins), nullptr, nullptr,
-                                P<u32>(s->ops_off), P<u32>(s->labs_off), P<Opnd>(s->ops), P<Label>(s->labs), 1);
+    k_decode<<<lg, lb, 0, st>>>(t, len, P<u32>(s->nlpos), nlf, nlines, P<LineRec>(s->lines), P<LineIns>(s->lins),
+                                nullptr, nullptr, P<u32>(s->ops_off), P<u32>(s->labs_off), P<Opnd>(s->ops),
+                                P<Label>(s->labs), 1);
     s->stats.total_launches++;
     CK(cudaGetLastError());
     CK(cudaEventRecord(s->ev[2], st));
