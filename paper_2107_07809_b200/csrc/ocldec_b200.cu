@@ -26,8 +26,7 @@
 #include <vector>
 
 #include "../../include/ocldec_b200.h"
-#include "od_gen.cuh"
-#include "od_kernel.cuh"
+#include "od_device.cuh"
 #include "od_scan.cuh"
 
 using namespace od;
@@ -283,271 +282,6 @@ __global__ void __launch_bounds__(256) k_decode(const u8 *__restrict__ t, u64 le
     }
 }
 
-// ------------------------------------------------------------------ P2-P4a
-struct KRes {
-    u32 status;     // KStatus, KS_SKIP = 4 for only_kernel filtering, 5 = staging full
-    u32 structured;
-    u32 fallbacks;
-    u32 ninstr;
-    u64 stage_off;
-    u32 out_len;
-    u32 name_off;   // kernel name span (chunk-relative; >= chunk len: aux area)
-    u32 name_len;
-    u32 pad[3];
-};
-enum : u32 { KS_SKIP = 4, KS_STAGE_FULL = 5 };
-
-struct DecompArgs {
-    const u8 *t;
-    const LineRec *lines;
-    const LineIns *lins;
-    const Opnd *ops;
-    const Label *labs;
-    const u32 *kstart;
-    u32 nk, nlines, line_base, fold_local_size;
-    const u32 *order;   // kernels of this wave (size-sorted)
-    const u64 *boff;    // arena offsets (exclusive scan of budgets, per order slot)
-    u64 boff0;          // boff of the first slot of the wave
-    u32 count;          // kernels in the wave
-    u32 scale;
-    u8 *arena;
-    u8 *stage;
-    u64 stage_cap;
-    unsigned long long *stage_top;
-    KRes *res;
-    const u8 *only;  // only_kernel name (device) or null
-    u32 only_len;
-    u64 *prof;
-    u32 lanes_per; // lanes per kernel: 32 / kernels-per-warp
-    const KSize *sizes; // per kernel (k_ksize)
-};
-
-// Three launches per wave, one per pipeline phase (od_lower.cuh dk_front /
-// dk_lower / dk_emit): every warp on an SM runs the same phase's code.  kpw
-// kernels per warp (lane 0 of each 32/kpw-lane group works), kernels
-// size-sorted (largest first) so the block scheduler starts big kernels
-// first; each kernel gets an exact arena slice sized by kernel_budget(lines),
-// whose base holds its KState between the launches.
-struct Slot0 {
-    u32 k;
-    u8 *base;
-};
-__device__ __forceinline__ bool dk_slot(const DecompArgs &a, Slot0 *o) {
-    const u32 g = blockIdx.x * blockDim.x + threadIdx.x;
-    if ((threadIdx.x & 31) % a.lanes_per)
-        return false;
-    const u32 i = g / a.lanes_per;
-    if (i >= a.count)
-        return false;
-    o->k = a.order[i];
-    o->base = a.arena + (a.boff[i] - a.boff0);
-    return true;
-}
-
-// 1: a phase kernel runs on a local-memory copy of the KState; 0: in place in
-// HBM (measured per phase: lowering is faster in place, the others on the copy;
-// local memory interleaves words across the 32 lanes, so a lone active lane
-// spreads its state over 32x the L1 lines).
-#ifndef OD_LOCAL_STATE
-#define OD_LOCAL_STATE 1
-#endif
-#ifndef OD_LOCAL_LOWER
-#define OD_LOCAL_LOWER 0
-#endif
-
-// Minimum resident blocks per SM for the phase kernels (register caps).
-#ifndef OD_MINB_FRONT
-#define OD_MINB_FRONT 10
-#endif
-#ifndef OD_MINB_LOWER
-#define OD_MINB_LOWER 16
-#endif
-#ifndef OD_MINB_FOLD
-#define OD_MINB_FOLD 12
-#endif
-#ifndef OD_MINB_EMIT
-#define OD_MINB_EMIT 16
-#endif
-
-// The phase kernels run on a local (stack) copy of the KState: its hot
-// counters (arena tops, writer position, stack tops) then live in L1
-// write-back local memory instead of write-through global memory.  Copies
-// are word loops (an aggregate copy here was miscompiled by nvcc 12.9).
-__device__ __forceinline__ void kstate_load(KState &S, const KState *g) {
-    static_assert(sizeof(KState) % 8 == 0, "KState is copied in u64 words");
-    const u64 *src = reinterpret_cast<const u64 *>(g);
-    u64 *dst = reinterpret_cast<u64 *>(&S);
-    for (u32 q = 0; q < sizeof(KState) / 8; ++q)
-        dst[q] = src[q];
-    kstate_fix(S);
-}
-__device__ __forceinline__ void kstate_store(KState *g, const KState &S) {
-    const u64 *src = reinterpret_cast<const u64 *>(&S);
-    u64 *dst = reinterpret_cast<u64 *>(g);
-    for (u32 q = 0; q < sizeof(KState) / 8; ++q)
-        dst[q] = src[q];
-}
-
-__global__ void __launch_bounds__(128, OD_MINB_FRONT) k_front(DecompArgs a) {
-    Slot0 sl;
-    if (!dk_slot(a, &sl))
-        return;
-    const u32 k = sl.k;
-    const u32 i = (blockIdx.x * blockDim.x + threadIdx.x) / a.lanes_per;
-    KState *g = reinterpret_cast<KState *>(sl.base);
-    const u64 kb = (sizeof(KState) + 255) & ~255ull;
-    // Field-wise setup of the state in HBM.  (nvcc 12.9 miscompiled an
-    // aggregate copy of a locally built KIn here into a copy of the first
-    // bytes of the kernel parameters.)
-    static_assert(sizeof(KState) % 8 == 0, "KState is zeroed in u64 words");
-    for (u32 q = 0; q < sizeof(KState) / 8; ++q)
-        reinterpret_cast<u64 *>(g)[q] = 0;
-    KIn &in = g->in;
-    in.t = a.t;
-    in.lines = a.lines;
-    in.lins = a.lins;
-    in.ops = a.ops;
-    in.labs = a.labs;
-    in.lbeg = a.kstart[k];
-    in.lend = k + 1 < a.nk ? a.kstart[k + 1] : a.nlines;
-    in.line_base = a.line_base;
-    in.fold_local_size = a.fold_local_size;
-    in.scale = a.scale;
-    in.prof = a.prof;
-    {
-        const KSize z = a.sizes[k];
-        in.nblk_cap = a.scale <= 1 ? z.nb : 0;
-        in.ncfg = z.ncfg;
-        in.nins = z.nins;
-        in.nlab = z.nlab;
-    }
-    g->mem.base = sl.base + kb;
-    g->mem.top = 0;
-    g->mem.cap = a.boff[i + 1] - a.boff[i] - kb;
-    g->mem.oom = false;
-    g->out.status = KS_OK;
-    kstate_fix(*g);
-    Span nm;
-    {
-        Span w, rest, extra;
-        const LineRec &L = a.lines[in.lbeg];
-        split_word(a.t, Span{L.off, L.len}, &w, &rest);
-        split_word(a.t, rest, &nm, &extra);
-    }
-    if (a.only && (nm.len != a.only_len || !bytes_eq(a.t + nm.off, a.only, nm.len))) {
-        g->out.status = KS_SKIP;
-        g->done = 1;
-    } else {
-#ifdef OD_DEBUG_FRONT
-        printf("k=%u g=%p K.in=%p &g->in=%p g->in.t=%p g->in.lines=%p lbeg=%u lend=%u mem.base=%p cap=%llu\n",
-               k, g, g->K.in, &g->in, g->in.t, g->in.lines, g->in.lbeg, g->in.lend, g->mem.base,
-               (unsigned long long)g->mem.cap);
-#endif
-#if OD_LOCAL_STATE
-        KState S;
-        kstate_load(S, g);
-        dk_front(S);
-        kstate_store(g, S);
-#else
-        kstate_fix(*g);
-        dk_front(*g);
-#endif
-    }
-}
-
-__global__ void __launch_bounds__(128, OD_MINB_LOWER) k_lower(DecompArgs a) {
-    Slot0 sl;
-    if (!dk_slot(a, &sl))
-        return;
-    KState *g = reinterpret_cast<KState *>(sl.base);
-    if (g->done)
-        return;
-#if OD_LOCAL_LOWER
-    KState S;
-    kstate_load(S, g);
-    dk_lower(S);
-    kstate_store(g, S);
-#else
-    kstate_fix(*g); // the previous phase ran on a local copy: re-point into HBM
-    dk_lower(*g);
-#endif
-}
-
-__global__ void __launch_bounds__(128, OD_MINB_FOLD) k_fold(DecompArgs a) {
-    Slot0 sl;
-    if (!dk_slot(a, &sl))
-        return;
-    KState *g = reinterpret_cast<KState *>(sl.base);
-    if (g->done)
-        return;
-#if OD_LOCAL_STATE
-    KState S;
-    kstate_load(S, g);
-    dk_fold(S);
-    kstate_store(g, S);
-#else
-    kstate_fix(*g);
-    dk_fold(*g);
-#endif
-}
-
-__global__ void __launch_bounds__(128, OD_MINB_EMIT) k_emit(DecompArgs a) {
-    Slot0 sl;
-    if (!dk_slot(a, &sl))
-        return;
-    KState *g = reinterpret_cast<KState *>(sl.base);
-    KOut o;
-    const u8 *src = nullptr;
-    if (!g->done) {
-#if OD_LOCAL_STATE
-        KState S;
-        kstate_load(S, g);
-        dk_emit(S);
-        o = S.out;
-        src = S.w.p;
-#else
-        kstate_fix(*g);
-        dk_emit(*g);
-        o = g->out;
-        src = g->w.p;
-#endif
-    } else {
-        o = g->out;
-    }
-    const u32 k = sl.k;
-    KRes r;
-    r.pad[0] = r.pad[1] = r.pad[2] = 0;
-    r.stage_off = 0;
-    r.out_len = 0;
-    r.status = o.status;
-    r.structured = o.structured;
-    r.fallbacks = o.fallbacks;
-    r.ninstr = o.ninstr;
-    {
-        Span nm, w, rest, extra;
-        const LineRec &L = a.lines[a.kstart[k]];
-        split_word(a.t, Span{L.off, L.len}, &w, &rest);
-        split_word(a.t, rest, &nm, &extra);
-        r.name_off = nm.off;
-        r.name_len = nm.len;
-    }
-    if (o.status == KS_OK && o.out_len) {
-        u64 padded = (o.out_len + 15ull) & ~15ull;
-        u64 so = atomicAdd(a.stage_top, (unsigned long long)padded);
-        if (so + padded > a.stage_cap) {
-            r.status = KS_STAGE_FULL;
-        } else {
-            const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
-            uint4 *d4 = reinterpret_cast<uint4 *>(a.stage + so);
-            for (u64 q = 0; q < padded / 16; ++q)
-                d4[q] = s4[q];
-            r.stage_off = so;
-            r.out_len = o.out_len;
-        }
-    }
-    a.res[k] = r;
-}
-
 // Per-kernel sizes (a pass over the kernel's decoded lines), size key and
 // arena budget.
 __global__ void k_ksize(const u32 *kstart, u32 nk, u32 nlines, const LineRec *lines, const LineIns *lins,
@@ -622,38 +356,6 @@ __global__ void k_gather(const KRes *__restrict__ res, const u64 *__restrict__ o
         d[i] = s[i];
     if (lane == 0 && out_base + off[warp] + r.out_len < total)
         d[r.out_len] = '\n';
-}
-
-// ------------------------------------------------------------------ generator
-struct GenArgs {
-    GenCfg cfg;
-    u64 k0, count;
-    u64 *len;   // per kernel length (sizing) -> offsets after scan
-    u32 *ninstr;
-    u8 *buf;
-};
-
-__global__ void k_gen(GenArgs a, int mode) {
-    u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= a.count)
-        return;
-    Writer w;
-    if (mode == 0) {
-        w.p = nullptr;
-        w.n = 0;
-        w.cap = 0;
-        w.overflow = false;
-        u32 ni = gen_kernel(a.cfg, a.k0 + i, &w);
-        a.len[i] = w.n;
-        a.ninstr[i] = ni;
-    } else {
-        u64 off = a.len[i];
-        w.p = a.buf + off;
-        w.n = 0;
-        w.cap = 0xffffffffu;
-        w.overflow = false;
-        gen_kernel(a.cfg, a.k0 + i, &w);
-    }
 }
 
 struct U64Val {

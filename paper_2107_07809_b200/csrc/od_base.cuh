@@ -15,7 +15,14 @@
 #if defined(__CUDACC__)
 #define OD_HD __host__ __device__
 #define OD_INL __host__ __device__ inline
-#define OD_NOINL __host__ __device__ __noinline__
+#define OD_NOINL __host__ __device__ __noinline__ inline
+// Hot lowering helpers: out of line by default (instruction-cache size);
+// -DOD_HOT_INLINE=1 inlines them into their callers (locality experiment).
+#if defined(OD_HOT_INLINE) && OD_HOT_INLINE
+#define OD_HOT __host__ __device__ __forceinline__
+#else
+#define OD_HOT __host__ __device__ __noinline__ inline
+#endif
 #else
 #define OD_HD
 #define OD_INL inline
@@ -24,6 +31,7 @@
 #else
 #define OD_NOINL inline
 #endif
+#define OD_HOT OD_NOINL
 #define __host__
 #define __device__
 struct uint4 {

@@ -1,0 +1,137 @@
+// ocldec-b200: declarations shared by the translation units of the device
+// library (ocldec_b200.cu: host + parse kernels; od_front.cu: k_front;
+// od_phases.cu: k_lower/k_fold/k_emit; od_genk.cu: the corpus generator).
+// Separate units let each phase get its own ptxas options (Makefile).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "od_gen.cuh"
+#include "od_kernel.cuh"
+
+namespace od {
+
+// ------------------------------------------------------------------ P2-P4a (decompile phases)
+struct KRes {
+    u32 status;     // KStatus, KS_SKIP = 4 for only_kernel filtering, 5 = staging full
+    u32 structured;
+    u32 fallbacks;
+    u32 ninstr;
+    u64 stage_off;
+    u32 out_len;
+    u32 name_off;   // kernel name span (chunk-relative; >= chunk len: aux area)
+    u32 name_len;
+    u32 pad[3];
+};
+enum : u32 { KS_SKIP = 4, KS_STAGE_FULL = 5 };
+
+struct DecompArgs {
+    const u8 *t;
+    const LineRec *lines;
+    const LineIns *lins;
+    const Opnd *ops;
+    const Label *labs;
+    const u32 *kstart;
+    u32 nk, nlines, line_base, fold_local_size;
+    const u32 *order;   // kernels of this wave (size-sorted)
+    const u64 *boff;    // arena offsets (exclusive scan of budgets, per order slot)
+    u64 boff0;          // boff of the first slot of the wave
+    u32 count;          // kernels in the wave
+    u32 scale;
+    u8 *arena;
+    u8 *stage;
+    u64 stage_cap;
+    unsigned long long *stage_top;
+    KRes *res;
+    const u8 *only;  // only_kernel name (device) or null
+    u32 only_len;
+    u64 *prof;
+    u32 lanes_per; // lanes per kernel: 32 / kernels-per-warp
+    const KSize *sizes; // per kernel (k_ksize)
+};
+
+// Three launches per wave, one per pipeline phase (od_lower.cuh dk_front /
+// dk_lower / dk_emit): every warp on an SM runs the same phase's code.  kpw
+// kernels per warp (lane 0 of each 32/kpw-lane group works), kernels
+// size-sorted (largest first) so the block scheduler starts big kernels
+// first; each kernel gets an exact arena slice sized by kernel_budget(lines),
+// whose base holds its KState between the launches.
+struct Slot0 {
+    u32 k;
+    u8 *base;
+};
+__device__ __forceinline__ bool dk_slot(const DecompArgs &a, Slot0 *o) {
+    const u32 g = blockIdx.x * blockDim.x + threadIdx.x;
+    if ((threadIdx.x & 31) % a.lanes_per)
+        return false;
+    const u32 i = g / a.lanes_per;
+    if (i >= a.count)
+        return false;
+    o->k = a.order[i];
+    o->base = a.arena + (a.boff[i] - a.boff0);
+    return true;
+}
+
+// 1: a phase kernel runs on a local-memory copy of the KState; 0: in place in
+// HBM (measured per phase: lowering is faster in place, the others on the copy;
+// local memory interleaves words across the 32 lanes, so a lone active lane
+// spreads its state over 32x the L1 lines).
+#ifndef OD_LOCAL_STATE
+#define OD_LOCAL_STATE 1
+#endif
+#ifndef OD_LOCAL_LOWER
+#define OD_LOCAL_LOWER 0
+#endif
+
+// Minimum resident blocks per SM for the phase kernels (register caps).
+#ifndef OD_MINB_FRONT
+#define OD_MINB_FRONT 10
+#endif
+#ifndef OD_MINB_LOWER
+#define OD_MINB_LOWER 16
+#endif
+#ifndef OD_MINB_FOLD
+#define OD_MINB_FOLD 12
+#endif
+#ifndef OD_MINB_EMIT
+#define OD_MINB_EMIT 16
+#endif
+
+// The phase kernels run on a local (stack) copy of the KState: its hot
+// counters (arena tops, writer position, stack tops) then live in L1
+// write-back local memory instead of write-through global memory.  Copies
+// are word loops (an aggregate copy here was miscompiled by nvcc 12.9).
+__device__ __forceinline__ void kstate_load(KState &S, const KState *g) {
+    static_assert(sizeof(KState) % 8 == 0, "KState is copied in u64 words");
+    const u64 *src = reinterpret_cast<const u64 *>(g);
+    u64 *dst = reinterpret_cast<u64 *>(&S);
+    for (u32 q = 0; q < sizeof(KState) / 8; ++q)
+        dst[q] = src[q];
+    kstate_fix(S);
+}
+__device__ __forceinline__ void kstate_store(KState *g, const KState &S) {
+    const u64 *src = reinterpret_cast<const u64 *>(&S);
+    u64 *dst = reinterpret_cast<u64 *>(g);
+    for (u32 q = 0; q < sizeof(KState) / 8; ++q)
+        dst[q] = src[q];
+}
+
+
+__global__ void __launch_bounds__(128, OD_MINB_FRONT) k_front(DecompArgs a);
+__global__ void __launch_bounds__(128, OD_MINB_LOWER) k_lower(DecompArgs a);
+__global__ void __launch_bounds__(128, OD_MINB_FOLD) k_fold(DecompArgs a);
+__global__ void __launch_bounds__(128, OD_MINB_EMIT) k_emit(DecompArgs a);
+
+// ------------------------------------------------------------------ generator
+struct GenArgs {
+    GenCfg cfg;
+    u64 k0, count;
+    u64 *len;   // per kernel length (sizing) -> offsets after scan
+    u32 *ninstr;
+    u8 *buf;
+};
+
+__global__ void k_gen(GenArgs a, int mode);
+
+
+} // namespace od

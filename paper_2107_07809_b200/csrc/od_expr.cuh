@@ -58,7 +58,7 @@ struct EArena {
     OD_INL bool is_const_v(u32 i, u64 v) const { return is_const(i) && cval(i) == v; }
 
     // Expr::constant  expr.cpp:40-44
-    OD_NOINL u32 constant(u64 v, DT t) {
+    OD_HOT u32 constant(u64 v, DT t) {
         u32 bits = dt_bits(t) ? dt_bits(t) : 64;
         u64 mask = bits >= 64 ? ~0ull : ((1ull << bits) - 1);
         v &= mask;
@@ -76,7 +76,7 @@ struct EArena {
         e.memo = 0;
         return i;
     }
-    OD_NOINL u32 leaf(u8 kind, u8 op, u16 x, DT t, u32 a) {
+    OD_HOT u32 leaf(u8 kind, u8 op, u16 x, DT t, u32 a) {
         u32 i = alloc();
         if (!i)
             return 0;
@@ -97,7 +97,7 @@ struct EArena {
     OD_INL u32 var(u32 cls, u32 num, DT t) { return leaf(E_VAR, 0, (u16)cls, t, num); }
 
     // Expr::unary  expr.cpp:71-93
-    OD_NOINL u32 unary(u32 op, u32 a, DT t) {
+    OD_HOT u32 unary(u32 op, u32 a, DT t) {
         if (a) {
             const ENode &x = n[a];
             if (op == U_LO32 && x.kind == E_BINARY && x.op == O_CONCAT64)
@@ -131,7 +131,7 @@ struct EArena {
     }
 
     // Expr::binary  expr.cpp:95-132
-    OD_NOINL u32 binary(u32 op, u32 a, u32 b, DT t) {
+    OD_HOT u32 binary(u32 op, u32 a, u32 b, DT t) {
         if (a && b && is_const(a) && is_const(b) && !dt_is_float(t) && dt_bits(t) <= 32) {
             u32 x = (u32)cval(a), y = (u32)cval(b);
             bool folded = true;

@@ -1,0 +1,74 @@
+// ocldec-b200: k_front (dk_front: config, ABI, CFG, mask normalization,
+// region reduction, liveness, pool carving), its own translation unit.
+#include "od_device.cuh"
+
+namespace od {
+
+__global__ void __launch_bounds__(128, OD_MINB_FRONT) k_front(DecompArgs a) {
+    Slot0 sl;
+    if (!dk_slot(a, &sl))
+        return;
+    const u32 k = sl.k;
+    const u32 i = (blockIdx.x * blockDim.x + threadIdx.x) / a.lanes_per;
+    KState *g = reinterpret_cast<KState *>(sl.base);
+    const u64 kb = (sizeof(KState) + 255) & ~255ull;
+    // Field-wise setup of the state in HBM.  (nvcc 12.9 miscompiled an
+    // aggregate copy of a locally built KIn here into a copy of the first
+    // bytes of the kernel parameters.)
+    static_assert(sizeof(KState) % 8 == 0, "KState is zeroed in u64 words");
+    for (u32 q = 0; q < sizeof(KState) / 8; ++q)
+        reinterpret_cast<u64 *>(g)[q] = 0;
+    KIn &in = g->in;
+    in.t = a.t;
+    in.lines = a.lines;
+    in.lins = a.lins;
+    in.ops = a.ops;
+    in.labs = a.labs;
+    in.lbeg = a.kstart[k];
+    in.lend = k + 1 < a.nk ? a.kstart[k + 1] : a.nlines;
+    in.line_base = a.line_base;
+    in.fold_local_size = a.fold_local_size;
+    in.scale = a.scale;
+    in.prof = a.prof;
+    {
+        const KSize z = a.sizes[k];
+        in.nblk_cap = a.scale <= 1 ? z.nb : 0;
+        in.ncfg = z.ncfg;
+        in.nins = z.nins;
+        in.nlab = z.nlab;
+    }
+    g->mem.base = sl.base + kb;
+    g->mem.top = 0;
+    g->mem.cap = a.boff[i + 1] - a.boff[i] - kb;
+    g->mem.oom = false;
+    g->out.status = KS_OK;
+    kstate_fix(*g);
+    Span nm;
+    {
+        Span w, rest, extra;
+        const LineRec &L = a.lines[in.lbeg];
+        split_word(a.t, Span{L.off, L.len}, &w, &rest);
+        split_word(a.t, rest, &nm, &extra);
+    }
+    if (a.only && (nm.len != a.only_len || !bytes_eq(a.t + nm.off, a.only, nm.len))) {
+        g->out.status = KS_SKIP;
+        g->done = 1;
+    } else {
+#ifdef OD_DEBUG_FRONT
+        printf("k=%u g=%p K.in=%p &g->in=%p g->in.t=%p g->in.lines=%p lbeg=%u lend=%u mem.base=%p cap=%llu\n",
+               k, g, g->K.in, &g->in, g->in.t, g->in.lines, g->in.lbeg, g->in.lend, g->mem.base,
+               (unsigned long long)g->mem.cap);
+#endif
+#if OD_LOCAL_STATE
+        KState S;
+        kstate_load(S, g);
+        dk_front(S);
+        kstate_store(g, S);
+#else
+        kstate_fix(*g);
+        dk_front(*g);
+#endif
+    }
+}
+
+} // namespace od

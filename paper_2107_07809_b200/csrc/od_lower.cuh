@@ -64,7 +64,7 @@ OD_INL void record_fresh(KCtx &K, u32 cls, u32 num, DT t) {
 }
 
 // bind_fresh  sym_state.cpp:63-78
-OD_NOINL u32 bind_fresh(KCtx &K, u32 p, DT t = DT_B32) {
+OD_HOT u32 bind_fresh(KCtx &K, u32 p, DT t = DT_B32) {
     Slot &s = K.regs[p];
     if (!s.expr) {
         log_slot(K, p);
@@ -115,7 +115,7 @@ OD_NOINL u32 read_pair_ids(KCtx &K, u32 lo_id) {
 }
 
 // dissolve_pair  sym_state.cpp:118-135
-OD_NOINL void dissolve_pair(KCtx &K, u32 id) {
+OD_HOT void dissolve_pair(KCtx &K, u32 id) {
     u32 p = phys_of(id);
     Slot &s = K.regs[p];
     if (s.integ == IN_ENTIRE || !s.expr)
@@ -142,7 +142,7 @@ OD_NOINL void dissolve_pair(KCtx &K, u32 id) {
     s.integ = IN_ENTIRE;
 }
 
-OD_NOINL void write_slot32(KCtx &K, u32 id, u32 value, DT t) {
+OD_HOT void write_slot32(KCtx &K, u32 id, u32 value, DT t) {
     if (id >= kNumRegIds) {
         K.oom = true;
         return;
@@ -234,7 +234,7 @@ OD_INL u32 operand_reg_id(const Opnd &o) {
 OD_NOINL u32 read_pair(KCtx &K, const Opnd &o);
 
 // read_operand  sym_state.cpp:205-227
-OD_NOINL u32 read_operand(KCtx &K, const Opnd &o) {
+OD_HOT u32 read_operand(KCtx &K, const Opnd &o) {
     switch (o.kind) {
     case OK_LITERAL: return K.E.constant((u64)o.value & 0xffffffffull, DT_B32);
     case OK_SREG:
@@ -338,7 +338,7 @@ struct Step {
     OD_INL u32 read64(const Opnd &o) { return read_pair(K, o); }
     OD_INL DT ty(u32 e) const { return K.E.n[e].type; }
 
-    OD_NOINL void write(const Opnd &o, u32 value, DT t) {
+    OD_HOT void write(const Opnd &o, u32 value, DT t) {
         u32 id = operand_reg_id(o);
         if (id >= kNumRegIds)
             return;
@@ -370,7 +370,7 @@ struct Step {
     }
 
     // Stepper::coerce  sym_state.cpp:300-310
-    OD_NOINL u32 coerce(u32 e, DT want) {
+    OD_HOT u32 coerce(u32 e, DT want) {
         if (!e)
             return e;
         DT et = ty(e);
@@ -381,6 +381,16 @@ struct Step {
         if (dt_is_float(want) != dt_is_float(et))
             return K.E.unary(U_CAST, e, want);
         return e;
+    }
+
+    // Shared handler tails (one out-of-line copy instead of one per handler:
+    // the lowering pass is bound by instruction fetch).  Reads happen in the
+    // order of the arguments, as in the handlers they replace.
+    OD_NOINL u32 rd(u32 k, DT t) { return coerce(read(op(k)), t); }
+    OD_NOINL void bin(u32 o, DT t, u32 ka, u32 kb) {
+        u32 a = rd(ka, t);
+        u32 b = rd(kb, t);
+        write(op(0), K.E.binary(o, a, b, t), t);
     }
 
     OD_NOINL void push_store(u32 addr, u32 value, DT et) {
@@ -507,15 +517,12 @@ struct Step {
             const bool k = r == R_ADDK || r == R_MULK;
             if (!k && nn < 3)
                 return false;
-            DT t = suffix_type0(I, DT_I32);
-            u32 a = coerce(read(op(k ? 0 : 1)), t);
-            u32 b = coerce(read(op(k ? 1 : 2)), t);
             u32 o = O_ADD;
             if (r == R_SUB)
                 o = O_SUB;
             else if (r == R_MUL || r == R_MULK)
                 o = O_MUL;
-            write(op(0), K.E.binary(o, a, b, t), t);
+            bin(o, suffix_type0(I, DT_I32), k ? 0 : 1, k ? 1 : 2);
             invalidate_slot(K, kRegIdScc, 1);
             return true;
         }
@@ -599,8 +606,8 @@ struct Step {
             if (nn < src0 + 2)
                 return false;
             DT t = suffix_type0(I, DT_U32);
-            u32 a = coerce(read(op(src0)), t);
-            u32 b = coerce(read(op(src0 + 1)), t);
+            u32 a = rd(src0, t);
+            u32 b = rd(src0 + 1, t);
             if (r == R_SUBREV) {
                 u32 x = a;
                 a = b;
@@ -691,23 +698,25 @@ struct Step {
             if (narrow == 2)
                 return false;
             DT t = suffix_type0(I, DT_U32);
-            u32 a = coerce(read(op(1)), t);
-            u32 b = coerce(read(op(2)), t);
-            if (narrow == 1) {
-                a = mask24(a);
-                b = mask24(b);
-            }
             u32 o = O_MUL;
             if (r == R_MUL_HI)
                 o = dt_is_signed(t) ? O_MULHIS : O_MULHI;
+            if (narrow != 1) {
+                bin(o, t, 1, 2);
+                return true;
+            }
+            u32 a = rd(1, t);
+            u32 b = rd(2, t);
+            a = mask24(a);
+            b = mask24(b);
             write(op(0), K.E.binary(o, a, b, t), t);
             return true;
         }
         if (r == R_MAC && nn >= 3) {
             DT t = suffix_type0(I, DT_F32);
-            u32 a = coerce(read(op(1)), t);
-            u32 b = coerce(read(op(2)), t);
-            u32 d = coerce(read(op(0)), t);
+            u32 a = rd(1, t);
+            u32 b = rd(2, t);
+            u32 d = rd(0, t);
             u32 v = K.E.binary(O_ADD, K.E.binary(O_MUL, a, b, t), d, t);
             write(op(0), v, t);
             return true;
@@ -717,9 +726,9 @@ struct Step {
             if (narrow == 2)
                 return false;
             DT t = suffix_type0(I, DT_F32);
-            u32 a = coerce(read(op(1)), t);
-            u32 b = coerce(read(op(2)), t);
-            u32 c = coerce(read(op(3)), t);
+            u32 a = rd(1, t);
+            u32 b = rd(2, t);
+            u32 c = rd(3, t);
             if (narrow == 1) {
                 a = mask24(a);
                 b = mask24(b);
@@ -744,11 +753,7 @@ struct Step {
             return true;
         }
         if ((r == R_AND || r == R_OR || r == R_XOR) && nn >= 3) {
-            DT t = suffix_type0(I, DT_B32);
-            u32 a = coerce(read(op(1)), t);
-            u32 b = coerce(read(op(2)), t);
-            u32 o = r == R_AND ? O_AND : r == R_OR ? O_OR : O_XOR;
-            write(op(0), K.E.binary(o, a, b, t), t);
+            bin(r == R_AND ? O_AND : r == R_OR ? O_OR : O_XOR, suffix_type0(I, DT_B32), 1, 2);
             return true;
         }
         if (I.rflags & RF_CMP)

@@ -11,8 +11,9 @@ so = os.path.join(ROOT, "paper_2107_07809_b200", "libocldec_b200.so")
 want = sys.argv[1:] or ["k_front", "k_lower", "k_emit"]
 with tempfile.TemporaryDirectory() as d:
     subprocess.run(["cuobjdump", "-xelf", "all", so], cwd=d, capture_output=True)
-    cub = [f for f in os.listdir(d) if f.endswith(".cubin")][0]
-    dis = subprocess.run(["nvdisasm", os.path.join(d, cub)], capture_output=True, text=True).stdout
+    dis = ""
+    for cub in sorted(f for f in os.listdir(d) if ".cubin" in f):
+        dis += subprocess.run(["nvdisasm", os.path.join(d, cub)], capture_output=True, text=True).stdout
 per = {}
 cur = None
 for line in dis.splitlines():
