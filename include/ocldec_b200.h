@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define OCLDEC_B200_ABI_VERSION 1
+#define OCLDEC_B200_ABI_VERSION 2
 
 /* DecompileOptions (decompiler.hpp:29-35).  abi_overrides and the DOT dumps
  * are not supported by this version (fields reserved). */
@@ -47,6 +47,15 @@ typedef struct ocldec_b200_kernel {
     uint32_t instructions;        /* parse_text instruction count    */
 } ocldec_b200_kernel;
 
+/* Diagnostic (diagnostics.hpp:20-27): severity 0 note, 1 warning, 2 error;
+ * message at diag_text[msg_off, msg_off + msg_len); Diagnostic::render
+ * (diagnostics.cpp:22-26) is "<file>:<line>: <severity>: <message>". */
+typedef struct ocldec_b200_diag {
+    int32_t severity;
+    int32_t line;
+    uint64_t msg_off, msg_len;
+} ocldec_b200_diag;
+
 typedef struct ocldec_b200_result {
     uint64_t nkernels;
     ocldec_b200_kernel *kernels;
@@ -57,6 +66,9 @@ typedef struct ocldec_b200_result {
     int32_t split_error_kind;     /* 1 nameless .kernel, 2 .config outside, 3 .text outside */
     uint64_t instructions;        /* total parse_text instructions */
     double device_ms;             /* device time of the pipeline (CUDA events) */
+    uint64_t ndiags;              /* DecompileResult::diagnostics, in sink order */
+    ocldec_b200_diag *diags;
+    char *diag_text;
 } ocldec_b200_result;
 
 /* decompile_listing: host buffer in, host result out (H2D/D2H inside). */

@@ -7,7 +7,8 @@
 //   DecompiledKernel{name, source, structured, failed} (decompiler.hpp:39-52)
 //   LoweredBody::fallback_count                        (lower.hpp:23-41)
 //   DecompileResult::combined_source()                 (decompiler.cpp:105-115)
-//   DiagnosticSink entries for split errors            (decompiler.cpp:120-125)
+//   DecompileResult::diagnostics (DiagnosticSink, diagnostics.hpp:20-57):
+//   every note / warning / error the reference emits on this path
 // Inspection fields (config, instructions, cfg, regions, body tree, DOT) are
 // not produced.  All work runs on the GPU; errors from the device runtime are
 // thrown as std::runtime_error (API misuse / CUDA failure only — data errors
@@ -106,12 +107,13 @@ inline DecompileResult decompile_listing(const std::string &listing, const Decom
         d.instructions = k.instructions;
         res.kernels.push_back(std::move(d));
     }
-    if (r->split_error_line > 0) {
+    for (uint64_t i = 0; i < r->ndiags; ++i) {
+        const ocldec_b200_diag &d = r->diags[i];
         Diagnostic dg;
-        dg.severity = Diagnostic::Error;
-        dg.line = r->split_error_line;
-        dg.message = split_error_message(r->split_error_kind);
-        res.diagnostics.push_back(dg);
+        dg.severity = static_cast<Diagnostic::Severity>(d.severity);
+        dg.line = d.line;
+        dg.message.assign(r->diag_text + d.msg_off, d.msg_len);
+        res.diagnostics.push_back(std::move(dg));
     }
     ocldec_b200_free(r);
     return res;

@@ -107,9 +107,12 @@ def decompile_listing(listing: Union[str, bytes], opts: Optional[DecompileOption
                 source=src.decode("utf-8", errors="surrogateescape"),
                 structured=bool(k.structured), failed=bool(k.failed),
                 fallback_count=k.fallback_count, instructions=k.instructions))
-        if r.split_error_line > 0:
-            res.diagnostics.append(Diagnostic(2, r.split_error_line,
-                                              _SPLIT_MESSAGES.get(r.split_error_kind, "parse error")))
+        tlen = max((r.diags[i].msg_off + r.diags[i].msg_len for i in range(r.ndiags)), default=0)
+        text = ctypes.string_at(r.diag_text, tlen) if r.diag_text and tlen else b""
+        for i in range(r.ndiags):
+            d = r.diags[i]
+            msg = text[d.msg_off:d.msg_off + d.msg_len].decode("utf-8", errors="surrogateescape")
+            res.diagnostics.append(Diagnostic(d.severity, d.line, msg))
         return res
     finally:
         L.ocldec_b200_free(out)

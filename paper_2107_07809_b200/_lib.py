@@ -26,12 +26,18 @@ class Kernel(ctypes.Structure):
                 ("fallback_count", ctypes.c_int32), ("instructions", ctypes.c_uint32)]
 
 
+class Diag(ctypes.Structure):
+    _fields_ = [("severity", ctypes.c_int32), ("line", ctypes.c_int32),
+                ("msg_off", ctypes.c_uint64), ("msg_len", ctypes.c_uint64)]
+
+
 class Result(ctypes.Structure):
     _fields_ = [("nkernels", ctypes.c_uint64), ("kernels", ctypes.POINTER(Kernel)),
                 ("names", ctypes.c_void_p), ("combined", ctypes.c_void_p),
                 ("combined_len", ctypes.c_uint64), ("split_error_line", ctypes.c_int32),
                 ("split_error_kind", ctypes.c_int32), ("instructions", ctypes.c_uint64),
-                ("device_ms", ctypes.c_double)]
+                ("device_ms", ctypes.c_double), ("ndiags", ctypes.c_uint64),
+                ("diags", ctypes.POINTER(Diag)), ("diag_text", ctypes.c_void_p)]
 
 
 class Stats(ctypes.Structure):

@@ -425,6 +425,103 @@ int ensure_keep(DevBuf &b, size_t bytes, size_t keep, cudaStream_t st) {
 
 template <class T> T *P(DevBuf &b) { return reinterpret_cast<T *>(b.p); }
 
+// A kernel diagnostic with its listing spans copied out (the device text
+// buffer is reused by the next chunk).
+struct HostDiag {
+    u32 line;
+    u16 code, c;
+    std::string a, b;
+};
+
+int diag_severity(u16 code) {
+    switch (code) {
+    case DG_UNREACHABLE: return 0;
+    case DG_ARG_TYPE: case DG_OPERAND: case DG_MASK_MULTI: case DG_MASK_NONE: case DG_MASK_EXECZ_INV:
+    case DG_MASK_NO_RESTORE: case DG_MASK_EXECZ_RST: case DG_SLOAD_UNMAPPED: case DG_ADDC: case DG_GOTO:
+    case DG_EXEC_BRANCH:
+        return 1;
+    default: return 2;
+    }
+}
+
+bool is_type_suffix(const std::string &tok) { // parse_type_suffix  type_recovery.cpp:50-73
+    if (tok.size() < 2 || tok.size() > 3 || !strchr("iufb", tok[0]))
+        return false;
+    std::string w = tok.substr(1);
+    return w == "8" || w == "16" || w == "24" || w == "32" || w == "64";
+}
+
+// decompose_mnemonic's root (asm_frontend.cpp:375-423) of an s_ mnemonic.
+std::string mnemonic_root(const std::string &m) {
+    std::string rest = m.size() > 2 ? m.substr(2) : std::string();
+    std::vector<std::string> toks;
+    size_t p = 0;
+    for (;;) {
+        size_t q = rest.find('_', p);
+        toks.push_back(rest.substr(p, q == std::string::npos ? std::string::npos : q - p));
+        if (q == std::string::npos)
+            break;
+        p = q + 1;
+    }
+    size_t end = toks.size(), peeled = 0;
+    while (end > 1 && peeled < 2 && is_type_suffix(toks[end - 1])) {
+        --end;
+        ++peeled;
+    }
+    std::string root;
+    for (size_t i = 0; i < end; ++i) {
+        if (i)
+            root += '_';
+        root += toks[i];
+    }
+    return root;
+}
+
+// The reference's message text for a diagnostic.
+std::string diag_message(const HostDiag &d) {
+    switch (d.code) {
+    case DG_DIMS: return "bad .dims axes '" + d.a + "'";
+    case DG_CWS_COUNT: return "cws expects 1 to 3 sizes";
+    case DG_CWS_VALUE: return "bad cws value '" + d.a + "'";
+    case DG_SGPRS: return "bad sgprsnum value";
+    case DG_VGPRS: return "bad vgprsnum value";
+    case DG_ARG_FIELDS: return "arg directive needs name, type string and type";
+    case DG_ARG_TYPE: return "unrecognized argument type '" + d.a + "' for '" + d.b + "'";
+    case DG_OPERAND: {
+        std::string m;
+        switch (d.c) {
+        case 1: m = "unbalanced bracket in register operand '" + d.a + "'"; break;
+        case 2: m = "register range without ':' in '" + d.a + "'"; break;
+        case 3: m = "bad register range '" + d.a + "'"; break;
+        case 4: m = "negative register index in '" + d.a + "'"; break;
+        default: {
+            const bool scalar = !d.a.empty() && d.a[0] == 's';
+            m = "register '" + d.a + "' exceeds the " + (scalar ? "SGPR" : "VGPR") + " file (max " +
+                (scalar ? "103" : "255") + ")";
+        }
+        }
+        return m + "; keeping the line as inline assembly";
+    }
+    case DG_BR_NOLABEL: return "branch without a label operand";
+    case DG_BR_UNDEF: return "branch to undefined label '" + d.a + "'";
+    case DG_CBR_UNSUP: return "unsupported conditional branch s_" + mnemonic_root(d.a);
+    case DG_CBR_END: return "conditional branch at end of kernel";
+    case DG_UNREACHABLE: return "unreachable code";
+    case DG_MASK_MULTI:
+        return "exec mask saved in s[" + std::to_string(d.c) + ":" + std::to_string(d.c + 1) +
+               "] has multiple join points";
+    case DG_MASK_NONE: return "exec mask save without inversion or restore";
+    case DG_MASK_EXECZ_INV: return "execz branch does not meet the mask inversion";
+    case DG_MASK_NO_RESTORE: return "mask inversion without a matching restore";
+    case DG_MASK_EXECZ_RST: return "execz branch does not meet the mask restore";
+    case DG_SLOAD_UNMAPPED: return "scalar load from unmapped settings offset";
+    case DG_ADDC: return "v_addc_u32 outside the 64-bit add idiom; carry treated as zero";
+    case DG_GOTO: return "control flow not fully structured; emitting labeled blocks";
+    case DG_EXEC_BRANCH: return "exec-dependent branch kept as inline asm";
+    default: return "diagnostic " + std::to_string(d.code);
+    }
+}
+
 } // namespace
 
 struct ocldec_b200_session {
@@ -450,6 +547,9 @@ struct ocldec_b200_session {
     std::vector<u64> host_kernel_off;
     std::vector<u32> host_name_line; // chunk-relative .kernel line (host path names)
     std::vector<cudaEvent_t> pev;    // phase-launch events (pool)
+    DevBuf dpool, dtop;              // device diagnostic records of a chunk
+    std::vector<HostDiag> host_diag; // materialized diagnostics, all chunks
+    std::vector<u64> host_kdiag;     // per kernel: first host_diag index (count in host_res[k].ndiag)
     size_t pev_used = 0;
 };
 
@@ -653,6 +753,12 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     a.stage = P<u8>(s->stage);
     a.stage_cap = s->stage.cap;
     a.stage_top = reinterpret_cast<unsigned long long *>(cnt + 14);
+    if (ensure(s->dpool, std::max<u64>(1ull << 16, (u64)nk * 2) * sizeof(Diag)) || ensure(s->dtop, 16))
+        return -3;
+    CK(cudaMemsetAsync(s->dtop.p, 0, 8, st));
+    a.dpool = P<Diag>(s->dpool);
+    a.dcap = s->dpool.cap / sizeof(Diag);
+    a.dtop = P<unsigned long long>(s->dtop);
     a.res = P<KRes>(s->res);
     a.only = s->only_set ? P<u8>(s->only) : nullptr;
     a.only_len = s->only_len;
@@ -790,6 +896,18 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
             s->stage = nb;
             a.stage = P<u8>(s->stage);
             a.stage_cap = s->stage.cap;
+            u64 dt = 0;
+            if (d2h_sync(s, &dt, s->dtop.p, 8))
+                return -3;
+            if (dt > a.dcap) { // diagnostic pool full: grow it, keep the records written so far
+                const u64 old_cap = a.dcap;
+                if (ensure_keep(s->dpool, dt * 2 * sizeof(Diag), old_cap * sizeof(Diag), st))
+                    return -3;
+                a.dpool = P<Diag>(s->dpool);
+                a.dcap = s->dpool.cap / sizeof(Diag);
+                CK(cudaMemcpyAsync(s->dtop.p, &old_cap, 8, cudaMemcpyHostToDevice, st));
+                CK(cudaStreamSynchronize(st));
+            }
         }
         bool oom = false;
         for (u32 k : redo)
@@ -846,6 +964,42 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     std::vector<u32> ks(nk);
     if (d2h_sync(s, ks.data(), s->kstart.p, (u64)nk * 4))
         return -3;
+    // diagnostics: the records of the kept results, spans copied out
+    std::vector<Diag> dv;
+    {
+        u64 dt = 0;
+        if (d2h_sync(s, &dt, s->dtop.p, 8))
+            return -3;
+        dt = std::min<u64>(dt, a.dcap);
+        if (dt) {
+            dv.resize(dt);
+            if (d2h_sync(s, dv.data(), s->dpool.p, dt * sizeof(Diag)))
+                return -3;
+        }
+    }
+    auto span_text = [&](u32 off, u32 n, std::string *out) -> int {
+        out->resize(n);
+        if (n)
+            CK(cudaMemcpy(&(*out)[0], t + off, n, cudaMemcpyDeviceToHost));
+        return 0;
+    };
+    for (u32 k = 0; k < nk; ++k) {
+        s->host_kdiag.push_back(s->host_diag.size());
+        if (hr[k].status == KS_OK || hr[k].status == KS_FAILED) {
+            for (u32 q = 0; q < hr[k].ndiag && hr[k].diag_off + q < dv.size(); ++q) {
+                const Diag &d = dv[hr[k].diag_off + q];
+                HostDiag h;
+                h.line = d.line;
+                h.code = d.code;
+                h.c = d.c;
+                if (span_text(d.a_off, d.a_len, &h.a) || span_text(d.b_off, d.b_len, &h.b))
+                    return -3;
+                s->host_diag.push_back(std::move(h));
+            }
+        } else {
+            hr[k].ndiag = 0;
+        }
+    }
     for (u32 k = 0; k < nk; ++k) {
         s->host_res.push_back(hr[k]);
         s->host_kernel_off.push_back(base + offs[k]);
@@ -936,6 +1090,8 @@ void reset_stats(ocldec_b200_session *s) {
     s->host_res.clear();
     s->host_kernel_off.clear();
     s->host_name_line.clear();
+    s->host_diag.clear();
+    s->host_kdiag.clear();
     s->out_len = 0;
 }
 
@@ -1033,6 +1189,8 @@ int run_host_listing(ocldec_b200_session *s, const char *listing, size_t len, in
             hr->split_error_kind = (int32_t)co.err_kind;
             s->host_res.clear();
             s->host_kernel_off.clear();
+            s->host_diag.clear();
+            s->host_kdiag.clear();
             hr->names.clear();
             out_pos = 0;
             break;
@@ -1092,7 +1250,7 @@ void ocldec_b200_session_destroy(ocldec_b200_session *s) {
                       &s->scan_tmp, &s->scan_tot, &s->counters, &s->arena, &s->stage, &s->res,
                       &s->outoff, &s->out, &s->only, &s->retry, &s->gen_len, &s->gen_ninstr,
                       &s->gen_buf, &s->gen_off, &s->kmeta, &s->order, &s->budget, &s->sbudget,
-                      &s->boff, &s->hist, &s->prof, &s->ksizes};
+                      &s->boff, &s->hist, &s->prof, &s->ksizes, &s->dpool, &s->dtop};
     for (DevBuf *b : bufs)
         if (b->p)
             cudaFree(b->p);
@@ -1252,6 +1410,41 @@ int ocldec_b200_decompile(const char *listing, size_t len, const ocldec_b200_opt
     res->names = static_cast<char *>(malloc(nm.size() + 1));
     memcpy(res->names, nm.data(), nm.size());
     res->names[nm.size()] = 0;
+    // DecompileResult::diagnostics in sink order: the split error alone, or
+    // every kept kernel's diagnostics in listing order
+    std::vector<ocldec_b200_diag> dl;
+    std::string dt;
+    auto add = [&](int sev, int line, const std::string &msg) {
+        ocldec_b200_diag d;
+        d.severity = sev;
+        d.line = line;
+        d.msg_off = dt.size();
+        d.msg_len = msg.size();
+        dt += msg;
+        dl.push_back(d);
+    };
+    if (hr.split_error_line > 0) {
+        static const char *kSplit[] = {"parse error", ".kernel directive without a name",
+                                       ".config outside of a .kernel section", ".text outside of a .kernel section"};
+        add(2, hr.split_error_line, kSplit[hr.split_error_kind >= 1 && hr.split_error_kind <= 3 ? hr.split_error_kind : 0]);
+    } else {
+        for (size_t k = 0; k < nk; ++k) {
+            const KRes &r = s->host_res[k];
+            if (r.status == KS_SKIP)
+                continue;
+            for (u32 q = 0; q < r.ndiag; ++q) {
+                const HostDiag &h = s->host_diag[s->host_kdiag[k] + q];
+                add(diag_severity(h.code), (int)h.line, diag_message(h));
+            }
+        }
+    }
+    res->ndiags = dl.size();
+    res->diags = static_cast<ocldec_b200_diag *>(malloc((dl.size() + 1) * sizeof(ocldec_b200_diag)));
+    if (!dl.empty())
+        memcpy(res->diags, dl.data(), dl.size() * sizeof(ocldec_b200_diag));
+    res->diag_text = static_cast<char *>(malloc(dt.size() + 1));
+    memcpy(res->diag_text, dt.data(), dt.size());
+    res->diag_text[dt.size()] = 0;
     *out = res;
     return 0;
 }
@@ -1286,6 +1479,8 @@ void ocldec_b200_free(ocldec_b200_result *res) {
     free(res->kernels);
     free(res->names);
     free(res->combined);
+    free(res->diags);
+    free(res->diag_text);
     free(res);
 }
 

@@ -171,6 +171,16 @@ struct Span {
     u32 off, len;
 };
 
+// trim (asm_frontend.cpp:26-40): isspace on both ends.
+OD_INL Span trim_span(const u8 *t, Span s) {
+    u32 b = s.off, e = s.off + s.len;
+    while (b < e && (t[b] == ' ' || (t[b] >= 9 && t[b] <= 13)))
+        ++b;
+    while (e > b && (t[e - 1] == ' ' || (t[e - 1] >= 9 && t[e - 1] <= 13)))
+        --e;
+    return Span{b, e - b};
+}
+
 OD_INL u64 fnv1a64(const u8 *p, u32 n) {
     u64 h = 1469598103934665603ull;
     for (u32 i = 0; i < n; ++i) {

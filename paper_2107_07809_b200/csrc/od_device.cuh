@@ -21,7 +21,8 @@ struct KRes {
     u32 out_len;
     u32 name_off;   // kernel name span (chunk-relative; >= chunk len: aux area)
     u32 name_len;
-    u32 pad[3];
+    u32 ndiag;      // diagnostics of the kernel, at diag_off in the diagnostic pool
+    u64 diag_off;
 };
 enum : u32 { KS_SKIP = 4, KS_STAGE_FULL = 5 };
 
@@ -47,6 +48,9 @@ struct DecompArgs {
     u32 only_len;
     u64 *prof;
     u32 lanes_per; // lanes per kernel: 32 / kernels-per-warp
+    Diag *dpool;   // diagnostic records of finished kernels
+    u64 dcap;
+    unsigned long long *dtop;
     const KSize *sizes; // per kernel (k_ksize)
 };
 

@@ -247,6 +247,42 @@ struct AbiEntry {
     DT type;
 };
 
+// ------------------------------------------------------------ diagnostics
+// DiagnosticSink entries (diagnostics.hpp:20-57) of one kernel, in emission
+// order; the host renders the message text (ocldec_b200.cu render_diag) from
+// the code and the listing spans.  Catalogue: SURVEY A.4.
+enum DiagCode : u16 {
+    DG_DIMS = 1,        // error   "bad .dims axes '<a>'"                        asm_frontend.cpp:307
+    DG_CWS_COUNT,       // error   "cws expects 1 to 3 sizes"                    :313
+    DG_CWS_VALUE,       // error   "bad cws value '<a>'"                         :319
+    DG_SGPRS,           // error   "bad sgprsnum value"                          :329
+    DG_VGPRS,           // error   "bad vgprsnum value"                          :335
+    DG_ARG_FIELDS,      // error   "arg directive needs name, type string and type" :341
+    DG_ARG_TYPE,        // warning "unrecognized argument type '<a>' for '<b>'"  :365
+    DG_OPERAND,         // warning "<operand ParseError c, token a>; keeping the line as inline assembly" :159-183, 478
+    DG_BR_NOLABEL,      // error   "branch without a label operand"              cfg.cpp:105
+    DG_BR_UNDEF,        // error   "branch to undefined label '<a>'"             cfg.cpp:108
+    DG_CBR_UNSUP,       // error   "unsupported conditional branch s_<root of a>" cfg.cpp:127
+    DG_CBR_END,         // error   "conditional branch at end of kernel"         cfg.cpp:130
+    DG_UNREACHABLE,     // note    "unreachable code"                            cfg.cpp:154
+    DG_MASK_MULTI,      // warning "exec mask saved in s[c:c+1] has multiple join points" structurizer.cpp:533
+    DG_MASK_NONE,       // warning "exec mask save without inversion or restore" :539
+    DG_MASK_EXECZ_INV,  // warning "execz branch does not meet the mask inversion" :555
+    DG_MASK_NO_RESTORE, // warning "mask inversion without a matching restore"   :575
+    DG_MASK_EXECZ_RST,  // warning "execz branch does not meet the mask restore" :586
+    DG_SLOAD_UNMAPPED,  // warning "scalar load from unmapped settings offset"   sym_state.cpp:394
+    DG_ADDC,            // warning "v_addc_u32 outside the 64-bit add idiom; carry treated as zero" :688
+    DG_GOTO,            // warning "control flow not fully structured; emitting labeled blocks" lower.cpp:189
+    DG_EXEC_BRANCH,     // warning "exec-dependent branch kept as inline asm"    lower.cpp:225
+};
+
+struct Diag {
+    u32 line;
+    u16 code;
+    u16 c;    // small argument (operand error kind, mask SGPR)
+    u32 a_off, a_len, b_off, b_len; // listing spans
+};
+
 // The whole per-kernel working set.
 struct KCtx {
     const KIn *in;
@@ -330,7 +366,28 @@ struct KCtx {
 
     // rendering
     RenderCtx rc;
+
+    // diagnostics
+    Diag *dg;
+    u32 ndg, dg_cap;
 };
+
+OD_NOINL void diag(KCtx &K, u16 code, u32 line, u16 c = 0, Span a = Span{0, 0}, Span b = Span{0, 0}) {
+    if (!K.dg)
+        return;
+    if (K.ndg >= K.dg_cap) {
+        K.oom = true; // retried with a larger arena
+        return;
+    }
+    Diag &d = K.dg[K.ndg++];
+    d.line = line;
+    d.code = code;
+    d.c = c;
+    d.a_off = a.off;
+    d.a_len = a.len;
+    d.b_off = b.off;
+    d.b_len = b.len;
+}
 
 OD_INL const Opnd &op_at(const KCtx &K, const Ins &I, u32 k) { return K.in->ops[I.op_start + k]; }
 OD_INL DT suffix_type0(const Ins &I, DT fb) { return I.sfx[0] ? dt_from_suffix(I.sfx[0]) : fb; }
@@ -482,24 +539,39 @@ OD_NOINL bool parse_config(KCtx &K) {
             }
             if (ok)
                 c.dims = dims;
+            else
+                diag(K, DG_DIMS, in.line_base + l + 1, 0, axes);
         } else if (span_eq(t, key, "cws") || span_eq(t, key, "reqd_work_group_size")) {
             Span f[4];
             u32 nf = split_fields_spans(t, rest, f, 4);
-            if (nf == 0 || nf > 3)
+            if (nf == 0 || nf > 3) {
+                diag(K, DG_CWS_COUNT, in.line_base + l + 1);
                 continue;
+            }
             for (u32 i = 0; i < nf; ++i) {
                 i64 v;
-                if (!parse_int(t + f[i].off, f[i].len, &v) || v <= 0)
+                if (!parse_int(t + f[i].off, f[i].len, &v) || v <= 0) {
+                    diag(K, DG_CWS_VALUE, in.line_base + l + 1, 0, f[i]);
                     break;
+                }
                 c.cws[i] = (u32)v;
             }
+        } else if (span_eq(t, key, "sgprsnum") || span_eq(t, key, "sgprnum") || span_eq(t, key, "vgprsnum") ||
+                   span_eq(t, key, "vgprnum")) {
+            // the counts are not used downstream; only a bad value is reported
+            Span v = trim_span(t, rest);
+            i64 x;
+            if (!(parse_int(t + v.off, v.len, &x) && x >= 0))
+                diag(K, t[key.off] == 's' ? DG_SGPRS : DG_VGPRS, in.line_base + l + 1);
         } else if (span_eq(t, key, "useargs")) {
             c.useargs = 1;
         } else if (span_eq(t, key, "arg")) {
             Span f[4];
             u32 nf = split_fields_spans(t, rest, f, 4);
-            if (nf < 3)
+            if (nf < 3) {
+                diag(K, DG_ARG_FIELDS, in.line_base + l + 1);
                 continue;
+            }
             KArg &a = c.args[c.nargs];
             a.name = f[0];
             u32 space = AS_NONE;
@@ -520,6 +592,8 @@ OD_NOINL bool parse_config(KCtx &K) {
             }
             a.type = type_from_arg_decl(t, mt, space);
             a.implicit = (a.name.len >= 2 && t[a.name.off] == '_' && t[a.name.off + 1] == '.');
+            if (dt_base(a.type) == B_UNKNOWN)
+                diag(K, DG_ARG_TYPE, in.line_base + l + 1, 0, mt, a.name);
             // canonical sanitized-name id
             u32 id = c.nargs;
             for (u32 j = 0; j < c.nargs; ++j)
@@ -761,6 +835,10 @@ OD_NOINL bool collect_instructions(KCtx &K) {
         I.src.len = L.src_len;
         I.lab_b = pend_b;
         I.lab_n = nkl - pend_b;
+        if (L.flags & IF_PARSE_FAILED) { // parse_instruction's downgraded ParseError (asm_frontend.cpp:478)
+            const Opnd &e = ops[L.op_start];
+            diag(K, DG_OPERAND, I.line, e.special, Span{e.r.a, e.r.b});
+        }
         u32 m = 0;
         I.xkind = L.prefix == PX_S ? (u8)exec_kind_of(L.root, L.prefix, L.flags, L.nops, ops + L.op_start, &m)
                                    : (u8)XK_NONE;
@@ -830,13 +908,16 @@ OD_INL int lmap_get(const KCtx &K, Span name) {
 
 OD_INL int resolve_target(KCtx &K, const Ins &I) {
     if (I.nops == 0 || op_at(K, I, 0).kind != OK_SYMBOL) {
-        K.failed = true; // "branch without a label operand"
+        K.failed = true;
+        diag(K, DG_BR_NOLABEL, I.line);
         return -1;
     }
     const Opnd &o = op_at(K, I, 0);
     int b = lmap_get(K, Span{o.r.a, o.r.b});
-    if (b < 0)
-        K.failed = true; // "branch to undefined label"
+    if (b < 0) {
+        K.failed = true;
+        diag(K, DG_BR_UNDEF, I.line, 0, Span{o.r.a, o.r.b});
+    }
     return b;
 }
 
@@ -948,6 +1029,13 @@ OD_NOINL bool build_cfg(KCtx &K) {
             }
             if (cc < 0 || next < 0) {
                 K.failed = true;
+                if (cc < 0) { // the mnemonic: "s_" + root (+ suffixes) -> the host strips it
+                    Span w, rest;
+                    split_word(K.in->t, last.src, &w, &rest);
+                    diag(K, DG_CBR_UNSUP, last.line, 0, w);
+                } else {
+                    diag(K, DG_CBR_END, last.line);
+                }
                 break;
             }
             t.kind = T_COND;
@@ -972,6 +1060,9 @@ OD_NOINL bool build_cfg(KCtx &K) {
     if (K.failed)
         return true;
     mark_reachable(K);
+    for (u32 b = 0; b < K.nblk; ++b)
+        if (!K.blk[b].reachable)
+            diag(K, DG_UNREACHABLE, K.ins[K.blk[b].ib].line);
     return true;
 }
 
@@ -1133,8 +1224,10 @@ OD_NOINL bool apply_mask_pattern(KCtx &K, const MaskPattern &pat, u32 *touched, 
     i32 stop = -1;
     i32 starts[2] = {pat.then_entry, 0};
     u32 ns = mask_stops(K, starts, 1, pat.mask, pat.header, &stop);
-    if (ns != 1)
-        return false; // "multiple join points" / "save without inversion or restore"
+    if (ns != 1) {
+        diag(K, ns > 1 ? DG_MASK_MULTI : DG_MASK_NONE, h.term.line, (u16)pat.mask);
+        return false;
+    }
     const i32 invert = first_exec_op_is(K, (u32)stop, XK_INVERT, pat.mask) ? stop : -1;
     i32 then_entry = pat.then_entry, else_entry = -1, join = -1;
     bool reach_may_shrink = false;
@@ -1142,8 +1235,10 @@ OD_NOINL bool apply_mask_pattern(KCtx &K, const MaskPattern &pat, u32 *touched, 
     if (invert >= 0) {
         Block &ib = K.blk[invert];
         const bool invert_only = (ib.ie - ib.ib) <= 2 && ib.term.kind == T_COND && ib.term.cc == C_EXECZ;
-        if (pat.has_bypass && pat.bypass != invert)
+        if (pat.has_bypass && pat.bypass != invert) {
+            diag(K, DG_MASK_EXECZ_INV, h.term.line);
             return false;
+        }
         if (invert_only) {
             else_entry = ib.term.not_taken;
             join = ib.term.taken;
@@ -1157,8 +1252,10 @@ OD_NOINL bool apply_mask_pattern(KCtx &K, const MaskPattern &pat, u32 *touched, 
         } else {
             i32 rstop = -1;
             u32 nr = mask_stops(K, ib.succ, ib.nsucc, pat.mask, invert, &rstop);
-            if (nr != 1 || !first_exec_op_is(K, (u32)rstop, XK_RESTORE, pat.mask))
-                return false; // "mask inversion without a matching restore"
+            if (nr != 1 || !first_exec_op_is(K, (u32)rstop, XK_RESTORE, pat.mask)) {
+                diag(K, DG_MASK_NO_RESTORE, h.term.line);
+                return false;
+            }
             else_entry = invert;
             join = rstop;
             K.supp[ib.ib] = 1;
@@ -1166,8 +1263,10 @@ OD_NOINL bool apply_mask_pattern(KCtx &K, const MaskPattern &pat, u32 *touched, 
         }
         touched[(*ntouched)++] = (u32)invert;
     } else {
-        if (pat.has_bypass && pat.bypass != stop)
+        if (pat.has_bypass && pat.bypass != stop) {
+            diag(K, DG_MASK_EXECZ_RST, h.term.line);
             return false;
+        }
         join = stop;
     }
     if (join >= 0) {

@@ -445,7 +445,7 @@ struct Step {
                 }
                 return;
             }
-            // warning: scalar load from unmapped settings offset
+            diag(K, DG_SLOAD_UNMAPPED, I.line);
         }
         for (u32 i = 0; i < dwords; ++i) {
             u32 addr = K.E.binary(O_ADD, base, K.E.constant(offset + 4 * i, DT_U64), DT_U64);
@@ -687,7 +687,7 @@ struct Step {
                     return true;
                 }
             }
-            // warning: v_addc_u32 outside the 64-bit add idiom
+            diag(K, DG_ADDC, I.line);
             u32 v = K.E.binary(O_ADD, coerce(x, t), coerce(y, t), t);
             write(op(0), v, t);
             invalidate_slot(K, operand_reg_id(op(1)), op(1).count);
@@ -1181,6 +1181,7 @@ OD_NOINL void lower_structured(KCtx &K, u32 root, u32 out) {
 
 // lower_goto_form  lower.cpp:187-250
 OD_NOINL void lower_goto(KCtx &K, u32 out) {
+    diag(K, DG_GOTO, 0);
     for (u32 k = 0; k < K.nblk && !K.oom && !K.E.oom; ++k) {
         u32 id = k;
         if (k > 0 && (!K.blk[id].reachable || K.blk[id].absorbed))
@@ -1202,6 +1203,7 @@ OD_NOINL void lower_goto(KCtx &K, u32 out) {
         } else if (t.kind == T_COND) {
             u32 cond = taken_cond(K, t.cc, t.mask_source);
             if (!cond) {
+                diag(K, DG_EXEC_BRANCH, t.line);
                 const Ins &last = K.ins[B.ie - 1];
                 u32 r = new_stmt(K, SK_RAW);
                 K.st[r].a = last.src.off;
@@ -1402,6 +1404,15 @@ OD_INL PoolCaps pool_caps(u32 n, u32 s) {
 // scale s (every allocation it makes, in order; regions <= 2 * blocks + 4).
 // At s > 1 (a retry) the block bound falls back to one block per
 // instruction.
+// Diagnostics of one kernel: at most one per config line, two per
+// instruction (operand / stepper warnings), two per block (unreachable note,
+// mask or goto warning) and a few kernel-level ones.
+OD_INL u32 diag_cap_of(u32 ncfg, u32 nins, u32 nb, u32 s) { return (ncfg + 2 * (nins + 1) + 2 * nb + 16) * (s ? s : 1); }
+OD_INL u32 diag_cap(const KIn &in) {
+    const u32 nb = in.nblk_cap ? in.nblk_cap : in.nins + 3;
+    return diag_cap_of(in.ncfg, in.nins, nb, in.scale);
+}
+
 OD_INL u64 arena_budget(const KSize &z, u32 s) {
     const u64 ni = z.nins + 1;                                // + synthetic s_endpgm
     u64 b = ni + 2;                                           // blocks (build_cfg's cap)
@@ -1426,6 +1437,7 @@ OD_INL u64 arena_budget(const KSize &z, u32 s) {
          (2 * r + 8) * sizeof(Frame) + (u64)c.log * sizeof(UndoRec) + (u64)c.dstk * (sizeof(Slot) + 4) +
          (u64)c.fresh * sizeof(Fresh) + (u64)c.names * 8 + 3ull * c.stack * 4 + (u64)c.tasks * 8 +
          3 * (r + 8) * 4 + c.out;
+    t += (u64)diag_cap_of(z.ncfg, z.nins, s <= 1 ? z.nb : z.nins + 3, s) * sizeof(Diag); // diagnostics
     t += 64 * 16; // per-allocation alignment
     return (t + 255) & ~255ull;
 }
@@ -1496,6 +1508,13 @@ OD_NOINL void dk_front(KState &S) {
             return;                                                                                \
         }                                                                                          \
     } while (0)
+    {
+        const u32 cap = diag_cap(in);
+        K.dg = mem.get<Diag>(cap);
+        K.dg_cap = cap;
+        K.ndg = 0;
+        OD_CHECK(K.dg);
+    }
     OD_CHECK(parse_config(K));
     OD_CHECK(collect_instructions(K));
     out.ninstr = K.nins_real;

@@ -330,7 +330,9 @@ OD_NOINL Mnem decompose(const u8 *t, Span m, const RootTable *rt) {
 }
 
 // ------------------------------------------------------- operand parsing
-// Result of one token: 0 ok, 1 parse error (ParseError thrown in ref).
+// Result of one token: 0 ok, else the operand ParseError the reference throws
+// (asm_frontend.cpp:159-183): 1 unbalanced bracket, 2 range without ':',
+// 3 bad range, 4 negative index, 5 beyond the register file.
 OD_NOINL int parse_register(const u8 *t, Span tok, Opnd *op, bool *is_reg) {
     *is_reg = false;
     const u8 *p = t + tok.off;
@@ -354,12 +356,12 @@ OD_NOINL int parse_register(const u8 *t, Span tok, Opnd *op, bool *is_reg) {
         while (colon < inn && in[colon] != ':')
             ++colon;
         if (colon == inn)
-            return 1; // no ':'
+            return 2; // no ':'
         i64 lo, hi;
         bool okl = parse_int(in, colon, &lo);
         bool okh = parse_int(in + colon + 1, inn - colon - 1, &hi);
         if (!okl || !okh || lo < 0 || hi < lo)
-            return 1;
+            return 3; // bad range
         first = (u32)lo;
         count = (u32)(hi - lo + 1);
     } else {
@@ -367,12 +369,12 @@ OD_NOINL int parse_register(const u8 *t, Span tok, Opnd *op, bool *is_reg) {
         if (!parse_int(rest, rn, &idx))
             return 0; // "saveexec" and other identifiers
         if (idx < 0)
-            return 1;
+            return 4; // negative index
         first = (u32)idx;
         count = 1;
     }
     if ((u32)(first + count) > limit)
-        return 1;
+        return 5; // exceeds the register file
     op->kind = scalar ? OK_SREG : OK_VREG;
     op->special = 0;
     op->count = count;
@@ -415,8 +417,8 @@ OD_NOINL int parse_operand(const u8 *t, Span tok, Opnd *op) {
         return 0;
     }
     bool is_reg;
-    if (parse_register(t, tok, op, &is_reg))
-        return 1;
+    if (int err = parse_register(t, tok, op, &is_reg))
+        return err;
     if (is_reg)
         return 0;
     i64 v;
@@ -611,7 +613,17 @@ OD_NOINL int decode_line(const u8 *t, Span content, const RootTable *rt, LineIns
                 ++te;
             Span tok = {q, te - q};
             Opnd tmp;
-            if (parse_operand(t, tok, &tmp)) {
+            if (int err = parse_operand(t, tok, &tmp)) {
+                // the failing token goes to the line's first operand slot
+                // (diagnostics); the instruction itself has no operands
+                if (ops && ops_cap > 0) {
+                    ops[0].kind = OK_ANNOT;
+                    ops[0].special = (u8)err;
+                    ops[0].pad = 0;
+                    ops[0].count = 1;
+                    ops[0].r.a = tok.off;
+                    ops[0].r.b = tok.len;
+                }
                 out->flags |= IF_PARSE_FAILED;
                 out->prefix = PX_OTHER;
                 out->rflags = 0;

@@ -48,6 +48,8 @@ __global__ void __launch_bounds__(128, OD_MINB_EMIT) k_emit(DecompArgs a) {
     KState *g = reinterpret_cast<KState *>(sl.base);
     KOut o;
     const u8 *src = nullptr;
+    const Diag *dg = g->K.dg;
+    u32 ndg = g->K.ndg;
     if (!g->done) {
 #if OD_LOCAL_STATE
         KState S;
@@ -55,18 +57,21 @@ __global__ void __launch_bounds__(128, OD_MINB_EMIT) k_emit(DecompArgs a) {
         dk_emit(S);
         o = S.out;
         src = S.w.p;
+        ndg = S.K.ndg;
 #else
         kstate_fix(*g);
         dk_emit(*g);
         o = g->out;
         src = g->w.p;
+        ndg = g->K.ndg;
 #endif
     } else {
         o = g->out;
     }
     const u32 k = sl.k;
     KRes r;
-    r.pad[0] = r.pad[1] = r.pad[2] = 0;
+    r.ndiag = 0;
+    r.diag_off = 0;
     r.stage_off = 0;
     r.out_len = 0;
     r.status = o.status;
@@ -93,6 +98,18 @@ __global__ void __launch_bounds__(128, OD_MINB_EMIT) k_emit(DecompArgs a) {
                 d4[q] = s4[q];
             r.stage_off = so;
             r.out_len = o.out_len;
+        }
+    }
+    // diagnostics (the OOM attempts are re-run from scratch: not kept)
+    if (ndg && o.status != KS_OOM && r.status != KS_STAGE_FULL) {
+        const u64 dof = atomicAdd(a.dtop, (unsigned long long)ndg);
+        if (dof + ndg > a.dcap) {
+            r.status = KS_STAGE_FULL; // the host grows the pool and re-runs the kernel
+        } else {
+            for (u32 q = 0; q < ndg; ++q)
+                a.dpool[dof + q] = dg[q];
+            r.ndiag = ndg;
+            r.diag_off = dof;
         }
     }
     a.res[k] = r;
