@@ -373,6 +373,9 @@ struct KCtx {
 };
 
 OD_NOINL void diag(KCtx &K, u16 code, u32 line, u16 c = 0, Span a = Span{0, 0}, Span b = Span{0, 0}) {
+#ifdef OD_DIAG_OFF
+    return;
+#endif
     if (!K.dg)
         return;
     if (K.ndg >= K.dg_cap) {
@@ -486,32 +489,16 @@ OD_INL bool sanitized_eq(const u8 *t, Span a, Span b) {
 }
 
 // parse_config  asm_frontend.cpp:283-373 (diagnostics are not materialized)
-OD_NOINL bool parse_config(KCtx &K) {
+// One config line of parse_config (asm_frontend.cpp:287-371), out of line:
+// the scan over the section's lines stays a tight loop.
+OD_NOINL void config_line(KCtx &K, u32 l) {
     const KIn &in = *K.in;
     const u8 *t = in.t;
     KConfig &c = K.cfg;
-    c.dims = 1;
-    c.cws[0] = c.cws[1] = c.cws[2] = 1;
-    c.useargs = 0;
-    c.nargs = 0;
-    c.fold_local_size = in.fold_local_size;
-    // name: second word of the .kernel line
-    {
-        const LineRec &L = in.lines[in.lbeg];
-        Span w, rest, nm, extra;
-        split_word(t, Span{L.off, L.len}, &w, &rest);
-        split_word(t, rest, &nm, &extra);
-        c.name = nm;
-    }
-    const u32 ncfg = in.ncfg;
-    c.args = K.mem->get<KArg>(ncfg + 1);
-    K.arg_sname = K.mem->get<Span>(ncfg + 1);
-    if (!c.args || !K.arg_sname)
-        return false;
-    for (u32 l = in.lbeg + 1; l < in.lend; ++l) {
+    do {
         const LineRec &L = in.lines[l];
         if (L.role != LR_CONFIG)
-            continue;
+            break;
         Span w, rest;
         split_word(t, Span{L.off, L.len}, &w, &rest);
         Span key = w;
@@ -546,7 +533,7 @@ OD_NOINL bool parse_config(KCtx &K) {
             u32 nf = split_fields_spans(t, rest, f, 4);
             if (nf == 0 || nf > 3) {
                 diag(K, DG_CWS_COUNT, in.line_base + l + 1);
-                continue;
+                break;
             }
             for (u32 i = 0; i < nf; ++i) {
                 i64 v;
@@ -570,7 +557,7 @@ OD_NOINL bool parse_config(KCtx &K) {
             u32 nf = split_fields_spans(t, rest, f, 4);
             if (nf < 3) {
                 diag(K, DG_ARG_FIELDS, in.line_base + l + 1);
-                continue;
+                break;
             }
             KArg &a = c.args[c.nargs];
             a.name = f[0];
@@ -605,7 +592,35 @@ OD_NOINL bool parse_config(KCtx &K) {
             K.arg_sname[c.nargs] = a.name;
             c.nargs++;
         }
+    } while (false);
+}
+
+OD_NOINL bool parse_config(KCtx &K) {
+    const KIn &in = *K.in;
+    const u8 *t = in.t;
+    KConfig &c = K.cfg;
+    c.dims = 1;
+    c.cws[0] = c.cws[1] = c.cws[2] = 1;
+    c.useargs = 0;
+    c.nargs = 0;
+    c.fold_local_size = in.fold_local_size;
+    // name: second word of the .kernel line
+    {
+        const LineRec &L = in.lines[in.lbeg];
+        Span w, rest, nm, extra;
+        split_word(t, Span{L.off, L.len}, &w, &rest);
+        split_word(t, rest, &nm, &extra);
+        c.name = nm;
     }
+    const u32 ncfg = in.ncfg;
+    c.args = K.mem->get<KArg>(ncfg + 1);
+    K.arg_sname = K.mem->get<Span>(ncfg + 1);
+    if (!c.args || !K.arg_sname)
+        return false;
+    const LineRec *__restrict__ lines = in.lines;
+    for (u32 l = in.lbeg + 1, e = in.lend; l < e; ++l)
+        if (lines[l].role == LR_CONFIG)
+            config_line(K, l);
     return true;
 }
 
@@ -795,6 +810,18 @@ OD_INL KSize kernel_size(const LineRec *lines, const LineIns *lins, const Opnd *
     return z;
 }
 
+// parse_instruction's downgraded ParseErrors (asm_frontend.cpp:478), in
+// instruction order; out of the collection loop (rare).
+OD_NOINL void note_parse_failures(KCtx &K) {
+    for (u32 i = 0; i < K.nins; ++i) {
+        const Ins &I = K.ins[i];
+        if (!(I.flags & IF_PARSE_FAILED))
+            continue;
+        const Opnd &e = K.in->ops[I.op_start];
+        diag(K, DG_OPERAND, I.line, e.special, Span{e.r.a, e.r.b});
+    }
+}
+
 // parse_text + attach_trailing_labels (asm_frontend.cpp:486-521,
 // decompiler.cpp:20-31)
 OD_NOINL bool collect_instructions(KCtx &K) {
@@ -812,6 +839,7 @@ OD_NOINL bool collect_instructions(KCtx &K) {
     u32 *__restrict__ kl = K.kl;
     const u32 lbeg = in.lbeg, lend = in.lend, line_base = in.line_base;
     u32 ni = 0, nkl = 0, pend_b = 0;
+    u32 any_failed = 0;
     u32 last_line = line_base + lbeg + 1; // section.line
     for (u32 l = lbeg + 1; l < lend; ++l) {
         if (lines[l].role != LR_TEXT)
@@ -835,10 +863,7 @@ OD_NOINL bool collect_instructions(KCtx &K) {
         I.src.len = L.src_len;
         I.lab_b = pend_b;
         I.lab_n = nkl - pend_b;
-        if (L.flags & IF_PARSE_FAILED) { // parse_instruction's downgraded ParseError (asm_frontend.cpp:478)
-            const Opnd &e = ops[L.op_start];
-            diag(K, DG_OPERAND, I.line, e.special, Span{e.r.a, e.r.b});
-        }
+        any_failed |= L.flags & IF_PARSE_FAILED;
         u32 m = 0;
         I.xkind = L.prefix == PX_S ? (u8)exec_kind_of(L.root, L.prefix, L.flags, L.nops, ops + L.op_start, &m)
                                    : (u8)XK_NONE;
@@ -850,6 +875,8 @@ OD_NOINL bool collect_instructions(KCtx &K) {
     K.nins = ni;
     K.nkl = nkl;
     K.nins_real = K.nins;
+    if (any_failed)
+        note_parse_failures(K);
     if (K.nkl > pend_b) {
         Ins &I = K.ins[K.nins++];
         I.root = R_ENDPGM;
@@ -906,7 +933,7 @@ OD_INL int lmap_get(const KCtx &K, Span name) {
     return -1;
 }
 
-OD_INL int resolve_target(KCtx &K, const Ins &I) {
+OD_NOINL int resolve_target(KCtx &K, const Ins &I) {
     if (I.nops == 0 || op_at(K, I, 0).kind != OK_SYMBOL) {
         K.failed = true;
         diag(K, DG_BR_NOLABEL, I.line);
@@ -921,22 +948,47 @@ OD_INL int resolve_target(KCtx &K, const Ins &I) {
     return b;
 }
 
-OD_NOINL void mark_reachable(KCtx &K) {
-    for (u32 b = 0; b < K.nblk; ++b)
-        K.blk[b].reachable = 0;
-    if (!K.nblk)
-        return;
-    u32 sp = 0;
-    K.work[sp++] = 0;
+// Returns the number of reachable blocks.
+OD_NOINL u32 mark_reachable(KCtx &K) {
+    Block *__restrict__ blk = K.blk;
+    u32 *__restrict__ work = K.work;
+    const u32 nb = K.nblk;
+    for (u32 b = 0; b < nb; ++b)
+        blk[b].reachable = 0;
+    if (!nb)
+        return 0;
+    u32 sp = 0, nr = 0;
+    work[sp++] = 0;
     while (sp) {
-        u32 id = K.work[--sp];
-        Block &B = K.blk[id];
+        u32 id = work[--sp];
+        Block &B = blk[id];
         if (B.reachable)
             continue;
         B.reachable = 1;
+        ++nr;
         for (u32 s = 0; s < B.nsucc; ++s)
-            K.work[sp++] = (u32)B.succ[s];
+            work[sp++] = (u32)B.succ[s];
     }
+    return nr;
+}
+
+// build_cfg's conditional-branch ParseErrors (cfg.cpp:125-130).
+OD_NOINL void cbranch_error(KCtx &K, const Ins &last, bool unsupported) {
+    K.failed = true;
+    if (unsupported) { // the mnemonic: "s_" + root (+ suffixes); the host strips it
+        Span w, rest;
+        split_word(K.in->t, last.src, &w, &rest);
+        diag(K, DG_CBR_UNSUP, last.line, 0, w);
+    } else {
+        diag(K, DG_CBR_END, last.line);
+    }
+}
+
+// build_cfg's "unreachable code" notes (cfg.cpp:152-154), block order.
+OD_NOINL void note_unreachable(KCtx &K) {
+    for (u32 b = 0; b < K.nblk; ++b)
+        if (!K.blk[b].reachable)
+            diag(K, DG_UNREACHABLE, K.ins[K.blk[b].ib].line);
 }
 
 // build_cfg  cfg.cpp:64-156
@@ -1028,14 +1080,7 @@ OD_NOINL bool build_cfg(KCtx &K) {
             default: break;
             }
             if (cc < 0 || next < 0) {
-                K.failed = true;
-                if (cc < 0) { // the mnemonic: "s_" + root (+ suffixes) -> the host strips it
-                    Span w, rest;
-                    split_word(K.in->t, last.src, &w, &rest);
-                    diag(K, DG_CBR_UNSUP, last.line, 0, w);
-                } else {
-                    diag(K, DG_CBR_END, last.line);
-                }
+                cbranch_error(K, last, cc < 0);
                 break;
             }
             t.kind = T_COND;
@@ -1059,10 +1104,8 @@ OD_NOINL bool build_cfg(KCtx &K) {
     }
     if (K.failed)
         return true;
-    mark_reachable(K);
-    for (u32 b = 0; b < K.nblk; ++b)
-        if (!K.blk[b].reachable)
-            diag(K, DG_UNREACHABLE, K.ins[K.blk[b].ib].line);
+    if (mark_reachable(K) < K.nblk)
+        note_unreachable(K);
     return true;
 }
 

@@ -231,7 +231,7 @@ OD_INL u32 operand_reg_id(const Opnd &o) {
     }
 }
 
-OD_NOINL u32 read_pair(KCtx &K, const Opnd &o);
+OD_INL u32 read_pair(KCtx &K, const Opnd &o);
 
 // read_operand  sym_state.cpp:205-227
 OD_HOT u32 read_operand(KCtx &K, const Opnd &o) {
