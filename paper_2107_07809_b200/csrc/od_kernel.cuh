@@ -304,6 +304,8 @@ struct KCtx {
     Block *blk;
     u32 nblk, blk_cap;
     u32 *stamp;  // per-block traversal stamps
+    u32 *sx;     // compact successor pairs (kNoSucc = none), kept in sync with Block::succ
+    u32 *rbits;  // reachability bitmap (BasicBlock::reachable)
     u32 stamp_gen;
     u32 *work;   // block work stack
 
@@ -335,6 +337,7 @@ struct KCtx {
     i32 entry_r;
     u32 root_r;
     bool reduced;
+    u32 nif;      // IfThen / IfElse merges (joins need liveness)
 
     // liveness
     u32 *live_in; // [nblk][12]
@@ -948,26 +951,41 @@ OD_NOINL int resolve_target(KCtx &K, const Ins &I) {
     return b;
 }
 
+constexpr u32 kNoSucc = 0xffffffffu;
+
+OD_INL void sync_succ(KCtx &K, u32 b) {
+    const Block &B = K.blk[b];
+    K.sx[2 * b] = B.nsucc > 0 ? (u32)B.succ[0] : kNoSucc;
+    K.sx[2 * b + 1] = B.nsucc > 1 ? (u32)B.succ[1] : kNoSucc;
+}
+OD_INL bool blk_reach(const KCtx &K, u32 b) { return (K.rbits[b >> 5] >> (b & 31)) & 1; }
+OD_INL void set_reach(KCtx &K, u32 b) { K.rbits[b >> 5] |= 1u << (b & 31); }
+
 // Returns the number of reachable blocks.
 OD_NOINL u32 mark_reachable(KCtx &K) {
-    Block *__restrict__ blk = K.blk;
+    // cfg.mark_reachable (cfg.cpp:23-39) over the compact successor pairs
+    u32 *__restrict__ rb = K.rbits;
+    const u32 *__restrict__ sx = K.sx;
     u32 *__restrict__ work = K.work;
     const u32 nb = K.nblk;
-    for (u32 b = 0; b < nb; ++b)
-        blk[b].reachable = 0;
+    for (u32 w = 0; w < (nb + 31) / 32; ++w)
+        rb[w] = 0;
     if (!nb)
         return 0;
     u32 sp = 0, nr = 0;
     work[sp++] = 0;
     while (sp) {
-        u32 id = work[--sp];
-        Block &B = blk[id];
-        if (B.reachable)
+        const u32 id = work[--sp];
+        const u32 bit = 1u << (id & 31);
+        if (rb[id >> 5] & bit)
             continue;
-        B.reachable = 1;
+        rb[id >> 5] |= bit;
         ++nr;
-        for (u32 s = 0; s < B.nsucc; ++s)
-            work[sp++] = (u32)B.succ[s];
+        const u32 a = sx[2 * id], b = sx[2 * id + 1];
+        if (a != kNoSucc)
+            work[sp++] = a;
+        if (b != kNoSucc)
+            work[sp++] = b;
     }
     return nr;
 }
@@ -987,7 +1005,7 @@ OD_NOINL void cbranch_error(KCtx &K, const Ins &last, bool unsupported) {
 // build_cfg's "unreachable code" notes (cfg.cpp:152-154), block order.
 OD_NOINL void note_unreachable(KCtx &K) {
     for (u32 b = 0; b < K.nblk; ++b)
-        if (!K.blk[b].reachable)
+        if (!blk_reach(K, b))
             diag(K, DG_UNREACHABLE, K.ins[K.blk[b].ib].line);
 }
 
@@ -999,6 +1017,8 @@ OD_NOINL bool build_cfg(KCtx &K) {
         K.blk_cap = K.in->nblk_cap;
     K.blk = K.mem->get<Block>(K.blk_cap);
     K.stamp = K.mem->get<u32>(K.blk_cap);
+    K.sx = K.mem->get<u32>(2 * K.blk_cap);
+    K.rbits = K.mem->get<u32>(K.blk_cap / 32 + 1);
     K.work = K.mem->get<u32>(2 * K.blk_cap + 4);
     K.supp = K.mem->get<u8>(n + 1);
     u32 lc = 16;
@@ -1006,7 +1026,7 @@ OD_NOINL bool build_cfg(KCtx &K) {
         lc <<= 1;
     K.lmap_cap = lc;
     K.lmap = K.mem->get<u32>(2 * lc);
-    if (!K.blk || !K.stamp || !K.work || !K.supp || !K.lmap)
+    if (!K.blk || !K.stamp || !K.work || !K.supp || !K.lmap || !K.sx || !K.rbits)
         return false;
     for (u32 i = 0; i < 2 * lc; ++i)
         K.lmap[i] = 0;
@@ -1026,6 +1046,8 @@ OD_NOINL bool build_cfg(KCtx &K) {
         B.reachable = 1;
         B.absorbed = 0;
         B.xfront.kind = B.xback.kind = XK_NONE;
+        sync_succ(K, 0);
+        K.rbits[0] = 1;
         return true;
     }
     // leaders
@@ -1104,6 +1126,8 @@ OD_NOINL bool build_cfg(KCtx &K) {
     }
     if (K.failed)
         return true;
+    for (u32 b = 0; b < K.nblk; ++b)
+        sync_succ(K, b);
     if (mark_reachable(K) < K.nblk)
         note_unreachable(K);
     return true;
@@ -1156,6 +1180,9 @@ OD_NOINL u32 split_block(KCtx &K, u32 id, u32 at) {
     B.term.line = K.ins[N.ib].line;
     B.succ[0] = (i32)nid;
     B.nsucc = 1;
+    sync_succ(K, id);
+    sync_succ(K, nid);
+    set_reach(K, nid); // BasicBlock default (reachability is not recomputed)
     return nid;
 }
 
@@ -1233,14 +1260,11 @@ OD_NOINL u32 mask_stops(KCtx &K, const i32 *starts, u32 nstarts, u32 mask, i32 h
 
 // retarget_preds  structurizer.cpp:512-525
 OD_NOINL void retarget_preds(KCtx &K, i32 from, i32 to, i32 keep) {
+    const u32 f = (u32)from;
     for (u32 p = 0; p < K.nblk; ++p) {
-        Block &P = K.blk[p];
-        bool is_pred = false;
-        for (u32 s = 0; s < P.nsucc; ++s)
-            if (P.succ[s] == from)
-                is_pred = true;
-        if (!is_pred || (i32)p == keep)
+        if ((K.sx[2 * p] != f && K.sx[2 * p + 1] != f) || (i32)p == keep)
             continue;
+        Block &P = K.blk[p];
         for (u32 s = 0; s < P.nsucc; ++s)
             if (P.succ[s] == from)
                 P.succ[s] = to;
@@ -1248,6 +1272,7 @@ OD_NOINL void retarget_preds(KCtx &K, i32 from, i32 to, i32 keep) {
             P.term.taken = to;
         if (P.term.not_taken == from)
             P.term.not_taken = to;
+        sync_succ(K, p);
     }
 }
 
@@ -1291,6 +1316,7 @@ OD_NOINL bool apply_mask_pattern(KCtx &K, const MaskPattern &pat, u32 *touched, 
             retarget_preds(K, invert, join, pat.header);
             ib.absorbed = 1;
             ib.nsucc = 0;
+            sync_succ(K, (u32)invert);
             reach_may_shrink = true;
         } else {
             i32 rstop = -1;
@@ -1327,6 +1353,7 @@ OD_NOINL bool apply_mask_pattern(KCtx &K, const MaskPattern &pat, u32 *touched, 
     h.succ[0] = h.term.taken;
     h.succ[1] = h.term.not_taken;
     h.nsucc = 2;
+    sync_succ(K, (u32)pat.header);
     touched[(*ntouched)++] = (u32)pat.header;
     // cfg.mark_reachable() (structurizer.cpp:606).  Every new edge targets a
     // block the mask walk reached from the (reachable) header, so
@@ -1338,10 +1365,10 @@ OD_NOINL bool apply_mask_pattern(KCtx &K, const MaskPattern &pat, u32 *touched, 
 #ifdef OD_HOST_CHECK
     else {
         for (u32 b = 0; b < K.nblk; ++b)
-            K.stamp[b] = K.blk[b].reachable;
+            K.stamp[b] = blk_reach(K, b);
         mark_reachable(K);
         for (u32 b = 0; b < K.nblk; ++b)
-            if (K.stamp[b] != K.blk[b].reachable)
+            if (K.stamp[b] != (u32)blk_reach(K, b))
                 abort();
         K.stamp_gen = 0;
         for (u32 b = 0; b < K.nblk; ++b)
@@ -1357,7 +1384,7 @@ OD_NOINL void normalize(KCtx &K) {
     const u32 nb = K.nblk;
     for (u32 scan = 0; scan < nb; ++scan) {
         Block &b = K.blk[scan];
-        if (!b.reachable || b.xback.kind == XK_NONE)
+        if (!blk_reach(K, scan) || b.xback.kind == XK_NONE)
             continue;
         const XOp op = b.xback;
         if (op.kind != XK_SAVE || K.supp[b.ib + op.index])
@@ -1532,7 +1559,7 @@ OD_NOINL bool build_regions(KCtx &K) {
     for (u32 b = 0; b < K.nblk; ++b) {
         by_block[b] = 0;
         const Block &B = K.blk[b];
-        if (!B.reachable || B.absorbed)
+        if (!blk_reach(K, b) || B.absorbed)
             continue;
         u32 r = make_region(K, RK_BLOCK);
         K.rg[r].block_id = (i32)b;
@@ -1737,6 +1764,7 @@ OD_NOINL u32 match_if_else(KCtx &K, u32 r) {
         return 0;
     }
     u32 m = make_region(K, RK_IFELSE);
+    K.nif++;
     set_cond(K, m, term, false);
     K.rg[m].join_block = entry_block(K, j);
     u32 ch[4] = {r, then_r, else_r, j};
@@ -1781,6 +1809,7 @@ OD_NOINL u32 match_if(KCtx &K, u32 r) {
         return 0;
     }
     u32 m = make_region(K, RK_IFTHEN);
+    K.nif++;
     set_cond(K, m, term, then_is_taken);
     K.rg[m].join_block = entry_block(K, j);
     u32 ch[3] = {r, then_r, j};

@@ -1184,7 +1184,7 @@ OD_NOINL void lower_goto(KCtx &K, u32 out) {
     diag(K, DG_GOTO, 0);
     for (u32 k = 0; k < K.nblk && !K.oom && !K.E.oom; ++k) {
         u32 id = k;
-        if (k > 0 && (!K.blk[id].reachable || K.blk[id].absorbed))
+        if (k > 0 && (!blk_reach(K, id) || K.blk[id].absorbed))
             continue;
         const Block &B = K.blk[id];
         u32 l = new_stmt(K, SK_LABEL);
@@ -1423,7 +1423,7 @@ OD_INL u64 arena_budget(const KSize &z, u32 s) {
     t += (z.ncfg + 1) * (sizeof(KArg) + sizeof(Span));       // config
     t += (ni + 1) * sizeof(Ins) + (z.nlab + 1) * 4;           // instructions, labels
     t += (8 + z.ncfg) * sizeof(AbiEntry);                     // ABI map
-    t += b * (sizeof(Block) + 4) + (2 * b + 4) * 4 + (ni + 1); // blocks, stamps, work, supp
+    t += b * (sizeof(Block) + 4) + (2 * b + 4) * 4 + (ni + 1) + b * 8 + (b / 32 + 1) * 4; // blocks, stamps, work, supp, sx, rbits
     u64 lc = 16;
     while (lc < 2 * ((u64)z.nlab + 1))
         lc <<= 1;
@@ -1539,7 +1539,12 @@ OD_NOINL void dk_front(KState &S) {
     }
     OD_PROF(3, tp);
     out.structured = K.reduced ? 1 : 0;
-    OD_CHECK(liveness(K));
+    // live_in_sets is only read at if-joins (merge_at_join, lower.cpp:143-157):
+    // kernels whose region tree has no if (straight-line, or goto form) skip it.
+    if (K.reduced && K.nif)
+        OD_CHECK(liveness(K));
+    else
+        K.live_in = nullptr;
     OD_PROF(4, tp);
 
     // Carve the remaining arena into the dynamic pools.
