@@ -840,7 +840,7 @@ struct Step {
     }
 
     // step  sym_state.cpp:840-864
-    OD_NOINL void run() {
+    OD_INL void run() {
         if (I.flags & IF_PARSE_FAILED) {
             fallback();
             return;
