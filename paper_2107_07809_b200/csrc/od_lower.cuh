@@ -504,16 +504,27 @@ struct Step {
         if (nn > 0 && op(0).kind == OK_SPECIAL &&
             (op(0).special == SP_EXEC || op(0).special == SP_EXEC_LO || op(0).special == SP_EXEC_HI))
             return false;
-        if (r == R_LOAD_DWORD) return scalar_load(1), true;
-        if (r == R_LOAD_DWORDX2) return scalar_load(2), true;
-        if (r == R_LOAD_DWORDX4) return scalar_load(4), true;
-        if (r == R_MOV && nn >= 2) {
+        switch (r) { // one jump table (instruction fetch)
+        case R_LOAD_DWORD: return scalar_load(1), true;
+        case R_LOAD_DWORDX2: return scalar_load(2), true;
+        case R_LOAD_DWORDX4: return scalar_load(4), true;
+        case R_MOV:
+            if (nn < 2)
+                return false;
+            {
             DT t = suffix_type0(I, DT_B32);
             u32 v = dt_bits(t) == 64 ? read64(op(1)) : read(op(1));
             write(op(0), v, v ? ty(v) : DT_UNKNOWN);
             return true;
         }
-        if ((r == R_ADD || r == R_SUB || r == R_MUL || r == R_ADDK || r == R_MULK) && nn >= 2) {
+        case R_ADD:
+        case R_SUB:
+        case R_MUL:
+        case R_ADDK:
+        case R_MULK:
+            if (nn < 2)
+                return false;
+            {
             const bool k = r == R_ADDK || r == R_MULK;
             if (!k && nn < 3)
                 return false;
@@ -526,7 +537,13 @@ struct Step {
             invalidate_slot(K, kRegIdScc, 1);
             return true;
         }
-        if ((r == R_AND || r == R_OR || r == R_XOR || r == R_ANDN2) && nn >= 3) {
+        case R_AND:
+        case R_OR:
+        case R_XOR:
+        case R_ANDN2:
+            if (nn < 3)
+                return false;
+            {
             DT t = suffix_type0(I, DT_B32);
             const bool wide = dt_bits(t) == 64;
             u32 a = wide ? read64(op(1)) : read(op(1));
@@ -544,7 +561,12 @@ struct Step {
             invalidate_slot(K, kRegIdScc, 1);
             return true;
         }
-        if ((r == R_LSHL || r == R_LSHR || r == R_ASHR) && nn >= 3) {
+        case R_LSHL:
+        case R_LSHR:
+        case R_ASHR:
+            if (nn < 3)
+                return false;
+            {
             DT t = suffix_type0(I, DT_B32);
             const bool wide = dt_bits(t) == 64;
             u32 a = wide ? read64(op(1)) : read(op(1));
@@ -553,6 +575,9 @@ struct Step {
             write(op(0), K.E.binary(o, a, b, t), t);
             invalidate_slot(K, kRegIdScc, 1);
             return true;
+        }
+        default:
+            break;
         }
         if (I.rflags & RF_CMP)
             return compare(false);
@@ -583,12 +608,21 @@ struct Step {
     OD_NOINL bool vector() {
         const u32 r = I.root;
         const u32 nn = n();
-        if (r == R_MOV && nn >= 2) {
+        // one jump table instead of a chain of tests spread over the handlers
+        // (the lowering pass is bound by instruction fetch)
+        switch (r) {
+        case R_MOV:
+            if (nn < 2)
+                return false;
+            {
             u32 v = read(op(1));
             write(op(0), v, v ? ty(v) : DT_B32);
             return true;
         }
-        if (!(I.flags & IF_PARSE_FAILED) && r == R_CNDMASK && nn >= 4 && op_is_vreg(op(0))) {
+        case R_CNDMASK:
+            if ((I.flags & IF_PARSE_FAILED) || nn < 4 || !op_is_vreg(op(0)))
+                return false;
+            {
             u32 cond = read(op(3));
             u32 a = read(op(1));
             u32 b = read(op(2));
@@ -596,7 +630,12 @@ struct Step {
             write(op(0), K.E.ternary(cond, b, a, t), t);
             return true;
         }
-        if ((r == R_ADD || r == R_SUB || r == R_SUBREV) && nn >= 3) {
+        case R_ADD:
+        case R_SUB:
+        case R_SUBREV:
+            if (nn < 3)
+                return false;
+            {
             u32 src0 = 1;
             bool carry = false;
             if (op_is_special(op(1), SP_VCC) || op_is_sreg_pair(op(1))) {
@@ -643,7 +682,10 @@ struct Step {
                 K.pend.lo_version = K.regs[kRegIdVgpr0 + pd.lo_vgpr].version;
             return true;
         }
-        if (r == R_ADDC && nn >= 5) {
+        case R_ADDC:
+            if (nn < 5)
+                return false;
+            {
             const Pending pd = K.pend;
             K.pend.valid = 0;
             K.pend.base64 = K.pend.addend = 0;
@@ -693,7 +735,12 @@ struct Step {
             invalidate_slot(K, operand_reg_id(op(1)), op(1).count);
             return true;
         }
-        if ((r == R_MUL || r == R_MUL_LO || r == R_MUL_HI) && nn >= 3) {
+        case R_MUL:
+        case R_MUL_LO:
+        case R_MUL_HI:
+            if (nn < 3)
+                return false;
+            {
             const u32 narrow = src24();
             if (narrow == 2)
                 return false;
@@ -712,7 +759,10 @@ struct Step {
             write(op(0), K.E.binary(o, a, b, t), t);
             return true;
         }
-        if (r == R_MAC && nn >= 3) {
+        case R_MAC:
+            if (nn < 3)
+                return false;
+            {
             DT t = suffix_type0(I, DT_F32);
             u32 a = rd(1, t);
             u32 b = rd(2, t);
@@ -721,7 +771,10 @@ struct Step {
             write(op(0), v, t);
             return true;
         }
-        if (r == R_MAD && nn >= 4) {
+        case R_MAD:
+            if (nn < 4)
+                return false;
+            {
             const u32 narrow = src24();
             if (narrow == 2)
                 return false;
@@ -737,9 +790,15 @@ struct Step {
             write(op(0), v, t);
             return true;
         }
-        if ((r == R_LSHLREV || r == R_LSHRREV || r == R_ASHRREV || r == R_LSHL || r == R_LSHR ||
-             r == R_ASHR) &&
-            nn >= 3) {
+        case R_LSHLREV:
+        case R_LSHRREV:
+        case R_ASHRREV:
+        case R_LSHL:
+        case R_LSHR:
+        case R_ASHR:
+            if (nn < 3)
+                return false;
+            {
             const bool rev = r == R_LSHLREV || r == R_LSHRREV || r == R_ASHRREV;
             u32 shift = read(op(rev ? 1 : 2));
             u32 value = read(op(rev ? 2 : 1));
@@ -752,9 +811,17 @@ struct Step {
             write(op(0), K.E.binary(o, coerce(value, t), shift, t), t);
             return true;
         }
-        if ((r == R_AND || r == R_OR || r == R_XOR) && nn >= 3) {
+        case R_AND:
+        case R_OR:
+        case R_XOR:
+            if (nn < 3)
+                return false;
+            {
             bin(r == R_AND ? O_AND : r == R_OR ? O_OR : O_XOR, suffix_type0(I, DT_B32), 1, 2);
             return true;
+        }
+        default:
+            break;
         }
         if (I.rflags & RF_CMP)
             return compare(true);
@@ -1265,7 +1332,7 @@ OD_NOINL void emit_simple(KCtx &K, Writer &w, const Stmt &s, u32 depth) {
         w.lit(" = ");
         u32 v = s.b;
         if (v && is_bit_reinterpret(K.E.n[v].type, s.c)) {
-            w.puts(cast_name(s.c));
+            put_cast_name(w, s.c);
             w.put('(');
             render_expr(w, rc, v, 0);
             w.put(')');
