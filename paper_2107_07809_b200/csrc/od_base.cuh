@@ -364,15 +364,7 @@ struct Writer {
         const u32 k = n;
         if (k + len <= cap) {
             u8 *d = p + k;
-            u32 i = 0;
-            for (; i + 4 <= len; i += 4) {
-                const u8 a = s[i], b = s[i + 1], c = s[i + 2], e = s[i + 3];
-                d[i] = a;
-                d[i + 1] = b;
-                d[i + 2] = c;
-                d[i + 3] = e;
-            }
-            for (; i < len; ++i)
+            for (u32 i = 0; i < len; ++i)
                 d[i] = s[i];
         } else {
             for (u32 i = 0; i < len; ++i)

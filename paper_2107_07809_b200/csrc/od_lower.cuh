@@ -1332,7 +1332,7 @@ OD_NOINL void emit_simple(KCtx &K, Writer &w, const Stmt &s, u32 depth) {
         w.lit(" = ");
         u32 v = s.b;
         if (v && is_bit_reinterpret(K.E.n[v].type, s.c)) {
-            put_cast_name(w, s.c);
+            w.puts(cast_name(s.c));
             w.put('(');
             render_expr(w, rc, v, 0);
             w.put(')');

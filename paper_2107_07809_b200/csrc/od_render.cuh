@@ -237,31 +237,12 @@ OD_INL void render_scalar_type(Writer &w, DT t) {
         base = B_UNSIGNED;
     switch (base) {
     case B_VOID: w.lit("void"); return;
-    case B_FLOAT:
-        if (bits == 64)
-            w.lit("double");
-        else
-            w.lit("float");
-        return;
+    case B_FLOAT: w.puts(bits == 64 ? "double" : "float"); return;
     case B_SIGNED:
-        if (bits == 8)
-            w.lit("char");
-        else if (bits == 16)
-            w.lit("short");
-        else if (bits == 64)
-            w.lit("long");
-        else
-            w.lit("int");
+        w.puts(bits == 8 ? "char" : bits == 16 ? "short" : bits == 64 ? "long" : "int");
         return;
     default:
-        if (bits == 8)
-            w.lit("uchar");
-        else if (bits == 16)
-            w.lit("ushort");
-        else if (bits == 64)
-            w.lit("ulong");
-        else
-            w.lit("uint");
+        w.puts(bits == 8 ? "uchar" : bits == 16 ? "ushort" : bits == 64 ? "ulong" : "uint");
         return;
     }
 }
@@ -311,19 +292,6 @@ OD_INL const char *builtin_name(u32 fn) {
     case F_NUM_GROUPS: return "get_num_groups";
     case F_GLOBAL_OFFSET: return "get_global_offset";
     default: return "get_work_dim";
-    }
-}
-
-OD_NOINL void put_builtin_name(Writer &w, u32 fn) {
-    switch (fn) {
-    case F_GLOBAL_ID: w.lit("get_global_id"); return;
-    case F_LOCAL_ID: w.lit("get_local_id"); return;
-    case F_GROUP_ID: w.lit("get_group_id"); return;
-    case F_GLOBAL_SIZE: w.lit("get_global_size"); return;
-    case F_LOCAL_SIZE: w.lit("get_local_size"); return;
-    case F_NUM_GROUPS: w.lit("get_num_groups"); return;
-    case F_GLOBAL_OFFSET: w.lit("get_global_offset"); return;
-    default: w.lit("get_work_dim"); return;
     }
 }
 
@@ -460,22 +428,6 @@ OD_INL const char *cast_name(DT to) {
     return dt_bits(to) == 64 ? "as_ulong" : (dt_is_signed(to) ? "as_int" : "as_uint");
 }
 
-OD_NOINL void put_cast_name(Writer &w, DT to) {
-    if (dt_is_float(to)) {
-        if (dt_bits(to) == 64)
-            w.lit("as_double");
-        else
-            w.lit("as_float");
-        return;
-    }
-    if (dt_bits(to) == 64)
-        w.lit("as_ulong");
-    else if (dt_is_signed(to))
-        w.lit("as_int");
-    else
-        w.lit("as_uint");
-}
-
 // Render tasks (explicit stack, 64-bit entries: kind | arg<<8 | node<<32).
 enum RTask : u32 { RT_NODE = 0, RT_SA, RT_CHAR, RT_STR, RT_NAME };
 enum RStr : u32 { S_COMMA = 0, S_SHR32, S_QMARK, S_COLON, S_BINOP_BASE = 16 };
@@ -487,40 +439,6 @@ OD_INL const char *rstr(u32 id) {
     case S_QMARK: return " ? ";
     case S_COLON: return " : ";
     default: return binop_text(id - S_BINOP_BASE);
-    }
-}
-
-// The same strings with compile-time lengths (no strlen pass per write).
-OD_NOINL void put_rstr(Writer &w, u32 id) {
-    switch (id) {
-    case S_COMMA: w.lit(", "); return;
-    case S_SHR32: w.lit(" >> 32)"); return;
-    case S_QMARK: w.lit(" ? "); return;
-    case S_COLON: w.lit(" : "); return;
-    default: break;
-    }
-    switch (id - S_BINOP_BASE) {
-    case O_ADD: w.lit(" + "); return;
-    case O_SUB: w.lit(" - "); return;
-    case O_MUL: w.lit(" * "); return;
-    case O_DIV: w.lit(" / "); return;
-    case O_AND: w.lit(" & "); return;
-    case O_OR: w.lit(" | "); return;
-    case O_XOR: w.lit(" ^ "); return;
-    case O_SHL: w.lit(" << "); return;
-    case O_LSHR:
-    case O_ASHR: w.lit(" >> "); return;
-    case O_CMPEQ: w.lit(" == "); return;
-    case O_CMPNE: w.lit(" != "); return;
-    case O_CMPLT:
-    case O_CMPLTU: w.lit(" < "); return;
-    case O_CMPLE:
-    case O_CMPLEU: w.lit(" <= "); return;
-    case O_CMPGT:
-    case O_CMPGTU: w.lit(" > "); return;
-    case O_CMPGE:
-    case O_CMPGEU: w.lit(" >= "); return;
-    default: w.lit(" ? "); return;
     }
 }
 
@@ -673,7 +591,7 @@ OD_NOINL void render_expr(Writer &w, RenderCtx &rc, u32 root, int min_prec = 0) 
             continue;
         }
         if (kind == RT_STR) {
-            put_rstr(w, arg);
+            w.puts(rstr(arg));
             continue;
         }
         if (kind == RT_SA) {
@@ -693,15 +611,9 @@ OD_NOINL void render_expr(Writer &w, RenderCtx &rc, u32 root, int min_prec = 0) 
             }
             w.put('(');
             if (cu)
-                if (dt_bits(ct) == 64)
-                    w.lit("ulong");
-                else
-                    w.lit("uint");
+                w.puts(dt_bits(ct) == 64 ? "ulong" : "uint");
             else
-                if (dt_bits(ct) == 64)
-                    w.lit("long");
-                else
-                    w.lit("int");
+                w.puts(dt_bits(ct) == 64 ? "long" : "int");
             w.put(')');
             ts.push(RT_NODE, kUnary, e);
             continue;
@@ -716,7 +628,7 @@ OD_NOINL void render_expr(Writer &w, RenderCtx &rc, u32 root, int min_prec = 0) 
         switch (x.kind) {
         case E_CONST: render_const(w, E, e); break;
         case E_BUILTIN:
-            put_builtin_name(w, x.op);
+            w.puts(builtin_name(x.op));
             w.put('(');
             if (x.op != F_WORK_DIM)
                 w.put_u64(x.x);
@@ -750,7 +662,7 @@ OD_NOINL void render_expr(Writer &w, RenderCtx &rc, u32 root, int min_prec = 0) 
                 break;
             default: // U_CAST
                 if (x.a && is_bit_reinterpret(E.n[x.a].type, x.type)) {
-                    put_cast_name(w, x.type);
+                    w.puts(cast_name(x.type));
                     w.put('(');
                     ts.push(RT_CHAR, ')', 0);
                     ts.push(RT_NODE, 0, x.a);
