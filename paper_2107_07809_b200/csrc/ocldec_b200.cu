@@ -285,14 +285,22 @@ __global__ void __launch_bounds__(256) k_decode(const u8 *__restrict__ t, u64 le
 // Per-kernel sizes (a pass over the kernel's decoded lines), size key and
 // arena budget.
 __global__ void k_ksize(const u32 *kstart, u32 nk, u32 nlines, const LineRec *lines, const LineIns *lins,
-                        const Opnd *ops, KSize *sizes, u32 *key, u64 *budget) {
+                        const Opnd *ops, KSize *sizes, u32 *key, u64 *budget, u32 group) {
     u32 k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= nk)
         return;
     const u32 b = kstart[k], e = k + 1 < nk ? kstart[k + 1] : nlines;
     const KSize z = kernel_size(lines, lins, ops, b, e);
     sizes[k] = z;
-    key[k] = z.n;
+    // sort key: lines, optionally grouped by class (straight-line kernels
+    // first) so an SM's resident kernels share their hot code
+    const u32 n15 = z.n < 0x3fffu ? z.n : 0x3fffu;
+    u32 cls = 0;
+    if (group == 1)
+        cls = z.nb > 4 ? 0u : 2u;                           // straight-line first, then branching
+    else if (group == 2)
+        cls = z.nb <= 4 ? 3u : (z.nb <= 24 ? 2u : (z.nb <= 96 ? 1u : 0u)); // by block-count class
+    key[k] = group ? (cls << 14) | n15 : z.n;
     budget[k] = kernel_budget(z, 1);
 }
 
@@ -537,6 +545,7 @@ struct ocldec_b200_session {
     bool prof_on = false;
     u32 lanes_front = 32, lanes_lower = 32, lanes_emit = 32; // 32 / kernels per warp, per phase
     u32 smem_front = 0, smem_lower = 0, smem_emit = 0;        // occupancy limiters (dynamic smem)
+    u32 group_class = 0;                                      // wave order grouped by kernel class
     u64 out_len = 0;
     u64 nk_total = 0;
     u32 only_len = 0;
@@ -769,7 +778,7 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
         return -3;
     a.sizes = P<KSize>(s->ksizes);
     k_ksize<<<kg, kb, 0, st>>>(P<u32>(s->kstart), nk, nlines, P<LineRec>(s->lines), P<LineIns>(s->lins),
-                               P<Opnd>(s->ops), P<KSize>(s->ksizes), key, P<u64>(s->budget));
+                               P<Opnd>(s->ops), P<KSize>(s->ksizes), key, P<u64>(s->budget), s->group_class);
     CK(cudaMemsetAsync(s->hist.p, 0, kSizeBuckets * 4ull, st));
     k_hist<<<kg, kb, 0, st>>>(key, nk, P<u32>(s->hist));
     if (scan_exclusive(s, kSizeBuckets, SU32{0}, AddU32{}, U32Load{P<u32>(s->hist)},
@@ -1060,6 +1069,10 @@ int session_init(ocldec_b200_session *s, int device, size_t arena_bytes) {
         u32 occ = e && *e ? (u32)atoi(e) : 0;
         return occ ? (u32)((200u * 1024u) / occ) & ~1023u : 0u;
     };
+    {
+        const char *g = getenv("OCLDEC_B200_GROUP"); // 0 size only, 1 straight/branching (default), 2 block classes
+        s->group_class = g && *g ? (u32)(*g - '0') : 2u;
+    }
     s->smem_front = occ_smem("OCLDEC_B200_OCC_FRONT");
     s->smem_lower = occ_smem("OCLDEC_B200_OCC_LOWER");
     s->smem_emit = occ_smem("OCLDEC_B200_OCC_EMIT");
