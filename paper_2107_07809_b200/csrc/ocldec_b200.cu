@@ -334,6 +334,59 @@ __global__ void k_interleave(const u32 *order, const u64 *sb, u32 n, u32 *order_
     sb_out[p] = sb[i];
 }
 
+// Class of a kernel after k_front (the code the next launches run): 0 done
+// (failed / skipped), 1 straight-line, 2 structured with ifs, 3 goto form.
+struct Cnt4 {
+    u32 c[4];
+    __device__ static Cnt4 shfl_up(Cnt4 x, int d) {
+        Cnt4 r;
+        for (int q = 0; q < 4; ++q)
+            r.c[q] = __shfl_up_sync(0xffffffffu, x.c[q], d);
+        return r;
+    }
+};
+struct AddCnt4 {
+    __device__ Cnt4 operator()(Cnt4 a, Cnt4 b) const {
+        Cnt4 r;
+        for (int q = 0; q < 4; ++q)
+            r.c[q] = a.c[q] + b.c[q];
+        return r;
+    }
+};
+__device__ __forceinline__ u32 lower_class(const KState *g) {
+    if (g->done)
+        return 0;
+    if (!g->K.reduced)
+        return 3;
+    return g->K.nif ? 2 : 1;
+}
+struct ClsLoad {
+    const u8 *arena;
+    const u64 *boff;
+    u64 boff0;
+    __device__ Cnt4 operator()(u64 i) const {
+        const u32 c = lower_class(reinterpret_cast<const KState *>(arena + (boff[i] - boff0)));
+        Cnt4 v;
+        for (int q = 0; q < 4; ++q)
+            v.c[q] = q == (int)c ? 1u : 0u;
+        return v;
+    }
+};
+struct ClsStore {
+    u32 *perm;
+    const Cnt4 *total;
+    __device__ void operator()(u64 i, Cnt4 ex, Cnt4 v) const {
+        u32 base = 0;
+        for (int q = 0; q < 4; ++q) {
+            if (v.c[q]) {
+                perm[base + ex.c[q]] = (u32)i;
+                return;
+            }
+            base += total->c[q];
+        }
+    }
+};
+
 // ------------------------------------------------------------------ P4b
 struct OutLenLoad {
     const KRes *res;
@@ -540,7 +593,7 @@ struct ocldec_b200_session {
     size_t arena_bytes = 0;
     DevBuf text, tiles, tiles_off, nlpos, lines, lins, ops_cnt, labs_cnt, ops_off, labs_off, ops,
         labs, kstart, scan_tmp, scan_tot, counters, arena, stage, res, outoff, out, only, retry,
-        gen_len, gen_ninstr, gen_buf, gen_off, kmeta, order, budget, sbudget, boff, hist, prof, ksizes;
+        gen_len, gen_ninstr, gen_buf, gen_off, kmeta, order, budget, sbudget, boff, hist, prof, ksizes, perm, cnt4;
     u64 pool_bytes = 0;  // arena pool per decompile wave
     bool prof_on = false;
     u32 lanes_front = 32, lanes_lower = 32, lanes_emit = 32; // 32 / kernels per warp, per phase
@@ -850,7 +903,19 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
                     return -3;
             CK(cudaEventRecord(pe[0], ws));
             a.lanes_per = s->lanes_front;
+            a.perm = nullptr;
             k_front<<<grid(a.lanes_per), 128, s->smem_front, ws>>>(a);
+            if (!two && a.count >= 256 && s->group_class) {
+                // regroup the wave by what k_front found (straight / if-joins /
+                // goto form) so the later phases' resident kernels share code
+                if (ensure(s->perm, (u64)a.count * 4 + 16) || ensure(s->cnt4, 64))
+                    return -3;
+                if (scan_exclusive(s, a.count, Cnt4{{0, 0, 0, 0}}, AddCnt4{},
+                                   ClsLoad{a.arena, a.boff, a.boff0},
+                                   ClsStore{P<u32>(s->perm), P<Cnt4>(s->cnt4)}, P<Cnt4>(s->cnt4)))
+                    return -3;
+                a.perm = P<u32>(s->perm);
+            }
             CK(cudaEventRecord(pe[1], ws));
             a.lanes_per = s->lanes_lower;
             k_lower<<<grid(a.lanes_per), 128, s->smem_lower, ws>>>(a);
@@ -1263,7 +1328,7 @@ void ocldec_b200_session_destroy(ocldec_b200_session *s) {
                       &s->scan_tmp, &s->scan_tot, &s->counters, &s->arena, &s->stage, &s->res,
                       &s->outoff, &s->out, &s->only, &s->retry, &s->gen_len, &s->gen_ninstr,
                       &s->gen_buf, &s->gen_off, &s->kmeta, &s->order, &s->budget, &s->sbudget,
-                      &s->boff, &s->hist, &s->prof, &s->ksizes, &s->dpool, &s->dtop};
+                      &s->boff, &s->hist, &s->prof, &s->ksizes, &s->dpool, &s->dtop, &s->perm, &s->cnt4};
     for (DevBuf *b : bufs)
         if (b->p)
             cudaFree(b->p);

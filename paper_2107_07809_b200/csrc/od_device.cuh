@@ -48,6 +48,7 @@ struct DecompArgs {
     u32 only_len;
     u64 *prof;
     u32 lanes_per; // lanes per kernel: 32 / kernels-per-warp
+    const u32 *perm; // wave slot permutation for the launches after k_front (null: identity)
     Diag *dpool;   // diagnostic records of finished kernels
     u64 dcap;
     unsigned long long *dtop;
@@ -62,15 +63,19 @@ struct DecompArgs {
 // whose base holds its KState between the launches.
 struct Slot0 {
     u32 k;
+    u32 i;     // wave slot
     u8 *base;
 };
 __device__ __forceinline__ bool dk_slot(const DecompArgs &a, Slot0 *o) {
     const u32 g = blockIdx.x * blockDim.x + threadIdx.x;
     if ((threadIdx.x & 31) % a.lanes_per)
         return false;
-    const u32 i = g / a.lanes_per;
+    u32 i = g / a.lanes_per;
     if (i >= a.count)
         return false;
+    if (a.perm) // lower / fold / emit: slots grouped by the class k_front found
+        i = a.perm[i];
+    o->i = i;
     o->k = a.order[i];
     o->base = a.arena + (a.boff[i] - a.boff0);
     return true;

@@ -9,7 +9,7 @@ __global__ void __launch_bounds__(128, OD_MINB_FRONT) k_front(DecompArgs a) {
     if (!dk_slot(a, &sl))
         return;
     const u32 k = sl.k;
-    const u32 i = (blockIdx.x * blockDim.x + threadIdx.x) / a.lanes_per;
+    const u32 i = sl.i;
     KState *g = reinterpret_cast<KState *>(sl.base);
     const u64 kb = (sizeof(KState) + 255) & ~255ull;
     // Field-wise setup of the state in HBM.  (nvcc 12.9 miscompiled an
