@@ -355,10 +355,19 @@ struct Writer {
     // string literal: length known at compile time
     template <u32 N> OD_INL void lit(const char (&s)[N]) { putn(reinterpret_cast<const u8 *>(s), N - 1); }
     OD_NOINL void puts(const char *s) {
-        u32 len = 0;
-        while (s[len])
-            ++len;
-        putn(reinterpret_cast<const u8 *>(s), len);
+        u8 *const d = p;
+        const u32 c = cap;
+        u32 k = n;
+        bool ov = false;
+        for (u8 ch; (ch = (u8)*s) != 0; ++s, ++k) {
+            if (k < c)
+                d[k] = ch;
+            else
+                ov = true;
+        }
+        n = k;
+        if (ov)
+            overflow = true;
     }
     OD_NOINL void putn(const u8 *s, u32 len) {
         const u32 k = n;
