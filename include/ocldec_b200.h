@@ -26,15 +26,17 @@
 extern "C" {
 #endif
 
-#define OCLDEC_B200_ABI_VERSION 2
+#define OCLDEC_B200_ABI_VERSION 3
 
-/* DecompileOptions (decompiler.hpp:29-35).  abi_overrides and the DOT dumps
- * are not supported by this version (fields reserved). */
+/* DecompileOptions (decompiler.hpp:29-35).  The DOT dumps are not supported. */
 typedef struct ocldec_b200_options {
     int fold_local_size;     /* FoldOptions::fold_local_size (sym_state.hpp:27-29) */
     const char *only_kernel; /* restrict to one kernel by name, NULL = all        */
     int device;              /* CUDA device ordinal                               */
     size_t arena_bytes;      /* decompile arena pool per wave, 0 = default         */
+    const char *abi_map;     /* ABI override file text (the CLI's --abi-map), NULL = none:
+                                parse_abi_overrides abi_model.cpp:109-153 */
+    size_t abi_map_len;
 } ocldec_b200_options;
 
 /* DecompiledKernel (decompiler.hpp:39-52): the printed source and flags. */
@@ -69,12 +71,20 @@ typedef struct ocldec_b200_result {
     uint64_t ndiags;              /* DecompileResult::diagnostics, in sink order */
     ocldec_b200_diag *diags;
     char *diag_text;
+    uint64_t nabi_diags;          /* parse_abi_overrides' own sink (the CLI prints these
+                                     against the map file and stops on errors) */
+    ocldec_b200_diag *abi_diags;  /* messages also in diag_text */
 } ocldec_b200_result;
 
 /* decompile_listing: host buffer in, host result out (H2D/D2H inside). */
 int ocldec_b200_decompile(const char *listing, size_t len, const ocldec_b200_options *opts,
                           ocldec_b200_result **out);
 void ocldec_b200_free(ocldec_b200_result *res);
+/* parse_abi_overrides (abi_model.cpp:109-153) alone, on the host: writes its
+ * diagnostics as "<severity> <line> <message>\n" lines into buf (capacity
+ * cap, NUL-terminated); returns the number of errors, or -2 when buf is too
+ * small. */
+int ocldec_b200_abi_map_check(const char *text, size_t len, char *buf, size_t cap);
 const char *ocldec_b200_last_error(void);
 int ocldec_b200_version(void);
 

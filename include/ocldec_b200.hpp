@@ -9,6 +9,9 @@
 //   DecompileResult::combined_source()                 (decompiler.cpp:105-115)
 //   DecompileResult::diagnostics (DiagnosticSink, diagnostics.hpp:20-57):
 //   every note / warning / error the reference emits on this path
+//   DecompileOptions::abi_overrides (decompiler.hpp:31), given as the override
+//   file text the CLI's --abi-map reads (parse_abi_overrides, abi_model.cpp);
+//   its parse diagnostics come back in abi_diagnostics
 // Inspection fields (config, instructions, cfg, regions, body tree, DOT) are
 // not produced.  All work runs on the GPU; errors from the device runtime are
 // thrown as std::runtime_error (API misuse / CUDA failure only — data errors
@@ -16,6 +19,8 @@
 #ifndef OCLDEC_B200_HPP
 #define OCLDEC_B200_HPP
 
+#include <cstdlib>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -27,6 +32,7 @@ namespace ocldec_b200 {
 struct DecompileOptions {
     bool fold_local_size = false; // FoldOptions::fold_local_size (sym_state.hpp:27-29)
     std::string only_kernel;      // empty = all kernels (DecompileOptions::only_kernel)
+    std::string abi_map;          // ABI override file text; empty = none
     int device = 0;
 };
 
@@ -53,6 +59,7 @@ struct Diagnostic {
 struct DecompileResult {
     std::vector<DecompiledKernel> kernels;
     std::vector<Diagnostic> diagnostics;
+    std::vector<Diagnostic> abi_diagnostics; // parse_abi_overrides' sink
     double device_ms = 0;
     bool has_errors() const {
         for (const auto &d : diagnostics)
@@ -83,12 +90,37 @@ inline const char *split_error_message(int kind) {
     }
 }
 
+// parse_abi_overrides alone (the CLI's --abi-map check before decompiling).
+inline std::vector<Diagnostic> check_abi_map(const std::string &text) {
+    std::vector<char> buf(4096 + 4 * text.size());
+    int rc;
+    while ((rc = ocldec_b200_abi_map_check(text.data(), text.size(), buf.data(), buf.size())) == -2)
+        buf.resize(buf.size() * 2);
+    if (rc < 0)
+        throw std::runtime_error(std::string("ocldec_b200_abi_map_check: ") + ocldec_b200_last_error());
+    std::vector<Diagnostic> out;
+    const char *p = buf.data();
+    while (*p) {
+        const char *e = std::strchr(p, '\n');
+        Diagnostic d;
+        char *q = nullptr;
+        d.severity = static_cast<Diagnostic::Severity>(std::strtol(p, &q, 10));
+        d.line = static_cast<int>(std::strtol(q, &q, 10));
+        d.message.assign(static_cast<const char *>(q + 1), e);
+        out.push_back(std::move(d));
+        p = e + 1;
+    }
+    return out;
+}
+
 inline DecompileResult decompile_listing(const std::string &listing, const DecompileOptions &opts = {}) {
     ocldec_b200_options o{};
     o.fold_local_size = opts.fold_local_size ? 1 : 0;
     o.only_kernel = opts.only_kernel.empty() ? nullptr : opts.only_kernel.c_str();
     o.device = opts.device;
     o.arena_bytes = 0;
+    o.abi_map = opts.abi_map.empty() ? nullptr : opts.abi_map.data();
+    o.abi_map_len = opts.abi_map.size();
     ocldec_b200_result *r = nullptr;
     int rc = ocldec_b200_decompile(listing.data(), listing.size(), &o, &r);
     if (rc != 0)
@@ -107,14 +139,17 @@ inline DecompileResult decompile_listing(const std::string &listing, const Decom
         d.instructions = k.instructions;
         res.kernels.push_back(std::move(d));
     }
-    for (uint64_t i = 0; i < r->ndiags; ++i) {
-        const ocldec_b200_diag &d = r->diags[i];
-        Diagnostic dg;
-        dg.severity = static_cast<Diagnostic::Severity>(d.severity);
-        dg.line = d.line;
-        dg.message.assign(r->diag_text + d.msg_off, d.msg_len);
-        res.diagnostics.push_back(std::move(dg));
-    }
+    auto take = [&](const ocldec_b200_diag *v, uint64_t n, std::vector<Diagnostic> &out) {
+        for (uint64_t i = 0; i < n; ++i) {
+            Diagnostic dg;
+            dg.severity = static_cast<Diagnostic::Severity>(v[i].severity);
+            dg.line = v[i].line;
+            dg.message.assign(r->diag_text + v[i].msg_off, v[i].msg_len);
+            out.push_back(std::move(dg));
+        }
+    };
+    take(r->diags, r->ndiags, res.diagnostics);
+    take(r->abi_diags, r->nabi_diags, res.abi_diagnostics);
     ocldec_b200_free(r);
     return res;
 }

@@ -37,6 +37,10 @@ def lib():
         L.ref_decompile.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_char_p,
                                     ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_size_t)]
         L.ref_decompile.restype = ctypes.c_int
+        L.ref_decompile_abi.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_char_p,
+                                        ctypes.c_char_p, ctypes.c_size_t,
+                                        ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_size_t)]
+        L.ref_decompile_abi.restype = ctypes.c_int
         L.ref_free.argtypes = [ctypes.c_void_p]
         L.ref_decompile_batch.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
                                           ctypes.c_void_p, ctypes.c_void_p,
@@ -72,19 +76,27 @@ class RefResult:
     kernels: List[RefKernel] = field(default_factory=list)
     diagnostics: List[RefDiag] = field(default_factory=list)
     combined: bytes = b""
+    abi_diagnostics: List[RefDiag] = field(default_factory=list)  # parse_abi_overrides
 
 
 def _take(ptr: int, n: int) -> bytes:
     return ctypes.string_at(ptr, n)
 
 
-def decompile(listing: bytes, fold_local_size: bool = False, only_kernel: Optional[bytes] = None) -> RefResult:
+def decompile(listing: bytes, fold_local_size: bool = False, only_kernel: Optional[bytes] = None,
+              abi_map: Optional[bytes] = None) -> RefResult:
     if isinstance(listing, str):
         listing = listing.encode()
     L = lib()
     out = ctypes.c_void_p()
     n = ctypes.c_size_t()
-    L.ref_decompile(listing, len(listing), int(fold_local_size), only_kernel, ctypes.byref(out), ctypes.byref(n))
+    if abi_map is None:
+        L.ref_decompile(listing, len(listing), int(fold_local_size), only_kernel, ctypes.byref(out), ctypes.byref(n))
+    else:
+        if isinstance(abi_map, str):
+            abi_map = abi_map.encode()
+        L.ref_decompile_abi(listing, len(listing), int(fold_local_size), only_kernel, abi_map, len(abi_map),
+                            ctypes.byref(out), ctypes.byref(n))
     blob = _take(out.value, n.value)
     L.ref_free(out)
     res = RefResult()
@@ -103,6 +115,10 @@ def decompile(listing: bytes, fold_local_size: bool = False, only_kernel: Option
         elif head[0] == b"D":
             sev, line, mlen = (int(x) for x in head[1:])
             res.diagnostics.append(RefDiag(sev, line, blob[pos:pos + mlen]))
+            pos += mlen
+        elif head[0] == b"A":
+            sev, line, mlen = (int(x) for x in head[1:])
+            res.abi_diagnostics.append(RefDiag(sev, line, blob[pos:pos + mlen]))
             pos += mlen
         elif head[0] == b"C":
             clen = int(head[1])

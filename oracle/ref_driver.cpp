@@ -60,6 +60,8 @@ struct DecompileJob {
     size_t len;
     int fold_local_size;
     const char *only_kernel;
+    const char *abi_map; // override file text (parse_abi_overrides, abi_model.cpp:109-153) or null
+    size_t abi_len;
     std::string serialized;
 };
 
@@ -73,9 +75,18 @@ void *decompile_job(void *p) {
     opts.folds.fold_local_size = job->fold_local_size != 0;
     if (job->only_kernel)
         opts.only_kernel = std::string(job->only_kernel);
+    std::string out;
+    if (job->abi_map) {
+        ocldec::DiagnosticSink osink;
+        opts.abi_overrides = ocldec::parse_abi_overrides(std::string(job->abi_map, job->abi_len), osink);
+        for (const auto &d : osink.all()) {
+            out += "A " + std::to_string(int(d.severity)) + " " + std::to_string(d.line) + " " +
+                   std::to_string(d.message.size()) + "\n";
+            out += d.message;
+        }
+    }
     ocldec::DecompileResult res =
         ocldec::decompile_listing(std::string(job->listing, job->len), opts);
-    std::string out;
     for (const auto &k : res.kernels) {
         out += "K " + std::to_string(int(k.failed)) + " " + std::to_string(int(k.structured)) +
                " " + std::to_string(k.body.fallback_count) + " " + std::to_string(k.name.size()) +
@@ -141,7 +152,17 @@ extern "C" {
 // ref_free). Returns 0.
 int ref_decompile(const char *listing, size_t len, int fold_local_size, const char *only_kernel,
                   char **out, size_t *out_len) {
-    DecompileJob job{listing, len, fold_local_size, only_kernel, {}};
+    DecompileJob job{listing, len, fold_local_size, only_kernel, nullptr, 0, {}};
+    run_on_big_stack(decompile_job, &job);
+    *out = dup_out(job.serialized, out_len);
+    return 0;
+}
+
+// The same with an ABI override file (the CLI's --abi-map, ocldec.cpp:116-131):
+// its parse diagnostics come first as "A <severity> <line> <len>" records.
+int ref_decompile_abi(const char *listing, size_t len, int fold_local_size, const char *only_kernel,
+                      const char *abi_map, size_t abi_len, char **out, size_t *out_len) {
+    DecompileJob job{listing, len, fold_local_size, only_kernel, abi_map, abi_len, {}};
     run_on_big_stack(decompile_job, &job);
     *out = dup_out(job.serialized, out_len);
     return 0;

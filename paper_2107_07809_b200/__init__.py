@@ -18,7 +18,7 @@ from typing import List, Optional, Sequence, Union
 from . import _lib
 
 __all__ = ["DecompileOptions", "DecompiledKernel", "Diagnostic", "DecompileResult",
-           "decompile_listing", "generate_corpus", "Session", "SHAPES"]
+           "decompile_listing", "check_abi_map", "generate_corpus", "Session", "SHAPES"]
 
 # Synthetic corpus shapes (BASELINE.json configs).
 SHAPES = {"C1": 1, "C2": 2, "C3": 3, "C4": 4, "C5": 5}
@@ -26,10 +26,13 @@ SHAPES = {"C1": 1, "C2": 2, "C3": 3, "C4": 4, "C5": 5}
 
 @dataclass
 class DecompileOptions:
-    """DecompileOptions (decompiler.hpp:29-35).  abi_overrides and the DOT
-    dumps are not supported by this version."""
+    """DecompileOptions (decompiler.hpp:29-35).  ``abi_map`` is the override
+    file text the reference CLI's --abi-map reads (parse_abi_overrides,
+    abi_model.cpp:109-153) standing for ``abi_overrides``; the DOT dumps are
+    not supported by this version."""
     fold_local_size: bool = False           # FoldOptions (sym_state.hpp:27-29)
     only_kernel: Optional[str] = None       # restrict to one kernel by name
+    abi_map: Optional[Union[str, bytes]] = None
     device: int = 0
     arena_bytes: int = 0                    # per-thread arena, 0 = default
 
@@ -62,6 +65,7 @@ class DecompileResult:
     """DecompileResult (decompiler.hpp:54-60)."""
     kernels: List[DecompiledKernel] = field(default_factory=list)
     diagnostics: List[Diagnostic] = field(default_factory=list)
+    abi_diagnostics: List[Diagnostic] = field(default_factory=list)  # parse_abi_overrides' sink
     combined: bytes = b""
     device_ms: float = 0.0
 
@@ -86,9 +90,12 @@ def decompile_listing(listing: Union[str, bytes], opts: Optional[DecompileOption
     if isinstance(listing, str):
         listing = listing.encode("utf-8", errors="surrogateescape")
     opts = opts or DecompileOptions()
+    amap = opts.abi_map
+    if isinstance(amap, str):
+        amap = amap.encode("utf-8", errors="surrogateescape")
     o = _lib.Options(int(opts.fold_local_size),
                      opts.only_kernel.encode() if opts.only_kernel is not None else None,
-                     opts.device, opts.arena_bytes)
+                     opts.device, opts.arena_bytes, amap, len(amap) if amap is not None else 0)
     out = ctypes.POINTER(_lib.Result)()
     rc = L.ocldec_b200_decompile(listing, len(listing), ctypes.byref(o), ctypes.byref(out))
     if rc != 0:
@@ -107,15 +114,39 @@ def decompile_listing(listing: Union[str, bytes], opts: Optional[DecompileOption
                 source=src.decode("utf-8", errors="surrogateescape"),
                 structured=bool(k.structured), failed=bool(k.failed),
                 fallback_count=k.fallback_count, instructions=k.instructions))
-        tlen = max((r.diags[i].msg_off + r.diags[i].msg_len for i in range(r.ndiags)), default=0)
+        alld = [r.diags[i] for i in range(r.ndiags)] + [r.abi_diags[i] for i in range(r.nabi_diags)]
+        tlen = max((d.msg_off + d.msg_len for d in alld), default=0)
         text = ctypes.string_at(r.diag_text, tlen) if r.diag_text and tlen else b""
-        for i in range(r.ndiags):
-            d = r.diags[i]
+        for i, d in enumerate(alld):
             msg = text[d.msg_off:d.msg_off + d.msg_len].decode("utf-8", errors="surrogateescape")
-            res.diagnostics.append(Diagnostic(d.severity, d.line, msg))
+            (res.diagnostics if i < r.ndiags else res.abi_diagnostics).append(
+                Diagnostic(d.severity, d.line, msg))
         return res
     finally:
         L.ocldec_b200_free(out)
+
+
+def check_abi_map(text: Union[str, bytes]) -> List[Diagnostic]:
+    """parse_abi_overrides (abi_model.cpp:109-153) alone: the diagnostics the
+    reference CLI prints for an --abi-map file before decompiling."""
+    L = _lib.load()
+    if isinstance(text, str):
+        text = text.encode("utf-8", errors="surrogateescape")
+    cap = 4096 + 4 * len(text)
+    while True:
+        buf = ctypes.create_string_buffer(cap)
+        rc = L.ocldec_b200_abi_map_check(text, len(text), buf, cap)
+        if rc != -2:
+            break
+        cap *= 2
+    if rc < 0:
+        raise RuntimeError(f"ocldec_b200_abi_map_check failed ({rc}): {_lib.last_error()}")
+    out = []
+    for line in buf.value.split(b"\n"):
+        if line:
+            sev, ln, msg = line.split(b" ", 2)
+            out.append(Diagnostic(int(sev), int(ln), msg.decode("utf-8", errors="surrogateescape")))
+    return out
 
 
 def generate_corpus(shape: Union[int, str], count: int, seed: int = 1, k0: int = 0, stress: bool = False):

@@ -16,7 +16,8 @@ LIB_PATH = os.environ.get("OCLDEC_B200_LIB") or os.path.join(_HERE, "libocldec_b
 
 class Options(ctypes.Structure):
     _fields_ = [("fold_local_size", ctypes.c_int), ("only_kernel", ctypes.c_char_p),
-                ("device", ctypes.c_int), ("arena_bytes", ctypes.c_size_t)]
+                ("device", ctypes.c_int), ("arena_bytes", ctypes.c_size_t),
+                ("abi_map", ctypes.c_char_p), ("abi_map_len", ctypes.c_size_t)]
 
 
 class Kernel(ctypes.Structure):
@@ -37,7 +38,8 @@ class Result(ctypes.Structure):
                 ("combined_len", ctypes.c_uint64), ("split_error_line", ctypes.c_int32),
                 ("split_error_kind", ctypes.c_int32), ("instructions", ctypes.c_uint64),
                 ("device_ms", ctypes.c_double), ("ndiags", ctypes.c_uint64),
-                ("diags", ctypes.POINTER(Diag)), ("diag_text", ctypes.c_void_p)]
+                ("diags", ctypes.POINTER(Diag)), ("diag_text", ctypes.c_void_p),
+                ("nabi_diags", ctypes.c_uint64), ("abi_diags", ctypes.POINTER(Diag))]
 
 
 class Stats(ctypes.Structure):
@@ -55,7 +57,7 @@ EXPORTS = [
     "ocldec_b200_session_create", "ocldec_b200_session_destroy", "ocldec_b200_session_stream",
     "ocldec_b200_session_run", "ocldec_b200_session_stats", "ocldec_b200_session_output",
     "ocldec_b200_session_kernels", "ocldec_b200_gen_host", "ocldec_b200_gen_device",
-    "ocldec_b200_session_run_host", "ocldec_b200_copy",
+    "ocldec_b200_session_run_host", "ocldec_b200_copy", "ocldec_b200_abi_map_check",
 ]
 
 _lib = None
@@ -75,6 +77,8 @@ def load():
                                         ctypes.POINTER(ctypes.POINTER(Result))]
     L.ocldec_b200_decompile.restype = i32
     L.ocldec_b200_free.argtypes = [ctypes.POINTER(Result)]
+    L.ocldec_b200_abi_map_check.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_char_p, ctypes.c_size_t]
+    L.ocldec_b200_abi_map_check.restype = i32
     L.ocldec_b200_last_error.restype = ctypes.c_char_p
     L.ocldec_b200_version.restype = i32
     L.ocldec_b200_session_create.argtypes = [i32, ctypes.c_size_t]

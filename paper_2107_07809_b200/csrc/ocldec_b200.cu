@@ -285,12 +285,13 @@ __global__ void __launch_bounds__(256) k_decode(const u8 *__restrict__ t, u64 le
 // Per-kernel sizes (a pass over the kernel's decoded lines), size key and
 // arena budget.
 __global__ void k_ksize(const u32 *kstart, u32 nk, u32 nlines, const LineRec *lines, const LineIns *lins,
-                        const Opnd *ops, KSize *sizes, u32 *key, u64 *budget, u32 group) {
+                        const Opnd *ops, KSize *sizes, u32 *key, u64 *budget, u32 group, u32 novr) {
     u32 k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= nk)
         return;
     const u32 b = kstart[k], e = k + 1 < nk ? kstart[k + 1] : nlines;
-    const KSize z = kernel_size(lines, lins, ops, b, e);
+    KSize z = kernel_size(lines, lins, ops, b, e);
+    z.novr = novr;
     sizes[k] = z;
     // sort key: lines, optionally grouped by class (straight-line kernels
     // first) so an SM's resident kernels share their hot code
@@ -494,6 +495,125 @@ struct HostDiag {
     std::string a, b;
 };
 
+// ABI overrides parsed on the host (parse_abi_overrides, abi_model.cpp:109-153)
+// and resolved as far as they do not depend on the kernel (abi_model.cpp:196-243).
+struct HostOvr {
+    AbiOvr dev;
+    std::string tail, target; // for the messages
+};
+
+std::string trim_ovr(const std::string &s) { // trim_view  abi_model.cpp:72-78
+    size_t b = 0, e = s.size();
+    while (b < e && (s[b] == ' ' || s[b] == '\t'))
+        ++b;
+    while (e > b && (s[e - 1] == ' ' || s[e - 1] == '\t' || s[e - 1] == '\r'))
+        --e;
+    return s.substr(b, e - b);
+}
+
+bool parse_u32_ovr(std::string s, u32 *out) { // parse_u32  abi_model.cpp:59-70
+    int base = 10;
+    if (s.size() > 2 && s[0] == '0' && (s[1] == 'x' || s[1] == 'X')) {
+        base = 16;
+        s = s.substr(2);
+    }
+    if (s.empty())
+        return false;
+    u64 v = 0;
+    for (char c : s) {
+        int d;
+        if (c >= '0' && c <= '9')
+            d = c - '0';
+        else if (base == 16 && c >= 'a' && c <= 'f')
+            d = c - 'a' + 10;
+        else if (base == 16 && c >= 'A' && c <= 'F')
+            d = c - 'A' + 10;
+        else
+            return false;
+        if (d >= base)
+            return false;
+        v = v * base + d;
+        if (v > 0xffffffffull)
+            return false;
+    }
+    *out = (u32)v;
+    return true;
+}
+
+struct OvrDiag {
+    int sev, line;
+    std::string msg;
+};
+
+std::vector<HostOvr> parse_overrides(const std::string &text, std::vector<OvrDiag> *diags) {
+    std::vector<HostOvr> out;
+    size_t pos = 0;
+    int line_no = 0;
+    while (pos < text.size()) { // std::getline
+        size_t nl = text.find('\n', pos);
+        std::string raw = text.substr(pos, nl == std::string::npos ? std::string::npos : nl - pos);
+        pos = nl == std::string::npos ? text.size() : nl + 1;
+        ++line_no;
+        std::string line = trim_ovr(raw);
+        if (line.empty() || line[0] == '#')
+            continue;
+        size_t eq = line.find('=');
+        if (eq == std::string::npos) {
+            diags->push_back({2, line_no, "override line is not key=value"});
+            continue;
+        }
+        std::string key = trim_ovr(line.substr(0, eq)), value = trim_ovr(line.substr(eq + 1));
+        HostOvr o;
+        memset(&o.dev, 0, sizeof(o.dev));
+        size_t colon = key.find(':');
+        u32 offset;
+        if (!parse_u32_ovr(trim_ovr(colon == std::string::npos ? key : key.substr(0, colon)), &offset)) {
+            diags->push_back({2, line_no, "bad offset in override key"});
+            continue;
+        }
+        o.dev.offset = offset;
+        o.dev.dwords = 1;
+        if (colon != std::string::npos) {
+            u32 w;
+            if (!parse_u32_ovr(trim_ovr(key.substr(colon + 1)), &w) || (w != 1 && w != 2)) {
+                diags->push_back({2, line_no, "override width must be 1 or 2 dwords"});
+                continue;
+            }
+            o.dev.dwords = (u8)w;
+        }
+        if (value.empty()) {
+            diags->push_back({2, line_no, "override has an empty target"});
+            continue;
+        }
+        o.target = value;
+        size_t tc = value.find(':');
+        std::string head = tc == std::string::npos ? value : value.substr(0, tc);
+        o.tail = tc == std::string::npos ? std::string() : value.substr(tc + 1);
+        if (head == "arg") {
+            o.dev.kind = OV_ARG;
+        } else {
+            int fn = head == "global_offset" ? F_GLOBAL_OFFSET
+                     : head == "global_size" ? F_GLOBAL_SIZE
+                     : head == "work_dim"    ? F_WORK_DIM
+                     : head == "local_size"  ? F_LOCAL_SIZE
+                     : head == "num_groups"  ? F_NUM_GROUPS
+                                             : -1;
+            u32 dim = 0;
+            if (fn < 0)
+                o.dev.kind = OV_BAD_TARGET;
+            else if (!o.tail.empty() && (!parse_u32_ovr(o.tail, &dim) || dim > 2))
+                o.dev.kind = OV_BAD_DIM;
+            else {
+                o.dev.kind = OV_BUILTIN;
+                o.dev.fn = (u8)fn;
+                o.dev.dim = (u8)dim;
+            }
+        }
+        out.push_back(std::move(o));
+    }
+    return out;
+}
+
 int diag_severity(u16 code) {
     switch (code) {
     case DG_UNREACHABLE: return 0;
@@ -539,7 +659,7 @@ std::string mnemonic_root(const std::string &m) {
 }
 
 // The reference's message text for a diagnostic.
-std::string diag_message(const HostDiag &d) {
+std::string diag_message(const HostDiag &d, const std::vector<HostOvr> *ovr = nullptr) {
     switch (d.code) {
     case DG_DIMS: return "bad .dims axes '" + d.a + "'";
     case DG_CWS_COUNT: return "cws expects 1 to 3 sizes";
@@ -579,6 +699,9 @@ std::string diag_message(const HostDiag &d) {
     case DG_ADDC: return "v_addc_u32 outside the 64-bit add idiom; carry treated as zero";
     case DG_GOTO: return "control flow not fully structured; emitting labeled blocks";
     case DG_EXEC_BRANCH: return "exec-dependent branch kept as inline asm";
+    case DG_OVR_ARG: return "override names unknown argument '" + (ovr && d.c < ovr->size() ? (*ovr)[d.c].tail : "") + "'";
+    case DG_OVR_TARGET: return "unknown override target '" + (ovr && d.c < ovr->size() ? (*ovr)[d.c].target : "") + "'";
+    case DG_OVR_DIM: return "override dimension must be 0..2";
     default: return "diagnostic " + std::to_string(d.code);
     }
 }
@@ -611,6 +734,10 @@ struct ocldec_b200_session {
     std::vector<cudaEvent_t> pev;    // phase-launch events (pool)
     DevBuf dpool, dtop;              // device diagnostic records of a chunk
     std::vector<HostDiag> host_diag; // materialized diagnostics, all chunks
+    std::vector<HostOvr> ovr_host;   // ABI overrides of the current call
+    std::vector<OvrDiag> ovr_diags;  // their parse diagnostics
+    DevBuf dovr, dovr_text;
+    u32 novr = 0;
     std::vector<u64> host_kdiag;     // per kernel: first host_diag index (count in host_res[k].ndiag)
     size_t pev_used = 0;
 };
@@ -821,6 +948,9 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     a.dpool = P<Diag>(s->dpool);
     a.dcap = s->dpool.cap / sizeof(Diag);
     a.dtop = P<unsigned long long>(s->dtop);
+    a.ovr = s->novr ? P<AbiOvr>(s->dovr) : nullptr;
+    a.novr = s->novr;
+    a.ovr_text = s->novr ? P<u8>(s->dovr_text) : nullptr;
     a.res = P<KRes>(s->res);
     a.only = s->only_set ? P<u8>(s->only) : nullptr;
     a.only_len = s->only_len;
@@ -831,7 +961,8 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
         return -3;
     a.sizes = P<KSize>(s->ksizes);
     k_ksize<<<kg, kb, 0, st>>>(P<u32>(s->kstart), nk, nlines, P<LineRec>(s->lines), P<LineIns>(s->lins),
-                               P<Opnd>(s->ops), P<KSize>(s->ksizes), key, P<u64>(s->budget), s->group_class);
+                               P<Opnd>(s->ops), P<KSize>(s->ksizes), key, P<u64>(s->budget), s->group_class,
+                               s->novr);
     CK(cudaMemsetAsync(s->hist.p, 0, kSizeBuckets * 4ull, st));
     k_hist<<<kg, kb, 0, st>>>(key, nk, P<u32>(s->hist));
     if (scan_exclusive(s, kSizeBuckets, SU32{0}, AddU32{}, U32Load{P<u32>(s->hist)},
@@ -1225,6 +1356,40 @@ size_t chunk_target() {
     return (size_t)5 << 29; // 2.5 GiB: chunk + aux area stay in u32 offsets
 }
 
+// Parses an ABI override file (or clears the overrides) and uploads the
+// resolved list for build_abi.
+int set_overrides(ocldec_b200_session *s, const char *text, size_t len) {
+    s->ovr_host.clear();
+    s->ovr_diags.clear();
+    s->novr = 0;
+    if (!text)
+        return 0;
+    s->ovr_host = parse_overrides(std::string(text, len), &s->ovr_diags);
+    if (s->ovr_host.empty())
+        return 0;
+    if (s->ovr_host.size() > 65535) {
+        g_err = "more than 65535 ABI overrides";
+        return -1;
+    }
+    std::vector<AbiOvr> dv;
+    std::string blob;
+    for (HostOvr &o : s->ovr_host) {
+        if (o.dev.kind == OV_ARG) {
+            o.dev.name_off = (u32)blob.size();
+            o.dev.name_len = (u32)o.tail.size();
+            blob += o.tail;
+        }
+        dv.push_back(o.dev);
+    }
+    if (ensure(s->dovr, dv.size() * sizeof(AbiOvr)) || ensure(s->dovr_text, blob.size() + 16))
+        return -3;
+    CK(cudaMemcpy(s->dovr.p, dv.data(), dv.size() * sizeof(AbiOvr), cudaMemcpyHostToDevice));
+    if (!blob.empty())
+        CK(cudaMemcpy(s->dovr_text.p, blob.data(), blob.size(), cudaMemcpyHostToDevice));
+    s->novr = (u32)dv.size();
+    return 0;
+}
+
 // decompile_listing over a host buffer: chunking at .kernel lines, H2D of
 // each chunk, the device pipeline, names back to the host.  Output stays in
 // s->out[0, out_bytes).
@@ -1328,7 +1493,8 @@ void ocldec_b200_session_destroy(ocldec_b200_session *s) {
                       &s->scan_tmp, &s->scan_tot, &s->counters, &s->arena, &s->stage, &s->res,
                       &s->outoff, &s->out, &s->only, &s->retry, &s->gen_len, &s->gen_ninstr,
                       &s->gen_buf, &s->gen_off, &s->kmeta, &s->order, &s->budget, &s->sbudget,
-                      &s->boff, &s->hist, &s->prof, &s->ksizes, &s->dpool, &s->dtop, &s->perm, &s->cnt4};
+                      &s->boff, &s->hist, &s->prof, &s->ksizes, &s->dpool, &s->dtop, &s->perm, &s->cnt4,
+                      &s->dovr, &s->dovr_text};
     for (DevBuf *b : bufs)
         if (b->p)
             cudaFree(b->p);
@@ -1354,6 +1520,7 @@ int ocldec_b200_session_run(ocldec_b200_session *s, const void *d_listing, size_
     CK(cudaSetDevice(s->device));
     reset_stats(s);
     s->only_set = false;
+    set_overrides(s, nullptr, 0);
     s->stats.in_bytes = len;
     u64 out_pos = 0;
     u32 line_base = 0;
@@ -1449,6 +1616,8 @@ int ocldec_b200_decompile(const char *listing, size_t len, const ocldec_b200_opt
         return -3;
     CK(cudaSetDevice(s->device));
     HostRun hr;
+    if (int rc0 = set_overrides(s, o.abi_map, o.abi_map ? o.abi_map_len : 0))
+        return rc0;
     int rc = run_host_listing(s, listing, len, o.fold_local_size, o.only_kernel, &hr);
     if (rc)
         return rc;
@@ -1512,14 +1681,19 @@ int ocldec_b200_decompile(const char *listing, size_t len, const ocldec_b200_opt
                 continue;
             for (u32 q = 0; q < r.ndiag; ++q) {
                 const HostDiag &h = s->host_diag[s->host_kdiag[k] + q];
-                add(diag_severity(h.code), (int)h.line, diag_message(h));
+                add(diag_severity(h.code), (int)h.line, diag_message(h, &s->ovr_host));
             }
         }
     }
-    res->ndiags = dl.size();
+    const size_t nk_diags = dl.size();
+    for (const OvrDiag &d : s->ovr_diags)
+        add(d.sev, d.line, d.msg);
+    res->ndiags = nk_diags;
+    res->nabi_diags = dl.size() - nk_diags;
     res->diags = static_cast<ocldec_b200_diag *>(malloc((dl.size() + 1) * sizeof(ocldec_b200_diag)));
     if (!dl.empty())
         memcpy(res->diags, dl.data(), dl.size() * sizeof(ocldec_b200_diag));
+    res->abi_diags = res->diags + nk_diags;
     res->diag_text = static_cast<char *>(malloc(dt.size() + 1));
     memcpy(res->diag_text, dt.data(), dt.size());
     res->diag_text[dt.size()] = 0;
@@ -1536,6 +1710,7 @@ int ocldec_b200_session_run_host(ocldec_b200_session *s, const char *listing, si
     }
     CK(cudaSetDevice(s->device));
     HostRun hr;
+    set_overrides(s, nullptr, 0);
     int rc = run_host_listing(s, listing, len, fold_local_size, nullptr, &hr);
     if (rc)
         return rc;
@@ -1551,13 +1726,33 @@ int ocldec_b200_session_run_host(ocldec_b200_session *s, const char *listing, si
     return 0;
 }
 
+int ocldec_b200_abi_map_check(const char *text, size_t len, char *buf, size_t cap) {
+    if ((!text && len) || (!buf && cap)) {
+        g_err = "bad arguments";
+        return -1;
+    }
+    std::vector<OvrDiag> d;
+    parse_overrides(std::string(text ? text : "", len), &d);
+    std::string out;
+    int errors = 0;
+    for (const OvrDiag &x : d) {
+        out += std::to_string(x.sev) + " " + std::to_string(x.line) + " " + x.msg + "\n";
+        errors += x.sev == 2;
+    }
+    if (out.size() + 1 > cap)
+        return -2;
+    memcpy(buf, out.data(), out.size());
+    buf[out.size()] = 0;
+    return errors;
+}
+
 void ocldec_b200_free(ocldec_b200_result *res) {
     if (!res)
         return;
     free(res->kernels);
     free(res->names);
     free(res->combined);
-    free(res->diags);
+    free(res->diags); // abi_diags points into the same array
     free(res->diag_text);
     free(res);
 }

@@ -49,6 +49,9 @@ struct DecompArgs {
     u64 *prof;
     u32 lanes_per; // lanes per kernel: 32 / kernels-per-warp
     const u32 *perm; // wave slot permutation for the launches after k_front (null: identity)
+    const AbiOvr *ovr; // ABI overrides of the run (novr)
+    u32 novr;
+    const u8 *ovr_text;
     Diag *dpool;   // diagnostic records of finished kernels
     u64 dcap;
     unsigned long long *dtop;

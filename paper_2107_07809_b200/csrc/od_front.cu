@@ -37,6 +37,9 @@ __global__ void __launch_bounds__(128, OD_MINB_FRONT) k_front(DecompArgs a) {
         in.nins = z.nins;
         in.nlab = z.nlab;
     }
+    in.ovr = a.ovr;
+    in.novr = a.novr;
+    in.ovr_text = a.ovr_text;
     g->mem.base = sl.base + kb;
     g->mem.top = 0;
     g->mem.cap = a.boff[i + 1] - a.boff[i] - kb;

@@ -41,6 +41,15 @@ struct Bump {
 
 enum KStatus : u32 { KS_OK = 0, KS_FAILED = 1, KS_OOM = 2, KS_SPLIT_ERROR = 3 };
 
+// One ABI override (DecompileOptions::abi_overrides, abi_model.hpp:64-68),
+// resolved on the host except for the per-kernel argument lookup.
+enum OvrKind : u8 { OV_ARG = 0, OV_BUILTIN, OV_BAD_TARGET, OV_BAD_DIM };
+struct AbiOvr {
+    u32 offset;
+    u8 dwords, kind, fn, dim;
+    u32 name_off, name_len; // OV_ARG: argument name in the override text
+};
+
 // Inputs for one kernel section.
 struct KIn {
     const u8 *t;          // listing bytes (+ aux area)
@@ -54,6 +63,9 @@ struct KIn {
     u32 scale;            // pool capacity multiplier (retries)
     u32 nblk_cap;         // block capacity (KSize::nb; 0 = one per instruction)
     u32 ncfg, nins, nlab; // KSize counts of the section (config lines, instructions, labels)
+    const AbiOvr *ovr;    // ABI overrides (novr), applied by build_abi
+    u32 novr;
+    const u8 *ovr_text;
     u64 *prof;            // optional per-phase cycle counters
 };
 
@@ -274,6 +286,9 @@ enum DiagCode : u16 {
     DG_ADDC,            // warning "v_addc_u32 outside the 64-bit add idiom; carry treated as zero" :688
     DG_GOTO,            // warning "control flow not fully structured; emitting labeled blocks" lower.cpp:189
     DG_EXEC_BRANCH,     // warning "exec-dependent branch kept as inline asm"    lower.cpp:225
+    DG_OVR_ARG,         // error   "override names unknown argument '<tail c>'" abi_model.cpp:209
+    DG_OVR_TARGET,      // error   "unknown override target '<target c>'"       :227
+    DG_OVR_DIM,         // error   "override dimension must be 0..2"            :234
 };
 
 struct Diag {
@@ -637,9 +652,10 @@ OD_INL void abi_add(KCtx &K, const AbiEntry &e) {
     K.abi[K.nabi++] = e;
 }
 
-// build_abi_map  abi_model.cpp:155-245 (no overrides)
+// build_abi_map  abi_model.cpp:155-245; overrides resolved on the host by
+// parse_overrides (parse_abi_overrides abi_model.cpp:109-153)
 OD_NOINL bool build_abi(KCtx &K) {
-    K.abi = K.mem->get<AbiEntry>(8 + K.cfg.nargs);
+    K.abi = K.mem->get<AbiEntry>(8 + K.cfg.nargs + K.in->novr);
     if (!K.abi)
         return false;
     K.nabi = 0;
@@ -688,6 +704,42 @@ OD_NOINL bool build_abi(KCtx &K) {
         if (e.dwords <= 2)
             abi_add(K, e);
         offset += sz;
+    }
+    // overrides last (abi_model.cpp:196-243); AbiMap::add replaces exact matches
+    const KIn &in = *K.in;
+    for (u32 q = 0; q < in.novr; ++q) {
+        const AbiOvr &o = in.ovr[q];
+        AbiEntry e;
+        e.offset = o.offset;
+        e.dwords = o.dwords;
+        e.has_builtin = 0;
+        e.fn = 0;
+        e.dim = 0;
+        e.arg_index = -1;
+        e.type = DT_UNKNOWN;
+        if (o.kind == OV_ARG) {
+            i32 hit = -1;
+            for (u32 i = 0; i < K.cfg.nargs && hit < 0; ++i) {
+                const Span nm = K.cfg.args[i].name;
+                if (nm.len == o.name_len && bytes_eq(t + nm.off, in.ovr_text + o.name_off, nm.len))
+                    hit = (i32)i;
+            }
+            if (hit < 0) {
+                diag(K, DG_OVR_ARG, 0, (u16)q);
+                continue;
+            }
+            e.arg_index = hit;
+            e.type = K.cfg.args[hit].type;
+        } else if (o.kind == OV_BUILTIN) {
+            e.has_builtin = 1;
+            e.fn = o.fn;
+            e.dim = o.dim;
+            e.type = o.fn == F_GLOBAL_OFFSET ? DT_U64 : DT_U32;
+        } else {
+            diag(K, o.kind == OV_BAD_TARGET ? DG_OVR_TARGET : DG_OVR_DIM, 0, (u16)q);
+            continue;
+        }
+        abi_add(K, e);
     }
     return true;
 }
@@ -782,6 +834,7 @@ struct KSize {
     u32 nins; // instruction lines
     u32 nlab; // labels
     u32 nb;   // blocks: leaders (first, labelled, after a branch/endpgm) + exec-op splits + the synthetic end
+    u32 novr; // ABI overrides of the run
 };
 
 OD_INL KSize kernel_size(const LineRec *lines, const LineIns *lins, const Opnd *ops, u32 lbeg, u32 lend) {
@@ -810,6 +863,7 @@ OD_INL KSize kernel_size(const LineRec *lines, const LineIns *lins, const Opnd *
             ++xops;
     }
     z.nb = 3 + labelled + enders + xops;
+    z.novr = 0;
     return z;
 }
 

@@ -1489,7 +1489,7 @@ OD_INL u64 arena_budget(const KSize &z, u32 s) {
     u64 t = 0;
     t += (z.ncfg + 1) * (sizeof(KArg) + sizeof(Span));       // config
     t += (ni + 1) * sizeof(Ins) + (z.nlab + 1) * 4;           // instructions, labels
-    t += (8 + z.ncfg) * sizeof(AbiEntry);                     // ABI map
+    t += (8 + z.ncfg + z.novr) * sizeof(AbiEntry);           // ABI map
     t += b * (sizeof(Block) + 4) + (2 * b + 4) * 4 + (ni + 1) + b * 8 + (b / 32 + 1) * 4; // blocks, stamps, work, supp, sx, rbits
     u64 lc = 16;
     while (lc < 2 * ((u64)z.nlab + 1))

@@ -133,6 +133,9 @@ int main(int argc, char **argv) {
         kin.line_base = 0;
         kin.fold_local_size = argc > 1 && std::string(argv[1]) == "--fold-local-size";
         kin.prof = nullptr;
+        kin.ovr = nullptr;
+        kin.novr = 0;
+        kin.ovr_text = nullptr;
         KOut ko;
         const u8 *src = nullptr;
         std::vector<u8> arena;

@@ -4,11 +4,14 @@
 // (/root/reference/proj/tools/ocldec.cpp:81-177) for the options this path
 // supports:
 //   ocldec-b200 <input> [-o|--output FILE] [--kernel NAME] [--fold-local-size]
+//               [--abi-map FILE]
 // The output is combined_source() written atomically (temp file + rename,
 // ocldec.cpp:35-57) to FILE or <input stem>.cl (ocldec.cpp:59-66).
 // Diagnostics go to stderr as "file:line: severity: message"; exit status is 1
 // when no kernel was produced or any kernel failed, 0 otherwise.
-// --abi-map / --dump-cfg / --dump-regions are rejected (not supported).
+// --abi-map FILE is parsed first; its diagnostics are printed against FILE and
+// any error exits 1 before decompiling (ocldec.cpp:120-131).
+// --dump-cfg / --dump-regions are rejected (not supported).
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -66,7 +69,8 @@ std::string default_output(const std::string &input) {
 int usage(const char *argv0, int code) {
     std::fprintf(code ? stderr : stdout,
                  "Decompiles AMD GCN disassembly listings (CLRX syntax) to OpenCL C on the GPU\n"
-                 "Usage: %s input [-o OUTPUT] [--kernel NAME] [--fold-local-size] [--device N]\n",
+                 "Usage: %s input [-o OUTPUT] [--kernel NAME] [--fold-local-size] [--abi-map FILE]\n"
+                 "       [--device N]\n",
                  argv0);
     return code;
 }
@@ -74,7 +78,7 @@ int usage(const char *argv0, int code) {
 } // namespace
 
 int main(int argc, char **argv) {
-    std::string input, output, only;
+    std::string input, output, only, abi_path;
     ocldec_b200::DecompileOptions opts;
     for (int i = 1; i < argc; ++i) {
         std::string a = argv[i];
@@ -84,9 +88,12 @@ int main(int argc, char **argv) {
             std::printf("ocldec-b200 (C ABI %d)\n", OCLDEC_B200_ABI_VERSION);
             return 0;
         }
-        if ((a == "-o" || a == "--output" || a == "--kernel" || a == "--device") && i + 1 < argc) {
+        if ((a == "-o" || a == "--output" || a == "--kernel" || a == "--device" || a == "--abi-map") &&
+            i + 1 < argc) {
             std::string v = argv[++i];
-            if (a == "--kernel")
+            if (a == "--abi-map")
+                abi_path = v;
+            else if (a == "--kernel")
                 opts.only_kernel = v;
             else if (a == "--device")
                 opts.device = std::atoi(v.c_str());
@@ -98,7 +105,7 @@ int main(int argc, char **argv) {
             opts.fold_local_size = true;
             continue;
         }
-        if (a == "--abi-map" || a == "--dump-cfg" || a == "--dump-regions") {
+        if (a == "--dump-cfg" || a == "--dump-regions") {
             std::cerr << "ocldec-b200: error: " << a << " is not supported by this build\n";
             return 1;
         }
@@ -115,6 +122,24 @@ int main(int argc, char **argv) {
     if (!read_file(input, listing, err)) {
         std::cerr << "ocldec-b200: error: " << err << "\n";
         return 1;
+    }
+    if (!abi_path.empty()) {
+        if (!read_file(abi_path, opts.abi_map, err)) {
+            std::cerr << "ocldec-b200: error: " << err << "\n";
+            return 1;
+        }
+        bool bad = false;
+        try {
+            for (const auto &d : ocldec_b200::check_abi_map(opts.abi_map)) {
+                std::cerr << d.render(abi_path) << "\n";
+                bad = bad || d.severity == ocldec_b200::Diagnostic::Error;
+            }
+        } catch (const std::exception &e) {
+            std::cerr << "ocldec-b200: error: " << e.what() << "\n";
+            return 1;
+        }
+        if (bad)
+            return 1;
     }
     ocldec_b200::DecompileResult result;
     try {
