@@ -28,7 +28,7 @@ extern "C" {
 
 #define OCLDEC_B200_ABI_VERSION 3
 
-/* DecompileOptions (decompiler.hpp:29-35).  The DOT dumps are not supported. */
+/* DecompileOptions (decompiler.hpp:29-35). */
 typedef struct ocldec_b200_options {
     int fold_local_size;     /* FoldOptions::fold_local_size (sym_state.hpp:27-29) */
     const char *only_kernel; /* restrict to one kernel by name, NULL = all        */
@@ -37,6 +37,9 @@ typedef struct ocldec_b200_options {
     const char *abi_map;     /* ABI override file text (the CLI's --abi-map), NULL = none:
                                 parse_abi_overrides abi_model.cpp:109-153 */
     size_t abi_map_len;
+    int dump_cfg;            /* DecompileOptions::dump_cfg: DecompiledKernel::cfg_dot (to_dot, cfg.cpp:400-424) */
+    int dump_regions;        /* DecompileOptions::dump_regions: ReduceResult::dumps
+                                (region_graph_dot, structurizer.cpp:669-688, one per reduction step) */
 } ocldec_b200_options;
 
 /* DecompiledKernel (decompiler.hpp:39-52): the printed source and flags. */
@@ -58,6 +61,15 @@ typedef struct ocldec_b200_diag {
     uint64_t msg_off, msg_len;
 } ocldec_b200_diag;
 
+/* One DOT dump of a kernel: step -1 is cfg_dot, step i >= 0 is
+ * reduction.dumps[i] ("step<i>"); text at dump_text[off, off + len). */
+typedef struct ocldec_b200_dump {
+    uint64_t kernel;              /* index into ocldec_b200_result.kernels */
+    int32_t step;
+    int32_t reserved;
+    uint64_t off, len;
+} ocldec_b200_dump;
+
 typedef struct ocldec_b200_result {
     uint64_t nkernels;
     ocldec_b200_kernel *kernels;
@@ -74,6 +86,9 @@ typedef struct ocldec_b200_result {
     uint64_t nabi_diags;          /* parse_abi_overrides' own sink (the CLI prints these
                                      against the map file and stops on errors) */
     ocldec_b200_diag *abi_diags;  /* messages also in diag_text */
+    uint64_t ndumps;              /* DOT dumps (options dump_cfg / dump_regions), by kernel then step */
+    ocldec_b200_dump *dumps;
+    char *dump_text;
 } ocldec_b200_result;
 
 /* decompile_listing: host buffer in, host result out (H2D/D2H inside). */

@@ -12,8 +12,9 @@
 //   DecompileOptions::abi_overrides (decompiler.hpp:31), given as the override
 //   file text the CLI's --abi-map reads (parse_abi_overrides, abi_model.cpp);
 //   its parse diagnostics come back in abi_diagnostics
-// Inspection fields (config, instructions, cfg, regions, body tree, DOT) are
-// not produced.  All work runs on the GPU; errors from the device runtime are
+//   DecompiledKernel::cfg_dot and reduction.dumps (the DOT dumps)
+// The other inspection fields (config, instructions, cfg, regions, body tree)
+// are not produced.  All work runs on the GPU; errors from the device runtime are
 // thrown as std::runtime_error (API misuse / CUDA failure only — data errors
 // come back in the result exactly as the reference reports them).
 #ifndef OCLDEC_B200_HPP
@@ -33,6 +34,8 @@ struct DecompileOptions {
     bool fold_local_size = false; // FoldOptions::fold_local_size (sym_state.hpp:27-29)
     std::string only_kernel;      // empty = all kernels (DecompileOptions::only_kernel)
     std::string abi_map;          // ABI override file text; empty = none
+    bool dump_cfg = false;        // DecompileOptions::dump_cfg (decompiler.hpp:33)
+    bool dump_regions = false;    // DecompileOptions::dump_regions (decompiler.hpp:34)
     int device = 0;
 };
 
@@ -43,6 +46,8 @@ struct DecompiledKernel {
     bool failed = false;
     int fallback_count = 0;
     unsigned instructions = 0;
+    std::string cfg_dot;                   // DecompiledKernel::cfg_dot when dump_cfg
+    std::vector<std::string> region_dumps; // ReduceResult::dumps when dump_regions
 };
 
 // Diagnostic (diagnostics.hpp:20-27); render() matches diagnostics.cpp:22-26.
@@ -121,6 +126,8 @@ inline DecompileResult decompile_listing(const std::string &listing, const Decom
     o.arena_bytes = 0;
     o.abi_map = opts.abi_map.empty() ? nullptr : opts.abi_map.data();
     o.abi_map_len = opts.abi_map.size();
+    o.dump_cfg = opts.dump_cfg ? 1 : 0;
+    o.dump_regions = opts.dump_regions ? 1 : 0;
     ocldec_b200_result *r = nullptr;
     int rc = ocldec_b200_decompile(listing.data(), listing.size(), &o, &r);
     if (rc != 0)
@@ -138,6 +145,15 @@ inline DecompileResult decompile_listing(const std::string &listing, const Decom
         d.fallback_count = k.fallback_count;
         d.instructions = k.instructions;
         res.kernels.push_back(std::move(d));
+    }
+    for (uint64_t i = 0; i < r->ndumps; ++i) {
+        const ocldec_b200_dump &d = r->dumps[i];
+        DecompiledKernel &k = res.kernels[d.kernel];
+        std::string text(r->dump_text + d.off, d.len);
+        if (d.step < 0)
+            k.cfg_dot = std::move(text);
+        else
+            k.region_dumps.push_back(std::move(text));
     }
     auto take = [&](const ocldec_b200_diag *v, uint64_t n, std::vector<Diagnostic> &out) {
         for (uint64_t i = 0; i < n; ++i) {

@@ -41,6 +41,10 @@ def lib():
                                         ctypes.c_char_p, ctypes.c_size_t,
                                         ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_size_t)]
         L.ref_decompile_abi.restype = ctypes.c_int
+        L.ref_decompile_ex.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_char_p,
+                                       ctypes.c_char_p, ctypes.c_size_t, ctypes.c_int,
+                                       ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_size_t)]
+        L.ref_decompile_ex.restype = ctypes.c_int
         L.ref_free.argtypes = [ctypes.c_void_p]
         L.ref_decompile_batch.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
                                           ctypes.c_void_p, ctypes.c_void_p,
@@ -62,6 +66,8 @@ class RefKernel:
     failed: bool
     structured: bool
     fallback_count: int
+    cfg_dot: bytes = b""                                   # DecompiledKernel::cfg_dot (dump_cfg)
+    region_dumps: List[bytes] = field(default_factory=list)  # ReduceResult::dumps (dump_regions)
 
 
 @dataclass
@@ -84,17 +90,22 @@ def _take(ptr: int, n: int) -> bytes:
 
 
 def decompile(listing: bytes, fold_local_size: bool = False, only_kernel: Optional[bytes] = None,
-              abi_map: Optional[bytes] = None) -> RefResult:
+              abi_map: Optional[bytes] = None, dump_cfg: bool = False,
+              dump_regions: bool = False) -> RefResult:
     if isinstance(listing, str):
         listing = listing.encode()
     L = lib()
     out = ctypes.c_void_p()
     n = ctypes.c_size_t()
-    if abi_map is None:
+    if isinstance(abi_map, str):
+        abi_map = abi_map.encode()
+    dumps = int(dump_cfg) | (2 if dump_regions else 0)
+    if dumps:
+        L.ref_decompile_ex(listing, len(listing), int(fold_local_size), only_kernel, abi_map,
+                           len(abi_map) if abi_map is not None else 0, dumps, ctypes.byref(out), ctypes.byref(n))
+    elif abi_map is None:
         L.ref_decompile(listing, len(listing), int(fold_local_size), only_kernel, ctypes.byref(out), ctypes.byref(n))
     else:
-        if isinstance(abi_map, str):
-            abi_map = abi_map.encode()
         L.ref_decompile_abi(listing, len(listing), int(fold_local_size), only_kernel, abi_map, len(abi_map),
                             ctypes.byref(out), ctypes.byref(n))
     blob = _take(out.value, n.value)
@@ -120,6 +131,15 @@ def decompile(listing: bytes, fold_local_size: bool = False, only_kernel: Option
             sev, line, mlen = (int(x) for x in head[1:])
             res.abi_diagnostics.append(RefDiag(sev, line, blob[pos:pos + mlen]))
             pos += mlen
+        elif head[0] == b"G":
+            ki, glen = int(head[1]), int(head[2])
+            res.kernels[ki].cfg_dot = blob[pos:pos + glen]
+            pos += glen
+        elif head[0] == b"R":
+            ki, step, rlen = int(head[1]), int(head[2]), int(head[3])
+            assert step == len(res.kernels[ki].region_dumps)
+            res.kernels[ki].region_dumps.append(blob[pos:pos + rlen])
+            pos += rlen
         elif head[0] == b"C":
             clen = int(head[1])
             res.combined = blob[pos:pos + clen]

@@ -63,18 +63,22 @@ struct DecompileJob {
     const char *abi_map; // override file text (parse_abi_overrides, abi_model.cpp:109-153) or null
     size_t abi_len;
     std::string serialized;
+    int dumps = 0; // 1: dump_cfg, 2: dump_regions (DecompileOptions, decompiler.hpp:33-34)
 };
 
 // Serialization (parsed by oracle/oracle.py):
 //   "K <failed> <structured> <fallbacks> <name_len> <src_len>\n" name source
 //   "D <severity> <line> <msg_len>\n" message
 //   "C <len>\n" combined_source
+//   "G <kernel> <len>\n" cfg_dot, "R <kernel> <step> <len>\n" reduction.dumps[step]
 void *decompile_job(void *p) {
     auto *job = static_cast<DecompileJob *>(p);
     ocldec::DecompileOptions opts;
     opts.folds.fold_local_size = job->fold_local_size != 0;
     if (job->only_kernel)
         opts.only_kernel = std::string(job->only_kernel);
+    opts.dump_cfg = (job->dumps & 1) != 0;
+    opts.dump_regions = (job->dumps & 2) != 0;
     std::string out;
     if (job->abi_map) {
         ocldec::DiagnosticSink osink;
@@ -98,6 +102,18 @@ void *decompile_job(void *p) {
         out += "D " + std::to_string(int(d.severity)) + " " + std::to_string(d.line) + " " +
                std::to_string(d.message.size()) + "\n";
         out += d.message;
+    }
+    for (size_t i = 0; i < res.kernels.size(); ++i) {
+        const auto &k = res.kernels[i];
+        if (!k.cfg_dot.empty()) {
+            out += "G " + std::to_string(i) + " " + std::to_string(k.cfg_dot.size()) + "\n";
+            out += k.cfg_dot;
+        }
+        for (size_t j = 0; j < k.reduction.dumps.size(); ++j) {
+            out += "R " + std::to_string(i) + " " + std::to_string(j) + " " +
+                   std::to_string(k.reduction.dumps[j].size()) + "\n";
+            out += k.reduction.dumps[j];
+        }
     }
     std::string combined = res.combined_source();
     out += "C " + std::to_string(combined.size()) + "\n";
@@ -163,6 +179,16 @@ int ref_decompile(const char *listing, size_t len, int fold_local_size, const ch
 int ref_decompile_abi(const char *listing, size_t len, int fold_local_size, const char *only_kernel,
                       const char *abi_map, size_t abi_len, char **out, size_t *out_len) {
     DecompileJob job{listing, len, fold_local_size, only_kernel, abi_map, abi_len, {}};
+    run_on_big_stack(decompile_job, &job);
+    *out = dup_out(job.serialized, out_len);
+    return 0;
+}
+
+// Everything: options, ABI override text (null = none) and the DOT dumps
+// (dumps bit 0: dump_cfg, bit 1: dump_regions).
+int ref_decompile_ex(const char *listing, size_t len, int fold_local_size, const char *only_kernel,
+                     const char *abi_map, size_t abi_len, int dumps, char **out, size_t *out_len) {
+    DecompileJob job{listing, len, fold_local_size, only_kernel, abi_map, abi_len, {}, dumps};
     run_on_big_stack(decompile_job, &job);
     *out = dup_out(job.serialized, out_len);
     return 0;

@@ -28,11 +28,12 @@ SHAPES = {"C1": 1, "C2": 2, "C3": 3, "C4": 4, "C5": 5}
 class DecompileOptions:
     """DecompileOptions (decompiler.hpp:29-35).  ``abi_map`` is the override
     file text the reference CLI's --abi-map reads (parse_abi_overrides,
-    abi_model.cpp:109-153) standing for ``abi_overrides``; the DOT dumps are
-    not supported by this version."""
+    abi_model.cpp:109-153) standing for ``abi_overrides``."""
     fold_local_size: bool = False           # FoldOptions (sym_state.hpp:27-29)
     only_kernel: Optional[str] = None       # restrict to one kernel by name
     abi_map: Optional[Union[str, bytes]] = None
+    dump_cfg: bool = False                  # DecompiledKernel.cfg_dot (to_dot, cfg.cpp:400-424)
+    dump_regions: bool = False              # region_dumps (region_graph_dot, structurizer.cpp:669-688)
     device: int = 0
     arena_bytes: int = 0                    # per-thread arena, 0 = default
 
@@ -58,6 +59,8 @@ class DecompiledKernel:
     failed: bool
     fallback_count: int
     instructions: int
+    cfg_dot: str = ""                                        # when dump_cfg
+    region_dumps: List[str] = field(default_factory=list)   # reduction.dumps when dump_regions
 
 
 @dataclass
@@ -95,7 +98,8 @@ def decompile_listing(listing: Union[str, bytes], opts: Optional[DecompileOption
         amap = amap.encode("utf-8", errors="surrogateescape")
     o = _lib.Options(int(opts.fold_local_size),
                      opts.only_kernel.encode() if opts.only_kernel is not None else None,
-                     opts.device, opts.arena_bytes, amap, len(amap) if amap is not None else 0)
+                     opts.device, opts.arena_bytes, amap, len(amap) if amap is not None else 0,
+                     int(opts.dump_cfg), int(opts.dump_regions))
     out = ctypes.POINTER(_lib.Result)()
     rc = L.ocldec_b200_decompile(listing, len(listing), ctypes.byref(o), ctypes.byref(out))
     if rc != 0:
@@ -114,6 +118,16 @@ def decompile_listing(listing: Union[str, bytes], opts: Optional[DecompileOption
                 source=src.decode("utf-8", errors="surrogateescape"),
                 structured=bool(k.structured), failed=bool(k.failed),
                 fallback_count=k.fallback_count, instructions=k.instructions))
+        if r.ndumps:
+            dl = [r.dumps[i] for i in range(r.ndumps)]
+            dtext = ctypes.string_at(r.dump_text, max(d.off + d.len for d in dl))
+            for d in dl:
+                txt = dtext[d.off:d.off + d.len].decode("utf-8", errors="surrogateescape")
+                k = res.kernels[d.kernel]
+                if d.step < 0:
+                    k.cfg_dot = txt
+                else:
+                    k.region_dumps.append(txt)
         alld = [r.diags[i] for i in range(r.ndiags)] + [r.abi_diags[i] for i in range(r.nabi_diags)]
         tlen = max((d.msg_off + d.msg_len for d in alld), default=0)
         text = ctypes.string_at(r.diag_text, tlen) if r.diag_text and tlen else b""

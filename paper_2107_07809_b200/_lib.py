@@ -17,7 +17,8 @@ LIB_PATH = os.environ.get("OCLDEC_B200_LIB") or os.path.join(_HERE, "libocldec_b
 class Options(ctypes.Structure):
     _fields_ = [("fold_local_size", ctypes.c_int), ("only_kernel", ctypes.c_char_p),
                 ("device", ctypes.c_int), ("arena_bytes", ctypes.c_size_t),
-                ("abi_map", ctypes.c_char_p), ("abi_map_len", ctypes.c_size_t)]
+                ("abi_map", ctypes.c_char_p), ("abi_map_len", ctypes.c_size_t),
+                ("dump_cfg", ctypes.c_int), ("dump_regions", ctypes.c_int)]
 
 
 class Kernel(ctypes.Structure):
@@ -32,6 +33,11 @@ class Diag(ctypes.Structure):
                 ("msg_off", ctypes.c_uint64), ("msg_len", ctypes.c_uint64)]
 
 
+class Dump(ctypes.Structure):
+    _fields_ = [("kernel", ctypes.c_uint64), ("step", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("off", ctypes.c_uint64), ("len", ctypes.c_uint64)]
+
+
 class Result(ctypes.Structure):
     _fields_ = [("nkernels", ctypes.c_uint64), ("kernels", ctypes.POINTER(Kernel)),
                 ("names", ctypes.c_void_p), ("combined", ctypes.c_void_p),
@@ -39,7 +45,8 @@ class Result(ctypes.Structure):
                 ("split_error_kind", ctypes.c_int32), ("instructions", ctypes.c_uint64),
                 ("device_ms", ctypes.c_double), ("ndiags", ctypes.c_uint64),
                 ("diags", ctypes.POINTER(Diag)), ("diag_text", ctypes.c_void_p),
-                ("nabi_diags", ctypes.c_uint64), ("abi_diags", ctypes.POINTER(Diag))]
+                ("nabi_diags", ctypes.c_uint64), ("abi_diags", ctypes.POINTER(Diag)),
+                ("ndumps", ctypes.c_uint64), ("dumps", ctypes.POINTER(Dump)), ("dump_text", ctypes.c_void_p)]
 
 
 class Stats(ctypes.Structure):

@@ -735,6 +735,9 @@ struct ocldec_b200_session {
     DevBuf dpool, dtop;              // device diagnostic records of a chunk
     std::vector<HostDiag> host_diag; // materialized diagnostics, all chunks
     std::vector<HostOvr> ovr_host;   // ABI overrides of the current call
+    u32 dump_flags = 0;              // DOT dumps of the current call (DumpFlags)
+    DevBuf xtext, xrec, xtop, xcfg;  // device dump pool (DumpCfg)
+    std::vector<std::vector<std::pair<int32_t, std::string>>> host_dumps; // per host_res kernel
     std::vector<OvrDiag> ovr_diags;  // their parse diagnostics
     DevBuf dovr, dovr_text;
     u32 novr = 0;
@@ -951,6 +954,23 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     a.ovr = s->novr ? P<AbiOvr>(s->dovr) : nullptr;
     a.novr = s->novr;
     a.ovr_text = s->novr ? P<u8>(s->dovr_text) : nullptr;
+    a.dump = nullptr;
+    DumpCfg dc{};
+    if (s->dump_flags) {
+        if (ensure(s->xtext, std::max<u64>(16ull << 20, std::min<u64>((u64)len * 2, 1ull << 30))) ||
+            ensure(s->xrec, std::max<u64>(1ull << 16, (u64)nk * 8) * sizeof(DumpRec)) ||
+            ensure(s->xtop, 16) || ensure(s->xcfg, sizeof(DumpCfg)))
+            return -3;
+        CK(cudaMemsetAsync(s->xtop.p, 0, 16, st));
+        dc.text = P<u8>(s->xtext);
+        dc.cap = s->xtext.cap;
+        dc.rec = P<DumpRec>(s->xrec);
+        dc.rcap = s->xrec.cap / sizeof(DumpRec);
+        dc.top = P<unsigned long long>(s->xtop);
+        dc.flags = s->dump_flags;
+        CK(cudaMemcpyAsync(s->xcfg.p, &dc, sizeof(dc), cudaMemcpyHostToDevice, st));
+        a.dump = P<DumpCfg>(s->xcfg);
+    }
     a.res = P<KRes>(s->res);
     a.only = s->only_set ? P<u8>(s->only) : nullptr;
     a.only_len = s->only_len;
@@ -1104,6 +1124,26 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
             u64 dt = 0;
             if (d2h_sync(s, &dt, s->dtop.p, 8))
                 return -3;
+            if (s->dump_flags) { // dump pool full: grow it, keep what was written
+                u64 xt[2];
+                if (d2h_sync(s, xt, s->xtop.p, 16))
+                    return -3;
+                if (xt[0] > dc.cap || xt[1] > dc.rcap) {
+                    const u64 tkeep = std::min<u64>(xt[0], dc.cap), rkeep = std::min<u64>(xt[1], dc.rcap);
+                    if (ensure_keep(s->xtext, std::max<u64>(xt[0], dc.cap) * 2, tkeep, st) ||
+                        ensure_keep(s->xrec, std::max<u64>(xt[1], dc.rcap) * 2 * sizeof(DumpRec),
+                                    rkeep * sizeof(DumpRec), st))
+                        return -3;
+                    dc.text = P<u8>(s->xtext);
+                    dc.cap = s->xtext.cap;
+                    dc.rec = P<DumpRec>(s->xrec);
+                    dc.rcap = s->xrec.cap / sizeof(DumpRec);
+                    const u64 nt[2] = {tkeep, rkeep};
+                    CK(cudaMemcpyAsync(s->xtop.p, nt, 16, cudaMemcpyHostToDevice, st));
+                    CK(cudaMemcpyAsync(s->xcfg.p, &dc, sizeof(dc), cudaMemcpyHostToDevice, st));
+                    CK(cudaStreamSynchronize(st));
+                }
+            }
             if (dt > a.dcap) { // diagnostic pool full: grow it, keep the records written so far
                 const u64 old_cap = a.dcap;
                 if (ensure_keep(s->dpool, dt * 2 * sizeof(Diag), old_cap * sizeof(Diag), st))
@@ -1205,6 +1245,30 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
             hr[k].ndiag = 0;
         }
     }
+    if (s->dump_flags) {
+        // DOT dumps: one record per (kernel, step); a retried kernel wrote
+        // its dumps again (identical), so the last record of a key wins
+        u64 xt[2];
+        if (d2h_sync(s, xt, s->xtop.p, 16))
+            return -3;
+        const u64 nr = std::min<u64>(xt[1], dc.rcap), nt = std::min<u64>(xt[0], dc.cap);
+        std::vector<DumpRec> rv(nr);
+        std::string tx(nt, '\0');
+        if ((nr && d2h_sync(s, rv.data(), s->xrec.p, nr * sizeof(DumpRec))) ||
+            (nt && d2h_sync(s, &tx[0], s->xtext.p, nt)))
+            return -3;
+        std::vector<std::map<int32_t, std::string>> per(nk);
+        for (const DumpRec &d : rv)
+            if (d.k < nk && d.off + d.len <= nt)
+                per[d.k][d.step] = tx.substr(d.off, d.len);
+        for (u32 k = 0; k < nk; ++k) {
+            std::vector<std::pair<int32_t, std::string>> v;
+            if (hr[k].status == KS_OK || hr[k].status == KS_FAILED)
+                for (auto &e : per[k])
+                    v.emplace_back(e.first, std::move(e.second));
+            s->host_dumps.push_back(std::move(v));
+        }
+    }
     for (u32 k = 0; k < nk; ++k) {
         s->host_res.push_back(hr[k]);
         s->host_kernel_off.push_back(base + offs[k]);
@@ -1301,6 +1365,7 @@ void reset_stats(ocldec_b200_session *s) {
     s->host_name_line.clear();
     s->host_diag.clear();
     s->host_kdiag.clear();
+    s->host_dumps.clear();
     s->out_len = 0;
 }
 
@@ -1434,6 +1499,7 @@ int run_host_listing(ocldec_b200_session *s, const char *listing, size_t len, in
             s->host_kernel_off.clear();
             s->host_diag.clear();
             s->host_kdiag.clear();
+            s->host_dumps.clear();
             hr->names.clear();
             out_pos = 0;
             break;
@@ -1618,7 +1684,9 @@ int ocldec_b200_decompile(const char *listing, size_t len, const ocldec_b200_opt
     HostRun hr;
     if (int rc0 = set_overrides(s, o.abi_map, o.abi_map ? o.abi_map_len : 0))
         return rc0;
+    s->dump_flags = (o.dump_cfg ? DUMP_CFG : 0u) | (o.dump_regions ? DUMP_REGIONS : 0u);
     int rc = run_host_listing(s, listing, len, o.fold_local_size, o.only_kernel, &hr);
+    s->dump_flags = 0;
     if (rc)
         return rc;
     auto *res = static_cast<ocldec_b200_result *>(calloc(1, sizeof(ocldec_b200_result)));
@@ -1654,6 +1722,33 @@ int ocldec_b200_decompile(const char *listing, size_t len, const ocldec_b200_opt
         res->instructions += r.ninstr;
     }
     res->nkernels = nkept;
+    {
+        // DecompiledKernel::cfg_dot and ReduceResult::dumps, kernel by kernel
+        std::vector<ocldec_b200_dump> dv;
+        std::string dtx;
+        u64 kk = 0;
+        for (size_t k = 0; k < nk && k < s->host_dumps.size(); ++k) {
+            if (s->host_res[k].status == KS_SKIP)
+                continue;
+            for (const auto &e : s->host_dumps[k]) {
+                ocldec_b200_dump d{};
+                d.kernel = kk;
+                d.step = e.first;
+                d.off = dtx.size();
+                d.len = e.second.size();
+                dtx += e.second;
+                dv.push_back(d);
+            }
+            ++kk;
+        }
+        res->ndumps = dv.size();
+        res->dumps = static_cast<ocldec_b200_dump *>(malloc((dv.size() + 1) * sizeof(ocldec_b200_dump)));
+        if (!dv.empty())
+            memcpy(res->dumps, dv.data(), dv.size() * sizeof(ocldec_b200_dump));
+        res->dump_text = static_cast<char *>(malloc(dtx.size() + 1));
+        memcpy(res->dump_text, dtx.data(), dtx.size());
+        res->dump_text[dtx.size()] = 0;
+    }
     res->names = static_cast<char *>(malloc(nm.size() + 1));
     memcpy(res->names, nm.data(), nm.size());
     res->names[nm.size()] = 0;
@@ -1752,6 +1847,8 @@ void ocldec_b200_free(ocldec_b200_result *res) {
     free(res->kernels);
     free(res->names);
     free(res->combined);
+    free(res->dumps);
+    free(res->dump_text);
     free(res->diags); // abi_diags points into the same array
     free(res->diag_text);
     free(res);

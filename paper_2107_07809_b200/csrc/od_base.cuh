@@ -155,6 +155,16 @@ OD_INL u32 ctz64(u64 m) {
 #endif
 }
 
+OD_INL u64 fetch_add_u64(unsigned long long *p, u64 v) {
+#ifdef __CUDA_ARCH__
+    return (u64)atomicAdd(p, (unsigned long long)v);
+#else
+    const u64 o = *p;
+    *p += v;
+    return o;
+#endif
+}
+
 constexpr u32 kNoRank = 0xffffffffu;
 
 // ------------------------------------------------------------- characters

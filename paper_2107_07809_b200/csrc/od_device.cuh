@@ -24,7 +24,7 @@ struct KRes {
     u32 ndiag;      // diagnostics of the kernel, at diag_off in the diagnostic pool
     u64 diag_off;
 };
-enum : u32 { KS_SKIP = 4, KS_STAGE_FULL = 5 };
+
 
 struct DecompArgs {
     const u8 *t;
@@ -52,6 +52,7 @@ struct DecompArgs {
     const AbiOvr *ovr; // ABI overrides of the run (novr)
     u32 novr;
     const u8 *ovr_text;
+    const DumpCfg *dump; // DOT dumps (null: none)
     Diag *dpool;   // diagnostic records of finished kernels
     u64 dcap;
     unsigned long long *dtop;

@@ -40,6 +40,8 @@ __global__ void __launch_bounds__(128, OD_MINB_FRONT) k_front(DecompArgs a) {
     in.ovr = a.ovr;
     in.novr = a.novr;
     in.ovr_text = a.ovr_text;
+    in.dump = a.dump;
+    in.kidx = k;
     g->mem.base = sl.base + kb;
     g->mem.top = 0;
     g->mem.cap = a.boff[i + 1] - a.boff[i] - kb;

@@ -39,7 +39,7 @@ struct Bump {
     }
 };
 
-enum KStatus : u32 { KS_OK = 0, KS_FAILED = 1, KS_OOM = 2, KS_SPLIT_ERROR = 3 };
+enum KStatus : u32 { KS_OK = 0, KS_FAILED = 1, KS_OOM = 2, KS_SPLIT_ERROR = 3, KS_SKIP = 4, KS_STAGE_FULL = 5 };
 
 // One ABI override (DecompileOptions::abi_overrides, abi_model.hpp:64-68),
 // resolved on the host except for the per-kernel argument lookup.
@@ -48,6 +48,23 @@ struct AbiOvr {
     u32 offset;
     u8 dwords, kind, fn, dim;
     u32 name_off, name_len; // OV_ARG: argument name in the override text
+};
+
+// DOT dumps (DecompileOptions::dump_cfg / dump_regions, decompiler.hpp:33-34):
+// text appended to a run-wide pool, one record per dump.
+enum DumpFlags : u32 { DUMP_CFG = 1, DUMP_REGIONS = 2 };
+struct DumpRec {
+    u32 k;      // kernel (chunk result index)
+    i32 step;   // -1: cfg_dot, else ReduceResult::dumps[step]
+    u64 off, len;
+};
+struct DumpCfg {
+    u8 *text;
+    u64 cap;
+    DumpRec *rec;
+    u64 rcap;
+    unsigned long long *top; // [0] text bytes, [1] records (may pass the caps: pool full)
+    u32 flags;
 };
 
 // Inputs for one kernel section.
@@ -66,6 +83,8 @@ struct KIn {
     const AbiOvr *ovr;    // ABI overrides (novr), applied by build_abi
     u32 novr;
     const u8 *ovr_text;
+    const DumpCfg *dump;  // DOT dumps (null: none)
+    u32 kidx;             // chunk result index (dump records)
     u64 *prof;            // optional per-phase cycle counters
 };
 
@@ -353,6 +372,8 @@ struct KCtx {
     u32 root_r;
     bool reduced;
     u32 nif;      // IfThen / IfElse merges (joins need liveness)
+    u32 nmerge;   // merges so far (dump step numbers)
+    bool dump_full; // the dump pool overflowed
 
     // liveness
     u32 *live_in; // [nblk][12]
@@ -1955,6 +1976,164 @@ OD_NOINL u32 region_rpo(KCtx &K) {
 // Here the order is maintained across merges (region_replace) and a region
 // whose matchers failed is only retried once a merge touched its
 // neighbourhood, which selects the same region at every step.
+// ========================================================== DOT dumps
+// Two passes over the same printer: count (p == null), then write.
+struct DotSink {
+    u8 *p;
+    u64 n;
+    OD_INL void c(u8 ch) {
+        if (p)
+            p[n] = ch;
+        ++n;
+    }
+    OD_NOINL void s(const char *z) {
+        while (*z)
+            c((u8)*z++);
+    }
+    OD_NOINL void m(const u8 *b, u32 len) {
+        for (u32 i = 0; i < len; ++i)
+            c(b[i]);
+    }
+    OD_NOINL void u(u64 v) {
+        u8 b[24];
+        int i = 0;
+        do {
+            b[i++] = (u8)('0' + v % 10);
+            v /= 10;
+        } while (v);
+        while (i)
+            c(b[--i]);
+    }
+};
+
+// to_dot  cfg.cpp:400-424 (after normalize_if_else, decompiler.cpp:72-73)
+OD_NOINL void cfg_dot(const KCtx &K, DotSink &o) {
+    const u8 *t = K.in->t;
+    Span nm;
+    {
+        Span w, rest, extra;
+        const LineRec &L = K.in->lines[K.in->lbeg];
+        split_word(t, Span{L.off, L.len}, &w, &rest);
+        split_word(t, rest, &nm, &extra);
+    }
+    o.s("digraph \"");
+    o.m(t + nm.off, nm.len);
+    o.s("\" {\n  node [shape=box, fontname=\"monospace\"];\n");
+    for (u32 b = 0; b < K.nblk; ++b) {
+        const Block &B = K.blk[b];
+        o.s("  b");
+        o.u(b);
+        o.s(" [label=\"B");
+        o.u(b);
+        for (u32 l = 0; l < B.lab_n; ++l) {
+            const Label &L = klabel(K, B.lab_b + l);
+            o.c(' ');
+            o.m(t + L.off, L.len);
+        }
+        o.s("\\n");
+        o.u(B.ie - B.ib);
+        o.s(" ins");
+        if (!blk_reach(K, b))
+            o.s(" (dead)");
+        o.s("\"];\n");
+    }
+    for (u32 b = 0; b < K.nblk; ++b) {
+        const Block &B = K.blk[b];
+        if (B.term.kind == T_COND) {
+            o.s("  b");
+            o.u(b);
+            o.s(" -> b");
+            o.u((u32)B.term.taken);
+            o.s(" [label=\"T\"];\n  b");
+            o.u(b);
+            o.s(" -> b");
+            o.u((u32)B.term.not_taken);
+            o.s(" [label=\"F\"];\n");
+        } else {
+            for (u32 q = 0; q < B.nsucc; ++q) {
+                o.s("  b");
+                o.u(b);
+                o.s(" -> b");
+                o.u((u32)B.succ[q]);
+                o.s(";\n");
+            }
+        }
+    }
+    o.s("}\n");
+}
+
+// region_graph_dot  structurizer.cpp:669-688.  Live regions in id order (the
+// reference appends each merged region to live_, so its order is by id);
+// a region is dead once it is a child of a merged region.
+OD_NOINL void region_dot(const KCtx &K, DotSink &o, u32 step) {
+    const u32 gen = ++const_cast<KCtx &>(K).rstamp_gen;
+    for (u32 r = 1; r <= K.nrg; ++r)
+        if (K.rg[r].kind != RK_BLOCK)
+            for (u32 c = 0; c < K.rg[r].ch_n; ++c)
+                K.rstamp[K.child[K.rg[r].ch_b + c]] = gen;
+    o.s("digraph \"step");
+    o.u(step);
+    o.s("\" {\n  node [shape=ellipse, fontname=\"monospace\"];\n");
+    for (u32 r = 1; r <= K.nrg; ++r) {
+        if (K.rstamp[r] == gen)
+            continue;
+        const Region &R = K.rg[r];
+        o.s("  r");
+        o.u(r);
+        o.s(" [label=\"");
+        o.u(r);
+        switch (R.kind) {
+        case RK_BLOCK:
+            o.s(" B");
+            o.u((u32)R.block_id);
+            break;
+        case RK_LINEAR: o.s(" lin"); break;
+        case RK_IFTHEN: o.s(" if"); break;
+        default: o.s(" if/else"); break;
+        }
+        o.s("\"];\n");
+    }
+    for (u32 r = 1; r <= K.nrg; ++r) {
+        if (K.rstamp[r] == gen)
+            continue;
+        const Region &R = K.rg[r];
+        for (u32 q = 0; q < R.nsucc; ++q) {
+            o.s("  r");
+            o.u(r);
+            o.s(" -> r");
+            o.u((u32)R.succ[q]);
+            o.s(";\n");
+        }
+    }
+    o.s("}\n");
+}
+
+// Appends one dump (step < 0: the CFG) to the run's pool.
+OD_NOINL void dump_emit(KCtx &K, i32 step) {
+    const DumpCfg &D = *K.in->dump;
+    DotSink c{nullptr, 0};
+    if (step < 0)
+        cfg_dot(K, c);
+    else
+        region_dot(K, c, (u32)step);
+    const u64 off = fetch_add_u64(&D.top[0], c.n);
+    const u64 ri = fetch_add_u64(&D.top[1], 1);
+    if (off + c.n > D.cap || ri >= D.rcap) {
+        K.dump_full = true;
+        return;
+    }
+    DotSink w{D.text + off, 0};
+    if (step < 0)
+        cfg_dot(K, w);
+    else
+        region_dot(K, w, (u32)step);
+    DumpRec &R = D.rec[ri];
+    R.k = K.in->kidx;
+    R.step = step;
+    R.off = off;
+    R.len = c.n;
+}
+
 OD_NOINL void reduce(KCtx &K) {
     const u32 n = region_rpo(K);
     K.ncand_w = n / 64 + 1;
@@ -1965,6 +2144,9 @@ OD_NOINL void reduce(KCtx &K) {
         K.at[i] = K.rpo[i];
         K.cand[i >> 6] |= 1ull << (i & 63);
     }
+    const bool dump = K.in->dump && (K.in->dump->flags & DUMP_REGIONS);
+    if (dump)
+        dump_emit(K, 0);
     while (K.nlive > 1 && !K.oom) {
         u32 pos = kNoRank;
         for (u32 w = 0; w < K.ncand_w; ++w)
@@ -1982,6 +2164,8 @@ OD_NOINL void reduce(KCtx &K) {
             m = match_linear(K, r);
         if (!m && !K.oom)
             K.cand[pos >> 6] &= ~(1ull << (pos & 63)); // fails until its neighbourhood changes
+        if (m && dump)
+            dump_emit(K, (i32)++K.nmerge);
     }
     K.reduced = K.nlive == 1;
     K.root_r = K.reduced ? (u32)K.entry_r : 0; // the one live region holds the entry

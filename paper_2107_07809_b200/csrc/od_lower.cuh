@@ -1597,10 +1597,17 @@ OD_NOINL void dk_front(KState &S) {
     normalize(K);
     OD_CHECK(!K.oom);
     OD_PROF(2, tp);
+    if (in.dump && (in.dump->flags & DUMP_CFG))
+        dump_emit(K, -1);
     OD_CHECK(build_regions(K));
     reduce(K);
     if (K.oom) {
         out.status = KS_OOM;
+        S.done = 1;
+        return;
+    }
+    if (K.dump_full) { // grow the dump pool and run the kernel again
+        out.status = KS_STAGE_FULL;
         S.done = 1;
         return;
     }

@@ -8,6 +8,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -121,6 +122,12 @@ int main(int argc, char **argv) {
         labs.resize(l0 + lins[l].nlabels);
     }
     std::string combined, per;
+    // OD_DUMP=1|2|3: DOT dumps (DumpFlags), printed as "G/R" records
+    std::vector<u8> dtext(getenv("OD_DUMP") ? (256u << 20) : 0);
+    std::vector<DumpRec> drec(getenv("OD_DUMP") ? (1u << 20) : 0);
+    unsigned long long dtop[2] = {0, 0};
+    DumpCfg dcfg{dtext.data(), dtext.size(), drec.data(), drec.size(), dtop,
+                 getenv("OD_DUMP") ? (u32)atoi(getenv("OD_DUMP")) : 0u};
     for (size_t k = 0; k < kstart.size(); ++k) {
         KIn kin;
         kin.t = t.data();
@@ -136,6 +143,8 @@ int main(int argc, char **argv) {
         kin.ovr = nullptr;
         kin.novr = 0;
         kin.ovr_text = nullptr;
+        kin.dump = dcfg.flags ? &dcfg : nullptr;
+        kin.kidx = (u32)k;
         KOut ko;
         const u8 *src = nullptr;
         std::vector<u8> arena;
@@ -189,6 +198,20 @@ int main(int argc, char **argv) {
             if (!combined.empty())
                 combined += "\n";
             combined += s;
+        }
+    }
+    {
+        // last record of each (kernel, step) wins (retries re-emit)
+        std::map<std::pair<u32, i32>, std::string> dm;
+        for (u64 i = 0; i < dtop[1]; ++i)
+            dm[{drec[i].k, drec[i].step}] = std::string((const char *)dtext.data() + drec[i].off, drec[i].len);
+        for (auto &e : dm) {
+            if (e.first.second < 0)
+                per += "G " + std::to_string(e.first.first) + " " + std::to_string(e.second.size()) + "\n";
+            else
+                per += "R " + std::to_string(e.first.first) + " " + std::to_string(e.first.second) + " " +
+                       std::to_string(e.second.size()) + "\n";
+            per += e.second;
         }
     }
     fwrite(per.data(), 1, per.size(), stdout);

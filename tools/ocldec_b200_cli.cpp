@@ -4,14 +4,15 @@
 // (/root/reference/proj/tools/ocldec.cpp:81-177) for the options this path
 // supports:
 //   ocldec-b200 <input> [-o|--output FILE] [--kernel NAME] [--fold-local-size]
-//               [--abi-map FILE]
+//               [--abi-map FILE] [--dump-cfg] [--dump-regions]
 // The output is combined_source() written atomically (temp file + rename,
 // ocldec.cpp:35-57) to FILE or <input stem>.cl (ocldec.cpp:59-66).
 // Diagnostics go to stderr as "file:line: severity: message"; exit status is 1
 // when no kernel was produced or any kernel failed, 0 otherwise.
 // --abi-map FILE is parsed first; its diagnostics are printed against FILE and
 // any error exits 1 before decompiling (ocldec.cpp:120-131).
-// --dump-cfg / --dump-regions are rejected (not supported).
+// --dump-cfg / --dump-regions write <out stem>.<kernel>.cfg.dot and
+// <out stem>.<kernel>.step<N>.dot next to the output (ocldec.cpp:68-77, 150-165).
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -57,6 +58,16 @@ bool write_atomic(const std::string &path, const std::string &content, std::stri
     return true;
 }
 
+// <output stem>.<kernel> (ocldec.cpp:68-77)
+std::string dump_stem(const std::string &output, const std::string &kernel) {
+    std::string stem = output;
+    size_t slash = stem.find_last_of("/\\");
+    size_t dot = stem.find_last_of('.');
+    if (dot != std::string::npos && (slash == std::string::npos || dot > slash))
+        stem.resize(dot);
+    return stem + "." + kernel;
+}
+
 std::string default_output(const std::string &input) {
     std::string stem = input;
     size_t slash = stem.find_last_of("/\\");
@@ -70,7 +81,7 @@ int usage(const char *argv0, int code) {
     std::fprintf(code ? stderr : stdout,
                  "Decompiles AMD GCN disassembly listings (CLRX syntax) to OpenCL C on the GPU\n"
                  "Usage: %s input [-o OUTPUT] [--kernel NAME] [--fold-local-size] [--abi-map FILE]\n"
-                 "       [--device N]\n",
+                 "       [--dump-cfg] [--dump-regions] [--device N]\n",
                  argv0);
     return code;
 }
@@ -106,8 +117,8 @@ int main(int argc, char **argv) {
             continue;
         }
         if (a == "--dump-cfg" || a == "--dump-regions") {
-            std::cerr << "ocldec-b200: error: " << a << " is not supported by this build\n";
-            return 1;
+            (a == "--dump-cfg" ? opts.dump_cfg : opts.dump_regions) = true;
+            continue;
         }
         if (!a.empty() && a[0] == '-')
             return usage(argv[0], 1);
@@ -160,6 +171,20 @@ int main(int argc, char **argv) {
         any_failed = any_failed || k.failed;
     if (output.empty())
         output = default_output(input);
+    if (opts.dump_cfg || opts.dump_regions) {
+        for (const auto &k : result.kernels) {
+            const std::string stem = dump_stem(output, k.name);
+            if (opts.dump_cfg && !k.cfg_dot.empty() && !write_atomic(stem + ".cfg.dot", k.cfg_dot, err)) {
+                std::cerr << "ocldec-b200: error: " << err << "\n";
+                return 1;
+            }
+            for (size_t i = 0; i < k.region_dumps.size(); ++i)
+                if (!write_atomic(stem + ".step" + std::to_string(i) + ".dot", k.region_dumps[i], err)) {
+                    std::cerr << "ocldec-b200: error: " << err << "\n";
+                    return 1;
+                }
+        }
+    }
     if (!write_atomic(output, result.combined_source(), err)) {
         std::cerr << "ocldec-b200: error: " << err << "\n";
         return 1;
