@@ -457,8 +457,10 @@ struct DevBuf {
 int ensure(DevBuf &b, size_t bytes) {
     if (bytes <= b.cap && b.p)
         return 0;
-    if (b.p)
+    if (b.p) {
+        cudaDeviceSynchronize(); // copies on the copy stream may still read it
         cudaFree(b.p);
+    }
     size_t want = std::max(bytes + 256, b.cap + b.cap / 2);
     b.p = nullptr;
     b.cap = 0;
@@ -478,8 +480,10 @@ int ensure_keep(DevBuf &b, size_t bytes, size_t keep, cudaStream_t st) {
         CK(cudaMemcpyAsync(np, b.p, std::min(keep, b.cap), cudaMemcpyDeviceToDevice, st));
         CK(cudaStreamSynchronize(st));
     }
-    if (b.p)
+    if (b.p) {
+        cudaDeviceSynchronize(); // copies on the copy stream may still read it
         cudaFree(b.p);
+    }
     b.p = np;
     b.cap = want;
     return 0;
@@ -713,6 +717,9 @@ struct ocldec_b200_session {
     int nsm = 148;
     cudaStream_t stream = nullptr;
     cudaStream_t stream2 = nullptr; // second decompile-wave stream
+    cudaStream_t cstream = nullptr; // host<->device copies overlapped with the chunks
+    cudaEvent_t cev[3];             // [0..1] text buffer loaded, [2] chunk output ready
+    DevBuf text2;                   // second chunk text buffer (double buffering)
     size_t arena_bytes = 0;
     DevBuf text, tiles, tiles_off, nlpos, lines, lins, ops_cnt, labs_cnt, ops_off, labs_off, ops,
         labs, kstart, scan_tmp, scan_tot, counters, arena, stage, res, outoff, out, only, retry,
@@ -1305,6 +1312,9 @@ int session_init(ocldec_b200_session *s, int device, size_t arena_bytes) {
     }
     for (auto &e : s->ev)
         CK(cudaEventCreate(&e));
+    CK(cudaStreamCreateWithFlags(&s->cstream, cudaStreamNonBlocking));
+    for (auto &e : s->cev)
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     // arena pool for one decompile wave (per-kernel slices sized by arena_budget)
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
@@ -1370,9 +1380,10 @@ void reset_stats(ocldec_b200_session *s) {
 }
 
 // Splits a host listing into chunks of < ~1 GiB at ".kernel" line starts.
-std::vector<u64> host_chunks(const char *p, size_t len, size_t target) {
+// The first chunk is `first` bytes (its load is the one copy nothing hides).
+std::vector<u64> host_chunks(const char *p, size_t len, size_t target, size_t first) {
     std::vector<u64> starts{0};
-    size_t next = target;
+    size_t next = first;
     while (next < len) {
         // find a line whose first word is exactly ".kernel"
         size_t i = next;
@@ -1405,6 +1416,7 @@ struct HostRun {
     u64 out_bytes = 0;
     int32_t split_error_line = 0, split_error_kind = 0;
     double device_ms = 0;
+    bool want_names = true; // kernel names for the result (not needed by session_run_host)
     std::vector<std::string> names;
 };
 
@@ -1458,8 +1470,13 @@ int set_overrides(ocldec_b200_session *s, const char *text, size_t len) {
 // decompile_listing over a host buffer: chunking at .kernel lines, H2D of
 // each chunk, the device pipeline, names back to the host.  Output stays in
 // s->out[0, out_bytes).
+// With host_out, each chunk's output is copied back into host_out on the copy
+// stream while the next chunk runs (host_out must hold out_cap bytes; output
+// beyond it is not copied).  The next chunk's text is loaded the same way
+// into the other of two text buffers, so the PCIe traffic hides behind the
+// decompiler except for the first load and the last store.
 int run_host_listing(ocldec_b200_session *s, const char *listing, size_t len, int fold_local_size,
-                     const char *only_kernel, HostRun *hr) {
+                     const char *only_kernel, HostRun *hr, char *host_out, u64 out_cap) {
     reset_stats(s);
     s->stats.in_bytes = len;
     s->only_len = 0;
@@ -1473,25 +1490,52 @@ int run_host_listing(ocldec_b200_session *s, const char *listing, size_t len, in
     } else {
         s->only_set = false;
     }
-    std::vector<u64> starts = host_chunks(listing, len, chunk_target());
+    const size_t target = chunk_target();
+    std::vector<u64> starts = host_chunks(listing, len, target, std::max<size_t>(target / 4, 1));
+    const size_t nch = starts.size();
+    auto cb = [&](size_t c) { return starts[c]; };
+    auto ce = [&](size_t c) { return c + 1 < nch ? starts[c + 1] : (u64)len; };
+    u64 maxn = 0;
+    for (size_t c = 0; c < nch; ++c)
+        maxn = std::max<u64>(maxn, ce(c) - cb(c));
+    DevBuf *tb[2] = {&s->text, &s->text2};
+    if (ensure(s->text, 2 * maxn + 4096) || (nch > 1 && ensure(s->text2, 2 * maxn + 4096)))
+        return -3;
+    auto load = [&](size_t c) -> int {
+        const u64 n = ce(c) - cb(c);
+        if (n)
+            CK(cudaMemcpyAsync(tb[c & 1]->p, listing + cb(c), n, cudaMemcpyHostToDevice, s->cstream));
+        CK(cudaEventRecord(s->cev[c & 1], s->cstream));
+        return 0;
+    };
     u64 out_pos = 0;
     u32 line_base = 0;
     bool nonempty = false;
     cudaEvent_t e0 = s->ev[5], e1 = s->ev[6];
     CK(cudaEventRecord(e0, s->stream));
-    for (size_t c = 0; c < starts.size(); ++c) {
-        u64 b = starts[c];
-        u64 e = c + 1 < starts.size() ? starts[c + 1] : len;
-        u64 n = e - b;
-        if (ensure(s->text, 2 * n + 4096))
+    if (nch && load(0))
+        return -3;
+    for (size_t c = 0; c < nch; ++c) {
+        u64 b = cb(c);
+        u64 n = ce(c) - b;
+        // the other buffer's chunk (c - 1) is finished: run_chunk returns synchronized
+        if (c + 1 < nch && load(c + 1))
             return -3;
-        if (n)
-            CK(cudaMemcpyAsync(s->text.p, listing + b, n, cudaMemcpyHostToDevice, s->stream));
+        CK(cudaStreamWaitEvent(s->stream, s->cev[c & 1], 0));
+        u8 *tc = P<u8>(*tb[c & 1]);
         ChunkOut co;
         size_t before = s->host_res.size();
-        int rc = run_chunk(s, P<u8>(s->text), n, true, line_base, fold_local_size, out_pos, nonempty, &co);
-        if (rc)
+        int rc = run_chunk(s, tc, n, true, line_base, fold_local_size, out_pos, nonempty, &co);
+        if (rc) {
+            cudaStreamSynchronize(s->cstream);
             return rc;
+        }
+        if (host_out && co.err_line == 0xffffffffu && co.out_bytes && out_pos + co.out_bytes <= out_cap) {
+            CK(cudaEventRecord(s->cev[2], s->stream));
+            CK(cudaStreamWaitEvent(s->cstream, s->cev[2], 0));
+            CK(cudaMemcpyAsync(host_out + out_pos, P<u8>(s->out) + out_pos, co.out_bytes, cudaMemcpyDeviceToHost,
+                               s->cstream));
+        }
         if (co.err_line != 0xffffffffu) {
             hr->split_error_line = (int32_t)(line_base + co.err_line + 1);
             hr->split_error_kind = (int32_t)co.err_kind;
@@ -1504,7 +1548,7 @@ int run_host_listing(ocldec_b200_session *s, const char *listing, size_t len, in
             out_pos = 0;
             break;
         }
-        for (size_t k = before; k < s->host_res.size(); ++k) {
+        for (size_t k = before; hr->want_names && k < s->host_res.size(); ++k) {
             const KRes &r = s->host_res[k];
             std::string nm;
             if (r.name_off + (u64)r.name_len <= n) {
@@ -1512,7 +1556,7 @@ int run_host_listing(ocldec_b200_session *s, const char *listing, size_t len, in
             } else {
                 nm.resize(r.name_len);
                 if (r.name_len)
-                    CK(cudaMemcpy(&nm[0], P<u8>(s->text) + r.name_off, r.name_len, cudaMemcpyDeviceToHost));
+                    CK(cudaMemcpy(&nm[0], tc + r.name_off, r.name_len, cudaMemcpyDeviceToHost));
             }
             hr->names.push_back(nm);
         }
@@ -1524,6 +1568,7 @@ int run_host_listing(ocldec_b200_session *s, const char *listing, size_t len, in
     }
     CK(cudaEventRecord(e1, s->stream));
     CK(cudaStreamSynchronize(s->stream));
+    CK(cudaStreamSynchronize(s->cstream));
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     hr->device_ms = ms;
@@ -1554,7 +1599,7 @@ void ocldec_b200_session_destroy(ocldec_b200_session *s) {
     if (!s)
         return;
     cudaSetDevice(s->device);
-    DevBuf *bufs[] = {&s->text, &s->tiles, &s->tiles_off, &s->nlpos, &s->lines, &s->lins, &s->ops_cnt,
+    DevBuf *bufs[] = {&s->text, &s->text2, &s->tiles, &s->tiles_off, &s->nlpos, &s->lines, &s->lins, &s->ops_cnt,
                       &s->labs_cnt, &s->ops_off, &s->labs_off, &s->ops, &s->labs, &s->kstart,
                       &s->scan_tmp, &s->scan_tot, &s->counters, &s->arena, &s->stage, &s->res,
                       &s->outoff, &s->out, &s->only, &s->retry, &s->gen_len, &s->gen_ninstr,
@@ -1572,6 +1617,10 @@ void ocldec_b200_session_destroy(ocldec_b200_session *s) {
         cudaStreamDestroy(s->stream);
     if (s->stream2)
         cudaStreamDestroy(s->stream2);
+    if (s->cstream)
+        cudaStreamDestroy(s->cstream);
+    for (auto &e : s->cev)
+        cudaEventDestroy(e);
     delete s;
 }
 
@@ -1685,7 +1734,7 @@ int ocldec_b200_decompile(const char *listing, size_t len, const ocldec_b200_opt
     if (int rc0 = set_overrides(s, o.abi_map, o.abi_map ? o.abi_map_len : 0))
         return rc0;
     s->dump_flags = (o.dump_cfg ? DUMP_CFG : 0u) | (o.dump_regions ? DUMP_REGIONS : 0u);
-    int rc = run_host_listing(s, listing, len, o.fold_local_size, o.only_kernel, &hr);
+    int rc = run_host_listing(s, listing, len, o.fold_local_size, o.only_kernel, &hr, nullptr, 0);
     s->dump_flags = 0;
     if (rc)
         return rc;
@@ -1806,17 +1855,14 @@ int ocldec_b200_session_run_host(ocldec_b200_session *s, const char *listing, si
     CK(cudaSetDevice(s->device));
     HostRun hr;
     set_overrides(s, nullptr, 0);
-    int rc = run_host_listing(s, listing, len, fold_local_size, nullptr, &hr);
+    hr.want_names = false;
+    int rc = run_host_listing(s, listing, len, fold_local_size, nullptr, &hr, host_out, host_out ? out_cap : 0);
     if (rc)
         return rc;
     *out_len = hr.out_bytes;
     if (hr.out_bytes > out_cap || !host_out) {
         g_err = "output buffer too small";
         return -2;
-    }
-    if (hr.out_bytes) {
-        CK(cudaMemcpyAsync(host_out, s->out.p, hr.out_bytes, cudaMemcpyDeviceToHost, s->stream));
-        CK(cudaStreamSynchronize(s->stream));
     }
     return 0;
 }

@@ -189,3 +189,36 @@ def test_host_chunking_vs_oracle(monkeypatch):
     monkeypatch.setenv("OCLDEC_B200_CHUNK_BYTES", str(len(listing) // 7))
     res = P.decompile_listing(listing, P.DecompileOptions(arena_bytes=(96 << 20) + 4096))
     assert res.combined == ref
+
+
+@pytest.mark.skipif(not O.available(), reason="oracle not built")
+@pytest.mark.parametrize("pinned", [True, False])
+def test_session_run_host_overlapped_chunks(monkeypatch, pinned):
+    """session_run_host loads chunk c+1 and stores chunk c's output on a copy
+    stream while chunk c runs (two text buffers).  The stored bytes must be
+    the reference's combined output, with pinned or pageable host buffers,
+    and a too-small output buffer must give -2 and the needed length."""
+    import numpy as np
+    import torch
+    listing, _, _ = P.generate_corpus("C4", 500, seed=17, stress=True)
+    ref = O.decompile(listing).combined
+    monkeypatch.setenv("OCLDEC_B200_CHUNK_BYTES", str(len(listing) // 5))
+    cap = 2 * len(listing) + 4096
+    if pinned:
+        hin = torch.frombuffer(bytearray(listing), dtype=torch.uint8).pin_memory()
+        hout = torch.empty(cap, dtype=torch.uint8).pin_memory()
+        pin_ptr, out_ptr = hin.data_ptr(), hout.data_ptr()
+    else:
+        hin = np.frombuffer(listing, dtype=np.uint8).copy()
+        hout = np.zeros(cap, dtype=np.uint8)
+        pin_ptr, out_ptr = hin.ctypes.data, hout.ctypes.data
+    s = P.Session()
+    try:
+        for _ in range(2):  # buffers reused across calls
+            n = s.run_host(pin_ptr, len(listing), out_ptr, cap)
+            got = bytes(hout[:n].numpy()) if pinned else hout[:n].tobytes()
+            assert got == ref
+        with pytest.raises(RuntimeError, match="-2"):
+            s.run_host(pin_ptr, len(listing), out_ptr, len(ref) // 2)
+    finally:
+        s.close()
