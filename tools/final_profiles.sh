@@ -9,4 +9,7 @@ timeout 1200 $NCU --set full --clock-control none --import-source on -k regex:'k
 timeout 900 $NCU --set full --clock-control none --import-source on \
   -k regex:'k_nl_count|k_nl_write|k_classify|k_decode|k_gather|k_ksize' -c 7 \
   -o $O/parse python bench.py --kernels 200000 --steps 1 --warmup 3 --no-e2e --no-cpu > $O/ncu_parse.log 2>&1
+timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file $O/launches.csv python bench.py --kernels 50000 --steps 1 --warmup 3 --no-e2e --no-cpu \
+  > $O/ncu_launch.log 2>&1
 ls -la $O
