@@ -244,6 +244,21 @@ class Session:
         d["prof_cycles"] = list(d["prof_cycles"])
         return d
 
+    def kernels(self):
+        """Per-kernel (offset, length, flags, fallbacks) of the last run as numpy
+        arrays; flags bit0 failed, bit1 structured (ocldec_b200_session_kernels)."""
+        import numpy as np
+        n = int(self.stats()["kernels"])
+        off = np.zeros(n + 1, dtype=np.uint64)
+        ln = np.zeros(n + 1, dtype=np.uint64)
+        fl = np.zeros(n + 1, dtype=np.uint32)
+        fb = np.zeros(n + 1, dtype=np.uint32)
+        rc = self._L.ocldec_b200_session_kernels(self._s, off.ctypes.data, ln.ctypes.data, fl.ctypes.data,
+                                                 fb.ctypes.data)
+        if rc:
+            raise RuntimeError(f"session_kernels failed ({rc}): {_lib.last_error()}")
+        return off[:n], ln[:n], fl[:n], fb[:n]
+
     def output(self):
         p, n = ctypes.c_void_p(), ctypes.c_uint64()
         self._L.ocldec_b200_session_output(self._s, ctypes.byref(p), ctypes.byref(n))
