@@ -245,8 +245,11 @@ OD_INL bool parse_int(const u8 *p, u32 n, i64 *out) {
             d = c - 'A' + 10;
         else
             return false;
-        // overflow check for v * base + d
-        if (v > (~0ull - d) / base)
+        // overflow of v * base + d, i.e. v > (2^64 - 1 - d) / base, without
+        // the 64-bit division: base 16 overflows iff v >= 2^60; base 10 iff
+        // v > 1844674407370955161, or v equals it and d > 5
+        if (base == 16 ? (v >> 60) != 0
+                       : (v > 1844674407370955161ull || (v == 1844674407370955161ull && d > 5)))
             return false;
         v = v * base + d;
     }

@@ -248,9 +248,21 @@ OD_NOINL Mnem decompose(const u8 *t, Span m, const RootTable *rt) {
     r.sfx[0] = r.sfx[1] = 0;
     const u8 *p = t + m.off;
     u32 n = m.len;
-    u32 us = 0;
-    while (us < n && p[us] != '_')
-        ++us;
+    // one pass over the word: the first '_' (prefix end), the number of '_'
+    // after it, and the last two of those (suffix token boundaries)
+    u32 us = n, nus = 0;
+    i32 u1 = -1, u2 = -1;
+    for (u32 i = 0; i < n; ++i) {
+        if (p[i] != '_')
+            continue;
+        if (us == n) {
+            us = i;
+        } else {
+            ++nus;
+            u2 = u1;
+            u1 = (i32)i;
+        }
+    }
     if (us == n)
         return r;
     u8 px = PX_OTHER;
@@ -266,31 +278,29 @@ OD_NOINL Mnem decompose(const u8 *t, Span m, const RootTable *rt) {
         return r;
     r.prefix = px;
     const u8 *rest = p + us + 1;
-    u32 rn = n - us - 1;
-    // token boundaries of rest split on '_'; an empty rest has no tokens.
-    // Peel at most two suffix tokens off the tail keeping >= 1 token.
-    u32 ntok = 0;
-    if (rn > 0) {
-        ntok = 1;
-        for (u32 i = 0; i < rn; ++i)
-            if (rest[i] == '_')
-                ++ntok;
-    }
-    u32 root_len = rn; // bytes of the root (tokens[0, root_end) joined)
-    u32 root_end = ntok;
-    u32 peeled[2];
+    const u32 rn = n - us - 1;
+    // tokens of rest split on '_' (an empty rest has none); peel at most two
+    // suffix tokens off the tail keeping >= 1 token
+    const u32 ntok = rn > 0 ? nus + 1 : 0;
+    const i32 off = (i32)us + 1; // rest-relative '_' positions: u - off
+    u32 root_len = rn;
     u32 npeel = 0;
-    while (root_end > 1 && npeel < 2) {
-        // last token of rest[0, root_len)
-        u32 s = root_len;
-        while (s > 0 && rest[s - 1] != '_')
-            --s;
-        u32 sf = parse_sfx(rest + s, root_len - s);
-        if (!sf)
-            break;
-        peeled[npeel++] = sf;
-        --root_end;
-        root_len = s - 1; // drop "_tok"
+    u32 peeled[2];
+    if (ntok > 1) {
+        const u32 s1 = (u32)(u1 - off) + 1;
+        const u32 sf = parse_sfx(rest + s1, root_len - s1);
+        if (sf) {
+            peeled[npeel++] = sf;
+            root_len = s1 - 1;
+            if (ntok > 2) {
+                const u32 s2 = (u32)(u2 - off) + 1;
+                const u32 sf2 = parse_sfx(rest + s2, root_len - s2);
+                if (sf2) {
+                    peeled[npeel++] = sf2;
+                    root_len = s2 - 1;
+                }
+            }
+        }
     }
     if (npeel == 1)
         r.sfx[0] = (u16)peeled[0];
@@ -301,16 +311,28 @@ OD_NOINL Mnem decompose(const u8 *t, Span m, const RootTable *rt) {
     if (ntok == 0)
         root_len = 0;
     // root flags (rfind(x, 0) == 0 tests)
-    if (starts_with(rest, root_len, "cbranch_"))
-        r.rflags |= RF_CBRANCH;
-    if (starts_with(rest, root_len, "cmp_"))
-        r.rflags |= RF_CMP;
-    if (starts_with(rest, root_len, "store"))
-        r.rflags |= RF_STORE;
-    if (starts_with(rest, root_len, "lshr"))
-        r.rflags |= RF_LSHR;
-    if (starts_with(rest, root_len, "ashr"))
-        r.rflags |= RF_ASHR;
+    // (the five prefixes differ in their first byte or, for c, the second)
+    switch (root_len ? rest[0] : 0) {
+    case 'c':
+        if (starts_with(rest, root_len, "cbranch_"))
+            r.rflags |= RF_CBRANCH;
+        else if (starts_with(rest, root_len, "cmp_"))
+            r.rflags |= RF_CMP;
+        break;
+    case 's':
+        if (starts_with(rest, root_len, "store"))
+            r.rflags |= RF_STORE;
+        break;
+    case 'l':
+        if (starts_with(rest, root_len, "lshr"))
+            r.rflags |= RF_LSHR;
+        break;
+    case 'a':
+        if (starts_with(rest, root_len, "ashr"))
+            r.rflags |= RF_ASHR;
+        break;
+    default: break;
+    }
     // perfect-hash lookup + verification
     u32 slot = root_hash_slot(rest, root_len);
     u16 id = rt->slot[slot];
