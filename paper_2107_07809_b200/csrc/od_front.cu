@@ -4,10 +4,26 @@
 
 namespace od {
 
+__device__ __noinline__ void front_one(const DecompArgs &a, const Slot0 &sl, u64 **names, u32 *names_cap);
+
 __global__ void __launch_bounds__(128, OD_MINB_FRONT) k_front(DecompArgs a) {
     Slot0 sl;
-    if (!dk_slot(a, &sl))
-        return;
+    u64 *names = nullptr; // this lane's name set, zeroed below by the whole warp
+    u32 names_cap = 0;
+    if (dk_slot(a, &sl))
+        front_one(a, sl, &names, &names_cap);
+    // NameSet::keys must start zeroed: 32 lanes store 16 bytes each per
+    // iteration instead of the kernel's lone lane walking the table
+    const u32 lane = threadIdx.x & 31;
+    for (u32 src = 0; src < 32; ++src) {
+        uint4 *p = reinterpret_cast<uint4 *>(__shfl_sync(0xffffffffu, (unsigned long long)names, src));
+        const u32 n4 = __shfl_sync(0xffffffffu, names_cap, src) / 2;
+        for (u32 q = lane; q < n4; q += 32)
+            p[q] = uint4{0, 0, 0, 0};
+    }
+}
+
+__device__ __noinline__ void front_one(const DecompArgs &a, const Slot0 &sl, u64 **names, u32 *names_cap) {
     const u32 k = sl.k;
     const u32 i = sl.i;
     KState *g = reinterpret_cast<KState *>(sl.base);
@@ -42,6 +58,7 @@ __global__ void __launch_bounds__(128, OD_MINB_FRONT) k_front(DecompArgs a) {
     in.ovr_text = a.ovr_text;
     in.dump = a.dump;
     in.kidx = k;
+    in.names_zeroed_by_caller = 1;
     g->mem.base = sl.base + kb;
     g->mem.top = 0;
     g->mem.cap = a.boff[i + 1] - a.boff[i] - kb;
@@ -73,6 +90,10 @@ __global__ void __launch_bounds__(128, OD_MINB_FRONT) k_front(DecompArgs a) {
         kstate_fix(*g);
         dk_front(*g);
 #endif
+        if (!g->done && g->K.pool.keys) {
+            *names = g->K.pool.keys;
+            *names_cap = g->K.pool.cap;
+        }
     }
 }
 

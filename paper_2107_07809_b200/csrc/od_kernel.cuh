@@ -84,6 +84,7 @@ struct KIn {
     u32 novr;
     const u8 *ovr_text;
     const DumpCfg *dump;  // DOT dumps (null: none)
+    u32 names_zeroed_by_caller; // k_front's warp zeroes the name set after dk_front
     u32 kidx;             // chunk result index (dump records)
     u64 *prof;            // optional per-phase cycle counters
 };
@@ -265,6 +266,23 @@ struct NameSet {
         keys[i] = k;
         ++count;
         return true;
+    }
+    // hoist_fresh_decls' dedupe over names already in the set: true the
+    // first time (cls, num) is marked (bit 63 of its key).
+    OD_INL bool mark(u32 cls, u32 num) {
+        const u64 k = ((u64)(cls + 1) << 32) | num;
+        u64 h = k * 0x9E3779B97F4A7C15ull;
+        u32 i = (u32)(h >> 32) & (cap - 1);
+        while (keys[i]) {
+            if ((keys[i] & ~(1ull << 63)) == k) {
+                if (keys[i] >> 63)
+                    return false;
+                keys[i] |= 1ull << 63;
+                return true;
+            }
+            i = (i + 1) & (cap - 1);
+        }
+        return true; // not recorded (cannot happen: bind_fresh inserts every fresh name)
     }
 };
 

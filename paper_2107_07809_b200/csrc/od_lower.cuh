@@ -1666,7 +1666,8 @@ OD_NOINL void dk_front(KState &S) {
     w.overflow = false;
     OD_CHECK(K.E.n && K.st && K.lists && K.frames && K.log && K.dstk && K.dstk_id && K.fresh &&
              K.pool.keys && K.fs.st.p && K.fs.terms.p && K.eqst.p && K.rc.ts.p && S.estk && w.p);
-    name_set_clear(K.pool);
+    if (!in.names_zeroed_by_caller) // (k_front: the whole warp zeroes it, coalesced)
+        name_set_clear(K.pool);
     memset(&K.E.n[0], 0, sizeof(ENode));
     K.E.top = 1; // node 0 = null
     K.E.oom = false;
@@ -1700,12 +1701,10 @@ OD_NOINL void dk_lower(KState &S) {
     out.fallbacks = K.fallbacks;
 
     // hoist_fresh_decls: first occurrence per name, in record order.
-    name_set_clear(K.pool);
-    K.pool.count = 0;
     S.hoist = new_list(K);
     for (u32 i = 0; i < K.nfresh; ++i) {
         const Fresh &f = K.fresh[i];
-        if (!K.pool.insert(f.cls, f.num))
+        if (!K.pool.mark(f.cls, f.num))
             continue;
         u32 d = new_stmt(K, SK_DECL);
         K.st[d].cls = (u16)f.cls;

@@ -145,6 +145,7 @@ int main(int argc, char **argv) {
         kin.ovr_text = nullptr;
         kin.dump = dcfg.flags ? &dcfg : nullptr;
         kin.kidx = (u32)k;
+        kin.names_zeroed_by_caller = 0;
         KOut ko;
         const u8 *src = nullptr;
         std::vector<u8> arena;
