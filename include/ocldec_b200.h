@@ -40,6 +40,9 @@ typedef struct ocldec_b200_options {
     int dump_cfg;            /* DecompileOptions::dump_cfg: DecompiledKernel::cfg_dot (to_dot, cfg.cpp:400-424) */
     int dump_regions;        /* DecompileOptions::dump_regions: ReduceResult::dumps
                                 (region_graph_dot, structurizer.cpp:669-688, one per reduction step) */
+    int record_reduction;    /* DecompiledKernel::reduction's merges and root / residue as a
+                                step -2 dump (text: "merge <kind> <result> <absorbed...>" lines,
+                                then "root <id>" or "residue <ids...>"; structurizer.hpp:54-104) */
 } ocldec_b200_options;
 
 /* DecompiledKernel (decompiler.hpp:39-52): the printed source and flags. */
@@ -61,8 +64,9 @@ typedef struct ocldec_b200_diag {
     uint64_t msg_off, msg_len;
 } ocldec_b200_diag;
 
-/* One DOT dump of a kernel: step -1 is cfg_dot, step i >= 0 is
- * reduction.dumps[i] ("step<i>"); text at dump_text[off, off + len). */
+/* One dump of a kernel: step -1 is cfg_dot, step -2 the reduction record,
+ * step i >= 0 is reduction.dumps[i] ("step<i>"); text at
+ * dump_text[off, off + len). */
 typedef struct ocldec_b200_dump {
     uint64_t kernel;              /* index into ocldec_b200_result.kernels */
     int32_t step;

@@ -36,7 +36,23 @@ struct DecompileOptions {
     std::string abi_map;          // ABI override file text; empty = none
     bool dump_cfg = false;        // DecompileOptions::dump_cfg (decompiler.hpp:33)
     bool dump_regions = false;    // DecompileOptions::dump_regions (decompiler.hpp:34)
+    bool record_reduction = false; // fill DecompiledKernel::reduction (merges, root / residue)
     int device = 0;
+};
+
+// MergeRecord (structurizer.hpp:54-58); kind: 1 Linear, 2 IfThen, 3 IfElse.
+struct MergeRecord {
+    int kind = 1;
+    std::vector<int> absorbed;
+    int result = 0;
+};
+
+// ReduceResult's inspection part (structurizer.hpp:98-104), region ids.
+struct Reduction {
+    std::vector<MergeRecord> merges;
+    bool reduced = false;
+    int root = 0;             // when reduced
+    std::vector<int> residue; // top-level regions when not
 };
 
 struct DecompiledKernel {
@@ -48,7 +64,42 @@ struct DecompiledKernel {
     unsigned instructions = 0;
     std::string cfg_dot;                   // DecompiledKernel::cfg_dot when dump_cfg
     std::vector<std::string> region_dumps; // ReduceResult::dumps when dump_regions
+    Reduction reduction;                   // when record_reduction
 };
+
+inline Reduction parse_reduction(const std::string &text) {
+    Reduction r;
+    size_t p = 0;
+    while (p < text.size()) {
+        size_t e = text.find('\n', p);
+        if (e == std::string::npos)
+            e = text.size();
+        std::vector<int> v;
+        std::string word;
+        const char *c = text.c_str() + p, *end = text.c_str() + e;
+        while (c < end && *c != ' ')
+            word += *c++;
+        while (c < end) {
+            char *q = nullptr;
+            v.push_back(static_cast<int>(std::strtol(c, &q, 10)));
+            c = q;
+        }
+        if (word == "merge" && v.size() >= 2) {
+            MergeRecord m;
+            m.kind = v[0];
+            m.result = v[1];
+            m.absorbed.assign(v.begin() + 2, v.end());
+            r.merges.push_back(std::move(m));
+        } else if (word == "root" && !v.empty()) {
+            r.reduced = true;
+            r.root = v[0];
+        } else if (word == "residue") {
+            r.residue = v;
+        }
+        p = e + 1;
+    }
+    return r;
+}
 
 // Diagnostic (diagnostics.hpp:20-27); render() matches diagnostics.cpp:22-26.
 struct Diagnostic {
@@ -128,6 +179,7 @@ inline DecompileResult decompile_listing(const std::string &listing, const Decom
     o.abi_map_len = opts.abi_map.size();
     o.dump_cfg = opts.dump_cfg ? 1 : 0;
     o.dump_regions = opts.dump_regions ? 1 : 0;
+    o.record_reduction = opts.record_reduction ? 1 : 0;
     ocldec_b200_result *r = nullptr;
     int rc = ocldec_b200_decompile(listing.data(), listing.size(), &o, &r);
     if (rc != 0)
@@ -150,8 +202,10 @@ inline DecompileResult decompile_listing(const std::string &listing, const Decom
         const ocldec_b200_dump &d = r->dumps[i];
         DecompiledKernel &k = res.kernels[d.kernel];
         std::string text(r->dump_text + d.off, d.len);
-        if (d.step < 0)
+        if (d.step == -1)
             k.cfg_dot = std::move(text);
+        else if (d.step == -2)
+            k.reduction = parse_reduction(text);
         else
             k.region_dumps.push_back(std::move(text));
     }

@@ -68,6 +68,7 @@ class RefKernel:
     fallback_count: int
     cfg_dot: bytes = b""                                   # DecompiledKernel::cfg_dot (dump_cfg)
     region_dumps: List[bytes] = field(default_factory=list)  # ReduceResult::dumps (dump_regions)
+    reduction: bytes = b""  # merges + root/residue as text (ref_driver.cpp serialization)
 
 
 @dataclass
@@ -91,7 +92,7 @@ def _take(ptr: int, n: int) -> bytes:
 
 def decompile(listing: bytes, fold_local_size: bool = False, only_kernel: Optional[bytes] = None,
               abi_map: Optional[bytes] = None, dump_cfg: bool = False,
-              dump_regions: bool = False) -> RefResult:
+              dump_regions: bool = False, reduction: bool = False) -> RefResult:
     if isinstance(listing, str):
         listing = listing.encode()
     L = lib()
@@ -99,7 +100,7 @@ def decompile(listing: bytes, fold_local_size: bool = False, only_kernel: Option
     n = ctypes.c_size_t()
     if isinstance(abi_map, str):
         abi_map = abi_map.encode()
-    dumps = int(dump_cfg) | (2 if dump_regions else 0)
+    dumps = int(dump_cfg) | (2 if dump_regions else 0) | (4 if reduction else 0)
     if dumps:
         L.ref_decompile_ex(listing, len(listing), int(fold_local_size), only_kernel, abi_map,
                            len(abi_map) if abi_map is not None else 0, dumps, ctypes.byref(out), ctypes.byref(n))
@@ -140,6 +141,10 @@ def decompile(listing: bytes, fold_local_size: bool = False, only_kernel: Option
             assert step == len(res.kernels[ki].region_dumps)
             res.kernels[ki].region_dumps.append(blob[pos:pos + rlen])
             pos += rlen
+        elif head[0] == b"M":
+            ki, mlen = int(head[1]), int(head[2])
+            res.kernels[ki].reduction = blob[pos:pos + mlen]
+            pos += mlen
         elif head[0] == b"C":
             clen = int(head[1])
             res.combined = blob[pos:pos + clen]

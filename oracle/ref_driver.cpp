@@ -63,7 +63,8 @@ struct DecompileJob {
     const char *abi_map; // override file text (parse_abi_overrides, abi_model.cpp:109-153) or null
     size_t abi_len;
     std::string serialized;
-    int dumps = 0; // 1: dump_cfg, 2: dump_regions (DecompileOptions, decompiler.hpp:33-34)
+    int dumps = 0; // 1: dump_cfg, 2: dump_regions (DecompileOptions, decompiler.hpp:33-34),
+                   // 4: the reduction record (merges, root / residue)
 };
 
 // Serialization (parsed by oracle/oracle.py):
@@ -71,6 +72,8 @@ struct DecompileJob {
 //   "D <severity> <line> <msg_len>\n" message
 //   "C <len>\n" combined_source
 //   "G <kernel> <len>\n" cfg_dot, "R <kernel> <step> <len>\n" reduction.dumps[step]
+//   "M <kernel> <len>\n" reduction: "merge <kind> <result> <absorbed...>" lines,
+//   then "root <id>" or "residue <ids...>"
 void *decompile_job(void *p) {
     auto *job = static_cast<DecompileJob *>(p);
     ocldec::DecompileOptions opts;
@@ -108,6 +111,25 @@ void *decompile_job(void *p) {
         if (!k.cfg_dot.empty()) {
             out += "G " + std::to_string(i) + " " + std::to_string(k.cfg_dot.size()) + "\n";
             out += k.cfg_dot;
+        }
+        if ((job->dumps & 4) && !k.failed) {
+            std::string m;
+            for (const auto &mr : k.reduction.merges) {
+                m += "merge " + std::to_string(int(mr.kind)) + " " + std::to_string(mr.result);
+                for (int a : mr.absorbed)
+                    m += " " + std::to_string(a);
+                m += "\n";
+            }
+            if (k.reduction.reduced) {
+                m += "root " + std::to_string(k.reduction.root->id) + "\n";
+            } else {
+                m += "residue";
+                for (const auto *r : k.reduction.residue)
+                    m += " " + std::to_string(r->id);
+                m += "\n";
+            }
+            out += "M " + std::to_string(i) + " " + std::to_string(m.size()) + "\n";
+            out += m;
         }
         for (size_t j = 0; j < k.reduction.dumps.size(); ++j) {
             out += "R " + std::to_string(i) + " " + std::to_string(j) + " " +

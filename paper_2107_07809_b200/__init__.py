@@ -17,7 +17,7 @@ from typing import List, Optional, Sequence, Union
 
 from . import _lib
 
-__all__ = ["DecompileOptions", "DecompiledKernel", "Diagnostic", "DecompileResult",
+__all__ = ["DecompileOptions", "DecompiledKernel", "Reduction", "Diagnostic", "DecompileResult",
            "decompile_listing", "check_abi_map", "generate_corpus", "Session", "SHAPES"]
 
 # Synthetic corpus shapes (BASELINE.json configs).
@@ -34,6 +34,7 @@ class DecompileOptions:
     abi_map: Optional[Union[str, bytes]] = None
     dump_cfg: bool = False                  # DecompiledKernel.cfg_dot (to_dot, cfg.cpp:400-424)
     dump_regions: bool = False              # region_dumps (region_graph_dot, structurizer.cpp:669-688)
+    record_reduction: bool = False          # DecompiledKernel.reduction (merges, root / residue)
     device: int = 0
     arena_bytes: int = 0                    # per-thread arena, 0 = default
 
@@ -51,6 +52,31 @@ class Diagnostic:
 
 
 @dataclass
+class Reduction:
+    """ReduceResult's inspection part (structurizer.hpp:54-58, 98-104):
+    merges as (kind, result, absorbed) with kind 1 Linear, 2 IfThen,
+    3 IfElse; root when reduced, else the residue (region ids)."""
+    merges: List[tuple] = field(default_factory=list)
+    reduced: bool = False
+    root: int = 0
+    residue: List[int] = field(default_factory=list)
+    text: str = ""
+
+    @staticmethod
+    def parse(text: str) -> "Reduction":
+        r = Reduction(text=text)
+        for line in text.splitlines():
+            w = line.split()
+            if w and w[0] == "merge":
+                r.merges.append((int(w[1]), int(w[2]), [int(x) for x in w[3:]]))
+            elif w and w[0] == "root":
+                r.reduced, r.root = True, int(w[1])
+            elif w and w[0] == "residue":
+                r.residue = [int(x) for x in w[1:]]
+        return r
+
+
+@dataclass
 class DecompiledKernel:
     """DecompiledKernel (decompiler.hpp:39-52): printed source and flags."""
     name: str
@@ -61,6 +87,7 @@ class DecompiledKernel:
     instructions: int
     cfg_dot: str = ""                                        # when dump_cfg
     region_dumps: List[str] = field(default_factory=list)   # reduction.dumps when dump_regions
+    reduction: Optional["Reduction"] = None                 # when record_reduction
 
 
 @dataclass
@@ -99,7 +126,7 @@ def decompile_listing(listing: Union[str, bytes], opts: Optional[DecompileOption
     o = _lib.Options(int(opts.fold_local_size),
                      opts.only_kernel.encode() if opts.only_kernel is not None else None,
                      opts.device, opts.arena_bytes, amap, len(amap) if amap is not None else 0,
-                     int(opts.dump_cfg), int(opts.dump_regions))
+                     int(opts.dump_cfg), int(opts.dump_regions), int(opts.record_reduction))
     out = ctypes.POINTER(_lib.Result)()
     rc = L.ocldec_b200_decompile(listing, len(listing), ctypes.byref(o), ctypes.byref(out))
     if rc != 0:
@@ -124,8 +151,10 @@ def decompile_listing(listing: Union[str, bytes], opts: Optional[DecompileOption
             for d in dl:
                 txt = dtext[d.off:d.off + d.len].decode("utf-8", errors="surrogateescape")
                 k = res.kernels[d.kernel]
-                if d.step < 0:
+                if d.step == -1:
                     k.cfg_dot = txt
+                elif d.step == -2:
+                    k.reduction = Reduction.parse(txt)
                 else:
                     k.region_dumps.append(txt)
         alld = [r.diags[i] for i in range(r.ndiags)] + [r.abi_diags[i] for i in range(r.nabi_diags)]

@@ -18,7 +18,8 @@ class Options(ctypes.Structure):
     _fields_ = [("fold_local_size", ctypes.c_int), ("only_kernel", ctypes.c_char_p),
                 ("device", ctypes.c_int), ("arena_bytes", ctypes.c_size_t),
                 ("abi_map", ctypes.c_char_p), ("abi_map_len", ctypes.c_size_t),
-                ("dump_cfg", ctypes.c_int), ("dump_regions", ctypes.c_int)]
+                ("dump_cfg", ctypes.c_int), ("dump_regions", ctypes.c_int),
+                ("record_reduction", ctypes.c_int)]
 
 
 class Kernel(ctypes.Structure):

@@ -1733,7 +1733,8 @@ int ocldec_b200_decompile(const char *listing, size_t len, const ocldec_b200_opt
     HostRun hr;
     if (int rc0 = set_overrides(s, o.abi_map, o.abi_map ? o.abi_map_len : 0))
         return rc0;
-    s->dump_flags = (o.dump_cfg ? DUMP_CFG : 0u) | (o.dump_regions ? DUMP_REGIONS : 0u);
+    s->dump_flags = (o.dump_cfg ? DUMP_CFG : 0u) | (o.dump_regions ? DUMP_REGIONS : 0u) |
+                    (o.record_reduction ? DUMP_MERGES : 0u);
     int rc = run_host_listing(s, listing, len, o.fold_local_size, o.only_kernel, &hr, nullptr, 0);
     s->dump_flags = 0;
     if (rc)

@@ -52,10 +52,10 @@ struct AbiOvr {
 
 // DOT dumps (DecompileOptions::dump_cfg / dump_regions, decompiler.hpp:33-34):
 // text appended to a run-wide pool, one record per dump.
-enum DumpFlags : u32 { DUMP_CFG = 1, DUMP_REGIONS = 2 };
+enum DumpFlags : u32 { DUMP_CFG = 1, DUMP_REGIONS = 2, DUMP_MERGES = 4 };
 struct DumpRec {
     u32 k;      // kernel (chunk result index)
-    i32 step;   // -1: cfg_dot, else ReduceResult::dumps[step]
+    i32 step;   // -1: cfg_dot, -2: ReduceResult merges/root/residue text, else dumps[step]
     u64 off, len;
 };
 struct DumpCfg {
@@ -2126,14 +2126,55 @@ OD_NOINL void region_dot(const KCtx &K, DotSink &o, u32 step) {
     o.s("}\n");
 }
 
-// Appends one dump (step < 0: the CFG) to the run's pool.
+// ReduceResult as text (the inspection record of reduce, structurizer.cpp:
+// 354-403): one "merge <kind> <result> <absorbed...>" line per MergeRecord in
+// order (merged regions are created in merge order, after the leaves), then
+// "root <id>" or "residue <ids...>" (live regions in id order).
+OD_NOINL void reduce_text(const KCtx &K, DotSink &o) {
+    const u32 gen = ++const_cast<KCtx &>(K).rstamp_gen;
+    for (u32 r = 1; r <= K.nrg; ++r) {
+        const Region &R = K.rg[r];
+        if (R.kind == RK_BLOCK)
+            continue;
+        o.s("merge ");
+        o.u(R.kind);
+        o.c(' ');
+        o.u(r);
+        for (u32 c = 0; c < R.ch_n; ++c) {
+            o.c(' ');
+            o.u(K.child[R.ch_b + c]);
+            K.rstamp[K.child[R.ch_b + c]] = gen;
+        }
+        o.c('\n');
+    }
+    if (K.reduced) {
+        o.s("root ");
+        o.u(K.root_r);
+    } else {
+        o.s("residue");
+        for (u32 r = 1; r <= K.nrg; ++r)
+            if (K.rstamp[r] != gen) {
+                o.c(' ');
+                o.u(r);
+            }
+    }
+    o.c('\n');
+}
+
+OD_INL void dump_print(KCtx &K, DotSink &o, i32 step) {
+    if (step == -1)
+        cfg_dot(K, o);
+    else if (step == -2)
+        reduce_text(K, o);
+    else
+        region_dot(K, o, (u32)step);
+}
+
+// Appends one dump (step -1: the CFG, -2: the reduction record) to the run's pool.
 OD_NOINL void dump_emit(KCtx &K, i32 step) {
     const DumpCfg &D = *K.in->dump;
     DotSink c{nullptr, 0};
-    if (step < 0)
-        cfg_dot(K, c);
-    else
-        region_dot(K, c, (u32)step);
+    dump_print(K, c, step);
     const u64 off = fetch_add_u64(&D.top[0], c.n);
     const u64 ri = fetch_add_u64(&D.top[1], 1);
     if (off + c.n > D.cap || ri >= D.rcap) {
@@ -2141,10 +2182,7 @@ OD_NOINL void dump_emit(KCtx &K, i32 step) {
         return;
     }
     DotSink w{D.text + off, 0};
-    if (step < 0)
-        cfg_dot(K, w);
-    else
-        region_dot(K, w, (u32)step);
+    dump_print(K, w, step);
     DumpRec &R = D.rec[ri];
     R.k = K.in->kidx;
     R.step = step;

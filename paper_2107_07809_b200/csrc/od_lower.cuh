@@ -1606,6 +1606,8 @@ OD_NOINL void dk_front(KState &S) {
         S.done = 1;
         return;
     }
+    if (in.dump && (in.dump->flags & DUMP_MERGES))
+        dump_emit(K, -2);
     if (K.dump_full) { // grow the dump pool and run the kernel again
         out.status = KS_STAGE_FULL;
         S.done = 1;

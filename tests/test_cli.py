@@ -38,6 +38,22 @@ def test_cli_missing_input(tmp_path):
     assert "cannot open" in p.stderr
 
 
+def test_cpp_shim_parses_reduction(tmp_path):
+    src = tmp_path / "red.cpp"
+    src.write_text('#include "ocldec_b200.hpp"\n'
+                   'int main() {\n'
+                   '  auto r = ocldec_b200::parse_reduction("merge 3 5 1 2 3\\nmerge 1 6 5 4\\nroot 6\\n");\n'
+                   '  auto g = ocldec_b200::parse_reduction("merge 2 4 1 2\\nresidue 3 4\\n");\n'
+                   '  bool ok = r.merges.size() == 2 && r.merges[0].kind == 3 && r.merges[0].result == 5 &&\n'
+                   '            r.merges[0].absorbed == std::vector<int>{1, 2, 3} && r.reduced && r.root == 6 &&\n'
+                   '            !g.reduced && g.residue == std::vector<int>{3, 4} && g.merges[0].absorbed.size() == 2;\n'
+                   '  return ok ? 0 : 1; }\n')
+    exe = tmp_path / "red"
+    subprocess.run(["g++", "-std=c++17", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)],
+                   check=True)
+    assert subprocess.run([str(exe)]).returncode == 0
+
+
 def test_cpp_shim_compiles(tmp_path):
     src = tmp_path / "shim.cpp"
     src.write_text('#include "ocldec_b200.hpp"\n'

@@ -1,4 +1,5 @@
-"""Inspection outputs: the DOT dumps.
+"""Inspection outputs: the DOT dumps and the
+reduction record (ReduceResult's merges, root / residue).
 
 DecompileOptions::dump_cfg gives DecompiledKernel::cfg_dot — to_dot
 (cfg.cpp:400-424) of the flow graph after mask normalization
@@ -63,6 +64,28 @@ def test_dumps_generated(shape, stress, count):
     # one option at a time, and with a kernel filter
     _check(listing, cfg=True, regions=False)
     _check(listing, cfg=False, regions=True, only_kernel=res.kernels[len(res.kernels) // 2].name)
+
+
+@pytest.mark.parametrize("shape,stress,count", [("C1", 1, 50), ("C3", 1, 600), ("C4", 1, 40)])
+def test_reduction_record(shape, stress, count):
+    """ReduceResult::merges (kind, absorbed, result) in order and the root or
+    residue region ids (structurizer.cpp:354-403), kernel by kernel."""
+    listing, _, _ = P.generate_corpus(shape, count, seed=88 + count, stress=bool(stress))
+    res = P.decompile_listing(listing, P.DecompileOptions(record_reduction=True))
+    ref = O.decompile(listing, reduction=True)
+    assert res.combined == ref.combined
+    for a, b in zip(res.kernels, ref.kernels):
+        if b.failed:
+            assert a.reduction is None
+            continue
+        assert _enc(a.reduction.text) == b.reduction, a.name
+        assert a.reduction.reduced == b.structured
+    assert any(k.reduction and not k.reduction.reduced for k in res.kernels) or shape == "C1"
+    for rec in (json.loads(x) for x in open(os.path.join(GOLDEN, "corpus.jsonl"))):
+        r = P.decompile_listing(_enc(rec["listing"]), P.DecompileOptions(record_reduction=True))
+        f = O.decompile(_enc(rec["listing"]), reduction=True)
+        assert [_enc(k.reduction.text) if k.reduction else b"" for k in r.kernels] == \
+               [k.reduction for k in f.kernels]
 
 
 def test_dump_pool_growth():

@@ -13,9 +13,9 @@ import paper_2107_07809_b200 as P  # noqa: E402
 
 def dev_dumps(listing):
     p = subprocess.run(["build/devhost"], input=listing, capture_output=True, timeout=600,
-                       env=dict(os.environ, OD_DUMP="3"))
+                       env=dict(os.environ, OD_DUMP="7"))
     out = p.stdout
-    g, r = {}, {}
+    g, r, m = {}, {}, {}
     pos = 0
     while pos < len(out):
         nl = out.index(b"\n", pos)
@@ -27,24 +27,32 @@ def dev_dumps(listing):
             n = int(head[2])
             g[int(head[1])] = out[pos:pos + n]
             pos += n
+        elif head[0] == b"M":
+            n = int(head[2])
+            m[int(head[1])] = out[pos:pos + n]
+            pos += n
         elif head[0] == b"R":
             n = int(head[3])
             r.setdefault(int(head[1]), []).append((int(head[2]), out[pos:pos + n]))
             pos += n
         elif head[0] == b"C":
             break
-    return g, r
+    return g, r, m
 
 
 def check(name, listing):
-    ref = O.decompile(listing, dump_cfg=True, dump_regions=True)
-    g, r = dev_dumps(listing)
+    ref = O.decompile(listing, dump_cfg=True, dump_regions=True, reduction=True)
+    g, r, mm = dev_dumps(listing)
     bad = 0
     for i, k in enumerate(ref.kernels):
         if g.get(i, b"") != k.cfg_dot:
             bad += 1
             if bad < 3:
                 print(f"CFG DIFF {name} k{i}\n--- ref\n{k.cfg_dot.decode()}\n--- got\n{g.get(i, b'').decode()}")
+        if mm.get(i, b"") != k.reduction:
+            bad += 1
+            if bad < 3:
+                print(f"REDUCTION DIFF {name} k{i}\n--- ref\n{k.reduction.decode()}--- got\n{mm.get(i, b'').decode()}")
         steps = [t for _, t in sorted(r.get(i, []))]
         if steps != k.region_dumps:
             bad += 1

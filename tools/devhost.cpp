@@ -207,7 +207,9 @@ int main(int argc, char **argv) {
         for (u64 i = 0; i < dtop[1]; ++i)
             dm[{drec[i].k, drec[i].step}] = std::string((const char *)dtext.data() + drec[i].off, drec[i].len);
         for (auto &e : dm) {
-            if (e.first.second < 0)
+            if (e.first.second == -2)
+                per += "M " + std::to_string(e.first.first) + " " + std::to_string(e.second.size()) + "\n";
+            else if (e.first.second < 0)
                 per += "G " + std::to_string(e.first.first) + " " + std::to_string(e.second.size()) + "\n";
             else
                 per += "R " + std::to_string(e.first.first) + " " + std::to_string(e.first.second) + " " +
