@@ -284,13 +284,49 @@ __global__ void __launch_bounds__(256) k_decode(const u8 *__restrict__ t, u64 le
 
 // Per-kernel sizes (a pass over the kernel's decoded lines), size key and
 // arena budget.
+// One warp per kernel: kernel_size's sums (od_kernel.cuh) over a lane-strided
+// walk of the kernel's lines (coalesced record reads), reduced across the warp.
 __global__ void k_ksize(const u32 *kstart, u32 nk, u32 nlines, const LineRec *lines, const LineIns *lins,
                         const Opnd *ops, KSize *sizes, u32 *key, u64 *budget, u32 group, u32 novr) {
-    u32 k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= nk)
+    const u32 k = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    const u32 lane = threadIdx.x & 31;
+    if (k >= nk) // whole warps: nk is warp-uniform
         return;
     const u32 b = kstart[k], e = k + 1 < nk ? kstart[k + 1] : nlines;
-    KSize z = kernel_size(lines, lins, ops, b, e);
+    u32 ncfg = 0, nins = 0, nlab = 0, labelled = 0, enders = 0, xops = 0;
+    for (u32 l = b + 1 + lane; l < e; l += 32) {
+        const u8 role = lines[l].role;
+        if (role == LR_CONFIG) {
+            ++ncfg;
+            continue;
+        }
+        if (role != LR_TEXT)
+            continue;
+        const LineIns &L = lins[l];
+        nlab += L.nlabels;
+        labelled += L.nlabels ? 1 : 0;
+        if (!(L.flags & IF_HAS_INS))
+            continue;
+        ++nins;
+        if (L.prefix == PX_S && (L.root == R_BRANCH || L.root == R_ENDPGM || (L.rflags & RF_CBRANCH)))
+            ++enders;
+        u32 m;
+        if (L.prefix == PX_S && exec_kind_of(L.root, L.prefix, L.flags, L.nops, ops + L.op_start, &m) != XK_NONE)
+            ++xops;
+    }
+    const u32 full = 0xffffffffu;
+    ncfg = __reduce_add_sync(full, ncfg);
+    nins = __reduce_add_sync(full, nins);
+    nlab = __reduce_add_sync(full, nlab);
+    const u32 nbx = __reduce_add_sync(full, labelled + enders + xops);
+    if (lane)
+        return;
+    KSize z;
+    z.n = e - b;
+    z.ncfg = ncfg;
+    z.nins = nins;
+    z.nlab = nlab;
+    z.nb = 3 + nbx;
     z.novr = novr;
     sizes[k] = z;
     // sort key: lines, optionally grouped by class (straight-line kernels
@@ -987,7 +1023,7 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     if (ensure(s->ksizes, (u64)nk * sizeof(KSize) + 16))
         return -3;
     a.sizes = P<KSize>(s->ksizes);
-    k_ksize<<<kg, kb, 0, st>>>(P<u32>(s->kstart), nk, nlines, P<LineRec>(s->lines), P<LineIns>(s->lins),
+    k_ksize<<<(u32)(((u64)nk * 32 + kb - 1) / kb), kb, 0, st>>>(P<u32>(s->kstart), nk, nlines, P<LineRec>(s->lines), P<LineIns>(s->lins),
                                P<Opnd>(s->ops), P<KSize>(s->ksizes), key, P<u64>(s->budget), s->group_class,
                                s->novr);
     CK(cudaMemsetAsync(s->hist.p, 0, kSizeBuckets * 4ull, st));
