@@ -10,11 +10,11 @@ __global__ void __launch_bounds__(128, OD_MINB_FRONT) k_front(DecompArgs a) {
     Slot0 sl;
     u64 *names = nullptr; // this lane's name set, zeroed below by the whole warp
     u32 names_cap = 0;
+    const u32 lane = threadIdx.x & 31;
     if (dk_slot(a, &sl))
         front_one(a, sl, &names, &names_cap);
     // NameSet::keys must start zeroed: 32 lanes store 16 bytes each per
     // iteration instead of the kernel's lone lane walking the table
-    const u32 lane = threadIdx.x & 31;
     for (u32 src = 0; src < 32; ++src) {
         uint4 *p = reinterpret_cast<uint4 *>(__shfl_sync(0xffffffffu, (unsigned long long)names, src));
         const u32 n4 = __shfl_sync(0xffffffffu, names_cap, src) / 2;

@@ -41,10 +41,30 @@ __global__ void __launch_bounds__(128, OD_MINB_FOLD) k_fold(DecompArgs a) {
 #endif
 }
 
+__device__ __noinline__ void emit_one(const DecompArgs &a, const Slot0 &sl, const uint4 **cs, uint4 **cd,
+                                      u32 *cn);
+
 __global__ void __launch_bounds__(128, OD_MINB_EMIT) k_emit(DecompArgs a) {
     Slot0 sl;
-    if (!dk_slot(a, &sl))
-        return;
+    const uint4 *cs = nullptr; // this lane's kernel text in its arena ...
+    uint4 *cd = nullptr;       // ... and its place in the stage
+    u32 cn = 0;                // 16-byte words
+    if (dk_slot(a, &sl))
+        emit_one(a, sl, &cs, &cd, &cn);
+    // the whole warp copies each lane's text: coalesced 512-byte rows
+    // instead of one lane's 16-byte stream
+    const u32 lane = threadIdx.x & 31;
+    for (u32 src = 0; src < 32; ++src) {
+        const uint4 *s4 = reinterpret_cast<const uint4 *>(__shfl_sync(0xffffffffu, (unsigned long long)cs, src));
+        uint4 *d4 = reinterpret_cast<uint4 *>(__shfl_sync(0xffffffffu, (unsigned long long)cd, src));
+        const u32 n = __shfl_sync(0xffffffffu, cn, src);
+        for (u32 q = lane; q < n; q += 32)
+            d4[q] = s4[q];
+    }
+}
+
+__device__ __noinline__ void emit_one(const DecompArgs &a, const Slot0 &sl, const uint4 **cs, uint4 **cd,
+                                      u32 *cn) {
     KState *g = reinterpret_cast<KState *>(sl.base);
     KOut o;
     const u8 *src = nullptr;
@@ -92,10 +112,9 @@ __global__ void __launch_bounds__(128, OD_MINB_EMIT) k_emit(DecompArgs a) {
         if (so + padded > a.stage_cap) {
             r.status = KS_STAGE_FULL;
         } else {
-            const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
-            uint4 *d4 = reinterpret_cast<uint4 *>(a.stage + so);
-            for (u64 q = 0; q < padded / 16; ++q)
-                d4[q] = s4[q];
+            *cs = reinterpret_cast<const uint4 *>(src);
+            *cd = reinterpret_cast<uint4 *>(a.stage + so);
+            *cn = (u32)(padded / 16);
             r.stage_off = so;
             r.out_len = o.out_len;
         }
