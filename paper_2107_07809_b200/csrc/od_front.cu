@@ -4,15 +4,30 @@
 
 namespace od {
 
-__device__ __noinline__ void front_one(const DecompArgs &a, const Slot0 &sl, u64 **names, u32 *names_cap);
+__device__ __noinline__ void front_one(const DecompArgs &a, const Slot0 &sl, u64 **names, u32 *names_cap,
+                                       Slot **regs);
 
 __global__ void __launch_bounds__(128, OD_MINB_FRONT) k_front(DecompArgs a) {
     Slot0 sl;
     u64 *names = nullptr; // this lane's name set, zeroed below by the whole warp
     u32 names_cap = 0;
+    Slot *regs = nullptr; // and its register file (RegisterFile defaults)
     const u32 lane = threadIdx.x & 31;
     if (dk_slot(a, &sl))
-        front_one(a, sl, &names, &names_cap);
+        front_one(a, sl, &names, &names_cap, &regs);
+    {
+        Slot d;
+        reset_slot(d);
+        d.pad[0] = d.pad[1] = d.pad[2] = 0;
+        static_assert(sizeof(Slot) == 16, "one 16-byte store per slot");
+        const uint4 dv = *reinterpret_cast<const uint4 *>(&d);
+        for (u32 src = 0; src < 32; ++src) {
+            uint4 *p = reinterpret_cast<uint4 *>(__shfl_sync(0xffffffffu, (unsigned long long)regs, src));
+            if (p)
+                for (u32 q = lane; q < kPhysSlots; q += 32)
+                    p[q] = dv;
+        }
+    }
     // NameSet::keys must start zeroed: 32 lanes store 16 bytes each per
     // iteration instead of the kernel's lone lane walking the table
     for (u32 src = 0; src < 32; ++src) {
@@ -23,7 +38,8 @@ __global__ void __launch_bounds__(128, OD_MINB_FRONT) k_front(DecompArgs a) {
     }
 }
 
-__device__ __noinline__ void front_one(const DecompArgs &a, const Slot0 &sl, u64 **names, u32 *names_cap) {
+__device__ __noinline__ void front_one(const DecompArgs &a, const Slot0 &sl, u64 **names, u32 *names_cap,
+                                       Slot **regs) {
     const u32 k = sl.k;
     const u32 i = sl.i;
     KState *g = reinterpret_cast<KState *>(sl.base);
@@ -93,6 +109,7 @@ __device__ __noinline__ void front_one(const DecompArgs &a, const Slot0 &sl, u64
         if (!g->done && g->K.pool.keys) {
             *names = g->K.pool.keys;
             *names_cap = g->K.pool.cap;
+            *regs = g->K.regs;
         }
     }
 }

@@ -84,7 +84,8 @@ struct KIn {
     u32 novr;
     const u8 *ovr_text;
     const DumpCfg *dump;  // DOT dumps (null: none)
-    u32 names_zeroed_by_caller; // k_front's warp zeroes the name set after dk_front
+    u32 names_zeroed_by_caller; // k_front's warp zeroes the name set and writes the
+                                // default register slots after dk_front
     u32 kidx;             // chunk result index (dump records)
     u64 *prof;            // optional per-phase cycle counters
 };

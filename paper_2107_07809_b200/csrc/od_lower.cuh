@@ -1628,7 +1628,12 @@ OD_NOINL void dk_front(KState &S) {
     out.u_regions = K.nrg;
     K.regs = mem.get<Slot>(kPhysSlots);
     OD_CHECK(K.regs);
-    full_register_init(K);
+    if (in.names_zeroed_by_caller) { // k_front's warp writes the default slots
+        for (u32 w = 0; w < kLiveWords; ++w)
+            K.dirty[w] = 0;
+    } else {
+        full_register_init(K);
+    }
     const PoolCaps pc = pool_caps(in.lend - in.lbeg, in.scale ? in.scale : 1);
     K.E.cap = pc.nodes;
     K.E.n = mem.get<ENode>(K.E.cap);
