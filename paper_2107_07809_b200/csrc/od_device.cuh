@@ -98,7 +98,7 @@ __device__ __forceinline__ bool dk_slot(const DecompArgs &a, Slot0 *o) {
 
 // Minimum resident blocks per SM for the phase kernels (register caps).
 #ifndef OD_MINB_FRONT
-#define OD_MINB_FRONT 10
+#define OD_MINB_FRONT 16
 #endif
 #ifndef OD_MINB_LOWER
 #define OD_MINB_LOWER 16
