@@ -5,7 +5,52 @@
 namespace od {
 
 __device__ __noinline__ void front_one(const DecompArgs &a, const Slot0 &sl, u64 **names, u32 *names_cap,
-                                       Slot **regs);
+                                       Slot **regs, const Collected &col, bool collected);
+
+// collect_fill (od_kernel.cuh) for one kernel by the whole warp: 32 lines per
+// step, label and instruction positions from warp scans, the labels pending
+// before each instruction from the previous instruction line's label count.
+__device__ __noinline__ Collected warp_collect(const DecompArgs &a, u32 lbeg, u32 lend, Ins *ins, u32 *kl) {
+    const u32 lane = threadIdx.x & 31;
+    const u32 full = 0xffffffffu;
+    const u32 lt = (1u << lane) - 1;
+    Collected c{0, 0, 0, a.line_base + lbeg + 1, 0};
+    for (u32 l0 = lbeg + 1; l0 < lend; l0 += 32) {
+        const u32 l = l0 + lane;
+        LineIns L;
+        bool has = false;
+        u32 nl = 0;
+        if (l < lend && a.lines[l].role == LR_TEXT) {
+            L = a.lins[l];
+            nl = L.nlabels;
+            has = (L.flags & IF_HAS_INS) != 0;
+        }
+        u32 incl = nl;
+        for (u32 d = 1; d < 32; d <<= 1) {
+            const u32 t = __shfl_up_sync(full, incl, d);
+            if (lane >= d)
+                incl += t;
+        }
+        const u32 lab_incl = c.nkl + incl;
+        for (u32 k = 0; k < nl; ++k)
+            kl[lab_incl - nl + k] = L.lab_start + k;
+        const u32 hb = __ballot_sync(full, has);
+        const u32 before = hb & lt;
+        const u32 pv = __shfl_sync(full, lab_incl, before ? 31 - __clz(before) : lane);
+        if (has)
+            collect_ins(ins[c.nins + __popc(before)], L, a.ops, a.line_base + l + 1, before ? pv : c.pend_b,
+                        lab_incl - (before ? pv : c.pend_b));
+        c.any_failed |= __ballot_sync(full, has && (L.flags & IF_PARSE_FAILED)) ? 1u : 0u;
+        if (hb) {
+            const u32 last = 31 - __clz(hb);
+            c.pend_b = __shfl_sync(full, lab_incl, last);
+            c.last_line = a.line_base + l0 + last + 1;
+        }
+        c.nins += __popc(hb);
+        c.nkl = __shfl_sync(full, lab_incl, 31);
+    }
+    return c;
+}
 
 __global__ void __launch_bounds__(128, OD_MINB_FRONT) k_front(DecompArgs a) {
     Slot0 sl;
@@ -13,8 +58,33 @@ __global__ void __launch_bounds__(128, OD_MINB_FRONT) k_front(DecompArgs a) {
     u32 names_cap = 0;
     Slot *regs = nullptr; // and its register file (RegisterFile defaults)
     const u32 lane = threadIdx.x & 31;
-    if (dk_slot(a, &sl))
-        front_one(a, sl, &names, &names_cap, &regs);
+    const bool mine = dk_slot(a, &sl);
+    // the warp collects each of its kernels' instructions first
+    Collected col{0, 0, 0, 0, 0};
+    bool collected = false;
+    const u32 kb = (sizeof(KState) + 255) & ~255ull;
+    for (u32 src = 0; src < 32; ++src) {
+        const u32 k = __shfl_sync(0xffffffffu, mine ? sl.k : 0xffffffffu, src);
+        if (k == 0xffffffffu)
+            continue;
+        const u32 i = __shfl_sync(0xffffffffu, sl.i, src);
+        u8 *base = reinterpret_cast<u8 *>(__shfl_sync(0xffffffffu, (unsigned long long)sl.base, src));
+        const KSize z = a.sizes[k];
+        u64 kl_off;
+        const u64 need = collect_bytes(z.nins, z.nlab, &kl_off);
+        if (need > a.boff[i + 1] - a.boff[i] - kb)
+            continue; // the lane's own front runs out of arena and retries
+        const u32 lbeg = a.kstart[k], lend = k + 1 < a.nk ? a.kstart[k + 1] : a.nlines;
+        const Collected c = warp_collect(a, lbeg, lend, reinterpret_cast<Ins *>(base + kb),
+                                         reinterpret_cast<u32 *>(base + kb + kl_off));
+        if (lane == src) {
+            col = c;
+            collected = true;
+        }
+    }
+    __syncwarp();
+    if (mine)
+        front_one(a, sl, &names, &names_cap, &regs, col, collected);
     {
         Slot d;
         reset_slot(d);
@@ -39,7 +109,7 @@ __global__ void __launch_bounds__(128, OD_MINB_FRONT) k_front(DecompArgs a) {
 }
 
 __device__ __noinline__ void front_one(const DecompArgs &a, const Slot0 &sl, u64 **names, u32 *names_cap,
-                                       Slot **regs) {
+                                       Slot **regs, const Collected &col, bool collected) {
     const u32 k = sl.k;
     const u32 i = sl.i;
     KState *g = reinterpret_cast<KState *>(sl.base);
@@ -75,6 +145,12 @@ __device__ __noinline__ void front_one(const DecompArgs &a, const Slot0 &sl, u64
     in.dump = a.dump;
     in.kidx = k;
     in.names_zeroed_by_caller = 1;
+    in.collected = collected ? 1 : 0;
+    in.c_nins = col.nins;
+    in.c_nkl = col.nkl;
+    in.c_pend_b = col.pend_b;
+    in.c_last_line = col.last_line;
+    in.c_any_failed = col.any_failed;
     g->mem.base = sl.base + kb;
     g->mem.top = 0;
     g->mem.cap = a.boff[i + 1] - a.boff[i] - kb;

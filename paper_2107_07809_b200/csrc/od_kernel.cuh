@@ -86,6 +86,8 @@ struct KIn {
     const DumpCfg *dump;  // DOT dumps (null: none)
     u32 names_zeroed_by_caller; // k_front's warp zeroes the name set and writes the
                                 // default register slots after dk_front
+    u32 collected;        // k_front's warp filled the instruction / label arrays:
+    u32 c_nins, c_nkl, c_pend_b, c_last_line, c_any_failed; // ... with this tail
     u32 kidx;             // chunk result index (dump records)
     u64 *prof;            // optional per-phase cycle counters
 };
@@ -920,13 +922,50 @@ OD_NOINL void note_parse_failures(KCtx &K) {
 }
 
 // parse_text + attach_trailing_labels (asm_frontend.cpp:486-521,
-// decompiler.cpp:20-31)
-OD_NOINL bool collect_instructions(KCtx &K) {
+// decompiler.cpp:20-31), in three parts: the instruction and label arrays are
+// the kernel's first arena allocations (k_front's warp fills them at these
+// fixed addresses before the kernel's lane starts), the fill (here: the
+// serial form), and the common tail.
+OD_INL u64 collect_bytes(u32 nins, u32 nlab, u64 *kl_off) {
+    const u64 ib = (u64)(nins + 2) * sizeof(Ins); // + synthetic s_endpgm
+    *kl_off = (ib + 15) & ~15ull;
+    return *kl_off + (u64)(nlab + 1) * 4;
+}
+
+OD_NOINL bool collect_alloc(KCtx &K) {
+    K.ins = K.mem->get<Ins>(K.in->nins + 2);
+    K.kl = K.mem->get<u32>(K.in->nlab + 1);
+    return K.ins && K.kl;
+}
+
+// One text line of the collection: its labels, then its instruction (if any)
+// with the labels pending since the previous instruction.
+OD_INL void collect_ins(Ins &I, const LineIns &L, const Opnd *ops, u32 line, u32 lab_b, u32 lab_n) {
+    I.root = L.root;
+    I.prefix = L.prefix;
+    I.rflags = L.rflags;
+    I.sfx[0] = L.sfx[0];
+    I.sfx[1] = L.sfx[1];
+    I.nops = L.nops;
+    I.flags = L.flags;
+    I.op_start = L.op_start;
+    I.line = line;
+    I.src.off = L.src_off;
+    I.src.len = L.src_len;
+    I.lab_b = lab_b;
+    I.lab_n = lab_n;
+    u32 m = 0;
+    I.xkind = L.prefix == PX_S ? (u8)exec_kind_of(L.root, L.prefix, L.flags, L.nops, ops + L.op_start, &m)
+                               : (u8)XK_NONE;
+    I.xmask = m;
+}
+
+struct Collected {
+    u32 nins, nkl, pend_b, last_line, any_failed;
+};
+
+OD_NOINL Collected collect_fill(KCtx &K) {
     const KIn &in = *K.in;
-    K.ins = K.mem->get<Ins>(in.nins + 2); // + synthetic s_endpgm
-    K.kl = K.mem->get<u32>(in.nlab + 1);
-    if (!K.ins || !K.kl)
-        return false;
     // locals: the stores below go through generic pointers, which would
     // otherwise force the KCtx fields to be reloaded every iteration
     const LineRec *__restrict__ lines = in.lines;
@@ -935,46 +974,30 @@ OD_NOINL bool collect_instructions(KCtx &K) {
     Ins *__restrict__ ins = K.ins;
     u32 *__restrict__ kl = K.kl;
     const u32 lbeg = in.lbeg, lend = in.lend, line_base = in.line_base;
-    u32 ni = 0, nkl = 0, pend_b = 0;
-    u32 any_failed = 0;
-    u32 last_line = line_base + lbeg + 1; // section.line
+    Collected c{0, 0, 0, line_base + lbeg + 1, 0}; // last_line starts at section.line
     for (u32 l = lbeg + 1; l < lend; ++l) {
         if (lines[l].role != LR_TEXT)
             continue;
         const LineIns L = lins[l];
         for (u32 k = 0; k < L.nlabels; ++k)
-            kl[nkl++] = L.lab_start + k;
+            kl[c.nkl++] = L.lab_start + k;
         if (!(L.flags & IF_HAS_INS))
             continue;
-        Ins I;
-        I.root = L.root;
-        I.prefix = L.prefix;
-        I.rflags = L.rflags;
-        I.sfx[0] = L.sfx[0];
-        I.sfx[1] = L.sfx[1];
-        I.nops = L.nops;
-        I.flags = L.flags;
-        I.op_start = L.op_start;
-        I.line = line_base + l + 1;
-        I.src.off = L.src_off;
-        I.src.len = L.src_len;
-        I.lab_b = pend_b;
-        I.lab_n = nkl - pend_b;
-        any_failed |= L.flags & IF_PARSE_FAILED;
-        u32 m = 0;
-        I.xkind = L.prefix == PX_S ? (u8)exec_kind_of(L.root, L.prefix, L.flags, L.nops, ops + L.op_start, &m)
-                                   : (u8)XK_NONE;
-        I.xmask = m;
-        ins[ni++] = I;
-        pend_b = nkl;
-        last_line = I.line;
+        c.any_failed |= L.flags & IF_PARSE_FAILED;
+        collect_ins(ins[c.nins++], L, ops, line_base + l + 1, c.pend_b, c.nkl - c.pend_b);
+        c.pend_b = c.nkl;
+        c.last_line = line_base + l + 1;
     }
-    K.nins = ni;
-    K.nkl = nkl;
+    return c;
+}
+
+OD_NOINL void collect_finish(KCtx &K, const Collected &c) {
+    K.nins = c.nins;
+    K.nkl = c.nkl;
     K.nins_real = K.nins;
-    if (any_failed)
+    if (c.any_failed)
         note_parse_failures(K);
-    if (K.nkl > pend_b) {
+    if (K.nkl > c.pend_b) {
         Ins &I = K.ins[K.nins++];
         I.root = R_ENDPGM;
         I.prefix = PX_S;
@@ -983,15 +1006,14 @@ OD_NOINL bool collect_instructions(KCtx &K) {
         I.nops = 0;
         I.flags = IF_HAS_INS | IF_SYNTH;
         I.op_start = 0;
-        I.line = last_line;
+        I.line = c.last_line;
         I.src.off = 0;
         I.src.len = 0;
-        I.lab_b = pend_b;
-        I.lab_n = K.nkl - pend_b;
+        I.lab_b = c.pend_b;
+        I.lab_n = K.nkl - c.pend_b;
         I.xkind = XK_NONE;
         I.xmask = 0;
     }
-    return true;
 }
 
 // ============================================================== CFG

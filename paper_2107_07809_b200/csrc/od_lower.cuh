@@ -1575,6 +1575,7 @@ OD_NOINL void dk_front(KState &S) {
             return;                                                                                \
         }                                                                                          \
     } while (0)
+    OD_CHECK(collect_alloc(K)); // first in the arena (k_front's warp may have filled them)
     {
         const u32 cap = diag_cap(in);
         K.dg = mem.get<Diag>(cap);
@@ -1583,7 +1584,10 @@ OD_NOINL void dk_front(KState &S) {
         OD_CHECK(K.dg);
     }
     OD_CHECK(parse_config(K));
-    OD_CHECK(collect_instructions(K));
+    if (in.collected)
+        collect_finish(K, Collected{in.c_nins, in.c_nkl, in.c_pend_b, in.c_last_line, in.c_any_failed});
+    else
+        collect_finish(K, collect_fill(K));
     out.ninstr = K.nins_real;
     OD_CHECK(build_abi(K));
     OD_PROF(0, tp);

@@ -146,6 +146,7 @@ int main(int argc, char **argv) {
         kin.dump = dcfg.flags ? &dcfg : nullptr;
         kin.kidx = (u32)k;
         kin.names_zeroed_by_caller = 0;
+        kin.collected = 0;
         KOut ko;
         const u8 *src = nullptr;
         std::vector<u8> arena;
