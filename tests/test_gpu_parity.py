@@ -222,3 +222,51 @@ def test_session_run_host_overlapped_chunks(monkeypatch, pinned):
             s.run_host(pin_ptr, len(listing), out_ptr, len(ref) // 2)
     finally:
         s.close()
+
+
+def _one_huge_kernel(shape, count, seed):
+    """The first kernel's header, then the .text lines of `count` generated
+    kernels as one kernel (labels renamed apart, s_endpgm dropped but the
+    last)."""
+    import re
+    listing, _, _ = P.generate_corpus(shape, count, seed=seed)
+    head, body, seen_text, in_text, k = [], [], False, False, 0
+    for line in listing.split(b"\n"):
+        s = line.strip()
+        if s.startswith(b".kernel"):
+            in_text = False
+            k += 1
+            continue
+        line = re.sub(rb"\bL(\d+)\b", b"L\\1_%d" % k, line)  # labels unique per source kernel
+        if s.startswith(b".text"):
+            in_text = True
+            seen_text = True
+            continue
+        if in_text:
+            if s != b"s_endpgm":
+                body.append(line)
+        elif not seen_text:
+            head.append(line)
+    return b"\n".join([b".kernel huge"] + head + [b"  .text"] + body + [b"    s_endpgm", b""])
+
+
+@pytest.mark.skipif(not O.available(), reason="oracle not built")
+def test_huge_kernel_and_long_lines():
+    """Maximum sizes: one kernel of ~25k branching instructions (arena
+    budget, one thread doing the whole kernel), and lines far longer than the
+    decode stage (the decoder reads those from HBM)."""
+    big = _one_huge_kernel("C3", 300, seed=21)
+    ref = O.decompile(big)
+    assert len(ref.kernels) == 1 and not ref.kernels[0].failed
+    res = P.decompile_listing(big)
+    assert res.combined == ref.combined
+    assert res.kernels[0].instructions > 15_000
+    long_arg = b"s" * 40_000
+    listing = (b".kernel k\n  .text\n  v_mov_b32 v1, v2 ; " + b"c" * 70_000 + b"\n"
+               b"  s_nop " + long_arg + b"\n  v_add_u32 v1, vcc, " + b"0x" + b"0" * 30_000 + b"5, v1\n"
+               b"  s_endpgm\n")
+    r = P.decompile_listing(listing)
+    f = O.decompile(listing)
+    assert r.combined == f.combined
+    assert [(d.severity, d.line, d.message.encode()) for d in r.diagnostics] == \
+           [(d.severity, d.line, d.message) for d in f.diagnostics]
