@@ -95,6 +95,9 @@ __device__ __forceinline__ bool dk_slot(const DecompArgs &a, Slot0 *o) {
 #ifndef OD_LOCAL_LOWER
 #define OD_LOCAL_LOWER 0
 #endif
+#ifndef OD_LOCAL_FOLD
+#define OD_LOCAL_FOLD OD_LOCAL_STATE
+#endif
 
 // Minimum resident blocks per SM for the phase kernels (register caps).
 #ifndef OD_MINB_FRONT

@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(128, OD_MINB_FOLD) k_fold(DecompArgs a) {
     KState *g = reinterpret_cast<KState *>(sl.base);
     if (g->done)
         return;
-#if OD_LOCAL_STATE
+#if OD_LOCAL_FOLD
     KState S;
     kstate_load(S, g);
     dk_fold(S);
