@@ -4,10 +4,12 @@
 // Pass plan per chunk of the listing:
 //   P1a k_nl_count/k_nl_write  16-byte vector loads, block scan of newline
 //                              flags -> newline positions
-//   P1b k_classify             thread per line: comment strip, trim, first word
+//   P1b k_classify             thread per line: comment strip, trim, first word,
+//                              operand / label bounds for the decode pools
 //   P1c section scan           (kernel count, last directive) pair scan -> line roles
-//   P1d k_decode (x2)          thread per text line: labels, perfect-hash
-//                              mnemonic, operands (sizing pass, scan, fill pass)
+//   P1d k_decode               thread per text line: labels, perfect-hash
+//                              mnemonic, operands (pool offsets scanned from
+//                              the bounds)
 //   P2-P4a k_front/k_lower/k_fold/k_emit  thread per .kernel section, size-sorted waves with
 //                              exact per-kernel arenas: config/ABI, CFG,
 //                              exec-mask normalization, region reduction,
@@ -124,8 +126,13 @@ __global__ void k_nl_write(const u8 *__restrict__ base, u64 len, u32 mis, const 
 
 // ------------------------------------------------------------------ P1b
 // Thread per line: comment strip + rtrim + first-word kind.
+// Also sizes the decode pools: an upper bound of the line's operands (one
+// more than its runs of ',' / ' ' / '\t': every token after the first follows
+// such a run) and of its labels (its ':' count), over the raw line, which
+// contains whatever the comment strip keeps.
 __global__ void k_classify(const u8 *__restrict__ t, u64 len, const u32 *__restrict__ nlpos,
-                           u32 nlf, u32 nlines, LineRec *lines, u32 *complex_bytes) {
+                           u32 nlf, u32 nlines, LineRec *lines, u32 *complex_bytes, u32 *ops_ub,
+                           u32 *labs_ub) {
     u32 l = blockIdx.x * blockDim.x + threadIdx.x;
     if (l >= nlines)
         return;
@@ -148,6 +155,20 @@ __global__ void k_classify(const u8 *__restrict__ t, u64 len, const u32 *__restr
         atomicAdd(complex_bytes, e - b);
     }
     lines[l] = r;
+    u32 runs = 0, colons = 0;
+    if (cx || r.len) {
+        bool prev = false;
+        for (u32 i = b; i < e; ++i) {
+            const u8 c = t[i];
+            const bool sep = c == ',' || c == ' ' || c == '\t';
+            runs += sep && !prev;
+            prev = sep;
+            colons += c == ':';
+        }
+        ++runs;
+    }
+    ops_ub[l] = runs;
+    labs_ub[l] = colons;
 }
 
 // Complex lines (with a terminated /* */ mid-line) are materialized into the
@@ -891,7 +912,10 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
         return -3;
     k_nl_write<<<ntiles, kTileThreads, 0, st>>>(t, len, mis, P<u32>(s->tiles_off), P<u32>(s->nlpos));
     const u32 lb = 256, lg = (nlines + lb - 1) / lb;
-    k_classify<<<lg, lb, 0, st>>>(t, len, P<u32>(s->nlpos), nlf, nlines, P<LineRec>(s->lines), cnt + 1);
+    if (ensure(s->ops_cnt, (nlines + 1) * 4ull) || ensure(s->labs_cnt, (nlines + 1) * 4ull))
+        return -3;
+    k_classify<<<lg, lb, 0, st>>>(t, len, P<u32>(s->nlpos), nlf, nlines, P<LineRec>(s->lines), cnt + 1,
+                                  P<u32>(s->ops_cnt), P<u32>(s->labs_cnt));
     s->stats.total_launches += 3;
     CK(cudaGetLastError());
     u32 cbytes = 0;
@@ -939,14 +963,10 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     if (nk == 0)
         return 0;
     CK(cudaEventRecord(s->ev[1], st));
-    // P1d decode: sizing, scans, fill
-    if (ensure(s->lins, (u64)(nlines + 1) * sizeof(LineIns)) || ensure(s->ops_cnt, (nlines + 1) * 4ull) ||
-        ensure(s->labs_cnt, (nlines + 1) * 4ull) || ensure(s->ops_off, (nlines + 1) * 4ull) ||
+    // P1d decode: pool offsets from k_classify's bounds, then the fill
+    if (ensure(s->lins, (u64)(nlines + 1) * sizeof(LineIns)) || ensure(s->ops_off, (nlines + 1) * 4ull) ||
         ensure(s->labs_off, (nlines + 1) * 4ull))
         return -3;
-    k_decode<<<lg, lb, 0, st>>>(t, len, P<u32>(s->nlpos), nlf, nlines, P<LineRec>(s->lines), P<LineIns>(s->lins),
-                                P<u32>(s->ops_cnt), P<u32>(s->labs_cnt), nullptr, nullptr, nullptr, nullptr, 0);
-    s->stats.total_launches++;
     if (scan_exclusive(s, nlines, SU32{0}, AddU32{}, U32Load{P<u32>(s->ops_cnt)},
                        U32Store{P<u32>(s->ops_off)}, reinterpret_cast<SU32 *>(cnt + 8)) ||
         scan_exclusive(s, nlines, SU32{0}, AddU32{}, U32Load{P<u32>(s->labs_cnt)},
