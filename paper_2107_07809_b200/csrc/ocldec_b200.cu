@@ -233,8 +233,8 @@ __global__ void k_init_roots() {
         build_root_table(&d_roots);
 }
 
-// mode 0: sizing (writes per-line operand/label counts); mode 1: fill.
-// The block's 256 lines are one contiguous span of the listing: it is staged
+// One pass per text line into the operand / label pools at the offsets
+// scanned from k_classify's bounds.  The block's 256 lines are one contiguous span of the listing: it is staged
 // in shared memory (16-byte vector loads for the aligned interior) and every
 // thread decodes its line from there.  Lines whose content lives in the aux
 // area (comment-stripped copies) and oversized spans read the listing in HBM.
@@ -242,8 +242,8 @@ constexpr u32 kDecodeStage = 16384;
 
 __global__ void __launch_bounds__(256) k_decode(const u8 *__restrict__ t, u64 len, const u32 *__restrict__ nlpos,
                                                 u32 nlf, u32 nlines, const LineRec *__restrict__ lines,
-                                                LineIns *lins, u32 *ops_cnt, u32 *labs_cnt, const u32 *ops_off,
-                                                const u32 *labs_off, Opnd *ops, Label *labs, int mode) {
+                                                LineIns *lins, const u32 *ops_off, const u32 *labs_off,
+                                                Opnd *ops, Label *labs) {
     __shared__ RootTable rt;
     __shared__ __align__(16) u8 stage[kDecodeStage];
     for (u32 i = threadIdx.x; i < sizeof(RootTable) / 4; i += blockDim.x)
@@ -277,30 +277,18 @@ __global__ void __launch_bounds__(256) k_decode(const u8 *__restrict__ t, u64 le
     if (l >= nlines)
         return;
     const LineRec L = lines[l];
-    if (L.role != LR_TEXT) {
-        if (mode == 0) {
-            ops_cnt[l] = 0;
-            labs_cnt[l] = 0;
-        }
+    if (L.role != LR_TEXT)
         return;
-    }
     // the decoder addresses the listing by chunk offsets: tb[off] == t[off]
     const bool in_stage = staged && !L.complex && L.off >= sb && (u64)L.off + L.len <= se;
     const u8 *tb = in_stage ? stage - ab : t;
     LineIns li;
-    if (mode == 0) {
-        u32 no, nl;
-        count_line(tb, Span{L.off, L.len}, &no, &nl);
-        ops_cnt[l] = no;
-        labs_cnt[l] = nl;
-    } else {
-        u32 oo = ops_off[l], lo = labs_off[l];
-        const u32 cap = (l + 1 < nlines ? ops_off[l + 1] : 0xffffffffu) - oo;
-        decode_line(tb, Span{L.off, L.len}, &rt, &li, ops + oo, cap, labs + lo);
-        li.op_start = oo;
-        li.lab_start = lo;
-        lins[l] = li;
-    }
+    const u32 oo = ops_off[l], lo = labs_off[l];
+    const u32 cap = (l + 1 < nlines ? ops_off[l + 1] : 0xffffffffu) - oo;
+    decode_line(tb, Span{L.off, L.len}, &rt, &li, ops + oo, cap, labs + lo);
+    li.op_start = oo;
+    li.lab_start = lo;
+    lins[l] = li;
 }
 
 // Per-kernel sizes (a pass over the kernel's decoded lines), size key and
@@ -978,8 +966,7 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     if (ensure(s->ops, (pools[0] + 1ull) * sizeof(Opnd)) || ensure(s->labs, (pools[1] + 1ull) * sizeof(Label)))
         return -3;
     k_decode<<<lg, lb, 0, st>>>(t, len, P<u32>(s->nlpos), nlf, nlines, P<LineRec>(s->lines), P<LineIns>(s->lins),
-                                nullptr, nullptr, P<u32>(s->ops_off), P<u32>(s->labs_off), P<Opnd>(s->ops),
-                                P<Label>(s->labs), 1);
+                                P<u32>(s->ops_off), P<u32>(s->labs_off), P<Opnd>(s->ops), P<Label>(s->labs));
     s->stats.total_launches++;
     CK(cudaGetLastError());
     CK(cudaEventRecord(s->ev[2], st));

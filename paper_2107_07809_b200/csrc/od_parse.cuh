@@ -463,78 +463,6 @@ OD_NOINL int parse_operand(const u8 *t, Span tok, Opnd *op) {
     return 0;
 }
 
-// Sizing pass of decode_line: the label count and an upper bound of the
-// operand count (every token of every top-level field; exact unless an
-// operand ParseError demotes the line, which then has none).  No mnemonic
-// decoding, no operand parsing.
-OD_NOINL void count_line(const u8 *t, Span content, u32 *nops_ub, u32 *nlab_out) {
-    u32 b = content.off, e = content.off + content.len;
-    while (b < e && c_space(t[b]))
-        ++b;
-    u32 nlab = 0;
-    while (b < e && c_ident_start(t[b])) {
-        u32 x = b;
-        while (x < e && c_ident_char(t[x]))
-            ++x;
-        if (x >= e || t[x] != ':')
-            break;
-        ++nlab;
-        b = x + 1;
-        while (b < e && c_space(t[b]))
-            ++b;
-    }
-    *nlab_out = nlab > 65535 ? 65535 : nlab;
-    *nops_ub = 0;
-    if (b == e)
-        return;
-    Span word, rest;
-    split_word(t, Span{b, e - b}, &word, &rest);
-    if (span_eq(t, word, "s_waitcnt")) {
-        *nops_ub = rest.len ? 1 : 0;
-        return;
-    }
-    u32 nops = 0;
-    int depth = 0;
-    bool inq = false;
-    u32 fstart = rest.off;
-    const u32 rend = rest.off + rest.len;
-    for (u32 i = rest.off; i <= rend; ++i) {
-        bool cut = false;
-        if (i == rend) {
-            cut = true;
-        } else {
-            u8 c = t[i];
-            if (c == '"')
-                inq = !inq;
-            if (!inq) {
-                if (c == '[' || c == '(')
-                    ++depth;
-                else if (c == ']' || c == ')')
-                    --depth;
-                else if (c == ',' && depth == 0)
-                    cut = true;
-            }
-        }
-        if (!cut)
-            continue;
-        u32 fb = fstart, fe = i;
-        while (fb < fe && c_space(t[fb]))
-            ++fb;
-        while (fe > fb && c_space(t[fe - 1]))
-            --fe;
-        u32 q = fb;
-        while (q < fe) {
-            while (q < fe && !c_space(t[q]))
-                ++q;
-            ++nops;
-            while (q < fe && c_space(t[q]))
-                ++q;
-        }
-        fstart = i + 1;
-    }
-    *nops_ub = nops;
-}
-
 // Decodes one text line: label peeling (parse_text, asm_frontend.cpp:486-521)
 // plus parse_instruction (:439-484).  When ops/labs are null only the
 // counts are produced (sizing pass).  Returns 1 when an operand ParseError
