@@ -62,3 +62,27 @@ def test_shapes_sizes():
         _, offs, ni = P.generate_corpus(shape, 16, seed=9)
         per = ni / 16
         assert lo <= per <= hi, (shape, per)
+
+
+def test_ctypes_mirror_matches_header_layout(tmp_path):
+    """The ctypes structs the Python front door uses (_lib.py) have the C
+    header's sizes and field offsets (no silent ABI drift)."""
+    structs = {"ocldec_b200_options": _lib.Options, "ocldec_b200_kernel": _lib.Kernel,
+               "ocldec_b200_diag": _lib.Diag, "ocldec_b200_dump": _lib.Dump,
+               "ocldec_b200_result": _lib.Result, "ocldec_b200_stats": _lib.Stats}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "ocldec_b200.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'  printf("{cname} size %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            lines.append(f'  printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("  return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    for line in filter(None, out):
+        cname, field, value = line.split()
+        py = structs[cname]
+        got = ctypes.sizeof(py) if field == "size" else getattr(py, field).offset
+        assert got == int(value), (cname, field, got, value)
