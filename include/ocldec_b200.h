@@ -151,6 +151,15 @@ int ocldec_b200_session_output(ocldec_b200_session *s, const void **d_out, uint6
 int ocldec_b200_session_kernels(ocldec_b200_session *s, uint64_t *off, uint64_t *len,
                                 uint32_t *flags, uint32_t *fallbacks);
 
+/* Kernel names of the last run: name k is the caller's listing bytes
+ * [off[k], off[k] + len[k]) (off[k] == UINT64_MAX when the .kernel line held
+ * a stripped comment and the name is not one span of the listing). */
+int ocldec_b200_session_names(ocldec_b200_session *s, uint64_t *off, uint32_t *len);
+/* DecompileResult::diagnostics of the last run, in sink order, as
+ * "<severity> <line> <message>\n" lines (NUL-terminated) in buf; returns the
+ * count, or -2 when cap < *need. */
+int ocldec_b200_session_diagnostics(ocldec_b200_session *s, char *buf, uint64_t cap, uint64_t *need);
+
 /* cudaMemcpy(dst, src, n, cudaMemcpyDefault): host<->device staging helper
  * for callers without their own CUDA runtime binding. */
 int ocldec_b200_copy(void *dst, const void *src, uint64_t n);

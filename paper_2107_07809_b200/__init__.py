@@ -288,6 +288,33 @@ class Session:
             raise RuntimeError(f"session_kernels failed ({rc}): {_lib.last_error()}")
         return off[:n], ln[:n], fl[:n], fb[:n]
 
+    def names(self):
+        """(listing offset, length) of each kernel's name in the last run
+        (offset 2**64-1: not a single listing span); ocldec_b200_session_names."""
+        import numpy as np
+        n = int(self.stats()["kernels"])
+        off = np.zeros(n + 1, dtype=np.uint64)
+        ln = np.zeros(n + 1, dtype=np.uint32)
+        rc = self._L.ocldec_b200_session_names(self._s, off.ctypes.data, ln.ctypes.data)
+        if rc:
+            raise RuntimeError(f"session_names failed ({rc}): {_lib.last_error()}")
+        return off[:n], ln[:n]
+
+    def diagnostics(self) -> List[Diagnostic]:
+        """DecompileResult::diagnostics of the last run (ocldec_b200_session_diagnostics)."""
+        need = ctypes.c_uint64()
+        self._L.ocldec_b200_session_diagnostics(self._s, None, 0, ctypes.byref(need))
+        buf = ctypes.create_string_buffer(need.value)
+        rc = self._L.ocldec_b200_session_diagnostics(self._s, buf, need.value, ctypes.byref(need))
+        if rc < 0:
+            raise RuntimeError(f"session_diagnostics failed ({rc}): {_lib.last_error()}")
+        out = []
+        for line in buf.raw[:need.value - 1].split(b"\n"):
+            if line:
+                sev, ln, msg = line.split(b" ", 2)
+                out.append(Diagnostic(int(sev), int(ln), msg.decode("utf-8", errors="surrogateescape")))
+        return out
+
     def output(self):
         p, n = ctypes.c_void_p(), ctypes.c_uint64()
         self._L.ocldec_b200_session_output(self._s, ctypes.byref(p), ctypes.byref(n))

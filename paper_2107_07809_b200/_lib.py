@@ -66,6 +66,7 @@ EXPORTS = [
     "ocldec_b200_session_run", "ocldec_b200_session_stats", "ocldec_b200_session_output",
     "ocldec_b200_session_kernels", "ocldec_b200_gen_host", "ocldec_b200_gen_device",
     "ocldec_b200_session_run_host", "ocldec_b200_copy", "ocldec_b200_abi_map_check",
+    "ocldec_b200_session_names", "ocldec_b200_session_diagnostics",
 ]
 
 _lib = None
@@ -104,6 +105,8 @@ def load():
     L.ocldec_b200_session_stats.argtypes = [vp, ctypes.POINTER(Stats)]
     L.ocldec_b200_session_output.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(u64)]
     L.ocldec_b200_session_kernels.argtypes = [vp, vp, vp, vp, vp]
+    L.ocldec_b200_session_names.argtypes = [vp, vp, vp]
+    L.ocldec_b200_session_diagnostics.argtypes = [vp, ctypes.c_char_p, u64, ctypes.POINTER(u64)]
     L.ocldec_b200_gen_host.argtypes = [i32, i32, u64, u64, u64, vp, u64, vp, ctypes.POINTER(u64),
                                        ctypes.POINTER(u64)]
     L.ocldec_b200_gen_host.restype = ctypes.c_int64

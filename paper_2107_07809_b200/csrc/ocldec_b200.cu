@@ -783,6 +783,8 @@ struct ocldec_b200_session {
     std::vector<KRes> host_res;      // last run, all chunks
     std::vector<u64> host_kernel_off;
     std::vector<u32> host_name_line; // chunk-relative .kernel line (host path names)
+    std::vector<u64> host_name_off;  // listing offset of each kernel's name (~0: not a listing span)
+    u64 chunk_base = 0;              // listing offset of the chunk run_chunk is working on
     std::vector<cudaEvent_t> pev;    // phase-launch events (pool)
     DevBuf dpool, dtop;              // device diagnostic records of a chunk
     std::vector<HostDiag> host_diag; // materialized diagnostics, all chunks
@@ -1323,6 +1325,8 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
         s->host_res.push_back(hr[k]);
         s->host_kernel_off.push_back(base + offs[k]);
         s->host_name_line.push_back(ks[k]);
+        s->host_name_off.push_back((u64)hr[k].name_off + hr[k].name_len <= len ? s->chunk_base + hr[k].name_off
+                                                                              : ~0ull);
         s->stats.instructions += hr[k].ninstr;
         s->stats.failed += hr[k].status == KS_FAILED;
         s->stats.goto_form += hr[k].status == KS_OK && !hr[k].structured;
@@ -1416,6 +1420,7 @@ void reset_stats(ocldec_b200_session *s) {
     s->host_res.clear();
     s->host_kernel_off.clear();
     s->host_name_line.clear();
+    s->host_name_off.clear();
     s->host_diag.clear();
     s->host_kdiag.clear();
     s->host_dumps.clear();
@@ -1568,6 +1573,7 @@ int run_host_listing(ocldec_b200_session *s, const char *listing, size_t len, in
         u8 *tc = P<u8>(*tb[c & 1]);
         ChunkOut co;
         size_t before = s->host_res.size();
+        s->chunk_base = b;
         int rc = run_chunk(s, tc, n, true, line_base, fold_local_size, out_pos, nonempty, &co);
         if (rc) {
             cudaStreamSynchronize(s->cstream);
@@ -1693,6 +1699,7 @@ int ocldec_b200_session_run(ocldec_b200_session *s, const void *d_listing, size_
         u64 b = chunk_starts[c];
         u64 e = c + 1 < nchunks ? chunk_starts[c + 1] : len;
         ChunkOut co;
+        s->chunk_base = b;
         int rc = run_chunk(s, base + b, e - b, false, line_base, fold_local_size, out_pos, nonempty, &co);
         if (rc)
             return rc;
@@ -1754,6 +1761,45 @@ int ocldec_b200_session_kernels(ocldec_b200_session *s, uint64_t *off, uint64_t 
             fallbacks[k] = r.fallbacks;
     }
     return 0;
+}
+
+int ocldec_b200_session_names(ocldec_b200_session *s, uint64_t *off, uint32_t *len) {
+    if (!s)
+        return -1;
+    for (size_t k = 0; k < s->host_res.size(); ++k) {
+        if (off)
+            off[k] = s->host_name_off[k];
+        if (len)
+            len[k] = s->host_res[k].name_len;
+    }
+    return 0;
+}
+
+int ocldec_b200_session_diagnostics(ocldec_b200_session *s, char *buf, uint64_t cap, uint64_t *need) {
+    if (!s || (!buf && cap))
+        return -1;
+    std::string out;
+    int n = 0;
+    for (size_t k = 0; k < s->host_res.size() && k < s->host_kdiag.size(); ++k) {
+        const KRes &r = s->host_res[k];
+        if (r.status == KS_SKIP)
+            continue;
+        for (u32 q = 0; q < r.ndiag; ++q) {
+            const HostDiag &h = s->host_diag[s->host_kdiag[k] + q];
+            out += std::to_string(diag_severity(h.code)) + " " + std::to_string(h.line) + " " +
+                   diag_message(h, &s->ovr_host) + "\n";
+            ++n;
+        }
+    }
+    if (need)
+        *need = out.size() + 1;
+    if (out.size() + 1 > cap) {
+        g_err = "diagnostics buffer too small";
+        return -2;
+    }
+    memcpy(buf, out.data(), out.size());
+    buf[out.size()] = 0;
+    return n;
 }
 
 int ocldec_b200_decompile(const char *listing, size_t len, const ocldec_b200_options *opts,

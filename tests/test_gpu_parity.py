@@ -270,3 +270,32 @@ def test_huge_kernel_and_long_lines():
     assert r.combined == f.combined
     assert [(d.severity, d.line, d.message.encode()) for d in r.diagnostics] == \
            [(d.severity, d.line, d.message) for d in f.diagnostics]
+
+
+@pytest.mark.skipif(not O.available(), reason="oracle not built")
+def test_session_batch_names_and_diagnostics():
+    """The batch (session) form returns what SURVEY §8(b) lists for it: per
+    kernel source spans, flags and fallbacks, name spans into the caller's
+    listing, and the diagnostics in sink order, over a multi-chunk run."""
+    import numpy as np
+    listing, offs, _ = P.generate_corpus("C3", 700, seed=314, stress=True)
+    ref = O.decompile(listing)
+    s = P.Session(0)
+    try:
+        d_buf, n, _, _ = s.generate("C3", 700, seed=314, stress=True)
+        assert n == len(listing)
+        s.run(d_buf, n, [int(offs[k]) for k in (0, 200, 450)])
+        noff, nlen = s.names()
+        names = [listing[int(o):int(o) + int(ln)] for o, ln in zip(noff, nlen)]
+        assert names == [k.name for k in ref.kernels]
+        koff, klen, kfl, kfb = s.kernels()
+        out = s.output_bytes()
+        srcs = [out[int(o):int(o) + int(ln)] for o, ln in zip(koff, klen)]
+        assert srcs == [k.source for k in ref.kernels]
+        assert [bool(f & 1) for f in kfl] == [k.failed for k in ref.kernels]
+        assert list(kfb) == [k.fallback_count for k in ref.kernels]
+        assert [(d.severity, d.line, d.message.encode("utf-8", "surrogateescape")) for d in s.diagnostics()] == \
+               [(d.severity, d.line, d.message) for d in ref.diagnostics]
+        assert len(ref.diagnostics) > 50
+    finally:
+        s.close()
