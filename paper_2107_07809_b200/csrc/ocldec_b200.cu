@@ -1428,9 +1428,16 @@ void reset_stats(ocldec_b200_session *s) {
 }
 
 // Splits a host listing into chunks of < ~1 GiB at ".kernel" line starts.
-// The first chunk is `first` bytes (its load is the one copy nothing hides).
+// The first chunk is `first` bytes (its load is the one copy nothing hides);
+// the rest is cut into as few chunks of at most `target` bytes as fit, of
+// about equal size (every phase launch ends in a tail).
 std::vector<u64> host_chunks(const char *p, size_t len, size_t target, size_t first) {
     std::vector<u64> starts{0};
+    if (len > first) {
+        const size_t rem = len - first;
+        const size_t nch = (rem + target - 1) / target;
+        target = (rem + nch - 1) / nch;
+    }
     size_t next = first;
     while (next < len) {
         // find a line whose first word is exactly ".kernel"
