@@ -914,7 +914,7 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     if (cbytes) {
         if (len + (u64)cbytes >= 0xffff0000ull) {
             g_err = "chunk plus comment-stripped lines exceed 4 GiB";
-            return -1;
+            return -5; // the host path retries with smaller chunks
         }
         if (!can_extend) {
             // copy the chunk into the session buffer (with aux room) and redo
@@ -1485,7 +1485,9 @@ size_t chunk_target() {
         if (v >= 1)
             return v;
     }
-    return (size_t)5 << 29; // 2.5 GiB: chunk + aux area stay in u32 offsets
+    // 3 GiB: few chunks (each phase launch ends in a tail); a chunk whose
+    // comment-stripped copies would push it past 4 GiB is retried smaller
+    return (size_t)3 << 30;
 }
 
 // Parses an ABI override file (or clears the overrides) and uploads the
@@ -1530,8 +1532,25 @@ int set_overrides(ocldec_b200_session *s, const char *text, size_t len) {
 // beyond it is not copied).  The next chunk's text is loaded the same way
 // into the other of two text buffers, so the PCIe traffic hides behind the
 // decompiler except for the first load and the last store.
+int run_host_listing_at(ocldec_b200_session *s, const char *listing, size_t len, int fold_local_size,
+                        const char *only_kernel, HostRun *hr, char *host_out, u64 out_cap, size_t target);
+
 int run_host_listing(ocldec_b200_session *s, const char *listing, size_t len, int fold_local_size,
                      const char *only_kernel, HostRun *hr, char *host_out, u64 out_cap) {
+    size_t target = chunk_target();
+    for (;;) {
+        const bool names = hr->want_names;
+        *hr = HostRun{};
+        hr->want_names = names;
+        int rc = run_host_listing_at(s, listing, len, fold_local_size, only_kernel, hr, host_out, out_cap, target);
+        if (rc != -5 || target <= (64u << 20))
+            return rc == -5 ? -1 : rc;
+        target /= 2; // chunk + comment-stripped copies past the u32 range
+    }
+}
+
+int run_host_listing_at(ocldec_b200_session *s, const char *listing, size_t len, int fold_local_size,
+                        const char *only_kernel, HostRun *hr, char *host_out, u64 out_cap, size_t target) {
     reset_stats(s);
     s->stats.in_bytes = len;
     s->only_len = 0;
@@ -1545,7 +1564,6 @@ int run_host_listing(ocldec_b200_session *s, const char *listing, size_t len, in
     } else {
         s->only_set = false;
     }
-    const size_t target = chunk_target();
     std::vector<u64> starts = host_chunks(listing, len, target, std::max<size_t>(target / 4, 1));
     const size_t nch = starts.size();
     auto cb = [&](size_t c) { return starts[c]; };
@@ -1709,7 +1727,7 @@ int ocldec_b200_session_run(ocldec_b200_session *s, const void *d_listing, size_
         s->chunk_base = b;
         int rc = run_chunk(s, base + b, e - b, false, line_base, fold_local_size, out_pos, nonempty, &co);
         if (rc)
-            return rc;
+            return rc == -5 ? -1 : rc; // (chunk + comment-stripped copies: the caller picks smaller chunks)
         if (co.err_line != 0xffffffffu) {
             g_err = "split_kernels error";
             s->stats.lines += co.nlines;

@@ -299,3 +299,17 @@ def test_session_batch_names_and_diagnostics():
         assert len(ref.diagnostics) > 50
     finally:
         s.close()
+
+
+def test_comment_heavy_chunk_retries_smaller(monkeypatch):
+    """A chunk whose comment-stripped copies would push it past the u32
+    offset range (chunk + aux >= 4 GiB) is re-run in smaller chunks by the
+    host path, with the same output as the listing without the comments."""
+    listing, _, _ = P.generate_corpus("C2", 300_000, seed=5)
+    assert len(listing) > (2 << 30) - (128 << 20)
+    commented = listing.replace(b"\n", b" /* c */\n")  # every line needs the aux copy
+    monkeypatch.setenv("OCLDEC_B200_CHUNK_BYTES", str(7 << 29))  # one 3.5 GiB chunk: overflows
+    a = P.decompile_listing(commented)
+    monkeypatch.setenv("OCLDEC_B200_CHUNK_BYTES", str(1 << 30))
+    b = P.decompile_listing(listing)
+    assert a.combined == b.combined and len(a.kernels) == 300_000
