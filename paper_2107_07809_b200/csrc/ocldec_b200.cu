@@ -1099,7 +1099,7 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
             a.count = w1 - w0;
             a.scale = scale;
             a.arena = P<u8>(s->arena) + (second ? half : 0);
-            auto grid = [&](u32 lp) { return (u32)(((u64)a.count * lp + 127) / 128); };
+            auto grid = [&](u32 lp) { return (u32)(((u64)a.count * lp + OD_BLOCK - 1) / OD_BLOCK); };
             cudaEvent_t pe[5];
             for (auto &e : pe)
                 if (phase_event(s, &e))
@@ -1107,7 +1107,7 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
             CK(cudaEventRecord(pe[0], ws));
             a.lanes_per = s->lanes_front;
             a.perm = nullptr;
-            k_front<<<grid(a.lanes_per), 128, s->smem_front, ws>>>(a);
+            k_front<<<grid(a.lanes_per), OD_BLOCK, s->smem_front, ws>>>(a);
             if (!two && a.count >= 256 && s->group_class) {
                 // regroup the wave by what k_front found (straight / if-joins /
                 // goto form) so the later phases' resident kernels share code
@@ -1121,12 +1121,12 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
             }
             CK(cudaEventRecord(pe[1], ws));
             a.lanes_per = s->lanes_lower;
-            k_lower<<<grid(a.lanes_per), 128, s->smem_lower, ws>>>(a);
+            k_lower<<<grid(a.lanes_per), OD_BLOCK, s->smem_lower, ws>>>(a);
             CK(cudaEventRecord(pe[2], ws));
-            k_fold<<<grid(a.lanes_per), 128, s->smem_lower, ws>>>(a);
+            k_fold<<<grid(a.lanes_per), OD_BLOCK, s->smem_lower, ws>>>(a);
             CK(cudaEventRecord(pe[3], ws));
             a.lanes_per = s->lanes_emit;
-            k_emit<<<grid(a.lanes_per), 128, s->smem_emit, ws>>>(a);
+            k_emit<<<grid(a.lanes_per), OD_BLOCK, s->smem_emit, ws>>>(a);
             CK(cudaEventRecord(pe[4], ws));
             s->stats.decompile_launches += 4;
             s->stats.total_launches += 4;

@@ -99,7 +99,13 @@ __device__ __forceinline__ bool dk_slot(const DecompArgs &a, Slot0 *o) {
 #define OD_LOCAL_FOLD OD_LOCAL_STATE
 #endif
 
-// Minimum resident blocks per SM for the phase kernels (register caps).
+// Threads per block of the phase kernels (one kernel per warp).
+#ifndef OD_BLOCK
+#define OD_BLOCK 128
+#endif
+
+// Minimum resident blocks per SM for the phase kernels (register caps), in
+// 128-thread blocks.
 #ifndef OD_MINB_FRONT
 #define OD_MINB_FRONT 16
 #endif
@@ -133,10 +139,10 @@ __device__ __forceinline__ void kstate_store(KState *g, const KState &S) {
 }
 
 
-__global__ void __launch_bounds__(128, OD_MINB_FRONT) k_front(DecompArgs a);
-__global__ void __launch_bounds__(128, OD_MINB_LOWER) k_lower(DecompArgs a);
-__global__ void __launch_bounds__(128, OD_MINB_FOLD) k_fold(DecompArgs a);
-__global__ void __launch_bounds__(128, OD_MINB_EMIT) k_emit(DecompArgs a);
+__global__ void __launch_bounds__(OD_BLOCK, OD_MINB_FRONT * 128 / OD_BLOCK) k_front(DecompArgs a);
+__global__ void __launch_bounds__(OD_BLOCK, OD_MINB_LOWER * 128 / OD_BLOCK) k_lower(DecompArgs a);
+__global__ void __launch_bounds__(OD_BLOCK, OD_MINB_FOLD * 128 / OD_BLOCK) k_fold(DecompArgs a);
+__global__ void __launch_bounds__(OD_BLOCK, OD_MINB_EMIT * 128 / OD_BLOCK) k_emit(DecompArgs a);
 
 // ------------------------------------------------------------------ generator
 struct GenArgs {

@@ -52,7 +52,7 @@ __device__ __noinline__ Collected warp_collect(const DecompArgs &a, u32 lbeg, u3
     return c;
 }
 
-__global__ void __launch_bounds__(128, OD_MINB_FRONT) k_front(DecompArgs a) {
+__global__ void __launch_bounds__(OD_BLOCK, OD_MINB_FRONT * 128 / OD_BLOCK) k_front(DecompArgs a) {
     Slot0 sl;
     u64 *names = nullptr; // this lane's name set, zeroed below by the whole warp
     u32 names_cap = 0;

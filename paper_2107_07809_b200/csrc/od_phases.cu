@@ -5,7 +5,7 @@
 
 namespace od {
 
-__global__ void __launch_bounds__(128, OD_MINB_LOWER) k_lower(DecompArgs a) {
+__global__ void __launch_bounds__(OD_BLOCK, OD_MINB_LOWER * 128 / OD_BLOCK) k_lower(DecompArgs a) {
     Slot0 sl;
     if (!dk_slot(a, &sl))
         return;
@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(128, OD_MINB_LOWER) k_lower(DecompArgs a) {
 #endif
 }
 
-__global__ void __launch_bounds__(128, OD_MINB_FOLD) k_fold(DecompArgs a) {
+__global__ void __launch_bounds__(OD_BLOCK, OD_MINB_FOLD * 128 / OD_BLOCK) k_fold(DecompArgs a) {
     Slot0 sl;
     if (!dk_slot(a, &sl))
         return;
@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(128, OD_MINB_FOLD) k_fold(DecompArgs a) {
 __device__ __noinline__ void emit_one(const DecompArgs &a, const Slot0 &sl, const uint4 **cs, uint4 **cd,
                                       u32 *cn);
 
-__global__ void __launch_bounds__(128, OD_MINB_EMIT) k_emit(DecompArgs a) {
+__global__ void __launch_bounds__(OD_BLOCK, OD_MINB_EMIT * 128 / OD_BLOCK) k_emit(DecompArgs a) {
     Slot0 sl;
     const uint4 *cs = nullptr; // this lane's kernel text in its arena ...
     uint4 *cd = nullptr;       // ... and its place in the stage
