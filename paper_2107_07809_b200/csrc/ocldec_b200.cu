@@ -1428,12 +1428,15 @@ void reset_stats(ocldec_b200_session *s) {
 }
 
 // Splits a host listing into chunks of < ~1 GiB at ".kernel" line starts.
-// The first chunk is `first` bytes (its load is the one copy nothing hides);
-// the rest is cut into as few chunks of at most `target` bytes as fit, of
-// about equal size (every phase launch ends in a tail).
+// As few chunks of at most `target` bytes as fit, of about equal size (every
+// phase launch ends in a tail); with first > 0 the first chunk is `first`
+// bytes and the rest is balanced.
 std::vector<u64> host_chunks(const char *p, size_t len, size_t target, size_t first) {
     std::vector<u64> starts{0};
-    if (len > first) {
+    if (!first) {
+        const size_t nch = len ? (len + target - 1) / target : 1;
+        first = target = (len + nch - 1) / nch;
+    } else if (len > first) {
         const size_t rem = len - first;
         const size_t nch = (rem + target - 1) / target;
         target = (rem + nch - 1) / nch;
@@ -1564,7 +1567,12 @@ int run_host_listing_at(ocldec_b200_session *s, const char *listing, size_t len,
     } else {
         s->only_set = false;
     }
-    std::vector<u64> starts = host_chunks(listing, len, target, std::max<size_t>(target / 4, 1));
+    // equal chunks (0); OCLDEC_B200_FIRST_CHUNK=bytes makes the first one
+    // that size instead (a smaller first load, one more chunk: measured slower)
+    size_t first = 0;
+    if (const char *e = getenv("OCLDEC_B200_FIRST_CHUNK"))
+        first = strtoull(e, nullptr, 0);
+    std::vector<u64> starts = host_chunks(listing, len, target, first);
     const size_t nch = starts.size();
     auto cb = [&](size_t c) { return starts[c]; };
     auto ce = [&](size_t c) { return c + 1 < nch ? starts[c + 1] : (u64)len; };
