@@ -1,0 +1,48 @@
+"""CPU tests of bench.py's host logic: the chunking of the device run (equal
+chunks at kernel boundaries, as few as fit under the cap) and the reference
+arm's JSON line contract."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+
+
+@pytest.mark.parametrize("total,cap,want", [(19_160_000_000, 3 << 30, 6), (10_000, 3 << 30, 1),
+                                            (7_000_000, 1_000_000, 7), (7_000_001, 1_000_000, 8)])
+def test_chunks_equal_and_capped(total, cap, want):
+    offs = np.linspace(0, total, 4001).astype(np.int64)  # 4000 kernels of equal size
+    starts = bench.chunk_starts_from(offs, cap)
+    assert starts[0] == 0 and len(starts) == want
+    assert all(s in set(offs.tolist()) for s in starts)  # kernel boundaries only
+    sizes = np.diff(starts + [total])
+    kernel = total // 4000 + 1
+    assert sizes.max() <= cap + kernel
+    assert sizes.max() - sizes.min() <= 2 * kernel + (total // want) // 50
+
+
+def test_reference_arm_line(tmp_path):
+    """--impl reference prints one JSON line with the contract's keys (a tiny
+    sample; the full arm runs for minutes)."""
+    from oracle import oracle as O
+    if not O.available():
+        pytest.skip("oracle not built")
+    code = ("import sys, bench; sys.argv=['bench.py','--impl','reference','--steps','1','--warmup','0'];"
+            "bench.run_reference = bench.run_reference; args = bench.parse();"
+            "import oracle.oracle as O; orig = O.decompile_batch;"
+            "O.decompile_batch = lambda c, o, n, **k: orig(c, o[:3], min(n, 2), **k);"
+            "bench.run_reference(args)")
+    p = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    for key in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["cpu_baseline"]["kind"] == "reference"
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
