@@ -113,7 +113,7 @@ __device__ __forceinline__ bool dk_slot(const DecompArgs &a, Slot0 *o) {
 #define OD_MINB_LOWER 16
 #endif
 #ifndef OD_MINB_FOLD
-#define OD_MINB_FOLD 12
+#define OD_MINB_FOLD 10
 #endif
 #ifndef OD_MINB_EMIT
 #define OD_MINB_EMIT 16
