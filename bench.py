@@ -135,45 +135,64 @@ def chunk_starts_from(offsets, target=CHUNK_BYTES):
     return starts
 
 
+def cpu_model():
+    """CPU model string of this host (/proc/cpuinfo)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def _ref_sample(cfg, seconds, nthreads, cap):
+    """A deterministic sample (kernels 0..n-1 of the config's corpus at its
+    bench seed) sized for about `seconds` of reference work on nthreads.
+    Inputs come from the oracle library's host build of the generator, so
+    the CPU arms never load the product library."""
+    from oracle import oracle as O
+    n = 64 if cfg in ("C2", "C3", "C4") else 2
+    listing, offs, ni = O.generate_corpus(cfg, n, seed=SEEDS[cfg])
+    secs, instrs, _, _ = O.decompile_batch(listing, offs, nthreads)
+    per = max(ni / n, 1)
+    n2 = max(n, min(int(instrs / max(secs, 1e-6) * seconds / per), cap))
+    listing, offs, ni = O.generate_corpus(cfg, n2, seed=SEEDS[cfg])
+    return listing, offs, ni, n2
+
+
 def cpu_baseline(cfg, seconds, nthreads):
     """The reference (oracle/_ref, built from its sources) on host cores over a
-    bounded deterministic sample of the same corpus."""
+    bounded deterministic sample of the same corpus: all host threads, then
+    one thread on a smaller sample (SURVEY §8(d) CPU-baseline recipe)."""
     from oracle import oracle as O
-    import paper_2107_07809_b200 as P
-    # probe, then size the sample for ~`seconds` of CPU work
-    n = 64 if cfg in ("C2", "C3", "C4") else 2
-    k0 = 0
-    listing, offs, ni = P.generate_corpus(cfg, n, seed=SEEDS[cfg], k0=k0)
+    listing, offs, ni, n2 = _ref_sample(cfg, seconds, nthreads, 400_000)
     secs, instrs, _, _ = O.decompile_batch(listing, offs, nthreads)
-    rate = instrs / max(secs, 1e-6)
-    want = int(rate * seconds)
-    per = max(ni / n, 1)
-    n2 = max(n, min(int(want / per), 400_000))
-    listing, offs, ni = P.generate_corpus(cfg, n2, seed=SEEDS[cfg], k0=k0)
-    secs, instrs, _, _ = O.decompile_batch(listing, offs, nthreads)
+    l1, o1, _, n1 = _ref_sample(cfg, max(2.0, seconds / 4), 1, 20_000)
+    s1, i1, _, _ = O.decompile_batch(l1, o1, 1)
     return {"value": instrs / secs, "unit": "instr/s", "cores": nthreads, "kind": "reference",
+            "cpu_model": cpu_model(), "nproc": os.cpu_count(),
             "sample": f"{n2} kernels of {cfg} (k=0..{n2 - 1}), {instrs} instrs, {len(listing)} bytes, "
                       f"{secs:.1f} s wall, decompile_listing per kernel on {nthreads} pthreads",
-            "seconds": secs, "instructions": instrs, "in_bytes": len(listing)}
+            "seconds": secs, "instructions": instrs, "in_bytes": len(listing),
+            "one_thread": {"value": i1 / s1, "unit": "instr/s", "cores": 1,
+                           "sample": f"{n1} kernels of {cfg} (k=0..{n1 - 1}), {i1} instrs, {s1:.1f} s wall"}}
 
 
 def run_reference(args):
     """--impl reference: the reference's own CPU implementation timed on the
-    host cores, same metric/config; rank 0 only."""
+    host cores, same metric/config; rank 0 only.  Loads only
+    oracle/_ref/libocldec_ref.so (the reference compiled from its sources,
+    plus the host build of the input generator): never the product."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from oracle import oracle as O
-    import paper_2107_07809_b200 as P
     nthreads = os.cpu_count() or 1
     cfg = args.config
     # one step = a bounded sample (~6 s on the box's cores) of the config
-    n = 64
-    listing, offs, ni = P.generate_corpus(cfg, n, seed=SEEDS[cfg])
-    secs, instrs, _, _ = O.decompile_batch(listing, offs, nthreads)
-    per = max(ni / n, 1)
-    n_step = max(n, min(int(instrs / max(secs, 1e-6) * 6.0 / per), 200_000))
-    listing, offs, ni = P.generate_corpus(cfg, n_step, seed=SEEDS[cfg])
+    listing, offs, ni, n_step = _ref_sample(cfg, 6.0, nthreads, 200_000)
     for _ in range(args.warmup):
         O.decompile_batch(listing, offs, nthreads)
     tot_s = tot_i = 0.0
@@ -190,7 +209,7 @@ def run_reference(args):
         "data": "synthetic (counter-based generator)",
         "config": {"workload": f"{cfg} sample on host cores", "kernels_per_step": n_step},
         "cpu_baseline": {"value": value, "unit": "instr/s", "cores": nthreads, "kind": "reference",
-                         "sample": sample},
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": "instr/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 

@@ -55,6 +55,14 @@ def lib():
                                      ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
         L.ref_make_nest.argtypes = [ctypes.c_uint64, ctypes.POINTER(ctypes.c_int)]
         L.ref_make_nest.restype = ctypes.c_void_p
+        L.ref_gen_host.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                   ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
+                                   ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
+        L.ref_gen_host.restype = ctypes.c_int64
+        L.ref_decompile_par.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_size_t,
+                                        ctypes.c_size_t, ctypes.c_int, ctypes.c_int,
+                                        ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_size_t)]
+        L.ref_decompile_par.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -90,27 +98,7 @@ def _take(ptr: int, n: int) -> bytes:
     return ctypes.string_at(ptr, n)
 
 
-def decompile(listing: bytes, fold_local_size: bool = False, only_kernel: Optional[bytes] = None,
-              abi_map: Optional[bytes] = None, dump_cfg: bool = False,
-              dump_regions: bool = False, reduction: bool = False) -> RefResult:
-    if isinstance(listing, str):
-        listing = listing.encode()
-    L = lib()
-    out = ctypes.c_void_p()
-    n = ctypes.c_size_t()
-    if isinstance(abi_map, str):
-        abi_map = abi_map.encode()
-    dumps = int(dump_cfg) | (2 if dump_regions else 0) | (4 if reduction else 0)
-    if dumps:
-        L.ref_decompile_ex(listing, len(listing), int(fold_local_size), only_kernel, abi_map,
-                           len(abi_map) if abi_map is not None else 0, dumps, ctypes.byref(out), ctypes.byref(n))
-    elif abi_map is None:
-        L.ref_decompile(listing, len(listing), int(fold_local_size), only_kernel, ctypes.byref(out), ctypes.byref(n))
-    else:
-        L.ref_decompile_abi(listing, len(listing), int(fold_local_size), only_kernel, abi_map, len(abi_map),
-                            ctypes.byref(out), ctypes.byref(n))
-    blob = _take(out.value, n.value)
-    L.ref_free(out)
+def _parse(blob: bytes) -> "RefResult":
     res = RefResult()
     pos = 0
     while pos < len(blob):
@@ -152,6 +140,69 @@ def decompile(listing: bytes, fold_local_size: bool = False, only_kernel: Option
         else:  # pragma: no cover
             raise ValueError(f"bad oracle record {head!r}")
     return res
+
+
+def decompile(listing: bytes, fold_local_size: bool = False, only_kernel: Optional[bytes] = None,
+              abi_map: Optional[bytes] = None, dump_cfg: bool = False,
+              dump_regions: bool = False, reduction: bool = False) -> RefResult:
+    if isinstance(listing, str):
+        listing = listing.encode()
+    L = lib()
+    out = ctypes.c_void_p()
+    n = ctypes.c_size_t()
+    if isinstance(abi_map, str):
+        abi_map = abi_map.encode()
+    dumps = int(dump_cfg) | (2 if dump_regions else 0) | (4 if reduction else 0)
+    if dumps:
+        L.ref_decompile_ex(listing, len(listing), int(fold_local_size), only_kernel, abi_map,
+                           len(abi_map) if abi_map is not None else 0, dumps, ctypes.byref(out), ctypes.byref(n))
+    elif abi_map is None:
+        L.ref_decompile(listing, len(listing), int(fold_local_size), only_kernel, ctypes.byref(out), ctypes.byref(n))
+    else:
+        L.ref_decompile_abi(listing, len(listing), int(fold_local_size), only_kernel, abi_map, len(abi_map),
+                            ctypes.byref(out), ctypes.byref(n))
+    blob = _take(out.value, n.value)
+    L.ref_free(out)
+    return _parse(blob)
+
+
+def decompile_par(listing: bytes, kernel_starts, nthreads: int = 0, per: int = 64,
+                  fold_local_size: bool = False) -> RefResult:
+    """decompile_listing of the whole listing, computed in parallel over slices
+    of `per` kernels (ref_driver.cpp ref_decompile_par): same kernels,
+    diagnostics (listing-global lines) and combined_source as decompile()."""
+    import numpy as np
+    L = lib()
+    ks = np.ascontiguousarray(kernel_starts, dtype=np.uint64)
+    out = ctypes.c_void_p()
+    n = ctypes.c_size_t()
+    L.ref_decompile_par(listing, len(listing), ks.ctypes.data, len(ks), per, nthreads or (os.cpu_count() or 1),
+                        int(fold_local_size), ctypes.byref(out), ctypes.byref(n))
+    blob = _take(out.value, n.value)
+    L.ref_free(out)
+    return _parse(blob)
+
+
+SHAPES = {"C1": 1, "C2": 2, "C3": 3, "C4": 4, "C5": 5}
+
+
+def generate_corpus(shape, count: int, seed: int = 1, k0: int = 0, stress: bool = False, nthreads: int = 0):
+    """The synthetic corpus (od_gen.cuh, host build linked into the oracle
+    library): byte-identical to paper_2107_07809_b200.generate_corpus, without
+    loading the product library.  Returns (listing, offsets[count+1], instrs)."""
+    import numpy as np
+    L = lib()
+    shape = SHAPES.get(shape, shape) if isinstance(shape, str) else shape
+    nt = nthreads or min(16, os.cpu_count() or 1)
+    offs = np.zeros(count + 1, dtype=np.uint64)
+    ni = ctypes.c_uint64()
+    need = L.ref_gen_host(shape, int(stress), seed, k0, count, None, 0, offs.ctypes.data, ctypes.byref(ni), nt)
+    buf = ctypes.create_string_buffer(int(need) + 1)
+    n = L.ref_gen_host(shape, int(stress), seed, k0, count, ctypes.cast(buf, ctypes.c_void_p), need + 1,
+                       offs.ctypes.data, ctypes.byref(ni), nt)
+    if n < 0:
+        raise RuntimeError("oracle corpus generation failed")
+    return buf.raw[:n], offs, int(ni.value)
 
 
 def corpus():

@@ -182,6 +182,49 @@ void *batch_worker(void *p) {
     return nullptr;
 }
 
+struct ParSlice {
+    const char *text;
+    size_t len;
+    int fold_local_size;
+    std::string kernels; // "K" records
+    std::string diags;   // "D" records, lines shifted to the whole listing
+    std::string combined;
+    uint64_t line_base = 0;
+};
+
+struct ParJob {
+    std::vector<ParSlice> *slices;
+    std::atomic<size_t> *next;
+};
+
+void *par_worker(void *p) {
+    auto *job = static_cast<ParJob *>(p);
+    for (;;) {
+        size_t i = job->next->fetch_add(1);
+        if (i >= job->slices->size())
+            break;
+        ParSlice &sl = (*job->slices)[i];
+        ocldec::DecompileOptions opts;
+        opts.folds.fold_local_size = sl.fold_local_size != 0;
+        ocldec::DecompileResult res = ocldec::decompile_listing(std::string(sl.text, sl.len), opts);
+        for (const auto &k : res.kernels) {
+            sl.kernels += "K " + std::to_string(int(k.failed)) + " " + std::to_string(int(k.structured)) +
+                          " " + std::to_string(k.body.fallback_count) + " " + std::to_string(k.name.size()) +
+                          " " + std::to_string(k.source.size()) + "\n";
+            sl.kernels += k.name;
+            sl.kernels += k.source;
+        }
+        for (const auto &d : res.diagnostics.all()) {
+            const uint64_t line = d.line > 0 ? uint64_t(d.line) + sl.line_base : uint64_t(d.line);
+            sl.diags += "D " + std::to_string(int(d.severity)) + " " + std::to_string(line) + " " +
+                        std::to_string(d.message.size()) + "\n";
+            sl.diags += d.message;
+        }
+        sl.combined = res.combined_source();
+    }
+    return nullptr;
+}
+
 } // namespace
 
 extern "C" {
@@ -274,6 +317,66 @@ char *ref_make_nest(uint64_t seed, int *conditionals) {
     if (conditionals)
         *conditionals = spec.conditionals;
     return dup_out(spec.listing, nullptr);
+}
+
+
+// decompile_listing over a listing whose kernel sections start at the byte
+// offsets kstart[0..nk) (each a ".kernel" line; kstart[0] may follow a
+// preamble that split_kernels ignores), computed in parallel: the sections
+// are independent (decompiler.cpp:55-101), so slices of `per` kernels are
+// decompiled on nthreads pthreads (1 GiB stacks) and joined as
+// combined_source joins them (decompiler.cpp:105-115), diagnostic lines
+// shifted by each slice's line offset.  Same serialization as ref_decompile
+// (no dumps).  Only for listings without split_kernels errors.
+int ref_decompile_par(const char *listing, size_t len, const uint64_t *kstart, size_t nk, size_t per,
+                      int nthreads, int fold_local_size, char **out, size_t *out_len) {
+    if (per < 1)
+        per = 1;
+    if (nthreads < 1)
+        nthreads = 1;
+    std::vector<ParSlice> slices;
+    uint64_t line = 0, pos = 0;
+    for (size_t k0 = 0; k0 < nk; k0 += per) {
+        const uint64_t a = k0 == 0 ? 0 : kstart[k0];
+        const uint64_t b = k0 + per < nk ? kstart[k0 + per] : len;
+        for (; pos < a; ++pos)
+            line += listing[pos] == '\n';
+        ParSlice sl;
+        sl.text = listing + a;
+        sl.len = b - a;
+        sl.fold_local_size = fold_local_size;
+        sl.line_base = line;
+        slices.push_back(std::move(sl));
+    }
+    std::atomic<size_t> next{0};
+    std::vector<pthread_t> threads(static_cast<size_t>(nthreads));
+    std::vector<ParJob> jobs(static_cast<size_t>(nthreads));
+    pthread_attr_t attr;
+    pthread_attr_init(&attr);
+    pthread_attr_setstacksize(&attr, kBigStack);
+    for (int t = 0; t < nthreads; ++t) {
+        jobs[size_t(t)] = ParJob{&slices, &next};
+        pthread_create(&threads[size_t(t)], &attr, par_worker, &jobs[size_t(t)]);
+    }
+    for (int t = 0; t < nthreads; ++t)
+        pthread_join(threads[size_t(t)], nullptr);
+    pthread_attr_destroy(&attr);
+    std::string ser, combined;
+    for (const auto &sl : slices)
+        ser += sl.kernels;
+    for (const auto &sl : slices)
+        ser += sl.diags;
+    for (const auto &sl : slices) {
+        if (sl.combined.empty())
+            continue;
+        if (!combined.empty())
+            combined += "\n";
+        combined += sl.combined;
+    }
+    ser += "C " + std::to_string(combined.size()) + "\n";
+    ser += combined;
+    *out = dup_out(ser, out_len);
+    return 0;
 }
 
 } // extern "C"

@@ -34,13 +34,18 @@ def test_reference_arm_line(tmp_path):
     if not O.available():
         pytest.skip("oracle not built")
     code = ("import sys, bench; sys.argv=['bench.py','--impl','reference','--steps','1','--warmup','0'];"
-            "bench.run_reference = bench.run_reference; args = bench.parse();"
-            "import oracle.oracle as O; orig = O.decompile_batch;"
-            "O.decompile_batch = lambda c, o, n, **k: orig(c, o[:3], min(n, 2), **k);"
-            "bench.run_reference(args)")
+            "args = bench.parse(); orig = bench._ref_sample;"
+            "bench._ref_sample = lambda cfg, s, n, cap: orig(cfg, 0.01, min(n, 2), 64);"
+            "bench.run_reference(args);"
+            "maps = open('/proc/self/maps').read();"
+            "print('PRODUCT_LOADED' if 'libocldec_b200' in maps else 'PRODUCT_NOT_LOADED',"
+            " 'ORACLE_LOADED' if 'libocldec_ref' in maps else 'ORACLE_NOT_LOADED', file=sys.stderr)")
     p = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stderr[-2000:]
     line = json.loads(p.stdout.strip().splitlines()[-1])
+    # the reference arm times the reference alone: the product library is
+    # never loaded into that process
+    assert "PRODUCT_NOT_LOADED" in p.stderr and "ORACLE_LOADED" in p.stderr, p.stderr[-500:]
     for key in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
                 "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
         assert key in line, key

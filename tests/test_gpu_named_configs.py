@@ -1,0 +1,92 @@
+"""Parity at the named configs' bench seeds.
+
+The whole C2 and C3 corpora the bench names (10,000 kernels each, seeds
+0x210707809C2 / 0x210707809C3) and a 128-kernel C5 sample spread over the
+1M-kernel index range (seed 0x210707809C5) are decompiled on the GPU through
+the C ABI and compared with the reference (oracle/_ref, the reference
+compiled from its own sources) kernel by kernel: source bytes, name,
+failed / structured flags, fallback count, the diagnostics list (severity,
+listing-global line, message) and combined_source.  Bit-exact: the path is
+byte and integer work.
+
+The oracle runs decompile_listing over slices of the listing in parallel
+(ref_decompile_par); slices are independent by construction
+(decompiler.cpp:55-101) and their results are joined exactly as
+combined_source joins kernels (decompiler.cpp:105-115).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2107_07809_b200 as P
+from oracle import oracle as O
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not O.available(), reason="oracle not built")]
+
+SEEDS = {"C2": 0x210707809C2, "C3": 0x210707809C3, "C5": 0x210707809C5}
+
+
+def _compare(listing, kstarts, res):
+    ref = O.decompile_par(listing, kstarts)
+    assert len(res.kernels) == len(ref.kernels)
+    for i, (g, r) in enumerate(zip(res.kernels, ref.kernels)):
+        assert g.name.encode() == r.name, i
+        assert (g.failed, g.structured, g.fallback_count) == (r.failed, r.structured, r.fallback_count), \
+            (i, g.name)
+        assert g.source.encode("utf-8", "surrogateescape") == r.source, (i, g.name)
+    got_d = [(d.severity, d.line, d.message.encode("utf-8", "surrogateescape")) for d in res.diagnostics]
+    want_d = [(d.severity, d.line, d.message) for d in ref.diagnostics]
+    assert got_d == want_d
+    assert res.combined == ref.combined
+    return ref
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3"])
+def test_full_named_corpus_vs_oracle(cfg):
+    listing, offs, ni = O.generate_corpus(cfg, 10_000, seed=SEEDS[cfg])
+    # the product's generator builds the same bytes (the bench corpus)
+    plisting, poffs, pni = P.generate_corpus(cfg, 10_000, seed=SEEDS[cfg])
+    assert plisting == listing and pni == ni
+    res = P.decompile_listing(listing)
+    assert sum(k.instructions for k in res.kernels) == ni
+    _compare(listing, offs[:-1], res)
+
+
+def _c5_sample(n=128, span=1_000_000):
+    ks = [int(i * (span - 1) // (n - 1)) for i in range(n)]
+    parts, starts, ni, pos = [], [], 0, 0
+    for k in ks:
+        b, _, i = O.generate_corpus("C5", 1, seed=SEEDS["C5"], k0=k)
+        starts.append(pos)
+        parts.append(b)
+        pos += len(b)
+        ni += i
+    return b"".join(parts), np.array(starts, dtype=np.uint64), ni, ks
+
+
+def test_c5_sample_vs_oracle():
+    """128 kernels of the 1M-kernel C5 corpus, k spread evenly over
+    [0, 1M): long (~10k-instruction) deep-CFG kernels with 64-bit pairs."""
+    listing, starts, ni, ks = _c5_sample()
+    assert ni > 128 * 7000
+    res = P.decompile_listing(listing)
+    assert sum(k.instructions for k in res.kernels) == ni
+    ref = _compare(listing, starts, res)
+    assert sum(k.structured for k in ref.kernels) > 0
+
+
+def test_c5_device_generated_sample_matches_host():
+    """The device generator (the bench's C5 input) builds the sampled kernels
+    byte for byte as the host generator the oracle consumed."""
+    s = P.Session(0)
+    try:
+        for k in (0, 499_999, 999_999):
+            d_buf, n, d_offs, ni = s.generate("C5", 1, seed=SEEDS["C5"], k0=k)
+            host = bytearray(n)
+            import ctypes
+            P.copy(ctypes.addressof((ctypes.c_char * n).from_buffer(host)), d_buf, n)
+            want, _, wni = O.generate_corpus("C5", 1, seed=SEEDS["C5"], k0=k)
+            assert bytes(host) == want and ni == wni
+    finally:
+        s.close()
