@@ -127,9 +127,10 @@ __global__ void k_nl_write(const u8 *__restrict__ base, u64 len, u32 mis, const 
 // ------------------------------------------------------------------ P1b
 // Thread per line: comment strip + rtrim + first-word kind.
 // Also sizes the decode pools: an upper bound of the line's operands (one
-// more than its runs of ',' / ' ' / '\t': every token after the first follows
-// such a run) and of its labels (its ':' count), over the raw line, which
-// contains whatever the comment strip keeps.
+// more than its runs of ',' / isspace bytes, the decoder's own separator
+// predicate c_space: every token after the first follows such a run) and of
+// its labels (its ':' count), over the raw line, which contains whatever the
+// comment strip keeps.
 __global__ void k_classify(const u8 *__restrict__ t, u64 len, const u32 *__restrict__ nlpos,
                            u32 nlf, u32 nlines, LineRec *lines, u32 *complex_bytes, u32 *ops_ub,
                            u32 *labs_ub) {
@@ -160,7 +161,7 @@ __global__ void k_classify(const u8 *__restrict__ t, u64 len, const u32 *__restr
         bool prev = false;
         for (u32 i = b; i < e; ++i) {
             const u8 c = t[i];
-            const bool sep = c == ',' || c == ' ' || c == '\t';
+            const bool sep = c == ',' || c_space(c);
             runs += sep && !prev;
             prev = sep;
             colons += c == ':';
@@ -243,7 +244,7 @@ constexpr u32 kDecodeStage = 16384;
 __global__ void __launch_bounds__(256) k_decode(const u8 *__restrict__ t, u64 len, const u32 *__restrict__ nlpos,
                                                 u32 nlf, u32 nlines, const LineRec *__restrict__ lines,
                                                 LineIns *lins, const u32 *ops_off, const u32 *labs_off,
-                                                Opnd *ops, Label *labs) {
+                                                Opnd *ops, Label *labs, u32 ops_total, u32 *overflow) {
     __shared__ RootTable rt;
     __shared__ __align__(16) u8 stage[kDecodeStage];
     for (u32 i = threadIdx.x; i < sizeof(RootTable) / 4; i += blockDim.x)
@@ -284,8 +285,12 @@ __global__ void __launch_bounds__(256) k_decode(const u8 *__restrict__ t, u64 le
     const u8 *tb = in_stage ? stage - ab : t;
     LineIns li;
     const u32 oo = ops_off[l], lo = labs_off[l];
-    const u32 cap = (l + 1 < nlines ? ops_off[l + 1] : 0xffffffffu) - oo;
+    const u32 cap = (l + 1 < nlines ? ops_off[l + 1] : ops_total) - oo;
     decode_line(tb, Span{L.off, L.len}, &rt, &li, ops + oo, cap, labs + lo);
+    if (li.nops > cap) { // k_classify's bound is exact-or-above by construction
+        atomicOr(overflow, 1u);
+        li.nops = (u16)cap;
+    }
     li.op_start = oo;
     li.lab_start = lo;
     lins[l] = li;
@@ -434,24 +439,33 @@ struct ClsStore {
 };
 
 // ------------------------------------------------------------------ P4b
+struct U64Val {
+    u64 v;
+    __device__ static U64Val shfl_up(U64Val x, int d) { return U64Val{__shfl_up_sync(0xffffffffu, x.v, d)}; }
+};
+struct AddU64 {
+    __device__ U64Val operator()(U64Val a, U64Val b) const { return U64Val{a.v + b.v}; }
+};
+// Output lengths (+1 for the separator) scanned in u64: a chunk's combined
+// output may pass 4 GiB (inline-asm fallback lines expand 2-4x).
 struct OutLenLoad {
     const KRes *res;
-    __device__ SU32 operator()(u64 i) const {
-        u32 n = res[i].status == KS_OK ? res[i].out_len : 0;
-        return SU32{n ? n + 1 : 0};
+    __device__ U64Val operator()(u64 i) const {
+        u64 n = res[i].status == KS_OK ? res[i].out_len : 0;
+        return U64Val{n ? n + 1 : 0};
     }
 };
 struct OutOffStore {
     u64 *off;
-    __device__ void operator()(u64 i, SU32 ex, SU32) const { off[i] = ex.v; }
+    __device__ void operator()(u64 i, U64Val ex, U64Val) const { off[i] = ex.v; }
 };
 
 // Warp per kernel: staging -> combined output (+ the "\n" separator that
 // combined_source puts between non-empty sources).
 __global__ void k_gather(const KRes *__restrict__ res, const u64 *__restrict__ off, u32 nk,
                          const u8 *__restrict__ stage, u8 *out, u64 out_base, u64 total) {
-    u32 warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    u32 lane = threadIdx.x & 31;
+    const u64 warp = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const u32 lane = threadIdx.x & 31;
     if (warp >= nk)
         return;
     const KRes r = res[warp];
@@ -465,13 +479,6 @@ __global__ void k_gather(const KRes *__restrict__ res, const u64 *__restrict__ o
         d[r.out_len] = '\n';
 }
 
-struct U64Val {
-    u64 v;
-    __device__ static U64Val shfl_up(U64Val x, int d) { return U64Val{__shfl_up_sync(0xffffffffu, x.v, d)}; }
-};
-struct AddU64 {
-    __device__ U64Val operator()(U64Val a, U64Val b) const { return U64Val{a.v + b.v}; }
-};
 struct U64Load {
     const u64 *p;
     __device__ U64Val operator()(u64 i) const { return U64Val{p[i]}; }
@@ -492,6 +499,18 @@ struct U32SumLoad64 {
     const u32 *p;
     __device__ U64Val operator()(u64 i) const { return U64Val{p[i]}; }
 };
+
+// Diagnostic spans of a chunk packed into one buffer (one D2H instead of a
+// copy per span): warp per span, spans[i] = {src offset, length, dst offset}.
+__global__ void k_span_gather(const u8 *__restrict__ t, const uint4 *__restrict__ spans, u32 n, u8 *out) {
+    const u64 w = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (w >= n)
+        return;
+    const uint4 sp = spans[w];
+    const u64 dst = (u64)sp.z | ((u64)sp.w << 32);
+    for (u32 i = threadIdx.x & 31; i < sp.y; i += 32)
+        out[dst + i] = t[(u64)sp.x + i];
+}
 
 // ================================================================== host side
 struct DevBuf {
@@ -874,7 +893,7 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
         return 0;
     if (len >= 0xf0000000ull) {
         g_err = "chunk larger than 3.75 GiB";
-        return -1;
+        return -5; // the host path retries with smaller chunks
     }
     const u32 mis = (u32)((uintptr_t)t & 15);
     const u64 span = len + mis;
@@ -968,7 +987,8 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     if (ensure(s->ops, (pools[0] + 1ull) * sizeof(Opnd)) || ensure(s->labs, (pools[1] + 1ull) * sizeof(Label)))
         return -3;
     k_decode<<<lg, lb, 0, st>>>(t, len, P<u32>(s->nlpos), nlf, nlines, P<LineRec>(s->lines), P<LineIns>(s->lins),
-                                P<u32>(s->ops_off), P<u32>(s->labs_off), P<Opnd>(s->ops), P<Label>(s->labs));
+                                P<u32>(s->ops_off), P<u32>(s->labs_off), P<Opnd>(s->ops), P<Label>(s->labs),
+                                pools[0], cnt + 3);
     s->stats.total_launches++;
     CK(cudaGetLastError());
     CK(cudaEventRecord(s->ev[2], st));
@@ -1146,7 +1166,7 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     std::vector<KRes> hr(nk);
     u32 scale = 1;
     std::vector<KSize> zs;
-    for (int attempt = 0; attempt < 6; ++attempt) {
+    for (int attempt = 0;; ++attempt) {
         if (d2h_sync(s, hr.data(), a.res, (u64)nk * sizeof(KRes)))
             return -3;
         std::vector<u32> redo;
@@ -1158,6 +1178,10 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
             }
         if (redo.empty())
             break;
+        if (attempt == 8) { // arenas 4^8 x the sized budget: never silently drop a kernel
+            g_err = "internal error: " + std::to_string(redo.size()) + " kernels outgrew every arena retry";
+            return -3;
+        }
         s->stats.retried += redo.size();
         if (stage_full) {
             u64 top = 0;
@@ -1227,12 +1251,18 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     }
     CK(cudaEventRecord(s->ev[3], st));
     // P4b offsets + gather
-    if (scan_exclusive(s, nk, SU32{0}, AddU32{}, OutLenLoad{a.res}, OutOffStore{P<u64>(s->outoff)},
-                       reinterpret_cast<SU32 *>(cnt + 10)))
+    if (scan_exclusive(s, nk, U64Val{0}, AddU64{}, OutLenLoad{a.res}, OutOffStore{P<u64>(s->outoff)},
+                       reinterpret_cast<U64Val *>(cnt + 10)))
         return -3;
-    u32 tot = 0;
-    if (d2h_sync(s, &tot, cnt + 10, 4))
+    u32 cblk[16]; // the chunk's counters: [3] decode overflow, [10..11] output total (u64)
+    if (d2h_sync(s, cblk, cnt, sizeof cblk))
         return -3;
+    if (cblk[3]) {
+        g_err = "internal error: an operand pool bound was exceeded";
+        return -3;
+    }
+    u64 tot = 0;
+    memcpy(&tot, cblk + 10, 8);
     // tot = sum(len + 1) over non-empty; the last separator is dropped
     u64 chunk_bytes = tot ? tot - 1 : 0;
     u64 base = out_base;
@@ -1246,7 +1276,7 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     }
     if (ensure_keep(s->out, base + chunk_bytes + 16, base, st))
         return -3;
-    k_gather<<<(nk * 32 + 255) / 256, 256, 0, st>>>(a.res, P<u64>(s->outoff), nk, P<u8>(s->stage),
+    k_gather<<<(u32)(((u64)nk * 32 + 255) / 256), 256, 0, st>>>(a.res, P<u64>(s->outoff), nk, P<u8>(s->stage),
                                                      P<u8>(s->out), base, base + chunk_bytes);
     s->stats.total_launches++;
     CK(cudaGetLastError());
@@ -1274,11 +1304,40 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
                 return -3;
         }
     }
-    auto span_text = [&](u32 off, u32 n, std::string *out) -> int {
-        out->resize(n);
-        if (n)
-            CK(cudaMemcpy(&(*out)[0], t + off, n, cudaMemcpyDeviceToHost));
-        return 0;
+    // the kept records' listing spans, packed on the device, one D2H
+    std::vector<uint4> spans;
+    u64 span_bytes = 0;
+    auto add_span = [&](u32 off, u32 n) {
+        if (n) {
+            spans.push_back(make_uint4(off, n, (u32)span_bytes, (u32)(span_bytes >> 32)));
+            span_bytes += n;
+        }
+    };
+    for (u32 k = 0; k < nk; ++k)
+        if (hr[k].status == KS_OK || hr[k].status == KS_FAILED)
+            for (u32 q = 0; q < hr[k].ndiag && hr[k].diag_off + q < dv.size(); ++q) {
+                const Diag &d = dv[hr[k].diag_off + q];
+                add_span(d.a_off, d.a_len);
+                add_span(d.b_off, d.b_len);
+            }
+    std::string span_text(span_bytes, '\0');
+    if (!spans.empty()) {
+        DevBuf &sb = s->scan_tmp; // free between scans
+        const u64 sl = spans.size() * sizeof(uint4);
+        if (ensure(sb, sl + span_bytes + 16))
+            return -3;
+        CK(cudaMemcpyAsync(sb.p, spans.data(), sl, cudaMemcpyHostToDevice, st));
+        k_span_gather<<<(u32)((spans.size() * 32 + 255) / 256), 256, 0, st>>>(t, P<uint4>(sb), (u32)spans.size(),
+                                                                           P<u8>(sb) + sl);
+        s->stats.total_launches++;
+        CK(cudaGetLastError());
+        if (d2h_sync(s, &span_text[0], P<u8>(sb) + sl, span_bytes))
+            return -3;
+    }
+    u64 span_pos = 0;
+    auto take_span = [&](u32 n, std::string *out) {
+        out->assign(span_text, span_pos, n);
+        span_pos += n;
     };
     for (u32 k = 0; k < nk; ++k) {
         s->host_kdiag.push_back(s->host_diag.size());
@@ -1289,8 +1348,8 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
                 h.line = d.line;
                 h.code = d.code;
                 h.c = d.c;
-                if (span_text(d.a_off, d.a_len, &h.a) || span_text(d.b_off, d.b_len, &h.b))
-                    return -3;
+                take_span(d.a_len, &h.a);
+                take_span(d.b_len, &h.b);
                 s->host_diag.push_back(std::move(h));
             }
         } else {
@@ -1427,7 +1486,7 @@ void reset_stats(ocldec_b200_session *s) {
     s->out_len = 0;
 }
 
-// Splits a host listing into chunks of < ~1 GiB at ".kernel" line starts.
+// Splits a host listing into chunks at ".kernel" line starts.
 // As few chunks of at most `target` bytes as fit, of about equal size (every
 // phase launch ends in a tail); with first > 0 the first chunk is `first`
 // bytes and the rest is balanced.

@@ -90,3 +90,23 @@ def test_c5_device_generated_sample_matches_host():
             assert bytes(host) == want and ni == wni
     finally:
         s.close()
+
+
+def test_vertical_tab_and_formfeed_separators():
+    """Operands separated by \\v, \\f and a mid-line \\r (isspace bytes the
+    reference's tokenizer splits on, asm_frontend.cpp:80-107) are sized and
+    decoded like spaces, on every line including the listing's last."""
+    body = (".kernel vt\n  .config\n    .dims x\n  .text\n"
+            "    v_mov_b32 v0\vv1\vv2\n"
+            "    v_add_u32\fv3,\fvcc,\fv0,\vv1\n"
+            "    s_mov_b32 s0\r\vs1\n"
+            "    v_mul_lo_u32 v4\vv3\fv0\vv1\fv2\n"
+            "    s_endpgm\v\f")
+    for listing in (body.encode(), body.encode() + b"\n", (body + "\n" + body.replace(".kernel vt", ".kernel vt2")).encode()):
+        res = P.decompile_listing(listing)
+        ref = O.decompile(listing)
+        assert res.combined == ref.combined
+        assert [(k.failed, k.structured, k.fallback_count) for k in res.kernels] == \
+               [(k.failed, k.structured, k.fallback_count) for k in ref.kernels]
+        assert [(d.severity, d.line, d.message.encode()) for d in res.diagnostics] == \
+               [(d.severity, d.line, d.message) for d in ref.diagnostics]
