@@ -192,7 +192,8 @@ def run_reference(args):
     nthreads = os.cpu_count() or 1
     cfg = args.config
     # one step = a bounded sample (~6 s on the box's cores) of the config
-    listing, offs, ni, n_step = _ref_sample(cfg, 6.0, nthreads, 200_000)
+    secs_step = float(os.environ.get("OCLDEC_BENCH_REF_SECONDS", "6.0"))
+    listing, offs, ni, n_step = _ref_sample(cfg, secs_step, nthreads, 200_000)
     for _ in range(args.warmup):
         O.decompile_batch(listing, offs, nthreads)
     tot_s = tot_i = 0.0
@@ -214,8 +215,26 @@ def run_reference(args):
     }))
 
 
+def spawn_ranks(args):
+    """`bench.py --gpus N` outside torchrun: re-launch this command as N
+    ranks (one process per GPU) under torch.distributed.run, rendezvous on
+    127.0.0.1.  Returns only when no re-launch is needed."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse()
+    spawn_ranks(args)
     if args.impl == "reference":
         run_reference(args)
         return
@@ -247,7 +266,10 @@ def main():
         sess.run(d_buf, nbytes, starts, sync=False)
         st = sess.stats()
         if world > 1:
-            D.exchange(st["out_bytes"], st["lines"], 0, st["kernels"], device="cuda")
+            # the one exchange step: every rank's {out_bytes, lines, split
+            # error, kernels} -> its offset in the job's combined output
+            st["placement"] = D.place(D.exchange(st["out_bytes"], st["lines"], 0, st["kernels"], device="cuda"),
+                                      rank)
         return st
 
     for _ in range(max(args.warmup, 3)):
@@ -362,6 +384,7 @@ def main():
         "clocks": clk.summary(),
         "e2e": e2e,
         "stats": {k: st[k] for k in ("failed", "goto_form", "fallbacks", "retried", "lines")},
+        "job_out_bytes": st["placement"].total_bytes if world > 1 else out_b,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         try:

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define OCLDEC_B200_ABI_VERSION 3
+#define OCLDEC_B200_ABI_VERSION 4
 
 /* DecompileOptions (decompiler.hpp:29-35). */
 typedef struct ocldec_b200_options {
@@ -99,6 +99,17 @@ typedef struct ocldec_b200_result {
 int ocldec_b200_decompile(const char *listing, size_t len, const ocldec_b200_options *opts,
                           ocldec_b200_result **out);
 void ocldec_b200_free(ocldec_b200_result *res);
+/* decompile_listing sharded across devices: the listing is
+ * cut into ndevices byte-balanced runs of whole kernel sections (at
+ * ".kernel" lines); one host thread per shard drives its device's session;
+ * the shards' {out_bytes, lines, split error, kernels} tuples give each
+ * shard's offset in combined_source, its listing-global line base and the
+ * global split error (decompiler.cpp:105-125); each thread then copies its
+ * text straight into the result at its offset.  The result is identical to
+ * ocldec_b200_decompile's.  A device may be listed more than once (several
+ * sessions on one device).  opts->device is ignored. */
+int ocldec_b200_decompile_multi(const char *listing, size_t len, const ocldec_b200_options *opts,
+                                const int *devices, int ndevices, ocldec_b200_result **out);
 /* parse_abi_overrides (abi_model.cpp:109-153) alone, on the host: writes its
  * diagnostics as "<severity> <line> <message>\n" lines into buf (capacity
  * cap, NUL-terminated); returns the number of errors, or -2 when buf is too

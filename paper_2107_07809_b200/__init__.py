@@ -109,8 +109,13 @@ _SPLIT_MESSAGES = {1: ".kernel directive without a name",
                    3: ".text outside of a .kernel section"}
 
 
-def decompile_listing(listing: Union[str, bytes], opts: Optional[DecompileOptions] = None) -> DecompileResult:
+def decompile_listing(listing: Union[str, bytes], opts: Optional[DecompileOptions] = None,
+                      devices: Optional[Sequence[int]] = None) -> DecompileResult:
     """ocldec::decompile_listing (decompiler.cpp:117-133) on the GPU.
+
+    ``devices``: shard the listing by kernel sections across these CUDA
+    devices, one host thread per device (ocldec_b200_decompile_multi); the
+    result is identical to the single-device call.
 
     A split_kernels ParseError yields zero kernels and one error diagnostic,
     as in the reference (decompiler.cpp:120-125); a kernel-level ParseError
@@ -128,7 +133,12 @@ def decompile_listing(listing: Union[str, bytes], opts: Optional[DecompileOption
                      opts.device, opts.arena_bytes, amap, len(amap) if amap is not None else 0,
                      int(opts.dump_cfg), int(opts.dump_regions), int(opts.record_reduction))
     out = ctypes.POINTER(_lib.Result)()
-    rc = L.ocldec_b200_decompile(listing, len(listing), ctypes.byref(o), ctypes.byref(out))
+    if devices:
+        devs = (ctypes.c_int * len(devices))(*devices)
+        rc = L.ocldec_b200_decompile_multi(listing, len(listing), ctypes.byref(o), devs, len(devices),
+                                           ctypes.byref(out))
+    else:
+        rc = L.ocldec_b200_decompile(listing, len(listing), ctypes.byref(o), ctypes.byref(out))
     if rc != 0:
         raise RuntimeError(f"ocldec_b200_decompile failed ({rc}): {_lib.last_error()}")
     try:

@@ -61,7 +61,7 @@ class Stats(ctypes.Structure):
 
 
 EXPORTS = [
-    "ocldec_b200_decompile", "ocldec_b200_free", "ocldec_b200_last_error", "ocldec_b200_version",
+    "ocldec_b200_decompile", "ocldec_b200_decompile_multi", "ocldec_b200_free", "ocldec_b200_last_error", "ocldec_b200_version",
     "ocldec_b200_session_create", "ocldec_b200_session_destroy", "ocldec_b200_session_stream",
     "ocldec_b200_session_run", "ocldec_b200_session_stats", "ocldec_b200_session_output",
     "ocldec_b200_session_kernels", "ocldec_b200_gen_host", "ocldec_b200_gen_device",
@@ -84,6 +84,10 @@ def load():
     vp, u64, i32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int
     L.ocldec_b200_decompile.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(Options),
                                         ctypes.POINTER(ctypes.POINTER(Result))]
+    L.ocldec_b200_decompile_multi.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(Options),
+                                              ctypes.POINTER(ctypes.c_int), ctypes.c_int,
+                                              ctypes.POINTER(ctypes.POINTER(Result))]
+    L.ocldec_b200_decompile_multi.restype = i32
     L.ocldec_b200_decompile.restype = i32
     L.ocldec_b200_free.argtypes = [ctypes.POINTER(Result)]
     L.ocldec_b200_abi_map_check.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_char_p, ctypes.c_size_t]

@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/ocldec_b200.h"
@@ -1894,97 +1895,134 @@ int ocldec_b200_session_diagnostics(ocldec_b200_session *s, char *buf, uint64_t 
     return n;
 }
 
-int ocldec_b200_decompile(const char *listing, size_t len, const ocldec_b200_options *opts,
-                          ocldec_b200_result **out) {
-    if (!out || (!listing && len)) {
-        g_err = "bad arguments";
-        return -1;
-    }
-    *out = nullptr;
-    ocldec_b200_options o{};
-    if (opts)
-        o = *opts;
-    std::lock_guard<std::mutex> lock(g_cache_mu);
-    ocldec_b200_session *&s = g_cache[{o.device, o.arena_bytes}];
-    if (!s)
-        s = ocldec_b200_session_create(o.device, o.arena_bytes);
-    if (!s)
-        return -3;
-    CK(cudaSetDevice(s->device));
+} // extern "C"
+
+namespace {
+
+// One shard of a decompile call: a contiguous run of kernel sections of the
+// caller's listing, decompiled on one session (one device).  SURVEY §8(e):
+// the only cross-shard coupling is the placement computed from each shard's
+// {out_bytes, lines, split error, kernels} tuple.
+struct Shard {
+    ocldec_b200_session *s = nullptr;
+    const char *p = nullptr;
+    size_t len = 0;
     HostRun hr;
-    if (int rc0 = set_overrides(s, o.abi_map, o.abi_map ? o.abi_map_len : 0))
-        return rc0;
+    int rc = 0;
+    std::string err;       // g_err of the shard's thread
+    u64 lines = 0;         // listing lines in the shard
+    u64 line_base = 0;     // lines before the shard
+    u64 out_off = 0;       // where its text goes in combined_source
+    bool lead_nl = false;  // a "\n" separator precedes it
+};
+
+void run_shard(Shard &sh, const ocldec_b200_options &o) {
+    ocldec_b200_session *s = sh.s;
+    sh.rc = 0;
+    if (cudaSetDevice(s->device) != cudaSuccess) {
+        sh.rc = -3;
+        sh.err = "cudaSetDevice failed";
+        return;
+    }
+    if (int rc0 = set_overrides(s, o.abi_map, o.abi_map ? o.abi_map_len : 0)) {
+        sh.rc = rc0;
+        sh.err = g_err;
+        return;
+    }
     s->dump_flags = (o.dump_cfg ? DUMP_CFG : 0u) | (o.dump_regions ? DUMP_REGIONS : 0u) |
                     (o.record_reduction ? DUMP_MERGES : 0u);
-    int rc = run_host_listing(s, listing, len, o.fold_local_size, o.only_kernel, &hr, nullptr, 0);
+    sh.rc = run_host_listing(s, sh.p, sh.len, o.fold_local_size, o.only_kernel, &sh.hr, nullptr, 0);
     s->dump_flags = 0;
-    if (rc)
-        return rc;
-    auto *res = static_cast<ocldec_b200_result *>(calloc(1, sizeof(ocldec_b200_result)));
-    res->split_error_line = hr.split_error_line;
-    res->split_error_kind = hr.split_error_kind;
-    res->device_ms = hr.device_ms;
-    const u64 out_pos = hr.out_bytes;
-    res->combined = static_cast<char *>(malloc(out_pos + 1));
-    if (out_pos) {
-        CK(cudaMemcpyAsync(res->combined, s->out.p, out_pos, cudaMemcpyDeviceToHost, s->stream));
-        CK(cudaStreamSynchronize(s->stream));
+    sh.lines = s->stats.lines;
+    if (sh.rc)
+        sh.err = g_err;
+}
+
+// The shard's combined output into the result buffer at its placement.
+void copy_shard_out(Shard &sh, char *combined) {
+    if (!sh.hr.out_bytes)
+        return;
+    if (cudaSetDevice(sh.s->device) != cudaSuccess ||
+        cudaMemcpyAsync(combined + sh.out_off, sh.s->out.p, sh.hr.out_bytes, cudaMemcpyDeviceToHost,
+                        sh.s->stream) != cudaSuccess ||
+        cudaStreamSynchronize(sh.s->stream) != cudaSuccess) {
+        sh.rc = -3;
+        sh.err = "device to host copy of the combined output failed";
+        return;
     }
-    res->combined[out_pos] = 0;
-    res->combined_len = out_pos;
-    size_t nk = s->host_res.size();
-    res->kernels = static_cast<ocldec_b200_kernel *>(calloc(nk + 1, sizeof(ocldec_b200_kernel)));
+    if (sh.lead_nl)
+        combined[sh.out_off - 1] = '\n';
+}
+
+// Runs fn(i) for every shard, one host thread per shard when there are
+// several (one per device: each thread drives its own session's stream).
+template <class Fn> void for_shards(std::vector<Shard> &sh, Fn fn) {
+    if (sh.size() == 1) {
+        fn(0);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (size_t i = 0; i < sh.size(); ++i)
+        th.emplace_back([&, i] { fn(i); });
+    for (auto &t : th)
+        t.join();
+}
+
+// decompile_listing over shards: run, place, copy out, and assemble the
+// DecompileResult (decompiler.cpp:117-133 / combined_source :105-115).
+int decompile_shards(std::vector<Shard> &sh, const ocldec_b200_options &o, ocldec_b200_result **out) {
+    for_shards(sh, [&](size_t i) { run_shard(sh[i], o); });
+    for (Shard &x : sh)
+        if (x.rc) {
+            g_err = x.err;
+            return x.rc;
+        }
+    // placement: the one exchange step (here within the process)
+    int32_t err_line = 0, err_kind = 0;
+    u64 lines = 0, pos = 0;
+    bool any = false;
+    double dev_ms = 0;
+    for (Shard &x : sh) {
+        x.line_base = lines;
+        if (!err_line && x.hr.split_error_line > 0) {
+            err_line = (int32_t)(lines + x.hr.split_error_line);
+            err_kind = x.hr.split_error_kind;
+        }
+        lines += x.lines;
+        dev_ms = std::max(dev_ms, x.hr.device_ms);
+        if (x.hr.out_bytes) {
+            x.lead_nl = any;
+            pos += any ? 1 : 0;
+            x.out_off = pos;
+            pos += x.hr.out_bytes;
+            any = true;
+        }
+    }
+    const u64 out_len = err_line ? 0 : pos;
+    auto *res = static_cast<ocldec_b200_result *>(calloc(1, sizeof(ocldec_b200_result)));
+    res->split_error_line = err_line;
+    res->split_error_kind = err_kind;
+    res->device_ms = dev_ms;
+    res->combined = static_cast<char *>(malloc(out_len + 1));
+    res->combined[out_len] = 0;
+    res->combined_len = out_len;
+    if (!err_line) {
+        for_shards(sh, [&](size_t i) { copy_shard_out(sh[i], res->combined); });
+        for (Shard &x : sh)
+            if (x.rc) {
+                g_err = x.err;
+                ocldec_b200_free(res);
+                return x.rc;
+            }
+    }
+    u64 nk_all = 0;
+    for (Shard &x : sh)
+        nk_all += err_line ? 0 : x.s->host_res.size();
+    res->kernels = static_cast<ocldec_b200_kernel *>(calloc(nk_all + 1, sizeof(ocldec_b200_kernel)));
     std::string nm;
     u64 nkept = 0;
-    for (size_t k = 0; k < nk; ++k) {
-        const KRes &r = s->host_res[k];
-        if (r.status == KS_SKIP)
-            continue;
-        ocldec_b200_kernel &K = res->kernels[nkept++];
-        K.name_off = nm.size();
-        K.name_len = hr.names[k].size();
-        nm += hr.names[k];
-        K.src_off = s->host_kernel_off[k];
-        K.src_len = r.status == KS_OK ? r.out_len : 0;
-        K.failed = r.status == KS_FAILED;
-        K.structured = r.structured;
-        K.fallback_count = (int32_t)r.fallbacks;
-        K.instructions = r.ninstr;
-        res->instructions += r.ninstr;
-    }
-    res->nkernels = nkept;
-    {
-        // DecompiledKernel::cfg_dot and ReduceResult::dumps, kernel by kernel
-        std::vector<ocldec_b200_dump> dv;
-        std::string dtx;
-        u64 kk = 0;
-        for (size_t k = 0; k < nk && k < s->host_dumps.size(); ++k) {
-            if (s->host_res[k].status == KS_SKIP)
-                continue;
-            for (const auto &e : s->host_dumps[k]) {
-                ocldec_b200_dump d{};
-                d.kernel = kk;
-                d.step = e.first;
-                d.off = dtx.size();
-                d.len = e.second.size();
-                dtx += e.second;
-                dv.push_back(d);
-            }
-            ++kk;
-        }
-        res->ndumps = dv.size();
-        res->dumps = static_cast<ocldec_b200_dump *>(malloc((dv.size() + 1) * sizeof(ocldec_b200_dump)));
-        if (!dv.empty())
-            memcpy(res->dumps, dv.data(), dv.size() * sizeof(ocldec_b200_dump));
-        res->dump_text = static_cast<char *>(malloc(dtx.size() + 1));
-        memcpy(res->dump_text, dtx.data(), dtx.size());
-        res->dump_text[dtx.size()] = 0;
-    }
-    res->names = static_cast<char *>(malloc(nm.size() + 1));
-    memcpy(res->names, nm.data(), nm.size());
-    res->names[nm.size()] = 0;
-    // DecompileResult::diagnostics in sink order: the split error alone, or
-    // every kept kernel's diagnostics in listing order
+    std::vector<ocldec_b200_dump> dv;
+    std::string dtx;
     std::vector<ocldec_b200_diag> dl;
     std::string dt;
     auto add = [&](int sev, int line, const std::string &msg) {
@@ -1996,23 +2034,64 @@ int ocldec_b200_decompile(const char *listing, size_t len, const ocldec_b200_opt
         dt += msg;
         dl.push_back(d);
     };
-    if (hr.split_error_line > 0) {
+    if (err_line) {
         static const char *kSplit[] = {"parse error", ".kernel directive without a name",
                                        ".config outside of a .kernel section", ".text outside of a .kernel section"};
-        add(2, hr.split_error_line, kSplit[hr.split_error_kind >= 1 && hr.split_error_kind <= 3 ? hr.split_error_kind : 0]);
+        add(2, err_line, kSplit[err_kind >= 1 && err_kind <= 3 ? err_kind : 0]);
     } else {
-        for (size_t k = 0; k < nk; ++k) {
-            const KRes &r = s->host_res[k];
-            if (r.status == KS_SKIP)
-                continue;
-            for (u32 q = 0; q < r.ndiag; ++q) {
-                const HostDiag &h = s->host_diag[s->host_kdiag[k] + q];
-                add(diag_severity(h.code), (int)h.line, diag_message(h, &s->ovr_host));
+        for (Shard &x : sh) {
+            ocldec_b200_session *s = x.s;
+            const size_t nk = s->host_res.size();
+            for (size_t k = 0; k < nk; ++k) {
+                const KRes &r = s->host_res[k];
+                if (r.status == KS_SKIP)
+                    continue;
+                ocldec_b200_kernel &K = res->kernels[nkept];
+                K.name_off = nm.size();
+                K.name_len = x.hr.names[k].size();
+                nm += x.hr.names[k];
+                K.src_off = x.out_off + s->host_kernel_off[k];
+                K.src_len = r.status == KS_OK ? r.out_len : 0;
+                K.failed = r.status == KS_FAILED;
+                K.structured = r.structured;
+                K.fallback_count = (int32_t)r.fallbacks;
+                K.instructions = r.ninstr;
+                res->instructions += r.ninstr;
+                // DecompiledKernel::cfg_dot and ReduceResult::dumps
+                if (k < s->host_dumps.size())
+                    for (const auto &e : s->host_dumps[k]) {
+                        ocldec_b200_dump d{};
+                        d.kernel = nkept;
+                        d.step = e.first;
+                        d.off = dtx.size();
+                        d.len = e.second.size();
+                        dtx += e.second;
+                        dv.push_back(d);
+                    }
+                // DecompileResult::diagnostics in sink order (line 0: override
+                // errors, not listing lines)
+                for (u32 q = 0; q < r.ndiag; ++q) {
+                    const HostDiag &h = s->host_diag[s->host_kdiag[k] + q];
+                    add(diag_severity(h.code), h.line ? (int)(h.line + x.line_base) : 0,
+                        diag_message(h, &s->ovr_host));
+                }
+                ++nkept;
             }
         }
     }
+    res->nkernels = nkept;
+    res->ndumps = dv.size();
+    res->dumps = static_cast<ocldec_b200_dump *>(malloc((dv.size() + 1) * sizeof(ocldec_b200_dump)));
+    if (!dv.empty())
+        memcpy(res->dumps, dv.data(), dv.size() * sizeof(ocldec_b200_dump));
+    res->dump_text = static_cast<char *>(malloc(dtx.size() + 1));
+    memcpy(res->dump_text, dtx.data(), dtx.size());
+    res->dump_text[dtx.size()] = 0;
+    res->names = static_cast<char *>(malloc(nm.size() + 1));
+    memcpy(res->names, nm.data(), nm.size());
+    res->names[nm.size()] = 0;
     const size_t nk_diags = dl.size();
-    for (const OvrDiag &d : s->ovr_diags)
+    for (const OvrDiag &d : sh[0].s->ovr_diags)
         add(d.sev, d.line, d.msg);
     res->ndiags = nk_diags;
     res->nabi_diags = dl.size() - nk_diags;
@@ -2025,6 +2104,70 @@ int ocldec_b200_decompile(const char *listing, size_t len, const ocldec_b200_opt
     res->diag_text[dt.size()] = 0;
     *out = res;
     return 0;
+}
+
+// The cached session for (device, arena, slot): slot > 0 when one call puts
+// several shards on the same device.
+ocldec_b200_session *cached_session(int device, size_t arena, int slot) {
+    ocldec_b200_session *&s = g_cache[{device, arena + (size_t)slot * 0x100000000000000ull}];
+    if (!s)
+        s = ocldec_b200_session_create(device, arena);
+    return s;
+}
+
+} // namespace
+
+extern "C" {
+
+int ocldec_b200_decompile(const char *listing, size_t len, const ocldec_b200_options *opts,
+                          ocldec_b200_result **out) {
+    if (!out || (!listing && len)) {
+        g_err = "bad arguments";
+        return -1;
+    }
+    *out = nullptr;
+    ocldec_b200_options o{};
+    if (opts)
+        o = *opts;
+    std::lock_guard<std::mutex> lock(g_cache_mu);
+    std::vector<Shard> sh(1);
+    sh[0].s = cached_session(o.device, o.arena_bytes, 0);
+    if (!sh[0].s)
+        return -3;
+    sh[0].p = listing;
+    sh[0].len = len;
+    return decompile_shards(sh, o, out);
+}
+
+int ocldec_b200_decompile_multi(const char *listing, size_t len, const ocldec_b200_options *opts,
+                                const int *devices, int ndevices, ocldec_b200_result **out) {
+    if (!out || (!listing && len) || !devices || ndevices < 1) {
+        g_err = "bad arguments";
+        return -1;
+    }
+    *out = nullptr;
+    ocldec_b200_options o{};
+    if (opts)
+        o = *opts;
+    std::lock_guard<std::mutex> lock(g_cache_mu);
+    // byte-balanced shards cut at ".kernel" lines (fewer when the listing has
+    // fewer sections than devices)
+    const size_t target = std::max<size_t>(1, (len + ndevices - 1) / (size_t)ndevices);
+    std::vector<u64> starts = host_chunks(listing, len, target, 0);
+    if (starts.size() > (size_t)ndevices)
+        starts.resize((size_t)ndevices);
+    std::vector<Shard> sh(starts.size());
+    for (size_t i = 0; i < sh.size(); ++i) {
+        int slot = 0;
+        for (size_t j = 0; j < i; ++j)
+            slot += devices[j] == devices[i];
+        sh[i].s = cached_session(devices[i], o.arena_bytes, slot);
+        if (!sh[i].s)
+            return -3;
+        sh[i].p = listing + starts[i];
+        sh[i].len = (i + 1 < sh.size() ? starts[i + 1] : (u64)len) - starts[i];
+    }
+    return decompile_shards(sh, o, out);
 }
 
 int ocldec_b200_session_run_host(ocldec_b200_session *s, const char *listing, size_t len,

@@ -51,3 +51,20 @@ def test_reference_arm_line(tmp_path):
         assert key in line, key
     assert line["impl"] == "reference" and line["cpu_baseline"]["kind"] == "reference"
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_gpus_flag_spawns_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself as 2 ranks
+    (torch.distributed.run, 127.0.0.1): the reference arm prints one line from
+    rank 0 and both ranks exit 0."""
+    from oracle import oracle as O
+    if not O.available():
+        pytest.skip("oracle not built")
+    env = dict(os.environ, OCLDEC_BENCH_REF_SECONDS="0.02")
+    env.pop("WORLD_SIZE", None)
+    p = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2", "--steps", "1",
+                        "--warmup", "0", "--config", "C3"], cwd=ROOT, capture_output=True, text=True,
+                       timeout=600, env=env)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [json.loads(x) for x in p.stdout.strip().splitlines() if x.startswith("{")]
+    assert len(lines) == 1 and lines[0]["impl"] == "reference" and lines[0]["n_gpus"] == 2
