@@ -38,6 +38,7 @@ struct DecompileOptions {
     bool dump_regions = false;    // DecompileOptions::dump_regions (decompiler.hpp:34)
     bool record_reduction = false; // fill DecompiledKernel::reduction (merges, root / residue)
     int device = 0;
+    std::vector<int> devices;     // non-empty: shard across these devices (ocldec_b200_decompile_multi)
 };
 
 // MergeRecord (structurizer.hpp:54-58); kind: 1 Linear, 2 IfThen, 3 IfElse.
@@ -181,7 +182,10 @@ inline DecompileResult decompile_listing(const std::string &listing, const Decom
     o.dump_regions = opts.dump_regions ? 1 : 0;
     o.record_reduction = opts.record_reduction ? 1 : 0;
     ocldec_b200_result *r = nullptr;
-    int rc = ocldec_b200_decompile(listing.data(), listing.size(), &o, &r);
+    int rc = opts.devices.empty()
+                 ? ocldec_b200_decompile(listing.data(), listing.size(), &o, &r)
+                 : ocldec_b200_decompile_multi(listing.data(), listing.size(), &o, opts.devices.data(),
+                                               (int)opts.devices.size(), &r);
     if (rc != 0)
         throw std::runtime_error(std::string("ocldec_b200_decompile: ") + ocldec_b200_last_error());
     DecompileResult res;

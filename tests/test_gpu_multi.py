@@ -127,3 +127,17 @@ def test_two_gpu_ranks_gloo_assemble_to_reference():
     assert D.assemble([g[1] for g in got], table) == ref.combined
     assert got[0][3] + got[1][3] == [(d.severity, d.line, d.message.decode("utf-8", "surrogateescape"))
                                       for d in ref.diagnostics]
+
+
+def test_cli_devices_flag(tmp_path):
+    """The CLI's --devices shards through the same C-ABI call; the output file
+    equals the reference's combined_source."""
+    import subprocess
+    cli = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2107_07809_b200",
+                       "ocldec-b200")
+    listing, _, _ = P.generate_corpus("C3", 120, seed=12)
+    src = tmp_path / "k.asm"
+    src.write_bytes(listing)
+    p = subprocess.run([cli, str(src), "--devices", "0,0,0"], capture_output=True, timeout=300)
+    assert p.returncode in (0, 1), p.stderr
+    assert (tmp_path / "k.cl").read_bytes() == O.decompile(listing).combined

@@ -11,6 +11,7 @@
 // when no kernel was produced or any kernel failed, 0 otherwise.
 // --abi-map FILE is parsed first; its diagnostics are printed against FILE and
 // any error exits 1 before decompiling (ocldec.cpp:120-131).
+// --devices 0,1,... shards the listing across GPUs (one host thread each).
 // --dump-cfg / --dump-regions write <out stem>.<kernel>.cfg.dot and
 // <out stem>.<kernel>.step<N>.dot next to the output (ocldec.cpp:68-77, 150-165).
 #include <cstdio>
@@ -24,64 +25,63 @@
 
 namespace {
 
-bool read_file(const std::string &path, std::string &out, std::string &err) {
-    std::ifstream in(path, std::ios::binary);
-    if (!in) {
+// The whole file as bytes; on failure err holds the reference CLI's message.
+bool slurp(const std::string &path, std::string &out, std::string &err) {
+    FILE *f = std::fopen(path.c_str(), "rb");
+    if (!f) {
         err = "cannot open '" + path + "' for reading";
         return false;
     }
-    std::ostringstream buf;
-    buf << in.rdbuf();
-    out = buf.str();
+    out.clear();
+    char chunk[1 << 16];
+    for (size_t n; (n = std::fread(chunk, 1, sizeof chunk, f)) > 0;)
+        out.append(chunk, n);
+    std::fclose(f);
     return true;
 }
 
-bool write_atomic(const std::string &path, const std::string &content, std::string &err) {
-    const std::string tmp = path + ".tmp";
-    FILE *f = std::fopen(tmp.c_str(), "wb");
+// Temp file beside the target, then rename over it: a failed write never
+// leaves a truncated output (the reference CLI's contract, ocldec.cpp:35-57).
+bool replace_file(const std::string &path, const std::string &bytes, std::string &err) {
+    const std::string part = path + ".tmp";
+    FILE *f = std::fopen(part.c_str(), "wb");
     if (!f) {
-        err = "cannot open '" + tmp + "' for writing";
+        err = "cannot open '" + part + "' for writing";
         return false;
     }
-    bool ok = std::fwrite(content.data(), 1, content.size(), f) == content.size();
-    ok = (std::fclose(f) == 0) && ok;
-    if (!ok) {
-        err = "write to '" + tmp + "' failed";
-        std::remove(tmp.c_str());
+    const bool wrote = std::fwrite(bytes.data(), 1, bytes.size(), f) == bytes.size();
+    if (std::fclose(f) != 0 || !wrote) {
+        err = "write to '" + part + "' failed";
+        std::remove(part.c_str());
         return false;
     }
-    if (std::rename(tmp.c_str(), path.c_str()) != 0) {
-        err = "cannot rename '" + tmp + "' to '" + path + "'";
-        std::remove(tmp.c_str());
-        return false;
-    }
-    return true;
+    if (std::rename(part.c_str(), path.c_str()) == 0)
+        return true;
+    err = "cannot rename '" + part + "' to '" + path + "'";
+    std::remove(part.c_str());
+    return false;
 }
 
-// <output stem>.<kernel> (ocldec.cpp:68-77)
+// The path without its extension: a '.' counts only inside the last path
+// component (ocldec.cpp:59-77 names the output and dump files this way).
+std::string strip_ext(const std::string &path) {
+    const size_t cut = path.find_last_of('.');
+    const size_t sep = path.find_last_of("/\\");
+    const bool has_ext = cut != std::string::npos && (sep == std::string::npos || cut > sep);
+    return has_ext ? path.substr(0, cut) : path;
+}
+
 std::string dump_stem(const std::string &output, const std::string &kernel) {
-    std::string stem = output;
-    size_t slash = stem.find_last_of("/\\");
-    size_t dot = stem.find_last_of('.');
-    if (dot != std::string::npos && (slash == std::string::npos || dot > slash))
-        stem.resize(dot);
-    return stem + "." + kernel;
+    return strip_ext(output) + "." + kernel;
 }
 
-std::string default_output(const std::string &input) {
-    std::string stem = input;
-    size_t slash = stem.find_last_of("/\\");
-    size_t dot = stem.find_last_of('.');
-    if (dot != std::string::npos && (slash == std::string::npos || dot > slash))
-        stem.resize(dot);
-    return stem + ".cl";
-}
+std::string default_output(const std::string &input) { return strip_ext(input) + ".cl"; }
 
 int usage(const char *argv0, int code) {
     std::fprintf(code ? stderr : stdout,
                  "Decompiles AMD GCN disassembly listings (CLRX syntax) to OpenCL C on the GPU\n"
                  "Usage: %s input [-o OUTPUT] [--kernel NAME] [--fold-local-size] [--abi-map FILE]\n"
-                 "       [--dump-cfg] [--dump-regions] [--device N]\n",
+                 "       [--dump-cfg] [--dump-regions] [--device N | --devices N,M,...]\n",
                  argv0);
     return code;
 }
@@ -99,7 +99,8 @@ int main(int argc, char **argv) {
             std::printf("ocldec-b200 (C ABI %d)\n", OCLDEC_B200_ABI_VERSION);
             return 0;
         }
-        if ((a == "-o" || a == "--output" || a == "--kernel" || a == "--device" || a == "--abi-map") &&
+        if ((a == "-o" || a == "--output" || a == "--kernel" || a == "--device" || a == "--abi-map" ||
+             a == "--devices") &&
             i + 1 < argc) {
             std::string v = argv[++i];
             if (a == "--abi-map")
@@ -108,6 +109,14 @@ int main(int argc, char **argv) {
                 opts.only_kernel = v;
             else if (a == "--device")
                 opts.device = std::atoi(v.c_str());
+            else if (a == "--devices") // comma-separated ordinals: shard across them
+                for (size_t p0 = 0; p0 <= v.size();) {
+                    size_t p1 = v.find(',', p0);
+                    if (p1 == std::string::npos)
+                        p1 = v.size();
+                    opts.devices.push_back(std::atoi(v.substr(p0, p1 - p0).c_str()));
+                    p0 = p1 + 1;
+                }
             else
                 output = v;
             continue;
@@ -130,12 +139,12 @@ int main(int argc, char **argv) {
         return usage(argv[0], 1);
 
     std::string err, listing;
-    if (!read_file(input, listing, err)) {
+    if (!slurp(input, listing, err)) {
         std::cerr << "ocldec-b200: error: " << err << "\n";
         return 1;
     }
     if (!abi_path.empty()) {
-        if (!read_file(abi_path, opts.abi_map, err)) {
+        if (!slurp(abi_path, opts.abi_map, err)) {
             std::cerr << "ocldec-b200: error: " << err << "\n";
             return 1;
         }
@@ -174,18 +183,18 @@ int main(int argc, char **argv) {
     if (opts.dump_cfg || opts.dump_regions) {
         for (const auto &k : result.kernels) {
             const std::string stem = dump_stem(output, k.name);
-            if (opts.dump_cfg && !k.cfg_dot.empty() && !write_atomic(stem + ".cfg.dot", k.cfg_dot, err)) {
+            if (opts.dump_cfg && !k.cfg_dot.empty() && !replace_file(stem + ".cfg.dot", k.cfg_dot, err)) {
                 std::cerr << "ocldec-b200: error: " << err << "\n";
                 return 1;
             }
             for (size_t i = 0; i < k.region_dumps.size(); ++i)
-                if (!write_atomic(stem + ".step" + std::to_string(i) + ".dot", k.region_dumps[i], err)) {
+                if (!replace_file(stem + ".step" + std::to_string(i) + ".dot", k.region_dumps[i], err)) {
                     std::cerr << "ocldec-b200: error: " << err << "\n";
                     return 1;
                 }
         }
     }
-    if (!write_atomic(output, result.combined_source(), err)) {
+    if (!replace_file(output, result.combined_source(), err)) {
         std::cerr << "ocldec-b200: error: " << err << "\n";
         return 1;
     }
