@@ -190,6 +190,26 @@ int ocldec_b200_gen_device(ocldec_b200_session *s, int shape, int stress, uint64
                            uint64_t k0, uint64_t count, const void **d_buf, uint64_t *len,
                            const uint64_t **d_offsets, uint64_t *instructions);
 
+/* Streaming run of a generated corpus (~320 GB of listing
+ * for 1M kernels, more than HBM): kernels [k0, k0+count) are sized on the
+ * device, cut into chunks of at most chunk_bytes (0 = default) at kernel
+ * boundaries, and each chunk is generated into the session's text buffer and
+ * decompiled before the next one is generated; no whole-corpus buffer.  Each
+ * chunk's combined output replaces the previous one on the device.  With
+ * sample_stride > 0, kernel k with k % sample_stride == 0 gets the FNV-1a
+ * hash and length of its source at index k / sample_stride - ceil(k0 /
+ * sample_stride) of sample_hash / sample_len (either may be NULL). */
+typedef struct ocldec_b200_stream_stats {
+    uint64_t kernels, instructions, in_bytes, out_bytes, chunks, failed, goto_form, fallbacks;
+    double ms_decompile; /* device time of the decompile passes (parse + decompile + gather), all chunks */
+    double ms_generate;  /* device time of the generator (sizing + per-chunk text) */
+    double ms_wall;      /* device time of the whole call */
+} ocldec_b200_stream_stats;
+int ocldec_b200_session_run_generated(ocldec_b200_session *s, int shape, int stress, uint64_t seed,
+                                      uint64_t k0, uint64_t count, uint64_t chunk_bytes, int fold_local_size,
+                                      uint64_t sample_stride, uint64_t *sample_hash, uint64_t *sample_len,
+                                      ocldec_b200_stream_stats *out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -267,6 +267,27 @@ class Session:
         if rc:
             raise RuntimeError(f"session_run failed ({rc}): {_lib.last_error()}")
 
+    def run_generated(self, shape: Union[int, str], count: int, seed: int = 1, k0: int = 0, stress: bool = False,
+                      chunk_bytes: int = 0, sample_stride: int = 0, fold_local_size: bool = False):
+        """Streams kernels [k0, k0+count) of a generated corpus through the
+        pipeline chunk by chunk (ocldec_b200_session_run_generated): no
+        whole-corpus buffer.  Returns (stats dict, sample hashes, sample lengths)."""
+        import numpy as np
+        shape = SHAPES.get(shape, shape) if isinstance(shape, str) else shape
+        ns = 0
+        if sample_stride:
+            ns = (k0 + count + sample_stride - 1) // sample_stride - (k0 + sample_stride - 1) // sample_stride
+        hs = np.zeros(max(ns, 1), dtype=np.uint64)
+        ls = np.zeros(max(ns, 1), dtype=np.uint64)
+        st = _lib.StreamStats()
+        rc = self._L.ocldec_b200_session_run_generated(self._s, shape, int(stress), seed, k0, count, chunk_bytes,
+                                                       int(fold_local_size), sample_stride, hs.ctypes.data,
+                                                       ls.ctypes.data, ctypes.byref(st))
+        if rc:
+            raise RuntimeError(f"run_generated failed ({rc}): {_lib.last_error()}")
+        d = {n: getattr(st, n) for n, _ in _lib.StreamStats._fields_}
+        return d, hs[:ns], ls[:ns]
+
     def run_host(self, host_ptr: int, length: int, out_ptr: int, out_cap: int, fold_local_size: bool = False) -> int:
         """Host buffers in and out (ocldec_b200_session_run_host); returns output length."""
         n = ctypes.c_uint64()

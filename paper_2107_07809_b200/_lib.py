@@ -60,13 +60,19 @@ class Stats(ctypes.Structure):
         ("ms_fold", ctypes.c_double)]
 
 
+class StreamStats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in (
+        "kernels", "instructions", "in_bytes", "out_bytes", "chunks", "failed", "goto_form", "fallbacks")] + [
+        ("ms_decompile", ctypes.c_double), ("ms_generate", ctypes.c_double), ("ms_wall", ctypes.c_double)]
+
+
 EXPORTS = [
     "ocldec_b200_decompile", "ocldec_b200_decompile_multi", "ocldec_b200_free", "ocldec_b200_last_error", "ocldec_b200_version",
     "ocldec_b200_session_create", "ocldec_b200_session_destroy", "ocldec_b200_session_stream",
     "ocldec_b200_session_run", "ocldec_b200_session_stats", "ocldec_b200_session_output",
     "ocldec_b200_session_kernels", "ocldec_b200_gen_host", "ocldec_b200_gen_device",
     "ocldec_b200_session_run_host", "ocldec_b200_copy", "ocldec_b200_abi_map_check",
-    "ocldec_b200_session_names", "ocldec_b200_session_diagnostics",
+    "ocldec_b200_session_names", "ocldec_b200_session_diagnostics", "ocldec_b200_session_run_generated",
 ]
 
 _lib = None
@@ -117,6 +123,9 @@ def load():
     L.ocldec_b200_gen_device.argtypes = [vp, i32, i32, u64, u64, u64, ctypes.POINTER(vp),
                                          ctypes.POINTER(u64), ctypes.POINTER(vp), ctypes.POINTER(u64)]
     L.ocldec_b200_gen_device.restype = i32
+    L.ocldec_b200_session_run_generated.argtypes = [vp, i32, i32, u64, u64, u64, u64, i32, u64, vp, vp,
+                                                    ctypes.POINTER(StreamStats)]
+    L.ocldec_b200_session_run_generated.restype = i32
     _lib = L
     return L
 

@@ -2270,6 +2270,7 @@ int ocldec_b200_gen_device(ocldec_b200_session *s, int shape, int stress, uint64
     a.len = P<u64>(s->gen_len);
     a.ninstr = P<u32>(s->gen_ninstr);
     a.buf = nullptr;
+    a.base = 0;
     CK(cudaMemsetAsync(a.len + count, 0, 8, s->stream));
     k_gen<<<(u32)((count + 127) / 128), 128, 0, s->stream>>>(a, 0);
     CK(cudaGetLastError());
@@ -2299,6 +2300,168 @@ int ocldec_b200_gen_device(ocldec_b200_session *s, int shape, int stress, uint64
     *d_offsets = P<u64>(s->gen_off);
     if (instructions)
         *instructions = ni;
+    return 0;
+}
+
+// Streams a generated corpus through the pipeline: kernels [k0, k0+count)
+// of (shape, stress, seed) are sized on the device, cut into chunks of at
+// most chunk_bytes at kernel boundaries, and each chunk is generated into
+// the session's text buffer and decompiled before the next is generated, so
+// no whole-corpus buffer exists (C5: ~320 GB of listing for 1M kernels).
+// Each chunk's output replaces the previous one in the session's output
+// buffer.  Every sample_stride-th kernel (k % sample_stride == 0, 0 = none)
+// gets the FNV-1a hash and length of its source in sample_hash/sample_len
+// (indexed k / sample_stride), for comparison with the reference.
+int ocldec_b200_session_run_generated(ocldec_b200_session *s, int shape, int stress, uint64_t seed,
+                                      uint64_t k0, uint64_t count, uint64_t chunk_bytes, int fold_local_size,
+                                      uint64_t sample_stride, uint64_t *sample_hash, uint64_t *sample_len,
+                                      ocldec_b200_stream_stats *out) {
+    if (!s || !out) {
+        g_err = "bad arguments";
+        return -1;
+    }
+    CK(cudaSetDevice(s->device));
+    *out = ocldec_b200_stream_stats{};
+    reset_stats(s);
+    s->only_set = false;
+    set_overrides(s, nullptr, 0);
+    if (!chunk_bytes)
+        chunk_bytes = chunk_target();
+    chunk_bytes = std::min<u64>(chunk_bytes, 0xe0000000ull);
+    cudaStream_t st = s->stream;
+    cudaEvent_t e0, e1, g0, g1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventCreate(&g0));
+    CK(cudaEventCreate(&g1));
+    CK(cudaEventRecord(e0, st));
+    // sizing pass over the whole range: per-kernel bytes and instructions
+    if (ensure(s->gen_len, (count + 1) * 8) || ensure(s->gen_ninstr, (count + 1) * 4) ||
+        ensure(s->gen_off, (count + 1) * 8) || ensure(s->counters, 64))
+        return -3;
+    GenArgs a;
+    a.cfg = GenCfg{(u32)shape, (u32)stress, seed};
+    a.k0 = k0;
+    a.count = count;
+    a.len = P<u64>(s->gen_len);
+    a.ninstr = P<u32>(s->gen_ninstr);
+    a.buf = nullptr;
+    a.base = 0;
+    CK(cudaMemsetAsync(a.len + count, 0, 8, st));
+    k_gen<<<(u32)((count + 127) / 128), 128, 0, st>>>(a, 0);
+    CK(cudaGetLastError());
+    if (scan_exclusive(s, count + 1, U64Val{0}, AddU64{}, U64Load{a.len}, U64Store{P<u64>(s->gen_off)},
+                       reinterpret_cast<U64Val *>(P<u32>(s->counters) + 8)))
+        return -3;
+    std::vector<u64> offs(count + 1);
+    if (d2h_sync(s, offs.data(), s->gen_off.p, (count + 1) * 8))
+        return -3;
+    float ms = 0;
+    {
+        cudaEvent_t t;
+        CK(cudaEventCreate(&t));
+        CK(cudaEventRecord(t, st));
+        CK(cudaEventSynchronize(t));
+        CK(cudaEventElapsedTime(&ms, e0, t));
+        cudaEventDestroy(t);
+    }
+    out->ms_generate += ms;
+    // chunks: as few as fit under chunk_bytes, about equal
+    const u64 total = offs[count];
+    const u64 nch = std::max<u64>(1, (total + chunk_bytes - 1) / chunk_bytes);
+    const u64 tgt = (total + nch - 1) / nch;
+    std::vector<u64> kb{0};
+    for (u64 k = 0; k < count;) {
+        u64 e = std::upper_bound(offs.begin() + k + 1, offs.begin() + count + 1, offs[kb.back()] + tgt) -
+                offs.begin() - 1;
+        if (e <= k)
+            e = k + 1;
+        kb.push_back(e);
+        k = e;
+    }
+    u64 maxn = 0;
+    for (size_t c = 0; c + 1 < kb.size(); ++c)
+        maxn = std::max<u64>(maxn, offs[kb[c + 1]] - offs[kb[c]]);
+    if (maxn >= 0xf0000000ull) {
+        g_err = "a single generated kernel exceeds the chunk size limit";
+        return -1;
+    }
+    if (ensure(s->text, maxn + (maxn >> 2) + 4096))
+        return -3;
+    u32 line_base = 0;
+    for (size_t c = 0; c + 1 < kb.size(); ++c) {
+        const u64 ka = kb[c], kz = kb[c + 1], n = offs[kz] - offs[ka];
+        GenArgs g = a;
+        g.k0 = k0 + ka;
+        g.count = kz - ka;
+        g.len = P<u64>(s->gen_off) + ka;
+        g.buf = P<u8>(s->text);
+        g.base = offs[ka];
+        CK(cudaEventRecord(g0, st));
+        k_gen<<<(u32)((g.count + 127) / 128), 128, 0, st>>>(g, 1);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(g1, st));
+        const size_t before = s->host_res.size();
+        ChunkOut co;
+        s->chunk_base = 0;
+        int rc = run_chunk(s, P<u8>(s->text), n, true, line_base, fold_local_size, 0, false, &co);
+        if (rc)
+            return rc;
+        if (co.err_line != 0xffffffffu) {
+            g_err = "split_kernels error in a generated chunk";
+            return -4;
+        }
+        CK(cudaEventElapsedTime(&ms, g0, g1));
+        out->ms_generate += ms;
+        // sampled kernels: source hash (FNV-1a, as the oracle's batch driver)
+        for (size_t q = before; sample_stride && q < s->host_res.size(); ++q) {
+            const u64 k = ka + (q - before);
+            if ((k0 + k) % sample_stride)
+                continue;
+            const KRes &r = s->host_res[q];
+            std::string src(r.status == KS_OK ? r.out_len : 0, '\0');
+            if (!src.empty())
+                CK(cudaMemcpy(&src[0], P<u8>(s->out) + s->host_kernel_off[q], src.size(), cudaMemcpyDeviceToHost));
+            u64 h = 1469598103934665603ull;
+            for (unsigned char ch : src) {
+                h ^= ch;
+                h *= 1099511628211ull;
+            }
+            const u64 si = (k0 + k) / sample_stride - (k0 + sample_stride - 1) / sample_stride;
+            if (sample_hash)
+                sample_hash[si] = h;
+            if (sample_len)
+                sample_len[si] = src.size();
+        }
+        line_base += co.nlines;
+        s->stats.lines += co.nlines;
+        s->stats.kernels += co.nk;
+        out->in_bytes += n;
+        out->out_bytes += co.out_bytes;
+        out->chunks++;
+        // per-kernel host records are not kept across chunks
+        s->host_res.clear();
+        s->host_kernel_off.clear();
+        s->host_name_line.clear();
+        s->host_name_off.clear();
+        s->host_diag.clear();
+        s->host_kdiag.clear();
+        s->host_dumps.clear();
+    }
+    CK(cudaEventRecord(e1, st));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    out->ms_wall = ms;
+    out->ms_decompile = s->stats.ms_parse + s->stats.ms_decompile + s->stats.ms_emit;
+    out->kernels = s->stats.kernels;
+    out->instructions = s->stats.instructions;
+    out->failed = s->stats.failed;
+    out->goto_form = s->stats.goto_form;
+    out->fallbacks = s->stats.fallbacks;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(g0);
+    cudaEventDestroy(g1);
     return 0;
 }
 

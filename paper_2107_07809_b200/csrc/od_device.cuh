@@ -151,6 +151,7 @@ struct GenArgs {
     u64 *len;   // per kernel length (sizing) -> offsets after scan
     u32 *ninstr;
     u8 *buf;
+    u64 base;   // write pass: kernel i goes to buf + len[i] - base
 };
 
 __global__ void k_gen(GenArgs a, int mode);

@@ -18,7 +18,7 @@ __global__ void k_gen(GenArgs a, int mode) {
         a.len[i] = w.n;
         a.ninstr[i] = ni;
     } else {
-        u64 off = a.len[i];
+        u64 off = a.len[i] - a.base;
         w.p = a.buf + off;
         w.n = 0;
         w.cap = 0xffffffffu;

@@ -110,3 +110,29 @@ def test_vertical_tab_and_formfeed_separators():
                [(k.failed, k.structured, k.fallback_count) for k in ref.kernels]
         assert [(d.severity, d.line, d.message.encode()) for d in res.diagnostics] == \
                [(d.severity, d.line, d.message) for d in ref.diagnostics]
+
+
+def test_streamed_generation_matches_reference_hashes():
+    """ocldec_b200_session_run_generated (the C5 streaming path: generate a
+    chunk on the device, decompile it, next chunk) forced into several
+    chunks: the sampled kernels' source hashes equal the reference's, and the
+    totals equal a resident run of the same corpus."""
+    s = P.Session(0)
+    try:
+        for cfg, n, stride in (("C5", 40, 3), ("C3", 3000, 97)):
+            st, hs, ls = s.run_generated(cfg, n, seed=SEEDS[cfg], k0=11, chunk_bytes=2 << 20 if cfg == "C5" else 1 << 18,
+                                         sample_stride=stride)
+            assert st["chunks"] > 2 and st["kernels"] == n and st["failed"] == 0
+            ks = [k for k in range(11, 11 + n) if k % stride == 0]
+            parts = [O.generate_corpus(cfg, 1, seed=SEEDS[cfg], k0=k) for k in ks]
+            listing = b"".join(p[0] for p in parts)
+            offs = np.cumsum([0] + [len(p[0]) for p in parts]).astype(np.uint64)
+            _, _, rh, rl = O.decompile_batch(listing, offs, os.cpu_count() or 1, want_hashes=True)
+            assert list(hs) == list(rh) and list(ls) == list(rl)
+            # totals equal the whole-corpus run
+            host, _, ni = P.generate_corpus(cfg, n, seed=SEEDS[cfg], k0=11)
+            assert st["instructions"] == ni and st["in_bytes"] == len(host)
+            # each chunk's combined output, joined by combined_source's "\n"
+            assert st["out_bytes"] + st["chunks"] - 1 == len(P.decompile_listing(host).combined)
+    finally:
+        s.close()
