@@ -263,6 +263,9 @@ def run_stream(args, P, torch, dist, world, rank, local, nk):
             st, hs, ls = sess.run_generated(cfg, k1 - k0, seed=SEEDS[cfg], k0=k0, sample_stride=stride)
             for key in acc:
                 acc[key] += st[key]
+            ss = sess.stats()
+            for key in ("ms_parse", "ms_front", "ms_lower", "ms_fold", "ms_render", "ms_emit"):
+                acc[key] = acc.get(key, 0.0) + ss[key]
     torch.cuda.synchronize()
     tot = np.array([acc["ms_decompile"], acc["ms_wall"], st["instructions"], st["in_bytes"], st["out_bytes"],
                     st["kernels"]], dtype=np.float64)
@@ -293,6 +296,9 @@ def run_stream(args, P, torch, dist, world, rank, local, nk):
                      "algorithmic_bytes": "in+out text bytes of the corpus"},
         "clocks": clk.summary(),
         "stats": {k: st[k] for k in ("failed", "goto_form", "fallbacks")},
+        "passes_ms_per_step_rank0": {name: acc[k] / args.steps for k, name in (
+            ("ms_parse", "parse"), ("ms_front", "k_front"), ("ms_lower", "k_lower"), ("ms_fold", "k_fold"),
+            ("ms_render", "k_emit"), ("ms_emit", "gather"))},
     }
     if rank == 0 and world == 1 and not args.no_e2e:
         # e2e on a bounded resident sample: the whole C5 listing does not fit

@@ -814,6 +814,7 @@ struct ocldec_b200_session {
     std::vector<std::vector<std::pair<int32_t, std::string>>> host_dumps; // per host_res kernel
     std::vector<OvrDiag> ovr_diags;  // their parse diagnostics
     DevBuf dovr, dovr_text;
+    DevBuf sgen;                     // streamed generation: the current group of chunks
     u32 novr = 0;
     std::vector<u64> host_kdiag;     // per kernel: first host_diag index (count in host_res[k].ndiag)
     size_t pev_used = 0;
@@ -1747,7 +1748,7 @@ void ocldec_b200_session_destroy(ocldec_b200_session *s) {
                       &s->outoff, &s->out, &s->only, &s->retry, &s->gen_len, &s->gen_ninstr,
                       &s->gen_buf, &s->gen_off, &s->kmeta, &s->order, &s->budget, &s->sbudget,
                       &s->boff, &s->hist, &s->prof, &s->ksizes, &s->dpool, &s->dtop, &s->perm, &s->cnt4,
-                      &s->dovr, &s->dovr_text};
+                      &s->dovr, &s->dovr_text, &s->xtext, &s->xrec, &s->xtop, &s->xcfg, &s->sgen};
     for (DevBuf *b : bufs)
         if (b->p)
             cudaFree(b->p);
@@ -2329,11 +2330,11 @@ int ocldec_b200_session_run_generated(ocldec_b200_session *s, int shape, int str
         chunk_bytes = chunk_target();
     chunk_bytes = std::min<u64>(chunk_bytes, 0xe0000000ull);
     cudaStream_t st = s->stream;
-    cudaEvent_t e0, e1, g0, g1;
+    cudaEvent_t e0, e1, g0e, g1e;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    CK(cudaEventCreate(&g0));
-    CK(cudaEventCreate(&g1));
+    CK(cudaEventCreate(&g0e));
+    CK(cudaEventCreate(&g1e));
     CK(cudaEventRecord(e0, st));
     // sizing pass over the whole range: per-kernel bytes and instructions
     if (ensure(s->gen_len, (count + 1) * 8) || ensure(s->gen_ninstr, (count + 1) * 4) ||
@@ -2386,33 +2387,49 @@ int ocldec_b200_session_run_generated(ocldec_b200_session *s, int shape, int str
         g_err = "a single generated kernel exceeds the chunk size limit";
         return -1;
     }
-    if (ensure(s->text, maxn + (maxn >> 2) + 4096))
-        return -3;
+    // Chunks are generated G at a time (one k_gen launch over G chunks'
+    // kernels: the generator is one thread per kernel, so a lone chunk keeps
+    // only a few warps per SM busy), then decompiled one after the other
+    // from the group buffer.
+    size_t G = 8;
+    if (const char *e = getenv("OCLDEC_B200_GEN_GROUP"))
+        G = std::max<size_t>(1, strtoull(e, nullptr, 0));
+    const size_t nchunks = kb.size() - 1;
     u32 line_base = 0;
-    for (size_t c = 0; c + 1 < kb.size(); ++c) {
+    size_t g0 = 0, g1 = 0;
+    for (size_t c = 0; c < nchunks; ++c) {
         const u64 ka = kb[c], kz = kb[c + 1], n = offs[kz] - offs[ka];
-        GenArgs g = a;
-        g.k0 = k0 + ka;
-        g.count = kz - ka;
-        g.len = P<u64>(s->gen_off) + ka;
-        g.buf = P<u8>(s->text);
-        g.base = offs[ka];
-        CK(cudaEventRecord(g0, st));
-        k_gen<<<(u32)((g.count + 127) / 128), 128, 0, st>>>(g, 1);
-        CK(cudaGetLastError());
-        CK(cudaEventRecord(g1, st));
+        if (c == g1) { // generate the next group
+            g0 = c;
+            g1 = std::min(nchunks, c + G);
+            const u64 gb = offs[kb[g1]] - offs[kb[g0]];
+            if (ensure(s->sgen, gb + 64))
+                return -3;
+            GenArgs g = a;
+            g.k0 = k0 + kb[g0];
+            g.count = kb[g1] - kb[g0];
+            g.len = P<u64>(s->gen_off) + kb[g0];
+            g.buf = P<u8>(s->sgen);
+            g.base = offs[kb[g0]];
+            CK(cudaEventRecord(g0e, st));
+            k_gen<<<(u32)((g.count + 127) / 128), 128, 0, st>>>(g, 1);
+            CK(cudaGetLastError());
+            CK(cudaEventRecord(g1e, st));
+            CK(cudaEventSynchronize(g1e));
+            CK(cudaEventElapsedTime(&ms, g0e, g1e));
+            out->ms_generate += ms;
+        }
         const size_t before = s->host_res.size();
         ChunkOut co;
         s->chunk_base = 0;
-        int rc = run_chunk(s, P<u8>(s->text), n, true, line_base, fold_local_size, 0, false, &co);
+        int rc = run_chunk(s, P<u8>(s->sgen) + (offs[ka] - offs[kb[g0]]), n, false, line_base, fold_local_size,
+                           0, false, &co);
         if (rc)
             return rc;
         if (co.err_line != 0xffffffffu) {
             g_err = "split_kernels error in a generated chunk";
             return -4;
         }
-        CK(cudaEventElapsedTime(&ms, g0, g1));
-        out->ms_generate += ms;
         // sampled kernels: source hash (FNV-1a, as the oracle's batch driver)
         for (size_t q = before; sample_stride && q < s->host_res.size(); ++q) {
             const u64 k = ka + (q - before);
@@ -2460,8 +2477,8 @@ int ocldec_b200_session_run_generated(ocldec_b200_session *s, int shape, int str
     out->fallbacks = s->stats.fallbacks;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    cudaEventDestroy(g0);
-    cudaEventDestroy(g1);
+    cudaEventDestroy(g0e);
+    cudaEventDestroy(g1e);
     return 0;
 }
 

@@ -155,6 +155,14 @@ OD_INL u32 ctz64(u64 m) {
 #endif
 }
 
+OD_INL u32 popc32(u32 m) {
+#ifdef __CUDA_ARCH__
+    return (u32)__popc(m);
+#else
+    return (u32)__builtin_popcount(m);
+#endif
+}
+
 OD_INL u64 fetch_add_u64(unsigned long long *p, u64 v) {
 #ifdef __CUDA_ARCH__
     return (u64)atomicAdd(p, (unsigned long long)v);
@@ -162,6 +170,80 @@ OD_INL u64 fetch_add_u64(unsigned long long *p, u64 v) {
     const u64 o = *p;
     *p += v;
     return o;
+#endif
+}
+
+// ------------------------------------------------------- warp cooperation
+// k_front runs each kernel's front on all 32 lanes of its warp redundantly
+// (every lane holds the same state and takes the same branches).  Loops over
+// independent items are split across the lanes executing them (the active
+// mask m): lane wrank(m) takes items wrank, wrank + wsize, ...; results are
+// combined with warp reductions or written to distinct arena words and
+// published with wsync.  The same code is correct on a lone lane (m has one
+// bit: the loop covers every item), which is how the other phases and the
+// host build run it.
+OD_INL u32 wmask() {
+#ifdef __CUDA_ARCH__
+    return __activemask();
+#else
+    return 1u;
+#endif
+}
+OD_INL u32 wrank(u32 m) {
+#ifdef __CUDA_ARCH__
+    return (u32)__popc(m & ((1u << (threadIdx.x & 31)) - 1));
+#else
+    (void)m;
+    return 0;
+#endif
+}
+OD_INL u32 wsize(u32 m) {
+#ifdef __CUDA_ARCH__
+    return (u32)__popc(m);
+#else
+    (void)m;
+    return 1;
+#endif
+}
+OD_INL bool wleader(u32 m) { return wrank(m) == 0; }
+OD_INL void wsync(u32 m) {
+#ifdef __CUDA_ARCH__
+    __syncwarp(m);
+#else
+    (void)m;
+#endif
+}
+OD_INL u32 wor(u32 m, u32 v) {
+#ifdef __CUDA_ARCH__
+    return __reduce_or_sync(m, v);
+#else
+    (void)m;
+    return v;
+#endif
+}
+OD_INL u32 wmax(u32 m, u32 v) {
+#ifdef __CUDA_ARCH__
+    return __reduce_max_sync(m, v);
+#else
+    (void)m;
+    return v;
+#endif
+}
+OD_INL u32 wadd(u32 m, u32 v) {
+#ifdef __CUDA_ARCH__
+    return __reduce_add_sync(m, v);
+#else
+    (void)m;
+    return v;
+#endif
+}
+// v of the mask's lowest lane
+OD_INL u64 wbcast64(u32 m, u64 v) {
+#ifdef __CUDA_ARCH__
+    return __shfl_sync(m, (unsigned long long)v, __ffs(m) - 1);
+#else
+    (void)m;
+    return v;
 #endif
 }
 

@@ -52,7 +52,57 @@ __device__ __noinline__ Collected warp_collect(const DecompArgs &a, u32 lbeg, u3
     return c;
 }
 
+// One kernel per warp (lanes_per == 32): the whole warp runs the kernel's
+// front redundantly (od_base.cuh "warp cooperation"), so the loops the front
+// splits across lanes (liveness, ...) run 32 wide.
+__device__ __noinline__ void front_warp(const DecompArgs &a) {
+    const u32 full = 0xffffffffu;
+    const u32 lane = threadIdx.x & 31;
+    Slot0 sl{0, 0, nullptr};
+    const bool mine = dk_slot(a, &sl); // lane 0 of the warp, when the wave has a kernel for it
+    if (!__shfl_sync(full, mine, 0))
+        return;
+    sl.k = __shfl_sync(full, sl.k, 0);
+    sl.i = __shfl_sync(full, sl.i, 0);
+    sl.base = reinterpret_cast<u8 *>(__shfl_sync(full, (unsigned long long)sl.base, 0));
+    Collected col{0, 0, 0, 0, 0};
+    bool collected = false;
+    {
+        const u32 kb = (sizeof(KState) + 255) & ~255ull;
+        const KSize z = a.sizes[sl.k];
+        u64 kl_off;
+        const u64 need = collect_bytes(z.nins, z.nlab, &kl_off);
+        if (need <= a.boff[sl.i + 1] - a.boff[sl.i] - kb) { // else the front runs out of arena and retries
+            const u32 lbeg = a.kstart[sl.k], lend = sl.k + 1 < a.nk ? a.kstart[sl.k + 1] : a.nlines;
+            col = warp_collect(a, lbeg, lend, reinterpret_cast<Ins *>(sl.base + kb),
+                               reinterpret_cast<u32 *>(sl.base + kb + kl_off));
+            collected = true;
+        }
+    }
+    __syncwarp();
+    u64 *names = nullptr;
+    u32 names_cap = 0;
+    Slot *regs = nullptr;
+    front_one(a, sl, &names, &names_cap, &regs, col, collected);
+    __syncwarp();
+    if (regs) {
+        Slot d;
+        reset_slot(d);
+        d.pad[0] = d.pad[1] = d.pad[2] = 0;
+        const uint4 dv = *reinterpret_cast<const uint4 *>(&d);
+        for (u32 q = lane; q < kPhysSlots; q += 32)
+            reinterpret_cast<uint4 *>(regs)[q] = dv;
+    }
+    if (names)
+        for (u32 q = lane; q < names_cap / 2; q += 32)
+            reinterpret_cast<uint4 *>(names)[q] = uint4{0, 0, 0, 0};
+}
+
 __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_FRONT * 128 / OD_BLOCK) k_front(DecompArgs a) {
+    if (a.lanes_per == 32) {
+        front_warp(a);
+        return;
+    }
     Slot0 sl;
     u64 *names = nullptr; // this lane's name set, zeroed below by the whole warp
     u32 names_cap = 0;

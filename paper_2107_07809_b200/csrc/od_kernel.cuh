@@ -1078,31 +1078,62 @@ OD_INL bool blk_reach(const KCtx &K, u32 b) { return (K.rbits[b >> 5] >> (b & 31
 OD_INL void set_reach(KCtx &K, u32 b) { K.rbits[b >> 5] |= 1u << (b & 31); }
 
 // Returns the number of reachable blocks.
+// cfg.mark_reachable (cfg.cpp:23-39): the set of blocks reachable from block
+// 0, computed by forward sweeps over the block list instead of a depth-first
+// walk (the set is the same): words of 32 blocks are visited in order, a set
+// bit's successors are marked, a successor in the same word is picked up in
+// the same visit, and an edge back into an earlier word reopens that word.
+// Every block is expanded once; the successor pairs stream in order.
 OD_NOINL u32 mark_reachable(KCtx &K) {
-    // cfg.mark_reachable (cfg.cpp:23-39) over the compact successor pairs
     u32 *__restrict__ rb = K.rbits;
     const u32 *__restrict__ sx = K.sx;
-    u32 *__restrict__ work = K.work;
+    u32 *__restrict__ done = K.work; // per word: blocks already expanded
     const u32 nb = K.nblk;
-    for (u32 w = 0; w < (nb + 31) / 32; ++w)
+    const u32 nw = (nb + 31) / 32;
+    for (u32 w = 0; w < nw; ++w) {
         rb[w] = 0;
+        done[w] = 0;
+    }
     if (!nb)
         return 0;
-    u32 sp = 0, nr = 0;
-    work[sp++] = 0;
-    while (sp) {
-        const u32 id = work[--sp];
-        const u32 bit = 1u << (id & 31);
-        if (rb[id >> 5] & bit)
-            continue;
-        rb[id >> 5] |= bit;
-        ++nr;
-        const u32 a = sx[2 * id], b = sx[2 * id + 1];
-        if (a != kNoSucc)
-            work[sp++] = a;
-        if (b != kNoSucc)
-            work[sp++] = b;
+    rb[0] = 1;
+    u32 lo = 0;
+    while (lo < nw) {
+        u32 w = lo;
+        lo = nw;
+        for (; w < nw; ++w) {
+            u32 cur = rb[w];
+            u32 pend = cur & ~done[w];
+            if (!pend)
+                continue;
+            u32 dn = done[w];
+            while (pend) {
+                const u32 i = ctz32(pend);
+                dn |= 1u << i;
+                const u32 b = 32 * w + i;
+                const u32 s2[2] = {sx[2 * b], sx[2 * b + 1]};
+                for (u32 q = 0; q < 2; ++q) {
+                    const u32 t = s2[q];
+                    if (t == kNoSucc)
+                        continue;
+                    const u32 tw = t >> 5, tb = 1u << (t & 31);
+                    if (tw == w) {
+                        cur |= tb;
+                    } else if (!(rb[tw] & tb)) {
+                        rb[tw] |= tb;
+                        if (tw < w && tw < lo)
+                            lo = tw;
+                    }
+                }
+                pend = cur & ~dn;
+            }
+            rb[w] = cur;
+            done[w] = dn;
+        }
     }
+    u32 nr = 0;
+    for (u32 w = 0; w < nw; ++w)
+        nr += popc32(rb[w]);
     return nr;
 }
 
@@ -1332,8 +1363,10 @@ OD_NOINL void canonicalize(KCtx &K) {
             }
         }
     }
-    for (u32 b = 0; b < K.nblk; ++b)
+    const u32 m = wmask(); // annotate_block edits only its own block
+    for (u32 b = wrank(m); b < K.nblk; b += wsize(m))
         annotate_block(K, b);
+    wsync(m);
 }
 
 OD_INL bool first_exec_op_is(const KCtx &K, u32 b, u32 kind, u32 mask) {
@@ -1377,7 +1410,8 @@ OD_NOINL u32 mask_stops(KCtx &K, const i32 *starts, u32 nstarts, u32 mask, i32 h
 // retarget_preds  structurizer.cpp:512-525
 OD_NOINL void retarget_preds(KCtx &K, i32 from, i32 to, i32 keep) {
     const u32 f = (u32)from;
-    for (u32 p = 0; p < K.nblk; ++p) {
+    const u32 m = wmask(); // blocks split across the warp: each edits only its own edges
+    for (u32 p = wrank(m); p < K.nblk; p += wsize(m)) {
         if ((K.sx[2 * p] != f && K.sx[2 * p + 1] != f) || (i32)p == keep)
             continue;
         Block &P = K.blk[p];
@@ -1390,6 +1424,7 @@ OD_NOINL void retarget_preds(KCtx &K, i32 from, i32 to, i32 keep) {
             P.term.not_taken = to;
         sync_succ(K, p);
     }
+    wsync(m);
 }
 
 struct MaskPattern {
@@ -2198,8 +2233,16 @@ OD_NOINL void dump_emit(KCtx &K, i32 step) {
     const DumpCfg &D = *K.in->dump;
     DotSink c{nullptr, 0};
     dump_print(K, c, step);
-    const u64 off = fetch_add_u64(&D.top[0], c.n);
-    const u64 ri = fetch_add_u64(&D.top[1], 1);
+    // one reservation per executing lane group (k_front runs redundantly on
+    // the warp): the leader reserves, every lane writes the same bytes
+    const u32 m = wmask();
+    u64 off = 0, ri = 0;
+    if (wleader(m)) {
+        off = fetch_add_u64(&D.top[0], c.n);
+        ri = fetch_add_u64(&D.top[1], 1);
+    }
+    off = wbcast64(m, off);
+    ri = wbcast64(m, ri);
     if (off + c.n > D.cap || ri >= D.rcap) {
         K.dump_full = true;
         return;
@@ -2384,8 +2427,10 @@ OD_NOINL void instruction_use_def(const KCtx &K, const Ins &I, LvSink &S) {
         lv_mark(S, kRegIdScc, true);
 }
 
-// live_in_sets  cfg.cpp:356-398 (word-parallel; the least fixpoint is
-// unique, so iteration order does not matter)
+// live_in_sets  cfg.cpp:356-398, split across the warp (north star (4)):
+// the per-block gen/kill sets are independent, one block per lane; the
+// fixpoint is bitwise, so every live word converges on its own, one word per
+// lane (the least fixpoint is unique: any order gives the reference's sets).
 OD_NOINL bool liveness(KCtx &K) {
     const u32 nb = K.nblk;
     u32 *use = K.mem->get<u32>((u64)nb * kLiveWords);
@@ -2393,6 +2438,7 @@ OD_NOINL bool liveness(KCtx &K) {
     K.live_in = K.mem->get<u32>((u64)nb * kLiveWords);
     if (!use || !def || !K.live_in)
         return false;
+    const u32 m = wmask(), r = wrank(m), nl = wsize(m);
     u32 any[kLiveWords]; // union of the use sets
     for (u32 w = 0; w < kLiveWords; ++w)
         any[w] = 0;
@@ -2404,7 +2450,7 @@ OD_NOINL bool liveness(KCtx &K) {
     const Ins *__restrict__ ins = K.ins;
     const u8 *__restrict__ supp = K.supp;
     u32 *__restrict__ live_in = K.live_in;
-    for (u32 b = 0; b < nb; ++b) {
+    for (u32 b = r; b < nb; b += nl) {
         for (u32 w = 0; w < kLiveWords; ++w) {
             S.U[w] = 0;
             S.D[w] = 0;
@@ -2424,6 +2470,9 @@ OD_NOINL bool liveness(KCtx &K) {
             any[w] |= S.U[w];
         }
     }
+    for (u32 w = 0; w < kLiveWords; ++w)
+        any[w] = wor(m, any[w]);
+    wsync(m); // every lane sees every block's sets
     // Only words holding some use bit can ever become live (live_in is a
     // subset of the union of the use sets), so the fixpoint runs over those.
     u32 wl[kLiveWords];
@@ -2431,29 +2480,28 @@ OD_NOINL bool liveness(KCtx &K) {
     for (u32 w = 0; w < kLiveWords; ++w)
         if (any[w])
             wl[nw++] = w;
-    bool changed = nw > 0;
-    while (changed) {
-        changed = false;
-        for (u32 bi = nb; bi-- > 0;) {
-            const Block &B = blk[bi];
-            const u32 ns = B.nsucc;
-            const u32 s0 = ns > 0 ? (u32)B.succ[0] : 0, s1 = ns > 1 ? (u32)B.succ[1] : 0;
-            u32 *L = live_in + bi * kLiveWords;
-            for (u32 k = 0; k < nw; ++k) {
-                const u32 w = wl[k];
+    for (u32 k = r; k < nw; k += nl) {
+        const u32 w = wl[k];
+        bool changed = true;
+        while (changed) {
+            changed = false;
+            for (u32 bi = nb; bi-- > 0;) {
+                const u32 a0 = K.sx[2 * bi], a1 = K.sx[2 * bi + 1];
                 u32 out = 0;
-                if (ns > 0)
-                    out |= live_in[s0 * kLiveWords + w];
-                if (ns > 1)
-                    out |= live_in[s1 * kLiveWords + w];
-                u32 in = use[bi * kLiveWords + w] | (out & ~def[bi * kLiveWords + w]);
-                if (in != L[w]) {
-                    L[w] = in;
+                if (a0 != kNoSucc)
+                    out |= live_in[a0 * kLiveWords + w];
+                if (a1 != kNoSucc)
+                    out |= live_in[a1 * kLiveWords + w];
+                const u32 in = use[bi * kLiveWords + w] | (out & ~def[bi * kLiveWords + w]);
+                u32 &L = live_in[bi * kLiveWords + w];
+                if (in != L) {
+                    L = in;
                     changed = true;
                 }
             }
         }
     }
+    wsync(m); // the live sets are read by every lane from here on
     return true;
 }
 

@@ -1525,7 +1525,8 @@ OD_INL u64 arena_budget(const KSize &z, u32 s) {
     do {                                                                                           \
         if (in.prof) {                                                                             \
             long long t1_ = clock64();                                                             \
-            atomicAdd((unsigned long long *)&in.prof[i], (unsigned long long)(t1_ - t0));          \
+            if (wleader(wmask()))                                                                  \
+                atomicAdd((unsigned long long *)&in.prof[i], (unsigned long long)(t1_ - t0));      \
             t0 = t1_;                                                                              \
         }                                                                                          \
     } while (0)
