@@ -237,6 +237,31 @@ OD_INL u32 wadd(u32 m, u32 v) {
     return v;
 #endif
 }
+OD_INL u32 wballot(u32 m, bool pred) {
+#ifdef __CUDA_ARCH__
+    return __ballot_sync(m, pred);
+#else
+    (void)m;
+    return pred ? 1u : 0u;
+#endif
+}
+// lanes of ballot b below this lane (b holds lane positions)
+OD_INL u32 wbelow(u32 b) {
+#ifdef __CUDA_ARCH__
+    return (u32)__popc(b & ((1u << (threadIdx.x & 31)) - 1));
+#else
+    (void)b;
+    return 0;
+#endif
+}
+OD_INL u32 wmin(u32 m, u32 v) {
+#ifdef __CUDA_ARCH__
+    return __reduce_min_sync(m, v);
+#else
+    (void)m;
+    return v;
+#endif
+}
 // v of the mask's lowest lane
 OD_INL u64 wbcast64(u32 m, u64 v) {
 #ifdef __CUDA_ARCH__

@@ -1157,6 +1157,73 @@ OD_NOINL void note_unreachable(KCtx &K) {
 }
 
 // build_cfg  cfg.cpp:64-156
+// Terminator of block bi (cfg.cpp:100-146) without its diagnostics: returns
+// the ParseError it would raise (0 none; 1 branch without a label operand,
+// 2 undefined label, 3 unsupported conditional branch, 4 conditional branch
+// at the end).
+OD_INL u32 block_term(KCtx &K, u32 bi) {
+    Block &B = K.blk[bi];
+    const Ins &last = K.ins[B.ie - 1];
+    const int next = bi + 1 < K.nblk ? (int)bi + 1 : -1;
+    Term &t = B.term;
+    t.line = last.line;
+    u32 err = 0;
+    auto target = [&](const Ins &I) -> int {
+        if (I.nops == 0 || op_at(K, I, 0).kind != OK_SYMBOL) {
+            err = 1;
+            return -1;
+        }
+        const Opnd &o = op_at(K, I, 0);
+        const int tb = lmap_get(K, Span{o.r.a, o.r.b});
+        if (tb < 0)
+            err = 2;
+        return tb;
+    };
+    if (is_endpgm(last)) {
+        t.kind = T_END;
+    } else if (last.prefix == PX_S && last.root == R_BRANCH) {
+        t.kind = T_UNCOND;
+        t.taken = target(last);
+    } else if (last.prefix == PX_S && (last.rflags & RF_CBRANCH)) {
+        int cc = -1;
+        switch (last.root) {
+        case R_CBRANCH_SCC0: cc = C_SCC0; break;
+        case R_CBRANCH_SCC1: cc = C_SCC1; break;
+        case R_CBRANCH_VCCZ: cc = C_VCCZ; break;
+        case R_CBRANCH_VCCNZ: cc = C_VCCNZ; break;
+        case R_CBRANCH_EXECZ: cc = C_EXECZ; break;
+        case R_CBRANCH_EXECNZ: cc = C_EXECNZ; break;
+        default: break;
+        }
+        if (cc < 0 || next < 0)
+            return cc < 0 ? 3 : 4;
+        t.kind = T_COND;
+        t.cc = (u8)cc;
+        t.taken = target(last);
+        t.not_taken = next;
+    } else if (next >= 0) {
+        t.kind = T_FALL;
+        t.taken = next;
+    } else {
+        t.kind = T_END;
+    }
+    if (t.kind == T_COND) {
+        B.succ[0] = t.taken;
+        B.succ[1] = t.not_taken;
+        B.nsucc = 2;
+    } else if (t.taken >= 0) {
+        B.succ[0] = t.taken;
+        B.nsucc = 1;
+    }
+    sync_succ(K, bi);
+    return err;
+}
+
+// build_cfg  cfg.cpp:64-156, split across the warp: leaders from a ballot
+// over 32 instructions at a time (block ids = a running prefix count), the
+// label map filled in block order, terminators per block in parallel.  The
+// reference stops at the first block (in order) whose terminator raises a
+// ParseError: the lowest such block's diagnostic is the one emitted.
 OD_NOINL bool build_cfg(KCtx &K) {
     u32 n = K.nins;
     K.blk_cap = n + 2;
@@ -1175,14 +1242,16 @@ OD_NOINL bool build_cfg(KCtx &K) {
     K.lmap = K.mem->get<u32>(2 * lc);
     if (!K.blk || !K.stamp || !K.work || !K.supp || !K.lmap || !K.sx || !K.rbits)
         return false;
-    for (u32 i = 0; i < 2 * lc; ++i)
+    const u32 m = wmask(), r = wrank(m), nl = wsize(m);
+    for (u32 i = r; i < 2 * lc; i += nl)
         K.lmap[i] = 0;
-    for (u32 i = 0; i < n; ++i)
+    for (u32 i = r; i < n; i += nl)
         K.supp[i] = 0;
-    for (u32 i = 0; i < K.blk_cap; ++i)
+    for (u32 i = r; i < K.blk_cap; i += nl)
         K.stamp[i] = 0;
     K.stamp_gen = 0;
     K.nblk = 0;
+    wsync(m);
     if (n == 0) {
         Block &B = K.blk[K.nblk++];
         B.ib = B.ie = 0;
@@ -1197,84 +1266,71 @@ OD_NOINL bool build_cfg(KCtx &K) {
         K.rbits[0] = 1;
         return true;
     }
-    // leaders
-    for (u32 i = 0; i < n; ++i) {
-        const Ins &I = K.ins[i];
-        bool lead = i == 0 || I.lab_n > 0;
-        if (i > 0) {
-            const Ins &P = K.ins[i - 1];
-            if (is_branch(P) || is_endpgm(P))
-                lead = true;
+    // leaders: instruction 0, labelled instructions, and the instruction after
+    // a branch or s_endpgm
+    u32 nb = 0;
+    for (u32 i0 = 0; i0 < n; i0 += nl) {
+        const u32 i = i0 + r;
+        bool lead = false;
+        if (i < n) {
+            lead = i == 0 || K.ins[i].lab_n > 0;
+            if (i > 0 && !lead) {
+                const Ins &P = K.ins[i - 1];
+                lead = is_branch(P) || is_endpgm(P);
+            }
         }
+        const u32 bal = wballot(m, lead);
         if (lead) {
-            if (K.nblk >= K.blk_cap)
-                return false; // size bound too tight: KS_OOM, retried at the worst case
-            if (K.nblk)
-                K.blk[K.nblk - 1].ie = i;
-            Block &B = K.blk[K.nblk];
-            B.ib = i;
-            B.ie = n;
-            B.lab_b = I.lab_b;
-            B.lab_n = I.lab_n;
-            term_default(B.term);
-            B.nsucc = 0;
-            B.reachable = 1;
-            B.absorbed = 0;
-            B.xfront.kind = B.xback.kind = XK_NONE;
-            for (u32 k = 0; k < I.lab_n; ++k)
-                lmap_put(K, I.lab_b + k, K.nblk);
-            K.nblk++;
-        }
-    }
-    for (u32 bi = 0; bi < K.nblk && !K.failed; ++bi) {
-        Block &B = K.blk[bi];
-        const Ins &last = K.ins[B.ie - 1];
-        int next = bi + 1 < K.nblk ? (int)bi + 1 : -1;
-        Term &t = B.term;
-        t.line = last.line;
-        if (is_endpgm(last)) {
-            t.kind = T_END;
-        } else if (last.prefix == PX_S && last.root == R_BRANCH) {
-            t.kind = T_UNCOND;
-            t.taken = resolve_target(K, last);
-        } else if (last.prefix == PX_S && (last.rflags & RF_CBRANCH)) {
-            int cc = -1;
-            switch (last.root) {
-            case R_CBRANCH_SCC0: cc = C_SCC0; break;
-            case R_CBRANCH_SCC1: cc = C_SCC1; break;
-            case R_CBRANCH_VCCZ: cc = C_VCCZ; break;
-            case R_CBRANCH_VCCNZ: cc = C_VCCNZ; break;
-            case R_CBRANCH_EXECZ: cc = C_EXECZ; break;
-            case R_CBRANCH_EXECNZ: cc = C_EXECNZ; break;
-            default: break;
+            const u32 id = nb + wbelow(bal);
+            if (id < K.blk_cap) {
+                const Ins &I = K.ins[i];
+                Block &B = K.blk[id];
+                B.ib = i;
+                B.ie = n;
+                B.lab_b = I.lab_b;
+                B.lab_n = I.lab_n;
+                term_default(B.term);
+                B.nsucc = 0;
+                B.reachable = 1;
+                B.absorbed = 0;
+                B.xfront.kind = B.xback.kind = XK_NONE;
+                if (id)
+                    K.blk[id - 1].ie = i;
             }
-            if (cc < 0 || next < 0) {
-                cbranch_error(K, last, cc < 0);
-                break;
-            }
-            t.kind = T_COND;
-            t.cc = (u8)cc;
-            t.taken = resolve_target(K, last);
-            t.not_taken = next;
-        } else if (next >= 0) {
-            t.kind = T_FALL;
-            t.taken = next;
-        } else {
-            t.kind = T_END;
         }
-        if (t.kind == T_COND) {
-            B.succ[0] = t.taken;
-            B.succ[1] = t.not_taken;
-            B.nsucc = 2;
-        } else if (t.taken >= 0) {
-            B.succ[0] = t.taken;
-            B.nsucc = 1;
-        }
+        nb += popc32(bal);
     }
-    if (K.failed)
+    wsync(m);
+    if (nb > K.blk_cap)
+        return false; // size bound too tight: KS_OOM, retried at the worst case
+    K.nblk = nb;
+    for (u32 bi = 0; bi < nb; ++bi) { // the label map, in block order (a repeated label maps to its last block)
+        const Block &B = K.blk[bi];
+        for (u32 k = 0; k < B.lab_n; ++k)
+            lmap_put(K, B.lab_b + k, bi);
+    }
+    wsync(m);
+    u32 first_err = 0xffffffffu;
+    for (u32 bi = r; bi < nb; bi += nl)
+        if (block_term(K, bi) && bi < first_err)
+            first_err = bi;
+    first_err = wmin(m, first_err);
+    wsync(m);
+    if (first_err != 0xffffffffu) { // the reference's ParseError: the first block's diagnostic
+        const Ins &last = K.ins[K.blk[first_err].ie - 1];
+        const int next = first_err + 1 < nb ? (int)first_err + 1 : -1;
+        if (last.prefix == PX_S && (last.rflags & RF_CBRANCH) && !is_endpgm(last) && last.root != R_BRANCH) {
+            const bool unsupported = !(last.root == R_CBRANCH_SCC0 || last.root == R_CBRANCH_SCC1 ||
+                                       last.root == R_CBRANCH_VCCZ || last.root == R_CBRANCH_VCCNZ ||
+                                       last.root == R_CBRANCH_EXECZ || last.root == R_CBRANCH_EXECNZ);
+            if (unsupported || next < 0) {
+                cbranch_error(K, last, unsupported);
+                return true;
+            }
+        }
+        resolve_target(K, last); // emits the branch-target diagnostic and fails the kernel
         return true;
-    for (u32 b = 0; b < K.nblk; ++b)
-        sync_succ(K, b);
+    }
     if (mark_reachable(K) < K.nblk)
         note_unreachable(K);
     return true;
@@ -1339,32 +1395,32 @@ OD_NOINL u32 split_block(KCtx &K, u32 id, u32 at) {
 // canonical, so one forward pass over the growing block list performs the
 // identical split sequence.
 OD_NOINL void canonicalize(KCtx &K) {
+    const u32 m = wmask(), r = wrank(m), nl = wsize(m);
     for (u32 b = 0; b < K.nblk; ++b) {
         Block &B = K.blk[b];
-        u32 size = B.ie - B.ib;
-        for (u32 i = B.ib; i < B.ie; ++i) {
-            if (K.supp[i])
-                continue;
-            const Ins &I = K.ins[i];
-            if (I.xkind == XK_NONE)
-                continue;
-            u32 index = i - B.ib;
-            if (I.xkind == XK_SAVE) {
-                bool tail = B.term.kind == T_COND && (B.term.cc == C_EXECZ || B.term.cc == C_EXECNZ);
-                u32 last = size - 1;
-                u32 want = tail ? last - 1 : last;
-                if (index < want) {
-                    split_block(K, b, index + 1);
-                    break;
-                }
-            } else if (index > 0) {
-                split_block(K, b, index);
+        const u32 size = B.ie - B.ib;
+        const bool tail = B.term.kind == T_COND && (B.term.cc == C_EXECZ || B.term.cc == C_EXECNZ);
+        const u32 want = tail ? size - 2 : size - 1; // (unsigned, as the reference's size_t)
+        // the first exec op that forces a split, 32 instructions at a time
+        for (u32 i0 = B.ib; i0 < B.ie; i0 += nl) {
+            const u32 i = i0 + r;
+            bool hit = false;
+            if (i < B.ie && !K.supp[i]) {
+                const Ins &I = K.ins[i];
+                const u32 index = i - B.ib;
+                hit = I.xkind != XK_NONE && (I.xkind == XK_SAVE ? index < want : index > 0);
+            }
+            const u32 bal = wballot(m, hit);
+            if (bal) {
+                const u32 pos = ctz32(bal);
+                const u32 first = i0 + popc32(m & ((1u << pos) - 1)) - B.ib;
+                split_block(K, b, K.ins[B.ib + first].xkind == XK_SAVE ? first + 1 : first);
                 break;
             }
         }
     }
-    const u32 m = wmask(); // annotate_block edits only its own block
-    for (u32 b = wrank(m); b < K.nblk; b += wsize(m))
+    wsync(m);
+    for (u32 b = r; b < K.nblk; b += nl) // annotate_block edits only its own block
         annotate_block(K, b);
     wsync(m);
 }
