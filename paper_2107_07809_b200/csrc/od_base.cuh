@@ -163,6 +163,25 @@ OD_INL u32 popc32(u32 m) {
 #endif
 }
 
+OD_INL u32 cas_u32(u32 *p, u32 cmp, u32 val) {
+#ifdef __CUDA_ARCH__
+    return atomicCAS(p, cmp, val);
+#else
+    const u32 o = *p;
+    if (o == cmp)
+        *p = val;
+    return o;
+#endif
+}
+OD_INL void max_u32(u32 *p, u32 v) {
+#ifdef __CUDA_ARCH__
+    atomicMax(p, v);
+#else
+    if (*p < v)
+        *p = v;
+#endif
+}
+
 OD_INL u64 fetch_add_u64(unsigned long long *p, u64 v) {
 #ifdef __CUDA_ARCH__
     return (u64)atomicAdd(p, (unsigned long long)v);

@@ -363,6 +363,7 @@ struct KCtx {
     u32 *rbits;  // reachability bitmap (BasicBlock::reachable)
     u32 stamp_gen;
     u32 *work;   // block work stack
+    bool acyclic; // the flow graph has no cycle (set by normalize)
 
     // label map
     u32 *lmap;   // label-list index + 1 (0 empty)
@@ -1024,19 +1025,25 @@ OD_INL bool is_endpgm(const Ins &I) { return I.prefix == PX_S && I.root == R_END
 
 OD_INL const Label &klabel(const KCtx &K, u32 kli) { return K.in->labs[K.kl[kli]]; }
 
-OD_INL void lmap_put(KCtx &K, u32 kli, u32 block) {
+// lmap_put for lanes inserting concurrently: a slot is claimed with a CAS on
+// its key; a label repeated across blocks keeps the highest block, which is
+// what inserting in block order (the last insert wins) gives.
+OD_INL void lmap_put_atomic(KCtx &K, u32 kli, u32 block) {
     const Label &L = klabel(K, kli);
     u32 i = (u32)(L.hash >> 32) & (K.lmap_cap - 1);
-    while (K.lmap[2 * i]) {
-        const Label &M = klabel(K, K.lmap[2 * i] - 1);
+    for (;;) {
+        const u32 cur = cas_u32(&K.lmap[2 * i], 0u, kli + 1);
+        if (cur == 0) {
+            max_u32(&K.lmap[2 * i + 1], block);
+            return;
+        }
+        const Label &M = klabel(K, cur - 1);
         if (M.hash == L.hash && M.len == L.len && bytes_eq(K.in->t + M.off, K.in->t + L.off, L.len)) {
-            K.lmap[2 * i + 1] = block;
+            max_u32(&K.lmap[2 * i + 1], block);
             return;
         }
         i = (i + 1) & (K.lmap_cap - 1);
     }
-    K.lmap[2 * i] = kli + 1;
-    K.lmap[2 * i + 1] = block;
 }
 
 OD_INL int lmap_get(const KCtx &K, Span name) {
@@ -1304,10 +1311,12 @@ OD_NOINL bool build_cfg(KCtx &K) {
     if (nb > K.blk_cap)
         return false; // size bound too tight: KS_OOM, retried at the worst case
     K.nblk = nb;
-    for (u32 bi = 0; bi < nb; ++bi) { // the label map, in block order (a repeated label maps to its last block)
+    // the label map (a label repeated across blocks maps to its last block),
+    // blocks split across the lanes
+    for (u32 bi = r; bi < nb; bi += nl) {
         const Block &B = K.blk[bi];
         for (u32 k = 0; k < B.lab_n; ++k)
-            lmap_put(K, B.lab_b + k, bi);
+            lmap_put_atomic(K, B.lab_b + k, bi);
     }
     wsync(m);
     u32 first_err = 0xffffffffu;
@@ -1464,12 +1473,15 @@ OD_NOINL u32 mask_stops(KCtx &K, const i32 *starts, u32 nstarts, u32 mask, i32 h
 }
 
 // retarget_preds  structurizer.cpp:512-525
-OD_NOINL void retarget_preds(KCtx &K, i32 from, i32 to, i32 keep) {
+// Returns whether some reachable block now has an edge to `to`.
+OD_NOINL bool retarget_preds(KCtx &K, i32 from, i32 to, i32 keep) {
     const u32 f = (u32)from;
     const u32 m = wmask(); // blocks split across the warp: each edits only its own edges
+    bool fed = false;
     for (u32 p = wrank(m); p < K.nblk; p += wsize(m)) {
         if ((K.sx[2 * p] != f && K.sx[2 * p + 1] != f) || (i32)p == keep)
             continue;
+        fed |= blk_reach(K, p);
         Block &P = K.blk[p];
         for (u32 s = 0; s < P.nsucc; ++s)
             if (P.succ[s] == from)
@@ -1480,7 +1492,49 @@ OD_NOINL void retarget_preds(KCtx &K, i32 from, i32 to, i32 keep) {
             P.term.not_taken = to;
         sync_succ(K, p);
     }
+    fed = wor(m, fed ? 1u : 0u) != 0;
     wsync(m);
+    return fed;
+}
+
+// Whether some reachable block has an edge to b (lanes over the blocks).
+OD_NOINL bool has_reachable_pred(const KCtx &K, u32 b) {
+    const u32 m = wmask();
+    bool any = false;
+    for (u32 p = wrank(m); p < K.nblk && !any; p += wsize(m))
+        any = (K.sx[2 * p] == b || K.sx[2 * p + 1] == b) && blk_reach(K, p);
+    return wor(m, any ? 1u : 0u) != 0;
+}
+
+// Whether the flow graph has no cycle (Kahn's algorithm over the successor
+// pairs).  normalize_if_else's rewrites never create one: a new edge
+// header -> else or pred -> join shortcuts a path that already existed, and
+// split_block only inserts a block on an edge.
+OD_NOINL bool flow_acyclic(KCtx &K) {
+    const u32 nb = K.nblk;
+    u32 *indeg = K.stamp, *q = K.work;
+    for (u32 b = 0; b < nb; ++b)
+        indeg[b] = 0;
+    for (u32 b = 0; b < nb; ++b)
+        for (u32 k = 0; k < 2; ++k)
+            if (K.sx[2 * b + k] != kNoSucc)
+                indeg[K.sx[2 * b + k]]++;
+    u32 qh = 0, qt = 0;
+    for (u32 b = 0; b < nb; ++b)
+        if (!indeg[b])
+            q[qt++] = b;
+    while (qh < qt) {
+        const u32 b = q[qh++];
+        for (u32 k = 0; k < 2; ++k) {
+            const u32 t = K.sx[2 * b + k];
+            if (t != kNoSucc && --indeg[t] == 0)
+                q[qt++] = t;
+        }
+    }
+    for (u32 b = 0; b < nb; ++b) // the traversal stamps start clear again
+        K.stamp[b] = 0;
+    K.stamp_gen = 0;
+    return qt == nb;
 }
 
 struct MaskPattern {
@@ -1506,6 +1560,7 @@ OD_NOINL bool apply_mask_pattern(KCtx &K, const MaskPattern &pat, u32 *touched, 
     const i32 invert = first_exec_op_is(K, (u32)stop, XK_INVERT, pat.mask) ? stop : -1;
     i32 then_entry = pat.then_entry, else_entry = -1, join = -1;
     bool reach_may_shrink = false;
+    i32 reach_drop = -1; // the one block that leaves the reachable set (acyclic shortcut)
     *ntouched = 0;
     if (invert >= 0) {
         Block &ib = K.blk[invert];
@@ -1520,11 +1575,20 @@ OD_NOINL bool apply_mask_pattern(KCtx &K, const MaskPattern &pat, u32 *touched, 
             K.supp[ib.ib] = 1;
             if (ib.ie - ib.ib > 1)
                 K.supp[ib.ib + 1] = 1;
-            retarget_preds(K, invert, join, pat.header);
+            const bool join_fed = retarget_preds(K, invert, join, pat.header);
             ib.absorbed = 1;
             ib.nsucc = 0;
             sync_succ(K, (u32)invert);
             reach_may_shrink = true;
+            // On an acyclic graph the inverted block is the only block that can
+            // drop out, unless the join lost its last reachable predecessor:
+            // every other block that lost an in-edge (the else entry) gained
+            // one from the header, and in an acyclic graph a set in which every
+            // non-entry block has a predecessor in the set is reachable.
+            if (K.acyclic && join >= 0 && (join_fed || has_reachable_pred(K, (u32)join))) {
+                reach_may_shrink = false;
+                reach_drop = invert;
+            }
         } else {
             i32 rstop = -1;
             u32 nr = mask_stops(K, ib.succ, ib.nsucc, pat.mask, invert, &rstop);
@@ -1567,10 +1631,13 @@ OD_NOINL bool apply_mask_pattern(KCtx &K, const MaskPattern &pat, u32 *touched, 
     // reachability can only shrink, and it can only shrink when the inverted
     // block loses its out-edges (invert-only form); in the other forms the
     // edge changes keep every block reachable, so the walk is skipped.
-    if (reach_may_shrink)
+    if (reach_may_shrink) {
         mark_reachable(K);
+    } else if (reach_drop >= 0) {
+        K.rbits[reach_drop >> 5] &= ~(1u << (reach_drop & 31));
+    }
 #ifdef OD_HOST_CHECK
-    else {
+    if (!reach_may_shrink) {
         for (u32 b = 0; b < K.nblk; ++b)
             K.stamp[b] = blk_reach(K, b);
         mark_reachable(K);
@@ -1588,6 +1655,7 @@ OD_NOINL bool apply_mask_pattern(KCtx &K, const MaskPattern &pat, u32 *touched, 
 // normalize_if_else  structurizer.cpp:613-654
 OD_NOINL void normalize(KCtx &K) {
     canonicalize(K);
+    K.acyclic = flow_acyclic(K);
     const u32 nb = K.nblk;
     for (u32 scan = 0; scan < nb; ++scan) {
         Block &b = K.blk[scan];
