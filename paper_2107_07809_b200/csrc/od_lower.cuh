@@ -1028,34 +1028,44 @@ OD_NOINL void abi_entry_state(KCtx &K) {
 
 // Collects the slots touched since log position p0 as a sorted delta on the
 // delta stack; returns (start, count).
+// The slots an arm touched (its undo-log entries from p0), ascending, with
+// their current values, pushed on the delta stack.  Split across the lanes
+// executing it: the log entries into per-lane slot bitmaps (OR-reduced), then
+// one lane per bitmap word writes that word's entries at their prefix rank.
 OD_NOINL void collect_delta(KCtx &K, u32 p0, u32 *start, u32 *count) {
+    const u32 m = wmask(), r = wrank(m), nl = wsize(m);
     u32 bm[kLiveWords];
     for (u32 w = 0; w < kLiveWords; ++w)
         bm[w] = 0;
-    for (u32 i = p0; i < K.nlog; ++i) {
-        u32 p = K.log[i].phys;
+    for (u32 i = p0 + r; i < K.nlog; i += nl) {
+        const u32 p = K.log[i].phys;
         bm[p >> 5] |= 1u << (p & 31);
     }
-    *start = K.ndstk;
+    u32 total = 0;
     for (u32 w = 0; w < kLiveWords; ++w) {
-        u32 m = bm[w];
-        while (m) {
-            u32 bit = ctz32(m);
-            m &= m - 1;
-            u32 p = w * 32 + bit;
-            if (K.ndstk >= K.dstk_cap) {
-                K.oom = true;
-                *count = K.ndstk - *start;
-                return;
-            }
-            K.dstk_id[K.ndstk] = p;
-            K.dstk[K.ndstk] = K.regs[p];
-            K.ndstk++;
-            if (K.ndstk > K.dstk_hw)
-                K.dstk_hw = K.ndstk;
+        bm[w] = wor(m, bm[w]);
+        total += popc32(bm[w]);
+    }
+    *start = K.ndstk;
+    const u32 room = K.dstk_cap > K.ndstk ? K.dstk_cap - K.ndstk : 0;
+    const u32 n = total < room ? total : room;
+    for (u32 w = r; w < kLiveWords; w += nl) {
+        u32 q = 0;
+        for (u32 v = 0; v < w; ++v)
+            q += popc32(bm[v]);
+        for (u32 bits = bm[w]; bits && q < n; bits &= bits - 1, ++q) {
+            const u32 p = w * 32 + ctz32(bits);
+            K.dstk_id[K.ndstk + q] = p;
+            K.dstk[K.ndstk + q] = K.regs[p];
         }
     }
-    *count = K.ndstk - *start;
+    wsync(m);
+    if (n < total)
+        K.oom = true; // the kernel is re-run with a larger arena
+    K.ndstk += n;
+    if (K.ndstk > K.dstk_hw)
+        K.dstk_hw = K.ndstk;
+    *count = n;
 }
 
 OD_INL u32 half_view(KCtx &K, const Slot &s) {
@@ -1066,90 +1076,167 @@ OD_INL u32 half_view(KCtx &K, const Slot &s) {
     return s.expr;
 }
 
+// The undo record of slot p at log position at (log_slot's record).
+OD_INL void log_at(KCtx &K, u32 at, u32 p) {
+    UndoRec &u = K.log[at];
+    const Slot &s = K.regs[p];
+    u.phys = p;
+    u.version = s.version;
+    u.expr = s.expr;
+    u.type = s.type;
+    u.integ = s.integ;
+}
+
 // merge_at_join (sym_state.cpp:866-957) + emit_join (lower.cpp:89-121) for
 // the union of touched slots.  regs must hold the split state S0.
+// Split across the lanes executing it (north star (4)): the union of the two
+// arms' sorted delta lists is a bitmap; each lane takes bitmap words, finds a
+// slot's then / else values at its rank in each list, and settles the slots
+// that pass through or die (not live at the join) itself.  The live joins,
+// which mint names, statements and expressions in slot order, are then
+// settled in ascending slot order as the reference does.  Undo records go
+// to the log at each slot's rank in the union, the reference's order.
 OD_NOINL void merge_join(KCtx &K, const Frame &F, u32 td, u32 tn, u32 ed, u32 en, bool has_else,
-                       const u32 *live) {
-    u32 i = 0, j = 0;
-    while (i < tn || j < en) {
-        u32 pt = i < tn ? K.dstk_id[td + i] : 0xffffffffu;
-        u32 pe = j < en ? K.dstk_id[ed + j] : 0xffffffffu;
-        u32 p = pt < pe ? pt : pe;
-        Slot a = K.regs[p], b = K.regs[p];
-        if (pt == p) {
-            a = K.dstk[td + i];
-            ++i;
+                         const u32 *live) {
+    const u32 m = wmask(), r = wrank(m), nl = wsize(m);
+    u32 Tm[kLiveWords], Em[kLiveWords], Jm[kLiveWords];
+    for (u32 w = 0; w < kLiveWords; ++w)
+        Tm[w] = Em[w] = Jm[w] = 0;
+    for (u32 i = r; i < tn; i += nl) {
+        const u32 p = K.dstk_id[td + i];
+        Tm[p >> 5] |= 1u << (p & 31);
+    }
+    for (u32 j = r; j < en; j += nl) {
+        const u32 p = K.dstk_id[ed + j];
+        Em[p >> 5] |= 1u << (p & 31);
+    }
+    u32 nu = 0;
+    for (u32 w = 0; w < kLiveWords; ++w) {
+        Tm[w] = wor(m, Tm[w]);
+        Em[w] = wor(m, Em[w]);
+        nu += popc32(Tm[w] | Em[w]);
+    }
+    const u32 log0 = K.nlog;
+    const bool logging = K.log_depth != 0;
+    if (logging && log0 + nu > K.log_cap)
+        K.oom = true; // the kernel is re-run with a larger arena
+    const bool rec = logging && !K.oom;
+    auto sides = [&](u32 w, u32 bit, u32 rt, u32 re, Slot *a, Slot *b) {
+        const u32 p = w * 32 + bit, below = (1u << bit) - 1;
+        *a = (Tm[w] >> bit) & 1 ? K.dstk[td + rt + popc32(Tm[w] & below)] : K.regs[p];
+        *b = (Em[w] >> bit) & 1 ? K.dstk[ed + re + popc32(Em[w] & below)] : K.regs[p];
+    };
+    for (u32 w = r; w < kLiveWords; w += nl) {
+        u32 rt = 0, re = 0, ru = 0; // list ranks before this word
+        for (u32 v = 0; v < w; ++v) {
+            rt += popc32(Tm[v]);
+            re += popc32(Em[v]);
+            ru += popc32(Tm[v] | Em[v]);
         }
-        if (pe == p) {
-            b = K.dstk[ed + j];
-            ++j;
-        }
-        Slot m = a; // merged starts as the then state
-        if (p == 360) {
-            // exec halves are skipped: the then side passes through
-        } else if (a.version == b.version &&
-                   (!a.expr || !b.expr || expr_equal(K.E, a.expr, b.expr, K.eqst))) {
-            if (!a.expr && b.expr)
-                m = b;
-        } else {
-            u32 top = a.version > b.version ? a.version : b.version;
-            u32 id = dense_of_phys(p);
-            if (!lv_test(live, id)) {
-                m.version = top;
-                m.expr = 0;
-                m.type = DT_UNKNOWN;
-                m.integ = IN_ENTIRE;
+        const u32 U = Tm[w] | Em[w];
+        u32 jm = 0;
+        for (u32 bits = U; bits; bits &= bits - 1) {
+            const u32 bit = ctz32(bits), p = w * 32 + bit;
+            Slot a, b;
+            sides(w, bit, rt, re, &a, &b);
+            Slot mg = a; // merged starts as the then state
+            if (p == 360) {
+                // exec halves are skipped: the then side passes through
+            } else if (a.version == b.version &&
+                       (!a.expr || !b.expr || expr_equal(K.E, a.expr, b.expr, K.eqst))) {
+                if (!a.expr && b.expr)
+                    mg = b;
             } else {
-                u32 tv, ev;
-                if (p >= 361) { // vcc, scc, m0: raw slot expressions
-                    tv = a.expr;
-                    ev = b.expr;
-                } else {
-                    tv = a.expr ? half_view(K, a) : 0;
-                    ev = b.expr ? half_view(K, b) : 0;
+                const u32 top = a.version > b.version ? a.version : b.version;
+                if (lv_test(live, dense_of_phys(p))) {
+                    jm |= 1u << bit; // live: settled below, in slot order
+                    continue;
                 }
-                DT vt = DT_B32;
-                if (tv && ev)
-                    vt = dt_unify(K.E.n[tv].type, K.E.n[ev].type);
-                else if (tv)
-                    vt = K.E.n[tv].type;
-                else if (ev)
-                    vt = K.E.n[ev].type;
-                if (dt_is_unknown(vt) || dt_is_pointer(vt))
-                    vt = dt_bits(vt) == 64 ? DT_B64 : DT_B32;
-                u32 serial = top + 1;
-                while (!K.pool.insert(p, serial))
-                    ++serial;
-                // emit_join for this fixup
-                u32 d = new_stmt(K, SK_DECL);
-                K.st[d].cls = (u16)p;
-                K.st[d].a = serial;
-                K.st[d].c = vt;
-                if (!has_else && ev)
-                    K.st[d].b = ev;
-                list_append(K, F.out, d);
-                if (tv) {
-                    u32 s = new_stmt(K, SK_ASSIGN);
-                    K.st[s].cls = (u16)p;
-                    K.st[s].a = serial;
-                    K.st[s].b = tv;
-                    list_append(K, F.then_l, s);
-                }
-                if (has_else && ev) {
-                    u32 s = new_stmt(K, SK_ASSIGN);
-                    K.st[s].cls = (u16)p;
-                    K.st[s].a = serial;
-                    K.st[s].b = ev;
-                    list_append(K, F.else_l, s);
-                }
-                m.version = top + 1;
-                m.expr = K.E.var(p, serial, vt);
-                m.type = vt;
-                m.integ = IN_ENTIRE;
+                mg.version = top;
+                mg.expr = 0;
+                mg.type = DT_UNKNOWN;
+                mg.integ = IN_ENTIRE;
             }
+            if (rec)
+                log_at(K, log0 + ru + popc32(U & ((1u << bit) - 1)), p);
+            K.regs[p] = mg;
         }
-        log_slot(K, p);
-        K.regs[p] = m;
+        Jm[w] = jm;
+    }
+    for (u32 w = 0; w < kLiveWords; ++w) {
+        Jm[w] = wor(m, Jm[w]);
+        K.dirty[w] |= Tm[w] | Em[w];
+    }
+    wsync(m);
+    // the live joins, ascending (names, statements and expressions are minted
+    // in this order)
+    u32 rt = 0, re = 0, ru = 0;
+    for (u32 w = 0; w < kLiveWords; ++w) {
+        const u32 U = Tm[w] | Em[w];
+        for (u32 bits = Jm[w]; bits; bits &= bits - 1) {
+            const u32 bit = ctz32(bits), p = w * 32 + bit;
+            Slot a, b;
+            sides(w, bit, rt, re, &a, &b);
+            Slot mg = a;
+            const u32 top = a.version > b.version ? a.version : b.version;
+            u32 tv, ev;
+            if (p >= 361) { // vcc, scc, m0: raw slot expressions
+                tv = a.expr;
+                ev = b.expr;
+            } else {
+                tv = a.expr ? half_view(K, a) : 0;
+                ev = b.expr ? half_view(K, b) : 0;
+            }
+            DT vt = DT_B32;
+            if (tv && ev)
+                vt = dt_unify(K.E.n[tv].type, K.E.n[ev].type);
+            else if (tv)
+                vt = K.E.n[tv].type;
+            else if (ev)
+                vt = K.E.n[ev].type;
+            if (dt_is_unknown(vt) || dt_is_pointer(vt))
+                vt = dt_bits(vt) == 64 ? DT_B64 : DT_B32;
+            u32 serial = top + 1;
+            while (!K.pool.insert(p, serial))
+                ++serial;
+            // emit_join for this fixup
+            u32 d = new_stmt(K, SK_DECL);
+            K.st[d].cls = (u16)p;
+            K.st[d].a = serial;
+            K.st[d].c = vt;
+            if (!has_else && ev)
+                K.st[d].b = ev;
+            list_append(K, F.out, d);
+            if (tv) {
+                u32 st = new_stmt(K, SK_ASSIGN);
+                K.st[st].cls = (u16)p;
+                K.st[st].a = serial;
+                K.st[st].b = tv;
+                list_append(K, F.then_l, st);
+            }
+            if (has_else && ev) {
+                u32 st = new_stmt(K, SK_ASSIGN);
+                K.st[st].cls = (u16)p;
+                K.st[st].a = serial;
+                K.st[st].b = ev;
+                list_append(K, F.else_l, st);
+            }
+            mg.version = top + 1;
+            mg.expr = K.E.var(p, serial, vt);
+            mg.type = vt;
+            mg.integ = IN_ENTIRE;
+            if (rec)
+                log_at(K, log0 + ru + popc32(U & ((1u << bit) - 1)), p);
+            K.regs[p] = mg;
+        }
+        rt += popc32(Tm[w]);
+        re += popc32(Em[w]);
+        ru += popc32(U);
+    }
+    if (rec) {
+        K.nlog = log0 + nu;
+        if (K.nlog > K.log_hw)
+            K.log_hw = K.nlog;
     }
 }
 

@@ -5,7 +5,32 @@
 
 namespace od {
 
+// One kernel per warp (lanes_per == 32): a kernel with if-joins is lowered
+// by the whole warp redundantly (od_base.cuh "warp cooperation"), so its
+// joins (merge_join, collect_delta) split their slot work across the lanes;
+// a straight-line or goto-form kernel is lowered by lane 0 alone.
+__device__ __noinline__ void lower_warp(const DecompArgs &a) {
+    const u32 full = 0xffffffffu;
+    Slot0 sl{0, 0, nullptr};
+    const bool mine = dk_slot(a, &sl);
+    if (!__shfl_sync(full, mine, 0))
+        return;
+    KState *g = reinterpret_cast<KState *>(__shfl_sync(full, (unsigned long long)sl.base, 0));
+    if (g->done)
+        return;
+    if (!g->K.nif && (threadIdx.x & 31))
+        return;
+    kstate_fix(*g); // the previous phase ran on a local copy: re-point into HBM
+    dk_lower(*g);
+}
+
 __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_LOWER * 128 / OD_BLOCK) k_lower(DecompArgs a) {
+#if !OD_LOCAL_LOWER
+    if (a.lanes_per == 32) {
+        lower_warp(a);
+        return;
+    }
+#endif
     Slot0 sl;
     if (!dk_slot(a, &sl))
         return;
