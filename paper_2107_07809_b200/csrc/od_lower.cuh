@@ -1142,10 +1142,12 @@ OD_NOINL void merge_join(KCtx &K, const Frame &F, u32 td, u32 tn, u32 ed, u32 en
             Slot mg = a; // merged starts as the then state
             if (p == 360) {
                 // exec halves are skipped: the then side passes through
-            } else if (a.version == b.version &&
-                       (!a.expr || !b.expr || expr_equal(K.E, a.expr, b.expr, K.eqst))) {
+            } else if (a.version == b.version && (!a.expr || !b.expr || a.expr == b.expr)) {
                 if (!a.expr && b.expr)
                     mg = b;
+            } else if (a.version == b.version) {
+                jm |= 1u << bit; // structural comparison (one shared scratch stack): settled below
+                continue;
             } else {
                 const u32 top = a.version > b.version ? a.version : b.version;
                 if (lv_test(live, dense_of_phys(p))) {
@@ -1168,8 +1170,8 @@ OD_NOINL void merge_join(KCtx &K, const Frame &F, u32 td, u32 tn, u32 ed, u32 en
         K.dirty[w] |= Tm[w] | Em[w];
     }
     wsync(m);
-    // the live joins, ascending (names, statements and expressions are minted
-    // in this order)
+    // the live joins and the structural comparisons, ascending (names,
+    // statements and expressions are minted in this order)
     u32 rt = 0, re = 0, ru = 0;
     for (u32 w = 0; w < kLiveWords; ++w) {
         const u32 U = Tm[w] | Em[w];
@@ -1179,6 +1181,25 @@ OD_NOINL void merge_join(KCtx &K, const Frame &F, u32 td, u32 tn, u32 ed, u32 en
             sides(w, bit, rt, re, &a, &b);
             Slot mg = a;
             const u32 top = a.version > b.version ? a.version : b.version;
+            const u32 at = log0 + ru + popc32(U & ((1u << bit) - 1));
+            if (a.version == b.version) {
+                if (expr_equal(K.E, a.expr, b.expr, K.eqst)) { // pass-through
+                    if (rec)
+                        log_at(K, at, p);
+                    K.regs[p] = mg;
+                    continue;
+                }
+                if (!lv_test(live, dense_of_phys(p))) { // dies at the join
+                    mg.version = top;
+                    mg.expr = 0;
+                    mg.type = DT_UNKNOWN;
+                    mg.integ = IN_ENTIRE;
+                    if (rec)
+                        log_at(K, at, p);
+                    K.regs[p] = mg;
+                    continue;
+                }
+            }
             u32 tv, ev;
             if (p >= 361) { // vcc, scc, m0: raw slot expressions
                 tv = a.expr;
@@ -1226,7 +1247,7 @@ OD_NOINL void merge_join(KCtx &K, const Frame &F, u32 td, u32 tn, u32 ed, u32 en
             mg.type = vt;
             mg.integ = IN_ENTIRE;
             if (rec)
-                log_at(K, log0 + ru + popc32(U & ((1u << bit) - 1)), p);
+                log_at(K, at, p);
             K.regs[p] = mg;
         }
         rt += popc32(Tm[w]);
