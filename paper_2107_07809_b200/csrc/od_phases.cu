@@ -5,10 +5,12 @@
 
 namespace od {
 
-// One kernel per warp (lanes_per == 32): a kernel with if-joins is lowered
+constexpr u32 kWideJoins = 64;
+
+// One kernel per warp (lanes_per == 32): a kernel with many if-joins is lowered
 // by the whole warp redundantly (od_base.cuh "warp cooperation"), so its
 // joins (merge_join, collect_delta) split their slot work across the lanes;
-// a straight-line or goto-form kernel is lowered by lane 0 alone.
+// other kernels are lowered by lane 0 alone.
 __device__ __noinline__ void lower_warp(const DecompArgs &a) {
     const u32 full = 0xffffffffu;
     Slot0 sl{0, 0, nullptr};
@@ -18,7 +20,10 @@ __device__ __noinline__ void lower_warp(const DecompArgs &a) {
     KState *g = reinterpret_cast<KState *>(__shfl_sync(full, (unsigned long long)sl.base, 0));
     if (g->done)
         return;
-    if (!g->K.nif && (threadIdx.x & 31))
+    // kWideJoins: below it the per-slot parallelism does not pay for the
+    // wider local-memory traffic of 32 active lanes (C4: k_lower +3 % with
+    // every joined kernel on the warp; C5's long kernels gain)
+    if (g->K.nif < kWideJoins && (threadIdx.x & 31))
         return;
     kstate_fix(*g); // the previous phase ran on a local copy: re-point into HBM
     dk_lower(*g);
