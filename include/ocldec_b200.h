@@ -171,6 +171,13 @@ int ocldec_b200_session_names(ocldec_b200_session *s, uint64_t *off, uint32_t *l
  * count, or -2 when cap < *need. */
 int ocldec_b200_session_diagnostics(ocldec_b200_session *s, char *buf, uint64_t cap, uint64_t *need);
 
+/* Whether session runs keep per-kernel host records (default 1): kernel
+ * names, source spans, flags and diagnostics for session_kernels /
+ * session_names / session_diagnostics.  With 0 the per-kernel results stay
+ * on the device and a run only gathers its totals (session_stats) and
+ * combined_source: no per-kernel device-to-host traffic or host loops. */
+int ocldec_b200_session_set_records(ocldec_b200_session *s, int keep);
+
 /* cudaMemcpy(dst, src, n, cudaMemcpyDefault): host<->device staging helper
  * for callers without their own CUDA runtime binding. */
 int ocldec_b200_copy(void *dst, const void *src, uint64_t n);

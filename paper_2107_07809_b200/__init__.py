@@ -267,6 +267,12 @@ class Session:
         if rc:
             raise RuntimeError(f"session_run failed ({rc}): {_lib.last_error()}")
 
+    def set_records(self, keep: bool):
+        """Keep per-kernel host records (names, spans, flags, diagnostics) of
+        later runs (default True); False leaves them on the device and only
+        totals and combined_source come back."""
+        self._L.ocldec_b200_session_set_records(self._s, int(keep))
+
     def run_generated(self, shape: Union[int, str], count: int, seed: int = 1, k0: int = 0, stress: bool = False,
                       chunk_bytes: int = 0, sample_stride: int = 0, fold_local_size: bool = False):
         """Streams kernels [k0, k0+count) of a generated corpus through the

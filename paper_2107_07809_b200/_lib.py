@@ -73,6 +73,7 @@ EXPORTS = [
     "ocldec_b200_session_kernels", "ocldec_b200_gen_host", "ocldec_b200_gen_device",
     "ocldec_b200_session_run_host", "ocldec_b200_copy", "ocldec_b200_abi_map_check",
     "ocldec_b200_session_names", "ocldec_b200_session_diagnostics", "ocldec_b200_session_run_generated",
+    "ocldec_b200_session_set_records",
 ]
 
 _lib = None
@@ -126,6 +127,8 @@ def load():
     L.ocldec_b200_session_run_generated.argtypes = [vp, i32, i32, u64, u64, u64, u64, i32, u64, vp, vp,
                                                     ctypes.POINTER(StreamStats)]
     L.ocldec_b200_session_run_generated.restype = i32
+    L.ocldec_b200_session_set_records.argtypes = [vp, i32]
+    L.ocldec_b200_session_set_records.restype = i32
     _lib = L
     return L
 

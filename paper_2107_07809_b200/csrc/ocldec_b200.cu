@@ -501,6 +501,34 @@ struct U32SumLoad64 {
     __device__ U64Val operator()(u64 i) const { return U64Val{p[i]}; }
 };
 
+// Per-chunk totals of the kernel results (the session path without
+// per-kernel host records): instructions, failed, goto form, fallbacks.
+__global__ void k_res_stats(const KRes *__restrict__ res, u32 nk, unsigned long long *tot) {
+    const u32 k = blockIdx.x * blockDim.x + threadIdx.x;
+    u64 ni = 0;
+    u32 f = 0, g = 0, fb = 0;
+    if (k < nk) {
+        const KRes r = res[k];
+        ni = r.ninstr;
+        f = r.status == KS_FAILED;
+        g = r.status == KS_OK && !r.structured;
+        fb = r.fallbacks;
+    }
+    const u32 full = 0xffffffffu;
+    for (u32 d = 16; d; d >>= 1) {
+        ni += __shfl_down_sync(full, ni, d);
+        f += __shfl_down_sync(full, f, d);
+        g += __shfl_down_sync(full, g, d);
+        fb += __shfl_down_sync(full, fb, d);
+    }
+    if ((threadIdx.x & 31) == 0 && (ni | f | g | fb)) {
+        atomicAdd(&tot[0], (unsigned long long)ni);
+        atomicAdd(&tot[1], (unsigned long long)f);
+        atomicAdd(&tot[2], (unsigned long long)g);
+        atomicAdd(&tot[3], (unsigned long long)fb);
+    }
+}
+
 // Diagnostic spans of a chunk packed into one buffer (one D2H instead of a
 // copy per span): warp per span, spans[i] = {src offset, length, dst offset}.
 __global__ void k_span_gather(const u8 *__restrict__ t, const uint4 *__restrict__ spans, u32 n, u8 *out) {
@@ -815,6 +843,8 @@ struct ocldec_b200_session {
     std::vector<OvrDiag> ovr_diags;  // their parse diagnostics
     DevBuf dovr, dovr_text;
     DevBuf sgen;                     // streamed generation: the current group of chunks
+    DevBuf rstat;                    // per-chunk result totals (k_res_stats)
+    bool keep_records = true;        // per-kernel host records (names, spans, flags, diagnostics)
     u32 novr = 0;
     std::vector<u64> host_kdiag;     // per kernel: first host_diag index (count in host_res[k].ndiag)
     size_t pev_used = 0;
@@ -1049,6 +1079,8 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     a.only = s->only_set ? P<u8>(s->only) : nullptr;
     a.only_len = s->only_len;
     a.prof = s->prof_on ? P<u64>(s->prof) : nullptr;
+    a.retry_cnt = cnt + 12;
+    CK(cudaMemsetAsync(cnt + 12, 0, 4, st));
     const u32 kb = 256, kg = (nk + kb - 1) / kb;
     u32 *key = P<u32>(s->kmeta);
     if (ensure(s->ksizes, (u64)nk * sizeof(KSize) + 16))
@@ -1169,6 +1201,12 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     u32 scale = 1;
     std::vector<KSize> zs;
     for (int attempt = 0;; ++attempt) {
+        u32 nretry = 0; // counted by k_emit: the results are copied only when some kernel must re-run
+        if (d2h_sync(s, &nretry, cnt + 12, 4))
+            return -3;
+        if (!nretry)
+            break;
+        CK(cudaMemsetAsync(cnt + 12, 0, 4, st));
         if (d2h_sync(s, hr.data(), a.res, (u64)nk * sizeof(KRes)))
             return -3;
         std::vector<u32> redo;
@@ -1284,6 +1322,31 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     CK(cudaGetLastError());
     CK(cudaEventRecord(s->ev[4], st));
     co->out_bytes = (base - out_base) + chunk_bytes;
+    if (!s->keep_records) {
+        // totals only: the per-kernel results stay on the device
+        if (ensure(s->rstat, 64))
+            return -3;
+        CK(cudaMemsetAsync(s->rstat.p, 0, 32, st));
+        k_res_stats<<<(nk + 255) / 256, 256, 0, st>>>(a.res, nk, P<unsigned long long>(s->rstat));
+        s->stats.total_launches++;
+        CK(cudaGetLastError());
+        u64 tot[4];
+        if (d2h_sync(s, tot, s->rstat.p, 32))
+            return -3;
+        s->stats.instructions += tot[0];
+        s->stats.failed += tot[1];
+        s->stats.goto_form += tot[2];
+        s->stats.fallbacks += tot[3];
+        float ms2 = 0;
+        cudaEventElapsedTime(&ms2, s->ev[0], s->ev[2]);
+        s->stats.ms_parse += ms2;
+        cudaEventElapsedTime(&ms2, s->ev[2], s->ev[3]);
+        s->stats.ms_decompile += ms2;
+        cudaEventElapsedTime(&ms2, s->ev[3], s->ev[4]);
+        s->stats.ms_emit += ms2;
+        sum_phase_events(s);
+        return 0;
+    }
     // keep per-kernel results for the host API
     if (d2h_sync(s, hr.data(), a.res, (u64)nk * sizeof(KRes)))
         return -3;
@@ -1748,7 +1811,7 @@ void ocldec_b200_session_destroy(ocldec_b200_session *s) {
                       &s->outoff, &s->out, &s->only, &s->retry, &s->gen_len, &s->gen_ninstr,
                       &s->gen_buf, &s->gen_off, &s->kmeta, &s->order, &s->budget, &s->sbudget,
                       &s->boff, &s->hist, &s->prof, &s->ksizes, &s->dpool, &s->dtop, &s->perm, &s->cnt4,
-                      &s->dovr, &s->dovr_text, &s->xtext, &s->xrec, &s->xtop, &s->xcfg, &s->sgen};
+                      &s->dovr, &s->dovr_text, &s->xtext, &s->xrec, &s->xtop, &s->xcfg, &s->sgen, &s->rstat};
     for (DevBuf *b : bufs)
         if (b->p)
             cudaFree(b->p);
@@ -1813,6 +1876,13 @@ int ocldec_b200_session_run(ocldec_b200_session *s, const void *d_listing, size_
     s->stats.out_bytes = out_pos;
     if (sync)
         CK(cudaStreamSynchronize(s->stream));
+    return 0;
+}
+
+int ocldec_b200_session_set_records(ocldec_b200_session *s, int keep) {
+    if (!s)
+        return -1;
+    s->keep_records = keep != 0;
     return 0;
 }
 

@@ -57,6 +57,7 @@ struct DecompArgs {
     u64 dcap;
     unsigned long long *dtop;
     const KSize *sizes; // per kernel (k_ksize)
+    u32 *retry_cnt;     // kernels that ended out of arena or staging room (k_emit counts them)
 };
 
 // Three launches per wave, one per pipeline phase (od_lower.cuh dk_front /

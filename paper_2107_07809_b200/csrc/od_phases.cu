@@ -161,6 +161,8 @@ __device__ __noinline__ void emit_one(const DecompArgs &a, const Slot0 &sl, cons
             r.diag_off = dof;
         }
     }
+    if (r.status == KS_OOM || r.status == KS_STAGE_FULL)
+        atomicAdd(a.retry_cnt, 1u);
     a.res[k] = r;
 }
 

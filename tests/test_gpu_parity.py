@@ -313,3 +313,25 @@ def test_comment_heavy_chunk_retries_smaller(monkeypatch):
     monkeypatch.setenv("OCLDEC_B200_CHUNK_BYTES", str(1 << 30))
     b = P.decompile_listing(listing)
     assert a.combined == b.combined and len(a.kernels) == 300_000
+
+
+def test_session_without_host_records_matches():
+    """ocldec_b200_session_set_records(0): the same combined output and totals
+    as a run that keeps per-kernel host records (the bench's device path)."""
+    listing, offs, ni = P.generate_corpus("C3", 3000, seed=71, stress=True)
+    import ctypes
+    s = P.Session(0)
+    try:
+        buf = ctypes.create_string_buffer(listing, len(listing))
+        out = []
+        for keep in (True, False):
+            s.set_records(keep)
+            cap = len(listing) * 3 + (1 << 20)
+            host_out = ctypes.create_string_buffer(cap)
+            n = s.run_host(ctypes.addressof(buf), len(listing), ctypes.addressof(host_out), cap)
+            st = s.stats()
+            out.append((host_out.raw[:n], st["instructions"], st["failed"], st["goto_form"], st["fallbacks"]))
+        assert out[0] == out[1]
+        assert out[0][0] == P.decompile_listing(listing).combined and out[0][1] == ni
+    finally:
+        s.close()
