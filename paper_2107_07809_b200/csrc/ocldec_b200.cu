@@ -462,7 +462,11 @@ struct OutOffStore {
 };
 
 // Warp per kernel: staging -> combined output (+ the "\n" separator that
-// combined_source puts between non-empty sources).
+// combined_source puts between non-empty sources).  The staged text is
+// 16-byte aligned, its destination is not: the head up to the destination's
+// next 16-byte boundary and the tail go bytewise; the body is written as
+// aligned 16-byte stores, each assembled from two aligned 16-byte source
+// loads with byte permutes (the source misalignment is the head length).
 __global__ void k_gather(const KRes *__restrict__ res, const u64 *__restrict__ off, u32 nk,
                          const u8 *__restrict__ stage, u8 *out, u64 out_base, u64 total) {
     const u64 warp = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -474,10 +478,32 @@ __global__ void k_gather(const KRes *__restrict__ res, const u64 *__restrict__ o
         return;
     const u8 *s = stage + r.stage_off;
     u8 *d = out + out_base + off[warp];
-    for (u32 i = lane; i < r.out_len; i += 32)
+    const u32 n = r.out_len;
+    const u32 h = min((u32)((16 - ((uintptr_t)d & 15)) & 15), n);
+    if (lane < h)
+        d[lane] = s[lane];
+    const u32 nv = (n - h) / 16;
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(s); // s + h + 16q spans s4[q], s4[q + 1] when h > 0
+    uint4 *d4 = reinterpret_cast<uint4 *>(d + h);
+    const u32 sh = h & 3, wo = h >> 2; // byte and word offset of the body in the source
+    for (u32 q = lane; q < nv; q += 32) {
+        if (!h) {
+            d4[q] = s4[q];
+            continue;
+        }
+        const uint4 a = s4[q], b = s4[q + 1];
+        const u32 w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        u32 o[4];
+        for (u32 k = 0; k < 4; ++k) {
+            const u32 lo = w[wo + k], hi = w[wo + k + 1 < 8 ? wo + k + 1 : 7];
+            o[k] = sh ? __byte_perm(lo, hi, 0x3210 + 0x1111 * sh) : lo;
+        }
+        d4[q] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+    for (u32 i = h + 16 * nv + lane; i < n; i += 32)
         d[i] = s[i];
-    if (lane == 0 && out_base + off[warp] + r.out_len < total)
-        d[r.out_len] = '\n';
+    if (lane == 0 && out_base + off[warp] + n < total)
+        d[n] = '\n';
 }
 
 struct U64Load {
