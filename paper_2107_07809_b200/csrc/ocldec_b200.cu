@@ -245,7 +245,8 @@ constexpr u32 kDecodeStage = 16384;
 __global__ void __launch_bounds__(256) k_decode(const u8 *__restrict__ t, u64 len, const u32 *__restrict__ nlpos,
                                                 u32 nlf, u32 nlines, const LineRec *__restrict__ lines,
                                                 LineIns *lins, const u32 *ops_off, const u32 *labs_off,
-                                                Opnd *ops, Label *labs, u32 ops_total, u32 *overflow) {
+                                                Opnd *ops, Label *labs, u32 ops_total, u32 *overflow,
+                                                const u32 *__restrict__ ops_ub) {
     __shared__ RootTable rt;
     __shared__ __align__(16) u8 stage[kDecodeStage];
     for (u32 i = threadIdx.x; i < sizeof(RootTable) / 4; i += blockDim.x)
@@ -274,8 +275,38 @@ __global__ void __launch_bounds__(256) k_decode(const u8 *__restrict__ t, u64 le
         for (u64 o = done + threadIdx.x; o < se; o += blockDim.x)
             stage[o - ab] = t[o];
     }
+    // Lines of one shape take the same decode paths: the block's lines are
+    // reordered by a shape key (operand bound from k_classify, long or
+    // short) with a counting sort in shared memory, so each warp decodes
+    // lines of similar shape (each line's decode is independent).
+    __shared__ u32 bucket[16];
+    __shared__ u16 order[256];
+    if (threadIdx.x < 16)
+        bucket[threadIdx.x] = 0;
     __syncthreads();
-    const u32 l = l0 + threadIdx.x;
+    u32 key = 15; // past the end, or not a text line
+    {
+        const u32 lk = l0 + threadIdx.x;
+        if (lk < nlines) {
+            const LineRec Lk = lines[lk];
+            if (Lk.role == LR_TEXT)
+                key = min(min(ops_ub[lk], 7u) * 2 + (Lk.len >= 36 ? 1u : 0u), 14u);
+        }
+    }
+    const u32 rank = atomicAdd(&bucket[key], 1u);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u32 acc = 0;
+        for (u32 b = 0; b < 16; ++b) {
+            const u32 c = bucket[b];
+            bucket[b] = acc;
+            acc += c;
+        }
+    }
+    __syncthreads();
+    order[bucket[key] + rank] = (u16)threadIdx.x;
+    __syncthreads();
+    const u32 l = l0 + order[threadIdx.x];
     if (l >= nlines)
         return;
     const LineRec L = lines[l];
@@ -1046,7 +1077,7 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
         return -3;
     k_decode<<<lg, lb, 0, st>>>(t, len, P<u32>(s->nlpos), nlf, nlines, P<LineRec>(s->lines), P<LineIns>(s->lins),
                                 P<u32>(s->ops_off), P<u32>(s->labs_off), P<Opnd>(s->ops), P<Label>(s->labs),
-                                pools[0], cnt + 3);
+                                pools[0], cnt + 3, P<u32>(s->ops_cnt));
     s->stats.total_launches++;
     CK(cudaGetLastError());
     CK(cudaEventRecord(s->ev[2], st));
