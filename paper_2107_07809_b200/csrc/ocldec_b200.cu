@@ -140,8 +140,34 @@ __global__ void k_classify(const u8 *__restrict__ t, u64 len, const u32 *__restr
         return;
     u32 b = l == 0 ? 0 : nlpos[l - 1] + 1;
     u32 e = l < nlf ? nlpos[l] : (u32)len;
-    bool cx;
-    u32 cut = strip_scan(t + b, e - b, &cx);
+    // one pass over the raw line: the pool bounds (separator runs, ':'
+    // count) and strip_comments' cut; a "/*" leaves the cut to strip_scan
+    bool cx = false;
+    u32 cut = e - b, runs = 0, colons = 0;
+    {
+        bool prev = false, inq = false, found = false, slow = false;
+        for (u32 i = b; i < e; ++i) {
+            const u8 c = t[i];
+            const bool sep = c == ',' || c_space(c);
+            runs += sep && !prev;
+            prev = sep;
+            colons += c == ':';
+            if (found)
+                continue;
+            if (c == '"')
+                inq = !inq;
+            if (!inq) {
+                if (c == '#' || c == ';') {
+                    cut = i - b;
+                    found = true;
+                } else if (c == '/' && i + 1 < e && t[i + 1] == '*') {
+                    found = slow = true;
+                }
+            }
+        }
+        if (slow)
+            cut = strip_scan(t + b, e - b, &cx);
+    }
     LineRec r;
     r.off = b;
     r.complex = cx;
@@ -157,20 +183,9 @@ __global__ void k_classify(const u8 *__restrict__ t, u64 len, const u32 *__restr
         atomicAdd(complex_bytes, e - b);
     }
     lines[l] = r;
-    u32 runs = 0, colons = 0;
-    if (cx || r.len) {
-        bool prev = false;
-        for (u32 i = b; i < e; ++i) {
-            const u8 c = t[i];
-            const bool sep = c == ',' || c_space(c);
-            runs += sep && !prev;
-            prev = sep;
-            colons += c == ':';
-        }
-        ++runs;
-    }
-    ops_ub[l] = runs;
-    labs_ub[l] = colons;
+    const bool content = cx || r.len;
+    ops_ub[l] = content ? runs + 1 : 0;
+    labs_ub[l] = content ? colons : 0;
 }
 
 // Complex lines (with a terminated /* */ mid-line) are materialized into the

@@ -1028,12 +1028,48 @@ OD_NOINL void abi_entry_state(KCtx &K) {
 
 // Collects the slots touched since log position p0 as a sorted delta on the
 // delta stack; returns (start, count).
+// collect_delta on a lone lane (the lowering of most kernels).
+OD_NOINL void collect_delta_seq(KCtx &K, u32 p0, u32 *start, u32 *count) {
+    u32 bm[kLiveWords];
+    for (u32 w = 0; w < kLiveWords; ++w)
+        bm[w] = 0;
+    for (u32 i = p0; i < K.nlog; ++i) {
+        u32 p = K.log[i].phys;
+        bm[p >> 5] |= 1u << (p & 31);
+    }
+    *start = K.ndstk;
+    for (u32 w = 0; w < kLiveWords; ++w) {
+        u32 m = bm[w];
+        while (m) {
+            u32 bit = ctz32(m);
+            m &= m - 1;
+            u32 p = w * 32 + bit;
+            if (K.ndstk >= K.dstk_cap) {
+                K.oom = true;
+                *count = K.ndstk - *start;
+                return;
+            }
+            K.dstk_id[K.ndstk] = p;
+            K.dstk[K.ndstk] = K.regs[p];
+            K.ndstk++;
+            if (K.ndstk > K.dstk_hw)
+                K.dstk_hw = K.ndstk;
+        }
+    }
+    *count = K.ndstk - *start;
+}
+
+
 // The slots an arm touched (its undo-log entries from p0), ascending, with
 // their current values, pushed on the delta stack.  Split across the lanes
 // executing it: the log entries into per-lane slot bitmaps (OR-reduced), then
 // one lane per bitmap word writes that word's entries at their prefix rank.
 OD_NOINL void collect_delta(KCtx &K, u32 p0, u32 *start, u32 *count) {
     const u32 m = wmask(), r = wrank(m), nl = wsize(m);
+    if (nl == 1) {
+        collect_delta_seq(K, p0, start, count);
+        return;
+    }
     u32 bm[kLiveWords];
     for (u32 w = 0; w < kLiveWords; ++w)
         bm[w] = 0;
@@ -1076,6 +1112,93 @@ OD_INL u32 half_view(KCtx &K, const Slot &s) {
     return s.expr;
 }
 
+// merge_join on a lone lane: one pass in slot order.
+OD_NOINL void merge_join_seq(KCtx &K, const Frame &F, u32 td, u32 tn, u32 ed, u32 en, bool has_else,
+                       const u32 *live) {
+    u32 i = 0, j = 0;
+    while (i < tn || j < en) {
+        u32 pt = i < tn ? K.dstk_id[td + i] : 0xffffffffu;
+        u32 pe = j < en ? K.dstk_id[ed + j] : 0xffffffffu;
+        u32 p = pt < pe ? pt : pe;
+        Slot a = K.regs[p], b = K.regs[p];
+        if (pt == p) {
+            a = K.dstk[td + i];
+            ++i;
+        }
+        if (pe == p) {
+            b = K.dstk[ed + j];
+            ++j;
+        }
+        Slot m = a; // merged starts as the then state
+        if (p == 360) {
+            // exec halves are skipped: the then side passes through
+        } else if (a.version == b.version &&
+                   (!a.expr || !b.expr || expr_equal(K.E, a.expr, b.expr, K.eqst))) {
+            if (!a.expr && b.expr)
+                m = b;
+        } else {
+            u32 top = a.version > b.version ? a.version : b.version;
+            u32 id = dense_of_phys(p);
+            if (!lv_test(live, id)) {
+                m.version = top;
+                m.expr = 0;
+                m.type = DT_UNKNOWN;
+                m.integ = IN_ENTIRE;
+            } else {
+                u32 tv, ev;
+                if (p >= 361) { // vcc, scc, m0: raw slot expressions
+                    tv = a.expr;
+                    ev = b.expr;
+                } else {
+                    tv = a.expr ? half_view(K, a) : 0;
+                    ev = b.expr ? half_view(K, b) : 0;
+                }
+                DT vt = DT_B32;
+                if (tv && ev)
+                    vt = dt_unify(K.E.n[tv].type, K.E.n[ev].type);
+                else if (tv)
+                    vt = K.E.n[tv].type;
+                else if (ev)
+                    vt = K.E.n[ev].type;
+                if (dt_is_unknown(vt) || dt_is_pointer(vt))
+                    vt = dt_bits(vt) == 64 ? DT_B64 : DT_B32;
+                u32 serial = top + 1;
+                while (!K.pool.insert(p, serial))
+                    ++serial;
+                // emit_join for this fixup
+                u32 d = new_stmt(K, SK_DECL);
+                K.st[d].cls = (u16)p;
+                K.st[d].a = serial;
+                K.st[d].c = vt;
+                if (!has_else && ev)
+                    K.st[d].b = ev;
+                list_append(K, F.out, d);
+                if (tv) {
+                    u32 s = new_stmt(K, SK_ASSIGN);
+                    K.st[s].cls = (u16)p;
+                    K.st[s].a = serial;
+                    K.st[s].b = tv;
+                    list_append(K, F.then_l, s);
+                }
+                if (has_else && ev) {
+                    u32 s = new_stmt(K, SK_ASSIGN);
+                    K.st[s].cls = (u16)p;
+                    K.st[s].a = serial;
+                    K.st[s].b = ev;
+                    list_append(K, F.else_l, s);
+                }
+                m.version = top + 1;
+                m.expr = K.E.var(p, serial, vt);
+                m.type = vt;
+                m.integ = IN_ENTIRE;
+            }
+        }
+        log_slot(K, p);
+        K.regs[p] = m;
+    }
+}
+
+
 // The undo record of slot p at log position at (log_slot's record).
 OD_INL void log_at(KCtx &K, u32 at, u32 p) {
     UndoRec &u = K.log[at];
@@ -1099,6 +1222,10 @@ OD_INL void log_at(KCtx &K, u32 at, u32 p) {
 OD_NOINL void merge_join(KCtx &K, const Frame &F, u32 td, u32 tn, u32 ed, u32 en, bool has_else,
                          const u32 *live) {
     const u32 m = wmask(), r = wrank(m), nl = wsize(m);
+    if (nl == 1) {
+        merge_join_seq(K, F, td, tn, ed, en, has_else, live);
+        return;
+    }
     u32 Tm[kLiveWords], Em[kLiveWords], Jm[kLiveWords];
     for (u32 w = 0; w < kLiveWords; ++w)
         Tm[w] = Em[w] = Jm[w] = 0;
