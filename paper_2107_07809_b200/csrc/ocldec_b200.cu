@@ -1248,6 +1248,10 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
             CK(cudaEventRecord(pe[1], ws));
             a.lanes_per = s->lanes_lower;
             k_lower<<<grid(a.lanes_per), OD_BLOCK, s->smem_lower, ws>>>(a);
+            if (a.lanes_per == 32 && !OD_LOCAL_LOWER) {
+                k_lower_wide<<<grid(a.lanes_per), OD_BLOCK, s->smem_lower, ws>>>(a);
+                s->stats.total_launches++;
+            }
             CK(cudaEventRecord(pe[2], ws));
             k_fold<<<grid(a.lanes_per), OD_BLOCK, s->smem_lower, ws>>>(a);
             CK(cudaEventRecord(pe[3], ws));
@@ -1591,12 +1595,14 @@ int session_init(ocldec_b200_session *s, int device, size_t arena_bytes) {
     s->smem_emit = occ_smem("OCLDEC_B200_OCC_EMIT");
     CK(cudaFuncSetAttribute(k_front, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CK(cudaFuncSetAttribute(k_lower, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_lower_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CK(cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     if (ensure(s->prof, 16 * 8))
         return -3;
     CK(cudaMemset(s->prof.p, 0, 16 * 8));
     CK(cudaFuncSetAttribute(k_front, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
     CK(cudaFuncSetAttribute(k_lower, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    CK(cudaFuncSetAttribute(k_lower_wide, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
     CK(cudaFuncSetAttribute(k_emit, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
     CK(cudaFuncSetAttribute(k_fold, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
     CK(cudaFuncSetAttribute(k_fold, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));

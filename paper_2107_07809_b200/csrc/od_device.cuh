@@ -142,6 +142,8 @@ __device__ __forceinline__ void kstate_store(KState *g, const KState &S) {
 
 __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_FRONT * 128 / OD_BLOCK) k_front(DecompArgs a);
 __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_LOWER * 128 / OD_BLOCK) k_lower(DecompArgs a);
+__global__ void __launch_bounds__(OD_BLOCK, OD_MINB_LOWER * 128 / OD_BLOCK) k_lower_wide(DecompArgs a);
+constexpr u32 kWideJoins = 64; // if-joins from which a kernel is lowered by the whole warp
 __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_FOLD * 128 / OD_BLOCK) k_fold(DecompArgs a);
 __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_EMIT * 128 / OD_BLOCK) k_emit(DecompArgs a);
 

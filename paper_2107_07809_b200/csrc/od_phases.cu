@@ -5,42 +5,18 @@
 
 namespace od {
 
-constexpr u32 kWideJoins = 64;
-
-// One kernel per warp (lanes_per == 32): a kernel with many if-joins is lowered
-// by the whole warp redundantly (od_base.cuh "warp cooperation"), so its
-// joins (merge_join, collect_delta) split their slot work across the lanes;
-// other kernels are lowered by lane 0 alone.
-__device__ __noinline__ void lower_warp(const DecompArgs &a) {
-    const u32 full = 0xffffffffu;
-    Slot0 sl{0, 0, nullptr};
-    const bool mine = dk_slot(a, &sl);
-    if (!__shfl_sync(full, mine, 0))
-        return;
-    KState *g = reinterpret_cast<KState *>(__shfl_sync(full, (unsigned long long)sl.base, 0));
-    if (g->done)
-        return;
-    // kWideJoins: below it the per-slot parallelism does not pay for the
-    // wider local-memory traffic of 32 active lanes (C4: k_lower +3 % with
-    // every joined kernel on the warp; C5's long kernels gain)
-    if (g->K.nif < kWideJoins && (threadIdx.x & 31))
-        return;
-    kstate_fix(*g); // the previous phase ran on a local copy: re-point into HBM
-    dk_lower(*g);
-}
-
+// Kernels with many if-joins (C5's long kernels) are lowered by the whole
+// warp redundantly (od_base.cuh "warp cooperation"), so their joins
+// (merge_join, collect_delta) split the slot work across the lanes: k_lower_
+// wide, one kernel per warp.  k_lower keeps the lone-lane lowering of every
+// other kernel in its own launch (the warp-wide entry cost the narrow path
+// 3 % on C4 when both lived in one kernel).
 __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_LOWER * 128 / OD_BLOCK) k_lower(DecompArgs a) {
-#if !OD_LOCAL_LOWER
-    if (a.lanes_per == 32) {
-        lower_warp(a);
-        return;
-    }
-#endif
     Slot0 sl;
     if (!dk_slot(a, &sl))
         return;
     KState *g = reinterpret_cast<KState *>(sl.base);
-    if (g->done)
+    if (g->done || (a.lanes_per == 32 && g->K.nif >= kWideJoins))
         return;
 #if OD_LOCAL_LOWER
     KState S;
@@ -51,6 +27,19 @@ __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_LOWER * 128 / OD_BLOCK) k_lo
     kstate_fix(*g); // the previous phase ran on a local copy: re-point into HBM
     dk_lower(*g);
 #endif
+}
+
+__global__ void __launch_bounds__(OD_BLOCK, OD_MINB_LOWER * 128 / OD_BLOCK) k_lower_wide(DecompArgs a) {
+    const u32 full = 0xffffffffu;
+    Slot0 sl{0, 0, nullptr};
+    const bool mine = dk_slot(a, &sl);
+    if (!__shfl_sync(full, mine, 0))
+        return;
+    KState *g = reinterpret_cast<KState *>(__shfl_sync(full, (unsigned long long)sl.base, 0));
+    if (g->done || g->K.nif < kWideJoins)
+        return;
+    kstate_fix(*g);
+    dk_lower(*g);
 }
 
 __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_FOLD * 128 / OD_BLOCK) k_fold(DecompArgs a) {
