@@ -1152,6 +1152,9 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     a.only_len = s->only_len;
     a.prof = s->prof_on ? P<u64>(s->prof) : nullptr;
     a.retry_cnt = cnt + 12;
+    // long kernels (C5: ~340 KB of listing each) have hundreds of if-joins:
+    // their joins are settled by the whole warp (k_lower_wide)
+    a.wide_joins = s->lanes_lower == 32 && !OD_LOCAL_LOWER && len / nk >= (64u << 10) ? kWideJoins : ~0u;
     CK(cudaMemsetAsync(cnt + 12, 0, 4, st));
     const u32 kb = 256, kg = (nk + kb - 1) / kb;
     u32 *key = P<u32>(s->kmeta);
@@ -1248,7 +1251,7 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
             CK(cudaEventRecord(pe[1], ws));
             a.lanes_per = s->lanes_lower;
             k_lower<<<grid(a.lanes_per), OD_BLOCK, s->smem_lower, ws>>>(a);
-            if (a.lanes_per == 32 && !OD_LOCAL_LOWER) {
+            if (a.wide_joins != ~0u) {
                 k_lower_wide<<<grid(a.lanes_per), OD_BLOCK, s->smem_lower, ws>>>(a);
                 s->stats.total_launches++;
             }

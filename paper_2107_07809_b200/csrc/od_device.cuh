@@ -58,6 +58,7 @@ struct DecompArgs {
     unsigned long long *dtop;
     const KSize *sizes; // per kernel (k_ksize)
     u32 *retry_cnt;     // kernels that ended out of arena or staging room (k_emit counts them)
+    u32 wide_joins;     // if-joins from which k_lower_wide lowers a kernel (~0u: k_lower takes all)
 };
 
 // Three launches per wave, one per pipeline phase (od_lower.cuh dk_front /
@@ -143,7 +144,7 @@ __device__ __forceinline__ void kstate_store(KState *g, const KState &S) {
 __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_FRONT * 128 / OD_BLOCK) k_front(DecompArgs a);
 __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_LOWER * 128 / OD_BLOCK) k_lower(DecompArgs a);
 __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_LOWER * 128 / OD_BLOCK) k_lower_wide(DecompArgs a);
-constexpr u32 kWideJoins = 64; // if-joins from which a kernel is lowered by the whole warp
+constexpr u32 kWideJoins = 64; // if-joins from which a kernel is lowered by the whole warp (long-kernel chunks)
 __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_FOLD * 128 / OD_BLOCK) k_fold(DecompArgs a);
 __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_EMIT * 128 / OD_BLOCK) k_emit(DecompArgs a);
 

@@ -9,14 +9,15 @@ namespace od {
 // warp redundantly (od_base.cuh "warp cooperation"), so their joins
 // (merge_join, collect_delta) split the slot work across the lanes: k_lower_
 // wide, one kernel per warp.  k_lower keeps the lone-lane lowering of every
-// other kernel in its own launch (the warp-wide entry cost the narrow path
-// 3 % on C4 when both lived in one kernel).
+// other kernel.  The host enables the split only for chunks of long kernels
+// (measured on C4, whose kernels are short: the second launch and the
+// warp-wide entry cost 3-8 % of k_lower and gain nothing).
 __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_LOWER * 128 / OD_BLOCK) k_lower(DecompArgs a) {
     Slot0 sl;
     if (!dk_slot(a, &sl))
         return;
     KState *g = reinterpret_cast<KState *>(sl.base);
-    if (g->done || (a.lanes_per == 32 && g->K.nif >= kWideJoins))
+    if (g->done || g->K.nif >= a.wide_joins)
         return;
 #if OD_LOCAL_LOWER
     KState S;
@@ -36,7 +37,7 @@ __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_LOWER * 128 / OD_BLOCK) k_lo
     if (!__shfl_sync(full, mine, 0))
         return;
     KState *g = reinterpret_cast<KState *>(__shfl_sync(full, (unsigned long long)sl.base, 0));
-    if (g->done || g->K.nif < kWideJoins)
+    if (g->done || g->K.nif < a.wide_joins)
         return;
     kstate_fix(*g);
     dk_lower(*g);
