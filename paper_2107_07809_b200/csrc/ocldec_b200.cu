@@ -917,6 +917,7 @@ struct ocldec_b200_session {
     DevBuf sgen;                     // streamed generation: the current group of chunks
     DevBuf rstat;                    // per-chunk result totals (k_res_stats)
     bool keep_records = true;        // per-kernel host records (names, spans, flags, diagnostics)
+    bool wide_lower = false;         // OCLDEC_B200_WIDE_LOWER: k_lower_wide for long-kernel chunks
     u32 novr = 0;
     std::vector<u64> host_kdiag;     // per kernel: first host_diag index (count in host_res[k].ndiag)
     size_t pev_used = 0;
@@ -1152,9 +1153,14 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     a.only_len = s->only_len;
     a.prof = s->prof_on ? P<u64>(s->prof) : nullptr;
     a.retry_cnt = cnt + 12;
-    // long kernels (C5: ~340 KB of listing each) have hundreds of if-joins:
-    // their joins are settled by the whole warp (k_lower_wide)
-    a.wide_joins = s->lanes_lower == 32 && !OD_LOCAL_LOWER && len / nk >= (64u << 10) ? kWideJoins : ~0u;
+    // OCLDEC_B200_WIDE_LOWER=1: in chunks of long kernels (C5: ~340 KB of
+    // listing, hundreds of if-joins each) kernels with >= kWideJoins joins are
+    // lowered by the whole warp (k_lower_wide, lane-parallel merge_join /
+    // collect_delta).  Off by default: measured no gain on C5 (the 32 active
+    // lanes widen the rest of the lowering's local-memory traffic) and a
+    // loss on C4.
+    a.wide_joins = s->wide_lower && s->lanes_lower == 32 && !OD_LOCAL_LOWER && len / nk >= (64u << 10)
+                       ? kWideJoins : ~0u;
     CK(cudaMemsetAsync(cnt + 12, 0, 4, st));
     const u32 kb = 256, kg = (nk + kb - 1) / kb;
     u32 *key = P<u32>(s->kmeta);
@@ -1570,6 +1576,10 @@ int session_init(ocldec_b200_session *s, int device, size_t arena_bytes) {
     CK(cudaMemGetInfo(&free_b, &total_b));
     s->pool_bytes = arena_bytes ? arena_bytes : std::min<size_t>(free_b * 2 / 5, (size_t)64 << 30);
     s->arena_bytes = s->pool_bytes;
+    {
+        const char *wl = getenv("OCLDEC_B200_WIDE_LOWER");
+        s->wide_lower = wl && *wl == '1';
+    }
     const char *pe = getenv("OCLDEC_B200_PROF");
     s->prof_on = pe && *pe && *pe != '0';
     // kernels per warp per phase (1, 2, 4, 8, 16 or 32); OCLDEC_B200_KPW sets all
