@@ -136,3 +136,26 @@ def test_streamed_generation_matches_reference_hashes():
             assert st["out_bytes"] + st["chunks"] - 1 == len(P.decompile_listing(host).combined)
     finally:
         s.close()
+
+
+def test_wide_lowering_option_matches_reference():
+    """OCLDEC_B200_WIDE_LOWER=1 (k_lower_wide: long kernels lowered by the whole
+    warp, lane-parallel merge_join / collect_delta) gives the reference's
+    bytes on a C5 sample."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, '.');"
+        "import paper_2107_07809_b200 as P; from oracle import oracle as O;"
+        "parts = [O.generate_corpus('C5', 1, seed=0x210707809C5, k0=k)[0] for k in range(0, 1000000, 41667)];"
+        "listing = b''.join(parts);"
+        "res = P.decompile_listing(listing);"
+        "offs = np.cumsum([0] + [len(p) for p in parts]).astype(np.uint64);"
+        "ref = O.decompile_par(listing, offs[:-1]);"
+        "assert res.combined == ref.combined;"
+        "print('ok', len(parts))")
+    env = dict(os.environ, OCLDEC_B200_WIDE_LOWER="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert p.returncode == 0 and "ok" in p.stdout, p.stderr[-2000:]
