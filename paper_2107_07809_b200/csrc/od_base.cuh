@@ -498,19 +498,6 @@ struct Writer {
         const u32 c = cap;
         u32 k = n;
         bool ov = false;
-        // word at a time from a 4-aligned source while no byte of the word is
-        // zero (the classic haszero test) and the word fits
-        while (((uintptr_t)s & 3) == 0 && k + 4 <= c) {
-            const u32 w = *reinterpret_cast<const u32 *>(s);
-            if ((w - 0x01010101u) & ~w & 0x80808080u)
-                break;
-            d[k] = (u8)w;
-            d[k + 1] = (u8)(w >> 8);
-            d[k + 2] = (u8)(w >> 16);
-            d[k + 3] = (u8)(w >> 24);
-            k += 4;
-            s += 4;
-        }
         for (u8 ch; (ch = (u8)*s) != 0; ++s, ++k) {
             if (k < c)
                 d[k] = ch;
