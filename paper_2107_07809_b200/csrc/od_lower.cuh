@@ -1970,41 +1970,10 @@ OD_NOINL void dk_lower(KState &S) {
 // trees only ever land in statements (never in register slots, whose
 // identity read_pair_ids/dissolve_pair compare), and fold_expr is a pure
 // function of its subtree, so folding after lowering gives the same text.
-// Marks every expression node with no builtin below it as folded to itself
-// (memo = own id): each fold of builtin_detector.cpp:86-169 matches a
-// builtin inside the folded subtree, so fold_expr would return such a node
-// unchanged; it now never walks it.  Children are created before their
-// parents, so one pass in id order settles every node.
-OD_NOINL void premark_fold(EArena &E) {
-    ENode *__restrict__ n = E.n;
-    const u32 top = E.top;
-    for (u32 i = 1; i < top; ++i) {
-        ENode &x = n[i];
-        bool open = x.kind == E_BUILTIN;
-        if (!open) {
-            u32 ch[3] = {0, 0, 0};
-            if (x.kind == E_UNARY || x.kind == E_DEREF) {
-                ch[0] = x.a;
-            } else if (x.kind == E_BINARY) {
-                ch[0] = x.a;
-                ch[1] = x.b;
-            } else if (x.kind == E_TERNARY) {
-                ch[0] = x.a;
-                ch[1] = x.b;
-                ch[2] = x.c;
-            }
-            for (u32 k = 0; k < 3; ++k)
-                open |= ch[k] && n[ch[k]].memo == 0;
-        }
-        x.memo = open ? 0 : i;
-    }
-}
-
 OD_NOINL void dk_fold(KState &S) {
     const KIn &in = S.in;
     KCtx &K = S.K;
     long long tp = OD_CLK();
-    premark_fold(K.E);
     for (u32 i = 1; i < K.nst && !K.E.oom; ++i) {
         Stmt &st = K.st[i];
         switch (st.kind) {
