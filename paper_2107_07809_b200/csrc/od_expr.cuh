@@ -53,11 +53,6 @@ struct EArena {
         return top++;
     }
     OD_INL const ENode &operator[](u32 i) const { return n[i]; }
-    // fold_expr's memo at creation: a node with no builtin below it folds to
-    // itself (every fold of builtin_detector.cpp:86-169 matches a builtin in
-    // the folded subtree), so it is born memoized as itself and fold_expr
-    // never walks it; a node over a builtin starts open (memo 0).
-    OD_INL bool open(u32 c) const { return c && n[c].memo == 0; }
     OD_INL u64 cval(u32 i) const { return (u64)n[i].a | ((u64)n[i].b << 32); }
     OD_INL bool is_const(u32 i) const { return i && n[i].kind == E_CONST; }
     OD_INL bool is_const_v(u32 i, u64 v) const { return is_const(i) && cval(i) == v; }
@@ -78,7 +73,7 @@ struct EArena {
         e.a = (u32)v;
         e.b = (u32)(v >> 32);
         e.c = 0;
-        e.memo = i; // no builtin below: fold_expr leaves it as is
+        e.memo = 0;
         return i;
     }
     OD_HOT u32 leaf(u8 kind, u8 op, u16 x, DT t, u32 a) {
@@ -93,7 +88,7 @@ struct EArena {
         e.a = a;
         e.b = 0;
         e.c = 0;
-        e.memo = kind == E_BUILTIN ? 0 : i;
+        e.memo = 0;
         return i;
     }
     OD_INL u32 builtin(u32 fn, u32 dim, DT t) { return leaf(E_BUILTIN, (u8)fn, (u16)dim, t, 0); }
@@ -131,7 +126,7 @@ struct EArena {
         e.a = a;
         e.b = 0;
         e.c = 0;
-        e.memo = open(a) ? 0 : i;
+        e.memo = 0;
         return i;
     }
 
@@ -178,7 +173,7 @@ struct EArena {
         e.a = a;
         e.b = b;
         e.c = 0;
-        e.memo = open(a) || open(b) ? 0 : i;
+        e.memo = 0;
         return i;
     }
 
@@ -197,7 +192,7 @@ struct EArena {
         e.a = cond;
         e.b = a;
         e.c = b;
-        e.memo = open(cond) || open(a) || open(b) ? 0 : i;
+        e.memo = 0;
         return i;
     }
 
@@ -214,7 +209,7 @@ struct EArena {
         e.a = addr;
         e.b = 0;
         e.c = 0;
-        e.memo = open(addr) ? 0 : i;
+        e.memo = 0;
         return i;
     }
 };
