@@ -107,6 +107,18 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def dataflow_profile():
+    """the dataflow pass is judged on occupancy and branch
+    efficiency.  ncu numbers of the phase kernels (tools/dataflow_json.py,
+    from the final build's --set full captures), never measured in this run."""
+    p = os.path.join(ROOT, "profiles", "dataflow_ncu.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    d["source"] = "profiles/dataflow_ncu.json (ncu --set full of the phase kernels, C4 / C5 samples)"
+    return d
+
+
 def pass_roof(nbytes, ms, peak):
     """Achieved GB/s of a byte-stream pass (algorithmic bytes / device time)."""
     gbs = nbytes / (ms / 1000.0) / 1e9 if ms else None
@@ -495,7 +507,10 @@ def main():
         # (P1: listing text read once) and the combined_source gather (P4b:
         # staged text read + written once)
         "passes_roofline": {"parse": pass_roof(in_b, ms_parse / args.steps, peak),
+                            # the emitter itself: k_emit renders out_bytes of OpenCL text
+                            "emit": pass_roof(out_b, ms_ph["k_emit"] / args.steps, peak),
                             "gather": pass_roof(2 * out_b, ms_emit / args.steps, peak)},
+        "dataflow": dataflow_profile(),
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "e2e": e2e,

@@ -1,0 +1,57 @@
+"""Writes profiles/dataflow_ncu.json: per decompile-phase kernel, from ncu
+--set full captures (tools/final_profiles_r2.sh) of a C4 and a C5 sample, the
+numbers SURVEY §8(d) judges the dataflow pass on -- achieved occupancy,
+average active threads per warp, branch efficiency -- plus issue activity.
+bench.py copies the file into its line (`dataflow`).  Developer aid:
+    python tools/dataflow_json.py gpurun_out/final_r2/phases.ncu-rep gpurun_out/final_r2/c5.ncu-rep"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+METRICS = {
+    "achieved_occupancy_pct": "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "active_threads_per_warp": "smsp__thread_inst_executed_per_inst_executed.ratio",
+    "branch_efficiency_pct": "smsp__sass_average_branch_targets_threads_uniform.pct",
+    "issue_slots_busy_pct": "sm__inst_issued.avg.pct_of_peak_sustained_active",
+    "duration_ms": "gpu__time_duration.sum",
+}
+
+
+def read(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS.values())],
+                         capture_output=True, text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    ki = hdr.index("Kernel Name")
+    res = {}
+    for r in rows[2:]:
+        name = r[ki].split("(")[0].split("::")[-1].strip()
+        d = {}
+        for key, m in METRICS.items():
+            j = hdr.index(m)
+            try:
+                v = float(r[j].replace(",", ""))
+            except ValueError:
+                v = None
+            if key == "duration_ms" and v is not None:
+                v *= {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1, "msecond": 1,
+                      "s": 1e3, "second": 1e3}[units[j]]
+            d[key] = v
+        res[name] = d
+    return res
+
+
+out = {"note": "ncu --set full, one launch per kernel; k_front runs each kernel on all 32 lanes of its warp "
+               "(redundant where the work is sequential), so its active-threads figure counts the redundant "
+               "lanes too; the lane-split loops are liveness, build_cfg, retarget_preds, annotate, canonicalize "
+               "(DESIGN.md section 4)",
+       "C4_30k": read(sys.argv[1])}
+if len(sys.argv) > 2:
+    out["C5_1500"] = read(sys.argv[2])
+dst = os.path.join(ROOT, "profiles", "dataflow_ncu.json")
+json.dump(out, open(dst, "w"), indent=1)
+print(json.dumps(out, indent=1))

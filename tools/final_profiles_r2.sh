@@ -1,0 +1,27 @@
+#!/bin/bash
+# Round-end evidence of the final build (round 2):
+#   phases.ncu-rep   ncu --set full of k_front/k_lower/k_fold/k_emit, C4 30k-kernel sample
+#   c5.ncu-rep       the same kernels on a C5 sample (1,500 long kernels, streamed)
+#   parse.ncu-rep    ncu --set full of the parse kernels + k_ksize + k_gather, C4 200k sample
+#   launches.csv     ncu launch list (gpu__time_duration) of a bench-shaped C4 run
+#   gputest.log      the GPU test suite
+O=gpurun_out/${1:-final_r2}
+mkdir -p $O
+NCU=/usr/local/cuda/bin/ncu
+timeout 1200 python -m pytest tests -m gpu -q > $O/gputest.log 2>&1; echo rc=$? >> $O/gputest.log
+timeout 1500 $NCU --set full --clock-control none --import-source on -k regex:'k_front|k_lower|k_fold|k_emit' -c 4 \
+  -o $O/phases python bench.py --kernels 30000 --steps 1 --warmup 3 --no-e2e --no-cpu > $O/ncu_phases.log 2>&1
+timeout 1500 $NCU --set full --clock-control none --import-source on -k regex:'k_front|k_lower|k_fold|k_emit' -c 4 \
+  -o $O/c5 python -c "
+import paper_2107_07809_b200 as P, json
+s = P.Session(0)
+st, _, _ = s.run_generated('C5', 1500, seed=0x210707809C5)
+print(json.dumps(st))
+" > $O/ncu_c5.log 2>&1
+timeout 1200 $NCU --set full --clock-control none --import-source on \
+  -k regex:'k_nl_count|k_nl_write|k_classify|k_decode|k_gather|k_ksize' -c 6 \
+  -o $O/parse python bench.py --kernels 200000 --steps 1 --warmup 0 --no-e2e --no-cpu > $O/ncu_parse.log 2>&1
+timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file $O/launches.csv python bench.py --kernels 50000 --steps 1 --warmup 3 --no-e2e --no-cpu \
+  > $O/ncu_launch.log 2>&1
+ls -la $O

@@ -28,16 +28,22 @@ hdr = rows[0]
 units = rows[1]
 res = {}
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-         "msecond": 1e-3, "second": 1}
+         "msecond": 1e-3, "second": 1, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1}
 ki = hdr.index("Kernel Name")
 for r in rows[2:]:
     name = r[ki].split("(")[0].split("::")[-1].strip()
     vals = {}
     for m in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"):
         j = hdr.index(m)
-        vals[m] = float(r[j].replace(",", "")) * scale.get(units[j], 1)
-    b = vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]
-    res[name] = {"dram_bytes": b, "dram_bytes_per_instr": b / ninstr,
+        if units[j] not in scale:
+            raise SystemExit(f"unknown ncu unit {units[j]!r} for {m}")
+        try:
+            vals[m] = float(r[j].replace(",", "")) * scale[units[j]]
+        except ValueError:  # ncu reports n/a when a counter could not be collected
+            vals[m] = None
+    rd, wr = vals["dram__bytes_read.sum"], vals["dram__bytes_write.sum"]
+    b = rd + wr if rd is not None and wr is not None else None
+    res[name] = {"dram_bytes": b, "dram_bytes_per_instr": b / ninstr if b is not None else None,
                  "algorithmic_bytes": in_b + out_b, "sample_instructions": ninstr,
                  "ncu_duration_s": vals["gpu__time_duration.sum"],
                  "source": os.path.basename(rep) + " (ncu --set full, C4 sample, one launch)"}
