@@ -37,6 +37,7 @@
 struct uint4 {
     uint32_t x, y, z, w;
 };
+inline uint4 make_uint4(uint32_t x, uint32_t y, uint32_t z, uint32_t w) { return uint4{x, y, z, w}; }
 #endif
 
 namespace od {

@@ -28,7 +28,7 @@ enum BOp : u8 { O_ADD = 0, O_SUB, O_MUL, O_MULHI, O_MULHIS, O_DIV, O_AND, O_OR, 
 enum BFn : u8 { F_GLOBAL_ID = 0, F_LOCAL_ID, F_GROUP_ID, F_GLOBAL_SIZE, F_LOCAL_SIZE,
                 F_NUM_GROUPS, F_GLOBAL_OFFSET, F_WORK_DIM };
 
-struct ENode {
+struct alignas(8) ENode {
     u8 kind;
     u8 op;   // UOp/BOp; BFn for builtins
     u16 x;   // builtin dim; var name class (physical register slot)
@@ -36,6 +36,8 @@ struct ENode {
     u32 a, b, c; // children; const value = a | b<<32; var number = a; arg name id = a
     u32 memo;    // fold_expr cache (0 = not folded yet)
 };
+
+static_assert(sizeof(ENode) == 24, "EArena::put writes a node as three 8-byte words");
 
 struct KConfig; // od_kernel.cuh
 
@@ -53,6 +55,13 @@ struct EArena {
         return top++;
     }
     OD_INL const ENode &operator[](u32 i) const { return n[i]; }
+    // A node in three 8-byte stores (ENode is 24 bytes, the pool 16-byte aligned).
+    OD_INL void put(u32 i, u8 kind, u8 op, u16 x, DT t, u32 a, u32 b, u32 c) {
+        u64 *q = reinterpret_cast<u64 *>(&n[i]);
+        q[0] = (u64)kind | ((u64)op << 8) | ((u64)x << 16) | ((u64)t << 32);
+        q[1] = (u64)a | ((u64)b << 32);
+        q[2] = (u64)c; // memo = 0
+    }
     OD_INL u64 cval(u32 i) const { return (u64)n[i].a | ((u64)n[i].b << 32); }
     OD_INL bool is_const(u32 i) const { return i && n[i].kind == E_CONST; }
     OD_INL bool is_const_v(u32 i, u64 v) const { return is_const(i) && cval(i) == v; }
@@ -65,30 +74,14 @@ struct EArena {
         u32 i = alloc();
         if (!i)
             return 0;
-        ENode &e = n[i];
-        e.kind = E_CONST;
-        e.op = 0;
-        e.x = 0;
-        e.type = t;
-        e.a = (u32)v;
-        e.b = (u32)(v >> 32);
-        e.c = 0;
-        e.memo = 0;
+        put(i, E_CONST, 0, 0, t, (u32)v, (u32)(v >> 32), 0);
         return i;
     }
     OD_HOT u32 leaf(u8 kind, u8 op, u16 x, DT t, u32 a) {
         u32 i = alloc();
         if (!i)
             return 0;
-        ENode &e = n[i];
-        e.kind = kind;
-        e.op = op;
-        e.x = x;
-        e.type = t;
-        e.a = a;
-        e.b = 0;
-        e.c = 0;
-        e.memo = 0;
+        put(i, kind, op, x, t, a, 0, 0);
         return i;
     }
     OD_INL u32 builtin(u32 fn, u32 dim, DT t) { return leaf(E_BUILTIN, (u8)fn, (u16)dim, t, 0); }
@@ -118,15 +111,7 @@ struct EArena {
         u32 i = alloc();
         if (!i)
             return 0;
-        ENode &e = n[i];
-        e.kind = E_UNARY;
-        e.op = (u8)op;
-        e.x = 0;
-        e.type = t;
-        e.a = a;
-        e.b = 0;
-        e.c = 0;
-        e.memo = 0;
+        put(i, E_UNARY, (u8)op, 0, t, a, 0, 0);
         return i;
     }
 
@@ -165,15 +150,7 @@ struct EArena {
         u32 i = alloc();
         if (!i)
             return 0;
-        ENode &e = n[i];
-        e.kind = E_BINARY;
-        e.op = (u8)op;
-        e.x = 0;
-        e.type = t;
-        e.a = a;
-        e.b = b;
-        e.c = 0;
-        e.memo = 0;
+        put(i, E_BINARY, (u8)op, 0, t, a, b, 0);
         return i;
     }
 
@@ -184,15 +161,7 @@ struct EArena {
         u32 i = alloc();
         if (!i)
             return 0;
-        ENode &e = n[i];
-        e.kind = E_TERNARY;
-        e.op = 0;
-        e.x = 0;
-        e.type = t;
-        e.a = cond;
-        e.b = a;
-        e.c = b;
-        e.memo = 0;
+        put(i, E_TERNARY, 0, 0, t, cond, a, b);
         return i;
     }
 
@@ -201,15 +170,7 @@ struct EArena {
         u32 i = alloc();
         if (!i)
             return 0;
-        ENode &e = n[i];
-        e.kind = E_DEREF;
-        e.op = 0;
-        e.x = 0;
-        e.type = dt_with_space(pointee, space);
-        e.a = addr;
-        e.b = 0;
-        e.c = 0;
-        e.memo = 0;
+        put(i, E_DEREF, 0, 0, dt_with_space(pointee, space), addr, 0, 0);
         return i;
     }
 };

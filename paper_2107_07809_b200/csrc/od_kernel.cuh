@@ -194,13 +194,16 @@ struct Slot {
     u8 pad[3];
 };
 
+// An undo record is the slot's old value with its slot id in the pad bytes:
+// one 16-byte load and one 16-byte store per record.
 struct UndoRec {
-    u32 phys;
     u32 version;
     u32 expr;
     DT type;
-    u32 integ;
+    u32 integ_phys; // integ | phys << 8
+    OD_INL u32 phys() const { return integ_phys >> 8; }
 };
+static_assert(sizeof(UndoRec) == 16 && sizeof(Slot) == 16, "undo records are Slot-shaped");
 
 struct Pending {
     u32 valid;

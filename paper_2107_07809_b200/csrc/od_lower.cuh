@@ -30,25 +30,16 @@ OD_INL void log_slot(KCtx &K, u32 p) {
         K.oom = true;
         return;
     }
-    UndoRec &u = K.log[K.nlog++];
+    const uint4 v = *reinterpret_cast<const uint4 *>(&K.regs[p]);
+    *reinterpret_cast<uint4 *>(&K.log[K.nlog++]) = make_uint4(v.x, v.y, v.z, (v.w & 0xffu) | (p << 8));
     if (K.nlog > K.log_hw)
         K.log_hw = K.nlog;
-    const Slot &s = K.regs[p];
-    u.phys = p;
-    u.version = s.version;
-    u.expr = s.expr;
-    u.type = s.type;
-    u.integ = s.integ;
 }
 
 OD_INL void undo_to(KCtx &K, u32 pos) {
     while (K.nlog > pos) {
-        const UndoRec &u = K.log[--K.nlog];
-        Slot &s = K.regs[u.phys];
-        s.version = u.version;
-        s.expr = u.expr;
-        s.type = u.type;
-        s.integ = (u8)u.integ;
+        const uint4 v = *reinterpret_cast<const uint4 *>(&K.log[--K.nlog]);
+        *reinterpret_cast<uint4 *>(&K.regs[v.w >> 8]) = make_uint4(v.x, v.y, v.z, v.w & 0xffu);
     }
 }
 
@@ -1034,7 +1025,7 @@ OD_NOINL void collect_delta_seq(KCtx &K, u32 p0, u32 *start, u32 *count) {
     for (u32 w = 0; w < kLiveWords; ++w)
         bm[w] = 0;
     for (u32 i = p0; i < K.nlog; ++i) {
-        u32 p = K.log[i].phys;
+        u32 p = K.log[i].phys();
         bm[p >> 5] |= 1u << (p & 31);
     }
     *start = K.ndstk;
@@ -1074,7 +1065,7 @@ OD_NOINL void collect_delta(KCtx &K, u32 p0, u32 *start, u32 *count) {
     for (u32 w = 0; w < kLiveWords; ++w)
         bm[w] = 0;
     for (u32 i = p0 + r; i < K.nlog; i += nl) {
-        const u32 p = K.log[i].phys;
+        const u32 p = K.log[i].phys();
         bm[p >> 5] |= 1u << (p & 31);
     }
     u32 total = 0;
@@ -1201,13 +1192,8 @@ OD_NOINL void merge_join_seq(KCtx &K, const Frame &F, u32 td, u32 tn, u32 ed, u3
 
 // The undo record of slot p at log position at (log_slot's record).
 OD_INL void log_at(KCtx &K, u32 at, u32 p) {
-    UndoRec &u = K.log[at];
-    const Slot &s = K.regs[p];
-    u.phys = p;
-    u.version = s.version;
-    u.expr = s.expr;
-    u.type = s.type;
-    u.integ = s.integ;
+    const uint4 v = *reinterpret_cast<const uint4 *>(&K.regs[p]);
+    *reinterpret_cast<uint4 *>(&K.log[at]) = make_uint4(v.x, v.y, v.z, (v.w & 0xffu) | (p << 8));
 }
 
 // merge_at_join (sym_state.cpp:866-957) + emit_join (lower.cpp:89-121) for
