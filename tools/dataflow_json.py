@@ -52,6 +52,6 @@ out = {"note": "ncu --set full, one launch per kernel; k_front runs each kernel 
        "C4_30k": read(sys.argv[1])}
 if len(sys.argv) > 2:
     out["C5_1500"] = read(sys.argv[2])
-dst = os.path.join(ROOT, "profiles", "dataflow_ncu.json")
+dst = os.environ.get("OUT") or os.path.join(ROOT, "profiles", "dataflow_ncu.json")
 json.dump(out, open(dst, "w"), indent=1)
 print(json.dumps(out, indent=1))

@@ -25,3 +25,14 @@ timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $O/launches.csv python bench.py --kernels 50000 --steps 1 --warmup 3 --no-e2e --no-cpu \
   > $O/ncu_launch.log 2>&1
 ls -la $O
+# summaries small enough to travel back (gpurun copies <= 64 MiB of gpurun_out/)
+for r in phases c5 parse; do
+  [ -f $O/$r.ncu-rep ] && $NCU -i $O/$r.ncu-rep --page details --csv > $O/${r}_details.csv 2>/dev/null
+done
+OUT=$O/dram_traffic.json python tools/traffic_json.py $O/phases.ncu-rep $O/ncu_phases.log > /dev/null 2>&1
+OUT=$O/dataflow_ncu.json python tools/dataflow_json.py $O/phases.ncu-rep $O/c5.ncu-rep > /dev/null 2>&1
+for k in k_front k_lower k_emit; do
+  $NCU -i $O/phases.ncu-rep -k $k --page source --csv --print-source cuda,sass 2>/dev/null | python tools/ncu_funcs.py /dev/stdin 25 > $O/funcs_$k.txt 2>&1
+done
+rm -f $O/*.ncu-rep
+du -sh $O

@@ -47,6 +47,6 @@ for r in rows[2:]:
                  "algorithmic_bytes": in_b + out_b, "sample_instructions": ninstr,
                  "ncu_duration_s": vals["gpu__time_duration.sum"],
                  "source": os.path.basename(rep) + " (ncu --set full, C4 sample, one launch)"}
-dst = os.path.join(ROOT, "profiles", "dram_traffic.json")
+dst = os.environ.get("OUT") or os.path.join(ROOT, "profiles", "dram_traffic.json")
 json.dump(res, open(dst, "w"), indent=1)
 print(json.dumps(res, indent=1))
