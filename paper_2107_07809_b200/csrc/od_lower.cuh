@@ -36,25 +36,6 @@ OD_INL void log_slot(KCtx &K, u32 p) {
         K.log_hw = K.nlog;
 }
 
-// A slot as one 16-byte word: version, expr, type, integ | pad << 8.
-OD_INL uint4 slot_load(const KCtx &K, u32 p) { return *reinterpret_cast<const uint4 *>(&K.regs[p]); }
-OD_INL void slot_store(KCtx &K, u32 p, u32 version, u32 expr, DT type, u32 integ, u32 w_old) {
-    *reinterpret_cast<uint4 *>(&K.regs[p]) = make_uint4(version, expr, type, (w_old & ~0xffu) | integ);
-}
-// log_slot with the slot's current value already loaded.
-OD_INL void log_slot_v(KCtx &K, u32 p, const uint4 &v) {
-    K.dirty[p >> 5] |= 1u << (p & 31);
-    if (!K.log_depth)
-        return;
-    if (K.nlog >= K.log_cap) {
-        K.oom = true;
-        return;
-    }
-    *reinterpret_cast<uint4 *>(&K.log[K.nlog++]) = make_uint4(v.x, v.y, v.z, (v.w & 0xffu) | (p << 8));
-    if (K.nlog > K.log_hw)
-        K.log_hw = K.nlog;
-}
-
 OD_INL void undo_to(KCtx &K, u32 pos) {
     while (K.nlog > pos) {
         const uint4 v = *reinterpret_cast<const uint4 *>(&K.log[--K.nlog]);
@@ -75,16 +56,17 @@ OD_INL void record_fresh(KCtx &K, u32 cls, u32 num, DT t) {
 
 // bind_fresh  sym_state.cpp:63-78
 OD_HOT u32 bind_fresh(KCtx &K, u32 p, DT t = DT_B32) {
-    const uint4 v = slot_load(K, p);
-    if (v.y)
-        return v.y;
-    log_slot_v(K, p, v);
-    const DT ty = dt_is_unknown(v.z) ? t : v.z;
-    const u32 e = K.E.var(p, v.x, ty);
-    slot_store(K, p, v.x, e, ty, IN_ENTIRE, v.w);
-    record_fresh(K, p, v.x, ty);
-    K.pool.insert(p, v.x);
-    return e;
+    Slot &s = K.regs[p];
+    if (!s.expr) {
+        log_slot(K, p);
+        if (dt_is_unknown(s.type))
+            s.type = t;
+        s.expr = K.E.var(p, s.version, s.type);
+        s.integ = IN_ENTIRE;
+        record_fresh(K, p, s.version, s.type);
+        K.pool.insert(p, s.version);
+    }
+    return s.expr;
 }
 
 // read_slot32  sym_state.cpp:82-94
@@ -157,10 +139,13 @@ OD_HOT void write_slot32(KCtx &K, u32 id, u32 value, DT t) {
         return;
     }
     dissolve_pair(K, id);
-    const u32 p = phys_of(id);
-    const uint4 v = slot_load(K, p);
-    log_slot_v(K, p, v);
-    slot_store(K, p, v.x + 1, value, t, IN_ENTIRE, v.w);
+    u32 p = phys_of(id);
+    log_slot(K, p);
+    Slot &s = K.regs[p];
+    s.version += 1;
+    s.expr = value;
+    s.type = t;
+    s.integ = IN_ENTIRE;
 }
 
 OD_NOINL void write_pair_ids(KCtx &K, u32 lo_id, u32 value, DT t) {
@@ -169,10 +154,13 @@ OD_NOINL void write_pair_ids(KCtx &K, u32 lo_id, u32 value, DT t) {
             K.oom = true;
             return;
         }
-        const u32 p = phys_of(lo_id);
-        const uint4 v = slot_load(K, p);
-        log_slot_v(K, p, v);
-        slot_store(K, p, v.x + 1, value, t, IN_ENTIRE, v.w);
+        u32 p = phys_of(lo_id);
+        log_slot(K, p);
+        Slot &s = K.regs[p];
+        s.version += 1;
+        s.expr = value;
+        s.type = t;
+        s.integ = IN_ENTIRE;
         return;
     }
     if (lo_id + 1 >= kRegIdExecLo) {
@@ -181,11 +169,18 @@ OD_NOINL void write_pair_ids(KCtx &K, u32 lo_id, u32 value, DT t) {
     }
     dissolve_pair(K, lo_id);
     dissolve_pair(K, lo_id + 1);
-    const uint4 lv = slot_load(K, lo_id), hv = slot_load(K, lo_id + 1);
-    log_slot_v(K, lo_id, lv);
-    log_slot_v(K, lo_id + 1, hv);
-    slot_store(K, lo_id, lv.x + 1, value, t, IN_LOW, lv.w);
-    slot_store(K, lo_id + 1, hv.x + 1, value, t, IN_HIGH, hv.w);
+    log_slot(K, lo_id);
+    log_slot(K, lo_id + 1);
+    Slot &lo = K.regs[lo_id];
+    Slot &hi = K.regs[lo_id + 1];
+    lo.version += 1;
+    hi.version += 1;
+    lo.expr = value;
+    hi.expr = value;
+    lo.type = t;
+    hi.type = t;
+    lo.integ = IN_LOW;
+    hi.integ = IN_HIGH;
 }
 
 // invalidate_slot  sym_state.cpp:169-180
@@ -196,10 +191,13 @@ OD_NOINL void invalidate_slot(KCtx &K, u32 id, u32 count) {
             return;
         }
         dissolve_pair(K, id + i);
-        const u32 p = phys_of(id + i);
-        const uint4 v = slot_load(K, p);
-        log_slot_v(K, p, v);
-        slot_store(K, p, v.x + 1, 0, DT_UNKNOWN, IN_ENTIRE, v.w);
+        u32 p = phys_of(id + i);
+        log_slot(K, p);
+        Slot &s = K.regs[p];
+        s.version += 1;
+        s.expr = 0;
+        s.type = DT_UNKNOWN;
+        s.integ = IN_ENTIRE;
         if (id + i >= kRegIdExecLo)
             break;
     }
