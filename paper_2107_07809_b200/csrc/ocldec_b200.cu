@@ -256,6 +256,13 @@ __global__ void k_init_roots() {
 // thread decodes its line from there.  Lines whose content lives in the aux
 // area (comment-stripped copies) and oversized spans read the listing in HBM.
 constexpr u32 kDecodeStage = 16384;
+// Shape key of the decode order: operand bound (0..7) x length class.
+#ifndef OD_DECODE_LEN_CLASSES
+#define OD_DECODE_LEN_CLASSES 2
+#endif
+#ifndef OD_DECODE_LEN_STEP
+#define OD_DECODE_LEN_STEP 6
+#endif
 
 __global__ void __launch_bounds__(256) k_decode(const u8 *__restrict__ t, u64 len, const u32 *__restrict__ nlpos,
                                                 u32 nlf, u32 nlines, const LineRec *__restrict__ lines,
@@ -294,25 +301,32 @@ __global__ void __launch_bounds__(256) k_decode(const u8 *__restrict__ t, u64 le
     // reordered by a shape key (operand bound from k_classify, long or
     // short) with a counting sort in shared memory, so each warp decodes
     // lines of similar shape (each line's decode is independent).
-    __shared__ u32 bucket[16];
+    constexpr u32 kNB = 8 * OD_DECODE_LEN_CLASSES + 1; // last bucket: not a text line
+    __shared__ u32 bucket[kNB];
     __shared__ u16 order[256];
-    if (threadIdx.x < 16)
+    if (threadIdx.x < kNB)
         bucket[threadIdx.x] = 0;
     __syncthreads();
-    u32 key = 15; // past the end, or not a text line
+    u32 key = kNB - 1; // past the end, or not a text line
     {
         const u32 lk = l0 + threadIdx.x;
         if (lk < nlines) {
             const LineRec Lk = lines[lk];
-            if (Lk.role == LR_TEXT)
-                key = min(min(ops_ub[lk], 7u) * 2 + (Lk.len >= 36 ? 1u : 0u), 14u);
+            if (Lk.role == LR_TEXT) {
+#if OD_DECODE_LEN_CLASSES == 2
+                const u32 lc = Lk.len >= 36 ? 1u : 0u;
+#else
+                const u32 lc = min(Lk.len / OD_DECODE_LEN_STEP, (u32)OD_DECODE_LEN_CLASSES - 1);
+#endif
+                key = min(ops_ub[lk], 7u) * OD_DECODE_LEN_CLASSES + lc;
+            }
         }
     }
     const u32 rank = atomicAdd(&bucket[key], 1u);
     __syncthreads();
     if (threadIdx.x == 0) {
         u32 acc = 0;
-        for (u32 b = 0; b < 16; ++b) {
+        for (u32 b = 0; b < kNB; ++b) {
             const u32 c = bucket[b];
             bucket[b] = acc;
             acc += c;
