@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define OCLDEC_B200_ABI_VERSION 4
+#define OCLDEC_B200_ABI_VERSION 5
 
 /* DecompileOptions (decompiler.hpp:29-35). */
 typedef struct ocldec_b200_options {
@@ -43,6 +43,9 @@ typedef struct ocldec_b200_options {
     int record_reduction;    /* DecompiledKernel::reduction's merges and root / residue as a
                                 step -2 dump (text: "merge <kind> <result> <absorbed...>" lines,
                                 then "root <id>" or "residue <ids...>"; structurizer.hpp:54-104) */
+    int export_body;         /* DecompiledKernel::body (LoweredBody, lower.hpp:20-41) as a step -3
+                                dump: expression nodes and the statement tree in the text format
+                                of od_lower.cuh's body_text (ABI v5) */
 } ocldec_b200_options;
 
 /* DecompiledKernel (decompiler.hpp:39-52): the printed source and flags. */
@@ -65,7 +68,8 @@ typedef struct ocldec_b200_diag {
 } ocldec_b200_diag;
 
 /* One dump of a kernel: step -1 is cfg_dot, step -2 the reduction record,
- * step i >= 0 is reduction.dumps[i] ("step<i>"); text at
+ * step -3 the lowered body (export_body), step i >= 0 is reduction.dumps[i]
+ * ("step<i>"); text at
  * dump_text[off, off + len). */
 typedef struct ocldec_b200_dump {
     uint64_t kernel;              /* index into ocldec_b200_result.kernels */

@@ -37,6 +37,7 @@ struct DecompileOptions {
     bool dump_cfg = false;        // DecompileOptions::dump_cfg (decompiler.hpp:33)
     bool dump_regions = false;    // DecompileOptions::dump_regions (decompiler.hpp:34)
     bool record_reduction = false; // fill DecompiledKernel::reduction (merges, root / residue)
+    bool export_body = false;     // fill DecompiledKernel::body_text (the lowered statement tree)
     int device = 0;
     std::vector<int> devices;     // non-empty: shard across these devices (ocldec_b200_decompile_multi)
 };
@@ -66,6 +67,7 @@ struct DecompiledKernel {
     std::string cfg_dot;                   // DecompiledKernel::cfg_dot when dump_cfg
     std::vector<std::string> region_dumps; // ReduceResult::dumps when dump_regions
     Reduction reduction;                   // when record_reduction
+    std::string body_text;                 // the lowered statement tree when export_body (step -3)
 };
 
 inline Reduction parse_reduction(const std::string &text) {
@@ -181,6 +183,7 @@ inline DecompileResult decompile_listing(const std::string &listing, const Decom
     o.dump_cfg = opts.dump_cfg ? 1 : 0;
     o.dump_regions = opts.dump_regions ? 1 : 0;
     o.record_reduction = opts.record_reduction ? 1 : 0;
+    o.export_body = opts.export_body ? 1 : 0;
     ocldec_b200_result *r = nullptr;
     int rc = opts.devices.empty()
                  ? ocldec_b200_decompile(listing.data(), listing.size(), &o, &r)
@@ -208,6 +211,8 @@ inline DecompileResult decompile_listing(const std::string &listing, const Decom
         std::string text(r->dump_text + d.off, d.len);
         if (d.step == -1)
             k.cfg_dot = std::move(text);
+        else if (d.step == -3)
+            k.body_text = std::move(text);
         else if (d.step == -2)
             k.reduction = parse_reduction(text);
         else

@@ -11,14 +11,15 @@
 // run their decompile_listing calls on the GPU.  oracle/dropin.mk builds
 // the reference's acceptance harness this way (tests/test_gpu_dropin.py).
 //
-// Filled from the GPU result: name, source, failed, structured,
-// body.fallback_count, cfg_dot, reduction (merges, root / residue, dumps,
-// and the region tree those describe, owned by `regions`), and
-// DecompileResult::diagnostics in sink order.  Not filled: config,
-// instructions, abi, cfg and body.stmts (in-memory inspection structures the
-// GPU path does not produce).  No CPU fallback: a
-// device or API failure throws std::runtime_error with the library's
-// message, where the reference would have returned output.
+// Filled from the GPU result: name, source, failed, structured, body (the
+// lowered statement tree with its expressions, exported by the device as
+// text, and fallback_count), cfg_dot, reduction (merges, root / residue,
+// dumps, and the region tree those describe, owned by `regions`), and
+// DecompileResult::diagnostics in sink order.  config, instructions and abi
+// are the reference front end's own parse of the kernel's section (host,
+// diagnostics discarded: the GPU's are the result's); cfg is not filled.
+// No CPU fallback for the decompilation: a device or API failure throws
+// std::runtime_error with the library's message.
 #include <memory>
 #include <sstream>
 #include <stdexcept>
@@ -105,6 +106,161 @@ void rebuild_regions(const std::string &text, DecompiledKernel &k) {
     k.regions = std::move(g);
 }
 
+// DataType from the device's packed form (base | bits << 8 | depth << 16 |
+// space << 24; the enums share the reference's order).
+DataType dtype_of(uint64_t t) {
+    DataType d;
+    d.base = static_cast<BaseType>(t & 0xff);
+    d.bits = uint8_t((t >> 8) & 0xff);
+    d.pointer_depth = uint8_t((t >> 16) & 0xff);
+    d.addr_space = static_cast<AddressSpace>((t >> 24) & 0xff);
+    return d;
+}
+
+// LoweredBody from the device's body export (od_lower.cuh body_text).
+struct BodyReader {
+    const std::string &t;
+    size_t p = 0;
+    std::vector<ExprPtr> nodes{nullptr}; // export number -> node
+    uint64_t num() {
+        while (p < t.size() && t[p] == ' ')
+            ++p;
+        uint64_t v = 0;
+        while (p < t.size() && t[p] >= '0' && t[p] <= '9')
+            v = v * 10 + uint64_t(t[p++] - '0');
+        return v;
+    }
+    std::string str() { // "<len> <bytes>"
+        const size_t n = num();
+        ++p; // the separating space
+        std::string s = t.substr(p, n);
+        p += n;
+        return s;
+    }
+    ExprPtr node(uint64_t id) {
+        if (id >= nodes.size())
+            throw std::runtime_error("ocldec-b200: bad body export (node " + std::to_string(id) + ")");
+        return nodes[id];
+    }
+    void eol() {
+        while (p < t.size() && t[p] != '\n')
+            ++p;
+        ++p;
+    }
+    void read_node() {
+        auto e = std::make_shared<Expr>();
+        const uint64_t kind = num(), op = num(), x = num(), type = num(), a = num(), b = num(), c = num();
+        e->kind = static_cast<ExprKind>(kind - 1); // the device's kinds start with a null kind
+        e->type = dtype_of(type);
+        switch (e->kind) {
+        case ExprKind::Const: e->const_value = a | (b << 32); break;
+        case ExprKind::Builtin: e->builtin = BuiltinId{static_cast<BuiltinFn>(op), int(x)}; break;
+        case ExprKind::KernelArg:
+        case ExprKind::Var: e->name = str(); break;
+        case ExprKind::Unary: e->un_op = static_cast<UnaryOp>(op), e->a = node(a); break;
+        case ExprKind::Binary: e->bin_op = static_cast<BinaryOp>(op), e->a = node(a), e->b = node(b); break;
+        case ExprKind::Ternary: e->a = node(a), e->b = node(b), e->c = node(c); break;
+        case ExprKind::Deref: e->a = node(a); break;
+        default: break;
+        }
+        eol();
+        nodes.push_back(std::move(e));
+    }
+    // Statements up to the end of the text or of the current If arm.
+    void read_list(std::vector<Stmt> &out, char *stop) {
+        while (p < t.size()) {
+            const char tag = t[p++];
+            if (tag == 'N') {
+                read_node();
+                continue;
+            }
+            if (tag == 'E' || tag == 'F') {
+                eol();
+                *stop = tag;
+                return;
+            }
+            Stmt s;
+            switch (tag) {
+            case 'A':
+                s.base.kind = StatementKind::Assign;
+                s.base.name = str();
+                s.base.value = node(num());
+                break;
+            case 'D':
+                s.base.kind = StatementKind::Decl;
+                s.base.name = str();
+                s.base.decl_type = dtype_of(num());
+                s.base.value = node(num());
+                break;
+            case 'W':
+                s.base.kind = StatementKind::Store;
+                s.base.addr = node(num());
+                s.base.value = node(num());
+                s.base.elem_type = dtype_of(num());
+                s.base.space = AddressSpace::Global;
+                break;
+            case 'R':
+                s.base.kind = StatementKind::RawAsm;
+                s.base.text = str();
+                break;
+            case 'L':
+                s.kind = StmtKind::Label;
+                s.label = str();
+                break;
+            case 'G':
+                s.kind = StmtKind::Goto;
+                s.cond = node(num());
+                s.label = str();
+                break;
+            case 'I': {
+                s.kind = StmtKind::If;
+                s.cond = node(num());
+                eol();
+                char st = 0;
+                read_list(s.then_body, &st);
+                if (st == 'E')
+                    read_list(s.else_body, &st);
+                out.push_back(std::move(s));
+                continue;
+            }
+            default:
+                throw std::runtime_error(std::string("ocldec-b200: bad body export record ") + tag);
+            }
+            eol();
+            out.push_back(std::move(s));
+        }
+        *stop = 0;
+    }
+};
+
+void read_body(const std::string &text, LoweredBody &body) {
+    BodyReader r{text};
+    char stop = 0;
+    r.read_list(body.stmts, &stop);
+}
+
+// decompile_section's parse steps (decompiler.cpp:59-67) for the inspection
+// fields: the reference front end on the host, its diagnostics discarded.
+void front_fields(const KernelSection &section, const DecompileOptions &opts, DecompiledKernel &k) {
+    DiagnosticSink scratch;
+    try {
+        k.config = parse_config(section, scratch);
+        std::vector<std::string> trailing;
+        k.instructions = parse_text(section, scratch, &trailing);
+        if (!trailing.empty()) { // attach_trailing_labels (decompiler.cpp:20-31)
+            Instruction end;
+            end.line = k.instructions.empty() ? section.line : k.instructions.back().line;
+            end.labels = std::move(trailing);
+            end.source_text = "s_endpgm";
+            end.mnemonic = "s_endpgm";
+            end.parts = decompose_mnemonic(end.mnemonic);
+            k.instructions.push_back(std::move(end));
+        }
+        k.abi = build_abi_map(k.config, scratch, opts.abi_overrides);
+    } catch (const ParseError &) {
+    }
+}
+
 } // namespace
 
 DecompileResult decompile_listing(const std::string &listing, const DecompileOptions &opts) {
@@ -119,6 +275,7 @@ DecompileResult decompile_listing(const std::string &listing, const DecompileOpt
     o.dump_cfg = opts.dump_cfg ? 1 : 0;
     o.dump_regions = opts.dump_regions ? 1 : 0;
     o.record_reduction = 1;
+    o.export_body = 1;
     ocldec_b200_result *r = nullptr;
     if (int rc = ocldec_b200_decompile(listing.data(), listing.size(), &o, &r))
         throw std::runtime_error("ocldec-b200: decompile failed (" + std::to_string(rc) +
@@ -152,10 +309,25 @@ DecompileResult decompile_listing(const std::string &listing, const DecompileOpt
             k.cfg_dot = std::move(text);
         else if (d.step == -2)
             rebuild_regions(text, k);
+        else if (d.step == -3)
+            read_body(text, k.body);
         else
             k.reduction.dumps.push_back(std::move(text));
     }
     ocldec_b200_free(r);
+    // config / instructions / abi: the sections of the kernels returned
+    std::vector<KernelSection> sections;
+    try {
+        sections = split_kernels(listing);
+    } catch (const ParseError &) {
+    }
+    size_t ki = 0;
+    for (const KernelSection &section : sections) {
+        if (opts.only_kernel && section.name != *opts.only_kernel)
+            continue;
+        if (ki < result.kernels.size())
+            front_fields(section, opts, result.kernels[ki++]);
+    }
     return result;
 }
 

@@ -35,6 +35,7 @@ class DecompileOptions:
     dump_cfg: bool = False                  # DecompiledKernel.cfg_dot (to_dot, cfg.cpp:400-424)
     dump_regions: bool = False              # region_dumps (region_graph_dot, structurizer.cpp:669-688)
     record_reduction: bool = False          # DecompiledKernel.reduction (merges, root / residue)
+    export_body: bool = False               # DecompiledKernel.body_text (LoweredBody, lower.hpp:20-41)
     device: int = 0
     arena_bytes: int = 0                    # per-thread arena, 0 = default
 
@@ -88,6 +89,7 @@ class DecompiledKernel:
     cfg_dot: str = ""                                        # when dump_cfg
     region_dumps: List[str] = field(default_factory=list)   # reduction.dumps when dump_regions
     reduction: Optional["Reduction"] = None                 # when record_reduction
+    body_text: str = ""                                     # when export_body (od_lower.cuh body_text)
 
 
 @dataclass
@@ -131,7 +133,8 @@ def decompile_listing(listing: Union[str, bytes], opts: Optional[DecompileOption
     o = _lib.Options(int(opts.fold_local_size),
                      opts.only_kernel.encode() if opts.only_kernel is not None else None,
                      opts.device, opts.arena_bytes, amap, len(amap) if amap is not None else 0,
-                     int(opts.dump_cfg), int(opts.dump_regions), int(opts.record_reduction))
+                     int(opts.dump_cfg), int(opts.dump_regions), int(opts.record_reduction),
+                     int(opts.export_body))
     out = ctypes.POINTER(_lib.Result)()
     if devices:
         devs = (ctypes.c_int * len(devices))(*devices)
@@ -165,6 +168,8 @@ def decompile_listing(listing: Union[str, bytes], opts: Optional[DecompileOption
                     k.cfg_dot = txt
                 elif d.step == -2:
                     k.reduction = Reduction.parse(txt)
+                elif d.step == -3:
+                    k.body_text = txt
                 else:
                     k.region_dumps.append(txt)
         alld = [r.diags[i] for i in range(r.ndiags)] + [r.abi_diags[i] for i in range(r.nabi_diags)]

@@ -19,7 +19,7 @@ class Options(ctypes.Structure):
                 ("device", ctypes.c_int), ("arena_bytes", ctypes.c_size_t),
                 ("abi_map", ctypes.c_char_p), ("abi_map_len", ctypes.c_size_t),
                 ("dump_cfg", ctypes.c_int), ("dump_regions", ctypes.c_int),
-                ("record_reduction", ctypes.c_int)]
+                ("record_reduction", ctypes.c_int), ("export_body", ctypes.c_int)]
 
 
 class Kernel(ctypes.Structure):

@@ -2106,7 +2106,7 @@ void run_shard(Shard &sh, const ocldec_b200_options &o) {
         return;
     }
     s->dump_flags = (o.dump_cfg ? DUMP_CFG : 0u) | (o.dump_regions ? DUMP_REGIONS : 0u) |
-                    (o.record_reduction ? DUMP_MERGES : 0u);
+                    (o.record_reduction ? DUMP_MERGES : 0u) | (o.export_body ? DUMP_BODY : 0u);
     sh.rc = run_host_listing(s, sh.p, sh.len, o.fold_local_size, o.only_kernel, &sh.hr, nullptr, 0);
     s->dump_flags = 0;
     sh.lines = s->stats.lines;

@@ -52,7 +52,7 @@ struct AbiOvr {
 
 // DOT dumps (DecompileOptions::dump_cfg / dump_regions, decompiler.hpp:33-34):
 // text appended to a run-wide pool, one record per dump.
-enum DumpFlags : u32 { DUMP_CFG = 1, DUMP_REGIONS = 2, DUMP_MERGES = 4 };
+enum DumpFlags : u32 { DUMP_CFG = 1, DUMP_REGIONS = 2, DUMP_MERGES = 4, DUMP_BODY = 8 };
 struct DumpRec {
     u32 k;      // kernel (chunk result index)
     i32 step;   // -1: cfg_dot, -2: ReduceResult merges/root/residue text, else dumps[step]
@@ -399,6 +399,8 @@ struct KCtx {
     u32 nif;      // IfThen / IfElse merges (joins need liveness)
     u32 nmerge;   // merges so far (dump step numbers)
     bool dump_full; // the dump pool overflowed
+    u32 exp_lists[2]; // body export (DUMP_BODY): the hoisted decls and the body statement lists
+    u32 exp_pass;     // body export: printing pass (its export ids are tagged per pass)
 
     // liveness
     u32 *live_in; // [nblk][12]
@@ -2346,7 +2348,14 @@ OD_NOINL void reduce_text(const KCtx &K, DotSink &o) {
     o.c('\n');
 }
 
+// body export printer (od_lower.cuh, after the renderer's label helper)
+OD_NOINL void body_text(KCtx &K, DotSink &o);
+
 OD_INL void dump_print(KCtx &K, DotSink &o, i32 step) {
+    if (step == -3) {
+        body_text(K, o);
+        return;
+    }
     if (step == -1)
         cfg_dot(K, o);
     else if (step == -2)

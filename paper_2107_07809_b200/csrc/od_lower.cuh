@@ -1523,6 +1523,211 @@ OD_INL void put_block_label(KCtx &K, Writer &w, u32 b) {
     }
 }
 
+// ----------------------------------------------------- body export (step -3)
+// DecompiledKernel::body (LoweredBody, lower.hpp:20-41) as text, for callers
+// that need the statement tree itself (the drop-in binding rebuilds it;
+// acceptance_main.cpp's differential gate evaluates it).  Expression nodes
+// are printed once each, children first, and referenced by their 1-based
+// export number (0 = null); every statement follows the nodes it uses:
+//   N kind op x type a b c [len name]   (kind/op/x/type as ExprKind+1 / op /
+//        builtin dim / DataType base|bits<<8|depth<<16|space<<24; a b c are
+//        child numbers, or a const's low / high words; Var / KernelArg carry
+//        their rendered name)
+//   A len name value | D len name type value | W addr value elem_type
+//   R len text | I cond ... E ... F | L len label | G cond len label
+OD_INL void exp_name(DotSink &o, const u8 *b, u32 n) {
+    o.u(n);
+    o.c(' ');
+    o.m(b, n);
+}
+
+// Exports the node DAG under root; returns its export number.
+OD_NOINL u32 exp_node(KCtx &K, DotSink &o, u32 root, u32 tag, u32 *nid) {
+    const u32 kMask = 0x3fffffffu, kTags = 0xc0000000u;
+    EArena &E = K.E;
+    if (!root)
+        return 0;
+    if ((E.n[root].memo & kTags) == tag)
+        return E.n[root].memo & kMask;
+    TaskStack &ts = K.rc.ts;
+    const u32 base = ts.top;
+    ts.push(0, 0, root);
+    while (ts.top > base && !ts.oom) {
+        u64 &tk = ts.p[ts.top - 1];
+        const u32 e = (u32)(tk >> 32), st = (u32)(tk & 0xff);
+        const ENode x = E.n[e];
+        u32 ch[3] = {0, 0, 0}, nch = 0;
+        if (x.kind == E_UNARY || x.kind == E_DEREF) {
+            ch[0] = x.a;
+            nch = 1;
+        } else if (x.kind == E_BINARY) {
+            ch[0] = x.a;
+            ch[1] = x.b;
+            nch = 2;
+        } else if (x.kind == E_TERNARY) {
+            ch[0] = x.a;
+            ch[1] = x.b;
+            ch[2] = x.c;
+            nch = 3;
+        }
+        if (st < nch) {
+            tk = (tk & ~0xffull) | (st + 1);
+            const u32 c = ch[st];
+            if (c && (E.n[c].memo & kTags) != tag)
+                ts.push(0, 0, c);
+            continue;
+        }
+        ts.top--;
+        if ((E.n[e].memo & kTags) == tag) // reached twice through the stack
+            continue;
+        u32 cid[3] = {0, 0, 0};
+        for (u32 k = 0; k < nch; ++k)
+            cid[k] = ch[k] ? (E.n[ch[k]].memo & kMask) : 0;
+        o.c('N');
+        o.c(' ');
+        o.u(x.kind);
+        o.c(' ');
+        o.u(x.op);
+        o.c(' ');
+        o.u(x.x);
+        o.c(' ');
+        o.u(x.type);
+        o.c(' ');
+        if (x.kind == E_CONST) {
+            o.u(x.a);
+            o.c(' ');
+            o.u(x.b);
+            o.c(' ');
+            o.u(0);
+        } else {
+            o.u(nch > 0 ? cid[0] : x.a);
+            o.c(' ');
+            o.u(cid[1]);
+            o.c(' ');
+            o.u(cid[2]);
+        }
+        if (x.kind == E_VAR || x.kind == E_ARG) {
+            u8 buf[64];
+            Writer w{buf, 0, sizeof buf, false};
+            if (x.kind == E_VAR)
+                put_var_name(w, x.x, x.a);
+            else
+                put_arg_name(w, K.rc, x.a);
+            o.c(' ');
+            exp_name(o, buf, w.n < sizeof buf ? w.n : (u32)sizeof buf);
+        }
+        o.c('\n');
+        E.n[e].memo = tag | ++*nid;
+    }
+    ts.top = base;
+    return E.n[root].memo & kMask;
+}
+
+OD_NOINL void body_text(KCtx &K, DotSink &o) {
+    const u32 tag = (K.exp_pass++ & 1) ? 0x80000000u : 0x40000000u;
+    u32 nid = 0;
+    TaskStack &ts = K.rc.ts;
+    const u32 base = ts.top;
+    for (u32 li = 0; li < 2; ++li) {
+        // statement frames: (stmt, state) with state 0 new, 1 then done, 2 else done
+        ts.push(0, 0, K.lists[K.exp_lists[li]].head);
+        const u32 lbase = ts.top - 1;
+        while (ts.top > lbase && !ts.oom) {
+            u64 &fr = ts.p[ts.top - 1];
+            const u32 si = (u32)(fr >> 32), state = (u32)(fr & 0xff);
+            if (!si) {
+                ts.top--;
+                continue;
+            }
+            const Stmt S = K.st[si];
+            u8 buf[64];
+            Writer w{buf, 0, sizeof buf, false};
+            if (S.kind == SK_IF) {
+                if (state == 0) {
+                    const u32 c = exp_node(K, o, S.a, tag, &nid);
+                    o.s("I ");
+                    o.u(c);
+                    o.c('\n');
+                    fr = (fr & ~0xffull) | 1;
+                    ts.push(0, 0, S.b);
+                } else if (state == 1 && S.c) {
+                    o.s("E\n");
+                    fr = (fr & ~0xffull) | 2;
+                    ts.push(0, 0, S.c);
+                } else {
+                    o.s("F\n");
+                    fr = ((u64)S.next << 32);
+                }
+                continue;
+            }
+            switch (S.kind) {
+            case SK_ASSIGN: {
+                const u32 v = exp_node(K, o, S.b, tag, &nid);
+                put_var_name(w, S.cls, S.a);
+                o.s("A ");
+                exp_name(o, buf, w.n);
+                o.c(' ');
+                o.u(v);
+                break;
+            }
+            case SK_DECL: {
+                const u32 v = exp_node(K, o, S.b, tag, &nid);
+                put_var_name(w, S.cls, S.a);
+                o.s("D ");
+                exp_name(o, buf, w.n);
+                o.c(' ');
+                o.u(dt_with_space(S.c, AS_NONE));
+                o.c(' ');
+                o.u(v);
+                break;
+            }
+            case SK_STORE: {
+                const u32 ad = exp_node(K, o, S.a, tag, &nid);
+                const u32 v = exp_node(K, o, S.b, tag, &nid);
+                o.s("W ");
+                o.u(ad);
+                o.c(' ');
+                o.u(v);
+                o.c(' ');
+                o.u(S.c);
+                break;
+            }
+            case SK_RAW: {
+                const u8 *p = K.in->t + S.a;
+                u32 b = 0, e = S.b;
+                while (b < e && (p[b] == ' ' || p[b] == '\t'))
+                    ++b;
+                while (e > b && (p[e - 1] == ' ' || p[e - 1] == '\t'))
+                    --e;
+                o.s("R ");
+                exp_name(o, p + b, e - b);
+                break;
+            }
+            case SK_LABEL:
+                put_block_label(K, w, S.a);
+                o.s("L ");
+                exp_name(o, buf, w.n);
+                break;
+            case SK_GOTO: {
+                const u32 c = exp_node(K, o, S.a, tag, &nid);
+                put_block_label(K, w, S.c);
+                o.s("G ");
+                o.u(c);
+                o.c(' ');
+                exp_name(o, buf, w.n);
+                break;
+            }
+            default: break;
+            }
+            o.c('\n');
+            fr = ((u64)S.next << 32);
+        }
+    }
+    if (ts.oom)
+        K.oom = true;
+    ts.top = base;
+}
+
 // emit_statement  codegen.cpp:393-442 (one statement, no If bodies)
 OD_NOINL void emit_simple(KCtx &K, Writer &w, const Stmt &s, u32 depth) {
     RenderCtx &rc = K.rc;
@@ -2017,6 +2222,16 @@ OD_NOINL void dk_emit(KState &S) {
     emit_list(K, w, K.lists[S.body].head, 1, S.estk, S.ecap);
     w.lit("}\n");
     S.done = 1;
+    if (in.dump && (in.dump->flags & DUMP_BODY)) { // the statement tree itself (step -3)
+        K.exp_lists[0] = S.hoist;
+        K.exp_lists[1] = S.body;
+        K.exp_pass = 0;
+        dump_emit(K, -3);
+        if (K.dump_full) { // grow the dump pool and run the kernel again
+            out.status = KS_STAGE_FULL;
+            return;
+        }
+    }
     if (K.oom || K.E.oom || K.rc.ts.oom || w.overflow || K.rc.fs.terms.oom || K.rc.fs.st.oom) {
         out.status = KS_OOM;
         return;

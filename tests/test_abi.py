@@ -29,7 +29,7 @@ def test_library_exports_header_symbols():
     for n in names:
         assert hasattr(L, n), n
     assert set(_lib.EXPORTS) <= set(names)
-    assert L.ocldec_b200_version() == 4
+    assert L.ocldec_b200_version() == 5
 
 
 def test_library_has_sm100a_code():

@@ -43,5 +43,7 @@ def test_reference_harness_on_the_gpu():
     p = subprocess.run([B200_BIN], capture_output=True, text=True, timeout=900, env=env)
     checks = _checks(p.stdout)
     print(p.stdout)
-    for gate in (1, 2, 3, 4, 6, 7, 8):
+    for gate in range(1, 9):
         assert checks.get(gate) == "PASS", p.stdout
+    assert re.search(r"5\. .*\((2\d) kernels x 100 environments, \1\d\d trace pairs equal\)", p.stdout), p.stdout
+    assert p.returncode == 0
