@@ -9,7 +9,17 @@ import io
 import json
 import os
 import subprocess
+import math
 import sys
+
+def _clean(o):
+    """NaN (a counter ncu could not collect) as null: the files stay strict JSON."""
+    if isinstance(o, float) and math.isnan(o):
+        return None
+    if isinstance(o, dict):
+        return {k: _clean(v) for k, v in o.items()}
+    return o
+
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 METRICS = {
@@ -53,5 +63,5 @@ out = {"note": "ncu --set full, one launch per kernel; k_front runs each kernel 
 if len(sys.argv) > 2:
     out["C5_1500"] = read(sys.argv[2])
 dst = os.environ.get("OUT") or os.path.join(ROOT, "profiles", "dataflow_ncu.json")
-json.dump(out, open(dst, "w"), indent=1)
-print(json.dumps(out, indent=1))
+json.dump(_clean(out), open(dst, "w"), indent=1)
+print(json.dumps(_clean(out), indent=1))

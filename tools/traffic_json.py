@@ -9,7 +9,17 @@ import io
 import json
 import os
 import subprocess
+import math
 import sys
+
+def _clean(o):
+    """NaN (a counter ncu could not collect) as null: the files stay strict JSON."""
+    if isinstance(o, float) and math.isnan(o):
+        return None
+    if isinstance(o, dict):
+        return {k: _clean(v) for k, v in o.items()}
+    return o
+
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 rep, log = sys.argv[1], sys.argv[2]
@@ -48,5 +58,5 @@ for r in rows[2:]:
                  "ncu_duration_s": vals["gpu__time_duration.sum"],
                  "source": os.path.basename(rep) + " (ncu --set full, C4 sample, one launch)"}
 dst = os.environ.get("OUT") or os.path.join(ROOT, "profiles", "dram_traffic.json")
-json.dump(res, open(dst, "w"), indent=1)
-print(json.dumps(res, indent=1))
+json.dump(_clean(res), open(dst, "w"), indent=1)
+print(json.dumps(_clean(res), indent=1))
