@@ -47,3 +47,17 @@ def test_reference_harness_on_the_gpu():
         assert checks.get(gate) == "PASS", p.stdout
     assert re.search(r"5\. .*\((2\d) kernels x 100 environments, \1\d\d trace pairs equal\)", p.stdout), p.stdout
     assert p.returncode == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(B200_BIN), reason="drop-in harness not built (make -C oracle -f dropin.mk)")
+def test_differential_gate_sees_the_gpu_body():
+    """Negative control: with the GPU's body withheld from the binding
+    (OCLDEC_B200_DROPIN_NO_BODY=1) the differential gate fails, so its pass
+    above is a comparison of the GPU's lowered bodies, not of empty traces."""
+    env = dict(os.environ, LD_LIBRARY_PATH=os.path.join(ROOT, "paper_2107_07809_b200"),
+               OCLDEC_B200_DROPIN_NO_BODY="1")
+    p = subprocess.run([B200_BIN], capture_output=True, text=True, timeout=900, env=env)
+    checks = _checks(p.stdout)
+    assert checks.get(5) == "FAIL", p.stdout
+    assert p.returncode != 0
