@@ -1280,6 +1280,10 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
             CK(cudaEventRecord(pe[3], ws));
             a.lanes_per = s->lanes_emit;
             k_emit<<<grid(a.lanes_per), OD_BLOCK, s->smem_emit, ws>>>(a);
+            if (s->dump_flags & DUMP_BODY) {
+                k_export<<<grid(a.lanes_per), OD_BLOCK, 0, ws>>>(a);
+                s->stats.total_launches++;
+            }
             CK(cudaEventRecord(pe[4], ws));
             s->stats.decompile_launches += 4;
             s->stats.total_launches += 4;

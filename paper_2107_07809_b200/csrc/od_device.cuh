@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_LOWER * 128 / OD_BLOCK) k_lo
 constexpr u32 kWideJoins = 64; // if-joins from which a kernel is lowered by the whole warp (long-kernel chunks)
 __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_FOLD * 128 / OD_BLOCK) k_fold(DecompArgs a);
 __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_EMIT * 128 / OD_BLOCK) k_emit(DecompArgs a);
+__global__ void __launch_bounds__(OD_BLOCK) k_export(DecompArgs a);
 
 // ------------------------------------------------------------------ generator
 struct GenArgs {

@@ -2193,6 +2193,19 @@ OD_NOINL void dk_fold(KState &S) {
 }
 
 // emit_kernel  codegen.cpp:446-467
+// The lowered statement tree as a step -3 dump (k_export, after k_emit, only
+// when DUMP_BODY is requested).  Returns false when the dump pool is full.
+OD_NOINL bool dk_export(KState &S) {
+    KCtx &K = S.K;
+    K.rc.fs = K.fs;
+    K.exp_lists[0] = S.hoist;
+    K.exp_lists[1] = S.body;
+    K.exp_pass = 0;
+    K.dump_full = false;
+    dump_emit(K, -3);
+    return !K.dump_full;
+}
+
 OD_NOINL void dk_emit(KState &S) {
     const KIn &in = S.in;
     KCtx &K = S.K;
@@ -2222,16 +2235,6 @@ OD_NOINL void dk_emit(KState &S) {
     emit_list(K, w, K.lists[S.body].head, 1, S.estk, S.ecap);
     w.lit("}\n");
     S.done = 1;
-    if (in.dump && (in.dump->flags & DUMP_BODY)) { // the statement tree itself (step -3)
-        K.exp_lists[0] = S.hoist;
-        K.exp_lists[1] = S.body;
-        K.exp_pass = 0;
-        dump_emit(K, -3);
-        if (K.dump_full) { // grow the dump pool and run the kernel again
-            out.status = KS_STAGE_FULL;
-            return;
-        }
-    }
     if (K.oom || K.E.oom || K.rc.ts.oom || w.overflow || K.rc.fs.terms.oom || K.rc.fs.st.oom) {
         out.status = KS_OOM;
         return;

@@ -61,6 +61,23 @@ __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_FOLD * 128 / OD_BLOCK) k_fol
 #endif
 }
 
+// DUMP_BODY: the lowered statement tree of every kernel that emitted, as a
+// step -3 dump (a separate launch: the emit path pays nothing for it).
+__global__ void __launch_bounds__(OD_BLOCK) k_export(DecompArgs a) {
+    Slot0 sl;
+    if (!dk_slot(a, &sl))
+        return;
+    const u32 k = sl.k;
+    if (a.res[k].status != KS_OK)
+        return;
+    KState S;
+    kstate_load(S, reinterpret_cast<KState *>(sl.base));
+    if (!dk_export(S))
+        a.res[k].status = KS_STAGE_FULL; // the host grows the dump pool and re-runs the kernel
+    if (a.res[k].status == KS_STAGE_FULL)
+        atomicAdd(a.retry_cnt, 1u);
+}
+
 __device__ __noinline__ void emit_one(const DecompArgs &a, const Slot0 &sl, const uint4 **cs, uint4 **cd,
                                       u32 *cn);
 
