@@ -114,7 +114,11 @@ def dataflow_profile():
     p = os.path.join(ROOT, "profiles", "dataflow_ncu.json")
     if not os.path.exists(p):
         return None
-    d = json.load(open(p))
+    def clean(o):  # NaN (a counter ncu could not collect) as null: the line stays strict JSON
+        if isinstance(o, float) and o != o:
+            return None
+        return {k: clean(v) for k, v in o.items()} if isinstance(o, dict) else o
+    d = clean(json.load(open(p)))
     d["source"] = "profiles/dataflow_ncu.json (ncu --set full of the phase kernels, C4 / C5 samples)"
     return d
 
