@@ -250,7 +250,7 @@ def spawn_ranks(args):
     os.execv(sys.executable, cmd)
 
 
-def run_stream(args, P, torch, dist, world, rank, local, nk):
+def run_stream(args, P, torch, dist, world, rank, local, nk, cdev="cuda"):
     """Streaming mode (C5: 1M kernels x ~10k instructions, ~320 GB of
     listing, more than HBM): the fixed corpus [0, nk) is split across ranks by
     kernel index (strong scaling); each rank generates a chunk of its range
@@ -286,9 +286,9 @@ def run_stream(args, P, torch, dist, world, rank, local, nk):
     tot = np.array([acc["ms_decompile"], acc["ms_wall"], st["instructions"], st["in_bytes"], st["out_bytes"],
                     st["kernels"]], dtype=np.float64)
     if world > 1:
-        t = torch.tensor(tot[:2], dtype=torch.float64, device="cuda")
+        t = torch.tensor(tot[:2], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        u = torch.tensor(tot[2:], dtype=torch.float64, device="cuda")
+        u = torch.tensor(tot[2:], dtype=torch.float64, device=cdev)
         dist.all_reduce(u, op=dist.ReduceOp.SUM)
         tot = np.concatenate([t.cpu().numpy(), u.cpu().numpy()])
     ms_dec, ms_wall, ninstr, in_b, out_b, nker = tot
@@ -373,13 +373,22 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU over NCCL; OCLDEC_BENCH_DIST=gloo runs the ranks'
+    # exchange over gloo instead (several ranks on one GPU: a test of the
+    # multi-rank path on a one-GPU box)
+    backend = os.environ.get("OCLDEC_BENCH_DIST", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
+    cdev = "cuda" if backend == "nccl" else "cpu"  # the collectives' tensors
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     cfg = args.config
     nk = args.kernels or DEFAULT_KERNELS[cfg]
     if args.stream or cfg == "C5":
-        run_stream(args, P, torch, dist, world, rank, local, nk)
+        run_stream(args, P, torch, dist, world, rank, local, nk, cdev)
         return
     sess = P.Session(local)
     # outputs of interest: combined_source (device; pinned host for e2e) and
@@ -400,7 +409,7 @@ def main():
         if world > 1:
             # the one exchange step: every rank's {out_bytes, lines, split
             # error, kernels} -> its offset in the job's combined output
-            st["placement"] = D.place(D.exchange(st["out_bytes"], st["lines"], 0, st["kernels"], device="cuda"),
+            st["placement"] = D.place(D.exchange(st["out_bytes"], st["lines"], 0, st["kernels"], device=cdev),
                                       rank)
         return st
 
@@ -433,7 +442,7 @@ def main():
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
@@ -447,26 +456,38 @@ def main():
     e2e = None
     if not args.no_e2e:
         try:
-            host_in = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
-            P.copy(host_in.data_ptr(), d_buf, nbytes)
-            out_cap = int(out_b * 1.1) + (1 << 20)
+            # N > 1: each rank's first 250k kernels (~4.8 GB of listing) keep
+            # the job's pinned host memory bounded (N x 28 GB otherwise)
+            e_nk = nk if world == 1 else min(nk, 250_000)
+            e_bytes = int(host_offs[e_nk])
+            e_instr = ninstr if e_nk == nk else None
+            host_in = torch.empty(e_bytes, dtype=torch.uint8, pin_memory=True)
+            P.copy(host_in.data_ptr(), d_buf, e_bytes)
+            out_cap = int(out_b * (e_bytes / nbytes) * 1.1) + (1 << 20)
             host_out = torch.empty(out_cap, dtype=torch.uint8, pin_memory=True)
             e_steps = max(1, min(args.steps, 3))
-            sess.run_host(host_in.data_ptr(), nbytes, host_out.data_ptr(), out_cap)  # warm
+            sess.run_host(host_in.data_ptr(), e_bytes, host_out.data_ptr(), out_cap)  # warm
+            if e_instr is None:
+                e_instr = sess.stats()["instructions"]
             torch.cuda.synchronize()
             if world > 1:
                 dist.barrier()
             t0 = time.perf_counter()
             for _ in range(e_steps):
-                n_out = sess.run_host(host_in.data_ptr(), nbytes, host_out.data_ptr(), out_cap)
+                n_out = sess.run_host(host_in.data_ptr(), e_bytes, host_out.data_ptr(), out_cap)
             t_e = (time.perf_counter() - t0) / e_steps
+            e_total = e_instr
             if world > 1:
-                t = torch.tensor([t_e], dtype=torch.float64, device="cuda")
+                t = torch.tensor([t_e], dtype=torch.float64, device=cdev)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 t_e = float(t.item())
-            e2e = {"value": total_instr / t_e, "unit": "instr/s", "h2d_bytes_per_step": int(nbytes),
+                u = torch.tensor([float(e_instr)], dtype=torch.float64, device=cdev)
+                dist.all_reduce(u, op=dist.ReduceOp.SUM)
+                e_total = float(u.item())
+            e2e = {"value": e_total / t_e, "unit": "instr/s", "h2d_bytes_per_step": int(e_bytes),
                    "d2h_bytes_per_step": int(n_out), "seconds_per_step": t_e,
-                   "path": "ocldec_b200_session_run_host (pinned host in/out)"}
+                   "path": "ocldec_b200_session_run_host (pinned host in/out)",
+                   "kernels_per_gpu": e_nk}
             del host_in, host_out
         except Exception as ex:  # pragma: no cover
             e2e = {"value": None, "unit": "instr/s", "error": str(ex)[:200]}
