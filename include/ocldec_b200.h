@@ -46,6 +46,11 @@ typedef struct ocldec_b200_options {
     int export_body;         /* DecompiledKernel::body (LoweredBody, lower.hpp:20-41) as a step -3
                                 dump: expression nodes and the statement tree in the text format
                                 of od_lower.cuh's body_text (ABI v5) */
+    int semantic_check;      /* the batched semantic check (ABI v5): per kernel,
+                                the reference's differential backend (interpret_asm vs
+                                evaluate_decompiled, oracle.cpp) restated on the device, over 8
+                                sampled environments; results in ocldec_b200_result.sem */
+    uint64_t semantic_seed;  /* environment stream seed (od_semenv.cuh) */
 } ocldec_b200_options;
 
 /* DecompiledKernel (decompiler.hpp:39-52): the printed source and flags. */
@@ -78,6 +83,19 @@ typedef struct ocldec_b200_dump {
     uint64_t off, len;
 } ocldec_b200_dump;
 
+/* One kernel's semantic check: status 0 equal traces in every environment,
+ * 1 a mismatch, 2 unsupported (either side left the interpreted subset, as
+ * OracleUnsupported), 3 not compared (the device's trace / variable room ran
+ * out), 4 not run (failed or skipped kernel); the hashes sum, over the
+ * environments, a mix of each write trace's FNV-1a hash and length
+ * (od_semenv.cuh), for the assembly and the decompiled body. */
+typedef struct ocldec_b200_semcheck {
+    uint32_t status;
+    uint32_t envs;
+    uint64_t hash_asm;
+    uint64_t hash_body;
+} ocldec_b200_semcheck;
+
 typedef struct ocldec_b200_result {
     uint64_t nkernels;
     ocldec_b200_kernel *kernels;
@@ -97,6 +115,7 @@ typedef struct ocldec_b200_result {
     uint64_t ndumps;              /* DOT dumps (options dump_cfg / dump_regions), by kernel then step */
     ocldec_b200_dump *dumps;
     char *dump_text;
+    ocldec_b200_semcheck *sem;    /* per kernel (aligned with kernels) when semantic_check, else NULL */
 } ocldec_b200_result;
 
 /* decompile_listing: host buffer in, host result out (H2D/D2H inside). */

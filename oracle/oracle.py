@@ -63,6 +63,9 @@ def lib():
                                         ctypes.c_size_t, ctypes.c_int, ctypes.c_int,
                                         ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_size_t)]
         L.ref_decompile_par.restype = ctypes.c_int
+        L.ref_semcheck.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_void_p,
+                                   ctypes.c_size_t]
+        L.ref_semcheck.restype = ctypes.c_int64
         _lib = L
     return _lib
 
@@ -181,6 +184,17 @@ def decompile_par(listing: bytes, kernel_starts, nthreads: int = 0, per: int = 6
     blob = _take(out.value, n.value)
     L.ref_free(out)
     return _parse(blob)
+
+
+def semcheck(listing: bytes, seed: int, cap: int = 1 << 20):
+    """The reference's interpret_asm / evaluate_decompiled (oracle.cpp:620-842)
+    per kernel over the semantic check's 8 environments (od_semenv.cuh):
+    [(status, envs, hash_asm, hash_body)], statuses as the device check's."""
+    import numpy as np
+    L = lib()
+    out = np.zeros(4 * cap, dtype=np.uint64)
+    n = L.ref_semcheck(listing, len(listing), seed, out.ctypes.data, cap)
+    return [tuple(int(x) for x in out[4 * k:4 * k + 4]) for k in range(min(n, cap))]
 
 
 SHAPES = {"C1": 1, "C2": 2, "C3": 3, "C4": 4, "C5": 5}

@@ -26,7 +26,9 @@
 #include <vector>
 
 #include "ocldec/decompiler.hpp"
+#include "ocldec/oracle.hpp"
 #include "corpus.hpp"
+#include "../paper_2107_07809_b200/csrc/od_semenv.cuh"
 #include "nestgen.hpp"
 
 namespace {
@@ -377,6 +379,89 @@ int ref_decompile_par(const char *listing, size_t len, const uint64_t *kstart, s
     ser += combined;
     *out = dup_out(ser, out_len);
     return 0;
+}
+
+
+// The reference side of the batched semantic check (od_oracle.cuh): for every
+// kernel of decompile_listing(listing), the reference's own interpret_asm and
+// evaluate_decompiled (oracle.cpp:620-842) over the 8 environments
+// od_semenv.cuh derives from (seed, kernel index, environment index).
+// out: 4 u64 per kernel {status, envs, hash_asm, hash_body} with the device
+// check's statuses (0 equal, 1 mismatch, 2 unsupported, 4 not run).  Returns
+// the kernel count (<= cap).
+struct SemJob {
+    const char *listing;
+    size_t len;
+    uint64_t seed;
+    uint64_t *out;
+    size_t cap;
+    size_t nk = 0;
+};
+
+void *semcheck_job(void *p) {
+    auto *job = static_cast<SemJob *>(p);
+    using namespace ocldec;
+    DecompileResult res = decompile_listing(std::string(job->listing, job->len));
+    job->nk = res.kernels.size();
+    for (size_t k = 0; k < res.kernels.size() && k < job->cap; ++k) {
+        const DecompiledKernel &K = res.kernels[k];
+        uint64_t *o = job->out + 4 * k;
+        if (K.failed) {
+            o[0] = od::SEM_NOT_RUN, o[1] = 0, o[2] = 0, o[3] = 0;
+            continue;
+        }
+        bool unsupported = false, mismatch = false;
+        uint64_t ha = 0, hb = 0;
+        const uint32_t envs = 8;
+        for (uint32_t n = 0; n < envs; ++n) {
+            od::SemRng r = od::sem_stream(job->seed, k, n);
+            od::SemEnv e;
+            const uint32_t cws[3] = {K.config.cws[0], K.config.cws[1], K.config.cws[2]};
+            od::sem_env(r, n, uint32_t(K.config.dims), cws, &e);
+            OracleEnv env;
+            env.dims = K.config.dims;
+            for (int d = 0; d < 3; ++d) {
+                env.cws[size_t(d)] = e.cws[d];
+                env.num_groups[size_t(d)] = e.num_groups[d];
+                env.group_id[size_t(d)] = e.group_id[d];
+                env.local_id[size_t(d)] = e.local_id[d];
+                env.global_offset[size_t(d)] = e.global_offset[d];
+            }
+            env.mem_seed = e.mem_seed;
+            for (const ArgDecl &a : K.config.args)
+                if (!a.is_implicit)
+                    env.arg_values[a.name] =
+                        od::sem_arg(r, &e, a.type.is_pointer(), a.type.is_float(), a.type.bits);
+            WriteTrace A, B;
+            try {
+                A = interpret_asm(K.instructions, K.config, K.abi, env);
+                B = evaluate_decompiled(K.body, K.config, env);
+            } catch (const std::exception &) { // OracleUnsupported (or an out-of-range register)
+                unsupported = true;
+                continue;
+            }
+            uint64_t h = od::kSemTraceSeed;
+            for (const TraceEntry &t : A)
+                h = od::sem_trace_step(h, t.addr, t.value);
+            ha += od::sem_env_mix(h, A.size(), n);
+            h = od::kSemTraceSeed;
+            for (const TraceEntry &t : B)
+                h = od::sem_trace_step(h, t.addr, t.value);
+            hb += od::sem_env_mix(h, B.size(), n);
+            mismatch |= !(A == B);
+        }
+        o[0] = unsupported ? od::SEM_UNSUPPORTED : mismatch ? od::SEM_MISMATCH : od::SEM_EQUAL;
+        o[1] = envs;
+        o[2] = ha;
+        o[3] = hb;
+    }
+    return nullptr;
+}
+
+int64_t ref_semcheck(const char *listing, size_t len, uint64_t seed, uint64_t *out, size_t cap) {
+    SemJob job{listing, len, seed, out, cap};
+    run_on_big_stack(semcheck_job, &job);
+    return int64_t(job.nk);
 }
 
 } // extern "C"

@@ -36,6 +36,8 @@ class DecompileOptions:
     dump_regions: bool = False              # region_dumps (region_graph_dot, structurizer.cpp:669-688)
     record_reduction: bool = False          # DecompiledKernel.reduction (merges, root / residue)
     export_body: bool = False               # DecompiledKernel.body_text (LoweredBody, lower.hpp:20-41)
+    semantic_check: bool = False            # DecompiledKernel.semantic (the batched semantic check)
+    semantic_seed: int = 0x5E3A171C
     device: int = 0
     arena_bytes: int = 0                    # per-thread arena, 0 = default
 
@@ -90,6 +92,8 @@ class DecompiledKernel:
     region_dumps: List[str] = field(default_factory=list)   # reduction.dumps when dump_regions
     reduction: Optional["Reduction"] = None                 # when record_reduction
     body_text: str = ""                                     # when export_body (od_lower.cuh body_text)
+    semantic: Optional[tuple] = None  # when semantic_check: (status, envs, hash_asm, hash_body);
+    # status 0 equal, 1 mismatch, 2 unsupported, 3 not compared (device room), 4 not run
 
 
 @dataclass
@@ -134,7 +138,7 @@ def decompile_listing(listing: Union[str, bytes], opts: Optional[DecompileOption
                      opts.only_kernel.encode() if opts.only_kernel is not None else None,
                      opts.device, opts.arena_bytes, amap, len(amap) if amap is not None else 0,
                      int(opts.dump_cfg), int(opts.dump_regions), int(opts.record_reduction),
-                     int(opts.export_body))
+                     int(opts.export_body), int(opts.semantic_check), opts.semantic_seed)
     out = ctypes.POINTER(_lib.Result)()
     if devices:
         devs = (ctypes.c_int * len(devices))(*devices)
@@ -158,6 +162,9 @@ def decompile_listing(listing: Union[str, bytes], opts: Optional[DecompileOption
                 source=src.decode("utf-8", errors="surrogateescape"),
                 structured=bool(k.structured), failed=bool(k.failed),
                 fallback_count=k.fallback_count, instructions=k.instructions))
+            if r.sem:
+                sc = r.sem[i]
+                res.kernels[-1].semantic = (sc.status, sc.envs, sc.hash_asm, sc.hash_body)
         if r.ndumps:
             dl = [r.dumps[i] for i in range(r.ndumps)]
             dtext = ctypes.string_at(r.dump_text, max(d.off + d.len for d in dl))

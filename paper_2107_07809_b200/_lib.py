@@ -19,7 +19,8 @@ class Options(ctypes.Structure):
                 ("device", ctypes.c_int), ("arena_bytes", ctypes.c_size_t),
                 ("abi_map", ctypes.c_char_p), ("abi_map_len", ctypes.c_size_t),
                 ("dump_cfg", ctypes.c_int), ("dump_regions", ctypes.c_int),
-                ("record_reduction", ctypes.c_int), ("export_body", ctypes.c_int)]
+                ("record_reduction", ctypes.c_int), ("export_body", ctypes.c_int),
+                ("semantic_check", ctypes.c_int), ("semantic_seed", ctypes.c_uint64)]
 
 
 class Kernel(ctypes.Structure):
@@ -39,6 +40,11 @@ class Dump(ctypes.Structure):
                 ("off", ctypes.c_uint64), ("len", ctypes.c_uint64)]
 
 
+class SemCheck(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_uint32), ("envs", ctypes.c_uint32), ("hash_asm", ctypes.c_uint64),
+                ("hash_body", ctypes.c_uint64)]
+
+
 class Result(ctypes.Structure):
     _fields_ = [("nkernels", ctypes.c_uint64), ("kernels", ctypes.POINTER(Kernel)),
                 ("names", ctypes.c_void_p), ("combined", ctypes.c_void_p),
@@ -47,7 +53,8 @@ class Result(ctypes.Structure):
                 ("device_ms", ctypes.c_double), ("ndiags", ctypes.c_uint64),
                 ("diags", ctypes.POINTER(Diag)), ("diag_text", ctypes.c_void_p),
                 ("nabi_diags", ctypes.c_uint64), ("abi_diags", ctypes.POINTER(Diag)),
-                ("ndumps", ctypes.c_uint64), ("dumps", ctypes.POINTER(Dump)), ("dump_text", ctypes.c_void_p)]
+                ("ndumps", ctypes.c_uint64), ("dumps", ctypes.POINTER(Dump)), ("dump_text", ctypes.c_void_p),
+                ("sem", ctypes.POINTER(SemCheck))]
 
 
 class Stats(ctypes.Structure):

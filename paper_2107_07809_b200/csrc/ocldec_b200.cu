@@ -30,6 +30,7 @@
 
 #include "../../include/ocldec_b200.h"
 #include "od_device.cuh"
+#include "od_oracle.cuh"
 #include "od_scan.cuh"
 
 using namespace od;
@@ -932,6 +933,10 @@ struct ocldec_b200_session {
     DevBuf rstat;                    // per-chunk result totals (k_res_stats)
     bool keep_records = true;        // per-kernel host records (names, spans, flags, diagnostics)
     bool wide_lower = false;         // OCLDEC_B200_WIDE_LOWER: k_lower_wide for long-kernel chunks
+    bool sem_on = false;             // the batched semantic check of the current call
+    u64 sem_seed = 0;
+    DevBuf semres, semscratch;       // per chunk kernel: SemResult; the check's lane scratch
+    std::vector<ocldec_b200_semcheck> host_sem; // per host_res kernel
     u32 novr = 0;
     std::vector<u64> host_kdiag;     // per kernel: first host_diag index (count in host_res[k].ndiag)
     size_t pev_used = 0;
@@ -1167,6 +1172,9 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     a.only_len = s->only_len;
     a.prof = s->prof_on ? P<u64>(s->prof) : nullptr;
     a.retry_cnt = cnt + 12;
+    if (s->sem_on && (ensure(s->semres, (u64)nk * sizeof(SemResult) + 16) ||
+                      ensure(s->semscratch, (u64)kSemBatch * kSemEnvs * kSemLaneBytes)))
+        return -3;
     // OCLDEC_B200_WIDE_LOWER=1: in chunks of long kernels (C5: ~340 KB of
     // listing, hundreds of if-joins each) kernels with >= kWideJoins joins are
     // lowered by the whole warp (k_lower_wide, lane-parallel merge_join /
@@ -1283,6 +1291,15 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
             if (s->dump_flags & DUMP_BODY) {
                 k_export<<<grid(a.lanes_per), OD_BLOCK, 0, ws>>>(a);
                 s->stats.total_launches++;
+            }
+            if (s->sem_on) { // the batched semantic check, kSemBatch kernels per launch
+                for (u32 b0 = 0; b0 < a.count; b0 += kSemBatch) {
+                    const u32 nb = std::min<u32>(kSemBatch, a.count - b0);
+                    k_semcheck<<<(nb * 32 + 127) / 128, 128, 0, ws>>>(a, b0, nb, P<u8>(s->semscratch),
+                                                                       P<SemResult>(s->semres), s->sem_seed,
+                                                                       s->stats.kernels);
+                    s->stats.total_launches++;
+                }
             }
             CK(cudaEventRecord(pe[4], ws));
             s->stats.decompile_launches += 4;
@@ -1548,6 +1565,13 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
             s->host_dumps.push_back(std::move(v));
         }
     }
+    if (s->sem_on) {
+        std::vector<SemResult> sv(nk);
+        if (d2h_sync(s, sv.data(), s->semres.p, (u64)nk * sizeof(SemResult)))
+            return -3;
+        for (u32 k = 0; k < nk; ++k)
+            s->host_sem.push_back(ocldec_b200_semcheck{sv[k].status, sv[k].envs, sv[k].hash_asm, sv[k].hash_body});
+    }
     for (u32 k = 0; k < nk; ++k) {
         s->host_res.push_back(hr[k]);
         s->host_kernel_off.push_back(base + offs[k]);
@@ -1657,6 +1681,7 @@ void reset_stats(ocldec_b200_session *s) {
     s->host_diag.clear();
     s->host_kdiag.clear();
     s->host_dumps.clear();
+    s->host_sem.clear();
     s->out_len = 0;
 }
 
@@ -1920,7 +1945,7 @@ void ocldec_b200_session_destroy(ocldec_b200_session *s) {
                       &s->outoff, &s->out, &s->only, &s->retry, &s->gen_len, &s->gen_ninstr,
                       &s->gen_buf, &s->gen_off, &s->kmeta, &s->order, &s->budget, &s->sbudget,
                       &s->boff, &s->hist, &s->prof, &s->ksizes, &s->dpool, &s->dtop, &s->perm, &s->cnt4,
-                      &s->dovr, &s->dovr_text, &s->xtext, &s->xrec, &s->xtop, &s->xcfg, &s->sgen, &s->rstat};
+                      &s->dovr, &s->dovr_text, &s->xtext, &s->xrec, &s->xtop, &s->xcfg, &s->sgen, &s->rstat, &s->semres, &s->semscratch};
     for (DevBuf *b : bufs)
         if (b->p)
             cudaFree(b->p);
@@ -2111,8 +2136,11 @@ void run_shard(Shard &sh, const ocldec_b200_options &o) {
     }
     s->dump_flags = (o.dump_cfg ? DUMP_CFG : 0u) | (o.dump_regions ? DUMP_REGIONS : 0u) |
                     (o.record_reduction ? DUMP_MERGES : 0u) | (o.export_body ? DUMP_BODY : 0u);
+    s->sem_on = o.semantic_check != 0;
+    s->sem_seed = o.semantic_seed;
     sh.rc = run_host_listing(s, sh.p, sh.len, o.fold_local_size, o.only_kernel, &sh.hr, nullptr, 0);
     s->dump_flags = 0;
+    s->sem_on = false;
     sh.lines = s->stats.lines;
     if (sh.rc)
         sh.err = g_err;
@@ -2199,6 +2227,8 @@ int decompile_shards(std::vector<Shard> &sh, const ocldec_b200_options &o, oclde
     for (Shard &x : sh)
         nk_all += err_line ? 0 : x.s->host_res.size();
     res->kernels = static_cast<ocldec_b200_kernel *>(calloc(nk_all + 1, sizeof(ocldec_b200_kernel)));
+    if (o.semantic_check)
+        res->sem = static_cast<ocldec_b200_semcheck *>(calloc(nk_all + 1, sizeof(ocldec_b200_semcheck)));
     std::string nm;
     u64 nkept = 0;
     std::vector<ocldec_b200_dump> dv;
@@ -2237,6 +2267,8 @@ int decompile_shards(std::vector<Shard> &sh, const ocldec_b200_options &o, oclde
                 K.fallback_count = (int32_t)r.fallbacks;
                 K.instructions = r.ninstr;
                 res->instructions += r.ninstr;
+                if (res->sem && k < s->host_sem.size())
+                    res->sem[nkept] = s->host_sem[k];
                 // DecompiledKernel::cfg_dot and ReduceResult::dumps
                 if (k < s->host_dumps.size())
                     for (const auto &e : s->host_dumps[k]) {
@@ -2400,6 +2432,7 @@ void ocldec_b200_free(ocldec_b200_result *res) {
     free(res->combined);
     free(res->dumps);
     free(res->dump_text);
+    free(res->sem);
     free(res->diags); // abi_diags points into the same array
     free(res->diag_text);
     free(res);

@@ -2,6 +2,7 @@
 // -Xptxas -O1: these launches are bound by instruction fetch, and ptxas -O1
 // emits smaller code for them (measured: lower -5 %, emit -12 %).
 #include "od_device.cuh"
+#include "od_oracle.cuh"
 
 namespace od {
 
@@ -76,6 +77,62 @@ __global__ void __launch_bounds__(OD_BLOCK) k_export(DecompArgs a) {
         a.res[k].status = KS_STAGE_FULL; // the host grows the dump pool and re-runs the kernel
     if (a.res[k].status == KS_STAGE_FULL)
         atomicAdd(a.retry_cnt, 1u);
+}
+
+// The batched semantic check (od_oracle.cuh): one kernel of the wave per
+// warp, environment `lane` on lanes 0..kSemEnvs-1; wave slots [w0, w0+n).
+__global__ void __launch_bounds__(128) k_semcheck(DecompArgs a, u32 w0, u32 n, u8 *scratch, SemResult *out,
+                                                  u64 seed, u64 kbase) {
+    const u32 wl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (wl >= n)
+        return;
+    const u32 i = w0 + wl;
+    const u32 k = a.order[i];
+    const u32 lanes = kSemEnvs;
+    const u32 m = (1u << lanes) - 1;
+    if (lane >= lanes)
+        return;
+    if (a.res[k].status != KS_OK) {
+        if (lane == 0)
+            out[k] = SemResult{SEM_NOT_RUN, 0, 0, 0};
+        return;
+    }
+    KState S;
+    kstate_load(S, reinterpret_cast<const KState *>(a.arena + (a.boff[i] - a.boff0)));
+    SemCtx c;
+    c.K = &S.K;
+    c.unsupported = false;
+    SemRng r = sem_stream(seed, kbase + k, lane);
+    sem_env(r, lane, S.K.cfg.dims, S.K.cfg.cws, &c.env);
+    sem_args(c, r);
+    u8 *base = scratch + ((u64)wl * lanes + lane) * kSemLaneBytes;
+    SemMem ma{reinterpret_cast<u64 *>(base), reinterpret_cast<u32 *>(base + kSemMemCap * 8), 0, c.env.mem_seed,
+              kSemTraceSeed, 0, false};
+    base += kSemMemCap * 16;
+    SemMem mb{reinterpret_cast<u64 *>(base), reinterpret_cast<u32 *>(base + kSemMemCap * 8), 0, c.env.mem_seed,
+              kSemTraceSeed, 0, false};
+    base += kSemMemCap * 16;
+    u64 *vk = reinterpret_cast<u64 *>(base), *vv = vk + kSemVarCap;
+    for (u32 q = 0; q < kSemVarCap; ++q)
+        vk[q] = 0;
+    base += kSemVarCap * 16;
+    SemMachine mach{c, ma};
+    mach.run();
+    SemEval ev{c, mb, SemVars{vk, vv, false}, reinterpret_cast<u64 *>(base), false, false};
+    ev.run(S.hoist, S.body);
+    const bool bad = mach.bad || ev.bad;
+    const bool full = ma.full || mb.full || ev.full || ev.vars.full;
+    const bool same = ma.hash == mb.hash && ma.count == mb.count;
+    const u32 any_bad = __ballot_sync(m, bad), any_full = __ballot_sync(m, full), any_diff = __ballot_sync(m, !same);
+    u64 ha = sem_env_mix(ma.hash, ma.count, lane), hb = sem_env_mix(mb.hash, mb.count, lane);
+    for (u32 d = lanes / 2; d; d >>= 1) {
+        ha += __shfl_down_sync(m, ha, d);
+        hb += __shfl_down_sync(m, hb, d);
+    }
+    if (lane == 0) {
+        const u32 st = any_bad ? SEM_UNSUPPORTED : any_full ? SEM_CAPACITY : any_diff ? SEM_MISMATCH : SEM_EQUAL;
+        out[k] = SemResult{st, lanes, ha, hb};
+    }
 }
 
 __device__ __noinline__ void emit_one(const DecompArgs &a, const Slot0 &sl, const uint4 **cs, uint4 **cd,

@@ -1,0 +1,56 @@
+"""The batched semantic check on the GPU.
+
+The device restates the reference's differential backend (oracle.cpp:
+interpret_asm on the listing vs evaluate_decompiled on the lowered body) and
+runs it for 8 environments per kernel (od_oracle.cuh, od_semenv.cuh).  The
+reference's own interpret_asm / evaluate_decompiled, fed the same
+environments (oracle/ref_driver.cpp ref_semcheck), must reach the same
+verdict per kernel, with the same write-trace hashes on both sides.  Kernels
+the device could not hold in its fixed per-lane room (status 3) are not
+compared; they must stay rare.
+"""
+import collections
+
+import pytest
+
+import paper_2107_07809_b200 as P
+from oracle import oracle as O
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not O.available(), reason="oracle not built")]
+
+SEED = 0x5E3A171C
+
+
+def _check(listing, max_capacity_frac=0.05):
+    res = P.decompile_listing(listing, P.DecompileOptions(semantic_check=True, semantic_seed=SEED))
+    ref = O.semcheck(listing, SEED)
+    assert len(ref) == len(res.kernels)
+    counts = collections.Counter()
+    for k, (g, r) in enumerate(zip(res.kernels, ref)):
+        gs = g.semantic
+        assert gs is not None
+        counts[gs[0]] += 1
+        if gs[0] == 3:
+            continue
+        assert gs[0] == r[0], (k, g.name, gs, r)
+        if gs[0] in (0, 1):
+            assert (gs[2], gs[3]) == (r[2], r[3]), (k, g.name, gs, r)
+    assert counts[3] <= max_capacity_frac * max(1, len(ref)), counts
+    return counts
+
+
+def test_reference_corpus_semantics():
+    listing = b"".join(x[1] for x in O.corpus())
+    counts = _check(listing)
+    assert counts[0] >= 20  # the harness's comparable kernels trace identically
+
+
+def test_nests_semantics():
+    _check(b"".join(O.make_nest(s) for s in range(1, 201)))
+
+
+@pytest.mark.parametrize("shape,stress,count", [("C1", 0, 50), ("C2", 0, 200), ("C2", 1, 200),
+                                                ("C3", 0, 300), ("C3", 1, 300), ("C4", 0, 300)])
+def test_generated_semantics(shape, stress, count):
+    listing, _, _ = O.generate_corpus(shape, count, seed=4321 + count, stress=bool(stress))
+    _check(listing, max_capacity_frac=0.25)
