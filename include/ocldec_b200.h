@@ -86,7 +86,9 @@ typedef struct ocldec_b200_dump {
 /* One kernel's semantic check: status 0 equal traces in every environment,
  * 1 a mismatch, 2 unsupported (either side left the interpreted subset, as
  * OracleUnsupported), 3 not compared (the device's trace / variable room ran
- * out), 4 not run (failed or skipped kernel); the hashes sum, over the
+ * out), 4 not run (failed or skipped kernel), 5 indeterminate (an operation
+ * met two NaNs with different payloads, whose result IEEE 754 leaves open, so
+ * the traces depend on the host compiler); the hashes sum, over the
  * environments, a mix of each write trace's FNV-1a hash and length
  * (od_semenv.cuh), for the assembly and the decompiled body. */
 typedef struct ocldec_b200_semcheck {

@@ -16,6 +16,7 @@
 // runs on a pthread with a 1 GiB stack.
 
 #include <pthread.h>
+#include <cstdio>
 
 #include <atomic>
 #include <chrono>
@@ -439,6 +440,15 @@ void *semcheck_job(void *p) {
             } catch (const std::exception &) { // OracleUnsupported (or an out-of-range register)
                 unsupported = true;
                 continue;
+            }
+            if (getenv("OCLDEC_SEM_DEBUG")) {
+                fprintf(stderr, "S %zu %u asm n=%zu [", k, n, A.size());
+                for (const TraceEntry &t : A)
+                    fprintf(stderr, " %llx:%x", (unsigned long long)t.addr, t.value);
+                fprintf(stderr, " ] body n=%zu [", B.size());
+                for (const TraceEntry &t : B)
+                    fprintf(stderr, " %llx:%x", (unsigned long long)t.addr, t.value);
+                fprintf(stderr, " ]\n");
             }
             uint64_t h = od::kSemTraceSeed;
             for (const TraceEntry &t : A)

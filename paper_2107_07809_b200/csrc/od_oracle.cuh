@@ -60,6 +60,7 @@ struct SemCtx {
     SemEnv env;
     u64 argv[32];  // per argument index: the value its sanitized name looks up (0 if none)
     bool unsupported;
+    bool nan_choice; // an operation met two different NaN payloads (sem_nan)
 };
 
 OD_INL bool sem_name_matches(const u8 *t, Span raw, Span other) {
@@ -113,6 +114,62 @@ OD_INL u64 sem_slot_value(const SemCtx &c, const AbiEntry *e) {
 }
 
 // ------------------------------------------------------------ interpreter
+// IEEE single arithmetic, round to nearest, never contracted into an FMA
+// (the reference's host build does the multiply and the add separately).
+// NaNs follow the host's SSE rules, not the GPU's canonical 0x7fffffff: a NaN
+// operand propagates quieted, and an invalid operation yields the default NaN
+// 0xffc00000.  When BOTH operands are NaNs with different payloads, IEEE 754
+// leaves the choice open and the reference's result depends on how its
+// compiler ordered the operands: the environment is then marked
+// indeterminate (SEM_INDETERMINATE) instead of guessing.
+OD_INL float sem_nan(SemCtx &c, float a, float b, float r) {
+    u32 ua, ub;
+    memcpy(&ua, &a, 4);
+    memcpy(&ub, &b, 4);
+    const bool na = (ua & 0x7fffffffu) > 0x7f800000u, nb = (ub & 0x7fffffffu) > 0x7f800000u;
+    if (na && nb && (ua | 0x400000u) != (ub | 0x400000u))
+        c.nan_choice = true;
+#ifdef __CUDA_ARCH__
+    if (!isnan(r))
+        return r;
+    if (na)
+        return __uint_as_float(ua | 0x400000u);
+    if (nb)
+        return __uint_as_float(ub | 0x400000u);
+    return __uint_as_float(0xffc00000u);
+#else
+    return r;
+#endif
+}
+OD_INL float sem_fmul(SemCtx &c, float a, float b) {
+#ifdef __CUDA_ARCH__
+    return sem_nan(c, a, b, __fmul_rn(a, b));
+#else
+    return sem_nan(c, a, b, a * b);
+#endif
+}
+OD_INL float sem_fadd(SemCtx &c, float a, float b) {
+#ifdef __CUDA_ARCH__
+    return sem_nan(c, a, b, __fadd_rn(a, b));
+#else
+    return sem_nan(c, a, b, a + b);
+#endif
+}
+OD_INL float sem_fsub(SemCtx &c, float a, float b) {
+#ifdef __CUDA_ARCH__
+    return sem_nan(c, a, b, __fsub_rn(a, b));
+#else
+    return sem_nan(c, a, b, a - b);
+#endif
+}
+OD_INL float sem_fdiv(SemCtx &c, float a, float b) {
+#ifdef __CUDA_ARCH__
+    return sem_nan(c, a, b, __fdiv_rn(a, b));
+#else
+    return sem_nan(c, a, b, a / b);
+#endif
+}
+
 struct SemMachine {
     SemCtx &c;
     SemMem &mem;
@@ -289,29 +346,6 @@ struct SemMachine {
         u32 b;
         memcpy(&b, &f, 4);
         return b;
-    }
-    // IEEE single arithmetic, round to nearest, never contracted into an FMA
-    // (the reference's host build does the multiply and the add separately)
-    static OD_INL float fmul(float a, float b) {
-#ifdef __CUDA_ARCH__
-        return __fmul_rn(a, b);
-#else
-        return a * b;
-#endif
-    }
-    static OD_INL float fadd(float a, float b) {
-#ifdef __CUDA_ARCH__
-        return __fadd_rn(a, b);
-#else
-        return a + b;
-#endif
-    }
-    static OD_INL float fsub(float a, float b) {
-#ifdef __CUDA_ARCH__
-        return __fsub_rn(a, b);
-#else
-        return a - b;
-#endif
     }
     OD_HD bool mul24(const Ins &I) {
         for (u32 k = 0; k < 2; ++k)
@@ -496,7 +530,7 @@ struct SemMachine {
                     return;
                 }
                 const float x = __uint_as_float_h((u32)a), y = __uint_as_float_h((u32)b);
-                write_vdst(op(I, 0), __float_as_uint_h(r == R_ADD ? fadd(x, y) : fsub(x, y)));
+                write_vdst(op(I, 0), __float_as_uint_h(r == R_ADD ? sem_fadd(c, x, y) : sem_fsub(c, x, y)));
                 return;
             }
             const u64 x = r == R_ADD ? a + b : a - b;
@@ -522,7 +556,7 @@ struct SemMachine {
                 const u64 prod = dt_is_signed(t) ? (u64)((i64)(i32)a * (i64)(i32)b) : a * b;
                 write_vdst(op(I, 0), (u32)(prod >> 32));
             } else if (dt_is_float(t)) {
-                write_vdst(op(I, 0), __float_as_uint_h(fmul(__uint_as_float_h((u32)a), __uint_as_float_h((u32)b))));
+                write_vdst(op(I, 0), __float_as_uint_h(sem_fmul(c, __uint_as_float_h((u32)a), __uint_as_float_h((u32)b))));
             } else {
                 write_vdst(op(I, 0), (u32)(a * b));
             }
@@ -533,15 +567,15 @@ struct SemMachine {
                 bad = true;
                 return;
             }
-            float x = fmul(__uint_as_float_h(read32(op(I, 1))), __uint_as_float_h(read32(op(I, 2))));
-            x = fadd(x, __uint_as_float_h(read32(op(I, 0))));
+            float x = sem_fmul(c, __uint_as_float_h(read32(op(I, 1))), __uint_as_float_h(read32(op(I, 2))));
+            x = sem_fadd(c, x, __uint_as_float_h(read32(op(I, 0))));
             write_vdst(op(I, 0), __float_as_uint_h(x));
             return;
         }
         if (r == R_MAD && n >= 4) {
             if (dt_is_float(t)) {
-                float x = fmul(__uint_as_float_h(read32(op(I, 1))), __uint_as_float_h(read32(op(I, 2))));
-                x = fadd(x, __uint_as_float_h(read32(op(I, 3))));
+                float x = sem_fmul(c, __uint_as_float_h(read32(op(I, 1))), __uint_as_float_h(read32(op(I, 2))));
+                x = sem_fadd(c, x, __uint_as_float_h(read32(op(I, 3))));
                 write_vdst(op(I, 0), __float_as_uint_h(x));
             } else {
                 u32 a = read32(op(I, 1)), b = read32(op(I, 2));
@@ -773,15 +807,10 @@ struct SemEval {
         if (dt_is_float(x.type) || (is_cmp(op) && dt_is_float(ta))) {
             const float p = SemMachine::__uint_as_float_h((u32)a), q = SemMachine::__uint_as_float_h((u32)b);
             switch (op) {
-            case O_ADD: return SemMachine::__float_as_uint_h(SemMachine::fadd(p, q));
-            case O_SUB: return SemMachine::__float_as_uint_h(SemMachine::fsub(p, q));
-            case O_MUL: return SemMachine::__float_as_uint_h(SemMachine::fmul(p, q));
-            case O_DIV:
-#ifdef __CUDA_ARCH__
-                return SemMachine::__float_as_uint_h(__fdiv_rn(p, q));
-#else
-                return SemMachine::__float_as_uint_h(p / q);
-#endif
+            case O_ADD: return SemMachine::__float_as_uint_h(sem_fadd(c, p, q));
+            case O_SUB: return SemMachine::__float_as_uint_h(sem_fsub(c, p, q));
+            case O_MUL: return SemMachine::__float_as_uint_h(sem_fmul(c, p, q));
+            case O_DIV: return SemMachine::__float_as_uint_h(sem_fdiv(c, p, q));
             case O_CMPEQ: return p == q;
             case O_CMPNE: return p != q;
             case O_CMPLT: return p < q;

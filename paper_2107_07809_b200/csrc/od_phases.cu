@@ -1,6 +1,7 @@
 // ocldec-b200: k_lower / k_fold / k_emit, one translation unit compiled with
 // -Xptxas -O1: these launches are bound by instruction fetch, and ptxas -O1
 // emits smaller code for them (measured: lower -5 %, emit -12 %).
+#include <cstdio>
 #include "od_device.cuh"
 #include "od_oracle.cuh"
 
@@ -102,6 +103,7 @@ __global__ void __launch_bounds__(128) k_semcheck(DecompArgs a, u32 w0, u32 n, u
     SemCtx c;
     c.K = &S.K;
     c.unsupported = false;
+    c.nan_choice = false;
     SemRng r = sem_stream(seed, kbase + k, lane);
     sem_env(r, lane, S.K.cfg.dims, S.K.cfg.cws, &c.env);
     sem_args(c, r);
@@ -120,17 +122,33 @@ __global__ void __launch_bounds__(128) k_semcheck(DecompArgs a, u32 w0, u32 n, u
     mach.run();
     SemEval ev{c, mb, SemVars{vk, vv, false}, reinterpret_cast<u64 *>(base), false, false};
     ev.run(S.hoist, S.body);
+#ifdef OD_SEM_DEBUG
+    if (kbase + k == OD_SEM_DEBUG) {
+        printf("S %u %u asm bad=%d n=%u [", (u32)(kbase + k), lane, (int)mach.bad, ma.count);
+        for (u32 q = 0; q < ma.n; ++q)
+            printf(" %llx:%x", (unsigned long long)ma.addr[q], ma.val[q]);
+        printf(" ] body bad=%d full=%d n=%u [", (int)ev.bad, (int)ev.full, mb.count);
+        for (u32 q = 0; q < mb.n; ++q)
+            printf(" %llx:%x", (unsigned long long)mb.addr[q], mb.val[q]);
+        printf(" ]\n");
+    }
+#endif
     const bool bad = mach.bad || ev.bad;
     const bool full = ma.full || mb.full || ev.full || ev.vars.full;
     const bool same = ma.hash == mb.hash && ma.count == mb.count;
     const u32 any_bad = __ballot_sync(m, bad), any_full = __ballot_sync(m, full), any_diff = __ballot_sync(m, !same);
+    const u32 any_nan = __ballot_sync(m, c.nan_choice);
     u64 ha = sem_env_mix(ma.hash, ma.count, lane), hb = sem_env_mix(mb.hash, mb.count, lane);
     for (u32 d = lanes / 2; d; d >>= 1) {
         ha += __shfl_down_sync(m, ha, d);
         hb += __shfl_down_sync(m, hb, d);
     }
     if (lane == 0) {
-        const u32 st = any_bad ? SEM_UNSUPPORTED : any_full ? SEM_CAPACITY : any_diff ? SEM_MISMATCH : SEM_EQUAL;
+        const u32 st = any_bad    ? SEM_UNSUPPORTED
+                       : any_full ? SEM_CAPACITY
+                       : any_nan  ? SEM_INDETERMINATE
+                       : any_diff ? SEM_MISMATCH
+                                  : SEM_EQUAL;
         out[k] = SemResult{st, lanes, ha, hb};
     }
 }

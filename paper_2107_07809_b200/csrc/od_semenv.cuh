@@ -125,6 +125,8 @@ enum SemStatus : u32 {
     SEM_UNSUPPORTED = 2, // either side left the interpreted subset (OracleUnsupported)
     SEM_CAPACITY = 3,    // the device's trace or variable room ran out (not compared)
     SEM_NOT_RUN = 4,     // the kernel failed or was skipped
+    SEM_INDETERMINATE = 5, // an operation met two NaNs of different payloads: IEEE 754
+                           // leaves the result's payload open (od_oracle.cuh sem_nan)
 };
 
 struct SemResult {

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../paper_2107_07809_b200/csrc/od_kernel.cuh"
+#include "../paper_2107_07809_b200/csrc/od_oracle.cuh"
 
 using namespace od;
 
@@ -167,6 +168,48 @@ int main(int argc, char **argv) {
                 fprintf(stderr, "F %zu %u %u %.1f\n", k, F.out.ninstr, F.K.nblk,
                         std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
                 t0 = std::chrono::steady_clock::now();
+            }
+            if (getenv("OD_SEMCHECK")) { // the semantic check on the host, per environment traces
+                KState A;
+                kstate_init(A, kin, mem);
+                dk_front(A);
+                if (!A.done) dk_lower(A);
+                if (!A.done) dk_fold(A);
+                if (!A.done) {
+                    const u64 seed = strtoull(getenv("OD_SEMCHECK"), nullptr, 0);
+                    for (u32 lane = 0; lane < kSemEnvs; ++lane) {
+                        SemCtx c;
+                        c.K = &A.K;
+                        c.unsupported = false;
+                        c.nan_choice = false;
+                        SemRng r = sem_stream(seed, k, lane);
+                        sem_env(r, lane, A.K.cfg.dims, A.K.cfg.cws, &c.env);
+                        sem_args(c, r);
+                        std::vector<u8> sc(kSemLaneBytes);
+                        u8 *base = sc.data();
+                        SemMem ma{reinterpret_cast<u64 *>(base), reinterpret_cast<u32 *>(base + kSemMemCap * 8), 0,
+                                  c.env.mem_seed, kSemTraceSeed, 0, false};
+                        base += kSemMemCap * 16;
+                        SemMem mb{reinterpret_cast<u64 *>(base), reinterpret_cast<u32 *>(base + kSemMemCap * 8), 0,
+                                  c.env.mem_seed, kSemTraceSeed, 0, false};
+                        base += kSemMemCap * 16;
+                        u64 *vk = reinterpret_cast<u64 *>(base), *vv = vk + kSemVarCap;
+                        base += kSemVarCap * 16;
+                        SemMachine m{c, ma};
+                        m.run();
+                        SemEval ev{c, mb, SemVars{vk, vv, false}, reinterpret_cast<u64 *>(base), false, false};
+                        ev.run(A.hoist, A.body);
+                        fprintf(stderr, "S %zu %u asm bad=%d nan=%d n=%u [", k, lane, m.bad, (int)c.nan_choice, ma.count);
+                        for (u32 q = 0; q < ma.n; ++q)
+                            fprintf(stderr, " %llx:%x", (unsigned long long)ma.addr[q], ma.val[q]);
+                        fprintf(stderr, " ] body bad=%d full=%d n=%u [", ev.bad, ev.full, mb.count);
+                        for (u32 q = 0; q < mb.n; ++q)
+                            fprintf(stderr, " %llx:%x", (unsigned long long)mb.addr[q], mb.val[q]);
+                        fprintf(stderr, " ]\n");
+                    }
+                }
+                mem = Bump{arena.data(), 0, cap, false};
+                arena.assign(cap, 0);
             }
             ko = decompile_kernel(kin, mem, &src);
             if (getenv("OD_TIME"))
