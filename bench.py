@@ -37,6 +37,9 @@ CHUNK_BYTES = int(os.environ.get("OCLDEC_B200_CHUNK_BYTES", 0) or 0) or (3 << 30
 METRIC = "GCN instructions decompiled/sec (device-timed) at 1/2/4/8 B200 vs host CPU"
 
 
+SEMANTIC_SEED = 0x5E3A171C
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -47,6 +50,8 @@ def parse():
     ap.add_argument("--kernels", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--semantic", action="store_true",
+                    help="also time the decompile step with the batched semantic check (SURVEY §8(f) rank 4)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--stream", action="store_true",
                     help="generate-and-decompile chunk by chunk (default for C5, whose corpus exceeds HBM)")
@@ -492,6 +497,29 @@ def main():
         except Exception as ex:  # pragma: no cover
             e2e = {"value": None, "unit": "instr/s", "error": str(ex)[:200]}
 
+    # ---- optional: the same step with the batched semantic check (8
+    # environments per kernel, the reference's interpret_asm vs
+    # evaluate_decompiled restated on the device), reported beside the line
+    semantic = None
+    if args.semantic:
+        sess.set_semantic(True, SEMANTIC_SEED)
+        step()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms_sem = e0.elapsed_time(e1) / args.steps
+        counts = sess.semantic_counts()
+        sess.set_semantic(False)
+        extra = ms_sem - ms_step
+        semantic = {"ms_per_step_with_check": ms_sem, "ms_per_step_check": extra,
+                    "kernels_per_s_check": nk / (extra / 1000.0) if extra > 0 else None,
+                    "envs_per_kernel": 8, "seed": SEMANTIC_SEED, "counts_last_step": counts}
+
     peak, peak_src = measured_peaks()
     # dominant kernel: the decompile phase launch with the most device time
     # (CUDA events around each launch on the session stream)
@@ -542,6 +570,8 @@ def main():
         "stats": {k: st[k] for k in ("failed", "goto_form", "fallbacks", "retried", "lines")},
         "job_out_bytes": st["placement"].total_bytes if world > 1 else out_b,
     }
+    if semantic:
+        line["semantic"] = semantic
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_seconds, os.cpu_count() or 1)

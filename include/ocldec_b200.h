@@ -203,6 +203,14 @@ int ocldec_b200_session_diagnostics(ocldec_b200_session *s, char *buf, uint64_t 
  * combined_source: no per-kernel device-to-host traffic or host loops. */
 int ocldec_b200_session_set_records(ocldec_b200_session *s, int keep);
 
+/* Whether session runs (session_run / run_host / run_generated) also run the
+ * batched semantic check (options.semantic_check for
+ * the one-shot calls) with this environment seed, and how many kernels of
+ * the last run ended in each ocldec_b200_semcheck status 0..5 (device
+ * counters; no per-kernel transfer). */
+int ocldec_b200_session_set_semantic(ocldec_b200_session *s, int on, uint64_t seed);
+int ocldec_b200_session_semantic_counts(ocldec_b200_session *s, uint64_t counts[6]);
+
 /* cudaMemcpy(dst, src, n, cudaMemcpyDefault): host<->device staging helper
  * for callers without their own CUDA runtime binding. */
 int ocldec_b200_copy(void *dst, const void *src, uint64_t n);

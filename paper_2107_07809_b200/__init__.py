@@ -285,6 +285,21 @@ class Session:
         totals and combined_source come back."""
         self._L.ocldec_b200_session_set_records(self._s, int(keep))
 
+    SEM_STATUS = ("equal", "mismatch", "unsupported", "capacity", "not_run", "indeterminate")
+
+    def set_semantic(self, on: bool, seed: int = 0):
+        """Run the batched semantic check (8 environments per kernel) in
+        every later session run, with this environment seed."""
+        if self._L.ocldec_b200_session_set_semantic(self._s, int(on), int(seed)):
+            raise RuntimeError(f"set_semantic failed: {_lib.last_error()}")
+
+    def semantic_counts(self) -> dict:
+        """Kernels of the last run per semantic-check status (SEM_STATUS)."""
+        c = (ctypes.c_uint64 * 6)()
+        if self._L.ocldec_b200_session_semantic_counts(self._s, c):
+            raise RuntimeError(f"semantic_counts failed: {_lib.last_error()}")
+        return dict(zip(self.SEM_STATUS, (int(x) for x in c)))
+
     def run_generated(self, shape: Union[int, str], count: int, seed: int = 1, k0: int = 0, stress: bool = False,
                       chunk_bytes: int = 0, sample_stride: int = 0, fold_local_size: bool = False):
         """Streams kernels [k0, k0+count) of a generated corpus through the

@@ -80,7 +80,7 @@ EXPORTS = [
     "ocldec_b200_session_kernels", "ocldec_b200_gen_host", "ocldec_b200_gen_device",
     "ocldec_b200_session_run_host", "ocldec_b200_copy", "ocldec_b200_abi_map_check",
     "ocldec_b200_session_names", "ocldec_b200_session_diagnostics", "ocldec_b200_session_run_generated",
-    "ocldec_b200_session_set_records",
+    "ocldec_b200_session_set_records", "ocldec_b200_session_set_semantic", "ocldec_b200_session_semantic_counts",
 ]
 
 _lib = None
@@ -136,6 +136,10 @@ def load():
     L.ocldec_b200_session_run_generated.restype = i32
     L.ocldec_b200_session_set_records.argtypes = [vp, i32]
     L.ocldec_b200_session_set_records.restype = i32
+    L.ocldec_b200_session_set_semantic.argtypes = [vp, i32, u64]
+    L.ocldec_b200_session_set_semantic.restype = i32
+    L.ocldec_b200_session_semantic_counts.argtypes = [vp, ctypes.POINTER(u64)]
+    L.ocldec_b200_session_semantic_counts.restype = i32
     _lib = L
     return L
 

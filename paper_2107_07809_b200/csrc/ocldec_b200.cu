@@ -935,7 +935,11 @@ struct ocldec_b200_session {
     bool wide_lower = false;         // OCLDEC_B200_WIDE_LOWER: k_lower_wide for long-kernel chunks
     bool sem_on = false;             // the batched semantic check of the current call
     u64 sem_seed = 0;
+    bool sem_session = false;        // session_set_semantic: every session run checks
+    u64 sem_session_seed = 0;
     DevBuf semres, semscratch;       // per chunk kernel: SemResult; the check's lane scratch
+    DevBuf semcnt;                   // kernels per SemStatus since the run began (u64[8])
+    bool sem_counted = false;        // the last run ran the check (semcnt is its count)
     std::vector<ocldec_b200_semcheck> host_sem; // per host_res kernel
     u32 novr = 0;
     std::vector<u64> host_kdiag;     // per kernel: first host_diag index (count in host_res[k].ndiag)
@@ -1173,7 +1177,7 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     a.prof = s->prof_on ? P<u64>(s->prof) : nullptr;
     a.retry_cnt = cnt + 12;
     if (s->sem_on && (ensure(s->semres, (u64)nk * sizeof(SemResult) + 16) ||
-                      ensure(s->semscratch, (u64)kSemBatch * kSemEnvs * kSemLaneBytes)))
+                      ensure(s->semscratch, 2ull * kSemBatch * kSemEnvs * kSemLaneBytes) || !s->semcnt.p))
         return -3;
     // OCLDEC_B200_WIDE_LOWER=1: in chunks of long kernels (C5: ~340 KB of
     // listing, hundreds of if-joins each) kernels with >= kWideJoins joins are
@@ -1292,14 +1296,16 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
                 k_export<<<grid(a.lanes_per), OD_BLOCK, 0, ws>>>(a);
                 s->stats.total_launches++;
             }
-            if (s->sem_on) { // the batched semantic check, kSemBatch kernels per launch
-                for (u32 b0 = 0; b0 < a.count; b0 += kSemBatch) {
-                    const u32 nb = std::min<u32>(kSemBatch, a.count - b0);
-                    k_semcheck<<<(nb * 32 + 127) / 128, 128, 0, ws>>>(a, b0, nb, P<u8>(s->semscratch),
-                                                                       P<SemResult>(s->semres), s->sem_seed,
-                                                                       s->stats.kernels);
-                    s->stats.total_launches++;
-                }
+            if (s->sem_on) { // the batched semantic check: one persistent launch per wave
+                // each wave stream has its own slot counter and scratch half
+                u32 *next = reinterpret_cast<u32 *>(P<u64>(s->semcnt) + (second ? 6 : 7));
+                CK(cudaMemsetAsync(next, 0, sizeof(u32), ws));
+                const u32 warps = std::min<u32>(kSemBatch, a.count);
+                u8 *scr = P<u8>(s->semscratch) + (second ? (u64)kSemBatch * kSemEnvs * kSemLaneBytes : 0);
+                k_semcheck<<<(warps * 32 + 127) / 128, 128, 0, ws>>>(a, a.count, next, scr,
+                                                                     P<SemResult>(s->semres), s->sem_seed,
+                                                                     s->stats.kernels, P<u64>(s->semcnt));
+                s->stats.total_launches++;
             }
             CK(cudaEventRecord(pe[4], ws));
             s->stats.decompile_launches += 4;
@@ -1682,6 +1688,9 @@ void reset_stats(ocldec_b200_session *s) {
     s->host_kdiag.clear();
     s->host_dumps.clear();
     s->host_sem.clear();
+    s->sem_counted = s->sem_on;
+    if (s->sem_on && !ensure(s->semcnt, 8 * sizeof(u64)))
+        cudaMemsetAsync(s->semcnt.p, 0, 8 * sizeof(u64), s->stream);
     s->out_len = 0;
 }
 
@@ -1945,7 +1954,7 @@ void ocldec_b200_session_destroy(ocldec_b200_session *s) {
                       &s->outoff, &s->out, &s->only, &s->retry, &s->gen_len, &s->gen_ninstr,
                       &s->gen_buf, &s->gen_off, &s->kmeta, &s->order, &s->budget, &s->sbudget,
                       &s->boff, &s->hist, &s->prof, &s->ksizes, &s->dpool, &s->dtop, &s->perm, &s->cnt4,
-                      &s->dovr, &s->dovr_text, &s->xtext, &s->xrec, &s->xtop, &s->xcfg, &s->sgen, &s->rstat, &s->semres, &s->semscratch};
+                      &s->dovr, &s->dovr_text, &s->xtext, &s->xrec, &s->xtop, &s->xcfg, &s->sgen, &s->rstat, &s->semres, &s->semscratch, &s->semcnt};
     for (DevBuf *b : bufs)
         if (b->p)
             cudaFree(b->p);
@@ -2017,6 +2026,28 @@ int ocldec_b200_session_set_records(ocldec_b200_session *s, int keep) {
     if (!s)
         return -1;
     s->keep_records = keep != 0;
+    return 0;
+}
+
+int ocldec_b200_session_set_semantic(ocldec_b200_session *s, int on, uint64_t seed) {
+    if (!s)
+        return -1;
+    s->sem_session = s->sem_on = on != 0;
+    s->sem_session_seed = s->sem_seed = seed;
+    return 0;
+}
+
+int ocldec_b200_session_semantic_counts(ocldec_b200_session *s, uint64_t counts[6]) {
+    if (!s || !counts)
+        return -1;
+    u64 c[8] = {};
+    if (s->sem_counted && s->semcnt.p) {
+        CK(cudaSetDevice(s->device));
+        CK(cudaMemcpyAsync(c, s->semcnt.p, sizeof c, cudaMemcpyDeviceToHost, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+    }
+    for (int i = 0; i < 6; ++i)
+        counts[i] = c[i];
     return 0;
 }
 
@@ -2140,7 +2171,8 @@ void run_shard(Shard &sh, const ocldec_b200_options &o) {
     s->sem_seed = o.semantic_seed;
     sh.rc = run_host_listing(s, sh.p, sh.len, o.fold_local_size, o.only_kernel, &sh.hr, nullptr, 0);
     s->dump_flags = 0;
-    s->sem_on = false;
+    s->sem_on = s->sem_session;
+    s->sem_seed = s->sem_session_seed;
     sh.lines = s->stats.lines;
     if (sh.rc)
         sh.err = g_err;

@@ -149,8 +149,8 @@ __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_FOLD * 128 / OD_BLOCK) k_fol
 __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_EMIT * 128 / OD_BLOCK) k_emit(DecompArgs a);
 __global__ void __launch_bounds__(OD_BLOCK) k_export(DecompArgs a);
 struct SemResult;
-__global__ void __launch_bounds__(128) k_semcheck(DecompArgs a, u32 w0, u32 n, u8 *scratch, SemResult *out,
-                                                  u64 seed, u64 kbase);
+__global__ void __launch_bounds__(128) k_semcheck(DecompArgs a, u32 n, u32 *next, u8 *scratch, SemResult *out,
+                                                  u64 seed, u64 kbase, u64 *counts);
 
 // ------------------------------------------------------------------ generator
 struct GenArgs {

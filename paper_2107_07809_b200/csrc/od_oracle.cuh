@@ -17,29 +17,60 @@
 namespace od {
 
 constexpr u64 kSemSettingsBase = 0xf000000000000000ull; // oracle.cpp:17-20
-constexpr u32 kSemMemCap = 256;    // stores per side and environment
+constexpr u32 kSemMemCap = 256;    // stores per side and environment (the trace log)
+constexpr u32 kSemMemSlots = 512;  // the overlay's open-addressing table (power of two, load <= 1/2)
 constexpr u32 kSemVarCap = 512;    // variable slots (open addressing, power of two)
 constexpr u32 kSemStackCap = 512;  // evaluation stack entries
-constexpr u64 kSemLaneBytes = 2ull * kSemMemCap * 16 + kSemVarCap * 16 + kSemStackCap * 16;
+constexpr u64 kSemMemBytes = kSemMemCap * 12ull + kSemMemSlots * 12ull;
+constexpr u64 kSemLaneBytes = 2 * kSemMemBytes + kSemVarCap * 16 + kSemStackCap * 16;
 constexpr u32 kSemEnvs = 8;        // environments (lanes) per kernel
 constexpr long kSemFuel = 1 << 20; // interpreter steps (oracle.cpp:121)
-constexpr u32 kSemBatch = 4096;    // kernels per k_semcheck launch (scratch: kSemBatch x kSemEnvs lanes)
+constexpr u32 kSemBatch = 2048;    // warps of a k_semcheck launch (scratch per wave stream: kSemBatch x kSemEnvs lanes)
 
 // Memory  oracle.cpp:41-56: a pristine hash overlaid by this run's writes;
-// the writes in order are the trace.
+// the writes in order are the trace.  The overlay is an open-addressing
+// table (one or two probes per access; key 0 = empty, address 0 kept aside),
+// the ordered log only feeds the debug dumps (OD_SEM_DEBUG, tools/devhost).
 struct SemMem {
-    u64 *addr;
+    u64 *addr; // log, kSemMemCap
     u32 *val;
+    u64 *tkey; // overlay, kSemMemSlots
+    u32 *tval;
     u32 n;
     u64 seed;
     u64 hash;
-    u32 count; // trace length (every store, also past the overlay's room)
+    u32 count; // trace length (every store, also past the log's room)
     bool full;
+    bool zset; // address 0 written
+    u32 zval;
+    // Carves this memory's arrays from base (advancing it) and clears it.
+    OD_INL void init(u8 *&base, u64 mem_seed) {
+        addr = reinterpret_cast<u64 *>(base);
+        tkey = addr + kSemMemCap;
+        val = reinterpret_cast<u32 *>(tkey + kSemMemSlots);
+        tval = val + kSemMemCap;
+        base += kSemMemBytes;
+        for (u32 i = 0; i < kSemMemSlots; ++i)
+            tkey[i] = 0;
+        n = 0;
+        seed = mem_seed;
+        hash = kSemTraceSeed;
+        count = 0;
+        full = false;
+        zset = false;
+        zval = 0;
+    }
+    static OD_INL u32 slot(u64 a) { return (u32)((a * 0x9e3779b97f4a7c15ull) >> 55) & (kSemMemSlots - 1); }
     OD_INL u32 load(u64 a) const {
-        for (u32 i = n; i-- > 0;)
-            if (addr[i] == a)
-                return val[i];
-        return sem_initial_memory(seed, a);
+        if (!a)
+            return zset ? zval : sem_initial_memory(seed, a);
+        for (u32 i = slot(a);; i = (i + 1) & (kSemMemSlots - 1)) {
+            const u64 k = tkey[i];
+            if (k == a)
+                return tval[i];
+            if (!k)
+                return sem_initial_memory(seed, a);
+        }
     }
     OD_INL void store(u64 a, u32 v) {
         hash = sem_trace_step(hash, a, v);
@@ -51,6 +82,19 @@ struct SemMem {
         addr[n] = a;
         val[n] = v;
         ++n;
+        if (!a) {
+            zset = true;
+            zval = v;
+            return;
+        }
+        for (u32 i = slot(a);; i = (i + 1) & (kSemMemSlots - 1)) {
+            const u64 k = tkey[i];
+            if (k == a || !k) { // at most kSemMemCap distinct addresses: always a free slot
+                tkey[i] = a;
+                tval[i] = v;
+                return;
+            }
+        }
     }
 };
 
@@ -178,8 +222,13 @@ struct SemMachine {
     u64 exec, vcc;
     u32 scc, m0;
     bool bad; // OracleUnsupported
+    long steps; // instructions executed (fuel used)
+    u32 wm;     // device: the lanes (environments) of this kernel's warp, stepped in pc order
+    u32 tc_key[16], tc_val[16]; // branch targets already resolved (pc + 1 -> instruction)
 
-    OD_INL const Opnd &op(const Ins &I, u32 k) const { return c.K->in->ops[I.op_start + k]; }
+    const Opnd *opsp; // c.K->in->ops, held by run() (one load instead of a pointer chain per operand)
+    const Ins *insp;  // c.K->ins
+    OD_INL const Opnd &op(const Ins &I, u32 k) const { return opsp[I.op_start + k]; }
     OD_INL u32 nops(const Ins &I) const { return (I.flags & IF_SYNTH) ? 0 : I.nops; }
     OD_INL bool lane_on() const { return (exec & 1) != 0; }
     OD_INL u32 sget(u32 i) {
@@ -358,6 +407,9 @@ struct SemMachine {
     }
     // target  oracle.cpp:233-240: the instruction the label sits on
     OD_HD u32 target(const Ins &I) {
+        const u32 pc = (u32)(&I - insp), h = pc & 15;
+        if (tc_key[h] == pc + 1) // loops branch to the same labels over and over
+            return tc_val[h];
         if (nops(I) == 0 || op(I, 0).kind != OK_SYMBOL) {
             bad = true;
             return 0;
@@ -368,7 +420,9 @@ struct SemMachine {
             bad = true;
             return 0;
         }
-        return c.K->blk[b].ib;
+        tc_key[h] = pc + 1;
+        tc_val[h] = c.K->blk[b].ib;
+        return tc_val[h];
     }
 
     // scalar  oracle.cpp:268-411; returns false on s_endpgm
@@ -666,29 +720,53 @@ struct SemMachine {
             v[d] = c.env.local_id[d];
             s[6 + d] = c.env.group_id[d];
         }
+        for (u32 i = 0; i < 16; ++i)
+            tc_key[i] = 0;
+        opsp = K.in->ops;
+        insp = K.ins;
         u32 pc = 0;
-        long fuel = kSemFuel;
-        while (pc < K.nins && !bad) {
-            if (--fuel < 0) {
+        steps = 0;
+        bool stop = false;
+        for (;;) {
+            stop = stop || pc >= K.nins || bad;
+#ifdef __CUDA_ARCH__
+            // The warp's lanes run the same instructions on different data;
+            // stepping only the lanes at the lowest pc keeps them at one
+            // instruction (one dispatch path) instead of serializing lanes
+            // that drifted apart.  Each lane still executes exactly its own
+            // instruction sequence.
+            const u32 key = stop ? ~0u : pc;
+            const u32 lo = __reduce_min_sync(wm, key);
+            if (lo == ~0u)
+                break;
+            if (key != lo)
+                continue;
+#else
+            if (stop)
+                break;
+#endif
+            if (++steps > kSemFuel) {
                 bad = true;
-                return;
+                continue;
             }
-            const Ins &I = K.ins[pc];
+            const Ins &I = insp[pc];
             if (I.flags & IF_PARSE_FAILED) {
                 bad = true;
-                return;
+                continue;
             }
             u32 next = pc + 1;
             if (I.prefix == PX_S) {
-                if (!scalar(I, next))
-                    return;
+                if (!scalar(I, next)) {
+                    stop = true;
+                    continue;
+                }
             } else if (I.prefix == PX_V) {
                 vector(I);
             } else if (I.prefix == PX_FLAT) {
                 flat(I);
             } else {
                 bad = true;
-                return;
+                continue;
             }
             pc = next;
         }

@@ -80,22 +80,18 @@ __global__ void __launch_bounds__(OD_BLOCK) k_export(DecompArgs a) {
         atomicAdd(a.retry_cnt, 1u);
 }
 
-// The batched semantic check (od_oracle.cuh): one kernel of the wave per
-// warp, environment `lane` on lanes 0..kSemEnvs-1; wave slots [w0, w0+n).
-__global__ void __launch_bounds__(128) k_semcheck(DecompArgs a, u32 w0, u32 n, u8 *scratch, SemResult *out,
-                                                  u64 seed, u64 kbase) {
-    const u32 wl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (wl >= n)
-        return;
-    const u32 i = w0 + wl;
+// The batched semantic check (od_oracle.cuh) of wave slot i: environment
+// `lane` on lanes 0..kSemEnvs-1 of the calling warp, in the warp's scratch.
+__device__ __noinline__ void sem_one(const DecompArgs &a, u32 i, u32 lane, u8 *wscratch, SemResult *out, u64 seed,
+                                     u64 kbase, u64 *counts) {
     const u32 k = a.order[i];
     const u32 lanes = kSemEnvs;
     const u32 m = (1u << lanes) - 1;
-    if (lane >= lanes)
-        return;
     if (a.res[k].status != KS_OK) {
-        if (lane == 0)
+        if (lane == 0) {
             out[k] = SemResult{SEM_NOT_RUN, 0, 0, 0};
+            atomicAdd(reinterpret_cast<unsigned long long *>(counts + SEM_NOT_RUN), 1ull);
+        }
         return;
     }
     KState S;
@@ -107,18 +103,16 @@ __global__ void __launch_bounds__(128) k_semcheck(DecompArgs a, u32 w0, u32 n, u
     SemRng r = sem_stream(seed, kbase + k, lane);
     sem_env(r, lane, S.K.cfg.dims, S.K.cfg.cws, &c.env);
     sem_args(c, r);
-    u8 *base = scratch + ((u64)wl * lanes + lane) * kSemLaneBytes;
-    SemMem ma{reinterpret_cast<u64 *>(base), reinterpret_cast<u32 *>(base + kSemMemCap * 8), 0, c.env.mem_seed,
-              kSemTraceSeed, 0, false};
-    base += kSemMemCap * 16;
-    SemMem mb{reinterpret_cast<u64 *>(base), reinterpret_cast<u32 *>(base + kSemMemCap * 8), 0, c.env.mem_seed,
-              kSemTraceSeed, 0, false};
-    base += kSemMemCap * 16;
+    u8 *base = wscratch + (u64)lane * kSemLaneBytes;
+    SemMem ma, mb;
+    ma.init(base, c.env.mem_seed);
+    mb.init(base, c.env.mem_seed);
     u64 *vk = reinterpret_cast<u64 *>(base), *vv = vk + kSemVarCap;
     for (u32 q = 0; q < kSemVarCap; ++q)
         vk[q] = 0;
     base += kSemVarCap * 16;
     SemMachine mach{c, ma};
+    mach.wm = m;
     mach.run();
     SemEval ev{c, mb, SemVars{vk, vv, false}, reinterpret_cast<u64 *>(base), false, false};
     ev.run(S.hoist, S.body);
@@ -150,6 +144,28 @@ __global__ void __launch_bounds__(128) k_semcheck(DecompArgs a, u32 w0, u32 n, u
                        : any_diff ? SEM_MISMATCH
                                   : SEM_EQUAL;
         out[k] = SemResult{st, lanes, ha, hb};
+        atomicAdd(reinterpret_cast<unsigned long long *>(counts + st), 1ull);
+    }
+}
+
+// Persistent over the wave: each warp takes the next unchecked slot from
+// the wave's counter, so a kernel that runs its environments to the fuel
+// limit (2^20 interpreted steps) overlaps the rest of the wave instead of
+// holding a whole batch launch.  Warps <= kSemBatch (the scratch's slots).
+__global__ void __launch_bounds__(128) k_semcheck(DecompArgs a, u32 n, u32 *next, u8 *scratch, SemResult *out,
+                                                  u64 seed, u64 kbase, u64 *counts) {
+    const u32 wl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (lane >= kSemEnvs)
+        return;
+    u8 *ws = scratch + (u64)wl * kSemEnvs * kSemLaneBytes;
+    for (;;) {
+        u32 i = 0;
+        if (lane == 0)
+            i = atomicAdd(next, 1u);
+        i = __shfl_sync((1u << kSemEnvs) - 1, i, 0);
+        if (i >= n)
+            return;
+        sem_one(a, i, lane, ws, out, seed, kbase, counts);
     }
 }
 

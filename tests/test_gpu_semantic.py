@@ -54,3 +54,31 @@ def test_nests_semantics():
 def test_generated_semantics(shape, stress, count):
     listing, _, _ = O.generate_corpus(shape, count, seed=4321 + count, stress=bool(stress))
     _check(listing, max_capacity_frac=0.25)
+
+
+def test_session_semantic_counts():
+    """Session runs with the check on (ocldec_b200_session_set_semantic, the
+    bench's --semantic leg): the device counters hold the same per-status
+    kernel counts as the one-shot call's per-kernel verdicts, over chunks,
+    and the combined output is unchanged by the check."""
+    listing, offs, _ = O.generate_corpus("C3", 600, seed=4321 + 600, stress=True)
+    res = P.decompile_listing(listing, P.DecompileOptions(semantic_check=True, semantic_seed=SEED))
+    want = collections.Counter(k.semantic[0] for k in res.kernels)
+    s = P.Session(0)
+    try:
+        d_buf, n, d_offs, _ = s.generate("C3", 600, seed=4321 + 600, stress=True)
+        s.set_records(False)
+        s.run(d_buf, n, [int(offs[k]) for k in (0, 150, 400)])
+        plain = s.output_bytes()
+        s.set_semantic(True, SEED)
+        s.run(d_buf, n, [int(offs[k]) for k in (0, 150, 400)])
+        got = s.semantic_counts()
+        assert s.output_bytes() == plain == res.combined
+        assert sum(got.values()) == 600
+        for i, name in enumerate(P.Session.SEM_STATUS):
+            assert got[name] == want.get(i, 0), (name, got, want)
+        s.set_semantic(False)
+        s.run(d_buf, n, [0])
+        assert sum(s.semantic_counts().values()) == 0  # a run without the check counts nothing
+    finally:
+        s.close()

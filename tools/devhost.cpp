@@ -187,19 +187,16 @@ int main(int argc, char **argv) {
                         sem_args(c, r);
                         std::vector<u8> sc(kSemLaneBytes);
                         u8 *base = sc.data();
-                        SemMem ma{reinterpret_cast<u64 *>(base), reinterpret_cast<u32 *>(base + kSemMemCap * 8), 0,
-                                  c.env.mem_seed, kSemTraceSeed, 0, false};
-                        base += kSemMemCap * 16;
-                        SemMem mb{reinterpret_cast<u64 *>(base), reinterpret_cast<u32 *>(base + kSemMemCap * 8), 0,
-                                  c.env.mem_seed, kSemTraceSeed, 0, false};
-                        base += kSemMemCap * 16;
+                        SemMem ma, mb;
+                        ma.init(base, c.env.mem_seed);
+                        mb.init(base, c.env.mem_seed);
                         u64 *vk = reinterpret_cast<u64 *>(base), *vv = vk + kSemVarCap;
                         base += kSemVarCap * 16;
                         SemMachine m{c, ma};
                         m.run();
                         SemEval ev{c, mb, SemVars{vk, vv, false}, reinterpret_cast<u64 *>(base), false, false};
                         ev.run(A.hoist, A.body);
-                        fprintf(stderr, "S %zu %u asm bad=%d nan=%d n=%u [", k, lane, m.bad, (int)c.nan_choice, ma.count);
+                        fprintf(stderr, "S %zu %u asm bad=%d nan=%d steps=%ld n=%u [", k, lane, m.bad, (int)c.nan_choice, m.steps, ma.count);
                         for (u32 q = 0; q < ma.n; ++q)
                             fprintf(stderr, " %llx:%x", (unsigned long long)ma.addr[q], ma.val[q]);
                         fprintf(stderr, " ] body bad=%d full=%d n=%u [", ev.bad, ev.full, mb.count);

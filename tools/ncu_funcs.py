@@ -9,7 +9,7 @@ from collections import defaultdict
 
 CSRC = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2107_07809_b200", "csrc")
 starts = {}
-pat = re.compile(r"^\s*(?:OD_NOINL|OD_INL|__global__|__device__)[^(]*?\b(\w+)\s*\(")
+pat = re.compile(r"^\s*(?:OD_NOINL|OD_INL|OD_HD|__global__|__device__)[^(]*?\b(\w+)\s*\(")
 REV = os.environ.get("REV")  # read the sources at this git revision (the profiled build)
 
 
