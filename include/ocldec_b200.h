@@ -45,7 +45,9 @@ typedef struct ocldec_b200_options {
                                 then "root <id>" or "residue <ids...>"; structurizer.hpp:54-104) */
     int export_body;         /* DecompiledKernel::body (LoweredBody, lower.hpp:20-41) as a step -3
                                 dump: expression nodes and the statement tree in the text format
-                                of od_lower.cuh's body_text (ABI v5) */
+                                of od_lower.cuh's body_text (ABI v5); and DecompiledKernel::cfg
+                                (cfg.hpp:60-84, after normalize_if_else) as a step -4 dump, one
+                                line per block (od_kernel.cuh cfg_text) */
     int semantic_check;      /* the batched semantic check (ABI v5): per kernel,
                                 the reference's differential backend (interpret_asm vs
                                 evaluate_decompiled, oracle.cpp) restated on the device, over 8
@@ -73,7 +75,8 @@ typedef struct ocldec_b200_diag {
 } ocldec_b200_diag;
 
 /* One dump of a kernel: step -1 is cfg_dot, step -2 the reduction record,
- * step -3 the lowered body (export_body), step i >= 0 is reduction.dumps[i]
+ * step -3 the lowered body and step -4 the flow graph (export_body), step
+ * i >= 0 is reduction.dumps[i]
  * ("step<i>"); text at
  * dump_text[off, off + len). */
 typedef struct ocldec_b200_dump {

@@ -68,6 +68,7 @@ struct DecompiledKernel {
     std::vector<std::string> region_dumps; // ReduceResult::dumps when dump_regions
     Reduction reduction;                   // when record_reduction
     std::string body_text;                 // the lowered statement tree when export_body (step -3)
+    std::string cfg_text;                  // the normalized flow graph when export_body (step -4)
 };
 
 inline Reduction parse_reduction(const std::string &text) {
@@ -213,6 +214,8 @@ inline DecompileResult decompile_listing(const std::string &listing, const Decom
             k.cfg_dot = std::move(text);
         else if (d.step == -3)
             k.body_text = std::move(text);
+        else if (d.step == -4)
+            k.cfg_text = std::move(text);
         else if (d.step == -2)
             k.reduction = parse_reduction(text);
         else

@@ -17,7 +17,12 @@
 // dumps, and the region tree those describe, owned by `regions`), and
 // DecompileResult::diagnostics in sink order.  config, instructions and abi
 // are the reference front end's own parse of the kernel's section (host,
-// diagnostics discarded: the GPU's are the result's); cfg is not filled.
+// diagnostics discarded: the GPU's are the result's).  cfg is the GPU's flow
+// graph after mask normalization (step -4 export): blocks, instruction
+// ranges, labels, terminators, successors, reachability, absorbed and
+// suppressed marks; preds, exec_ops and the masked terms' source operands
+// are rebuilt from those by the reference's own rebuild_preds /
+// annotate_exec (oracle/cfg_check.cpp checks the result field by field).
 // No CPU fallback for the decompilation: a device or API failure throws
 // std::runtime_error with the library's message.
 #include <cstdlib>
@@ -242,6 +247,71 @@ void read_body(const std::string &text, LoweredBody &body) {
 
 // decompile_section's parse steps (decompiler.cpp:59-67) for the inspection
 // fields: the reference front end on the host, its diagnostics discarded.
+// DecompiledKernel::cfg from the device's step -4 record (od_kernel.cuh
+// cfg_text) over the kernel's instruction list.
+void rebuild_cfg(const std::string &text, DecompiledKernel &k) {
+    std::istringstream in(text);
+    size_t nb = 0;
+    in >> nb;
+    Cfg cfg;
+    cfg.blocks.resize(nb);
+    for (size_t b = 0; b < nb; ++b) {
+        BasicBlock &B = cfg.blocks[b];
+        std::string tag;
+        size_t ib = 0, ie = 0;
+        unsigned kind = 0, cc = 0, taken = 0, not_taken = 0, line = 0, reach = 0, absorbed = 0, nsucc = 0;
+        in >> tag >> ib >> ie >> kind >> cc >> taken >> not_taken >> line >> reach >> absorbed >> nsucc;
+        if (!in || tag != "B" || ib > ie || ie > k.instructions.size())
+            throw std::runtime_error("ocldec-b200: malformed cfg record");
+        B.id = int(b);
+        B.instructions.assign(k.instructions.begin() + long(ib), k.instructions.begin() + long(ie));
+        B.suppressed.assign(ie - ib, false);
+        B.term.kind = TermKind(kind);
+        B.term.cc = CondCode(cc);
+        B.term.taken = int(taken) - 1;
+        B.term.not_taken = int(not_taken) - 1;
+        B.term.line = int(line);
+        B.reachable = reach != 0;
+        B.mask_absorbed = absorbed != 0;
+        for (unsigned q = 0; q < nsucc; ++q) {
+            int sc = 0;
+            in >> sc;
+            B.succs.push_back(sc);
+        }
+        size_t ns = 0;
+        in >> tag >> ns;
+        for (size_t q = 0; q < ns; ++q) {
+            size_t i = 0;
+            in >> i;
+            if (i < B.suppressed.size())
+                B.suppressed[i] = true;
+        }
+        size_t nl = 0;
+        in >> tag >> nl;
+        for (size_t q = 0; q < nl; ++q) {
+            std::string l;
+            in >> l;
+            B.labels.push_back(std::move(l));
+        }
+        if (B.term.kind == TermKind::Conditional && B.term.cc == CondCode::Masked) {
+            // the rewritten header's saved condition: the source operand of
+            // its (now suppressed) s_and_saveexec (structurizer.cpp:599-601)
+            for (size_t i = B.instructions.size(); i-- > 0;) {
+                const Instruction &ins = B.instructions[i];
+                if (B.suppressed[i] && !ins.parse_failed && ins.parts.prefix == "s" &&
+                    ins.parts.root == "and_saveexec" && ins.operands.size() >= 2) {
+                    B.term.mask_source = ins.operands[1];
+                    break;
+                }
+            }
+        }
+    }
+    cfg.entry = 0;
+    cfg.rebuild_preds();
+    annotate_exec(cfg);
+    k.cfg = std::move(cfg);
+}
+
 void front_fields(const KernelSection &section, const DecompileOptions &opts, DecompiledKernel &k) {
     DiagnosticSink scratch;
     try {
@@ -302,6 +372,7 @@ DecompileResult decompile_listing(const std::string &listing, const DecompileOpt
         d.failed = k.failed != 0;
         d.body.fallback_count = k.fallback_count;
     }
+    std::vector<std::string> cfg_text(r->nkernels);
     for (uint64_t i = 0; i < r->ndumps; ++i) {
         const ocldec_b200_dump &d = r->dumps[i];
         std::string text(r->dump_text + d.off, d.len);
@@ -312,6 +383,10 @@ DecompileResult decompile_listing(const std::string &listing, const DecompileOpt
             rebuild_regions(text, k);
         else if (d.step == -3 && !getenv("OCLDEC_B200_DROPIN_NO_BODY")) // (a negative control for tests)
             read_body(text, k.body);
+        else if (d.step == -4)
+            cfg_text[d.kernel] = std::move(text);
+        else if (d.step == -3)
+            ;
         else
             k.reduction.dumps.push_back(std::move(text));
     }
@@ -329,6 +404,9 @@ DecompileResult decompile_listing(const std::string &listing, const DecompileOpt
         if (ki < result.kernels.size())
             front_fields(section, opts, result.kernels[ki++]);
     }
+    for (size_t i = 0; i < result.kernels.size(); ++i)
+        if (!cfg_text[i].empty())
+            rebuild_cfg(cfg_text[i], result.kernels[i]);
     return result;
 }
 

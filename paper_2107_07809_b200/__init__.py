@@ -92,6 +92,7 @@ class DecompiledKernel:
     region_dumps: List[str] = field(default_factory=list)   # reduction.dumps when dump_regions
     reduction: Optional["Reduction"] = None                 # when record_reduction
     body_text: str = ""                                     # when export_body (od_lower.cuh body_text)
+    cfg_text: str = ""                                      # when export_body: the flow graph (od_kernel.cuh cfg_text)
     semantic: Optional[tuple] = None  # when semantic_check: (status, envs, hash_asm, hash_body);
     # status 0 equal, 1 mismatch, 2 unsupported, 3 not compared (device room), 4 not run
 
@@ -177,6 +178,8 @@ def decompile_listing(listing: Union[str, bytes], opts: Optional[DecompileOption
                     k.reduction = Reduction.parse(txt)
                 elif d.step == -3:
                     k.body_text = txt
+                elif d.step == -4:
+                    k.cfg_text = txt
                 else:
                     k.region_dumps.append(txt)
         alld = [r.diags[i] for i in range(r.ndiags)] + [r.abi_diags[i] for i in range(r.nabi_diags)]

@@ -2348,12 +2348,75 @@ OD_NOINL void reduce_text(const KCtx &K, DotSink &o) {
     o.c('\n');
 }
 
+// DecompiledKernel::cfg export (step -4, with DUMP_BODY): the flow graph as
+// normalize_if_else leaves it (decompiler.cpp:69-71), one line per block:
+//   B <ib> <ie> <kind> <cc> <taken> <not_taken> <line> <reachable> <absorbed>
+//     <nsucc> <succ...> S <nsupp> <suppressed index in block...> L <nlab> <label...>
+// Instruction ranges index the kernel's instruction list; kind / cc are
+// TermKind / CondCode (cfg.hpp:20-37).  preds (rebuild_preds), exec_ops
+// (annotate_exec) and the Masked term's source operand follow from these and
+// are rebuilt by the binding (integration/ocldec_b200_dropin.cpp).
+OD_NOINL void cfg_text(const KCtx &K, DotSink &o) {
+    const u8 *t = K.in->t;
+    o.u(K.nblk);
+    o.c('\n');
+    for (u32 b = 0; b < K.nblk; ++b) {
+        const Block &B = K.blk[b];
+        o.s("B ");
+        o.u(B.ib);
+        o.c(' ');
+        o.u(B.ie);
+        o.c(' ');
+        o.u(B.term.kind);
+        o.c(' ');
+        o.u(B.term.cc);
+        o.c(' ');
+        o.u((u64)(i64)(B.term.taken + 1)); // -1 -> 0
+        o.c(' ');
+        o.u((u64)(i64)(B.term.not_taken + 1));
+        o.c(' ');
+        o.u(B.term.line);
+        o.c(' ');
+        o.u(blk_reach(K, b) ? 1 : 0);
+        o.c(' ');
+        o.u(B.absorbed ? 1 : 0);
+        o.c(' ');
+        o.u(B.nsucc);
+        for (u32 q = 0; q < B.nsucc; ++q) {
+            o.c(' ');
+            o.u((u32)B.succ[q]);
+        }
+        u32 ns = 0;
+        for (u32 i = B.ib; i < B.ie; ++i)
+            ns += K.supp[i] ? 1 : 0;
+        o.s(" S ");
+        o.u(ns);
+        for (u32 i = B.ib; i < B.ie; ++i)
+            if (K.supp[i]) {
+                o.c(' ');
+                o.u(i - B.ib);
+            }
+        o.s(" L ");
+        o.u(B.lab_n);
+        for (u32 l = 0; l < B.lab_n; ++l) {
+            const Label &L = klabel(K, B.lab_b + l);
+            o.c(' ');
+            o.m(t + L.off, L.len);
+        }
+        o.c('\n');
+    }
+}
+
 // body export printer (od_lower.cuh, after the renderer's label helper)
 OD_NOINL void body_text(KCtx &K, DotSink &o);
 
 OD_INL void dump_print(KCtx &K, DotSink &o, i32 step) {
     if (step == -3) {
         body_text(K, o);
+        return;
+    }
+    if (step == -4) {
+        cfg_text(K, o);
         return;
     }
     if (step == -1)

@@ -2030,6 +2030,8 @@ OD_NOINL void dk_front(KState &S) {
     OD_PROF(2, tp);
     if (in.dump && (in.dump->flags & DUMP_CFG))
         dump_emit(K, -1);
+    if (in.dump && (in.dump->flags & DUMP_BODY))
+        dump_emit(K, -4);
     OD_CHECK(build_regions(K));
     reduce(K);
     if (K.oom) {

@@ -33,12 +33,10 @@ def test_reference_harness_as_shipped_passes():
 @pytest.mark.skipif(not os.path.exists(B200_BIN), reason="drop-in harness not built (make -C oracle -f dropin.mk)")
 def test_reference_harness_on_the_gpu():
     """The decompile_listing gates (2 builtin slots, 4 the 1000-nest shape
-    sweep through the rebuilt region tree, 6 grammar + fallback counts,
+    sweep through the rebuilt region tree, 5 differential execution of the
+    listing against the GPU's lowered body, 6 grammar + fallback counts,
     7 determinism incl. diagnostics, 8 the golden copy kernel) pass with the
-    GPU behind the reference's front door; 1 and 3 do not call it.  Gate 5
-    (differential execution) reads the instruction list, config, ABI map and
-    lowered body tree, which the GPU path does not produce (SURVEY §8(f)
-    rank 3); its outcome is recorded, not required."""
+    GPU behind the reference's front door; 1 and 3 do not call it."""
     env = dict(os.environ, LD_LIBRARY_PATH=os.path.join(ROOT, "paper_2107_07809_b200"))
     p = subprocess.run([B200_BIN], capture_output=True, text=True, timeout=900, env=env)
     checks = _checks(p.stdout)
@@ -61,3 +59,32 @@ def test_differential_gate_sees_the_gpu_body():
     checks = _checks(p.stdout)
     assert checks.get(5) == "FAIL", p.stdout
     assert p.returncode != 0
+
+
+CFG_BIN = os.path.join(ROOT, "oracle", "_ref", "cfg_check_b200")
+
+
+def _cfg_listings():
+    from oracle import oracle as O
+    yield "corpus", b"".join(x[1] for x in O.corpus())
+    yield "nests", b"".join(O.make_nest(s) for s in range(1, 301))
+    for shape, stress, count in (("C2", 1, 300), ("C3", 0, 300), ("C3", 1, 300), ("C4", 0, 100)):
+        yield f"{shape}-{stress}", O.generate_corpus(shape, count, seed=91 + count, stress=bool(stress))[0]
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(CFG_BIN), reason="drop-in harness not built (make -C oracle -f dropin.mk)")
+def test_cfg_matches_reference(tmp_path):
+    """DecompiledKernel::cfg through the drop-in (the device's step -4 flow
+    graph export) equals the reference's own build_cfg / annotate_exec /
+    normalize_if_else result for every kernel, field by field: blocks,
+    labels, instruction copies, suppressed marks, terminators (masked source
+    operands included), preds, succs, exec ops, reachability, absorption."""
+    env = dict(os.environ, LD_LIBRARY_PATH=os.path.join(ROOT, "paper_2107_07809_b200"))
+    for name, listing in _cfg_listings():
+        f = tmp_path / f"{name}.s"
+        f.write_bytes(listing)
+        p = subprocess.run([CFG_BIN, str(f)], capture_output=True, text=True, timeout=600, env=env)
+        m = re.search(r"cfg_check kernels=(\d+) compared=(\d+) mismatches=(\d+)", p.stdout)
+        assert m and p.returncode == 0, (name, p.stdout[-3000:], p.stderr[-2000:])
+        assert int(m.group(3)) == 0 and int(m.group(2)) >= 0.9 * int(m.group(1)), (name, p.stdout[-3000:])
