@@ -937,6 +937,7 @@ struct ocldec_b200_session {
     u64 sem_seed = 0;
     bool sem_session = false;        // session_set_semantic: every session run checks
     u64 sem_session_seed = 0;
+    u64 sem_kbase = 0;               // listing ordinal of the run's first kernel (a shard's offset)
     DevBuf semres, semscratch;       // per chunk kernel: SemResult; the check's lane scratch
     DevBuf semcnt;                   // kernels per SemStatus since the run began (u64[8])
     bool sem_counted = false;        // the last run ran the check (semcnt is its count)
@@ -1304,7 +1305,8 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
                 u8 *scr = P<u8>(s->semscratch) + (second ? (u64)kSemBatch * kSemEnvs * kSemLaneBytes : 0);
                 k_semcheck<<<(warps * 32 + 127) / 128, 128, 0, ws>>>(a, a.count, next, scr,
                                                                      P<SemResult>(s->semres), s->sem_seed,
-                                                                     s->stats.kernels, P<u64>(s->semcnt));
+                                                                     s->sem_kbase + s->stats.kernels,
+                                                                     P<u64>(s->semcnt));
                 s->stats.total_launches++;
             }
             CK(cudaEventRecord(pe[4], ws));
@@ -1698,6 +1700,29 @@ void reset_stats(ocldec_b200_session *s) {
 // As few chunks of at most `target` bytes as fit, of about equal size (every
 // phase launch ends in a tail); with first > 0 the first chunk is `first`
 // bytes and the rest is balanced.
+// Whether the line at p[ls..] has ".kernel" as its first word (the cut
+// points of host_chunks).
+bool kernel_line(const char *p, size_t len, size_t ls) {
+    size_t j = ls;
+    while (j < len && (p[j] == ' ' || p[j] == '\t'))
+        ++j;
+    return j + 7 <= len && memcmp(p + j, ".kernel", 7) == 0 &&
+           (j + 7 == len || p[j + 7] == ' ' || p[j + 7] == '\t' || p[j + 7] == '\n' || p[j + 7] == '\r');
+}
+
+// ".kernel" lines in p[0, len): a shard's kernel offset.
+u64 count_kernel_lines(const char *p, size_t len) {
+    u64 n = 0;
+    for (size_t ls = 0; ls < len;) {
+        n += kernel_line(p, len, ls) ? 1 : 0;
+        const void *nlp = memchr(p + ls, '\n', len - ls);
+        if (!nlp)
+            break;
+        ls = (size_t)((const char *)nlp - p) + 1;
+    }
+    return n;
+}
+
 std::vector<u64> host_chunks(const char *p, size_t len, size_t target, size_t first) {
     std::vector<u64> starts{0};
     if (!first) {
@@ -1718,11 +1743,7 @@ std::vector<u64> host_chunks(const char *p, size_t len, size_t target, size_t fi
             if (!nlp)
                 break;
             size_t ls = (const char *)nlp - p + 1;
-            size_t j = ls;
-            while (j < len && (p[j] == ' ' || p[j] == '\t'))
-                ++j;
-            if (j + 7 <= len && memcmp(p + j, ".kernel", 7) == 0 &&
-                (j + 7 == len || p[j + 7] == ' ' || p[j + 7] == '\t' || p[j + 7] == '\n' || p[j + 7] == '\r')) {
+            if (kernel_line(p, len, ls)) {
                 starts.push_back(ls);
                 found = true;
                 break;
@@ -2150,6 +2171,7 @@ struct Shard {
     u64 line_base = 0;     // lines before the shard
     u64 out_off = 0;       // where its text goes in combined_source
     bool lead_nl = false;  // a "\n" separator precedes it
+    u64 kbase = 0;         // .kernel sections before the shard (semantic-check environment keys)
 };
 
 void run_shard(Shard &sh, const ocldec_b200_options &o) {
@@ -2169,7 +2191,9 @@ void run_shard(Shard &sh, const ocldec_b200_options &o) {
                     (o.record_reduction ? DUMP_MERGES : 0u) | (o.export_body ? DUMP_BODY : 0u);
     s->sem_on = o.semantic_check != 0;
     s->sem_seed = o.semantic_seed;
+    s->sem_kbase = sh.kbase;
     sh.rc = run_host_listing(s, sh.p, sh.len, o.fold_local_size, o.only_kernel, &sh.hr, nullptr, 0);
+    s->sem_kbase = 0;
     s->dump_flags = 0;
     s->sem_on = s->sem_session;
     s->sem_seed = s->sem_session_seed;
@@ -2206,6 +2230,39 @@ template <class Fn> void for_shards(std::vector<Shard> &sh, Fn fn) {
         th.emplace_back([&, i] { fn(i); });
     for (auto &t : th)
         t.join();
+}
+
+// A shard's step -4 flow-graph record with its terminator lines (field 8 of
+// each "B" line, od_kernel.cuh cfg_text) moved to listing lines.
+std::string shift_cfg_lines(const std::string &t, u64 base) {
+    std::string o;
+    o.reserve(t.size() + 64);
+    size_t i = 0;
+    while (i < t.size()) {
+        size_t e = t.find('\n', i);
+        if (e == std::string::npos)
+            e = t.size();
+        if (t.compare(i, 2, "B ") == 0) {
+            size_t f = i; // start of field 8 (the line)
+            for (int w = 0; w < 7 && f < e; ++w)
+                f = t.find(' ', f) + 1;
+            size_t g = t.find(' ', f);
+            if (f > i && g != std::string::npos && g < e) {
+                const u64 line = strtoull(t.c_str() + f, nullptr, 10);
+                o.append(t, i, f - i);
+                o += std::to_string(line ? line + base : 0);
+                o.append(t, g, e - g);
+            } else {
+                o.append(t, i, e - i);
+            }
+        } else {
+            o.append(t, i, e - i);
+        }
+        if (e < t.size())
+            o += '\n';
+        i = e + 1;
+    }
+    return o;
 }
 
 // decompile_listing over shards: run, place, copy out, and assemble the
@@ -2308,8 +2365,11 @@ int decompile_shards(std::vector<Shard> &sh, const ocldec_b200_options &o, oclde
                         d.kernel = nkept;
                         d.step = e.first;
                         d.off = dtx.size();
-                        d.len = e.second.size();
-                        dtx += e.second;
+                        if (e.first == -4 && x.line_base)
+                            dtx += shift_cfg_lines(e.second, x.line_base);
+                        else
+                            dtx += e.second;
+                        d.len = dtx.size() - d.off;
                         dv.push_back(d);
                     }
                 // DecompileResult::diagnostics in sink order (line 0: override
@@ -2410,6 +2470,8 @@ int ocldec_b200_decompile_multi(const char *listing, size_t len, const ocldec_b2
             return -3;
         sh[i].p = listing + starts[i];
         sh[i].len = (i + 1 < sh.size() ? starts[i + 1] : (u64)len) - starts[i];
+        if (o.semantic_check && i > 0)
+            sh[i].kbase = sh[i - 1].kbase + count_kernel_lines(sh[i - 1].p, sh[i - 1].len);
     }
     return decompile_shards(sh, o, out);
 }

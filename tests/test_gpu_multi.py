@@ -141,3 +141,17 @@ def test_cli_devices_flag(tmp_path):
     p = subprocess.run([cli, str(src), "--devices", "0,0,0"], capture_output=True, timeout=300)
     assert p.returncode in (0, 1), p.stderr
     assert (tmp_path / "k.cl").read_bytes() == O.decompile(listing).combined
+
+
+def test_multi_semantic_check_and_exports():
+    """Sharded runs key each kernel's environments by its ordinal in the whole
+    listing, so the semantic verdicts and trace hashes equal the one-device
+    run's; the body and cfg exports also travel through the shards."""
+    listing, _, _ = P.generate_corpus("C2", 300, seed=77, stress=True)
+    opts = P.DecompileOptions(semantic_check=True, semantic_seed=0x5E3A171C, export_body=True)
+    one = P.decompile_listing(listing, opts)
+    multi = P.decompile_listing(listing, opts, devices=[0, 0, 0])
+    _same(multi, one)
+    assert [k.semantic for k in multi.kernels] == [k.semantic for k in one.kernels]
+    assert [(k.body_text, k.cfg_text) for k in multi.kernels] == [(k.body_text, k.cfg_text) for k in one.kernels]
+    assert sum(1 for k in one.kernels if k.cfg_text) >= 290
