@@ -90,7 +90,9 @@ __device__ __noinline__ void sem_one(const DecompArgs &a, u32 i, u32 lane, u8 *w
     if (a.res[k].status != KS_OK) {
         if (lane == 0) {
             out[k] = SemResult{SEM_NOT_RUN, 0, 0, 0};
-            atomicAdd(reinterpret_cast<unsigned long long *>(counts + SEM_NOT_RUN), 1ull);
+            // arena / pool retries re-run the kernel (and this check): counted then
+            if (a.res[k].status != KS_OOM && a.res[k].status != KS_STAGE_FULL)
+                atomicAdd(reinterpret_cast<unsigned long long *>(counts + SEM_NOT_RUN), 1ull);
         }
         return;
     }

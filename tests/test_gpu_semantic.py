@@ -82,3 +82,16 @@ def test_session_semantic_counts():
         assert sum(s.semantic_counts().values()) == 0  # a run without the check counts nothing
     finally:
         s.close()
+
+
+def test_semantic_with_pool_growth_retries():
+    """Kernels re-run after a pool grows (here the DOT-dump pool, on long C5
+    kernels) are checked again on their re-run: the verdicts equal a run
+    without retries."""
+    listing, _, _ = O.generate_corpus("C5", 3, seed=0x210707809C5)
+    base = P.decompile_listing(listing, P.DecompileOptions(semantic_check=True, semantic_seed=SEED))
+    grown = P.decompile_listing(listing, P.DecompileOptions(semantic_check=True, semantic_seed=SEED,
+                                                            dump_regions=True))
+    assert [k.semantic for k in grown.kernels] == [k.semantic for k in base.kernels]
+    assert all(k.semantic[0] != 4 for k in grown.kernels)
+    assert sum(len(k.region_dumps) for k in grown.kernels) > 0
