@@ -38,6 +38,8 @@ struct DecompileOptions {
     bool dump_regions = false;    // DecompileOptions::dump_regions (decompiler.hpp:34)
     bool record_reduction = false; // fill DecompiledKernel::reduction (merges, root / residue)
     bool export_body = false;     // fill DecompiledKernel::body_text (the lowered statement tree)
+    bool semantic_check = false;  // the batched semantic check (DecompiledKernel::semantic)
+    uint64_t semantic_seed = 0;   // its environment seed
     int device = 0;
     std::vector<int> devices;     // non-empty: shard across these devices (ocldec_b200_decompile_multi)
 };
@@ -69,6 +71,8 @@ struct DecompiledKernel {
     Reduction reduction;                   // when record_reduction
     std::string body_text;                 // the lowered statement tree when export_body (step -3)
     std::string cfg_text;                  // the normalized flow graph when export_body (step -4)
+    ocldec_b200_semcheck semantic{4, 0, 0, 0}; // when semantic_check: status (0 equal, 1 mismatch,
+                                               // 2 unsupported, 3 capacity, 4 not run, 5 indeterminate)
 };
 
 inline Reduction parse_reduction(const std::string &text) {
@@ -185,6 +189,8 @@ inline DecompileResult decompile_listing(const std::string &listing, const Decom
     o.dump_regions = opts.dump_regions ? 1 : 0;
     o.record_reduction = opts.record_reduction ? 1 : 0;
     o.export_body = opts.export_body ? 1 : 0;
+    o.semantic_check = opts.semantic_check ? 1 : 0;
+    o.semantic_seed = opts.semantic_seed;
     ocldec_b200_result *r = nullptr;
     int rc = opts.devices.empty()
                  ? ocldec_b200_decompile(listing.data(), listing.size(), &o, &r)
@@ -203,6 +209,8 @@ inline DecompileResult decompile_listing(const std::string &listing, const Decom
         d.structured = k.structured != 0;
         d.failed = k.failed != 0;
         d.fallback_count = k.fallback_count;
+        if (r->sem)
+            d.semantic = r->sem[i];
         d.instructions = k.instructions;
         res.kernels.push_back(std::move(d));
     }

@@ -17,13 +17,19 @@ with tempfile.TemporaryDirectory() as d:
 per = {}
 cur = None
 for line in dis.splitlines():
+    st = line.strip()
+    if st.startswith(".section") and ".text." not in st:
+        cur = None  # data sections (constant banks, tables) are not code
+        continue
     if line.startswith("$_Z") or line.startswith("_Z"):
         name = line.strip().rstrip(":")
+        parts = name.split("$")
+        entry = parts[1] if name.startswith("$") else parts[0]
         cur = None
         for w in want:
-            if w in name.split("$")[1 if name.startswith("$") else 0]:
-                sub = name.split("$")[-1] if name.startswith("$") else "(entry)"
-                cur = (w, sub)
+            # exact kernel identifier (k_lower must not match k_lower_wide)
+            if re.search(r"\d+" + re.escape(w) + r"E", entry):
+                cur = (w, parts[-1] if name.startswith("$") else "(entry)")
         if cur:
             per.setdefault(cur, 0)
         continue
