@@ -66,6 +66,9 @@ def lib():
         L.ref_semcheck.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_void_p,
                                    ctypes.c_size_t]
         L.ref_semcheck.restype = ctypes.c_int64
+        L.ref_semcheck_at.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_uint64,
+                                      ctypes.c_void_p, ctypes.c_size_t]
+        L.ref_semcheck_at.restype = ctypes.c_int64
         _lib = L
     return _lib
 
@@ -186,15 +189,43 @@ def decompile_par(listing: bytes, kernel_starts, nthreads: int = 0, per: int = 6
     return _parse(blob)
 
 
-def semcheck(listing: bytes, seed: int, cap: int = 1 << 20):
+def semcheck(listing: bytes, seed: int, cap: int = 1 << 20, nthreads: int = 1):
     """The reference's interpret_asm / evaluate_decompiled (oracle.cpp:620-842)
     per kernel over the semantic check's 8 environments (od_semenv.cuh):
-    [(status, envs, hash_asm, hash_body)], statuses as the device check's."""
+    [(status, envs, hash_asm, hash_body)], statuses as the device check's.
+    nthreads > 1 cuts the listing at ".kernel" lines into slices checked on
+    that many threads (each slice keyed by its kernels' ordinals in the whole
+    listing); for listings without a preamble or commented-out sections."""
     import numpy as np
     L = lib()
-    out = np.zeros(4 * cap, dtype=np.uint64)
-    n = L.ref_semcheck(listing, len(listing), seed, out.ctypes.data, cap)
-    return [tuple(int(x) for x in out[4 * k:4 * k + 4]) for k in range(min(n, cap))]
+    if nthreads <= 1:
+        out = np.zeros(4 * cap, dtype=np.uint64)
+        n = L.ref_semcheck(listing, len(listing), seed, out.ctypes.data, cap)
+        return [tuple(int(x) for x in out[4 * k:4 * k + 4]) for k in range(min(n, cap))]
+    starts = [0] if listing.startswith(b".kernel") else []
+    pos = listing.find(b"\n.kernel")
+    while pos >= 0:
+        starts.append(pos + 1)
+        pos = listing.find(b"\n.kernel", pos + 1)
+    if not starts or starts[0] != 0:
+        raise ValueError("semcheck(nthreads > 1) needs a listing that starts with .kernel")
+    per = max(1, (len(starts) + 4 * nthreads - 1) // (4 * nthreads))
+    slices = []
+    for i in range(0, len(starts), per):
+        b = starts[i]
+        e = starts[i + per] if i + per < len(starts) else len(listing)
+        slices.append((i, listing[b:e], min(per, len(starts) - i)))
+
+    def run(sl):
+        kb, text, nk = sl
+        out = np.zeros(4 * nk, dtype=np.uint64)
+        n = L.ref_semcheck_at(text, len(text), seed, kb, out.ctypes.data, nk)
+        return [tuple(int(x) for x in out[4 * k:4 * k + 4]) for k in range(min(n, nk))]
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(nthreads) as ex:
+        parts = list(ex.map(run, slices))
+    return [x for p in parts for x in p][:cap]
 
 
 SHAPES = {"C1": 1, "C2": 2, "C3": 3, "C4": 4, "C5": 5}

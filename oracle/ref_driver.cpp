@@ -396,6 +396,7 @@ struct SemJob {
     uint64_t seed;
     uint64_t *out;
     size_t cap;
+    uint64_t kbase = 0; // listing ordinal of the first kernel (slices of a larger listing)
     size_t nk = 0;
 };
 
@@ -415,7 +416,7 @@ void *semcheck_job(void *p) {
         uint64_t ha = 0, hb = 0;
         const uint32_t envs = 8;
         for (uint32_t n = 0; n < envs; ++n) {
-            od::SemRng r = od::sem_stream(job->seed, k, n);
+            od::SemRng r = od::sem_stream(job->seed, job->kbase + k, n);
             od::SemEnv e;
             const uint32_t cws[3] = {K.config.cws[0], K.config.cws[1], K.config.cws[2]};
             od::sem_env(r, n, uint32_t(K.config.dims), cws, &e);
@@ -470,6 +471,15 @@ void *semcheck_job(void *p) {
 
 int64_t ref_semcheck(const char *listing, size_t len, uint64_t seed, uint64_t *out, size_t cap) {
     SemJob job{listing, len, seed, out, cap};
+    run_on_big_stack(semcheck_job, &job);
+    return int64_t(job.nk);
+}
+
+// The same over a slice of a larger listing whose first kernel is kernel
+// `kbase` of the whole (oracle.py runs slices on several threads).
+int64_t ref_semcheck_at(const char *listing, size_t len, uint64_t seed, uint64_t kbase, uint64_t *out,
+                        size_t cap) {
+    SemJob job{listing, len, seed, out, cap, kbase};
     run_on_big_stack(semcheck_job, &job);
     return int64_t(job.nk);
 }

@@ -95,3 +95,27 @@ def test_semantic_with_pool_growth_retries():
     assert [k.semantic for k in grown.kernels] == [k.semantic for k in base.kernels]
     assert all(k.semantic[0] != 4 for k in grown.kernels)
     assert sum(len(k.region_dumps) for k in grown.kernels) > 0
+
+
+@pytest.mark.parametrize("shape,count,seed", [("C2", 10_000, 0x210707809C2), ("C3", 10_000, 0x210707809C3),
+                                              ("C4", 10_000, 0x210707809C4)])
+def test_named_configs_semantics(shape, count, seed):
+    """The named C2 and C3 corpora in full (10k kernels at the bench seeds) and
+    the first 10k kernels of C4: every device verdict and trace hash equals
+    the reference's (reference side on 16 threads)."""
+    import os
+    listing, _, _ = O.generate_corpus(shape, count, seed=seed)
+    res = P.decompile_listing(listing, P.DecompileOptions(semantic_check=True, semantic_seed=SEED))
+    ref = O.semcheck(listing, SEED, nthreads=min(16, os.cpu_count() or 1))
+    assert len(ref) == len(res.kernels) == count
+    counts = collections.Counter()
+    for k, (g, r) in enumerate(zip(res.kernels, ref)):
+        gs = g.semantic
+        counts[gs[0]] += 1
+        if gs[0] in (3, 5):
+            continue
+        assert gs[0] == r[0], (k, gs, r)
+        if gs[0] in (0, 1):
+            assert (gs[2], gs[3]) == (r[2], r[3]), (k, gs, r)
+    assert counts[3] + counts[5] <= 0.05 * count, counts
+    print(shape, dict(counts))

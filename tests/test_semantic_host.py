@@ -86,3 +86,10 @@ def test_nests(devhost):
 def test_generated(devhost, shape, stress, count):
     listing, _, _ = O.generate_corpus(shape, count, seed=4321 + count, stress=bool(stress))
     _compare(devhost, listing, 4 * count)
+
+
+def test_reference_semcheck_slices_equal_whole():
+    """The threaded reference check (slices keyed by their kernels' listing
+    ordinals) equals the single pass: the named-size GPU tests rely on it."""
+    listing, _, _ = O.generate_corpus("C3", 200, seed=5, stress=True)
+    assert O.semcheck(listing, int(SEED, 16), nthreads=8) == O.semcheck(listing, int(SEED, 16))
