@@ -50,7 +50,8 @@ def test_nests_semantics():
 
 
 @pytest.mark.parametrize("shape,stress,count", [("C1", 0, 50), ("C2", 0, 200), ("C2", 1, 200),
-                                                ("C3", 0, 300), ("C3", 1, 300), ("C4", 0, 300)])
+                                                ("C3", 0, 300), ("C3", 1, 300), ("C4", 0, 300),
+                                                ("C5", 0, 48)])
 def test_generated_semantics(shape, stress, count):
     listing, _, _ = O.generate_corpus(shape, count, seed=4321 + count, stress=bool(stress))
     _check(listing, max_capacity_frac=0.25)
