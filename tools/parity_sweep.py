@@ -17,11 +17,11 @@ rng = random.Random(int(os.environ.get("SWEEP_SEED", "20261017")))
 total = bad = 0
 t0 = time.time()
 for c in range(ncase):
-    shape = rng.choice(["C1", "C2", "C3", "C4"])
+    shape = rng.choice(os.environ.get("SWEEP_SHAPES", "C1,C2,C3,C4").split(","))
     stress = rng.random() < 0.5
     seed = rng.getrandbits(48)
     k0 = rng.getrandbits(20)
-    n = per if shape != "C1" else min(per, 500)
+    n = per if shape not in ("C1", "C5") else min(per, 500 if shape == "C1" else 100)
     listing, offs, _ = O.generate_corpus(shape, n, seed=seed, k0=k0, stress=stress)
     fold = rng.random() < 0.25
     gpu = P.decompile_listing(listing, P.DecompileOptions(fold_local_size=fold))
