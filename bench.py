@@ -282,7 +282,7 @@ def run_stream(args, P, torch, dist, world, rank, local, nk, cdev="cuda"):
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             st, hs, ls = sess.run_generated(cfg, k1 - k0, seed=SEEDS[cfg], k0=k0, sample_stride=stride)
-            for key in acc:
+            for key in ("ms_decompile", "ms_generate", "ms_wall"):
                 acc[key] += st[key]
             ss = sess.stats()
             for key in ("ms_parse", "ms_front", "ms_lower", "ms_fold", "ms_render", "ms_emit"):

@@ -159,3 +159,29 @@ def test_wide_lowering_option_matches_reference():
     p = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
                        timeout=600)
     assert p.returncode == 0 and "ok" in p.stdout, p.stderr[-2000:]
+
+
+def test_c5_chunk_on_two_wave_streams():
+    """A chunk of long C5 kernels large enough (>= 1024 kernels) for the two
+    wave streams the session uses on long-kernel chunks: the combined output,
+    flags and diagnostics equal the reference's, with the streams on (the
+    default for such chunks) and forced off."""
+    import subprocess
+    import sys
+    listing, offs, _ = O.generate_corpus("C5", 1100, seed=SEEDS["C5"], k0=500_000)
+    ref = O.decompile_par(listing, [int(x) for x in offs[:-1]], nthreads=min(16, os.cpu_count() or 1))
+    res = P.decompile_listing(listing)
+    assert res.combined == ref.combined
+    assert [(k.failed, k.structured, k.fallback_count) for k in res.kernels] == \
+           [(k.failed, k.structured, k.fallback_count) for k in ref.kernels]
+    # the same listing with the second stream disabled (a fresh process: the
+    # mode is read when a session is created)
+    code = ("import sys, hashlib; sys.path.insert(0, %r); import paper_2107_07809_b200 as P; "
+            "from oracle import oracle as O; "
+            "l, _, _ = O.generate_corpus('C5', 1100, seed=%d, k0=500000); "
+            "print(hashlib.sha256(P.decompile_listing(l).combined).hexdigest())"
+            % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), SEEDS["C5"]))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=900,
+                         env=dict(os.environ, OCLDEC_B200_TWO_STREAMS="0"))
+    import hashlib
+    assert out.stdout.strip() == hashlib.sha256(ref.combined).hexdigest(), out.stderr[-2000:]
