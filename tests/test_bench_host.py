@@ -68,3 +68,37 @@ def test_gpus_flag_spawns_ranks():
     assert p.returncode == 0, p.stderr[-2000:]
     lines = [json.loads(x) for x in p.stdout.strip().splitlines() if x.startswith("{")]
     assert len(lines) == 1 and lines[0]["impl"] == "reference" and lines[0]["n_gpus"] == 2
+
+
+def test_stream_mode_accumulates_steps(capsys):
+    """run_stream (the C5 streamed bench) over several steps: the per-step
+    totals add up and the line reports them per step (a fake session: the
+    host logic only)."""
+    import types
+
+    class FakeSession:
+        def __init__(self, dev):
+            self.n = 0
+
+        def run_generated(self, cfg, count, seed=1, k0=0, sample_stride=0, **kw):
+            self.n += 1
+            st = {"ms_decompile": 100.0, "ms_generate": 50.0, "ms_wall": 160.0, "instructions": 1000 * count,
+                  "in_bytes": 30000 * count, "out_bytes": 15000 * count, "kernels": count, "chunks": 1,
+                  "failed": 0, "goto_form": 0, "fallbacks": 0}
+            return st, np.zeros(1, dtype=np.uint64), np.zeros(1, dtype=np.uint64)
+
+        def close(self):
+            pass
+
+        def stats(self):
+            return {"ms_parse": 10.0, "ms_front": 20.0, "ms_lower": 40.0, "ms_fold": 5.0, "ms_render": 20.0,
+                    "ms_emit": 1.0}
+
+    fake_p = types.SimpleNamespace(Session=FakeSession)
+    fake_torch = types.SimpleNamespace(cuda=types.SimpleNamespace(synchronize=lambda: None))
+    args = types.SimpleNamespace(config="C5", steps=3, warmup=0, no_e2e=True, no_cpu=True)
+    bench.run_stream(args, fake_p, fake_torch, None, 1, 0, 0, 5000)
+    line = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    assert line["steps"] == 3 and line["ms_per_step"] == 100.0
+    assert line["passes_ms_per_step_rank0"]["k_lower"] == 40.0
+    assert line["value"] == 5000 * 1000 / 0.1
