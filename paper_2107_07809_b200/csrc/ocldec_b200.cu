@@ -939,6 +939,15 @@ struct ocldec_b200_session {
     bool sem_session = false;        // session_set_semantic: every session run checks
     u64 sem_session_seed = 0;
     u64 sem_kbase = 0;               // listing ordinal of the run's first kernel (a shard's offset)
+    long sem_budget = 1 << 14;       // in-wave steps per environment before a kernel is deferred
+                                     // (OCLDEC_B200_SEM_BUDGET; 0: never)
+    const u64 *sem_kmap = nullptr;   // deferred re-check: listing ordinal per kernel (device)
+    DevBuf semkmap, semdef, semspan, semdefbuf;
+    std::string def_text;            // the run's deferred kernels' sections ...
+    std::vector<u64> def_ord;        // ... and their listing ordinals
+    int def_fold = 0;
+    ocldec_b200_session *aux = nullptr; // re-checks the deferred kernels at the run's end
+    std::string ovr_src;             // the ABI override text of the current run (set_overrides)
     DevBuf semres, semscratch;       // per chunk kernel: SemResult; the check's lane scratch
     DevBuf semcnt;                   // kernels per SemStatus since the run began (u64[8])
     bool sem_counted = false;        // the last run ran the check (semcnt is its count)
@@ -1011,6 +1020,10 @@ struct ChunkOut {
 // Runs P1-P4 on one chunk t[0, len) (device).  can_extend: t is the
 // session's text buffer with room for the aux area.  Outputs are appended to
 // s->out at out_base; per-kernel results are appended to s->host_res.
+int collect_deferred(ocldec_b200_session *s, const u8 *t, u64 len, u32 nlf, const DecompArgs &a, u64 kb0,
+                     int fold_local_size);
+int finish_deferred(ocldec_b200_session *s);
+
 int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32 line_base,
               int fold_local_size, u64 out_base, bool prev_nonempty, ChunkOut *co) {
     cudaStream_t st = s->stream;
@@ -1179,8 +1192,12 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     a.prof = s->prof_on ? P<u64>(s->prof) : nullptr;
     a.retry_cnt = cnt + 12;
     if (s->sem_on && (ensure(s->semres, (u64)nk * sizeof(SemResult) + 16) ||
-                      ensure(s->semscratch, 2ull * kSemBatch * kSemEnvs * kSemLaneBytes) || !s->semcnt.p))
+                      ensure(s->semscratch, 2ull * kSemBatch * kSemEnvs * kSemLaneBytes) || !s->semcnt.p ||
+                      ensure(s->semdef, 4ull * (kSemDeferCap + 2))))
         return -3;
+    if (s->sem_on)
+        CK(cudaMemsetAsync(s->semdef.p, 0, 8, st));
+    const u64 sem_kb0 = s->stats.kernels; // kernels of the run before this chunk
     // OCLDEC_B200_WIDE_LOWER=1: in chunks of long kernels (C5: ~340 KB of
     // listing, hundreds of if-joins each) kernels with >= kWideJoins joins are
     // lowered by the whole warp (k_lower_wide, lane-parallel merge_join /
@@ -1307,10 +1324,10 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
                 CK(cudaMemsetAsync(next, 0, sizeof(u32), ws));
                 const u32 warps = std::min<u32>(kSemBatch, a.count);
                 u8 *scr = P<u8>(s->semscratch) + (second ? (u64)kSemBatch * kSemEnvs * kSemLaneBytes : 0);
-                k_semcheck<<<(warps * 32 + 127) / 128, 128, 0, ws>>>(a, a.count, next, scr,
-                                                                     P<SemResult>(s->semres), s->sem_seed,
-                                                                     s->sem_kbase + s->stats.kernels,
-                                                                     P<u64>(s->semcnt));
+                SemArgs sa{a.count, next, scr, P<SemResult>(s->semres), s->sem_seed,
+                           s->sem_kbase + s->stats.kernels, P<u64>(s->semcnt), s->sem_kmap,
+                           s->sem_budget, P<u32>(s->semdef), kSemDeferCap};
+                k_semcheck<<<(warps * 32 + 127) / 128, 128, 0, ws>>>(a, sa);
                 s->stats.total_launches++;
             }
             CK(cudaEventRecord(pe[4], ws));
@@ -1433,6 +1450,8 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
         g_err = "internal error: an operand pool bound was exceeded";
         return -3;
     }
+    if (s->sem_on && s->sem_budget > 0 && collect_deferred(s, t, len, nlf, a, sem_kb0, fold_local_size))
+        return -3;
     u64 tot = 0;
     memcpy(&tot, cblk + 10, 8);
     // tot = sum(len + 1) over non-empty; the last separator is dropped
@@ -1635,6 +1654,9 @@ int session_init(ocldec_b200_session *s, int device, size_t arena_bytes) {
     s->pool_bytes = arena_bytes ? arena_bytes : std::min<size_t>(free_b * 2 / 5, (size_t)64 << 30);
     s->arena_bytes = s->pool_bytes;
     {
+        const char *sb = getenv("OCLDEC_B200_SEM_BUDGET");
+        if (sb && *sb)
+            s->sem_budget = strtol(sb, nullptr, 0);
         const char *wl = getenv("OCLDEC_B200_WIDE_LOWER");
         s->wide_lower = wl && *wl == '1';
     }
@@ -1698,6 +1720,8 @@ void reset_stats(ocldec_b200_session *s) {
     s->host_kdiag.clear();
     s->host_dumps.clear();
     s->host_sem.clear();
+    s->def_text.clear();
+    s->def_ord.clear();
     s->sem_counted = s->sem_on;
     if (s->sem_on && !ensure(s->semcnt, 8 * sizeof(u64)))
         cudaMemsetAsync(s->semcnt.p, 0, 8 * sizeof(u64), s->stream);
@@ -1792,11 +1816,13 @@ size_t chunk_target() {
 // Parses an ABI override file (or clears the overrides) and uploads the
 // resolved list for build_abi.
 int set_overrides(ocldec_b200_session *s, const char *text, size_t len) {
+    s->ovr_src.clear();
     s->ovr_host.clear();
     s->ovr_diags.clear();
     s->novr = 0;
     if (!text)
         return 0;
+    s->ovr_src.assign(text, len);
     s->ovr_host = parse_overrides(std::string(text, len), &s->ovr_diags);
     if (s->ovr_host.empty())
         return 0;
@@ -1846,6 +1872,106 @@ int run_host_listing(ocldec_b200_session *s, const char *listing, size_t len, in
             return rc == -5 ? -1 : rc;
         target /= 2; // chunk + comment-stripped copies past the u32 range
     }
+}
+
+// The semantic check's deferred kernels of one chunk (k_semcheck listed
+// them: still running after sem_budget steps): their sections' bytes join
+// the run's deferred listing, with their listing ordinals.
+int collect_deferred(ocldec_b200_session *s, const u8 *t, u64 len, u32 nlf, const DecompArgs &a, u64 kb0,
+                     int fold_local_size) {
+    cudaStream_t st = s->stream;
+    u32 nd = 0;
+    if (d2h_sync(s, &nd, s->semdef.p, 4))
+        return -3;
+    nd = std::min<u32>(nd, kSemDeferCap);
+    if (!nd)
+        return 0;
+    std::vector<u32> lk(nd + 2);
+    if (d2h_sync(s, lk.data(), s->semdef.p, 4ull * (nd + 2)) || ensure(s->semspan, 24ull * nd + 16))
+        return -3;
+    u64 *span = P<u64>(s->semspan);
+    k_def_spans<<<(nd + 127) / 128, 128, 0, st>>>(P<u32>(s->semdef), nd, P<u32>(s->nlpos), nlf, a.kstart, a.nk, len,
+                                                   span);
+    std::vector<u64> sp(2ull * nd);
+    if (d2h_sync(s, sp.data(), span, 16ull * nd))
+        return -3;
+    std::vector<u64> dst(nd);
+    u64 tot = 0;
+    for (u32 j = 0; j < nd; ++j) {
+        dst[j] = tot;
+        tot += sp[2 * j + 1];
+    }
+    if (ensure(s->semdefbuf, tot + 16))
+        return -3;
+    CK(cudaMemcpyAsync(span + 2ull * nd, dst.data(), 8ull * nd, cudaMemcpyHostToDevice, st));
+    k_def_pack<<<(nd * 32 + 127) / 128, 128, 0, st>>>(t, span, span + 2ull * nd, nd, P<u8>(s->semdefbuf));
+    std::string bytes(tot, '\0');
+    if (d2h_sync(s, bytes.data(), s->semdefbuf.p, tot))
+        return -3;
+    for (u32 j = 0; j < nd; ++j) {
+        s->def_text.append(bytes, dst[j], sp[2 * j + 1]);
+        if (s->def_text.empty() || s->def_text.back() != '\n')
+            s->def_text += '\n';
+        s->def_ord.push_back(s->sem_kbase + kb0 + lk[2 + j]);
+    }
+    s->def_fold = fold_local_size;
+    return 0;
+}
+
+// The run's deferred kernels, re-checked together without a step budget on
+// an auxiliary session (same device, seed, fold and ABI options; each kernel
+// keyed by its ordinal in this run's listing, so its environments are the
+// ones the in-wave check would have used).  The verdicts replace the
+// deferred placeholders: per kernel (host records) and in the status counts.
+int finish_deferred(ocldec_b200_session *s) {
+    if (s->def_ord.empty())
+        return 0;
+    if (!s->aux) {
+        s->aux = ocldec_b200_session_create(s->device, 4ull << 30);
+        if (!s->aux)
+            return -3;
+    }
+    ocldec_b200_session *x = s->aux;
+    const size_t n = s->def_ord.size();
+    if (ensure(x->semkmap, 8ull * n + 8))
+        return -3;
+    CK(cudaMemcpy(x->semkmap.p, s->def_ord.data(), 8ull * n, cudaMemcpyHostToDevice));
+    x->keep_records = true;
+    x->sem_on = true;
+    x->sem_seed = s->sem_seed;
+    x->sem_budget = 0;
+    x->sem_kbase = 0;
+    x->sem_kmap = P<u64>(x->semkmap);
+    int rc = set_overrides(x, s->ovr_src.empty() ? nullptr : s->ovr_src.data(), s->ovr_src.size());
+    HostRun hr;
+    if (!rc)
+        rc = run_host_listing(x, s->def_text.data(), s->def_text.size(), s->def_fold, nullptr, &hr, nullptr, 0);
+    x->sem_kmap = nullptr;
+    x->sem_on = false;
+    if (rc) {
+        g_err = "semantic re-check of deferred kernels: " + g_err;
+        return rc;
+    }
+    if (x->host_sem.size() != n) {
+        g_err = "internal error: deferred semantic re-check lost kernels";
+        return -3;
+    }
+    u64 cnt[8];
+    CK(cudaMemcpyAsync(cnt, s->semcnt.p, sizeof cnt, cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    for (size_t i = 0; i < n; ++i) {
+        const ocldec_b200_semcheck &r = x->host_sem[i];
+        if (r.status < 6)
+            ++cnt[r.status];
+        const u64 idx = s->def_ord[i] - s->sem_kbase;
+        if (idx < s->host_sem.size())
+            s->host_sem[idx] = r;
+    }
+    CK(cudaMemcpyAsync(s->semcnt.p, cnt, 6 * sizeof(u64), cudaMemcpyHostToDevice, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    s->def_text.clear();
+    s->def_ord.clear();
+    return 0;
 }
 
 int run_host_listing_at(ocldec_b200_session *s, const char *listing, size_t len, int fold_local_size,
@@ -1953,7 +2079,7 @@ int run_host_listing_at(ocldec_b200_session *s, const char *listing, size_t len,
     hr->out_bytes = out_pos;
     s->out_len = out_pos;
     s->stats.out_bytes = out_pos;
-    return 0;
+    return finish_deferred(s);
 }
 
 } // namespace
@@ -1976,6 +2102,8 @@ ocldec_b200_session *ocldec_b200_session_create(int device, size_t arena_bytes) 
 void ocldec_b200_session_destroy(ocldec_b200_session *s) {
     if (!s)
         return;
+    if (s->aux)
+        ocldec_b200_session_destroy(s->aux);
     cudaSetDevice(s->device);
     DevBuf *bufs[] = {&s->text, &s->text2, &s->tiles, &s->tiles_off, &s->nlpos, &s->lines, &s->lins, &s->ops_cnt,
                       &s->labs_cnt, &s->ops_off, &s->labs_off, &s->ops, &s->labs, &s->kstart,
@@ -1983,7 +2111,7 @@ void ocldec_b200_session_destroy(ocldec_b200_session *s) {
                       &s->outoff, &s->out, &s->only, &s->retry, &s->gen_len, &s->gen_ninstr,
                       &s->gen_buf, &s->gen_off, &s->kmeta, &s->order, &s->budget, &s->sbudget,
                       &s->boff, &s->hist, &s->prof, &s->ksizes, &s->dpool, &s->dtop, &s->perm, &s->cnt4,
-                      &s->dovr, &s->dovr_text, &s->xtext, &s->xrec, &s->xtop, &s->xcfg, &s->sgen, &s->rstat, &s->semres, &s->semscratch, &s->semcnt};
+                      &s->dovr, &s->dovr_text, &s->xtext, &s->xrec, &s->xtop, &s->xcfg, &s->sgen, &s->rstat, &s->semres, &s->semscratch, &s->semcnt, &s->semkmap, &s->semdef, &s->semspan, &s->semdefbuf};
     for (DevBuf *b : bufs)
         if (b->p)
             cudaFree(b->p);
@@ -2046,6 +2174,8 @@ int ocldec_b200_session_run(ocldec_b200_session *s, const void *d_listing, size_
     }
     s->out_len = out_pos;
     s->stats.out_bytes = out_pos;
+    if (int rc = finish_deferred(s))
+        return rc;
     if (sync)
         CK(cudaStreamSynchronize(s->stream));
     return 0;
@@ -2793,7 +2923,7 @@ int ocldec_b200_session_run_generated(ocldec_b200_session *s, int shape, int str
     cudaEventDestroy(e1);
     cudaEventDestroy(g0e);
     cudaEventDestroy(g1e);
-    return 0;
+    return finish_deferred(s);
 }
 
 } // extern "C"

@@ -149,8 +149,11 @@ __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_FOLD * 128 / OD_BLOCK) k_fol
 __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_EMIT * 128 / OD_BLOCK) k_emit(DecompArgs a);
 __global__ void __launch_bounds__(OD_BLOCK) k_export(DecompArgs a);
 struct SemResult;
-__global__ void __launch_bounds__(128) k_semcheck(DecompArgs a, u32 n, u32 *next, u8 *scratch, SemResult *out,
-                                                  u64 seed, u64 kbase, u64 *counts);
+struct SemArgs;
+__global__ void __launch_bounds__(128) k_semcheck(DecompArgs a, SemArgs sa);
+__global__ void k_def_spans(const u32 *dlist, u32 n, const u32 *nlpos, u32 nlf, const u32 *kstart, u32 nk,
+                            u64 len, u64 *span);
+__global__ void k_def_pack(const u8 *t, const u64 *span, const u64 *dst_off, u32 n, u8 *dst);
 
 // ------------------------------------------------------------------ generator
 struct GenArgs {

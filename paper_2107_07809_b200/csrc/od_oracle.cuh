@@ -25,6 +25,8 @@ constexpr u64 kSemMemBytes = kSemMemCap * 12ull + kSemMemSlots * 12ull;
 constexpr u64 kSemLaneBytes = 2 * kSemMemBytes + kSemVarCap * 16 + kSemStackCap * 16;
 constexpr u32 kSemEnvs = 8;        // environments (lanes) per kernel
 constexpr long kSemFuel = 1 << 20; // interpreter steps (oracle.cpp:121)
+constexpr u32 kSemDeferCap = 1u << 16; // deferred kernels per chunk (k_semcheck's list)
+constexpr u32 kSemDeferKB = 256u << 10; // their estimated listing bytes per chunk, in KB (256 MB)
 constexpr u32 kSemBatch = 2048;    // warps of a k_semcheck launch (scratch per wave stream: kSemBatch x kSemEnvs lanes)
 
 // Memory  oracle.cpp:41-56: a pristine hash overlaid by this run's writes;
@@ -96,6 +98,20 @@ struct SemMem {
             }
         }
     }
+};
+
+// One k_semcheck launch (od_sem.cu).
+struct SemArgs {
+    u32 n;           // wave slots
+    u32 *next;       // the wave's slot counter
+    u8 *scratch;     // kSemBatch warps x kSemEnvs lanes x kSemLaneBytes
+    SemResult *out;  // per chunk kernel
+    u64 seed, kbase; // environment seed; listing ordinal of the chunk's kernel 0
+    u64 *counts;     // kernels per SemStatus
+    const u64 *kmap; // non-null: kernel k's listing ordinal is kmap[kbase + k] (deferred re-checks)
+    long budget;     // interpreted steps per environment before a kernel is deferred (0: never)
+    u32 *dlist;      // deferred kernels: [0] count, [1] estimated KB, then chunk kernel indices
+    u32 dcap;
 };
 
 // What the kernel sees of one environment.
@@ -703,7 +719,13 @@ struct SemMachine {
     }
 
     // Machine::run  oracle.cpp:221-231
-    OD_HD void run() {
+    // Machine::run  oracle.cpp:221-231, split so that a run can pause: run(limit)
+    // steps until every lane has stopped or has executed `limit` steps (held),
+    // and a later run(larger limit) continues from the same state.
+    u32 pc;
+    bool stop;
+    bool held; // this lane reached the step limit of the last run() unfinished
+    OD_HD void init() {
         const KCtx &K = *c.K;
         for (u32 i = 0; i < kSgprCount; ++i)
             s[i] = 0;
@@ -724,26 +746,37 @@ struct SemMachine {
             tc_key[i] = 0;
         opsp = K.in->ops;
         insp = K.ins;
-        u32 pc = 0;
+        pc = 0;
         steps = 0;
-        bool stop = false;
+        stop = false;
+        held = false;
+    }
+    // (one out-of-line copy: k_semcheck calls it twice, with and without a limit)
+    OD_NOINL void run(long limit = kSemFuel + 1) {
+        const KCtx &K = *c.K;
+        held = false;
         for (;;) {
             stop = stop || pc >= K.nins || bad;
+            const bool hold = !stop && steps >= limit;
 #ifdef __CUDA_ARCH__
             // The warp's lanes run the same instructions on different data;
             // stepping only the lanes at the lowest pc keeps them at one
             // instruction (one dispatch path) instead of serializing lanes
             // that drifted apart.  Each lane still executes exactly its own
             // instruction sequence.
-            const u32 key = stop ? ~0u : pc;
+            const u32 key = stop || hold ? ~0u : pc;
             const u32 lo = __reduce_min_sync(wm, key);
-            if (lo == ~0u)
+            if (lo == ~0u) {
+                held = hold;
                 break;
+            }
             if (key != lo)
                 continue;
 #else
-            if (stop)
+            if (stop || hold) {
+                held = hold;
                 break;
+            }
 #endif
             if (++steps > kSemFuel) {
                 bad = true;
@@ -1033,7 +1066,7 @@ struct SemEval {
     }
     // exec_body / exec_stmt  oracle.cpp:786-834, over the statement lists
     // (hoisted decls, then the body), If arms through a small list stack.
-    OD_HD void run(u32 hoist, u32 body) {
+    OD_NOINL void run(u32 hoist, u32 body) {
         const KCtx &K = *c.K;
         u32 lst[64];
         u32 sp = 0;

@@ -10,11 +10,16 @@ namespace od {
 
 // The batched semantic check (od_oracle.cuh) of wave slot i: environment
 // `lane` on lanes 0..kSemEnvs-1 of the calling warp, in the warp's scratch.
-__device__ __noinline__ void sem_one(const DecompArgs &a, u32 i, u32 lane, u8 *wscratch, SemResult *out, u64 seed,
-                                     u64 kbase, u64 *counts) {
+// With a step budget, a kernel whose environments are still running after
+// `budget` steps (typically a loop that will run the 2^20-step fuel out) is
+// listed as deferred instead of holding the wave: the host re-checks the
+// deferred kernels of the whole run together at its end.
+__device__ __noinline__ void sem_one(const DecompArgs &a, const SemArgs &sa, u32 i, u32 lane, u8 *wscratch) {
     const u32 k = a.order[i];
     const u32 lanes = kSemEnvs;
     const u32 m = (1u << lanes) - 1;
+    SemResult *out = sa.out;
+    u64 *counts = sa.counts;
     if (a.res[k].status != KS_OK) {
         if (lane == 0) {
             out[k] = SemResult{SEM_NOT_RUN, 0, 0, 0};
@@ -24,13 +29,19 @@ __device__ __noinline__ void sem_one(const DecompArgs &a, u32 i, u32 lane, u8 *w
         }
         return;
     }
-    KState S;
-    kstate_load(S, reinterpret_cast<const KState *>(a.arena + (a.boff[i] - a.boff0)));
+    const u64 ord = sa.kmap ? sa.kmap[sa.kbase + k] : sa.kbase + k;
+    // The kernel's state is read in place (one L1-cached copy per warp, not a
+    // 2.5 KB local copy per lane): its four self-pointers are fixed once.
+    KState *g = reinterpret_cast<KState *>(a.arena + (a.boff[i] - a.boff0));
+    if (lane == 0)
+        kstate_fix(*g);
+    __syncwarp(m);
+    const KState &S = *g;
     SemCtx c;
     c.K = &S.K;
     c.unsupported = false;
     c.nan_choice = false;
-    SemRng r = sem_stream(seed, kbase + k, lane);
+    SemRng r = sem_stream(sa.seed, ord, lane);
     sem_env(r, lane, S.K.cfg.dims, S.K.cfg.cws, &c.env);
     sem_args(c, r);
     u8 *base = wscratch + (u64)lane * kSemLaneBytes;
@@ -43,12 +54,33 @@ __device__ __noinline__ void sem_one(const DecompArgs &a, u32 i, u32 lane, u8 *w
     base += kSemVarCap * 16;
     SemMachine mach{c, ma};
     mach.wm = m;
+    mach.init();
+    if (sa.budget > 0) {
+        // a straight pass over a long kernel is not a loop: at least 8 steps per instruction
+        mach.run(max((long)sa.budget, 8l * (long)S.K.nins));
+        if (__ballot_sync(m, mach.held)) {
+            // the deferred sections travel to the host: at most kSemDeferKB of listing per chunk
+            const u32 kb = (u32)(((u64)S.K.nins * 64 + 1023) >> 10);
+            u32 slot = ~0u;
+            if (lane == 0 && atomicAdd(sa.dlist + 1, kb) + kb <= kSemDeferKB)
+                slot = atomicAdd(sa.dlist, 1u);
+            slot = __shfl_sync(m, slot, 0);
+            if (slot < sa.dcap) {
+                if (lane == 0) {
+                    sa.dlist[2 + slot] = k;
+                    out[k] = SemResult{SEM_DEFERRED, 0, 0, 0};
+                }
+                return;
+            }
+            // the deferral list or its byte budget is full: finish here
+        }
+    }
     mach.run();
     SemEval ev{c, mb, SemVars{vk, vv, false}, reinterpret_cast<u64 *>(base), false, false};
     ev.run(S.hoist, S.body);
 #ifdef OD_SEM_DEBUG
-    if (kbase + k == OD_SEM_DEBUG) {
-        printf("S %u %u asm bad=%d n=%u [", (u32)(kbase + k), lane, (int)mach.bad, ma.count);
+    if (ord == OD_SEM_DEBUG) {
+        printf("S %u %u asm bad=%d n=%u [", (u32)ord, lane, (int)mach.bad, ma.count);
         for (u32 q = 0; q < ma.n; ++q)
             printf(" %llx:%x", (unsigned long long)ma.addr[q], ma.val[q]);
         printf(" ] body bad=%d full=%d n=%u [", (int)ev.bad, (int)ev.full, mb.count);
@@ -79,24 +111,48 @@ __device__ __noinline__ void sem_one(const DecompArgs &a, u32 i, u32 lane, u8 *w
 }
 
 // Persistent over the wave: each warp takes the next unchecked slot from
-// the wave's counter, so a kernel that runs its environments to the fuel
-// limit (2^20 interpreted steps) overlaps the rest of the wave instead of
-// holding a whole batch launch.  Warps <= kSemBatch (the scratch's slots).
-__global__ void __launch_bounds__(128) k_semcheck(DecompArgs a, u32 n, u32 *next, u8 *scratch, SemResult *out,
-                                                  u64 seed, u64 kbase, u64 *counts) {
+// the wave's counter, so a kernel that runs long overlaps the rest of the
+// wave instead of holding a whole batch launch.  Warps <= kSemBatch (the
+// scratch's slots).
+__global__ void __launch_bounds__(128) k_semcheck(DecompArgs a, SemArgs sa) {
     const u32 wl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (lane >= kSemEnvs)
         return;
-    u8 *ws = scratch + (u64)wl * kSemEnvs * kSemLaneBytes;
+    u8 *ws = sa.scratch + (u64)wl * kSemEnvs * kSemLaneBytes;
     for (;;) {
         u32 i = 0;
         if (lane == 0)
-            i = atomicAdd(next, 1u);
+            i = atomicAdd(sa.next, 1u);
         i = __shfl_sync((1u << kSemEnvs) - 1, i, 0);
-        if (i >= n)
+        if (i >= sa.n)
             return;
-        sem_one(a, i, lane, ws, out, seed, kbase, counts);
+        sem_one(a, sa, i, lane, ws);
     }
+}
+
+// Byte spans of the listed kernels in the chunk text (their .kernel line to
+// the next kernel's, or the chunk end): the deferred kernels' sections.
+__global__ void k_def_spans(const u32 *dlist, u32 n, const u32 *nlpos, u32 nlf, const u32 *kstart, u32 nk,
+                            u64 len, u64 *span) {
+    const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n)
+        return;
+    const u32 k = dlist[2 + j];
+    auto line_start = [&](u32 l) -> u64 { return l == 0 ? 0 : l - 1 < nlf ? (u64)nlpos[l - 1] + 1 : len; };
+    const u64 b = line_start(kstart[k]);
+    const u64 e = k + 1 < nk ? line_start(kstart[k + 1]) : len;
+    span[2 * j] = b;
+    span[2 * j + 1] = e > b ? e - b : 0;
+}
+
+// Packs the spans' bytes at their offsets in dst (warp per span).
+__global__ void k_def_pack(const u8 *t, const u64 *span, const u64 *dst_off, u32 n, u8 *dst) {
+    const u32 w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= n)
+        return;
+    const u64 b = span[2 * w], l = span[2 * w + 1], o = dst_off[w];
+    for (u64 q = lane; q < l; q += 32)
+        dst[o + q] = t[b + q];
 }
 
 } // namespace od

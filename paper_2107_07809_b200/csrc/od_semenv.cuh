@@ -127,6 +127,7 @@ enum SemStatus : u32 {
     SEM_NOT_RUN = 4,     // the kernel failed or was skipped
     SEM_INDETERMINATE = 5, // an operation met two NaNs of different payloads: IEEE 754
                            // leaves the result's payload open (od_oracle.cuh sem_nan)
+    SEM_DEFERRED = 6,      // internal: over the in-wave step budget, re-checked at the run's end
 };
 
 struct SemResult {

@@ -193,6 +193,7 @@ int main(int argc, char **argv) {
                         u64 *vk = reinterpret_cast<u64 *>(base), *vv = vk + kSemVarCap;
                         base += kSemVarCap * 16;
                         SemMachine m{c, ma};
+                        m.init();
                         m.run();
                         SemEval ev{c, mb, SemVars{vk, vv, false}, reinterpret_cast<u64 *>(base), false, false};
                         ev.run(A.hoist, A.body);

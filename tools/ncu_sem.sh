@@ -7,7 +7,7 @@ timeout 1500 /usr/local/cuda/bin/ncu --section SourceCounters --section WarpStat
   --section LaunchStats --section Occupancy --section InstructionStats --section MemoryWorkloadAnalysis \
   --clock-control none --import-source on -k regex:k_semcheck -c 1 -o $O/sem \
   python bench.py --kernels ${NK:-4096} --steps 1 --warmup 3 --no-e2e --no-cpu --semantic > $O/ncu.log 2>&1
-/usr/local/cuda/bin/ncu -i $O/sem.ncu-rep --page source --csv --print-source cuda > $O/src_k_semcheck.csv 2>/dev/null
+/usr/local/cuda/bin/ncu -i $O/sem.ncu-rep --page source --csv --print-source cuda,sass 2>/dev/null | python tools/ncu_funcs.py /dev/stdin 30 > $O/funcs_k_semcheck.txt 2>/dev/null
 /usr/local/cuda/bin/ncu -i $O/sem.ncu-rep --page details --csv > $O/details.csv 2>/dev/null
 rm -f $O/sem.ncu-rep
 ls -la $O
