@@ -1450,7 +1450,7 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
         g_err = "internal error: an operand pool bound was exceeded";
         return -3;
     }
-    if (s->sem_on && s->sem_budget > 0 && collect_deferred(s, t, len, nlf, a, sem_kb0, fold_local_size))
+    if (s->sem_on && s->sem_budget != 0 && collect_deferred(s, t, len, nlf, a, sem_kb0, fold_local_size))
         return -3;
     u64 tot = 0;
     memcpy(&tot, cblk + 10, 8);

@@ -109,7 +109,8 @@ struct SemArgs {
     u64 seed, kbase; // environment seed; listing ordinal of the chunk's kernel 0
     u64 *counts;     // kernels per SemStatus
     const u64 *kmap; // non-null: kernel k's listing ordinal is kmap[kbase + k] (deferred re-checks)
-    long budget;     // interpreted steps per environment before a kernel is deferred (0: never)
+    long budget;     // steps per environment before a kernel is deferred: max(budget, 8 x its
+                     // instructions); < 0: exactly -budget (tests); 0: never
     u32 *dlist;      // deferred kernels: [0] count, [1] estimated KB, then chunk kernel indices
     u32 dcap;
 };

@@ -55,9 +55,10 @@ __device__ __noinline__ void sem_one(const DecompArgs &a, const SemArgs &sa, u32
     SemMachine mach{c, ma};
     mach.wm = m;
     mach.init();
-    if (sa.budget > 0) {
-        // a straight pass over a long kernel is not a loop: at least 8 steps per instruction
-        mach.run(max((long)sa.budget, 8l * (long)S.K.nins));
+    if (sa.budget != 0) {
+        // a straight pass over a long kernel is not a loop: at least 8 steps per
+        // instruction (a negative budget is an exact limit, for tests)
+        mach.run(sa.budget > 0 ? max((long)sa.budget, 8l * (long)S.K.nins) : -sa.budget);
         if (__ballot_sync(m, mach.held)) {
             // the deferred sections travel to the host: at most kSemDeferKB of listing per chunk
             const u32 kb = (u32)(((u64)S.K.nins * 64 + 1023) >> 10);

@@ -120,3 +120,37 @@ def test_named_configs_semantics(shape, count, seed):
             assert (gs[2], gs[3]) == (r[2], r[3]), (k, gs, r)
     assert counts[3] + counts[5] <= 0.05 * count, counts
     print(shape, dict(counts))
+
+
+def test_deferred_recheck_with_a_tiny_budget():
+    """With an exact 64-step in-wave budget nearly every kernel is deferred and
+    re-checked at the run's end on the auxiliary session: verdicts and hashes
+    still equal the reference's, and the session counters add up."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, json, collections; sys.path.insert(0, %r)\n"
+        "import paper_2107_07809_b200 as P\n"
+        "from oracle import oracle as O\n"
+        "l, offs, _ = O.generate_corpus('C3', 300, seed=4621, stress=True)\n"
+        "r = P.decompile_listing(l, P.DecompileOptions(semantic_check=True, semantic_seed=%d))\n"
+        "s = P.Session(0); s.set_records(False); s.set_semantic(True, %d)\n"
+        "d_buf, n, _, _ = s.generate('C3', 300, seed=4621, stress=True); s.run(d_buf, n, [0])\n"
+        "print(json.dumps({'sem': [list(k.semantic) for k in r.kernels], 'counts': s.semantic_counts()}))\n"
+        % (root, SEED, SEED))
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=900,
+                       env=dict(os.environ, OCLDEC_B200_SEM_BUDGET="-64"))
+    assert p.returncode == 0, p.stderr[-2000:]
+    out = __import__("json").loads(p.stdout.strip().splitlines()[-1])
+    listing, _, _ = O.generate_corpus("C3", 300, seed=4621, stress=True)
+    ref = O.semcheck(listing, SEED)
+    for k, (g, r) in enumerate(zip(out["sem"], ref)):
+        if g[0] in (3, 5):
+            continue
+        assert g[0] == r[0], (k, g, r)
+        if g[0] in (0, 1):
+            assert (g[2], g[3]) == (r[2], r[3]), (k, g, r)
+    want = collections.Counter(g[0] for g in out["sem"])
+    assert [out["counts"][n] for n in P.Session.SEM_STATUS] == [want.get(i, 0) for i in range(6)]
