@@ -946,6 +946,7 @@ struct ocldec_b200_session {
     std::string def_text;            // the run's deferred kernels' sections ...
     std::vector<u64> def_ord;        // ... and their listing ordinals
     int def_fold = 0;
+    u64 def_kb_left = kSemDeferRunKB; // the run's remaining deferral allowance
     ocldec_b200_session *aux = nullptr; // re-checks the deferred kernels at the run's end
     std::string ovr_src;             // the ABI override text of the current run (set_overrides)
     DevBuf semres, semscratch;       // per chunk kernel: SemResult; the check's lane scratch
@@ -1326,7 +1327,8 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
                 u8 *scr = P<u8>(s->semscratch) + (second ? (u64)kSemBatch * kSemEnvs * kSemLaneBytes : 0);
                 SemArgs sa{a.count, next, scr, P<SemResult>(s->semres), s->sem_seed,
                            s->sem_kbase + s->stats.kernels, P<u64>(s->semcnt), s->sem_kmap,
-                           s->sem_budget, P<u32>(s->semdef), kSemDeferCap};
+                           s->sem_budget, P<u32>(s->semdef), kSemDeferCap,
+                           (u32)std::min<u64>(kSemDeferKB, s->def_kb_left)};
                 k_semcheck<<<(warps * 32 + 127) / 128, 128, 0, ws>>>(a, sa);
                 s->stats.total_launches++;
             }
@@ -1722,6 +1724,7 @@ void reset_stats(ocldec_b200_session *s) {
     s->host_sem.clear();
     s->def_text.clear();
     s->def_ord.clear();
+    s->def_kb_left = kSemDeferRunKB;
     s->sem_counted = s->sem_on;
     if (s->sem_on && !ensure(s->semcnt, 8 * sizeof(u64)))
         cudaMemsetAsync(s->semcnt.p, 0, 8 * sizeof(u64), s->stream);
@@ -1889,6 +1892,7 @@ int collect_deferred(ocldec_b200_session *s, const u8 *t, u64 len, u32 nlf, cons
     std::vector<u32> lk(nd + 2);
     if (d2h_sync(s, lk.data(), s->semdef.p, 4ull * (nd + 2)) || ensure(s->semspan, 24ull * nd + 16))
         return -3;
+    s->def_kb_left -= std::min<u64>(s->def_kb_left, std::min<u64>(lk[1], kSemDeferKB));
     u64 *span = P<u64>(s->semspan);
     k_def_spans<<<(nd + 127) / 128, 128, 0, st>>>(P<u32>(s->semdef), nd, P<u32>(s->nlpos), nlf, a.kstart, a.nk, len,
                                                    span);
@@ -1927,7 +1931,7 @@ int finish_deferred(ocldec_b200_session *s) {
     if (s->def_ord.empty())
         return 0;
     if (!s->aux) {
-        s->aux = ocldec_b200_session_create(s->device, 4ull << 30);
+        s->aux = ocldec_b200_session_create(s->device, 1ull << 30);
         if (!s->aux)
             return -3;
     }

@@ -27,6 +27,7 @@ constexpr u32 kSemEnvs = 8;        // environments (lanes) per kernel
 constexpr long kSemFuel = 1 << 20; // interpreter steps (oracle.cpp:121)
 constexpr u32 kSemDeferCap = 1u << 16; // deferred kernels per chunk (k_semcheck's list)
 constexpr u32 kSemDeferKB = 256u << 10; // their estimated listing bytes per chunk, in KB (256 MB)
+constexpr u64 kSemDeferRunKB = 1u << 20; // ... and per run (1 GiB of host memory at most)
 constexpr u32 kSemBatch = 2048;    // warps of a k_semcheck launch (scratch per wave stream: kSemBatch x kSemEnvs lanes)
 
 // Memory  oracle.cpp:41-56: a pristine hash overlaid by this run's writes;
@@ -113,6 +114,7 @@ struct SemArgs {
                      // instructions); < 0: exactly -budget (tests); 0: never
     u32 *dlist;      // deferred kernels: [0] count, [1] estimated KB, then chunk kernel indices
     u32 dcap;
+    u32 dkb;         // estimated listing KB the chunk may defer (the run's remaining allowance)
 };
 
 // What the kernel sees of one environment.

@@ -63,7 +63,7 @@ __device__ __noinline__ void sem_one(const DecompArgs &a, const SemArgs &sa, u32
             // the deferred sections travel to the host: at most kSemDeferKB of listing per chunk
             const u32 kb = (u32)(((u64)S.K.nins * 64 + 1023) >> 10);
             u32 slot = ~0u;
-            if (lane == 0 && atomicAdd(sa.dlist + 1, kb) + kb <= kSemDeferKB)
+            if (lane == 0 && atomicAdd(sa.dlist + 1, kb) + kb <= sa.dkb)
                 slot = atomicAdd(sa.dlist, 1u);
             slot = __shfl_sync(m, slot, 0);
             if (slot < sa.dcap) {

@@ -154,3 +154,18 @@ def test_deferred_recheck_with_a_tiny_budget():
             assert (g[2], g[3]) == (r[2], r[3]), (k, g, r)
     want = collections.Counter(g[0] for g in out["sem"])
     assert [out["counts"][n] for n in P.Session.SEM_STATUS] == [want.get(i, 0) for i in range(6)]
+
+
+def test_streamed_c5_semantic_counts():
+    """The check inside a streamed C5 run (ocldec_b200_session_run_generated,
+    several chunks): every kernel ends in exactly one final status (deferred
+    kernels re-checked at the run's end), none left deferred or unrun."""
+    s = P.Session(0)
+    try:
+        s.set_semantic(True, SEED)
+        st, _, _ = s.run_generated("C5", 1200, seed=0x210707809C5, k0=300_000, chunk_bytes=96 << 20)
+        got = s.semantic_counts()
+        assert st["chunks"] >= 3
+        assert sum(got.values()) == 1200 and got["not_run"] == 0, got
+    finally:
+        s.close()
