@@ -133,6 +133,42 @@ __global__ void k_nl_write(const u8 *__restrict__ base, u64 len, u32 mis, const 
 // predicate c_space: every token after the first follows such a run) and of
 // its labels (its ':' count), over the raw line, which contains whatever the
 // comment strip keeps.
+// k_decode's staging: the block's 256 lines are one contiguous span of the
+// listing, staged in shared memory with 16-byte loads of its aligned interior
+// (bytewise for the first block of a misaligned chunk).  Returns false when
+// the span is larger than the stage (the lines then read the listing in
+// HBM).  [ab, se) is staged at stage[0]; [sb, se) is the block's raw span.
+constexpr u32 kLineStage = 16384;
+
+__device__ __forceinline__ bool stage_lines(const u8 *__restrict__ t, u64 len, const u32 *__restrict__ nlpos,
+                                            u32 nlf, u32 nlines, u8 *stage, u64 *sb_out, u64 *ab_out,
+                                            u64 *se_out) {
+    const u32 l0 = blockIdx.x * blockDim.x;
+    const u32 l1 = min(l0 + blockDim.x, nlines);
+    const u64 sb = l0 == 0 ? 0 : (u64)nlpos[l0 - 1] + 1;
+    const u64 se = l1 - 1 < nlf ? (u64)nlpos[l1 - 1] : len;
+    const u32 lead = (u32)((uintptr_t)(t + sb) & 15);
+    const bool vec = sb >= lead;
+    const u64 ab = vec ? sb - lead : sb;
+    const bool staged = se - ab <= kLineStage;
+    if (staged) {
+        u64 done = ab;
+        if (vec) {
+            const u64 nv = (se - ab) / 16;
+            const uint4 *src = reinterpret_cast<const uint4 *>(t + ab);
+            for (u64 q = threadIdx.x; q < nv; q += blockDim.x)
+                reinterpret_cast<uint4 *>(stage)[q] = src[q];
+            done = ab + 16 * nv;
+        }
+        for (u64 o = done + threadIdx.x; o < se; o += blockDim.x)
+            stage[o - ab] = t[o];
+    }
+    *sb_out = sb;
+    *ab_out = ab;
+    *se_out = se;
+    return staged;
+}
+
 __global__ void k_classify(const u8 *__restrict__ t, u64 len, const u32 *__restrict__ nlpos,
                            u32 nlf, u32 nlines, LineRec *lines, u32 *complex_bytes, u32 *ops_ub,
                            u32 *labs_ub) {
@@ -141,6 +177,9 @@ __global__ void k_classify(const u8 *__restrict__ t, u64 len, const u32 *__restr
         return;
     u32 b = l == 0 ? 0 : nlpos[l - 1] + 1;
     u32 e = l < nlf ? nlpos[l] : (u32)len;
+    // (staging the block's span in shared memory first, as k_decode does,
+    // measured slower: parse 245 -> 263 ms per C4 step)
+    const u8 *tb = t;
     // one pass over the raw line: the pool bounds (separator runs, ':'
     // count) and strip_comments' cut; a "/*" leaves the cut to strip_scan
     bool cx = false;
@@ -148,7 +187,7 @@ __global__ void k_classify(const u8 *__restrict__ t, u64 len, const u32 *__restr
     {
         bool prev = false, inq = false, found = false, slow = false;
         for (u32 i = b; i < e; ++i) {
-            const u8 c = t[i];
+            const u8 c = tb[i];
             const bool sep = c == ',' || c_space(c);
             runs += sep && !prev;
             prev = sep;
@@ -161,13 +200,13 @@ __global__ void k_classify(const u8 *__restrict__ t, u64 len, const u32 *__restr
                 if (c == '#' || c == ';') {
                     cut = i - b;
                     found = true;
-                } else if (c == '/' && i + 1 < e && t[i + 1] == '*') {
+                } else if (c == '/' && i + 1 < e && tb[i + 1] == '*') {
                     found = slow = true;
                 }
             }
         }
         if (slow)
-            cut = strip_scan(t + b, e - b, &cx);
+            cut = strip_scan(tb + b, e - b, &cx);
     }
     LineRec r;
     r.off = b;
@@ -176,8 +215,8 @@ __global__ void k_classify(const u8 *__restrict__ t, u64 len, const u32 *__restr
     r.pad = 0;
     r.aux = 0;
     if (!cx) {
-        r.len = rtrim_len(t + b, cut);
-        r.kind = classify_content(t, Span{r.off, r.len});
+        r.len = rtrim_len(tb + b, cut);
+        r.kind = classify_content(tb, Span{r.off, r.len});
     } else {
         r.len = e - b; // raw span, materialized later
         r.kind = LK_BLANK;
@@ -256,7 +295,6 @@ __global__ void k_init_roots() {
 // in shared memory (16-byte vector loads for the aligned interior) and every
 // thread decodes its line from there.  Lines whose content lives in the aux
 // area (comment-stripped copies) and oversized spans read the listing in HBM.
-constexpr u32 kDecodeStage = 16384;
 // Shape key of the decode order: operand bound (0..7) x length class.
 #ifndef OD_DECODE_LEN_CLASSES
 #define OD_DECODE_LEN_CLASSES 2
@@ -265,39 +303,23 @@ constexpr u32 kDecodeStage = 16384;
 #define OD_DECODE_LEN_STEP 6
 #endif
 
-__global__ void __launch_bounds__(256) k_decode(const u8 *__restrict__ t, u64 len, const u32 *__restrict__ nlpos,
+// 6 blocks per SM (40 registers, 16 bytes of spills) over the register-
+// limited 5: parse 263 -> 245 ms per C4 step (8 blocks: 254 ms)
+#ifndef OD_DECODE_MINB
+#define OD_DECODE_MINB 6
+#endif
+__global__ void __launch_bounds__(256, OD_DECODE_MINB) k_decode(const u8 *__restrict__ t, u64 len, const u32 *__restrict__ nlpos,
                                                 u32 nlf, u32 nlines, const LineRec *__restrict__ lines,
                                                 LineIns *lins, const u32 *ops_off, const u32 *labs_off,
                                                 Opnd *ops, Label *labs, u32 ops_total, u32 *overflow,
                                                 const u32 *__restrict__ ops_ub) {
     __shared__ RootTable rt;
-    __shared__ __align__(16) u8 stage[kDecodeStage];
+    __shared__ __align__(16) u8 stage[kLineStage];
     for (u32 i = threadIdx.x; i < sizeof(RootTable) / 4; i += blockDim.x)
         reinterpret_cast<u32 *>(&rt)[i] = reinterpret_cast<const u32 *>(&d_roots)[i];
-    // raw span of the block's lines
+    u64 sb, ab, se;
+    const bool staged = stage_lines(t, len, nlpos, nlf, nlines, stage, &sb, &ab, &se);
     const u32 l0 = blockIdx.x * blockDim.x;
-    const u32 l1 = min(l0 + blockDim.x, nlines);
-    const u64 sb = l0 == 0 ? 0 : (u64)nlpos[l0 - 1] + 1;
-    const u64 se = l1 - 1 < nlf ? (u64)nlpos[l1 - 1] : len;
-    // stage [ab, se): ab = sb rounded down to a 16-byte boundary of the
-    // listing (never before the chunk start: the first block of a misaligned
-    // chunk stages bytewise)
-    const u32 lead = (u32)((uintptr_t)(t + sb) & 15);
-    const bool vec = sb >= lead;
-    const u64 ab = vec ? sb - lead : sb;
-    const bool staged = se - ab <= kDecodeStage;
-    if (staged) {
-        u64 done = ab;
-        if (vec) {
-            const u64 nv = (se - ab) / 16;
-            const uint4 *src = reinterpret_cast<const uint4 *>(t + ab);
-            for (u64 q = threadIdx.x; q < nv; q += blockDim.x)
-                reinterpret_cast<uint4 *>(stage)[q] = src[q];
-            done = ab + 16 * nv;
-        }
-        for (u64 o = done + threadIdx.x; o < se; o += blockDim.x)
-            stage[o - ab] = t[o];
-    }
     // Lines of one shape take the same decode paths: the block's lines are
     // reordered by a shape key (operand bound from k_classify, long or
     // short) with a counting sort in shared memory, so each warp decodes
@@ -933,6 +955,12 @@ struct ocldec_b200_session {
     DevBuf sgen;                     // streamed generation: the current group of chunks
     DevBuf rstat;                    // per-chunk result totals (k_res_stats)
     bool keep_records = true;        // per-kernel host records (names, spans, flags, diagnostics)
+    // Small readbacks (counters, totals) go through mapped pinned memory
+    // written by a one-warp kernel, not a D2H copy: on the host-buffer path
+    // the copy engine is busy with the previous chunk's output, and a small
+    // cudaMemcpy queued behind it stalled the next chunk's parse (measured:
+    // parse 382 vs 245 ms per C4 step).
+    u8 *peek_h = nullptr, *peek_d = nullptr;
     bool wide_lower = false;         // OCLDEC_B200_WIDE_LOWER: k_lower_wide for long-kernel chunks
     bool sem_on = false;             // the batched semantic check of the current call
     u64 sem_seed = 0;
@@ -1004,7 +1032,22 @@ int scan_exclusive(ocldec_b200_session *s, u64 n, T ident, Op op, Load load, Sto
     return 0;
 }
 
+constexpr size_t kPeekBytes = 4096;
+
+__global__ void k_peek(u8 *dst, const u8 *src, u32 n) {
+    for (u32 i = threadIdx.x; i < n; i += blockDim.x)
+        dst[i] = src[i];
+}
+
 int d2h_sync(ocldec_b200_session *s, void *h, const void *d, size_t n) {
+    if (s->peek_d && n <= kPeekBytes) {
+        k_peek<<<1, 128, 0, s->stream>>>(s->peek_d, static_cast<const u8 *>(d), (u32)n);
+        s->stats.total_launches++;
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(s->stream));
+        memcpy(h, s->peek_h, n);
+        return 0;
+    }
     CK(cudaMemcpyAsync(h, d, n, cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));
     return 0;
@@ -1461,10 +1504,9 @@ int run_chunk(ocldec_b200_session *s, const u8 *t, u64 len, bool can_extend, u32
     u64 base = out_base;
     if (tot && prev_nonempty) {
         // separator between the previous chunk's last source and ours
-        u8 nl = '\n';
         if (ensure_keep(s->out, out_base + 1 + chunk_bytes + 16, out_base, st))
             return -3;
-        CK(cudaMemcpyAsync(P<u8>(s->out) + out_base, &nl, 1, cudaMemcpyHostToDevice, st));
+        CK(cudaMemsetAsync(P<u8>(s->out) + out_base, '\n', 1, st));
         base += 1;
     }
     if (ensure_keep(s->out, base + chunk_bytes + 16, base, st))
@@ -1650,6 +1692,10 @@ int session_init(ocldec_b200_session *s, int device, size_t arena_bytes) {
     CK(cudaStreamCreateWithFlags(&s->cstream, cudaStreamNonBlocking));
     for (auto &e : s->cev)
         CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    if (!getenv("OCLDEC_B200_NO_PEEK")) {
+        CK(cudaHostAlloc(reinterpret_cast<void **>(&s->peek_h), kPeekBytes, cudaHostAllocMapped));
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void **>(&s->peek_d), s->peek_h, 0));
+    }
     // arena pool for one decompile wave (per-kernel slices sized by arena_budget)
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
@@ -1758,15 +1804,33 @@ u64 count_kernel_lines(const char *p, size_t len) {
     return n;
 }
 
+// Chunk plan of the host-buffer path.  The first chunk's load and the last
+// chunk's output read-back are the only copies the pipeline cannot hide, so
+// with three or more chunks the first and last are made smaller and the
+// middle ones larger (up to 1.2 x target, under the 3.75 GiB chunk limit),
+// keeping the chunk count (each chunk costs its phase tails).  C4 1M:
+// 3.2 GB equal chunks -> 1.9 GB first, 3.9 GB middle, ~1.8 GB last.
+// OCLDEC_B200_TAPER=0 keeps equal chunks; `first` (OCLDEC_B200_FIRST_CHUNK)
+// fixes the first chunk and splits the rest equally.
 std::vector<u64> host_chunks(const char *p, size_t len, size_t target, size_t first) {
     std::vector<u64> starts{0};
+    size_t mid = 0;
     if (!first) {
         const size_t nch = len ? (len + target - 1) / target : 1;
-        first = target = (len + nch - 1) / nch;
+        const size_t avg = (len + nch - 1) / nch;
+        first = mid = avg;
+        const char *tp = getenv("OCLDEC_B200_TAPER");
+        if (nch >= 3 && !(tp && *tp == '0')) {
+            const size_t cap = target / 5 * 6;
+            size_t small = len > (nch - 2) * cap ? (len - (nch - 2) * cap) / 2 : 0;
+            small = std::min(std::max(small, avg / 3), avg);
+            first = small;
+            mid = (len - 2 * small + (nch - 3)) / (nch - 2);
+        }
     } else if (len > first) {
         const size_t rem = len - first;
         const size_t nch = (rem + target - 1) / target;
-        target = (rem + nch - 1) / nch;
+        mid = (rem + nch - 1) / nch;
     }
     size_t next = first;
     while (next < len) {
@@ -1787,7 +1851,7 @@ std::vector<u64> host_chunks(const char *p, size_t len, size_t target, size_t fi
         }
         if (!found)
             break;
-        next = starts.back() + target;
+        next = starts.back() + mid;
     }
     return starts;
 }
@@ -2129,6 +2193,8 @@ void ocldec_b200_session_destroy(ocldec_b200_session *s) {
         cudaStreamDestroy(s->stream2);
     if (s->cstream)
         cudaStreamDestroy(s->cstream);
+    if (s->peek_h)
+        cudaFreeHost(s->peek_h);
     for (auto &e : s->cev)
         cudaEventDestroy(e);
     delete s;
