@@ -1,4 +1,4 @@
-// ocldec-b200: k_lower / k_fold / k_emit, one translation unit compiled with
+// ocldec-b200: k_lower / k_emit, one translation unit compiled with
 // -Xptxas -O1: these launches are bound by instruction fetch, and ptxas -O1
 // emits smaller code for them (measured: lower -5 %, emit -12 %).
 #include "od_device.cuh"
@@ -43,23 +43,6 @@ __global__ void __launch_bounds__(OD_BLOCK, OD_MINB_LOWER * 128 / OD_BLOCK) k_lo
     dk_lower(*g);
 }
 
-__global__ void __launch_bounds__(OD_BLOCK, OD_MINB_FOLD * 128 / OD_BLOCK) k_fold(DecompArgs a) {
-    Slot0 sl;
-    if (!dk_slot(a, &sl))
-        return;
-    KState *g = reinterpret_cast<KState *>(sl.base);
-    if (g->done)
-        return;
-#if OD_LOCAL_FOLD
-    KState S;
-    kstate_load(S, g);
-    dk_fold(S);
-    kstate_store(g, S);
-#else
-    kstate_fix(*g);
-    dk_fold(*g);
-#endif
-}
 
 // DUMP_BODY: the lowered statement tree of every kernel that emitted, as a
 // step -3 dump (a separate launch: the emit path pays nothing for it).
